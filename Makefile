@@ -1,0 +1,24 @@
+# Top-level build.  `make` builds the product library and the CPU checkers.
+#   paper_2505_05950_b200/libfloe_b200.so : sm_100a kernels + C ABI (include/floe_gpu.h)
+#   oracle/liboracle.so, oracle/_ref/libfloe_ref.so : test infrastructure
+NVCC     ?= nvcc
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O3 -Xptxas -v --expt-relaxed-constexpr
+PKG      := paper_2505_05950_b200
+LIB      := $(PKG)/libfloe_b200.so
+SRCS     := $(PKG)/csrc/floe_gpu.cu
+HDRS     := $(wildcard $(PKG)/csrc/*.cuh) include/floe_gpu.h
+
+all: $(LIB) oracle
+
+$(LIB): $(SRCS) $(HDRS)
+	$(NVCC) $(NVFLAGS) -shared -cudart static -o $@ $(SRCS) 2> build_ptxas.log || (cat build_ptxas.log; exit 1)
+
+oracle:
+	$(MAKE) -C oracle
+
+clean:
+	rm -f $(LIB) build_ptxas.log
+	$(MAKE) -C oracle clean
+
+.PHONY: all oracle clean

@@ -1,0 +1,527 @@
+#!/usr/bin/env python
+"""bench.py -- FloE compressed-expert decode on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): one Mixtral-8x7B-shaped MoE layer --
+router top-2 of 8 compressed experts (INT2 g64 up projection, f16 gate/down
+records, ~80% contextual sparsity), mixing matrix stand-in for attention --
+single-token decode.  A step is one layer_forward of one token; value is
+decode tokens/s of that layer over all ranks.  N > 1 runs N independent
+replicas ("replicas only": single-sequence decode does not shard).
+The config-1 single-expert numbers ride along under "expert_ffn".
+
+Weights are the reference's own gen_model random streams (seed 7), generated
+and quantized on the device by the product library; thresholds are
+per-expert 0.8-quantiles of |v| over 8 calibration tokens (token_input(3, t)).
+Decode tokens are token_input(1, t).  L2 is flushed (256 MiB write) before
+every timed step, outside the step's CUDA events.
+
+Only the cpu_baseline leg and --impl reference touch oracle/ (the reference
+core compiled from its own sources, oracle/_ref/libfloe_ref.so).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "decode tokens/s (Mixtral-8x7B shape) + expert-FFN achieved HBM GB/s vs roofline"
+DH, DI, E, TOPK, BITS, G, KSP, SEED = 4096, 14336, 8, 2, 2, 64, 0.8, 7
+N_CAL = 8
+WORKLOAD = ("config2: one Mixtral-8x7B MoE layer (d=4096, ffn=14336, 8 experts, top-2), "
+            "INT2 g64 up + ~80% contextual gate/down sparsity, single-token decode")
+REC_BYTES = 4 * DH                   # one f16 gate|down channel record
+CODE_BYTES = DH * DI * BITS // 8     # 14,680,064
+META_BYTES = 4 * (DH * DI // G)      # 3,670,016
+MIX_BYTES = DH * DH * 2              # f16 mixing
+
+
+def weight_stream(layer, kind, expert):  # core/src/model.cpp:25-28
+    return ((layer * 5 + kind) * 65536 + expert) * 64
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                stderr=subprocess.DEVNULL)
+            time.sleep(0.25)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self) -> dict:
+        if not self.path or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(float(r[1]) for r in rows),
+                "sm_max_mhz": max(float(r[2]) for r in rows), "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows)}
+
+
+# ------------------------------------------------------------------ distributed
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def max_over_ranks(value: float, world: int, device=None) -> float:
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ our arm
+def build_layer(fb, torch, layer_idx=0):
+    """gen_model streams (model.cpp:42-74) for one layer, generated and quantized in HBM."""
+    sigma = float(np.float32(1.0) / np.sqrt(np.float32(DH)))
+    router = fb.gen_normals(SEED, weight_stream(layer_idx, 0, 0), E * DH, sigma, sharded=True)
+    mixing = fb.gen_normals(SEED, weight_stream(layer_idx, 1, 0), DH * DH, sigma, sharded=True)
+    experts = []
+    for e in range(E):
+        gate = fb.gen_normals(SEED, weight_stream(layer_idx, 2, e), DH * DI, sigma, sharded=True)
+        up = fb.gen_normals(SEED, weight_stream(layer_idx, 3, e), DH * DI, sigma, sharded=True)
+        down = fb.gen_normals(SEED, weight_stream(layer_idx, 4, e), DH * DI, sigma, sharded=True)
+        codes, scales, zeros = fb.quantize(up, BITS, G)
+        del up
+        experts.append(fb.GpuExpert(DH, DI, BITS, G, codes, scales, zeros, gate=gate, down=down,
+                                    threshold=0.0))
+        del gate, down, codes, scales, zeros
+    torch.cuda.synchronize()
+    return router.view(E, DH), mixing.view(DH, DH), experts
+
+
+def quantile_threshold(torch, mags, k):
+    """calibrate_threshold (sparsify.cpp:42-54): sorted[ceil(k N) - 1]."""
+    s, _ = torch.sort(mags)
+    n = s.numel()
+    rank = min(max(int(math.ceil(k * n)), 1), n)
+    return float(s[rank - 1].item())
+
+
+def calibrate(fb, torch, router, mixing, experts, ws):
+    """Per-expert t = 0.8-quantile of |qgemv(up_e, u)| over N_CAL calibration tokens,
+    u = h + mixing.h the block input (model.cpp:150-152)."""
+    mags = [[] for _ in experts]
+    for t in range(N_CAL):
+        h = fb.gen_normals(3, (1 << 40) + t, DH)
+        u = h + mixing @ h
+        for e, ex in enumerate(experts):
+            mags[e].append(fb.qgemv_channels(ex, u.contiguous(), ws).abs())
+    ths = []
+    for e, ex in enumerate(experts):
+        th = quantile_threshold(torch, torch.cat(mags[e]), KSP)
+        ex.set_threshold(th)
+        ths.append(th)
+    return ths
+
+
+def flush_l2(buf):
+    buf.add_(1.0)
+
+
+def time_steps(torch, fn, n, flush_buf, stream):
+    """n steps, each preceded by an L2 flush outside its CUDA events."""
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(n)]
+    for i in range(n):
+        flush_l2(flush_buf)
+        evs[i][0].record(stream)
+        fn(i)
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_05950_b200 as fb
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = fb.device_info()
+    hbm_peak, peak_kind = peaks()
+    stream = torch.cuda.current_stream()
+
+    # ---------------- setup (untimed) ----------------
+    t_setup = time.perf_counter()
+    router, mixing, experts = build_layer(fb, torch)
+    ws = fb.Workspace(DH, DI, TOPK)
+    thresholds = calibrate(fb, torch, router, mixing, experts, ws)
+    layer = fb.GpuLayer(router.cpu().numpy(), mixing.cpu().numpy(), experts, TOPK,
+                        mixing_f16=True)
+    n_tok = args.warmup + args.steps
+    tokens = torch.stack([fb.gen_normals(1, (1 << 40) + t, DH) for t in range(n_tok)])
+    flush = torch.zeros(64 << 20, dtype=torch.float32, device="cuda")  # 256 MiB > 126 MB L2
+    y = torch.empty(DH, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+
+    def step(i, off=args.warmup):
+        fb.layer_forward(layer, tokens[off + i], ws, out=y)
+
+    # ---------------- warmup + timed region ----------------
+    time_steps(torch, lambda i: step(i, 0), args.warmup, flush, stream)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        step_ms = time_steps(torch, step, args.steps, flush, stream)
+        barrier(world)
+        torch.cuda.synchronize()
+        wall_s = time.perf_counter() - t0
+    clocks = clk.summary()
+    my_ms = sum(step_ms)
+    max_ms = max_over_ranks(my_ms, world, torch.device("cuda", local))
+    value = world * args.steps / (max_ms / 1000.0)
+
+    # ---------------- profiled pass: per-kernel shares + byte accounting ----------------
+    ws.set_profiling(True)
+    ws.read_profile()
+    ws.reset_counters()
+    time_steps(torch, step, args.steps, flush, stream)
+    prof = ws.read_profile()
+    cnt = ws.read_counters()
+    ws.set_profiling(False)
+    kept_per_step = cnt["kept"] / max(args.steps, 1)
+    stage_bytes = {
+        "mixing": MIX_BYTES + 3 * 4 * DH,
+        "route": E * DH * 4 + 4 * DH,
+        "k1_up_threshold": TOPK * (CODE_BYTES + META_BYTES) + 4 * DH,
+        "k2_gate_down": kept_per_step * REC_BYTES + 2 * 4 * DH,
+    }
+    stage = {}
+    for k, p in prof.items():
+        avg_ms = p["ms"] / max(p["launches"], 1)
+        stage[k] = dict(avg_us=round(avg_ms * 1e3, 3), bytes=int(stage_bytes[k]),
+                        gbs=round(stage_bytes[k] / (avg_ms * 1e-3) / 1e9, 1) if avg_ms > 0 else None)
+    total_stage_ms = sum(p["ms"] for p in prof.values())
+    for k, p in prof.items():
+        stage[k]["share"] = round(p["ms"] / total_stage_ms, 4) if total_stage_ms else None
+    dominant = max(stage, key=lambda k: stage[k]["share"] or 0)
+    d = stage[dominant]
+    traffic = None
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(dominant)
+    roofline = {"bound": "hbm", "kernel": dominant, "achieved": d["gbs"], "peak": hbm_peak,
+                "peak_kind": peak_kind, "unit": "GB/s",
+                "frac": round(d["gbs"] / hbm_peak, 4) if d["gbs"] else None,
+                "traffic": traffic, "algorithmic_bytes_per_launch": d["bytes"],
+                "avg_launch_us": d["avg_us"]}
+    layer_bytes = sum(stage_bytes.values())
+    step_mean_ms = my_ms / args.steps
+
+    # ---------------- config 1: single expert (expert_ffn) ----------------
+    expert_ffn = run_expert(fb, torch, args, flush, stream, hbm_peak)
+
+    # ---------------- e2e through the host-buffer API ----------------
+    tokens_h = tokens.cpu().numpy()
+    y_h = np.empty(DH, np.float32)
+    for i in range(min(args.warmup, 3)):
+        fb.layer_forward_host(layer, tokens_h[i], ws, out=y_h)
+    e2e_s = 0.0
+    for i in range(args.steps):
+        flush_l2(flush)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        fb.layer_forward_host(layer, tokens_h[args.warmup + i], ws, out=y_h)
+        e2e_s += time.perf_counter() - t1
+    e2e_max = max_over_ranks(e2e_s, world, torch.device("cuda", local))
+    e2e = {"value": round(world * args.steps / e2e_max, 2), "unit": "tokens/s",
+           "h2d_bytes_per_step": 4 * DH, "d2h_bytes_per_step": 4 * DH,
+           "api": "floe_gpu_layer_forward_host (pinned staging, stream sync)"}
+
+    out = {
+        "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_mean_ms, 5),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32 accumulate (INT2 up codes, f16 gate/down records, f16 mixing)",
+        "data": "synthetic: reference gen_model streams (seed 7) generated+quantized on device",
+        "config": {"workload": WORKLOAD, "d_hidden": DH, "d_intermediate": DI, "experts": E,
+                   "top_k": TOPK, "bits": BITS, "group_size": G, "sparsity_k": KSP,
+                   "thresholds": [round(t, 6) for t in thresholds],
+                   "kept_channels_per_step": round(kept_per_step, 1),
+                   "parallelism": "replicas" if world > 1 else "single-gpu",
+                   "l2": "flushed before every step (256 MiB write, outside step events)",
+                   "tokens": "token_input(1, t)"},
+        "roofline": roofline,
+        "step_roofline": {"bytes_per_step": int(layer_bytes),
+                          "achieved": round(layer_bytes / (step_mean_ms * 1e-3) / 1e9, 1),
+                          "peak": hbm_peak, "unit": "GB/s",
+                          "frac": round(layer_bytes / (step_mean_ms * 1e-3) / 1e9 / hbm_peak, 4)},
+        "stages": stage,
+        "expert_ffn": expert_ffn,
+        "e2e": e2e,
+        "gpu_launches": 4 * args.steps,
+        "clocks": clocks,
+        "wall_s_timed_region": round(wall_s, 4),
+        "setup_s": round(setup_s, 2),
+        "device": dev,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(thresholds, tokens_h[args.warmup:])
+    if world > 1:
+        dist.destroy_process_group()
+    return out
+
+
+def run_expert(fb, torch, args, flush, stream, hbm_peak):
+    """Config 1: seeded_expert(4096, 14336, 99), seeded_input(4096, 100), INT2 g64,
+    t = calibrate_threshold(|v|, 0.8), generated on the device."""
+    sd = float(np.float32(1.0) / np.sqrt(np.float32(DH)))
+    gate = fb.gen_normals(99, 1, DH * DI, sd)
+    up = fb.gen_normals(99, 2, DH * DI, sd)
+    down = fb.gen_normals(99, 3, DH * DI, sd)
+    x = fb.gen_normals(100, 4, DH)
+    codes, scales, zeros = fb.quantize(up, BITS, G)
+    del up
+    ex = fb.GpuExpert(DH, DI, BITS, G, codes, scales, zeros, gate=gate, down=down)
+    del gate, down
+    ws = fb.Workspace(DH, DI, 1)
+    v = fb.qgemv_channels(ex, x, ws)
+    t = quantile_threshold(torch, v.abs(), KSP)
+    ex.set_threshold(t)
+    y = torch.empty(DH, dtype=torch.float32, device="cuda")
+    nk = torch.zeros(1, dtype=torch.int32, device="cuda")
+    step = lambda i: fb.expert_forward_sparse(ex, x, ws, out=y, n_kept=nk)  # noqa: E731
+    time_steps(torch, step, args.warmup, flush, stream)
+    ms = time_steps(torch, step, args.steps, flush, stream)
+    n_kept = int(nk.item())
+    ws.set_profiling(True)
+    ws.read_profile()
+    time_steps(torch, step, args.steps, flush, stream)
+    prof = ws.read_profile()
+    k1 = prof["k1_up_threshold"]["ms"] / max(prof["k1_up_threshold"]["launches"], 1)
+    k2 = prof["k2_gate_down"]["ms"] / max(prof["k2_gate_down"]["launches"], 1)
+    bytes_tok = CODE_BYTES + META_BYTES + n_kept * REC_BYTES + 8 * DH
+    mean_ms = sum(ms) / len(ms)
+    gbs = bytes_tok / (mean_ms * 1e-3) / 1e9
+    return {"workload": "config1: seeded_expert(4096,14336,99), INT2 g64, k=0.8, batch 1",
+            "value": round(1e3 / mean_ms, 1), "unit": "expert-tokens/s",
+            "us_per_expert_token": round(mean_ms * 1e3, 3), "kept": n_kept,
+            "threshold": round(t, 6), "bytes_per_expert_token": bytes_tok,
+            "achieved": round(gbs, 1), "peak": hbm_peak, "unit_bw": "GB/s",
+            "frac": round(gbs / hbm_peak, 4),
+            "k1_us": round(k1 * 1e3, 3), "k2_us": round(k2 * 1e3, 3),
+            "k1_gbs": round((CODE_BYTES + META_BYTES + 4 * DH) / (k1 * 1e-3) / 1e9, 1),
+            "k2_gbs": round((n_kept * REC_BYTES + 8 * DH) / (k2 * 1e-3) / 1e9, 1)}
+
+
+# ------------------------------------------------------------------ reference arm
+def build_reference_model(thresholds, workers):
+    """gen_model(seed 7) -> compress_model(INT2 g64, given thresholds) in the
+    UNMODIFIED reference core (oracle/_ref/libfloe_ref.so)."""
+    from oracle import oracle as O
+    if O.REF is None:
+        return None, None
+    th = np.ascontiguousarray(thresholds, np.float32)
+    cm = O.REF.ref_cmodel_build_thresholds(1, E, TOPK, DH, DI, SEED, th, BITS, G, workers)
+    if not cm:
+        raise RuntimeError(O.ref_error())
+    return O, cm
+
+
+def cpu_baseline(thresholds, tokens_h, budget_s=15.0):
+    """Reference layer_forward(CompressedModel) on ONE host thread (the reference
+    path is single-threaded), on a bounded sample of the same decode tokens."""
+    O, cm = build_reference_model(thresholds, os.cpu_count() or 1)
+    if cm is None:
+        return {"value": None, "unit": "tokens/s", "cores": 1, "kind": "reference",
+                "sample": "unavailable: oracle/_ref/libfloe_ref.so missing"}
+    y = np.empty(DH, np.float32)
+    t0 = time.perf_counter()
+    O.REF.ref_layer_forward(cm, 0, np.ascontiguousarray(tokens_h[0]), y)
+    one = time.perf_counter() - t0
+    n = int(min(max(budget_s / max(one, 1e-3), 2), 64, len(tokens_h)))
+    t0 = time.perf_counter()
+    for i in range(n):
+        O.REF.ref_layer_forward(cm, 0, np.ascontiguousarray(tokens_h[i]), y)
+    dt = time.perf_counter() - t0
+    O.REF.ref_cmodel_destroy(cm)
+    return {"value": round(n / dt, 4), "unit": "tokens/s", "cores": 1, "kind": "reference",
+            "sample": f"{n} decode tokens of the same layer through floe::layer_forward "
+                      f"(1 thread, {dt:.1f} s)", "cpu": cpu_model()}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip() + f" x{os.cpu_count()}"
+    except OSError:
+        pass
+    return f"unknown x{os.cpu_count()}"
+
+
+def reference_thresholds():
+    """Thresholds for the reference arm, computed by the reference itself the
+    same way the GPU arm computes them (0.8-quantile of |qgemv(up_e, u)| over
+    8 calibration tokens) but through floe::qgemv_channels on the host."""
+    from oracle import oracle as O
+    # the reference arm must not need a GPU: regenerate up projections on the host
+    sigma = float(np.float32(1.0) / np.sqrt(np.float32(DH)))
+    mixing = np.empty(DH * DH, np.float32)
+    O.C.fo_fill_gaussian(mixing, mixing.size, SEED, weight_stream(0, 1, 0), np.float32(sigma),
+                         O.THREADS)
+    mixing = mixing.reshape(DH, DH)
+    us = []
+    for t in range(N_CAL):
+        h = O.token_input(3, t, DH)
+        mixed = np.empty(DH, np.float32)
+        O.C.fo_gemv(DH, DH, mixing, h, mixed)
+        us.append(h + mixed)
+    ths = []
+    up = np.empty(DH * DI, np.float32)
+    for e in range(E):
+        O.C.fo_fill_gaussian(up, up.size, SEED, weight_stream(0, 3, e), np.float32(sigma),
+                             O.THREADS)
+        q = O.quantize(up, BITS, G)
+        mags = np.concatenate([np.abs(O.qgemv_channels(q, DH, u)) for u in us])
+        ths.append(O.calibrate_threshold(mags, KSP))
+    return ths
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's own CPU layer_forward on all host threads
+    (independent tokens per thread), rank 0 only."""
+    from oracle import oracle as O
+    if O.REF is None:
+        return {"impl": "reference", "metric": METRIC, "unit": "tokens/s",
+                "unavailable": "oracle/_ref/libfloe_ref.so not built (reference sources absent)"}
+    threads = os.cpu_count() or 1
+    t_setup = time.perf_counter()
+    ths = reference_thresholds()
+    O_, cm = build_reference_model(ths, threads)
+    setup_s = time.perf_counter() - t_setup
+    per_step = threads  # one token per thread per step
+    n_tok = (args.warmup + args.steps) * per_step
+    toks = np.stack([O.token_input(1, t, DH) for t in range(min(n_tok, 4096))])
+    toks = np.ascontiguousarray(np.resize(toks, (n_tok, DH)))
+    for s in range(args.warmup):
+        O.REF.ref_layer_forward_replicas(cm, 0, toks[s * per_step:(s + 1) * per_step], per_step,
+                                         threads)
+    times = []
+    for s in range(args.steps):
+        base = (args.warmup + s) * per_step
+        dt = O.REF.ref_layer_forward_replicas(cm, 0, toks[base:base + per_step], per_step,
+                                              threads)
+        if dt < 0:
+            raise RuntimeError("reference layer_forward failed")
+        times.append(dt)
+    O.REF.ref_cmodel_destroy(cm)
+    total = sum(times)
+    value = args.steps * per_step / total
+    return {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * total / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic: reference gen_model (seed 7) + compress_model, host",
+            "config": {"workload": WORKLOAD, "d_hidden": DH, "d_intermediate": DI, "experts": E,
+                       "top_k": TOPK, "bits": BITS, "group_size": G, "sparsity_k": KSP,
+                       "thresholds": [round(float(t), 6) for t in ths],
+                       "parallelism": f"{threads} host threads, independent tokens"},
+            "cpu_baseline": {"value": round(value, 4), "unit": "tokens/s", "cores": threads,
+                             "kind": "reference",
+                             "sample": f"{per_step} tokens per step (one per thread), "
+                                       f"floe::layer_forward(CompressedModel)", "cpu": cpu_model()},
+            "e2e": {"value": round(value, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "setup_s": round(setup_s, 2)}
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        out = run_reference(args, rank, world)
+        print(json.dumps(out), flush=True)
+        return
+    out = run_ours(args, rank, world, local)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

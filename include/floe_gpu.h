@@ -1,0 +1,256 @@
+/*
+ * floe_gpu.h -- C ABI of the B200-native FloE compressed-expert FFN path.
+ *
+ * This is the drop-in boundary.  Everything here is plain C: raw pointers,
+ * sizes, status codes, opaque handles.  No torch or C++ types cross it.  The
+ * C++ header include/floe_b200.hpp restores the reference's value-type API
+ * (floe::expert_forward_sparse, floe::layer_forward, floe::predict_mask,
+ * floe::predict_experts, floe::qgemv_channels) on top of these calls, and
+ * INTEGRATION.md shows the bindings a reference maintainer would add.
+ *
+ * Reference interfaces each entry point replaces (paths relative to
+ * /root/reference/proj/):
+ *   floe_gpu_expert_create          CompressedExpert construction/upload:
+ *                                   compress_expert   core/src/model.cpp:210-220
+ *                                   load_compressed   core/src/model.cpp:434-474
+ *   floe_gpu_expert_forward_sparse  Vec expert_forward_sparse(const CompressedExpert&,
+ *                                   const Vec&)       core/include/floe/model.hpp:111,
+ *                                                     core/src/model.cpp:128-142
+ *   floe_gpu_qgemv_channels         qgemv_channels    core/include/floe/quant.hpp:50-51,
+ *                                                     core/src/quant.cpp:122-136
+ *   floe_gpu_dequantize_up          dequantize        core/src/quant.cpp:111-120
+ *   floe_gpu_predict_mask           predict_mask      core/include/floe/predictor.hpp:80-82,
+ *                                                     core/src/predictor.cpp:179-189
+ *   floe_gpu_predict_experts        predict_experts   core/include/floe/predictor.hpp:75-77,
+ *                                                     core/src/predictor.cpp:164-177
+ *   floe_gpu_layer_forward          layer_forward(CompressedModel) / layer_forward_traced
+ *                                   core/include/floe/model.hpp:118,128-129,
+ *                                   core/src/model.cpp:145-208
+ *
+ * Conventions
+ *   - Every function returns FLOE_OK (0) or a nonzero floe_status.  The
+ *     message of the last failure on the calling thread is returned by
+ *     floe_gpu_last_error(); it keeps the reference's "<fn>: <reason>"
+ *     prefixes (e.g. "expert_forward_sparse: dimension mismatch").
+ *   - *_dev pointers are device pointers; *_host pointers are host memory.
+ *   - Compute calls are stream-ordered on the cudaStream_t passed as `stream`
+ *     (NULL = legacy default stream) and never synchronise the host, except
+ *     the *_host convenience calls, which return host results.
+ *   - Handles (experts, layers, predictors) are immutable after creation and
+ *     may be read concurrently from several streams.  A workspace holds the
+ *     per-call scratch (v, kept-channel lists, counters) and must not be used
+ *     by two streams at the same time.
+ *   - There is no CPU fallback: without a usable sm_100 device every compute
+ *     call fails with FLOE_ERR_CUDA.
+ */
+#ifndef FLOE_GPU_H
+#define FLOE_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FLOE_GPU_ABI_VERSION 1
+
+typedef enum floe_status {
+  FLOE_OK = 0,
+  FLOE_ERR_INVALID = 1,     /* argument/dimension error (reference: runtime_error) */
+  FLOE_ERR_CUDA = 2,        /* CUDA runtime/launch failure or no sm_100 device */
+  FLOE_ERR_OOM = 3,         /* device or pinned host allocation failed */
+  FLOE_ERR_UNSUPPORTED = 4  /* valid but not implemented on this path */
+} floe_status;
+
+typedef void *floe_stream_t; /* a cudaStream_t */
+
+typedef struct floe_gpu_expert floe_gpu_expert;
+typedef struct floe_gpu_workspace floe_gpu_workspace;
+typedef struct floe_gpu_layer floe_gpu_layer;
+typedef struct floe_gpu_predictor floe_gpu_predictor;
+
+/* Host view of one compressed expert: the fields of floe::CompressedExpert
+ * (core/include/floe/model.hpp:60-70) as raw arrays.  Exactly one of
+ * {gate_f32 + down_f32} or {records_f16} must be given:
+ *   gate_f32 / down_f32: f32 [d_intermediate][d_hidden] channel-major, as the
+ *       reference stores them; converted to f16 on the device with IEEE RNE
+ *       (identical to floe::f32_to_f16, core/src/io.cpp:19-51).
+ *   records_f16: the compact wire format of pack_compact(element_bytes=2)
+ *       (core/src/offload.cpp:27-53) for ALL channels: [di][gate|down][dh]. */
+typedef struct floe_expert_host_view {
+  uint32_t d_hidden;
+  uint32_t d_intermediate;
+  uint32_t bits;       /* 1,2,3,4,8 (quant.cpp:11-14) */
+  uint32_t group_size; /* must divide d_hidden*d_intermediate */
+  const uint8_t *codes;   /* packed_code_bytes(n, bits) bytes, LE in-byte */
+  const uint16_t *scales; /* f16 bit patterns, n/group_size */
+  const uint16_t *zeros;  /* f16 bit patterns, n/group_size */
+  const float *gate_f32;
+  const float *down_f32;
+  const uint16_t *records_f16;
+  float threshold; /* keep channel c iff |v[c]| >= threshold (model.cpp:135) */
+  uint32_t flags;  /* FLOE_VIEW_DEVICE: every pointer above is a device pointer */
+} floe_expert_host_view;
+
+#define FLOE_VIEW_DEVICE 1u
+
+typedef struct floe_expert_info {
+  uint32_t d_hidden, d_intermediate, bits, group_size;
+  float threshold;
+  uint64_t code_bytes;     /* packed up-projection codes */
+  uint64_t meta_bytes;     /* f16 scales + zeros */
+  uint64_t record_bytes;   /* one gate|down f16 channel record (4*d_hidden) */
+  int fast_path;           /* 1 when the specialised sm_100a kernels apply */
+} floe_expert_info;
+
+/* ---------------------------------------------------------------- runtime */
+const char *floe_gpu_last_error(void);
+int floe_gpu_abi_version(void);
+/* Device properties of the current device; fails if it is not sm_100. */
+int floe_gpu_device_info(int *sm_count, int *cc_major, int *cc_minor,
+                         size_t *total_mem);
+
+/* ---------------------------------------------------------------- experts */
+int floe_gpu_expert_create(const floe_expert_host_view *view,
+                           floe_gpu_expert **out);
+int floe_gpu_expert_destroy(floe_gpu_expert *e);
+int floe_gpu_expert_info(const floe_gpu_expert *e, floe_expert_info *info);
+/* Thresholds are per expert (ThresholdTable, core/src/model.cpp:237). */
+int floe_gpu_expert_set_threshold(floe_gpu_expert *e, float threshold);
+
+/* -------------------------------------------------------------- workspace */
+/* Scratch for calls on experts of at most d_intermediate channels and
+ * d_hidden inputs, up to max_slots experts per call (top_k for layers). */
+int floe_gpu_workspace_create(uint32_t d_hidden, uint32_t d_intermediate,
+                              uint32_t max_slots, floe_gpu_workspace **out);
+int floe_gpu_workspace_destroy(floe_gpu_workspace *ws);
+
+/* --------------------------------------------------------------- hot path */
+/* y = expert_forward_sparse(e, x) (model.cpp:128-142):
+ *   v = qgemv_channels(up_q, x); keep c iff |v[c]| >= threshold;
+ *   y = sum_{kept c} silu(gate_c . x) * v[c] * down_c.
+ * x_dev/y_dev: f32[d_hidden].  Optional outputs (NULL to skip):
+ *   v_dev       f32[d_intermediate]   the up-projection activations
+ *   mask_dev    u8 [d_intermediate]   sparsity_mask(v, threshold)
+ *   kept_dev    u32[d_intermediate]   kept channel ids, UNORDERED
+ *   n_kept_dev  u32[1]                number of kept channels          */
+int floe_gpu_expert_forward_sparse(const floe_gpu_expert *e,
+                                   floe_gpu_workspace *ws, const float *x_dev,
+                                   float *y_dev, float *v_dev,
+                                   uint8_t *mask_dev, uint32_t *kept_dev,
+                                   uint32_t *n_kept_dev, floe_stream_t stream);
+
+/* Same computation from/to HOST memory (the reference's value-type call):
+ * copies x in through pinned staging, runs the path, copies y back and
+ * synchronises `stream`.  v_host / mask_host optional. */
+int floe_gpu_expert_forward_sparse_host(const floe_gpu_expert *e,
+                                        floe_gpu_workspace *ws,
+                                        const float *x_host, float *y_host,
+                                        float *v_host, uint8_t *mask_host,
+                                        floe_stream_t stream);
+
+/* v = qgemv_channels(up_q, d_hidden, x) (quant.cpp:122-136). */
+int floe_gpu_qgemv_channels(const floe_gpu_expert *e, floe_gpu_workspace *ws,
+                            const float *x_dev, float *v_dev,
+                            floe_stream_t stream);
+
+/* out = dequantize(up_q) in f32, bit-exact with floe::dequantize. */
+int floe_gpu_dequantize_up(const floe_gpu_expert *e, float *out_dev,
+                           floe_stream_t stream);
+
+/* Reuse predictor (predictor.cpp:179-189): mask = |qgemv(up_next, x_prev)| >= t
+ * with an explicit threshold t.  Same optional outputs as forward. */
+int floe_gpu_predict_mask(const floe_gpu_expert *next, floe_gpu_workspace *ws,
+                          const float *x_prev_dev, float t, uint8_t *mask_dev,
+                          uint32_t *kept_dev, uint32_t *n_kept_dev,
+                          floe_stream_t stream);
+
+/* ---------------------------------------------------------------- layers */
+/* One compressed MoE block (floe::CompressedLayer + cfg.top_k).  router and
+ * mixing are f32 row-major ([E][dh], [dh][dh]) as in the reference;
+ * mixing_f16 != 0 stores the mixing matrix as f16 on the device (IEEE RNE),
+ * halving its bytes.  `experts` are borrowed (not owned) and must outlive
+ * the layer; all must share d_hidden/d_intermediate. */
+typedef struct floe_layer_host_view {
+  uint32_t d_hidden;
+  uint32_t n_experts;
+  uint32_t top_k;
+  const float *router;
+  const float *mixing;
+  int mixing_f16;
+  floe_gpu_expert *const *experts;
+} floe_layer_host_view;
+
+typedef struct floe_gpu_layer_trace {
+  float *block_input_dev;   /* f32[d_hidden]  (u)                        */
+  uint32_t *experts_dev;    /* u32[top_k]     ascending expert ids       */
+  float *weights_dev;       /* f32[top_k]     softmax routing weights    */
+  uint8_t *masks_dev;       /* u8[top_k][d_intermediate]                 */
+} floe_gpu_layer_trace;
+
+int floe_gpu_layer_create(const floe_layer_host_view *view,
+                          floe_gpu_layer **out);
+int floe_gpu_layer_destroy(floe_gpu_layer *l);
+/* y = layer_forward(m, layer, h): u = h + mixing.h; route(router, u, top_k);
+ * y = u + sum_j w_j * expert_forward_sparse(E_j, u).  trace may be NULL. */
+int floe_gpu_layer_forward(const floe_gpu_layer *l, floe_gpu_workspace *ws,
+                           const float *h_dev, float *y_dev,
+                           const floe_gpu_layer_trace *trace,
+                           floe_stream_t stream);
+
+/* Host-buffer layer call (the reference's value-type layer_forward): h in,
+ * y out, through pinned staging; synchronises `stream`. */
+int floe_gpu_layer_forward_host(const floe_gpu_layer *l, floe_gpu_workspace *ws,
+                                const float *h_host, float *y_host,
+                                floe_stream_t stream);
+
+/* ----------------------------------------------------- counters / profile */
+/* Device-side running totals kept by a workspace: calls (K1 launches) and
+ * kept channels summed over all slots -- the byte-accounting identity
+ * bytes = calls*(codes+meta) + kept*record_bytes uses them.  Stream-ordered
+ * reset; the read synchronises `stream`. */
+int floe_gpu_workspace_reset_counters(floe_gpu_workspace *ws, floe_stream_t stream);
+int floe_gpu_workspace_read_counters(floe_gpu_workspace *ws, uint64_t *calls,
+                                     uint64_t *kept_total, floe_stream_t stream);
+/* Per-stage CUDA-event timing: when enabled, forward calls record an event
+ * before and after every kernel on the launching stream and accumulate the
+ * elapsed device time per stage.  Stages: 0 mixing, 1 route, 2 K1 (up GEMV +
+ * threshold), 3 K2 (gate/down).  read synchronises; ms[4], launches[4]. */
+int floe_gpu_workspace_set_profiling(floe_gpu_workspace *ws, int enable);
+int floe_gpu_workspace_read_profile(floe_gpu_workspace *ws, double *ms,
+                                    uint64_t *launches);
+
+/* ------------------------------------------------------- synthetic model */
+/* Reference random streams on the device (rng.cpp:12-64): out[i] =
+ * sigma * (float)normal_i.  sharded = 1 reproduces gen_model's fill_gaussian
+ * (model.cpp:31-39: 64 shards, shard s on stream base+s); sharded = 0 is one
+ * sequential stream (acceptance_test.cpp seeded_expert / token_input).
+ * Double-precision Box-Muller: equal to the host stream except for rare
+ * last-ulp differences of the device libm (tests count them). */
+int floe_gpu_gen_normals(uint64_t seed, uint64_t stream_id, uint64_t n, float sigma,
+                         int sharded, float *out_dev, floe_stream_t stream);
+/* quantize (quant.cpp:43-86) on the device, bit-exact: codes must hold
+ * ceil(n*bits/8) bytes, scales/zeros n/group_size f16 patterns. */
+int floe_gpu_quantize(const float *x_dev, uint64_t n, uint32_t bits,
+                      uint32_t group_size, uint8_t *codes_dev,
+                      uint16_t *scales_dev, uint16_t *zeros_dev,
+                      floe_stream_t stream);
+
+/* ------------------------------------------------------------- predictor */
+/* InterExpertPredictor (predictor.hpp:20-33): maps w[target-1] (E x dh,
+ * row-major) and biases b[target-1] (E) for targets 1..layers-1. */
+int floe_gpu_predictor_create(uint32_t layers, uint32_t experts,
+                              uint32_t d_hidden, const float *w_host,
+                              const float *b_host, floe_gpu_predictor **out);
+int floe_gpu_predictor_destroy(floe_gpu_predictor *p);
+/* out_dev = predict_experts(p, x, layer, count): top_k of W x + b, ascending,
+ * ties toward the lower index.  layer 0 is an error, as in the reference. */
+int floe_gpu_predict_experts(const floe_gpu_predictor *p, const float *x_dev,
+                             uint32_t layer, uint32_t count, uint32_t *out_dev,
+                             floe_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLOE_GPU_H */

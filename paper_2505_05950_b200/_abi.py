@@ -1,0 +1,448 @@
+"""ctypes binding of include/floe_gpu.h (the product's C ABI).
+
+Device memory and streams come from PyTorch (plumbing only): device inputs are
+``torch.Tensor``s on ``cuda``, and ``stream`` defaults to torch's current
+stream so calls compose with torch ordering and CUDA-graph capture.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+_HERE = Path(__file__).resolve().parent
+_LIB_PATH = _HERE / "libfloe_b200.so"
+
+FLOE_OK = 0
+_STATUS = {1: "FLOE_ERR_INVALID", 2: "FLOE_ERR_CUDA", 3: "FLOE_ERR_OOM", 4: "FLOE_ERR_UNSUPPORTED"}
+
+
+class FloeError(RuntimeError):
+    """A nonzero floe_status; the message keeps the reference's '<fn>: <reason>' form."""
+
+    def __init__(self, msg: str, status: int = 1):
+        super().__init__(msg)
+        self.status = status
+
+
+class ExpertHostView(ct.Structure):
+    _fields_ = [("d_hidden", ct.c_uint32), ("d_intermediate", ct.c_uint32),
+                ("bits", ct.c_uint32), ("group_size", ct.c_uint32),
+                ("codes", ct.c_void_p), ("scales", ct.c_void_p), ("zeros", ct.c_void_p),
+                ("gate_f32", ct.c_void_p), ("down_f32", ct.c_void_p),
+                ("records_f16", ct.c_void_p), ("threshold", ct.c_float),
+                ("flags", ct.c_uint32)]
+
+
+FLOE_VIEW_DEVICE = 1
+
+
+class ExpertInfo(ct.Structure):
+    _fields_ = [("d_hidden", ct.c_uint32), ("d_intermediate", ct.c_uint32),
+                ("bits", ct.c_uint32), ("group_size", ct.c_uint32), ("threshold", ct.c_float),
+                ("code_bytes", ct.c_uint64), ("meta_bytes", ct.c_uint64),
+                ("record_bytes", ct.c_uint64), ("fast_path", ct.c_int)]
+
+
+class LayerHostView(ct.Structure):
+    _fields_ = [("d_hidden", ct.c_uint32), ("n_experts", ct.c_uint32), ("top_k", ct.c_uint32),
+                ("router", ct.c_void_p), ("mixing", ct.c_void_p), ("mixing_f16", ct.c_int),
+                ("experts", ct.c_void_p)]
+
+
+class LayerTrace(ct.Structure):
+    _fields_ = [("block_input_dev", ct.c_void_p), ("experts_dev", ct.c_void_p),
+                ("weights_dev", ct.c_void_p), ("masks_dev", ct.c_void_p)]
+
+
+_P = ct.c_void_p
+_U32 = ct.c_uint32
+_F = ct.c_float
+# name -> (restype, argtypes); the full exported surface of include/floe_gpu.h
+_SIGS = {
+    "floe_gpu_last_error": (ct.c_char_p, []),
+    "floe_gpu_abi_version": (ct.c_int, []),
+    "floe_gpu_device_info": (ct.c_int, [_P, _P, _P, _P]),
+    "floe_gpu_expert_create": (ct.c_int, [ct.POINTER(ExpertHostView), ct.POINTER(_P)]),
+    "floe_gpu_expert_destroy": (ct.c_int, [_P]),
+    "floe_gpu_expert_info": (ct.c_int, [_P, ct.POINTER(ExpertInfo)]),
+    "floe_gpu_expert_set_threshold": (ct.c_int, [_P, _F]),
+    "floe_gpu_workspace_create": (ct.c_int, [_U32, _U32, _U32, ct.POINTER(_P)]),
+    "floe_gpu_workspace_destroy": (ct.c_int, [_P]),
+    "floe_gpu_expert_forward_sparse": (ct.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "floe_gpu_expert_forward_sparse_host": (ct.c_int, [_P, _P, _P, _P, _P, _P, _P]),
+    "floe_gpu_qgemv_channels": (ct.c_int, [_P, _P, _P, _P, _P]),
+    "floe_gpu_dequantize_up": (ct.c_int, [_P, _P, _P]),
+    "floe_gpu_predict_mask": (ct.c_int, [_P, _P, _P, _F, _P, _P, _P, _P]),
+    "floe_gpu_layer_create": (ct.c_int, [ct.POINTER(LayerHostView), ct.POINTER(_P)]),
+    "floe_gpu_layer_destroy": (ct.c_int, [_P]),
+    "floe_gpu_layer_forward": (ct.c_int, [_P, _P, _P, _P, ct.POINTER(LayerTrace), _P]),
+    "floe_gpu_layer_forward_host": (ct.c_int, [_P, _P, _P, _P, _P]),
+    "floe_gpu_workspace_reset_counters": (ct.c_int, [_P, _P]),
+    "floe_gpu_workspace_read_counters": (ct.c_int, [_P, _P, _P, _P]),
+    "floe_gpu_workspace_set_profiling": (ct.c_int, [_P, ct.c_int]),
+    "floe_gpu_workspace_read_profile": (ct.c_int, [_P, _P, _P]),
+    "floe_gpu_gen_normals": (ct.c_int, [ct.c_uint64, ct.c_uint64, ct.c_uint64, _F, ct.c_int, _P,
+                                        _P]),
+    "floe_gpu_quantize": (ct.c_int, [_P, ct.c_uint64, _U32, _U32, _P, _P, _P, _P]),
+    "floe_gpu_predictor_create": (ct.c_int, [_U32, _U32, _U32, _P, _P, ct.POINTER(_P)]),
+    "floe_gpu_predictor_destroy": (ct.c_int, [_P]),
+    "floe_gpu_predict_experts": (ct.c_int, [_P, _P, _U32, _U32, _P, _P]),
+}
+
+_lib = None
+
+
+def library_path() -> Path:
+    return _LIB_PATH
+
+
+def lib():
+    """Load libfloe_b200.so (raises FloeError if it was never built)."""
+    global _lib
+    if _lib is None:
+        if not _LIB_PATH.exists():
+            raise FloeError(f"{_LIB_PATH} is not built: run `make` or __graft_entry__.build()", 2)
+        L = ct.CDLL(str(_LIB_PATH))
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    """Dynamic symbols of the built library whose name starts with floe_gpu_."""
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_LIB_PATH)], check=True,
+                         capture_output=True, text=True).stdout
+    return sorted(l.split()[-1] for l in out.splitlines() if l.split()[-1].startswith("floe_gpu_"))
+
+
+def _check(rc: int):
+    if rc != FLOE_OK:
+        raise FloeError(lib().floe_gpu_last_error().decode(), rc)
+
+
+def abi_version() -> int:
+    return lib().floe_gpu_abi_version()
+
+
+def device_info() -> dict:
+    sm, ma, mi, mem = ct.c_int(), ct.c_int(), ct.c_int(), ct.c_size_t()
+    _check(lib().floe_gpu_device_info(ct.byref(sm), ct.byref(ma), ct.byref(mi), ct.byref(mem)))
+    return dict(sm_count=sm.value, cc=(ma.value, mi.value), total_mem=mem.value)
+
+
+# ---------------------------------------------------------------------------
+def _torch():
+    import torch
+    return torch
+
+
+def _ptr(t) -> int:
+    if t is None:
+        return 0
+    if isinstance(t, int):
+        return t
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return t.data_ptr()
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        torch = _torch()
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _dev_f32(x, n: int, fn: str):
+    torch = _torch()
+    if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float32):
+        raise FloeError(f"{fn}: expected a float32 CUDA tensor")
+    if x.numel() != n:
+        raise FloeError(f"{fn}: dimension mismatch")
+    return x.contiguous()
+
+
+class Workspace:
+    """Per-stream scratch (floe_gpu_workspace)."""
+
+    def __init__(self, d_hidden: int, d_intermediate: int, max_slots: int = 1):
+        h = ct.c_void_p()
+        _check(lib().floe_gpu_workspace_create(d_hidden, d_intermediate, max_slots, ct.byref(h)))
+        self.handle = h.value
+        self.d_hidden, self.d_intermediate, self.max_slots = d_hidden, d_intermediate, max_slots
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().floe_gpu_workspace_destroy(self.handle)
+            self.handle = None
+
+    __del__ = close
+
+    STAGES = ("mixing", "route", "k1_up_threshold", "k2_gate_down")
+
+    def reset_counters(self, stream=None):
+        _check(lib().floe_gpu_workspace_reset_counters(self.handle, _stream(stream)))
+
+    def read_counters(self, stream=None) -> dict:
+        calls, kept = ct.c_uint64(), ct.c_uint64()
+        _check(lib().floe_gpu_workspace_read_counters(self.handle, ct.byref(calls),
+                                                      ct.byref(kept), _stream(stream)))
+        return dict(calls=calls.value, kept=kept.value)
+
+    def set_profiling(self, enable: bool):
+        _check(lib().floe_gpu_workspace_set_profiling(self.handle, 1 if enable else 0))
+
+    def read_profile(self) -> dict:
+        ms = (ct.c_double * 4)()
+        n = (ct.c_uint64 * 4)()
+        _check(lib().floe_gpu_workspace_read_profile(self.handle, ms, n))
+        return {k: dict(ms=ms[i], launches=n[i]) for i, k in enumerate(self.STAGES)}
+
+
+class GpuExpert:
+    """A compressed expert resident in HBM (floe::CompressedExpert on the device).
+
+    codes/scales/zeros are the reference's QuantizedTensor arrays; gate/down are
+    f32 [di][dh] (converted to f16 records on upload) or ``records`` is the
+    pack_compact f16 wire format of all channels.
+    """
+
+    def __init__(self, d_hidden, d_intermediate, bits, group_size, codes, scales, zeros,
+                 gate=None, down=None, records=None, threshold=0.0):
+        keep = []
+        on_device = not isinstance(codes, np.ndarray)  # torch CUDA tensors
+
+        def host(a, dt):
+            if a is None:
+                return None
+            if on_device:
+                a = a.contiguous()
+                keep.append(a)
+                return a.data_ptr()
+            a = np.ascontiguousarray(a, dt)
+            keep.append(a)
+            return a.ctypes.data
+
+        v = ExpertHostView(d_hidden, d_intermediate, bits, group_size,
+                           host(codes, np.uint8), host(scales, np.uint16), host(zeros, np.uint16),
+                           host(gate, np.float32), host(down, np.float32),
+                           host(records, np.uint16), float(threshold),
+                           FLOE_VIEW_DEVICE if on_device else 0)
+        h = ct.c_void_p()
+        _check(lib().floe_gpu_expert_create(ct.byref(v), ct.byref(h)))
+        self.handle = h.value
+        self.d_hidden, self.d_intermediate = d_hidden, d_intermediate
+        self.bits, self.group_size = bits, group_size
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().floe_gpu_expert_destroy(self.handle)
+            self.handle = None
+
+    __del__ = close
+
+    def info(self) -> dict:
+        i = ExpertInfo()
+        _check(lib().floe_gpu_expert_info(self.handle, ct.byref(i)))
+        return {f: getattr(i, f) for f, _ in ExpertInfo._fields_}
+
+    @property
+    def threshold(self) -> float:
+        return self.info()["threshold"]
+
+    def set_threshold(self, t: float):
+        _check(lib().floe_gpu_expert_set_threshold(self.handle, float(t)))
+
+    def bytes_per_token(self, n_kept: int) -> int:
+        """Algorithmic HBM bytes of one expert-token."""
+        i = self.info()
+        return (i["code_bytes"] + i["meta_bytes"] + n_kept * i["record_bytes"]
+                + 8 * self.d_hidden)
+
+    # -- raw device call (pointers as ints) ---------------------------------
+    def forward_raw(self, ws: Workspace, x_ptr: int, y_ptr: int, v_ptr=0, mask_ptr=0,
+                    kept_ptr=0, nkept_ptr=0, stream: int = 0):
+        _check(lib().floe_gpu_expert_forward_sparse(self.handle, ws.handle, x_ptr, y_ptr,
+                                                    v_ptr, mask_ptr, kept_ptr, nkept_ptr,
+                                                    stream))
+
+
+def expert_forward_sparse(e: GpuExpert, h, ws: Workspace, *, v=None, mask=None, kept=None,
+                          n_kept=None, out=None, stream=None):
+    """floe::expert_forward_sparse(const CompressedExpert&, const Vec&) (model.cpp:128-142).
+
+    ``h`` on the device (torch CUDA tensor) -> stream-ordered device call; ``h``
+    as a numpy array -> the host call (H2D, compute, D2H, synchronise).
+    """
+    if isinstance(h, np.ndarray):
+        h = np.ascontiguousarray(h, np.float32)
+        if h.size != e.d_hidden:
+            raise FloeError("expert_forward_sparse: dimension mismatch")
+        y = np.empty(e.d_hidden, np.float32) if out is None else out
+        _check(lib().floe_gpu_expert_forward_sparse_host(
+            e.handle, ws.handle, h.ctypes.data, y.ctypes.data, _ptr(v), _ptr(mask),
+            _stream(stream) if stream is not None else 0))
+        return y
+    torch = _torch()
+    h = _dev_f32(h, e.d_hidden, "expert_forward_sparse")
+    y = torch.empty(e.d_hidden, dtype=torch.float32, device=h.device) if out is None else out
+    e.forward_raw(ws, h.data_ptr(), y.data_ptr(), _ptr(v), _ptr(mask), _ptr(kept), _ptr(n_kept),
+                  _stream(stream))
+    return y
+
+
+def qgemv_channels(e: GpuExpert, x, ws: Workspace, stream=None):
+    """floe::qgemv_channels(up_q, d_hidden, x, y) (quant.cpp:122-136)."""
+    torch = _torch()
+    x = _dev_f32(x, e.d_hidden, "qgemv_channels")
+    v = torch.empty(e.d_intermediate, dtype=torch.float32, device=x.device)
+    _check(lib().floe_gpu_qgemv_channels(e.handle, ws.handle, x.data_ptr(), v.data_ptr(),
+                                         _stream(stream)))
+    return v
+
+
+def dequantize(e: GpuExpert, stream=None):
+    """floe::dequantize(up_q) on the device (bit-exact f32)."""
+    torch = _torch()
+    out = torch.empty(e.d_hidden * e.d_intermediate, dtype=torch.float32, device="cuda")
+    _check(lib().floe_gpu_dequantize_up(e.handle, out.data_ptr(), _stream(stream)))
+    return out
+
+
+def predict_mask(e_next: GpuExpert, x_prev, t: float, ws: Workspace, *, kept=None,
+                 n_kept=None, stream=None):
+    """floe::predict_mask(up_next, d_hidden, x_prev, t) (predictor.cpp:179-189) -> u8 mask."""
+    torch = _torch()
+    x_prev = _dev_f32(x_prev, e_next.d_hidden, "predict_mask")
+    mask = torch.empty(e_next.d_intermediate, dtype=torch.uint8, device=x_prev.device)
+    _check(lib().floe_gpu_predict_mask(e_next.handle, ws.handle, x_prev.data_ptr(), float(t),
+                                       mask.data_ptr(), _ptr(kept), _ptr(n_kept),
+                                       _stream(stream)))
+    return mask
+
+
+class GpuLayer:
+    """One compressed MoE block (floe::CompressedLayer + top_k) on the device."""
+
+    def __init__(self, router: np.ndarray, mixing: np.ndarray, experts: list[GpuExpert],
+                 top_k: int, mixing_f16: bool = True):
+        router = np.ascontiguousarray(router, np.float32)
+        mixing = np.ascontiguousarray(mixing, np.float32)
+        E = len(experts)
+        arr = (ct.c_void_p * E)(*[e.handle for e in experts])
+        v = LayerHostView(mixing.shape[0], E, top_k, router.ctypes.data, mixing.ctypes.data,
+                          1 if mixing_f16 else 0, ct.addressof(arr))
+        h = ct.c_void_p()
+        _check(lib().floe_gpu_layer_create(ct.byref(v), ct.byref(h)))
+        self.handle = h.value
+        self.experts = experts  # borrowed by the device layer: keep alive
+        self.d_hidden = mixing.shape[0]
+        self.d_intermediate = experts[0].d_intermediate
+        self.n_experts, self.top_k = E, top_k
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().floe_gpu_layer_destroy(self.handle)
+            self.handle = None
+
+    __del__ = close
+
+
+def layer_forward(layer: GpuLayer, h, ws: Workspace, *, traced: bool = False, out=None,
+                  stream=None):
+    """floe::layer_forward / layer_forward_traced (model.cpp:145-208)."""
+    torch = _torch()
+    h = _dev_f32(h, layer.d_hidden, "layer_forward")
+    y = torch.empty(layer.d_hidden, dtype=torch.float32, device=h.device) if out is None else out
+    tr = None
+    if traced:
+        k, di = layer.top_k, layer.d_intermediate
+        res = dict(block_input=torch.empty(layer.d_hidden, dtype=torch.float32, device=h.device),
+                   experts=torch.empty(k, dtype=torch.int32, device=h.device),
+                   weights=torch.empty(k, dtype=torch.float32, device=h.device),
+                   masks=torch.empty((k, di), dtype=torch.uint8, device=h.device))
+        tr = LayerTrace(res["block_input"].data_ptr(), res["experts"].data_ptr(),
+                        res["weights"].data_ptr(), res["masks"].data_ptr())
+    _check(lib().floe_gpu_layer_forward(layer.handle, ws.handle, h.data_ptr(), y.data_ptr(),
+                                        ct.byref(tr) if tr is not None else None,
+                                        _stream(stream)))
+    if traced:
+        res["out"] = y
+        return res
+    return y
+
+
+class GpuPredictor:
+    """floe::InterExpertPredictor on the device: w [layers-1][E][dh], b [layers-1][E]."""
+
+    def __init__(self, w: np.ndarray, b: np.ndarray):
+        w = np.ascontiguousarray(w, np.float32)
+        b = np.ascontiguousarray(b, np.float32)
+        L1, E, dh = w.shape
+        h = ct.c_void_p()
+        _check(lib().floe_gpu_predictor_create(L1 + 1, E, dh, w.ctypes.data, b.ctypes.data,
+                                               ct.byref(h)))
+        self.handle = h.value
+        self.layers, self.experts, self.d_hidden = L1 + 1, E, dh
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().floe_gpu_predictor_destroy(self.handle)
+            self.handle = None
+
+    __del__ = close
+
+
+def predict_experts(p: GpuPredictor, x, layer: int, count: int, stream=None):
+    """floe::predict_experts(p, x, layer, prefetch_count) (predictor.cpp:164-177)."""
+    torch = _torch()
+    x = _dev_f32(x, p.d_hidden, "predict_experts")
+    out = torch.empty(max(count, 1), dtype=torch.int32, device=x.device)
+    _check(lib().floe_gpu_predict_experts(p.handle, x.data_ptr(), layer, count, out.data_ptr(),
+                                          _stream(stream)))
+    return out[:count]
+
+
+def layer_forward_host(layer: GpuLayer, h: np.ndarray, ws: Workspace, out=None, stream=None):
+    """Host-buffer layer_forward (H2D, the four kernels, D2H, synchronise)."""
+    h = np.ascontiguousarray(h, np.float32)
+    if h.size != layer.d_hidden:
+        raise FloeError("layer_forward: dimension mismatch")
+    y = np.empty(layer.d_hidden, np.float32) if out is None else out
+    _check(lib().floe_gpu_layer_forward_host(layer.handle, ws.handle, h.ctypes.data,
+                                             y.ctypes.data,
+                                             _stream(stream) if stream is not None else 0))
+    return y
+
+
+def gen_normals(seed: int, stream_id: int, n: int, sigma: float = 1.0, sharded: bool = False,
+                out=None, stream=None):
+    """The reference's Rng(seed, stream) normals (x sigma) generated on the device."""
+    torch = _torch()
+    out = torch.empty(n, dtype=torch.float32, device="cuda") if out is None else out
+    _check(lib().floe_gpu_gen_normals(seed, stream_id, n, float(sigma), 1 if sharded else 0,
+                                      out.data_ptr(), _stream(stream)))
+    return out
+
+
+def quantize(x, bits: int, group_size: int, stream=None):
+    """floe::quantize on the device -> (codes u8, scales u16-as-int16, zeros) tensors."""
+    torch = _torch()
+    n = x.numel()
+    if group_size == 0 or n % group_size:
+        raise FloeError("quantize: group_size must divide element count")
+    codes = torch.empty((n * bits + 7) // 8, dtype=torch.uint8, device="cuda")
+    scales = torch.empty(n // group_size, dtype=torch.int16, device="cuda")
+    zeros = torch.empty(n // group_size, dtype=torch.int16, device="cuda")
+    _check(lib().floe_gpu_quantize(x.data_ptr(), n, bits, group_size, codes.data_ptr(),
+                                   scales.data_ptr(), zeros.data_ptr(), _stream(stream)))
+    return codes, scales, zeros

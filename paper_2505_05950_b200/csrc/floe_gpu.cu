@@ -1,0 +1,874 @@
+// floe_gpu.cu -- C ABI (include/floe_gpu.h) over the sm_100a kernels.
+//
+// Host-side responsibilities: device residency of compressed experts in the
+// layout DESIGN.md documents, per-stream workspaces, launch configuration,
+// stage profiling and the reference's error contract ("<fn>: <reason>"
+// messages).  There is deliberately no CPU fallback anywhere in this file.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/floe_gpu.h"
+#include "floe_fast.cuh"
+#include "floe_gen.cuh"
+
+using floe_k::ExpertDesc;
+using floe_k::K1Args;
+using floe_k::K2Args;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                   \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(e_ == cudaErrorMemoryAllocation ? FLOE_ERR_OOM : FLOE_ERR_CUDA,  \
+                  "%s: %s (%s)", __func__, cudaGetErrorString(e_), #call);         \
+  } while (0)
+
+#define CK_LAUNCH()                                                                \
+  do {                                                                             \
+    cudaError_t e_ = cudaGetLastError();                                           \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(FLOE_ERR_CUDA, "%s: kernel launch failed: %s", __func__,         \
+                  cudaGetErrorString(e_));                                         \
+  } while (0)
+
+struct DeviceInfo {
+  int ok = 0, sm = 0, major = 0, minor = 0;
+  size_t mem = 0;
+  std::string err;
+};
+
+const DeviceInfo &device_info() {
+  static DeviceInfo info;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    cudaDeviceProp p{};
+    if (e == cudaSuccess) e = cudaGetDeviceProperties(&p, dev);
+    if (e != cudaSuccess) {
+      info.err = std::string("no usable CUDA device: ") + cudaGetErrorString(e);
+      return;
+    }
+    info.sm = p.multiProcessorCount;
+    info.major = p.major;
+    info.minor = p.minor;
+    info.mem = p.totalGlobalMem;
+    if (p.major != 10) {
+      info.err = "device is sm_" + std::to_string(p.major * 10 + p.minor) +
+                 "; this library carries sm_100a code only";
+      return;
+    }
+    info.ok = 1;
+  });
+  return info;
+}
+
+int require_device(const char *fn) {
+  const DeviceInfo &d = device_info();
+  if (!d.ok) return fail(FLOE_ERR_CUDA, "%s: %s", fn, d.err.c_str());
+  return FLOE_OK;
+}
+
+bool bits_ok(uint32_t b) { return b == 1 || b == 2 || b == 3 || b == 4 || b == 8; }
+
+uint64_t packed_code_bytes(uint64_t n, uint32_t bits) { return (n * bits + 7) / 8; }
+
+// Specialised kernels: thread t of a TPB-thread CTA owns x[16t, 16t+16).
+int fast_tpb(uint32_t dh) {
+  if (dh == 4096) return 256;
+  if (dh == 2048) return 128;
+  return 0;
+}
+
+cudaStream_t S(floe_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+uint64_t up256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct floe_gpu_expert {
+  uint32_t dh = 0, di = 0, bits = 0, g = 0;
+  float threshold = 0.0f;
+  uint64_t code_bytes = 0, n_groups = 0;
+  void *block = nullptr;  // one device allocation for everything
+  ExpertDesc host_desc{};
+  ExpertDesc *dev_desc = nullptr;
+  bool fast_k1 = false, fast_k2 = false;
+};
+
+enum { kStageMixing = 0, kStageRoute = 1, kStageK1 = 2, kStageK2 = 3, kStages = 4 };
+
+struct floe_gpu_workspace {
+  uint32_t dh = 0, di = 0, slots = 0;
+  void *block = nullptr;
+  uint32_t *kept_idx = nullptr;
+  float *kept_v = nullptr;
+  uint32_t *count = nullptr, *count_final = nullptr, *done = nullptr, *tile_ctr = nullptr;
+  unsigned long long *stats = nullptr;
+  uint32_t *sel = nullptr;
+  float *weights = nullptr, *u = nullptr, *x = nullptr, *y = nullptr, *v = nullptr;
+  uint8_t *mask = nullptr;
+  // pinned host staging for the *_host calls
+  float *hx = nullptr, *hy = nullptr, *hv = nullptr;
+  uint8_t *hmask = nullptr;
+  unsigned long long *hstats = nullptr;
+  // stage profiling (CUDA events on the launching stream)
+  bool profiling = false;
+  std::vector<cudaEvent_t> pool;  // free events
+  struct Pending {
+    int stage;
+    cudaEvent_t a, b;
+  };
+  std::vector<Pending> pending;
+  double ms[kStages] = {0, 0, 0, 0};
+  uint64_t launches[kStages] = {0, 0, 0, 0};
+};
+
+struct floe_gpu_layer {
+  uint32_t dh = 0, di = 0, E = 0, top_k = 0, bits = 0, g = 0;
+  bool mix_f16 = false, fast_k1 = false, fast_k2 = false;
+  float *router = nullptr;
+  void *mixing = nullptr;
+  ExpertDesc *table = nullptr;
+};
+
+struct floe_gpu_predictor {
+  uint32_t layers = 0, experts = 0, dh = 0;
+  float *w = nullptr, *b = nullptr;
+};
+
+namespace {
+
+// ---- stage profiling --------------------------------------------------------
+cudaEvent_t take_event(floe_gpu_workspace *ws) {
+  if (!ws->pool.empty()) {
+    cudaEvent_t e = ws->pool.back();
+    ws->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct StageScope {  // records [a, b] around one kernel when profiling is on
+  floe_gpu_workspace *ws;
+  int stage;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  StageScope(floe_gpu_workspace *w, int s, cudaStream_t stream) : ws(w), stage(s), st(stream) {
+    if (ws && ws->profiling) {
+      a = take_event(ws);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~StageScope() {
+    if (a) {
+      cudaEvent_t b = take_event(ws);
+      cudaEventRecord(b, st);
+      ws->pending.push_back({stage, a, b});
+    }
+  }
+};
+
+// ---- launch helpers -------------------------------------------------------
+template <typename F>
+int set_smem(F *fn, uint32_t bytes) {
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess)
+    return fail(FLOE_ERR_CUDA, "set_smem: cudaFuncSetAttribute(%u B): %s", bytes,
+                cudaGetErrorString(e));
+  return FLOE_OK;
+}
+
+struct K1Launch {
+  const ExpertDesc *table;
+  const uint32_t *sel;
+  uint32_t slots, dh, di, bits, g;
+  bool fast;
+  int use_thr;
+  float thr;
+  const float *x;
+  float *v_out;
+  uint8_t *mask_out;
+  uint32_t *kept_out, *n_kept_out;
+  float *y_zero;
+};
+
+int launch_k1(const K1Launch &L, floe_gpu_workspace *ws, cudaStream_t st) {
+  K1Args a{};
+  a.table = L.table;
+  a.sel = L.sel;
+  a.x = L.x;
+  a.dh = L.dh;
+  a.di = L.di;
+  a.bits = L.bits;
+  a.group_size = L.g;
+  a.use_threshold = L.use_thr;
+  a.threshold = L.thr;
+  a.v_out = L.v_out;
+  a.mask_out = L.mask_out;
+  a.kept_idx = ws->kept_idx;
+  a.kept_v = ws->kept_v;
+  a.count = ws->count;
+  a.count_final = ws->count_final;
+  a.done = ws->done;
+  a.tile_ctr = ws->tile_ctr;
+  a.stats = ws->stats;
+  a.n_kept_out = L.n_kept_out;
+  a.kept_out = L.kept_out;
+  a.y_zero = L.y_zero;
+  const int tpb = fast_tpb(L.dh);
+  const int sm = device_info().sm;
+  StageScope prof(ws, kStageK1, st);
+  if (L.fast && (tpb == 256 || tpb == 128)) {
+    constexpr int NS = 4;
+    const uint32_t gpc = L.dh / L.g;
+    const uint32_t smem = NS * floe_k::k1_stage_bytes(tpb, gpc);
+    const uint32_t n_tiles = (L.di + floe_k::kK1Ch - 1) / floe_k::kK1Ch;
+    const uint32_t per_slot = std::max<uint32_t>(1, (2u * sm) / L.slots);
+    dim3 grid(std::min(n_tiles, per_slot), L.slots);
+    if (tpb == 256) {
+      if (int rc = set_smem(floe_k::k1_int2<256, NS>, smem)) return rc;
+      floe_k::k1_int2<256, NS><<<grid, 256, smem, st>>>(a);
+    } else {
+      if (int rc = set_smem(floe_k::k1_int2<128, NS>, smem)) return rc;
+      floe_k::k1_int2<128, NS><<<grid, 128, smem, st>>>(a);
+    }
+  } else {
+    dim3 grid((L.di + 255) / 256, L.slots);
+    floe_k::k1_generic<<<grid, 256, 0, st>>>(a);
+  }
+  CK_LAUNCH();
+  return FLOE_OK;
+}
+
+struct K2Launch {
+  const ExpertDesc *table;
+  const uint32_t *sel;
+  const float *weights;
+  uint32_t slots, dh, di;
+  bool fast;
+  const float *x;
+  float *y;
+};
+
+int launch_k2(const K2Launch &L, floe_gpu_workspace *ws, cudaStream_t st) {
+  K2Args a{};
+  a.table = L.table;
+  a.sel = L.sel;
+  a.weights = L.weights;
+  a.x = L.x;
+  a.dh = L.dh;
+  a.di = L.di;
+  a.slots = L.slots;
+  a.kept_idx = ws->kept_idx;
+  a.kept_v = ws->kept_v;
+  a.count_final = ws->count_final;
+  a.y = L.y;
+  const int sm = device_info().sm;
+  const int tpb = fast_tpb(L.dh);
+  StageScope prof(ws, kStageK2, st);
+  if (L.fast && (tpb == 256 || tpb == 128)) {
+    constexpr int NS = 4;
+    const uint32_t smem = NS * 4u * L.dh;
+    if (tpb == 256) {
+      if (int rc = set_smem(floe_k::k2_gate_down<256, NS>, smem)) return rc;
+      floe_k::k2_gate_down<256, NS><<<2 * sm, 256, smem, st>>>(a);
+    } else {
+      if (int rc = set_smem(floe_k::k2_gate_down<128, NS>, smem)) return rc;
+      floe_k::k2_gate_down<128, NS><<<2 * sm, 128, smem, st>>>(a);
+    }
+  } else {
+    floe_k::k2_generic<<<4 * sm, 128, 0, st>>>(a);
+  }
+  CK_LAUNCH();
+  return FLOE_OK;
+}
+
+int check_ws(const char *fn, const floe_gpu_workspace *ws, uint32_t dh, uint32_t di,
+             uint32_t slots) {
+  if (!ws) return fail(FLOE_ERR_INVALID, "%s: null workspace", fn);
+  if (ws->dh < dh || ws->di < di || ws->slots < slots)
+    return fail(FLOE_ERR_INVALID,
+                "%s: workspace too small (have dh=%u di=%u slots=%u, need %u/%u/%u)", fn,
+                ws->dh, ws->di, ws->slots, dh, di, slots);
+  return FLOE_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char *floe_gpu_last_error(void) { return g_err.c_str(); }
+int floe_gpu_abi_version(void) { return FLOE_GPU_ABI_VERSION; }
+
+int floe_gpu_device_info(int *sm_count, int *cc_major, int *cc_minor, size_t *total_mem) {
+  const DeviceInfo &d = device_info();
+  if (sm_count) *sm_count = d.sm;
+  if (cc_major) *cc_major = d.major;
+  if (cc_minor) *cc_minor = d.minor;
+  if (total_mem) *total_mem = d.mem;
+  if (!d.ok) return fail(FLOE_ERR_CUDA, "floe_gpu_device_info: %s", d.err.c_str());
+  return FLOE_OK;
+}
+
+// ---------------------------------------------------------------- experts --
+int floe_gpu_expert_create(const floe_expert_host_view *v, floe_gpu_expert **out) {
+  if (!v || !out) return fail(FLOE_ERR_INVALID, "expert_create: null argument");
+  *out = nullptr;
+  if (int rc = require_device("expert_create")) return rc;
+  if (v->d_hidden == 0 || v->d_intermediate == 0)
+    return fail(FLOE_ERR_INVALID, "expert_create: all dimensions must be >= 1");
+  if (!bits_ok(v->bits))
+    return fail(FLOE_ERR_INVALID, "quantize: bits must be one of {1,2,3,4,8}");
+  const uint64_t n = (uint64_t)v->d_hidden * v->d_intermediate;
+  if (v->group_size == 0 || n % v->group_size != 0)
+    return fail(FLOE_ERR_INVALID, "quantize: group_size must divide element count");
+  if (!v->codes || !v->scales || !v->zeros)
+    return fail(FLOE_ERR_INVALID, "expert_create: codes/scales/zeros required");
+  const bool have_f32 = v->gate_f32 && v->down_f32;
+  if (have_f32 == (v->records_f16 != nullptr))
+    return fail(FLOE_ERR_INVALID,
+                "expert_create: give exactly one of gate_f32+down_f32 or records_f16");
+  const bool on_device = (v->flags & FLOE_VIEW_DEVICE) != 0;
+
+  auto *e = new (std::nothrow) floe_gpu_expert();
+  if (!e) return fail(FLOE_ERR_OOM, "expert_create: host allocation failed");
+  e->dh = v->d_hidden;
+  e->di = v->d_intermediate;
+  e->bits = v->bits;
+  e->g = v->group_size;
+  e->threshold = v->threshold;
+  e->code_bytes = packed_code_bytes(n, v->bits);
+  e->n_groups = n / v->group_size;
+  const int tpb = fast_tpb(e->dh);
+  e->fast_k1 = tpb && e->bits == 2 && e->g % 16 == 0 && e->dh % e->g == 0;
+  e->fast_k2 = tpb != 0;
+
+  // One allocation, 256-B aligned sections: [desc][codes][scales][zeros][records]
+  const uint64_t o_codes = up256(sizeof(ExpertDesc));
+  const uint64_t o_scales = up256(o_codes + e->code_bytes);
+  const uint64_t o_zeros = up256(o_scales + 2 * e->n_groups);
+  const uint64_t o_rec = up256(o_zeros + 2 * e->n_groups);
+  const uint64_t total = o_rec + 4 * n;
+  cudaError_t ce = cudaMalloc(&e->block, total);
+  if (ce != cudaSuccess) {
+    delete e;
+    return fail(FLOE_ERR_OOM, "expert_create: cudaMalloc(%llu) failed: %s",
+                (unsigned long long)total, cudaGetErrorString(ce));
+  }
+  char *base = static_cast<char *>(e->block);
+  e->dev_desc = reinterpret_cast<ExpertDesc *>(base);
+  e->host_desc.codes = reinterpret_cast<const uint8_t *>(base + o_codes);
+  e->host_desc.scales = reinterpret_cast<const uint16_t *>(base + o_scales);
+  e->host_desc.zeros = reinterpret_cast<const uint16_t *>(base + o_zeros);
+  e->host_desc.records = reinterpret_cast<const __half *>(base + o_rec);
+  e->host_desc.threshold = v->threshold;
+
+  auto cleanup = [&](int rc) {
+    cudaFree(e->block);
+    delete e;
+    return rc;
+  };
+  cudaStream_t st;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess)
+    return cleanup(fail(FLOE_ERR_CUDA, "expert_create: stream creation failed"));
+  cudaError_t err = cudaSuccess;
+  auto cp = [&](void *dst, const void *src, size_t bytes) {
+    if (err == cudaSuccess) err = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st);
+  };
+  cp(e->dev_desc, &e->host_desc, sizeof(ExpertDesc));
+  cp(base + o_codes, v->codes, e->code_bytes);
+  cp(base + o_scales, v->scales, 2 * e->n_groups);
+  cp(base + o_zeros, v->zeros, 2 * e->n_groups);
+  __half *rec = reinterpret_cast<__half *>(base + o_rec);
+  if (v->records_f16) {
+    cp(rec, v->records_f16, 4 * n);
+  } else if (on_device) {
+    if (err == cudaSuccess) {
+      floe_k::pack_records<<<4096, 256, 0, st>>>(v->gate_f32, v->down_f32, e->dh, e->di, rec);
+      err = cudaGetLastError();
+    }
+  } else {
+    // Stage host f32 gate/down through a bounded device buffer, convert with RNE.
+    const uint64_t chunk_ch = std::max<uint64_t>(1, (64ull << 20) / (8ull * e->dh));
+    const uint64_t tmp_ch = std::min<uint64_t>(chunk_ch, e->di);
+    float *tmp = nullptr;
+    if (err == cudaSuccess) err = cudaMalloc(&tmp, 8ull * e->dh * tmp_ch);
+    for (uint64_t c0 = 0; c0 < e->di && err == cudaSuccess; c0 += tmp_ch) {
+      const uint64_t nc = std::min<uint64_t>(tmp_ch, e->di - c0);
+      cp(tmp, v->gate_f32 + c0 * e->dh, 4ull * e->dh * nc);
+      cp(tmp + (uint64_t)e->dh * tmp_ch, v->down_f32 + c0 * e->dh, 4ull * e->dh * nc);
+      if (err == cudaSuccess) {
+        floe_k::pack_records<<<1024, 256, 0, st>>>(tmp, tmp + (uint64_t)e->dh * tmp_ch, e->dh,
+                                                   nc, rec + c0 * 2 * e->dh);
+        err = cudaGetLastError();
+      }
+      if (err == cudaSuccess) err = cudaStreamSynchronize(st);  // tmp reused next chunk
+    }
+    if (tmp) cudaFree(tmp);
+  }
+  if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  if (err != cudaSuccess)
+    return cleanup(fail(FLOE_ERR_CUDA, "expert_create: upload failed: %s",
+                        cudaGetErrorString(err)));
+  *out = e;
+  return FLOE_OK;
+}
+
+int floe_gpu_expert_destroy(floe_gpu_expert *e) {
+  if (!e) return FLOE_OK;
+  cudaFree(e->block);
+  delete e;
+  return FLOE_OK;
+}
+
+int floe_gpu_expert_info(const floe_gpu_expert *e, floe_expert_info *info) {
+  if (!e || !info) return fail(FLOE_ERR_INVALID, "expert_info: null argument");
+  info->d_hidden = e->dh;
+  info->d_intermediate = e->di;
+  info->bits = e->bits;
+  info->group_size = e->g;
+  info->threshold = e->threshold;
+  info->code_bytes = e->code_bytes;
+  info->meta_bytes = 4 * e->n_groups;
+  info->record_bytes = 4ull * e->dh;
+  info->fast_path = e->fast_k1 && e->fast_k2;
+  return FLOE_OK;
+}
+
+int floe_gpu_expert_set_threshold(floe_gpu_expert *e, float t) {
+  if (!e) return fail(FLOE_ERR_INVALID, "expert_set_threshold: null expert");
+  e->threshold = t;
+  e->host_desc.threshold = t;
+  CK(cudaMemcpy(e->dev_desc, &e->host_desc, sizeof(ExpertDesc), cudaMemcpyHostToDevice));
+  return FLOE_OK;
+}
+
+// -------------------------------------------------------------- workspace --
+int floe_gpu_workspace_create(uint32_t dh, uint32_t di, uint32_t slots,
+                              floe_gpu_workspace **out) {
+  if (!out) return fail(FLOE_ERR_INVALID, "workspace_create: null argument");
+  *out = nullptr;
+  if (int rc = require_device("workspace_create")) return rc;
+  if (dh == 0 || di == 0 || slots == 0 || slots > (uint32_t)floe_k::kMaxSlots)
+    return fail(FLOE_ERR_INVALID, "workspace_create: need dh, di >= 1 and 1 <= slots <= %d",
+                floe_k::kMaxSlots);
+  auto *w = new (std::nothrow) floe_gpu_workspace();
+  if (!w) return fail(FLOE_ERR_OOM, "workspace_create: host allocation failed");
+  w->dh = dh;
+  w->di = di;
+  w->slots = slots;
+  const uint64_t sd = (uint64_t)slots * di;
+  const int MS = floe_k::kMaxSlots;
+  uint64_t o = 0;
+  const uint64_t o_idx = o;   o = up256(o + 4 * sd);
+  const uint64_t o_kv = o;    o = up256(o + 4 * sd);
+  const uint64_t o_cnt = o;   o = up256(o + 4 * 4 * MS);
+  const uint64_t o_st = o;    o = up256(o + 16);
+  const uint64_t o_sel = o;   o = up256(o + 4 * MS);
+  const uint64_t o_w = o;     o = up256(o + 4 * MS);
+  const uint64_t o_u = o;     o = up256(o + 4ull * dh);
+  const uint64_t o_x = o;     o = up256(o + 4ull * dh);
+  const uint64_t o_y = o;     o = up256(o + 4ull * dh);
+  const uint64_t o_v = o;     o = up256(o + 4 * sd);
+  const uint64_t o_m = o;     o = up256(o + sd);
+  cudaError_t ce = cudaMalloc(&w->block, o);
+  if (ce != cudaSuccess) {
+    delete w;
+    return fail(FLOE_ERR_OOM, "workspace_create: cudaMalloc failed: %s", cudaGetErrorString(ce));
+  }
+  char *b = static_cast<char *>(w->block);
+  w->kept_idx = reinterpret_cast<uint32_t *>(b + o_idx);
+  w->kept_v = reinterpret_cast<float *>(b + o_kv);
+  w->count = reinterpret_cast<uint32_t *>(b + o_cnt);
+  w->count_final = w->count + MS;
+  w->done = w->count + 2 * MS;
+  w->tile_ctr = w->count + 3 * MS;
+  w->stats = reinterpret_cast<unsigned long long *>(b + o_st);
+  w->sel = reinterpret_cast<uint32_t *>(b + o_sel);
+  w->weights = reinterpret_cast<float *>(b + o_w);
+  w->u = reinterpret_cast<float *>(b + o_u);
+  w->x = reinterpret_cast<float *>(b + o_x);
+  w->y = reinterpret_cast<float *>(b + o_y);
+  w->v = reinterpret_cast<float *>(b + o_v);
+  w->mask = reinterpret_cast<uint8_t *>(b + o_m);
+  ce = cudaMemset(w->block, 0, o);
+  if (ce == cudaSuccess) ce = cudaMallocHost(&w->hx, 4ull * dh);
+  if (ce == cudaSuccess) ce = cudaMallocHost(&w->hy, 4ull * dh);
+  if (ce == cudaSuccess) ce = cudaMallocHost(&w->hv, 4 * sd);
+  if (ce == cudaSuccess) ce = cudaMallocHost(reinterpret_cast<void **>(&w->hmask), sd);
+  if (ce == cudaSuccess) ce = cudaMallocHost(reinterpret_cast<void **>(&w->hstats), 16);
+  if (ce == cudaSuccess) ce = cudaDeviceSynchronize();
+  if (ce != cudaSuccess) {
+    floe_gpu_workspace_destroy(w);
+    return fail(FLOE_ERR_OOM, "workspace_create: %s", cudaGetErrorString(ce));
+  }
+  *out = w;
+  return FLOE_OK;
+}
+
+int floe_gpu_workspace_destroy(floe_gpu_workspace *w) {
+  if (!w) return FLOE_OK;
+  for (auto &p : w->pending) {
+    cudaEventDestroy(p.a);
+    cudaEventDestroy(p.b);
+  }
+  for (auto e : w->pool) cudaEventDestroy(e);
+  if (w->block) cudaFree(w->block);
+  if (w->hx) cudaFreeHost(w->hx);
+  if (w->hy) cudaFreeHost(w->hy);
+  if (w->hv) cudaFreeHost(w->hv);
+  if (w->hmask) cudaFreeHost(w->hmask);
+  if (w->hstats) cudaFreeHost(w->hstats);
+  delete w;
+  return FLOE_OK;
+}
+
+int floe_gpu_workspace_reset_counters(floe_gpu_workspace *w, floe_stream_t stream) {
+  if (!w) return fail(FLOE_ERR_INVALID, "workspace_reset_counters: null workspace");
+  CK(cudaMemsetAsync(w->stats, 0, 16, S(stream)));
+  return FLOE_OK;
+}
+
+int floe_gpu_workspace_read_counters(floe_gpu_workspace *w, uint64_t *calls,
+                                     uint64_t *kept_total, floe_stream_t stream) {
+  if (!w) return fail(FLOE_ERR_INVALID, "workspace_read_counters: null workspace");
+  CK(cudaMemcpyAsync(w->hstats, w->stats, 16, cudaMemcpyDeviceToHost, S(stream)));
+  CK(cudaStreamSynchronize(S(stream)));
+  if (calls) *calls = w->hstats[0];
+  if (kept_total) *kept_total = w->hstats[1];
+  return FLOE_OK;
+}
+
+int floe_gpu_workspace_set_profiling(floe_gpu_workspace *w, int enable) {
+  if (!w) return fail(FLOE_ERR_INVALID, "workspace_set_profiling: null workspace");
+  w->profiling = enable != 0;
+  return FLOE_OK;
+}
+
+int floe_gpu_workspace_read_profile(floe_gpu_workspace *w, double *ms, uint64_t *launches) {
+  if (!w) return fail(FLOE_ERR_INVALID, "workspace_read_profile: null workspace");
+  for (auto &p : w->pending) {
+    CK(cudaEventSynchronize(p.b));
+    float t = 0.0f;
+    CK(cudaEventElapsedTime(&t, p.a, p.b));
+    w->ms[p.stage] += t;
+    w->launches[p.stage] += 1;
+    w->pool.push_back(p.a);
+    w->pool.push_back(p.b);
+  }
+  w->pending.clear();
+  for (int s = 0; s < kStages; ++s) {
+    if (ms) ms[s] = w->ms[s];
+    if (launches) launches[s] = w->launches[s];
+    w->ms[s] = 0.0;
+    w->launches[s] = 0;
+  }
+  return FLOE_OK;
+}
+
+// --------------------------------------------------------------- hot path --
+int floe_gpu_expert_forward_sparse(const floe_gpu_expert *e, floe_gpu_workspace *ws,
+                                   const float *x, float *y, float *v_out,
+                                   uint8_t *mask_out, uint32_t *kept_out,
+                                   uint32_t *n_kept_out, floe_stream_t stream) {
+  if (!e || !x || !y) return fail(FLOE_ERR_INVALID, "expert_forward_sparse: null argument");
+  if (int rc = check_ws("expert_forward_sparse", ws, e->dh, e->di, 1)) return rc;
+  K1Launch k1{e->dev_desc, nullptr, 1, e->dh, e->di, e->bits, e->g, e->fast_k1, 0, 0.0f,
+              x, v_out, mask_out, kept_out, n_kept_out, y};
+  if (int rc = launch_k1(k1, ws, S(stream))) return rc;
+  K2Launch k2{e->dev_desc, nullptr, nullptr, 1, e->dh, e->di, e->fast_k2, x, y};
+  return launch_k2(k2, ws, S(stream));
+}
+
+int floe_gpu_expert_forward_sparse_host(const floe_gpu_expert *e, floe_gpu_workspace *ws,
+                                        const float *x_host, float *y_host, float *v_host,
+                                        uint8_t *mask_host, floe_stream_t stream) {
+  if (!e || !x_host || !y_host)
+    return fail(FLOE_ERR_INVALID, "expert_forward_sparse: null argument");
+  if (int rc = check_ws("expert_forward_sparse", ws, e->dh, e->di, 1)) return rc;
+  cudaStream_t st = S(stream);
+  std::memcpy(ws->hx, x_host, 4ull * e->dh);
+  CK(cudaMemcpyAsync(ws->x, ws->hx, 4ull * e->dh, cudaMemcpyHostToDevice, st));
+  if (int rc = floe_gpu_expert_forward_sparse(e, ws, ws->x, ws->y, v_host ? ws->v : nullptr,
+                                              mask_host ? ws->mask : nullptr, nullptr,
+                                              nullptr, stream))
+    return rc;
+  CK(cudaMemcpyAsync(ws->hy, ws->y, 4ull * e->dh, cudaMemcpyDeviceToHost, st));
+  if (v_host) CK(cudaMemcpyAsync(ws->hv, ws->v, 4ull * e->di, cudaMemcpyDeviceToHost, st));
+  if (mask_host) CK(cudaMemcpyAsync(ws->hmask, ws->mask, e->di, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::memcpy(y_host, ws->hy, 4ull * e->dh);
+  if (v_host) std::memcpy(v_host, ws->hv, 4ull * e->di);
+  if (mask_host) std::memcpy(mask_host, ws->hmask, e->di);
+  return FLOE_OK;
+}
+
+int floe_gpu_qgemv_channels(const floe_gpu_expert *e, floe_gpu_workspace *ws,
+                            const float *x, float *v_out, floe_stream_t stream) {
+  if (!e || !x || !v_out) return fail(FLOE_ERR_INVALID, "qgemv_channels: null argument");
+  if (int rc = check_ws("qgemv_channels", ws, e->dh, e->di, 1)) return rc;
+  K1Launch k1{e->dev_desc, nullptr, 1, e->dh, e->di, e->bits, e->g, e->fast_k1, 1,
+              __builtin_inff(), x, v_out, nullptr, nullptr, nullptr, nullptr};
+  return launch_k1(k1, ws, S(stream));
+}
+
+int floe_gpu_dequantize_up(const floe_gpu_expert *e, float *out, floe_stream_t stream) {
+  if (!e || !out) return fail(FLOE_ERR_INVALID, "dequantize: null argument");
+  const uint64_t n = (uint64_t)e->dh * e->di;
+  floe_k::dequant_up<<<4 * device_info().sm, 256, 0, S(stream)>>>(e->dev_desc, n, e->bits,
+                                                                   e->g, out);
+  CK_LAUNCH();
+  return FLOE_OK;
+}
+
+int floe_gpu_predict_mask(const floe_gpu_expert *next, floe_gpu_workspace *ws,
+                          const float *x_prev, float t, uint8_t *mask_out,
+                          uint32_t *kept_out, uint32_t *n_kept_out, floe_stream_t stream) {
+  if (!next || !x_prev) return fail(FLOE_ERR_INVALID, "predict_mask: null argument");
+  if (int rc = check_ws("predict_mask", ws, next->dh, next->di, 1)) return rc;
+  K1Launch k1{next->dev_desc, nullptr, 1, next->dh, next->di, next->bits, next->g,
+              next->fast_k1, 1, t, x_prev, nullptr, mask_out, kept_out, n_kept_out, nullptr};
+  return launch_k1(k1, ws, S(stream));
+}
+
+// ----------------------------------------------------------------- layers --
+int floe_gpu_layer_create(const floe_layer_host_view *v, floe_gpu_layer **out) {
+  if (!v || !out) return fail(FLOE_ERR_INVALID, "layer_create: null argument");
+  *out = nullptr;
+  if (int rc = require_device("layer_create")) return rc;
+  if (v->n_experts == 0 || v->d_hidden == 0)
+    return fail(FLOE_ERR_INVALID, "model config: all dimensions must be >= 1");
+  if (v->top_k == 0 || v->top_k > v->n_experts)
+    return fail(FLOE_ERR_INVALID, "model config: need 1 <= top_k <= experts");
+  if (v->n_experts > 32 || v->top_k > (uint32_t)floe_k::kMaxSlots)
+    return fail(FLOE_ERR_UNSUPPORTED, "layer_create: at most 32 experts and top_k <= %d",
+                floe_k::kMaxSlots);
+  if (!v->router || !v->mixing || !v->experts)
+    return fail(FLOE_ERR_INVALID, "layer_create: router, mixing and experts required");
+  const floe_gpu_expert *e0 = v->experts[0];
+  if (!e0) return fail(FLOE_ERR_INVALID, "layer_create: null expert");
+  for (uint32_t i = 0; i < v->n_experts; ++i) {
+    const floe_gpu_expert *e = v->experts[i];
+    if (!e || e->dh != v->d_hidden || e->di != e0->di || e->bits != e0->bits || e->g != e0->g)
+      return fail(FLOE_ERR_INVALID, "layer_create: expert %u shape differs from the layer", i);
+  }
+  auto *l = new (std::nothrow) floe_gpu_layer();
+  if (!l) return fail(FLOE_ERR_OOM, "layer_create: host allocation failed");
+  l->dh = v->d_hidden;
+  l->di = e0->di;
+  l->E = v->n_experts;
+  l->top_k = v->top_k;
+  l->bits = e0->bits;
+  l->g = e0->g;
+  l->mix_f16 = v->mixing_f16 != 0;
+  l->fast_k1 = e0->fast_k1;
+  l->fast_k2 = e0->fast_k2;
+  const uint64_t dh = l->dh;
+  std::vector<ExpertDesc> table(l->E);
+  for (uint32_t i = 0; i < l->E; ++i) table[i] = v->experts[i]->host_desc;
+  cudaError_t ce = cudaMalloc(&l->router, 4ull * l->E * dh);
+  if (ce == cudaSuccess) ce = cudaMalloc(&l->mixing, (l->mix_f16 ? 2ull : 4ull) * dh * dh);
+  if (ce == cudaSuccess) ce = cudaMalloc(&l->table, sizeof(ExpertDesc) * l->E);
+  if (ce == cudaSuccess)
+    ce = cudaMemcpy(l->router, v->router, 4ull * l->E * dh, cudaMemcpyDefault);
+  if (ce == cudaSuccess)
+    ce = cudaMemcpy(l->table, table.data(), sizeof(ExpertDesc) * l->E, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess) {
+    if (!l->mix_f16) {
+      ce = cudaMemcpy(l->mixing, v->mixing, 4ull * dh * dh, cudaMemcpyDefault);
+    } else {
+      float *tmp = nullptr;
+      ce = cudaMalloc(&tmp, 4ull * dh * dh);
+      if (ce == cudaSuccess) ce = cudaMemcpy(tmp, v->mixing, 4ull * dh * dh, cudaMemcpyDefault);
+      if (ce == cudaSuccess) {
+        floe_k::f32_to_f16_rn<<<1024, 256>>>(tmp, dh * dh, static_cast<__half *>(l->mixing));
+        ce = cudaGetLastError();
+      }
+      if (ce == cudaSuccess) ce = cudaDeviceSynchronize();
+      if (tmp) cudaFree(tmp);
+    }
+  }
+  if (ce != cudaSuccess) {
+    floe_gpu_layer_destroy(l);
+    return fail(FLOE_ERR_OOM, "layer_create: %s", cudaGetErrorString(ce));
+  }
+  *out = l;
+  return FLOE_OK;
+}
+
+int floe_gpu_layer_destroy(floe_gpu_layer *l) {
+  if (!l) return FLOE_OK;
+  if (l->router) cudaFree(l->router);
+  if (l->mixing) cudaFree(l->mixing);
+  if (l->table) cudaFree(l->table);
+  delete l;
+  return FLOE_OK;
+}
+
+int floe_gpu_layer_forward(const floe_gpu_layer *l, floe_gpu_workspace *ws, const float *h,
+                           float *y, const floe_gpu_layer_trace *tr, floe_stream_t stream) {
+  if (!l || !h || !y) return fail(FLOE_ERR_INVALID, "layer_forward: null argument");
+  if (int rc = check_ws("layer_forward", ws, l->dh, l->di, l->top_k)) return rc;
+  cudaStream_t st = S(stream);
+  const uint32_t rows_per_block = 8;
+  const size_t smem = 4ull * l->dh;
+  float *u_tr = tr ? tr->block_input_dev : nullptr;
+  {
+    StageScope prof(ws, kStageMixing, st);
+    const dim3 grid((l->dh + rows_per_block - 1) / rows_per_block);
+    if (l->mix_f16)
+      floe_k::mixing_gemv<__half><<<grid, 256, smem, st>>>(static_cast<const __half *>(l->mixing),
+                                                           h, l->dh, ws->u, y, u_tr);
+    else
+      floe_k::mixing_gemv<float><<<grid, 256, smem, st>>>(static_cast<const float *>(l->mixing),
+                                                          h, l->dh, ws->u, y, u_tr);
+    CK_LAUNCH();
+  }
+  {
+    StageScope prof(ws, kStageRoute, st);
+    floe_k::route_topk<<<1, 256, 0, st>>>(l->router, nullptr, ws->u, l->E, l->dh, l->top_k, 1,
+                                          ws->sel, ws->weights, tr ? tr->experts_dev : nullptr,
+                                          tr ? tr->weights_dev : nullptr);
+    CK_LAUNCH();
+  }
+  K1Launch k1{l->table, ws->sel, l->top_k, l->dh, l->di, l->bits, l->g, l->fast_k1, 0, 0.0f,
+              ws->u, nullptr, tr ? tr->masks_dev : nullptr, nullptr, nullptr, nullptr};
+  if (int rc = launch_k1(k1, ws, st)) return rc;
+  K2Launch k2{l->table, ws->sel, ws->weights, l->top_k, l->dh, l->di, l->fast_k2, ws->u, y};
+  return launch_k2(k2, ws, st);
+}
+
+int floe_gpu_layer_forward_host(const floe_gpu_layer *l, floe_gpu_workspace *ws,
+                                const float *h_host, float *y_host, floe_stream_t stream) {
+  if (!l || !h_host || !y_host) return fail(FLOE_ERR_INVALID, "layer_forward: null argument");
+  if (int rc = check_ws("layer_forward", ws, l->dh, l->di, l->top_k)) return rc;
+  cudaStream_t st = S(stream);
+  std::memcpy(ws->hx, h_host, 4ull * l->dh);
+  CK(cudaMemcpyAsync(ws->x, ws->hx, 4ull * l->dh, cudaMemcpyHostToDevice, st));
+  if (int rc = floe_gpu_layer_forward(l, ws, ws->x, ws->y, nullptr, stream)) return rc;
+  CK(cudaMemcpyAsync(ws->hy, ws->y, 4ull * l->dh, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::memcpy(y_host, ws->hy, 4ull * l->dh);
+  return FLOE_OK;
+}
+
+// ------------------------------------------------------- synthetic model ---
+int floe_gpu_gen_normals(uint64_t seed, uint64_t stream_id, uint64_t n, float sigma,
+                         int sharded, float *out, floe_stream_t stream) {
+  if (!out) return fail(FLOE_ERR_INVALID, "gen_normals: null output");
+  if (int rc = require_device("gen_normals")) return rc;
+  if (n == 0) return FLOE_OK;
+  floe_gen::gen_normals<<<8 * device_info().sm, 256, 0, S(stream)>>>(seed, stream_id, n, sigma,
+                                                                     sharded, out);
+  CK_LAUNCH();
+  return FLOE_OK;
+}
+
+int floe_gpu_quantize(const float *x, uint64_t n, uint32_t bits, uint32_t g, uint8_t *codes,
+                      uint16_t *scales, uint16_t *zeros, floe_stream_t stream) {
+  if (!x || !codes || !scales || !zeros) return fail(FLOE_ERR_INVALID, "quantize: null argument");
+  if (int rc = require_device("quantize")) return rc;
+  if (!bits_ok(bits)) return fail(FLOE_ERR_INVALID, "quantize: bits must be one of {1,2,3,4,8}");
+  if (g == 0 || n % g != 0)
+    return fail(FLOE_ERR_INVALID, "quantize: group_size must divide element count");
+  cudaStream_t st = S(stream);
+  const uint64_t groups = n / g;
+  const uint64_t nb = packed_code_bytes(n, bits);
+  const bool aligned = (32 % bits == 0) && ((uint64_t)g * bits) % 32 == 0 &&
+                       (reinterpret_cast<uintptr_t>(codes) & 3) == 0;
+  const int blocks = 8 * device_info().sm;
+  if (aligned) {
+    floe_gen::quantize_groups<<<blocks, 256, 0, st>>>(x, groups, g, bits, codes, scales, zeros, 1);
+    CK_LAUNCH();
+    return FLOE_OK;
+  }
+  // put_code ORs into shared bytes: build in a zeroed, word-padded buffer.
+  uint8_t *tmp = nullptr;
+  const uint64_t tb = ((nb + 3) & ~uint64_t(3)) + 8;
+  CK(cudaMallocAsync(reinterpret_cast<void **>(&tmp), tb, st));
+  CK(cudaMemsetAsync(tmp, 0, tb, st));
+  floe_gen::quantize_groups<<<blocks, 256, 0, st>>>(x, groups, g, bits, tmp, scales, zeros, 0);
+  CK_LAUNCH();
+  CK(cudaMemcpyAsync(codes, tmp, nb, cudaMemcpyDeviceToDevice, st));
+  CK(cudaFreeAsync(tmp, st));
+  return FLOE_OK;
+}
+
+// -------------------------------------------------------------- predictor --
+int floe_gpu_predictor_create(uint32_t layers, uint32_t experts, uint32_t dh,
+                              const float *w, const float *b, floe_gpu_predictor **out) {
+  if (!out || !w || !b) return fail(FLOE_ERR_INVALID, "predictor_create: null argument");
+  *out = nullptr;
+  if (int rc = require_device("predictor_create")) return rc;
+  if (layers < 2) return fail(FLOE_ERR_INVALID, "predictor file: needs at least two layers");
+  if (experts == 0 || experts > 32 || dh == 0)
+    return fail(FLOE_ERR_INVALID, "predictor_create: need 1 <= experts <= 32, d_hidden >= 1");
+  auto *p = new (std::nothrow) floe_gpu_predictor();
+  if (!p) return fail(FLOE_ERR_OOM, "predictor_create: host allocation failed");
+  p->layers = layers;
+  p->experts = experts;
+  p->dh = dh;
+  const uint64_t nw = (uint64_t)(layers - 1) * experts * dh, nb = (uint64_t)(layers - 1) * experts;
+  cudaError_t ce = cudaMalloc(&p->w, 4 * nw);
+  if (ce == cudaSuccess) ce = cudaMalloc(&p->b, 4 * nb);
+  if (ce == cudaSuccess) ce = cudaMemcpy(p->w, w, 4 * nw, cudaMemcpyDefault);
+  if (ce == cudaSuccess) ce = cudaMemcpy(p->b, b, 4 * nb, cudaMemcpyDefault);
+  if (ce != cudaSuccess) {
+    floe_gpu_predictor_destroy(p);
+    return fail(FLOE_ERR_OOM, "predictor_create: %s", cudaGetErrorString(ce));
+  }
+  *out = p;
+  return FLOE_OK;
+}
+
+int floe_gpu_predictor_destroy(floe_gpu_predictor *p) {
+  if (!p) return FLOE_OK;
+  if (p->w) cudaFree(p->w);
+  if (p->b) cudaFree(p->b);
+  delete p;
+  return FLOE_OK;
+}
+
+int floe_gpu_predict_experts(const floe_gpu_predictor *p, const float *x, uint32_t layer,
+                             uint32_t count, uint32_t *out, floe_stream_t stream) {
+  if (!p || !x || !out) return fail(FLOE_ERR_INVALID, "predict_experts: null argument");
+  if (layer == 0)
+    return fail(FLOE_ERR_INVALID, "predict_experts: layer 0 has no lookahead predictor");
+  if (layer >= p->layers) return fail(FLOE_ERR_INVALID, "predict_experts: bad layer");
+  if (count == 0 || count > p->experts) return fail(FLOE_ERR_INVALID, "top_k: k out of range");
+  const uint64_t off = (uint64_t)(layer - 1) * p->experts;
+  floe_k::route_topk<<<1, 256, 0, S(stream)>>>(p->w + off * p->dh, p->b + off, x, p->experts,
+                                               p->dh, count, 0, out, nullptr, nullptr, nullptr);
+  CK_LAUNCH();
+  return FLOE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,405 @@
+// floe_kernels.cuh -- sm_100a kernels of the FloE compressed-expert FFN path.
+//
+// Reference algorithm (paths relative to /root/reference/proj/):
+//   expert_forward_sparse(const CompressedExpert&, const Vec&)  core/src/model.cpp:128-142
+//     v = qgemv_channels(up_q, x)                               core/src/quant.cpp:122-136
+//     keep c iff !(|v[c]| < t)                                  core/src/model.cpp:135
+//     y += silu(gate_c . x) * v[c] * down_c  (kept c only)      core/src/model.cpp:136-140
+//
+// Kernels
+//   K1  k1_int2<TPB,NS>    (floe_fast.cuh) fused INT2 group-dequant GEMV +
+//                          |v|>=t epilogue + compaction, bulk-copy staged
+//   K1g k1_generic         same contract for any bits / group size / d_hidden
+//   K2  k2_gate_down<TPB,NS> (floe_fast.cuh) channel-sparse gate dot + SwiGLU +
+//                          down accumulation over bulk-copied channel records
+//   K2g k2_generic         same contract for any d_hidden
+//   dequant_up             bit-exact f32 dequantisation (debug / parity)
+//   mixing_gemv, route_topk, predict_experts_k   layer glue (model.cpp:83-93,145-169)
+//
+// HBM layout of one expert:
+//   codes    u8 [di][dh*bits/8]  unchanged reference packing (LE in byte)
+//   scales   u16[di][dh/g]       f16 bits, unchanged
+//   zeros    u16[di][dh/g]       f16 bits, unchanged
+//   records  f16[di][2][dh]      gate row c | down row c  (pack_compact wire format)
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cstdint>
+
+namespace floe_k {
+
+constexpr int kMaxSlots = 8;
+
+// Device-side descriptor of one resident expert.
+struct ExpertDesc {
+  const uint8_t *codes;
+  const uint16_t *scales;
+  const uint16_t *zeros;
+  const __half *records;  // [di][2*dh]
+  float threshold;
+  uint32_t pad_[3];
+};
+
+struct K1Args {
+  const ExpertDesc *table;  // expert descriptors
+  const uint32_t *sel;      // nullable: slot j uses table[sel[j]] (else table[j])
+  const float *x;           // f32[dh]
+  uint32_t dh, di, bits, group_size;
+  int use_threshold;        // 1: use `threshold` instead of the expert's
+  float threshold;
+  float *v_out;             // nullable, [slots][di]
+  uint8_t *mask_out;        // nullable, [slots][di]
+  uint32_t *kept_idx;       // [slots][di]  (workspace)
+  float *kept_v;            // [slots][di]  (workspace)
+  uint32_t *count;          // [slots]  running append counters (reset by last CTA)
+  uint32_t *count_final;    // [slots]  published counts for K2 / the caller
+  uint32_t *done;           // [1]      CTA completion counter (reset by last CTA)
+  uint32_t *tile_ctr;       // [slots]  dynamic tile claims (reset by last CTA)
+  unsigned long long *stats;  // nullable [2]: calls, kept channels (running totals)
+  uint32_t *n_kept_out;     // nullable, [slots]
+  uint32_t *kept_out;       // nullable, [slots][di]  caller copy of kept ids
+  float *y_zero;            // nullable: zeroed by CTA 0 (K2 accumulates into it)
+};
+
+struct K2Args {
+  const ExpertDesc *table;
+  const uint32_t *sel;       // nullable
+  const float *weights;      // nullable: per-slot combine weight (routing softmax)
+  const float *x;            // f32[dh]
+  uint32_t dh, di, slots;
+  const uint32_t *kept_idx;  // [slots][di]
+  const float *kept_v;       // [slots][di]
+  const uint32_t *count_final;  // [slots]
+  float *y;                  // f32[dh], accumulated with fp32 reductions
+};
+
+__device__ __forceinline__ float h2f(uint16_t h) {
+  return __half2float(__ushort_as_half(h));
+}
+
+__device__ __forceinline__ uint32_t ldg_stream_u32(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ uint4 ldg_stream_u128(const void *p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void red_add_v4(float *p, float a, float b, float c,
+                                           float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a),
+               "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
+// silu(z) = z / (1 + e^-z)  (core/src/la.cpp:31), IEEE division and expf.
+__device__ __forceinline__ float silu_ref(float z) { return z / (1.0f + expf(-z)); }
+
+// Reference get_code (core/src/quant.cpp:35-41) over a byte array.
+__device__ __forceinline__ uint32_t get_code(const uint8_t *codes, uint32_t bits,
+                                             uint64_t i) {
+  uint64_t bit = i * bits;
+  uint64_t idx = bit >> 3;
+  uint32_t off = (uint32_t)(bit & 7);
+  uint32_t v = (uint32_t)codes[idx] >> off;
+  if (off + bits > 8) v |= (uint32_t)codes[idx + 1] << (8 - off);
+  return v & ((1u << bits) - 1);
+}
+
+// ---------------------------------------------------------------------------
+// K1 epilogue shared by both K1 variants: threshold, outputs, compaction.
+// Called by one full warp; lane handles channel `c` (valid if c < di).
+__device__ __forceinline__ void k1_emit(const K1Args &a, uint32_t slot, uint32_t c,
+                                        bool valid, float v, float thr) {
+  const uint32_t lane = threadIdx.x & 31;
+  // model.cpp:135: `if (fabs(v) < t) continue;` -> NaN is kept, ties kept.
+  const bool keep = valid && !(fabsf(v) < thr);
+  const size_t off = (size_t)slot * a.di + c;
+  if (valid) {
+    if (a.v_out) a.v_out[off] = v;
+    if (a.mask_out) a.mask_out[off] = keep ? 1 : 0;
+  }
+  const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+  if (bal) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(&a.count[slot], (uint32_t)__popc(bal));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (keep) {
+      const uint32_t pos = base + __popc(bal & ((1u << lane) - 1));
+      const size_t o = (size_t)slot * a.di + pos;
+      a.kept_idx[o] = c;
+      a.kept_v[o] = v;
+      if (a.kept_out) a.kept_out[o] = c;
+    }
+  }
+}
+
+// Last-CTA bookkeeping: publish counts, reset the running counters so the
+// next stream-ordered call starts from zero (no memset node needed).
+__device__ __forceinline__ void k1_finish(const K1Args &a, uint32_t slots) {
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const uint32_t total = gridDim.x * gridDim.y;
+    last = atomicAdd(a.done, 1u) == total - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x < slots) {
+    __threadfence();
+    const uint32_t n = atomicExch(&a.count[threadIdx.x], 0u);
+    a.count_final[threadIdx.x] = n;
+    if (a.n_kept_out) a.n_kept_out[threadIdx.x] = n;
+    if (a.tile_ctr) a.tile_ctr[threadIdx.x] = 0;
+    if (a.stats) atomicAdd(&a.stats[1], (unsigned long long)n);
+    if (threadIdx.x == 0) {
+      *a.done = 0;
+      if (a.stats) atomicAdd(&a.stats[0], 1ull);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1 generic: any bits in {1,2,3,4,8}, any group size dividing n, any dh.
+// One warp per channel; per element the reference's own dequantize_at
+// expression (quant.cpp:104-109): float(code)*scale + zero.
+__global__ void __launch_bounds__(256) k1_generic(const K1Args a) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t slot = blockIdx.y;
+  const uint32_t e = a.sel ? a.sel[slot] : slot;
+  const ExpertDesc d = a.table[e];
+  const float thr = a.use_threshold ? a.threshold : d.threshold;
+  if (a.y_zero && blockIdx.x == 0 && slot == 0)
+    for (uint32_t i = threadIdx.x; i < a.dh; i += blockDim.x) a.y_zero[i] = 0.0f;
+
+  for (uint32_t cb = blockIdx.x * 8 * 32; cb < a.di; cb += gridDim.x * 8 * 32) {
+    // each warp handles 32 consecutive channels, one at a time, then emits
+    const uint32_t wc0 = cb + warp * 32;
+    float vmine = 0.0f;
+    for (uint32_t j = 0; j < 32; ++j) {
+      const uint32_t c = wc0 + j;
+      float acc = 0.0f;
+      if (c < a.di) {
+        const uint64_t base = (uint64_t)c * a.dh;
+        for (uint32_t k = lane; k < a.dh; k += 32) {
+          const uint64_t i = base + k;
+          const uint64_t g = i / a.group_size;
+          const float w = fmaf((float)get_code(d.codes, a.bits, i), h2f(d.scales[g]),
+                               h2f(d.zeros[g]));
+          acc = fmaf(w, a.x[k], acc);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == j) vmine = acc;
+    }
+    const uint32_t c = wc0 + lane;
+    k1_emit(a, slot, c, c < a.di, vmine, thr);
+  }
+  k1_finish(a, gridDim.y);
+}
+
+// ---------------------------------------------------------------------------
+// Map a flattened kept-entry index to (slot, channel, v).
+struct KeptEntry {
+  uint32_t slot, c;
+  float v;
+};
+
+__device__ __forceinline__ KeptEntry kept_entry(const K2Args &a, uint32_t p) {
+  uint32_t slot = 0;
+  uint32_t q = p;
+  while (slot + 1 < a.slots && q >= a.count_final[slot]) {
+    q -= a.count_final[slot];
+    ++slot;
+  }
+  KeptEntry k;
+  k.slot = slot;
+  const size_t o = (size_t)slot * a.di + q;
+  k.c = a.kept_idx[o];
+  k.v = a.kept_v[o];
+  return k;
+}
+
+__device__ __forceinline__ float slot_weight(const K2Args &a, uint32_t slot) {
+  return a.weights ? a.weights[slot] : 1.0f;
+}
+
+// ---------------------------------------------------------------------------
+// K2 generic: one CTA per kept entry (grid-stride), fp32 atomics into y.
+__global__ void __launch_bounds__(128) k2_generic(const K2Args a) {
+  uint32_t total = 0;
+  for (uint32_t s = 0; s < a.slots; ++s) total += a.count_final[s];
+  __shared__ float red[4];
+  for (uint32_t p = blockIdx.x; p < total; p += gridDim.x) {
+    const KeptEntry k = kept_entry(a, p);
+    const uint32_t e = a.sel ? a.sel[k.slot] : k.slot;
+    const __half *rec = a.table[e].records + (size_t)k.c * 2 * a.dh;
+    float acc = 0.0f;
+    for (uint32_t i = threadIdx.x; i < a.dh; i += blockDim.x)
+      acc = fmaf(__half2float(rec[i]), a.x[i], acc);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    const float g = red[0] + red[1] + red[2] + red[3];
+    __syncthreads();
+    const float aco = silu_ref(g) * k.v * slot_weight(a, k.slot);
+    for (uint32_t i = threadIdx.x; i < a.dh; i += blockDim.x)
+      atomicAdd(&a.y[i], aco * __half2float(rec[a.dh + i]));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// dequantize (quant.cpp:104-120): out[i] = float(code)*scale + zero.  The
+// product is exact (<= 8+11 significant bits), so one fmaf rounds exactly
+// like the reference's mul-then-add: bit-exact.
+__global__ void dequant_up(const ExpertDesc *table, uint64_t n, uint32_t bits,
+                           uint32_t group_size, float *out) {
+  const ExpertDesc d = table[0];
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t g = i / group_size;
+    out[i] = fmaf((float)get_code(d.codes, bits, i), h2f(d.scales[g]), h2f(d.zeros[g]));
+  }
+}
+
+// f32 -> f16 records with IEEE RNE (== floe::f32_to_f16 for finite values).
+__global__ void pack_records(const float *gate, const float *down, uint32_t dh,
+                             uint64_t di, __half *records) {
+  const uint64_t n = (uint64_t)dh * di;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t c = i / dh, k = i % dh;
+    records[c * 2 * dh + k] = __float2half_rn(gate[i]);
+    records[c * 2 * dh + dh + k] = __float2half_rn(down[i]);
+  }
+}
+
+__global__ void f32_to_f16_rn(const float *in, uint64_t n, __half *out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = __float2half_rn(in[i]);
+}
+
+// ---------------------------------------------------------------------------
+// Layer glue (block_forward, model.cpp:145-169).
+//
+// u = h + mixing.h ; y = u.  Warp per row, mixing in f32 or f16.
+template <typename T>
+__global__ void __launch_bounds__(256) mixing_gemv(const T *__restrict__ m,
+                                                   const float *__restrict__ h,
+                                                   uint32_t dh, float *u,
+                                                   float *y_init, float *u_trace) {
+  extern __shared__ float hs[];
+  for (uint32_t i = threadIdx.x; i < dh; i += blockDim.x) hs[i] = h[i];
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (row >= dh) return;
+  const T *mr = m + (size_t)row * dh;
+  float acc = 0.0f;
+  if constexpr (sizeof(T) == 2) {
+    for (uint32_t k = lane * 8; k < dh; k += 256) {
+      const uint4 q = ldg_stream_u128(mr + k);
+      const __half2 *hh = reinterpret_cast<const __half2 *>(&q);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __half22float2(hh[i]);
+        acc = fmaf(f.x, hs[k + 2 * i], acc);
+        acc = fmaf(f.y, hs[k + 2 * i + 1], acc);
+      }
+    }
+  } else {
+    for (uint32_t k = lane * 4; k < dh; k += 128) {
+      const uint4 q = ldg_stream_u128(mr + k);
+      acc = fmaf(__uint_as_float(q.x), hs[k], acc);
+      acc = fmaf(__uint_as_float(q.y), hs[k + 1], acc);
+      acc = fmaf(__uint_as_float(q.z), hs[k + 2], acc);
+      acc = fmaf(__uint_as_float(q.w), hs[k + 3], acc);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) {
+    const float uu = hs[row] + 1.0f * acc;  // drift_scale = 1 (model.cpp:151-152)
+    u[row] = uu;
+    y_init[row] = uu;
+    if (u_trace) u_trace[row] = uu;
+  }
+}
+
+// top_k (la.cpp:48-61) over a short vector held by one thread.
+__device__ inline void topk_small(const float *v, uint32_t n, uint32_t k,
+                                  uint32_t *out) {
+  uint32_t taken = 0;  // n <= 32
+  for (uint32_t r = 0; r < k; ++r) {
+    int best = -1;
+    for (uint32_t i = 0; i < n; ++i) {
+      if (taken & (1u << i)) continue;
+      if (best < 0 || v[i] > v[best] || (v[i] == v[best] && (int)i < best)) best = (int)i;
+    }
+    taken |= 1u << best;
+    out[r] = (uint32_t)best;
+  }
+  for (uint32_t i = 1; i < k; ++i)
+    for (uint32_t j = i; j > 0 && out[j - 1] > out[j]; --j) {
+      const uint32_t tmp = out[j];
+      out[j] = out[j - 1];
+      out[j - 1] = tmp;
+    }
+}
+
+// logits = W u (+ b); top_k; optional softmax over the selected logits
+// (route, model.cpp:83-93; predict_experts, predictor.cpp:164-177).
+// One CTA, one warp per row.  E <= 32.
+__global__ void __launch_bounds__(256) route_topk(const float *__restrict__ w,
+                                                  const float *__restrict__ b,
+                                                  const float *__restrict__ u,
+                                                  uint32_t E, uint32_t dh,
+                                                  uint32_t k, int softmax,
+                                                  uint32_t *sel, float *weights,
+                                                  uint32_t *sel_trace,
+                                                  float *w_trace) {
+  __shared__ float logits[32];
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t r = warp; r < E; r += blockDim.x / 32) {
+    float acc = 0.0f;
+    for (uint32_t i = lane; i < dh; i += 32) acc = fmaf(w[(size_t)r * dh + i], u[i], acc);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) logits[r] = b ? acc + b[r] : acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t s[32];
+    topk_small(logits, E, k, s);
+    float wv[32];
+    for (uint32_t i = 0; i < k; ++i) wv[i] = logits[s[i]];
+    if (softmax) {  // softmax_inplace (la.cpp:37-46)
+      float mx = wv[0];
+      for (uint32_t i = 1; i < k; ++i)
+        if (mx < wv[i]) mx = wv[i];
+      float sum = 0.0f;
+      for (uint32_t i = 0; i < k; ++i) {
+        wv[i] = expf(wv[i] - mx);
+        sum += wv[i];
+      }
+      for (uint32_t i = 0; i < k; ++i) wv[i] /= sum;
+    }
+    for (uint32_t i = 0; i < k; ++i) {
+      sel[i] = s[i];
+      if (weights) weights[i] = wv[i];
+      if (sel_trace) sel_trace[i] = s[i];
+      if (w_trace) w_trace[i] = wv[i];
+    }
+  }
+}
+
+}  // namespace floe_k
