@@ -49,19 +49,19 @@ __device__ __forceinline__ float dot16_int2(uint32_t w, const float2 (&xs)[8]) {
 // ---------------------------------------------------------------------------
 // K1: v[c] = sum_k deq(up[c,k]) x[k]; keep |v|>=t; compact kept channels.
 //
-// Tiles of 16 channels are claimed dynamically (one atomic per tile, issued
-// NS-1 tiles ahead) and bulk-copied: codes 16*dh/4 B, scales and zeros
-// 16*dh/g*2 B each.  Thread t owns x[16t, 16t+16) (one code word per
-// channel, all in group 16t/g) -- x stays in registers pre-scaled by 4^-i,
-// and the group-affine dequant is folded out of the inner loop:
-//   sum_k (c_k s + z) x_k  =  s * sum_k c_k x_k  +  z * sum_k x_k .
+// CTA b owns channels [di*b/G1, di*(b+1)/G1) (contiguous, balanced to one
+// channel) and walks them in sub-tiles of 16 channels, each bulk-copied:
+// codes 16*dh/4 B, scales and zeros 16*dh/g*2 B.  NS sub-tiles are in flight
+// and nothing on the issue path waits on global memory.  Thread t owns
+// x[16t, 16t+16) (one code word per channel, all in group 16t/g): x stays in
+// registers pre-scaled by 4^-i and the group-affine dequant is folded out of
+// the inner loop:  sum_k (c_k s + z) x_k = s * sum_k c_k x_k + z * sum_k x_k.
 template <int TPB, int NS>
 __global__ void __launch_bounds__(TPB, 2) k1_int2(const K1Args a) {
   constexpr int NW = TPB / 32;
   constexpr int CH = kK1Ch;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t full[NS];
-  __shared__ uint32_t stage_tile[NS];
   __shared__ float wsum[NW][CH];
 
   const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -73,29 +73,27 @@ __global__ void __launch_bounds__(TPB, 2) k1_int2(const K1Args a) {
   const uint32_t code_sz = round_up128(CH * TPB * 4u);
   const uint32_t meta_sz = round_up128(CH * gpc * 2u);
   const uint32_t stage_sz = code_sz + 2 * meta_sz;
-  const uint32_t n_tiles = (a.di + CH - 1) / CH;
+  const uint32_t c_lo = seg_begin(a.di, blockIdx.x, gridDim.x);
+  const uint32_t c_hi = seg_begin(a.di, blockIdx.x + 1, gridDim.x);
+  const uint32_t n_sub = (c_hi - c_lo + CH - 1) / CH;
 
-  auto issue = [&](uint32_t s) {  // thread 0 only
-    const uint32_t tile = atomicAdd(&a.tile_ctr[slot], 1u);
-    stage_tile[s] = tile;
-    if (tile < n_tiles) {
-      const uint32_t c0 = tile * CH;
-      const uint32_t nc = min((uint32_t)CH, a.di - c0);
-      const uint32_t cb = nc * TPB * 4u, mb = nc * gpc * 2u;
-      uint8_t *st = smem + s * stage_sz;
-      floe_ptx::mbar_arrive_expect_tx(&full[s], cb + 2 * mb);
-      floe_ptx::bulk_g2s(st, d.codes + (size_t)c0 * TPB * 4u, cb, &full[s]);
-      floe_ptx::bulk_g2s(st + code_sz, d.scales + (size_t)c0 * gpc, mb, &full[s]);
-      floe_ptx::bulk_g2s(st + code_sz + meta_sz, d.zeros + (size_t)c0 * gpc, mb, &full[s]);
-    }
+  auto issue = [&](uint32_t i) {  // thread 0 only: sub-tile i -> stage i % NS
+    const uint32_t s = i % NS;
+    const uint32_t c0 = c_lo + i * CH;
+    const uint32_t nc = min((uint32_t)CH, c_hi - c0);
+    const uint32_t cb = nc * TPB * 4u, mb = nc * gpc * 2u;
+    uint8_t *st = smem + s * stage_sz;
+    floe_ptx::mbar_arrive_expect_tx(&full[s], cb + 2 * mb);
+    floe_ptx::bulk_g2s(st, d.codes + (size_t)c0 * TPB * 4u, cb, &full[s]);
+    floe_ptx::bulk_g2s(st + code_sz, d.scales + (size_t)c0 * gpc, mb, &full[s]);
+    floe_ptx::bulk_g2s(st + code_sz + meta_sz, d.zeros + (size_t)c0 * gpc, mb, &full[s]);
   };
 
   if (t == 0) {
 #pragma unroll
     for (int s = 0; s < NS; ++s) floe_ptx::mbar_init(&full[s], 1);
     floe_ptx::fence_barrier_init();
-#pragma unroll
-    for (int s = 0; s < NS; ++s) issue(s);
+    for (uint32_t i = 0; i < n_sub && i < (uint32_t)NS; ++i) issue(i);
   }
   if (a.y_zero && blockIdx.x == 0 && slot == 0)
     for (uint32_t i = t; i < a.dh; i += TPB) a.y_zero[i] = 0.0f;
@@ -123,26 +121,28 @@ __global__ void __launch_bounds__(TPB, 2) k1_int2(const K1Args a) {
     for (int p = 0; p < 8; ++p) xs[p] = make_float2(xr[2 * p], xr[2 * p + 1]);
   }
   const uint32_t gcol = (16u * t) / a.group_size;
+  uint32_t running = 0;
   __syncthreads();
 
-  uint32_t phase = 0;  // bit s = parity of stage s
-  for (uint32_t s = 0;; s = (s + 1 == NS) ? 0 : s + 1) {
-    const uint32_t tile = stage_tile[s];
-    if (tile >= n_tiles) break;
-    floe_ptx::mbar_wait(&full[s], (phase >> s) & 1u);
-    phase ^= 1u << s;
+  for (uint32_t i = 0; i < n_sub; ++i) {
+    const uint32_t s = i % NS;
+    floe_ptx::mbar_wait(&full[s], (i / NS) & 1u);
     const uint8_t *st = smem + s * stage_sz;
     const uint32_t *cw = reinterpret_cast<const uint32_t *>(st);
     const uint16_t *sc = reinterpret_cast<const uint16_t *>(st + code_sz);
     const uint16_t *zr = reinterpret_cast<const uint16_t *>(st + code_sz + meta_sz);
-    const uint32_t c0 = tile * CH;
+    const uint32_t c0 = c_lo + i * CH;
+    const uint32_t nc = min((uint32_t)CH, c_hi - c0);
     float part[CH];
 #pragma unroll
     for (int j = 0; j < CH; ++j) {
-      const uint32_t w = cw[j * TPB + t];
-      const float sj = h2f(sc[j * gpc + gcol]);
-      const float zj = h2f(zr[j * gpc + gcol]);
-      part[j] = fmaf(sj, dot16_int2(w, xs), zj * xsum);  // channels past di read 0-padded garbage; masked below
+      part[j] = 0.0f;
+      if ((uint32_t)j < nc) {  // CTA-uniform
+        const uint32_t w = cw[j * TPB + t];
+        const float sj = h2f(sc[j * gpc + gcol]);
+        const float zj = h2f(zr[j * gpc + gcol]);
+        part[j] = fmaf(sj, dot16_int2(w, xs), zj * xsum);
+      }
     }
     // transposed butterfly over 16 channels, then fold the two half-warps:
     // lane l (and l^16) ends with the warp sum of channel l&15.
@@ -159,59 +159,54 @@ __global__ void __launch_bounds__(TPB, 2) k1_int2(const K1Args a) {
     part[0] += __shfl_xor_sync(0xffffffffu, part[0], 16);
     if (lane < CH) wsum[warp][lane] = part[0];
     __syncthreads();  // wsum complete; stage s fully consumed
-    if (t == 0) issue(s);
+    if (t == 0 && i + NS < n_sub) issue(i + NS);
     if (warp == 0) {
       float v = 0.0f;
 #pragma unroll
       for (int w = 0; w < NW; ++w) v += wsum[w][lane & (CH - 1)];
-      const uint32_t c = c0 + lane;
-      k1_emit(a, slot, c, lane < CH && c < a.di, v, thr);
+      seg_emit(a, slot, c_lo, c0 + lane, lane < nc, v, thr, running);
     }
-    __syncthreads();  // stage_tile[s] / wsum reuse
+    __syncthreads();  // wsum reuse
   }
-  k1_finish(a, gridDim.y);
+  if (t == 0) a.seg_count[slot * gridDim.x + blockIdx.x] = running;
 }
 
 // ---------------------------------------------------------------------------
 // K2: y += sum_{kept c} silu(gate_c . x) * v[c] * w_slot * down_c.
 //
-// Kept entries of all slots are split evenly over CTAs (balance is exact
-// regardless of where channels were kept).  Each entry's 4*dh-byte record
-// (gate row | down row, f16) arrives with ONE bulk copy.  Thread t owns
-// 16-byte chunks t and t+TPB of each half-record (elements [8t, 8t+8) and
-// [8(t+TPB), ...)), so shared-memory reads are conflict-free 128-bit loads.
+// Kept entries of all slots are split evenly over CTAs (exact balance however
+// the channels fell).  The CTA first resolves its entries' (record address,
+// v * routing weight) into shared memory with all threads in parallel, so the
+// issuing thread never waits on global memory; then each entry's 4*dh-byte
+// record (gate row | down row, f16) arrives with ONE bulk copy into an
+// NS-deep ring.  Thread t owns 16-byte chunks t and t+TPB of each half-record
+// (elements [8t, 8t+8) and [8(t+TPB), ...)): conflict-free 128-bit smem reads.
+constexpr uint32_t kK2Chunk = 256;  // entries resolved per preload round
+
 template <int TPB, int NS>
 __global__ void __launch_bounds__(TPB, 1) k2_gate_down(const K2Args a) {
   constexpr int NW = TPB / 32;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t full[NS];
-  __shared__ float stage_scale[NS];  // v[c] * routing weight of the entry
   __shared__ float red[2][NW];
+  __shared__ const __half *ent_rec[kK2Chunk];
+  __shared__ float ent_scale[kK2Chunk];
 
   const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const uint32_t rec_bytes = 4u * a.dh;  // == 64 * TPB
-  uint32_t total = 0;
-  for (uint32_t s = 0; s < a.slots; ++s) total += a.count_final[s];
+  const uint32_t nseg = a.slots * a.g1;
+  uint32_t *prefix = reinterpret_cast<uint32_t *>(smem + NS * rec_bytes);
+  seg_prefix(a.seg_count, nseg, prefix);
+  k2_publish(a, prefix);
+  const uint32_t total = prefix[nseg];
   const uint32_t begin = (uint32_t)(((uint64_t)total * blockIdx.x) / gridDim.x);
   const uint32_t end = (uint32_t)(((uint64_t)total * (blockIdx.x + 1)) / gridDim.x);
-  const uint32_t n = end - begin;
 
-  auto issue = [&](uint32_t i) {  // thread 0 only: entry begin+i -> stage i%NS
-    const uint32_t s = i % NS;
-    const KeptEntry k = kept_entry(a, begin + i);
-    const uint32_t e = a.sel ? a.sel[k.slot] : k.slot;
-    stage_scale[s] = k.v * slot_weight(a, k.slot);
-    floe_ptx::mbar_arrive_expect_tx(&full[s], rec_bytes);
-    floe_ptx::bulk_g2s(smem + s * rec_bytes, a.table[e].records + (size_t)k.c * 2 * a.dh,
-                       rec_bytes, &full[s]);
-  };
   if (t == 0) {
 #pragma unroll
     for (int s = 0; s < NS; ++s) floe_ptx::mbar_init(&full[s], 1);
     floe_ptx::fence_barrier_init();
-    for (uint32_t i = 0; i < n && i < (uint32_t)NS; ++i) issue(i);
   }
-
   float2 x2[8], y2[8];
   {
     const float4 *xa = reinterpret_cast<const float4 *>(a.x + 8 * t);
@@ -228,45 +223,65 @@ __global__ void __launch_bounds__(TPB, 1) k2_gate_down(const K2Args a) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) y2[i] = make_float2(0.0f, 0.0f);
   }
-  __syncthreads();
 
-  for (uint32_t i = 0; i < n; ++i) {
-    const uint32_t s = i % NS;
-    floe_ptx::mbar_wait(&full[s], (i / NS) & 1u);
-    const uint4 *rec = reinterpret_cast<const uint4 *>(smem + s * rec_bytes);
-    const uint4 g0 = rec[t], g1 = rec[t + TPB];
-    const uint4 d0 = rec[2 * TPB + t], d1 = rec[3 * TPB + t];
-    const float sc = stage_scale[s];
-    float2 acc = make_float2(0.0f, 0.0f);
-    {
-      const __half2 *h0 = reinterpret_cast<const __half2 *>(&g0);
-      const __half2 *h1 = reinterpret_cast<const __half2 *>(&g1);
+  uint32_t it = 0;  // global iteration count (ring position / parity)
+  for (uint32_t cb = begin; cb < end; cb += kK2Chunk) {
+    const uint32_t n = min(kK2Chunk, end - cb);
+    __syncthreads();  // previous chunk's ent_* fully consumed
+    for (uint32_t q = t; q < n; q += TPB) {
+      const KeptEntry k = kept_entry(a, prefix, cb + q);
+      const uint32_t e = a.sel ? a.sel[k.slot] : k.slot;
+      ent_rec[q] = a.table[e].records + (size_t)k.c * 2 * a.dh;
+      ent_scale[q] = k.v * slot_weight(a, k.slot);
+      if (a.kept_out) a.kept_out[(size_t)k.slot * a.di + k.slot_pos] = k.c;
+    }
+    __syncthreads();
+    if (t == 0)
+      for (uint32_t q = 0; q < n && q < (uint32_t)NS; ++q) {
+        const uint32_t s = (it + q) % NS;
+        floe_ptx::mbar_arrive_expect_tx(&full[s], rec_bytes);
+        floe_ptx::bulk_g2s(smem + s * rec_bytes, ent_rec[q], rec_bytes, &full[s]);
+      }
+    for (uint32_t q = 0; q < n; ++q, ++it) {
+      const uint32_t s = it % NS;
+      floe_ptx::mbar_wait(&full[s], (it / NS) & 1u);
+      const uint4 *rec = reinterpret_cast<const uint4 *>(smem + s * rec_bytes);
+      const uint4 g0 = rec[t], g1 = rec[t + TPB];
+      const uint4 d0 = rec[2 * TPB + t], d1 = rec[3 * TPB + t];
+      float2 acc = make_float2(0.0f, 0.0f);
+      {
+        const __half2 *h0 = reinterpret_cast<const __half2 *>(&g0);
+        const __half2 *h1 = reinterpret_cast<const __half2 *>(&g1);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        acc = __ffma2_rn(__half22float2(h0[q]), x2[q], acc);
-        acc = __ffma2_rn(__half22float2(h1[q]), x2[4 + q], acc);
+        for (int j = 0; j < 4; ++j) {
+          acc = __ffma2_rn(__half22float2(h0[j]), x2[j], acc);
+          acc = __ffma2_rn(__half22float2(h1[j]), x2[4 + j], acc);
+        }
+      }
+      float gp = acc.x + acc.y;
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) gp += __shfl_xor_sync(0xffffffffu, gp, o);
+      if (lane == 0) red[it & 1][warp] = gp;
+      __syncthreads();  // red complete; stage s fully read
+      if (t == 0 && q + NS < n) {
+        floe_ptx::mbar_arrive_expect_tx(&full[s], rec_bytes);
+        floe_ptx::bulk_g2s(smem + s * rec_bytes, ent_rec[q + NS], rec_bytes, &full[s]);
+      }
+      float g = 0.0f;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) g += red[it & 1][w];
+      const float aco = silu_ref(g) * ent_scale[q];
+      const float2 a2 = make_float2(aco, aco);
+      const __half2 *e0 = reinterpret_cast<const __half2 *>(&d0);
+      const __half2 *e1 = reinterpret_cast<const __half2 *>(&d1);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        y2[j] = __ffma2_rn(a2, __half22float2(e0[j]), y2[j]);
+        y2[4 + j] = __ffma2_rn(a2, __half22float2(e1[j]), y2[4 + j]);
       }
     }
-    float gp = acc.x + acc.y;
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) gp += __shfl_xor_sync(0xffffffffu, gp, o);
-    if (lane == 0) red[i & 1][warp] = gp;
-    __syncthreads();  // red complete; stage s fully read
-    if (t == 0 && i + NS < n) issue(i + NS);
-    float g = 0.0f;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) g += red[i & 1][w];
-    const float aco = silu_ref(g) * sc;
-    const float2 a2 = make_float2(aco, aco);
-    const __half2 *e0 = reinterpret_cast<const __half2 *>(&d0);
-    const __half2 *e1 = reinterpret_cast<const __half2 *>(&d1);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      y2[q] = __ffma2_rn(a2, __half22float2(e0[q]), y2[q]);
-      y2[4 + q] = __ffma2_rn(a2, __half22float2(e1[q]), y2[4 + q]);
-    }
   }
-  if (n > 0) {
+  if (end > begin) {
     float *ya = a.y + 8 * t, *yb = a.y + 8 * (t + TPB);
     red_add_v4(ya, y2[0].x, y2[0].y, y2[1].x, y2[1].y);
     red_add_v4(ya + 4, y2[2].x, y2[2].y, y2[3].x, y2[3].y);

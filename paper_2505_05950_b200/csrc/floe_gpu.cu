@@ -106,6 +106,8 @@ cudaStream_t S(floe_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
 uint64_t up256(uint64_t x) { return (x + 255) & ~uint64_t(255); }
 
+constexpr uint32_t kMaxSeg = 1024;  // K1 CTAs (segments) per slot
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -126,7 +128,10 @@ struct floe_gpu_workspace {
   void *block = nullptr;
   uint32_t *kept_idx = nullptr;
   float *kept_v = nullptr;
-  uint32_t *count = nullptr, *count_final = nullptr, *done = nullptr, *tile_ctr = nullptr;
+  uint32_t *seg_count = nullptr;  // [slots][kMaxSeg]
+  uint32_t g1 = 0;                // K1 grid.x of the last K1 launch (segments per slot)
+  float *mix_partial = nullptr;   // [dh/8][32] partial router logits
+  uint32_t *mix_done = nullptr;
   unsigned long long *stats = nullptr;
   uint32_t *sel = nullptr;
   float *weights = nullptr, *u = nullptr, *x = nullptr, *y = nullptr, *v = nullptr;
@@ -218,6 +223,14 @@ struct K1Launch {
   float *y_zero;
 };
 
+// Segments per slot of a K1 launch (= its grid.x); bounded by kMaxSeg.
+uint32_t k1_grid(uint32_t di, uint32_t slots, bool fast) {
+  const uint32_t sm = (uint32_t)device_info().sm;
+  const uint32_t want = fast ? std::max<uint32_t>(1, (2u * sm) / slots)
+                             : std::max<uint32_t>(1, std::min<uint32_t>((di + 63) / 64, 4u * sm));
+  return std::min<uint32_t>({want, (di + 15) / 16 ? (di + 15) / 16 : 1u, kMaxSeg});
+}
+
 int launch_k1(const K1Launch &L, floe_gpu_workspace *ws, cudaStream_t st) {
   K1Args a{};
   a.table = L.table;
@@ -233,24 +246,18 @@ int launch_k1(const K1Launch &L, floe_gpu_workspace *ws, cudaStream_t st) {
   a.mask_out = L.mask_out;
   a.kept_idx = ws->kept_idx;
   a.kept_v = ws->kept_v;
-  a.count = ws->count;
-  a.count_final = ws->count_final;
-  a.done = ws->done;
-  a.tile_ctr = ws->tile_ctr;
-  a.stats = ws->stats;
-  a.n_kept_out = L.n_kept_out;
-  a.kept_out = L.kept_out;
+  a.seg_count = ws->seg_count;
   a.y_zero = L.y_zero;
   const int tpb = fast_tpb(L.dh);
-  const int sm = device_info().sm;
+  const bool fast = L.fast && (tpb == 256 || tpb == 128);
+  const uint32_t g1 = k1_grid(L.di, L.slots, fast);
+  ws->g1 = g1;
   StageScope prof(ws, kStageK1, st);
-  if (L.fast && (tpb == 256 || tpb == 128)) {
+  dim3 grid(g1, L.slots);
+  if (fast) {
     constexpr int NS = 4;
     const uint32_t gpc = L.dh / L.g;
     const uint32_t smem = NS * floe_k::k1_stage_bytes(tpb, gpc);
-    const uint32_t n_tiles = (L.di + floe_k::kK1Ch - 1) / floe_k::kK1Ch;
-    const uint32_t per_slot = std::max<uint32_t>(1, (2u * sm) / L.slots);
-    dim3 grid(std::min(n_tiles, per_slot), L.slots);
     if (tpb == 256) {
       if (int rc = set_smem(floe_k::k1_int2<256, NS>, smem)) return rc;
       floe_k::k1_int2<256, NS><<<grid, 256, smem, st>>>(a);
@@ -259,7 +266,6 @@ int launch_k1(const K1Launch &L, floe_gpu_workspace *ws, cudaStream_t st) {
       floe_k::k1_int2<128, NS><<<grid, 128, smem, st>>>(a);
     }
   } else {
-    dim3 grid((L.di + 255) / 256, L.slots);
     floe_k::k1_generic<<<grid, 256, 0, st>>>(a);
   }
   CK_LAUNCH();
@@ -273,7 +279,8 @@ struct K2Launch {
   uint32_t slots, dh, di;
   bool fast;
   const float *x;
-  float *y;
+  float *y;  // nullptr: finalize only (n_kept / kept ids of a K1-only call)
+  uint32_t *n_kept_out, *kept_out;
 };
 
 int launch_k2(const K2Launch &L, floe_gpu_workspace *ws, cudaStream_t st) {
@@ -285,16 +292,27 @@ int launch_k2(const K2Launch &L, floe_gpu_workspace *ws, cudaStream_t st) {
   a.dh = L.dh;
   a.di = L.di;
   a.slots = L.slots;
+  a.g1 = ws->g1;
   a.kept_idx = ws->kept_idx;
   a.kept_v = ws->kept_v;
-  a.count_final = ws->count_final;
+  a.seg_count = ws->seg_count;
   a.y = L.y;
+  a.n_kept_out = L.n_kept_out;
+  a.kept_out = L.kept_out;
+  a.stats = L.y ? ws->stats : nullptr;
   const int sm = device_info().sm;
   const int tpb = fast_tpb(L.dh);
+  const uint32_t prefix_bytes = 4u * (L.slots * ws->g1 + 1);
+  if (!L.y) {  // finalize a K1-only call
+    if (!L.n_kept_out && !L.kept_out) return FLOE_OK;
+    floe_k::k2_generic<<<sm, 128, prefix_bytes, st>>>(a);
+    CK_LAUNCH();
+    return FLOE_OK;
+  }
   StageScope prof(ws, kStageK2, st);
   if (L.fast && (tpb == 256 || tpb == 128)) {
     constexpr int NS = 4;
-    const uint32_t smem = NS * 4u * L.dh;
+    const uint32_t smem = NS * 4u * L.dh + prefix_bytes;
     if (tpb == 256) {
       if (int rc = set_smem(floe_k::k2_gate_down<256, NS>, smem)) return rc;
       floe_k::k2_gate_down<256, NS><<<2 * sm, 256, smem, st>>>(a);
@@ -303,7 +321,8 @@ int launch_k2(const K2Launch &L, floe_gpu_workspace *ws, cudaStream_t st) {
       floe_k::k2_gate_down<128, NS><<<2 * sm, 128, smem, st>>>(a);
     }
   } else {
-    floe_k::k2_generic<<<4 * sm, 128, 0, st>>>(a);
+    if (int rc = set_smem(floe_k::k2_generic, prefix_bytes)) return rc;
+    floe_k::k2_generic<<<4 * sm, 128, prefix_bytes, st>>>(a);
   }
   CK_LAUNCH();
   return FLOE_OK;
@@ -367,7 +386,10 @@ int floe_gpu_expert_create(const floe_expert_host_view *v, floe_gpu_expert **out
   e->code_bytes = packed_code_bytes(n, v->bits);
   e->n_groups = n / v->group_size;
   const int tpb = fast_tpb(e->dh);
-  e->fast_k1 = tpb && e->bits == 2 && e->g % 16 == 0 && e->dh % e->g == 0;
+  // K1 fast path: INT2 words stay inside one group, and per-channel metadata
+  // rows are 16-byte multiples (bulk-copy granularity).
+  e->fast_k1 = tpb && e->bits == 2 && e->g % 16 == 0 && e->dh % e->g == 0 &&
+               (e->dh / e->g) % 8 == 0;
   e->fast_k2 = tpb != 0;
 
   // One allocation, 256-B aligned sections: [desc][codes][scales][zeros][records]
@@ -490,7 +512,9 @@ int floe_gpu_workspace_create(uint32_t dh, uint32_t di, uint32_t slots,
   uint64_t o = 0;
   const uint64_t o_idx = o;   o = up256(o + 4 * sd);
   const uint64_t o_kv = o;    o = up256(o + 4 * sd);
-  const uint64_t o_cnt = o;   o = up256(o + 4 * 4 * MS);
+  const uint64_t o_cnt = o;   o = up256(o + 4ull * MS * kMaxSeg);
+  const uint64_t o_mp = o;    o = up256(o + 4ull * 32 * ((dh + 7) / 8));
+  const uint64_t o_md = o;    o = up256(o + 16);
   const uint64_t o_st = o;    o = up256(o + 16);
   const uint64_t o_sel = o;   o = up256(o + 4 * MS);
   const uint64_t o_w = o;     o = up256(o + 4 * MS);
@@ -507,10 +531,9 @@ int floe_gpu_workspace_create(uint32_t dh, uint32_t di, uint32_t slots,
   char *b = static_cast<char *>(w->block);
   w->kept_idx = reinterpret_cast<uint32_t *>(b + o_idx);
   w->kept_v = reinterpret_cast<float *>(b + o_kv);
-  w->count = reinterpret_cast<uint32_t *>(b + o_cnt);
-  w->count_final = w->count + MS;
-  w->done = w->count + 2 * MS;
-  w->tile_ctr = w->count + 3 * MS;
+  w->seg_count = reinterpret_cast<uint32_t *>(b + o_cnt);
+  w->mix_partial = reinterpret_cast<float *>(b + o_mp);
+  w->mix_done = reinterpret_cast<uint32_t *>(b + o_md);
   w->stats = reinterpret_cast<unsigned long long *>(b + o_st);
   w->sel = reinterpret_cast<uint32_t *>(b + o_sel);
   w->weights = reinterpret_cast<float *>(b + o_w);
@@ -602,9 +625,10 @@ int floe_gpu_expert_forward_sparse(const floe_gpu_expert *e, floe_gpu_workspace 
   if (!e || !x || !y) return fail(FLOE_ERR_INVALID, "expert_forward_sparse: null argument");
   if (int rc = check_ws("expert_forward_sparse", ws, e->dh, e->di, 1)) return rc;
   K1Launch k1{e->dev_desc, nullptr, 1, e->dh, e->di, e->bits, e->g, e->fast_k1, 0, 0.0f,
-              x, v_out, mask_out, kept_out, n_kept_out, y};
+              x, v_out, mask_out, nullptr, nullptr, y};
   if (int rc = launch_k1(k1, ws, S(stream))) return rc;
-  K2Launch k2{e->dev_desc, nullptr, nullptr, 1, e->dh, e->di, e->fast_k2, x, y};
+  K2Launch k2{e->dev_desc, nullptr, nullptr, 1, e->dh, e->di, e->fast_k2, x, y,
+              n_kept_out, kept_out};
   return launch_k2(k2, ws, S(stream));
 }
 
@@ -655,8 +679,11 @@ int floe_gpu_predict_mask(const floe_gpu_expert *next, floe_gpu_workspace *ws,
   if (!next || !x_prev) return fail(FLOE_ERR_INVALID, "predict_mask: null argument");
   if (int rc = check_ws("predict_mask", ws, next->dh, next->di, 1)) return rc;
   K1Launch k1{next->dev_desc, nullptr, 1, next->dh, next->di, next->bits, next->g,
-              next->fast_k1, 1, t, x_prev, nullptr, mask_out, kept_out, n_kept_out, nullptr};
-  return launch_k1(k1, ws, S(stream));
+              next->fast_k1, 1, t, x_prev, nullptr, mask_out, nullptr, nullptr, nullptr};
+  if (int rc = launch_k1(k1, ws, S(stream))) return rc;
+  K2Launch fin{next->dev_desc, nullptr, nullptr, 1, next->dh, next->di, false, x_prev, nullptr,
+               n_kept_out, kept_out};
+  return launch_k2(fin, ws, S(stream));
 }
 
 // ----------------------------------------------------------------- layers --
@@ -742,27 +769,36 @@ int floe_gpu_layer_forward(const floe_gpu_layer *l, floe_gpu_workspace *ws, cons
   const size_t smem = 4ull * l->dh;
   float *u_tr = tr ? tr->block_input_dev : nullptr;
   {
+    // mixing GEMV + residual + router logits + top-k + softmax in one launch
     StageScope prof(ws, kStageMixing, st);
+    floe_k::MixArgs m{};
+    m.m = l->mixing;
+    m.h = h;
+    m.dh = l->dh;
+    m.router = l->router;
+    m.E = l->E;
+    m.k = l->top_k;
+    m.u = ws->u;
+    m.y_init = y;
+    m.u_trace = u_tr;
+    m.partial = ws->mix_partial;
+    m.done = ws->mix_done;
+    m.sel = ws->sel;
+    m.weights = ws->weights;
+    m.sel_trace = tr ? tr->experts_dev : nullptr;
+    m.w_trace = tr ? tr->weights_dev : nullptr;
     const dim3 grid((l->dh + rows_per_block - 1) / rows_per_block);
     if (l->mix_f16)
-      floe_k::mixing_gemv<__half><<<grid, 256, smem, st>>>(static_cast<const __half *>(l->mixing),
-                                                           h, l->dh, ws->u, y, u_tr);
+      floe_k::mixing_route<__half><<<grid, 256, smem, st>>>(m);
     else
-      floe_k::mixing_gemv<float><<<grid, 256, smem, st>>>(static_cast<const float *>(l->mixing),
-                                                          h, l->dh, ws->u, y, u_tr);
-    CK_LAUNCH();
-  }
-  {
-    StageScope prof(ws, kStageRoute, st);
-    floe_k::route_topk<<<1, 256, 0, st>>>(l->router, nullptr, ws->u, l->E, l->dh, l->top_k, 1,
-                                          ws->sel, ws->weights, tr ? tr->experts_dev : nullptr,
-                                          tr ? tr->weights_dev : nullptr);
+      floe_k::mixing_route<float><<<grid, 256, smem, st>>>(m);
     CK_LAUNCH();
   }
   K1Launch k1{l->table, ws->sel, l->top_k, l->dh, l->di, l->bits, l->g, l->fast_k1, 0, 0.0f,
               ws->u, nullptr, tr ? tr->masks_dev : nullptr, nullptr, nullptr, nullptr};
   if (int rc = launch_k1(k1, ws, st)) return rc;
-  K2Launch k2{l->table, ws->sel, ws->weights, l->top_k, l->dh, l->di, l->fast_k2, ws->u, y};
+  K2Launch k2{l->table, ws->sel, ws->weights, l->top_k, l->dh, l->di, l->fast_k2, ws->u, y,
+              nullptr, nullptr};
   return launch_k2(k2, ws, st);
 }
 

@@ -40,6 +40,12 @@ struct ExpertDesc {
   uint32_t pad_[3];
 };
 
+// Kept-channel lists ("segments").  K1 runs on a (G1, slots) grid; CTA b of
+// slot s owns the contiguous channel range [di*b/G1, di*(b+1)/G1) and writes
+// its kept channels, ascending, to kept_idx/kept_v[s*di + di*b/G1 + j] for
+// j < seg_count[s*G1 + b].  No atomics: every call overwrites every count.
+// K2 prefix-scans seg_count, so the global entry order is (slot, channel)
+// ascending -- deterministic, like the reference's ascending channel loop.
 struct K1Args {
   const ExpertDesc *table;  // expert descriptors
   const uint32_t *sel;      // nullable: slot j uses table[sel[j]] (else table[j])
@@ -51,13 +57,7 @@ struct K1Args {
   uint8_t *mask_out;        // nullable, [slots][di]
   uint32_t *kept_idx;       // [slots][di]  (workspace)
   float *kept_v;            // [slots][di]  (workspace)
-  uint32_t *count;          // [slots]  running append counters (reset by last CTA)
-  uint32_t *count_final;    // [slots]  published counts for K2 / the caller
-  uint32_t *done;           // [1]      CTA completion counter (reset by last CTA)
-  uint32_t *tile_ctr;       // [slots]  dynamic tile claims (reset by last CTA)
-  unsigned long long *stats;  // nullable [2]: calls, kept channels (running totals)
-  uint32_t *n_kept_out;     // nullable, [slots]
-  uint32_t *kept_out;       // nullable, [slots][di]  caller copy of kept ids
+  uint32_t *seg_count;      // [slots][G1]
   float *y_zero;            // nullable: zeroed by CTA 0 (K2 accumulates into it)
 };
 
@@ -66,28 +66,25 @@ struct K2Args {
   const uint32_t *sel;       // nullable
   const float *weights;      // nullable: per-slot combine weight (routing softmax)
   const float *x;            // f32[dh]
-  uint32_t dh, di, slots;
+  uint32_t dh, di, slots, g1;
   const uint32_t *kept_idx;  // [slots][di]
   const float *kept_v;       // [slots][di]
-  const uint32_t *count_final;  // [slots]
+  const uint32_t *seg_count;  // [slots][g1]
   float *y;                  // f32[dh], accumulated with fp32 reductions
+  uint32_t *n_kept_out;      // nullable [slots]
+  uint32_t *kept_out;        // nullable [slots][di]: kept ids, ascending per slot
+  unsigned long long *stats;  // nullable [2]: calls, kept channels (running totals)
 };
 
 __device__ __forceinline__ float h2f(uint16_t h) {
   return __half2float(__ushort_as_half(h));
 }
 
-__device__ __forceinline__ uint32_t ldg_stream_u32(const uint32_t *p) {
-  uint32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
-  return v;
-}
-
 __device__ __forceinline__ uint4 ldg_stream_u128(const void *p) {
   uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "l"(p));
   return v;
 }
 
@@ -112,13 +109,18 @@ __device__ __forceinline__ uint32_t get_code(const uint8_t *codes, uint32_t bits
   return v & ((1u << bits) - 1);
 }
 
-// ---------------------------------------------------------------------------
-// K1 epilogue shared by both K1 variants: threshold, outputs, compaction.
-// Called by one full warp; lane handles channel `c` (valid if c < di).
-__device__ __forceinline__ void k1_emit(const K1Args &a, uint32_t slot, uint32_t c,
-                                        bool valid, float v, float thr) {
+__device__ __forceinline__ uint32_t seg_begin(uint32_t di, uint32_t b, uint32_t g1) {
+  return (uint32_t)(((uint64_t)di * b) / g1);
+}
+
+// K1 epilogue, called by one full warp; lane handles channel c (if valid).
+// Appends kept channels to the CTA's segment in ascending order; `running`
+// (warp-uniform) is the segment's count so far.
+__device__ __forceinline__ void seg_emit(const K1Args &a, uint32_t slot, uint32_t seg_base,
+                                         uint32_t c, bool valid, float v, float thr,
+                                         uint32_t &running) {
   const uint32_t lane = threadIdx.x & 31;
-  // model.cpp:135: `if (fabs(v) < t) continue;` -> NaN is kept, ties kept.
+  // model.cpp:135: `if (fabs(v) < t) continue;` -> ties and NaN are kept.
   const bool keep = valid && !(fabsf(v) < thr);
   const size_t off = (size_t)slot * a.di + c;
   if (valid) {
@@ -126,43 +128,12 @@ __device__ __forceinline__ void k1_emit(const K1Args &a, uint32_t slot, uint32_t
     if (a.mask_out) a.mask_out[off] = keep ? 1 : 0;
   }
   const uint32_t bal = __ballot_sync(0xffffffffu, keep);
-  if (bal) {
-    uint32_t base = 0;
-    if (lane == 0) base = atomicAdd(&a.count[slot], (uint32_t)__popc(bal));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (keep) {
-      const uint32_t pos = base + __popc(bal & ((1u << lane) - 1));
-      const size_t o = (size_t)slot * a.di + pos;
-      a.kept_idx[o] = c;
-      a.kept_v[o] = v;
-      if (a.kept_out) a.kept_out[o] = c;
-    }
+  if (keep) {
+    const size_t o = (size_t)slot * a.di + seg_base + running + __popc(bal & ((1u << lane) - 1));
+    a.kept_idx[o] = c;
+    a.kept_v[o] = v;
   }
-}
-
-// Last-CTA bookkeeping: publish counts, reset the running counters so the
-// next stream-ordered call starts from zero (no memset node needed).
-__device__ __forceinline__ void k1_finish(const K1Args &a, uint32_t slots) {
-  __syncthreads();
-  __shared__ bool last;
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const uint32_t total = gridDim.x * gridDim.y;
-    last = atomicAdd(a.done, 1u) == total - 1;
-  }
-  __syncthreads();
-  if (last && threadIdx.x < slots) {
-    __threadfence();
-    const uint32_t n = atomicExch(&a.count[threadIdx.x], 0u);
-    a.count_final[threadIdx.x] = n;
-    if (a.n_kept_out) a.n_kept_out[threadIdx.x] = n;
-    if (a.tile_ctr) a.tile_ctr[threadIdx.x] = 0;
-    if (a.stats) atomicAdd(&a.stats[1], (unsigned long long)n);
-    if (threadIdx.x == 0) {
-      *a.done = 0;
-      if (a.stats) atomicAdd(&a.stats[0], 1ull);
-    }
-  }
+  running += __popc(bal);
 }
 
 // ---------------------------------------------------------------------------
@@ -177,15 +148,15 @@ __global__ void __launch_bounds__(256) k1_generic(const K1Args a) {
   const float thr = a.use_threshold ? a.threshold : d.threshold;
   if (a.y_zero && blockIdx.x == 0 && slot == 0)
     for (uint32_t i = threadIdx.x; i < a.dh; i += blockDim.x) a.y_zero[i] = 0.0f;
-
-  for (uint32_t cb = blockIdx.x * 8 * 32; cb < a.di; cb += gridDim.x * 8 * 32) {
-    // each warp handles 32 consecutive channels, one at a time, then emits
-    const uint32_t wc0 = cb + warp * 32;
-    float vmine = 0.0f;
-    for (uint32_t j = 0; j < 32; ++j) {
-      const uint32_t c = wc0 + j;
+  const uint32_t c0 = seg_begin(a.di, blockIdx.x, gridDim.x);
+  const uint32_t c1 = seg_begin(a.di, blockIdx.x + 1, gridDim.x);
+  __shared__ float vbuf[32];
+  uint32_t running = 0;
+  for (uint32_t cb = c0; cb < c1; cb += 32) {
+    for (uint32_t j = warp; j < 32; j += 8) {  // 4 channels per warp
+      const uint32_t c = cb + j;
       float acc = 0.0f;
-      if (c < a.di) {
+      if (c < c1) {
         const uint64_t base = (uint64_t)c * a.dh;
         for (uint32_t k = lane; k < a.dh; k += 32) {
           const uint64_t i = base + k;
@@ -197,33 +168,85 @@ __global__ void __launch_bounds__(256) k1_generic(const K1Args a) {
       }
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == j) vmine = acc;
+      if (lane == 0) vbuf[j] = acc;
     }
-    const uint32_t c = wc0 + lane;
-    k1_emit(a, slot, c, c < a.di, vmine, thr);
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t c = cb + lane;
+      seg_emit(a, slot, c0 - 0, c, c < c1, vbuf[lane], thr, running);
+    }
+    __syncthreads();
   }
-  k1_finish(a, gridDim.y);
+  if (threadIdx.x == 0) a.seg_count[slot * gridDim.x + blockIdx.x] = running;
 }
 
 // ---------------------------------------------------------------------------
-// Map a flattened kept-entry index to (slot, channel, v).
+// Segment prefix: prefix[i] = sum_{j<i} seg_count[j] for i in [0, n], in
+// shared memory, computed by the whole CTA (blockDim multiple of 32, <=1024).
+__device__ inline void seg_prefix(const uint32_t *counts, uint32_t n, uint32_t *prefix) {
+  __shared__ uint32_t warp_tot[32];
+  const uint32_t t = threadIdx.x, nt = blockDim.x;
+  const uint32_t per = (n + nt - 1) / nt;
+  const uint32_t lo = min(n, t * per), hi = min(n, lo + per);
+  uint32_t s = 0;
+  for (uint32_t i = lo; i < hi; ++i) s += counts[i];
+  // inclusive warp scan
+  uint32_t inc = s;
+  const uint32_t lane = t & 31, warp = t >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= (uint32_t)o) inc += y;
+  }
+  if (lane == 31) warp_tot[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t nw = nt / 32;
+    uint32_t wv = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, wv, o);
+      if (lane >= (uint32_t)o) wv += y;
+    }
+    if (lane < nw) warp_tot[lane] = wv;  // inclusive warp totals
+  }
+  __syncthreads();
+  uint32_t run = inc - s + (warp ? warp_tot[warp - 1] : 0);  // exclusive start of chunk
+  for (uint32_t i = lo; i < hi; ++i) {
+    prefix[i] = run;
+    run += counts[i];
+  }
+  if (t == nt - 1) prefix[n] = run;
+  __syncthreads();
+}
+
+// Entry p (0 <= p < prefix[n]) -> segment index (largest i with prefix[i] <= p).
+__device__ __forceinline__ uint32_t seg_find(const uint32_t *prefix, uint32_t n, uint32_t p) {
+  uint32_t lo = 0, hi = n;  // invariant: prefix[lo] <= p < prefix[hi]
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (prefix[mid] <= p) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+
 struct KeptEntry {
-  uint32_t slot, c;
+  uint32_t slot, c, slot_pos;
   float v;
 };
 
-__device__ __forceinline__ KeptEntry kept_entry(const K2Args &a, uint32_t p) {
-  uint32_t slot = 0;
-  uint32_t q = p;
-  while (slot + 1 < a.slots && q >= a.count_final[slot]) {
-    q -= a.count_final[slot];
-    ++slot;
-  }
+__device__ __forceinline__ KeptEntry kept_entry(const K2Args &a, const uint32_t *prefix,
+                                                uint32_t p) {
+  const uint32_t nseg = a.slots * a.g1;
+  const uint32_t idx = seg_find(prefix, nseg, p);
+  const uint32_t slot = idx / a.g1, b = idx % a.g1;
+  const size_t o = (size_t)slot * a.di + seg_begin(a.di, b, a.g1) + (p - prefix[idx]);
   KeptEntry k;
   k.slot = slot;
-  const size_t o = (size_t)slot * a.di + q;
   k.c = a.kept_idx[o];
   k.v = a.kept_v[o];
+  k.slot_pos = p - prefix[slot * a.g1];
   return k;
 }
 
@@ -231,14 +254,31 @@ __device__ __forceinline__ float slot_weight(const K2Args &a, uint32_t slot) {
   return a.weights ? a.weights[slot] : 1.0f;
 }
 
+// Per-call bookkeeping by CTA 0 of K2 (or of k1_finalize).
+__device__ __forceinline__ void k2_publish(const K2Args &a, const uint32_t *prefix) {
+  if (blockIdx.x != 0) return;
+  if (threadIdx.x < a.slots && a.n_kept_out)
+    a.n_kept_out[threadIdx.x] =
+        prefix[(threadIdx.x + 1) * a.g1] - prefix[threadIdx.x * a.g1];
+  if (threadIdx.x == 0 && a.stats) {
+    atomicAdd(&a.stats[0], 1ull);
+    atomicAdd(&a.stats[1], (unsigned long long)prefix[a.slots * a.g1]);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K2 generic: one CTA per kept entry (grid-stride), fp32 atomics into y.
 __global__ void __launch_bounds__(128) k2_generic(const K2Args a) {
-  uint32_t total = 0;
-  for (uint32_t s = 0; s < a.slots; ++s) total += a.count_final[s];
+  extern __shared__ uint32_t prefix[];
+  const uint32_t nseg = a.slots * a.g1;
+  seg_prefix(a.seg_count, nseg, prefix);
+  k2_publish(a, prefix);
+  const uint32_t total = prefix[nseg];
   __shared__ float red[4];
   for (uint32_t p = blockIdx.x; p < total; p += gridDim.x) {
-    const KeptEntry k = kept_entry(a, p);
+    const KeptEntry k = kept_entry(a, prefix, p);
+    if (a.kept_out && threadIdx.x == 0) a.kept_out[(size_t)k.slot * a.di + k.slot_pos] = k.c;
+    if (!a.y) continue;
     const uint32_t e = a.sel ? a.sel[k.slot] : k.slot;
     const __half *rec = a.table[e].records + (size_t)k.c * 2 * a.dh;
     float acc = 0.0f;
@@ -291,47 +331,124 @@ __global__ void f32_to_f16_rn(const float *in, uint64_t n, __half *out) {
 // ---------------------------------------------------------------------------
 // Layer glue (block_forward, model.cpp:145-169).
 //
-// u = h + mixing.h ; y = u.  Warp per row, mixing in f32 or f16.
+// u = h + mixing.h ; y = u ; logits = router.u ; top_k ; softmax -- one launch.
+// Warp per row of the mixing matrix with the whole row's loads in flight; each
+// CTA also reduces its rows' share of router.u into partial logits, and the
+// last CTA (done counter, reset in-kernel) sums them in a fixed order and
+// routes.  Deterministic: no float atomics.
+struct MixArgs {
+  const void *m;
+  const float *h;
+  uint32_t dh;
+  const float *router;  // [E][dh]
+  uint32_t E, k;
+  float *u, *y_init, *u_trace;
+  float *partial;  // [gridDim.x][E]
+  uint32_t *done;
+  uint32_t *sel;
+  float *weights;
+  uint32_t *sel_trace;
+  float *w_trace;
+};
+
+__device__ inline void topk_small(const float *v, uint32_t n, uint32_t k, uint32_t *out);
+
 template <typename T>
-__global__ void __launch_bounds__(256) mixing_gemv(const T *__restrict__ m,
-                                                   const float *__restrict__ h,
-                                                   uint32_t dh, float *u,
-                                                   float *y_init, float *u_trace) {
+__global__ void __launch_bounds__(256) mixing_route(const MixArgs a) {
   extern __shared__ float hs[];
-  for (uint32_t i = threadIdx.x; i < dh; i += blockDim.x) hs[i] = h[i];
+  __shared__ float pl[8][32];
+  __shared__ bool last;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t i = threadIdx.x; i < a.dh; i += blockDim.x) hs[i] = a.h[i];
   __syncthreads();
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-  if (row >= dh) return;
-  const T *mr = m + (size_t)row * dh;
-  float acc = 0.0f;
-  if constexpr (sizeof(T) == 2) {
-    for (uint32_t k = lane * 8; k < dh; k += 256) {
-      const uint4 q = ldg_stream_u128(mr + k);
-      const __half2 *hh = reinterpret_cast<const __half2 *>(&q);
+  const uint32_t row = blockIdx.x * 8 + warp;
+  float uu = 0.0f;
+  if (row < a.dh) {
+    const T *mr = static_cast<const T *>(a.m) + (size_t)row * a.dh;
+    constexpr uint32_t EPL = 16 / sizeof(T);  // elements per 128-bit load
+    constexpr int U = 16;                     // loads in flight per lane
+    float acc = 0.0f;
+    for (uint32_t k0 = 0; k0 < a.dh; k0 += 32 * EPL * U) {
+      uint4 q[U];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float2 f = __half22float2(hh[i]);
-        acc = fmaf(f.x, hs[k + 2 * i], acc);
-        acc = fmaf(f.y, hs[k + 2 * i + 1], acc);
+      for (int j = 0; j < U; ++j) {
+        const uint32_t k = k0 + (lane + 32 * j) * EPL;
+        q[j] = k < a.dh ? ldg_stream_u128(mr + k) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        const uint32_t k = k0 + (lane + 32 * j) * EPL;
+        if (k >= a.dh) break;
+        if constexpr (sizeof(T) == 2) {
+          const __half2 *hh = reinterpret_cast<const __half2 *>(&q[j]);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 f = __half22float2(hh[i]);
+            acc = fmaf(f.x, hs[k + 2 * i], acc);
+            acc = fmaf(f.y, hs[k + 2 * i + 1], acc);
+          }
+        } else {
+          acc = fmaf(__uint_as_float(q[j].x), hs[k], acc);
+          acc = fmaf(__uint_as_float(q[j].y), hs[k + 1], acc);
+          acc = fmaf(__uint_as_float(q[j].z), hs[k + 2], acc);
+          acc = fmaf(__uint_as_float(q[j].w), hs[k + 3], acc);
+        }
       }
     }
-  } else {
-    for (uint32_t k = lane * 4; k < dh; k += 128) {
-      const uint4 q = ldg_stream_u128(mr + k);
-      acc = fmaf(__uint_as_float(q.x), hs[k], acc);
-      acc = fmaf(__uint_as_float(q.y), hs[k + 1], acc);
-      acc = fmaf(__uint_as_float(q.z), hs[k + 2], acc);
-      acc = fmaf(__uint_as_float(q.w), hs[k + 3], acc);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    uu = hs[row] + 1.0f * acc;  // drift_scale = 1 (model.cpp:151-152)
+    if (lane == 0) {
+      a.u[row] = uu;
+      a.y_init[row] = uu;
+      if (a.u_trace) a.u_trace[row] = uu;
     }
   }
+  // this CTA's rows' contribution to router.u
+  if (lane < a.E) pl[warp][lane] = row < a.dh ? a.router[(size_t)lane * a.dh + row] * uu : 0.0f;
+  __syncthreads();
+  if (threadIdx.x < a.E) {
+    float s = 0.0f;
 #pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) {
-    const float uu = hs[row] + 1.0f * acc;  // drift_scale = 1 (model.cpp:151-152)
-    u[row] = uu;
-    y_init[row] = uu;
-    if (u_trace) u_trace[row] = uu;
+    for (int w = 0; w < 8; ++w) s += pl[w][threadIdx.x];
+    a.partial[blockIdx.x * a.E + threadIdx.x] = s;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  __shared__ float logits[32];
+  for (uint32_t e = warp; e < a.E; e += 8) {
+    float s = 0.0f;
+    for (uint32_t b = lane; b < gridDim.x; b += 32) s += __ldcg(&a.partial[b * a.E + e]);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) logits[e] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *a.done = 0;
+    uint32_t sidx[32];
+    topk_small(logits, a.E, a.k, sidx);
+    float wv[32];
+    for (uint32_t i = 0; i < a.k; ++i) wv[i] = logits[sidx[i]];
+    float mx = wv[0];  // softmax_inplace (la.cpp:37-46)
+    for (uint32_t i = 1; i < a.k; ++i)
+      if (mx < wv[i]) mx = wv[i];
+    float sum = 0.0f;
+    for (uint32_t i = 0; i < a.k; ++i) {
+      wv[i] = expf(wv[i] - mx);
+      sum += wv[i];
+    }
+    for (uint32_t i = 0; i < a.k; ++i) wv[i] /= sum;
+    for (uint32_t i = 0; i < a.k; ++i) {
+      a.sel[i] = sidx[i];
+      a.weights[i] = wv[i];
+      if (a.sel_trace) a.sel_trace[i] = sidx[i];
+      if (a.w_trace) a.w_trace[i] = wv[i];
+    }
   }
 }
 
