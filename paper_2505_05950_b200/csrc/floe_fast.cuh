@@ -1,12 +1,14 @@
 // floe_fast.cuh -- specialised sm_100a kernels for the Mixtral-shaped path
-// (INT2 codes, d_hidden = 16*TPB).  Both kernels stream their weights with
+// (INT2 codes, d_hidden in {2048, 4096}).  All three stream their weights with
 // 1-D bulk copies (cp.async.bulk, the TMA engine) into an NS-deep shared
-// memory ring tracked by mbarriers, so every SM keeps NS-1 tiles in flight
-// without spending registers on loads.
+// memory ring tracked by mbarriers, so each SM keeps up to ~160 KB in flight
+// without spending registers on loads, and nothing on an issue path waits on
+// a dependent global load.
 //
 // Reference (paths relative to /root/reference/proj/):
-//   K1 = qgemv_channels + threshold    core/src/quant.cpp:122-136, core/src/model.cpp:135
-//   K2 = gate dot + silu + down        core/src/model.cpp:136-140, core/src/la.cpp:25-31
+//   K1 = qgemv_channels + threshold     core/src/quant.cpp:122-136, core/src/model.cpp:135
+//   K2 = gate dot + silu + down         core/src/model.cpp:136-140, core/src/la.cpp:25-31
+//   mixing_route = block_forward head   core/src/model.cpp:150-154, 83-93
 #pragma once
 
 #include "floe_kernels.cuh"
@@ -14,157 +16,237 @@
 
 namespace floe_k {
 
-constexpr int kK1Ch = 16;  // channels per K1 tile
+constexpr int kK1Ch = 16;  // channels per K1 sub-tile
 
 __host__ __device__ constexpr uint32_t round_up128(uint32_t x) { return (x + 127u) & ~127u; }
 
-// Shared-memory bytes of one K1 stage for a given d_hidden / groups-per-channel.
-__host__ __device__ constexpr uint32_t k1_stage_bytes(uint32_t tpb, uint32_t gpc) {
-  return round_up128(kK1Ch * tpb * 4u) + 2u * round_up128(kK1Ch * gpc * 2u);
-}
-
-// Exact INT2 dot product of one code word with 16 pre-scaled inputs.
-// c*4^i is formed exactly as (2^23 + c*4^i) - 2^23 from one LOP3 and one
-// packed FADD2; the packed FFMA2 accumulates even/odd lanes of x.
-__device__ __forceinline__ float dot16_int2(uint32_t w, const float2 (&xs)[8]) {
-  const uint32_t magic = 0x4B000000u;
-  const uint32_t w2 = w >> 22;
-  const float2 off = make_float2(-8388608.0f, -8388608.0f);
-  float2 acc = make_float2(0.0f, 0.0f);
-#pragma unroll
-  for (int p = 0; p < 8; ++p) {
-    const int i0 = 2 * p, i1 = 2 * p + 1;
-    const uint32_t s0 = i0 < 11 ? w : w2, s1 = i1 < 11 ? w : w2;
-    const int h0 = i0 < 11 ? 2 * i0 : 2 * (i0 - 11);
-    const int h1 = i1 < 11 ? 2 * i1 : 2 * (i1 - 11);
-    float2 f;
-    f.x = __uint_as_float(floe_ptx::and_or(s0, 3u << h0, magic));
-    f.y = __uint_as_float(floe_ptx::and_or(s1, 3u << h1, magic));
-    f = __fadd2_rn(f, off);
-    acc = __ffma2_rn(f, xs[p], acc);
-  }
-  return acc.x + acc.y;
+// Shared-memory bytes of one K1 stage: codes (16 ch x dh/4 B) + interleaved
+// scale|zero metadata (16 ch x dh/g x 4 B).
+__host__ __device__ constexpr uint32_t k1_stage_bytes(uint32_t dh, uint32_t gpc) {
+  return round_up128(kK1Ch * dh / 4u) + round_up128(kK1Ch * gpc * 4u);
 }
 
 // ---------------------------------------------------------------------------
-// K1: v[c] = sum_k deq(up[c,k]) x[k]; keep |v|>=t; compact kept channels.
+// K1: v[c] = sum_k deq(up[c,k]) x[k]; keep |v| >= t; compact kept channels.
 //
-// CTA b owns channels [di*b/G1, di*(b+1)/G1) (contiguous, balanced to one
-// channel) and walks them in sub-tiles of 16 channels, each bulk-copied:
-// codes 16*dh/4 B, scales and zeros 16*dh/g*2 B.  NS sub-tiles are in flight
-// and nothing on the issue path waits on global memory.  Thread t owns
-// x[16t, 16t+16) (one code word per channel, all in group 16t/g): x stays in
-// registers pre-scaled by 4^-i and the group-affine dequant is folded out of
-// the inner loop:  sum_k (c_k s + z) x_k = s * sum_k c_k x_k + z * sum_k x_k.
-template <int TPB, int NS>
-__global__ void __launch_bounds__(TPB, 2) k1_int2(const K1Args a) {
+// Integer formulation (exact products, 24-bit input precision):
+//   x is scaled once per launch by S = 2^(22-E) (max|x| < 2^E) and rounded to
+//   a 23-bit integer X, split into three signed 8-bit limbs.  Per group g of a
+//   channel, sum_k c_k X_k is accumulated EXACTLY in int32 with IDP4A (four
+//   2-bit codes x four limb bytes per instruction), and
+//       v[c] = sum_g  s_g * (sum_k c_k X_k) / S  +  z_g * sum_k x_k ,
+//   i.e. the group-affine dequant c*s+z of dequantize_at (quant.cpp:104-109)
+//   folded out of the inner loop.  About 1.4 instructions per weight.
+//
+// Work split: CTA b owns channels [di*b/G1, di*(b+1)/G1) (balanced to one
+// channel), walked in sub-tiles of 16 channels, each ONE bulk copy of codes
+// plus one of interleaved metadata, NS sub-tiles in flight.  Thread t owns the
+// 64-element span (t % SPANS) of dh for every channel (x limbs stay in 48
+// registers) and channels q, q+CS, ... of each sub-tile (q = t / SPANS).
+//
+// Non-finite x (inf/NaN) cannot be represented in fixed point: the CTA then
+// takes an f32 per-element path with the reference's own expression.
+template <int SPANS, int NS>
+__global__ void __launch_bounds__(256, 2) k1_int2(const K1Args a) {
+  constexpr int TPB = 256;
   constexpr int NW = TPB / 32;
   constexpr int CH = kK1Ch;
+  constexpr int CS = TPB / SPANS;  // channel slots per CTA
+  constexpr int CPT = CH / CS;     // channels per thread per sub-tile
+  static_assert(SPANS == 64 || SPANS == 32, "dh must be 4096 or 2048");
+  constexpr uint32_t DH = SPANS * 64;
+  constexpr uint32_t ROW = DH / 4;  // code bytes per channel
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t full[NS];
-  __shared__ float wsum[NW][CH];
+  __shared__ float wsum[NW][CPT];
+  __shared__ float red_max[NW];
 
   const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint32_t span = t % SPANS, q = t / SPANS;
   const uint32_t slot = blockIdx.y;
-  const uint32_t e = a.sel ? a.sel[slot] : slot;
-  const ExpertDesc d = a.table[e];
-  const float thr = a.use_threshold ? a.threshold : d.threshold;
-  const uint32_t gpc = a.dh / a.group_size;
-  const uint32_t code_sz = round_up128(CH * TPB * 4u);
-  const uint32_t meta_sz = round_up128(CH * gpc * 2u);
-  const uint32_t stage_sz = code_sz + 2 * meta_sz;
   const uint32_t c_lo = seg_begin(a.di, blockIdx.x, gridDim.x);
   const uint32_t c_hi = seg_begin(a.di, blockIdx.x + 1, gridDim.x);
   const uint32_t n_sub = (c_hi - c_lo + CH - 1) / CH;
+  const uint32_t gpc = DH / a.group_size;
+  const uint32_t code_sz = round_up128(CH * ROW);
+  const uint32_t stage_sz = code_sz + round_up128(CH * gpc * 4u);
 
-  auto issue = [&](uint32_t i) {  // thread 0 only: sub-tile i -> stage i % NS
-    const uint32_t s = i % NS;
-    const uint32_t c0 = c_lo + i * CH;
-    const uint32_t nc = min((uint32_t)CH, c_hi - c0);
-    const uint32_t cb = nc * TPB * 4u, mb = nc * gpc * 2u;
-    uint8_t *st = smem + s * stage_sz;
-    floe_ptx::mbar_arrive_expect_tx(&full[s], cb + 2 * mb);
-    floe_ptx::bulk_g2s(st, d.codes + (size_t)c0 * TPB * 4u, cb, &full[s]);
-    floe_ptx::bulk_g2s(st + code_sz, d.scales + (size_t)c0 * gpc, mb, &full[s]);
-    floe_ptx::bulk_g2s(st + code_sz + meta_sz, d.zeros + (size_t)c0 * gpc, mb, &full[s]);
-  };
+  const uint32_t e = a.sel ? a.sel[slot] : slot;
+  const ExpertDesc d = a.table[e];
+  const float thr = a.use_threshold ? a.threshold : d.threshold;
 
   if (t == 0) {
 #pragma unroll
     for (int s = 0; s < NS; ++s) floe_ptx::mbar_init(&full[s], 1);
     floe_ptx::fence_barrier_init();
-    for (uint32_t i = 0; i < n_sub && i < (uint32_t)NS; ++i) issue(i);
+    for (uint32_t i = 0; i < n_sub && i < (uint32_t)NS; ++i) {
+      const uint32_t c0 = c_lo + i * CH, nc = min((uint32_t)CH, c_hi - c0);
+      floe_ptx::mbar_arrive_expect_tx(&full[i], nc * (ROW + gpc * 4u));
+      floe_ptx::bulk_g2s(smem + i * stage_sz, d.codes + (size_t)c0 * ROW, nc * ROW, &full[i]);
+      floe_ptx::bulk_g2s(smem + i * stage_sz + code_sz, d.meta + (size_t)c0 * gpc, nc * gpc * 4u,
+                         &full[i]);
+    }
   }
   if (a.y_zero && blockIdx.x == 0 && slot == 0)
     for (uint32_t i = t; i < a.dh; i += TPB) a.y_zero[i] = 0.0f;
 
-  float2 xs[8];
-  float xsum = 0.0f;
+  // ---- x: load this thread's 64-element span, block max|x| -> scale S ----
+  float xv[64];
   {
-    const float4 *x4 = reinterpret_cast<const float4 *>(a.x) + 4 * t;
-    float xr[16];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float4 f = x4[q];
-      xr[4 * q] = f.x;
-      xr[4 * q + 1] = f.y;
-      xr[4 * q + 2] = f.z;
-      xr[4 * q + 3] = f.w;
-    }
+    const float4 *x4 = reinterpret_cast<const float4 *>(a.x + 64 * span);
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      xsum += xr[i];
-      const int sh = i < 11 ? 2 * i : 2 * (i - 11);
-      xr[i] *= __int_as_float((127 - sh) << 23);  // * 4^-i, exact
+      const float4 f = x4[i];
+      xv[4 * i] = f.x;
+      xv[4 * i + 1] = f.y;
+      xv[4 * i + 2] = f.z;
+      xv[4 * i + 3] = f.w;
     }
-#pragma unroll
-    for (int p = 0; p < 8; ++p) xs[p] = make_float2(xr[2 * p], xr[2 * p + 1]);
   }
-  const uint32_t gcol = (16u * t) / a.group_size;
-  uint32_t running = 0;
+  float m = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 64; ++i) m = fmaxf(m, fabsf(xv[i]));  // NaN ignored by fmaxf
+  bool finite = true;
+#pragma unroll
+  for (int i = 0; i < 64; ++i) finite = finite && isfinite(xv[i]);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const bool warp_finite = __all_sync(0xffffffffu, finite);
+  if (lane == 0) red_max[warp] = warp_finite ? m : -1.0f;
   __syncthreads();
+  bool all_finite = true;
+  m = 0.0f;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    all_finite = all_finite && red_max[w] >= 0.0f;
+    m = fmaxf(m, red_max[w]);
+  }
+  int ex = 0;
+  frexpf(m, &ex);  // m < 2^ex
+  const float S = m > 0.0f ? ldexpf(1.0f, 22 - ex) : 1.0f;
+  const float invS = m > 0.0f ? ldexpf(1.0f, ex - 22) : 1.0f;
 
-  for (uint32_t i = 0; i < n_sub; ++i) {
-    const uint32_t s = i % NS;
-    floe_ptx::mbar_wait(&full[s], (i / NS) & 1u);
-    const uint8_t *st = smem + s * stage_sz;
-    const uint32_t *cw = reinterpret_cast<const uint32_t *>(st);
-    const uint16_t *sc = reinterpret_cast<const uint16_t *>(st + code_sz);
-    const uint16_t *zr = reinterpret_cast<const uint16_t *>(st + code_sz + meta_sz);
-    const uint32_t c0 = c_lo + i * CH;
-    const uint32_t nc = min((uint32_t)CH, c_hi - c0);
-    float part[CH];
+  // limbs: lw[l][i][mm] packs limb l of elements 16i+mm+4b (b = 0..3), the
+  // byte order produced by (w >> 2mm) & 0x03030303 on code word i.
+  uint32_t lw[3][4][4];
+  constexpr int GPT_MAX = 4;  // group parts per span (g = 16)
+  float xpart[GPT_MAX];
+  const uint32_t parts = a.group_size >= 64 ? 1u : 64u / a.group_size;  // 1, 2 or 4
+  const uint32_t words_per_part = 4u / parts;
 #pragma unroll
-    for (int j = 0; j < CH; ++j) {
-      part[j] = 0.0f;
-      if ((uint32_t)j < nc) {  // CTA-uniform
-        const uint32_t w = cw[j * TPB + t];
-        const float sj = h2f(sc[j * gpc + gcol]);
-        const float zj = h2f(zr[j * gpc + gcol]);
-        part[j] = fmaf(sj, dot16_int2(w, xs), zj * xsum);
+  for (int p = 0; p < GPT_MAX; ++p) xpart[p] = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int mm = 0; mm < 4; ++mm) {
+      uint32_t l0 = 0, l1 = 0, l2 = 0;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const float xf = xv[16 * i + mm + 4 * b];
+        const int X = all_finite ? __float2int_rn(xf * S) : 0;
+        const int X0 = ((X + 128) & 255) - 128;
+        const int R = (X - X0) >> 8;
+        const int X1 = ((R + 128) & 255) - 128;
+        const int X2 = (R - X1) >> 8;
+        l0 |= (uint32_t)(X0 & 255) << (8 * b);
+        l1 |= (uint32_t)(X1 & 255) << (8 * b);
+        l2 |= (uint32_t)(X2 & 255) << (8 * b);
       }
+      lw[0][i][mm] = l0;
+      lw[1][i][mm] = l1;
+      lw[2][i][mm] = l2;
     }
-    // transposed butterfly over 16 channels, then fold the two half-warps:
-    // lane l (and l^16) ends with the warp sum of channel l&15.
+  }
 #pragma unroll
-    for (int sft = 8; sft >= 1; sft >>= 1) {
+  for (int i = 0; i < 64; ++i) xpart[(i / 16) / words_per_part] += xv[i];
+  const uint32_t g0 = (64u * span) / a.group_size;  // first group of this span
+
+  uint32_t running = 0;
+  for (uint32_t it = 0; it < n_sub; ++it) {
+    const uint32_t s = it % NS;
+    floe_ptx::mbar_wait(&full[s], (it / NS) & 1u);
+    const uint8_t *st = smem + s * stage_sz;
+    const uint32_t c0 = c_lo + it * CH;
+    const uint32_t nc = min((uint32_t)CH, c_hi - c0);
+    float part[CPT];
+#pragma unroll
+    for (int r = 0; r < CPT; ++r) {
+      const uint32_t j = q + CS * r;
+      float acc = 0.0f;
+      if (j < nc) {
+        const uint4 w4 = *reinterpret_cast<const uint4 *>(st + j * ROW + 16 * span);
+        const uint32_t *meta = reinterpret_cast<const uint32_t *>(st + code_sz) + j * gpc + g0;
+        const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
+        if (all_finite) {
+#pragma unroll
+          for (int p = 0; p < GPT_MAX; ++p) {
+            if ((uint32_t)p >= parts) break;
+            int a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              if ((uint32_t)i / words_per_part != (uint32_t)p) continue;
+#pragma unroll
+              for (int mm = 0; mm < 4; ++mm) {
+                const int cb = (int)((wv[i] >> (2 * mm)) & 0x03030303u);
+                a0 = __dp4a(cb, (int)lw[0][i][mm], a0);
+                a1 = __dp4a(cb, (int)lw[1][i][mm], a1);
+                a2 = __dp4a(cb, (int)lw[2][i][mm], a2);
+              }
+            }
+            const int T = a2 * 65536 + a1 * 256 + a0;
+            const uint32_t mz = meta[p * (a.group_size >= 64 ? 0 : 1)];
+            const float sc = __half2float(__ushort_as_half((uint16_t)(mz & 0xffffu)));
+            const float zr = __half2float(__ushort_as_half((uint16_t)(mz >> 16)));
+            acc = fmaf(sc * invS, (float)T, fmaf(zr, xpart[p], acc));
+          }
+        } else {
+          // non-finite x: f32 per element, reference expression
+          const float *xg = a.x + 64 * span;
+          for (int i = 0; i < 64; ++i) {
+            const uint32_t mz = meta[(uint32_t)i / a.group_size * (a.group_size >= 64 ? 0 : 1)];
+            const float sc = __half2float(__ushort_as_half((uint16_t)(mz & 0xffffu)));
+            const float zr = __half2float(__ushort_as_half((uint16_t)(mz >> 16)));
+            const uint32_t code = (wv[i / 16] >> (2 * (i % 16))) & 3u;
+            acc = fmaf(fmaf((float)code, sc, zr), xg[i], acc);
+          }
+        }
+      }
+      part[r] = acc;
+    }
+    // transposed butterfly: CPT values -> lane holds channel r(lane) summed
+    // over the lanes of its warp; lanes with (lane & (32/CPT - 1)) == 0 write.
+#pragma unroll
+    for (int sft = 16, cnt = CPT / 2; cnt >= 1; sft >>= 1, cnt >>= 1) {
       const bool upper = (lane & sft) != 0;
 #pragma unroll
-      for (int j = 0; j < sft; ++j) {
-        const float send = upper ? part[j] : part[j + sft];
-        const float keep = upper ? part[j + sft] : part[j];
-        part[j] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+      for (int r = 0; r < cnt; ++r) {
+        const float send = upper ? part[r] : part[r + cnt];
+        const float keep = upper ? part[r + cnt] : part[r];
+        part[r] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
       }
     }
-    part[0] += __shfl_xor_sync(0xffffffffu, part[0], 16);
-    if (lane < CH) wsum[warp][lane] = part[0];
-    __syncthreads();  // wsum complete; stage s fully consumed
-    if (t == 0 && i + NS < n_sub) issue(i + NS);
-    if (warp == 0) {
-      float v = 0.0f;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) v += wsum[w][lane & (CH - 1)];
-      seg_emit(a, slot, c_lo, c0 + lane, lane < nc, v, thr, running);
+    for (int sft = 32 / CPT / 2; sft >= 1; sft >>= 1)
+      part[0] += __shfl_xor_sync(0xffffffffu, part[0], sft);
+    if ((lane & (32 / CPT - 1)) == 0) wsum[warp][lane / (32 / CPT)] = part[0];
+    __syncthreads();  // wsum complete; stage s fully consumed
+    if (t == 0 && it + NS < n_sub) {
+      const uint32_t c1 = c_lo + (it + NS) * CH, n1 = min((uint32_t)CH, c_hi - c1);
+      floe_ptx::mbar_arrive_expect_tx(&full[s], n1 * (ROW + gpc * 4u));
+      floe_ptx::bulk_g2s(smem + s * stage_sz, d.codes + (size_t)c1 * ROW, n1 * ROW, &full[s]);
+      floe_ptx::bulk_g2s(smem + s * stage_sz + code_sz, d.meta + (size_t)c1 * gpc,
+                         n1 * gpc * 4u, &full[s]);
+    }
+    if (warp == 0) {
+      // channel j = q + CS*r is reduced by warps q*SPANS/32 .. +SPANS/32-1
+      const uint32_t j = lane;
+      float v = 0.0f;
+      if (j < (uint32_t)CH) {
+        const uint32_t qq = j % CS, rr = j / CS;
+#pragma unroll
+        for (int w = 0; w < SPANS / 32; ++w) v += wsum[qq * (SPANS / 32) + w][rr];
+      }
+      seg_emit(a, slot, c_lo, c0 + j, j < nc, v, thr, running);
     }
     __syncthreads();  // wsum reuse
   }
@@ -174,14 +256,16 @@ __global__ void __launch_bounds__(TPB, 2) k1_int2(const K1Args a) {
 // ---------------------------------------------------------------------------
 // K2: y += sum_{kept c} silu(gate_c . x) * v[c] * w_slot * down_c.
 //
-// Kept entries of all slots are split evenly over CTAs (exact balance however
-// the channels fell).  The CTA first resolves its entries' (record address,
-// v * routing weight) into shared memory with all threads in parallel, so the
-// issuing thread never waits on global memory; then each entry's 4*dh-byte
-// record (gate row | down row, f16) arrives with ONE bulk copy into an
-// NS-deep ring.  Thread t owns 16-byte chunks t and t+TPB of each half-record
-// (elements [8t, 8t+8) and [8(t+TPB), ...)): conflict-free 128-bit smem reads.
-constexpr uint32_t kK2Chunk = 256;  // entries resolved per preload round
+// One CTA per SM.  Kept entries of all slots are split evenly over CTAs
+// (exact balance however the channels fell).  The per-slot record base
+// (sel -> table -> records) and routing weight are resolved once per CTA in
+// parallel with the segment scan; then all entries' (record address, v * w)
+// are resolved in one parallel round, so the issuing thread never waits on
+// global memory.  Each entry's 4*dh-byte record (gate row | down row, f16)
+// is ONE bulk copy into an NS-deep ring (NS*16 KB in flight per SM).
+// Thread t owns 16-byte chunks t and t+TPB of each half-record (elements
+// [8t, 8t+8) and [8(t+TPB), ...)): conflict-free 128-bit smem reads.
+constexpr uint32_t kK2Chunk = 512;  // entries resolved per preload round
 
 template <int TPB, int NS>
 __global__ void __launch_bounds__(TPB, 1) k2_gate_down(const K2Args a) {
@@ -191,12 +275,19 @@ __global__ void __launch_bounds__(TPB, 1) k2_gate_down(const K2Args a) {
   __shared__ float red[2][NW];
   __shared__ const __half *ent_rec[kK2Chunk];
   __shared__ float ent_scale[kK2Chunk];
+  __shared__ const __half *slot_rec[kMaxSlots];
+  __shared__ float slot_w[kMaxSlots];
 
   const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const uint32_t rec_bytes = 4u * a.dh;  // == 64 * TPB
   const uint32_t nseg = a.slots * a.g1;
+  if (t < a.slots) {
+    const uint32_t e = a.sel ? a.sel[t] : t;
+    slot_rec[t] = a.table[e].records;
+    slot_w[t] = slot_weight(a, t);
+  }
   uint32_t *prefix = reinterpret_cast<uint32_t *>(smem + NS * rec_bytes);
-  seg_prefix(a.seg_count, nseg, prefix);
+  seg_prefix(a.seg_count, nseg, prefix);  // contains __syncthreads
   k2_publish(a, prefix);
   const uint32_t total = prefix[nseg];
   const uint32_t begin = (uint32_t)(((uint64_t)total * blockIdx.x) / gridDim.x);
@@ -227,22 +318,25 @@ __global__ void __launch_bounds__(TPB, 1) k2_gate_down(const K2Args a) {
   uint32_t it = 0;  // global iteration count (ring position / parity)
   for (uint32_t cb = begin; cb < end; cb += kK2Chunk) {
     const uint32_t n = min(kK2Chunk, end - cb);
-    __syncthreads();  // previous chunk's ent_* fully consumed
-    for (uint32_t q = t; q < n; q += TPB) {
-      const KeptEntry k = kept_entry(a, prefix, cb + q);
-      const uint32_t e = a.sel ? a.sel[k.slot] : k.slot;
-      ent_rec[q] = a.table[e].records + (size_t)k.c * 2 * a.dh;
-      ent_scale[q] = k.v * slot_weight(a, k.slot);
-      if (a.kept_out) a.kept_out[(size_t)k.slot * a.di + k.slot_pos] = k.c;
+    __syncthreads();  // previous chunk's ent_* consumed; slot_* visible
+    for (uint32_t qq = t; qq < n; qq += TPB) {
+      const uint32_t p = cb + qq;
+      const uint32_t idx = seg_find(prefix, nseg, p);
+      const uint32_t slot = idx / a.g1, b = idx % a.g1;
+      const size_t o = (size_t)slot * a.di + seg_begin(a.di, b, a.g1) + (p - prefix[idx]);
+      const uint32_t c = a.kept_idx[o];
+      ent_rec[qq] = slot_rec[slot] + (size_t)c * 2 * a.dh;
+      ent_scale[qq] = a.kept_v[o] * slot_w[slot];
+      if (a.kept_out) a.kept_out[(size_t)slot * a.di + (p - prefix[slot * a.g1])] = c;
     }
     __syncthreads();
     if (t == 0)
-      for (uint32_t q = 0; q < n && q < (uint32_t)NS; ++q) {
-        const uint32_t s = (it + q) % NS;
+      for (uint32_t qq = 0; qq < n && qq < (uint32_t)NS; ++qq) {
+        const uint32_t s = (it + qq) % NS;
         floe_ptx::mbar_arrive_expect_tx(&full[s], rec_bytes);
-        floe_ptx::bulk_g2s(smem + s * rec_bytes, ent_rec[q], rec_bytes, &full[s]);
+        floe_ptx::bulk_g2s(smem + s * rec_bytes, ent_rec[qq], rec_bytes, &full[s]);
       }
-    for (uint32_t q = 0; q < n; ++q, ++it) {
+    for (uint32_t qq = 0; qq < n; ++qq, ++it) {
       const uint32_t s = it % NS;
       floe_ptx::mbar_wait(&full[s], (it / NS) & 1u);
       const uint4 *rec = reinterpret_cast<const uint4 *>(smem + s * rec_bytes);
@@ -263,14 +357,14 @@ __global__ void __launch_bounds__(TPB, 1) k2_gate_down(const K2Args a) {
       for (int o = 16; o >= 1; o >>= 1) gp += __shfl_xor_sync(0xffffffffu, gp, o);
       if (lane == 0) red[it & 1][warp] = gp;
       __syncthreads();  // red complete; stage s fully read
-      if (t == 0 && q + NS < n) {
+      if (t == 0 && qq + NS < n) {
         floe_ptx::mbar_arrive_expect_tx(&full[s], rec_bytes);
-        floe_ptx::bulk_g2s(smem + s * rec_bytes, ent_rec[q + NS], rec_bytes, &full[s]);
+        floe_ptx::bulk_g2s(smem + s * rec_bytes, ent_rec[qq + NS], rec_bytes, &full[s]);
       }
       float g = 0.0f;
 #pragma unroll
       for (int w = 0; w < NW; ++w) g += red[it & 1][w];
-      const float aco = silu_ref(g) * ent_scale[q];
+      const float aco = silu_ref(g) * ent_scale[qq];
       const float2 a2 = make_float2(aco, aco);
       const __half2 *e0 = reinterpret_cast<const __half2 *>(&d0);
       const __half2 *e1 = reinterpret_cast<const __half2 *>(&d1);
@@ -287,6 +381,148 @@ __global__ void __launch_bounds__(TPB, 1) k2_gate_down(const K2Args a) {
     red_add_v4(ya + 4, y2[2].x, y2[2].y, y2[3].x, y2[3].y);
     red_add_v4(yb, y2[4].x, y2[4].y, y2[5].x, y2[5].y);
     red_add_v4(yb + 4, y2[6].x, y2[6].y, y2[7].x, y2[7].y);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Block head: u = h + mixing.h; y = u; logits = router.u; top-k; softmax.
+//
+// One CTA per SM; CTA b owns rows [dh*b/G, dh*(b+1)/G), streamed in chunks of
+// RPC rows (32 KB) by bulk copy through an NS-deep ring, h bulk-copied once.
+// WPR = 8/RPC warps share a row (K-split, combined in smem).  Each CTA also
+// folds its rows into partial router logits; the last CTA (done counter,
+// reset in-kernel) sums the partials in a fixed order and routes.
+// Deterministic: no float atomics.
+constexpr uint32_t kMaxRowsPerCta = 48;
+
+template <typename T, int NS>
+__global__ void __launch_bounds__(256, 1) mixing_route_bulk(const MixArgs a) {
+  constexpr uint32_t CHUNK = 32768;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t full[NS + 1];  // [NS] = h
+  __shared__ float rsum[8];
+  __shared__ float usum[8];
+  __shared__ float pl[32];
+  __shared__ float logits[32];
+  __shared__ float rs[32 * kMaxRowsPerCta];  // router[e][this CTA's rows]
+  __shared__ bool last;
+  const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint32_t row_bytes = a.dh * (uint32_t)sizeof(T);
+  uint32_t rpc = CHUNK / row_bytes;  // rows per chunk (power of two, <= 8)
+  rpc = rpc >= 8 ? 8 : rpc >= 4 ? 4 : rpc >= 2 ? 2 : 1;
+  const uint32_t wpr = 8 / rpc;  // warps per row
+  const uint32_t r_lo = seg_begin(a.dh, blockIdx.x, gridDim.x);
+  const uint32_t r_hi = seg_begin(a.dh, blockIdx.x + 1, gridDim.x);
+  const uint32_t n_chunks = (r_hi - r_lo + rpc - 1) / rpc;
+  const uint32_t stage_sz = round_up128(rpc * row_bytes);
+  float *hs = reinterpret_cast<float *>(smem + NS * stage_sz);
+  const T *m = static_cast<const T *>(a.m);
+
+  if (t == 0) {
+#pragma unroll
+    for (int s = 0; s <= NS; ++s) floe_ptx::mbar_init(&full[s], 1);
+    floe_ptx::fence_barrier_init();
+    floe_ptx::mbar_arrive_expect_tx(&full[NS], 4u * a.dh);
+    floe_ptx::bulk_g2s(hs, a.h, 4u * a.dh, &full[NS]);
+    for (uint32_t i = 0; i < n_chunks && i < (uint32_t)NS; ++i) {
+      const uint32_t r0 = r_lo + i * rpc, nr = min(rpc, r_hi - r0);
+      floe_ptx::mbar_arrive_expect_tx(&full[i], nr * row_bytes);
+      floe_ptx::bulk_g2s(smem + i * stage_sz, m + (size_t)r0 * a.dh, nr * row_bytes, &full[i]);
+    }
+  }
+  if (t < 32) pl[t] = 0.0f;
+  // router slice for this CTA's rows, fetched while the bulk copies fly
+  for (uint32_t i = t; i < a.E * kMaxRowsPerCta; i += 256) {
+    const uint32_t e = i / kMaxRowsPerCta, lr = i % kMaxRowsPerCta;
+    if (r_lo + lr < r_hi) rs[i] = a.router[(size_t)e * a.dh + r_lo + lr];
+  }
+  __syncthreads();
+  floe_ptx::mbar_wait(&full[NS], 0);
+
+  const uint32_t my_row = warp / wpr, my_part = warp % wpr;
+  const uint32_t k_lo = a.dh * my_part / wpr, k_hi = a.dh * (my_part + 1) / wpr;
+  constexpr uint32_t EPL = 16 / sizeof(T);  // elements per 128-bit smem load
+  for (uint32_t ci = 0; ci < n_chunks; ++ci) {
+    const uint32_t s = ci % NS;
+    floe_ptx::mbar_wait(&full[s], (ci / NS) & 1u);
+    const uint32_t r0 = r_lo + ci * rpc, nr = min(rpc, r_hi - r0);
+    float acc = 0.0f;
+    if (my_row < nr) {
+      const T *rowp = reinterpret_cast<const T *>(smem + s * stage_sz) + (size_t)my_row * a.dh;
+      for (uint32_t k = k_lo + lane * EPL; k < k_hi; k += 32 * EPL) {
+        const uint4 qv = *reinterpret_cast<const uint4 *>(rowp + k);
+        const float4 h0 = *reinterpret_cast<const float4 *>(hs + k);
+        if constexpr (sizeof(T) == 2) {
+          const float4 h1 = *reinterpret_cast<const float4 *>(hs + k + 4);
+          const __half2 *hh = reinterpret_cast<const __half2 *>(&qv);
+          const float2 f0 = __half22float2(hh[0]), f1 = __half22float2(hh[1]);
+          const float2 f2 = __half22float2(hh[2]), f3 = __half22float2(hh[3]);
+          acc = fmaf(f0.x, h0.x, acc);
+          acc = fmaf(f0.y, h0.y, acc);
+          acc = fmaf(f1.x, h0.z, acc);
+          acc = fmaf(f1.y, h0.w, acc);
+          acc = fmaf(f2.x, h1.x, acc);
+          acc = fmaf(f2.y, h1.y, acc);
+          acc = fmaf(f3.x, h1.z, acc);
+          acc = fmaf(f3.y, h1.w, acc);
+        } else {
+          acc = fmaf(__uint_as_float(qv.x), h0.x, acc);
+          acc = fmaf(__uint_as_float(qv.y), h0.y, acc);
+          acc = fmaf(__uint_as_float(qv.z), h0.z, acc);
+          acc = fmaf(__uint_as_float(qv.w), h0.w, acc);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) rsum[warp] = acc;
+    __syncthreads();  // rsum complete; stage s consumed
+    if (t == 0 && ci + NS < n_chunks) {
+      const uint32_t r1 = r_lo + (ci + NS) * rpc, n1 = min(rpc, r_hi - r1);
+      floe_ptx::mbar_arrive_expect_tx(&full[s], n1 * row_bytes);
+      floe_ptx::bulk_g2s(smem + s * stage_sz, m + (size_t)r1 * a.dh, n1 * row_bytes, &full[s]);
+    }
+    if (warp == 0 && lane < nr) {
+      float dot = 0.0f;
+      for (uint32_t p = 0; p < wpr; ++p) dot += rsum[lane * wpr + p];
+      const uint32_t row = r0 + lane;
+      const float uu = hs[row] + 1.0f * dot;  // drift_scale = 1 (model.cpp:151-152)
+      a.u[row] = uu;
+      a.y_init[row] = uu;
+      if (a.u_trace) a.u_trace[row] = uu;
+      usum[lane] = uu;
+    }
+    __syncwarp();
+    if (warp == 0 && lane < a.E) {  // router partial logits for these rows
+      float sacc = pl[lane];
+      for (uint32_t r = 0; r < nr; ++r) {
+        const uint32_t lr = r0 + r - r_lo;
+        const float w = lr < kMaxRowsPerCta ? rs[lane * kMaxRowsPerCta + lr]
+                                            : a.router[(size_t)lane * a.dh + r0 + r];
+        sacc += w * usum[r];
+      }
+      pl[lane] = sacc;
+    }
+    __syncthreads();
+  }
+  if (t < a.E) a.partial[blockIdx.x * a.E + t] = pl[t];
+  __threadfence();
+  __syncthreads();
+  if (t == 0) last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (uint32_t e = warp; e < a.E; e += 8) {
+    float sacc = 0.0f;
+    for (uint32_t b = lane; b < gridDim.x; b += 32) sacc += __ldcg(&a.partial[b * a.E + e]);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+    if (lane == 0) logits[e] = sacc;
+  }
+  __syncthreads();
+  if (t == 0) {
+    *a.done = 0;
+    route_finish(logits, a.E, a.k, a.sel, a.weights, a.sel_trace, a.w_trace);
   }
 }
 

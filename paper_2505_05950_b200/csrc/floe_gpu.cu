@@ -257,13 +257,13 @@ int launch_k1(const K1Launch &L, floe_gpu_workspace *ws, cudaStream_t st) {
   if (fast) {
     constexpr int NS = 4;
     const uint32_t gpc = L.dh / L.g;
-    const uint32_t smem = NS * floe_k::k1_stage_bytes(tpb, gpc);
-    if (tpb == 256) {
-      if (int rc = set_smem(floe_k::k1_int2<256, NS>, smem)) return rc;
-      floe_k::k1_int2<256, NS><<<grid, 256, smem, st>>>(a);
+    const uint32_t smem = NS * floe_k::k1_stage_bytes(L.dh, gpc);
+    if (L.dh == 4096) {
+      if (int rc = set_smem(floe_k::k1_int2<64, NS>, smem)) return rc;
+      floe_k::k1_int2<64, NS><<<grid, 256, smem, st>>>(a);
     } else {
-      if (int rc = set_smem(floe_k::k1_int2<128, NS>, smem)) return rc;
-      floe_k::k1_int2<128, NS><<<grid, 128, smem, st>>>(a);
+      if (int rc = set_smem(floe_k::k1_int2<32, NS>, smem)) return rc;
+      floe_k::k1_int2<32, NS><<<grid, 256, smem, st>>>(a);
     }
   } else {
     floe_k::k1_generic<<<grid, 256, 0, st>>>(a);
@@ -311,14 +311,16 @@ int launch_k2(const K2Launch &L, floe_gpu_workspace *ws, cudaStream_t st) {
   }
   StageScope prof(ws, kStageK2, st);
   if (L.fast && (tpb == 256 || tpb == 128)) {
-    constexpr int NS = 4;
+    // one CTA per SM, 160 KB of records in flight per SM
+    constexpr int NS = 10;
     const uint32_t smem = NS * 4u * L.dh + prefix_bytes;
     if (tpb == 256) {
       if (int rc = set_smem(floe_k::k2_gate_down<256, NS>, smem)) return rc;
-      floe_k::k2_gate_down<256, NS><<<2 * sm, 256, smem, st>>>(a);
+      floe_k::k2_gate_down<256, NS><<<sm, 256, smem, st>>>(a);
     } else {
-      if (int rc = set_smem(floe_k::k2_gate_down<128, NS>, smem)) return rc;
-      floe_k::k2_gate_down<128, NS><<<2 * sm, 128, smem, st>>>(a);
+      if (int rc = set_smem(floe_k::k2_gate_down<128, 2 * NS>, smem + NS * 4u * L.dh))
+        return rc;
+      floe_k::k2_gate_down<128, 2 * NS><<<sm, 128, smem + NS * 4u * L.dh, st>>>(a);
     }
   } else {
     if (int rc = set_smem(floe_k::k2_generic, prefix_bytes)) return rc;
@@ -386,17 +388,19 @@ int floe_gpu_expert_create(const floe_expert_host_view *v, floe_gpu_expert **out
   e->code_bytes = packed_code_bytes(n, v->bits);
   e->n_groups = n / v->group_size;
   const int tpb = fast_tpb(e->dh);
-  // K1 fast path: INT2 words stay inside one group, and per-channel metadata
-  // rows are 16-byte multiples (bulk-copy granularity).
-  e->fast_k1 = tpb && e->bits == 2 && e->g % 16 == 0 && e->dh % e->g == 0 &&
-               (e->dh / e->g) % 8 == 0;
+  // K1 fast path: a thread's 64-element span holds whole groups or lies in
+  // one group, and per-channel metadata rows are 16-byte multiples.
+  const bool g_ok = e->g % 64 == 0 || (e->g % 16 == 0 && 64 % e->g == 0);
+  e->fast_k1 = tpb && e->bits == 2 && g_ok && e->dh % e->g == 0 && (e->dh / e->g) % 4 == 0;
   e->fast_k2 = tpb != 0;
 
-  // One allocation, 256-B aligned sections: [desc][codes][scales][zeros][records]
+  // One allocation, 256-B aligned sections:
+  //   [desc][codes][scales][zeros][meta = scale|zero<<16][records]
   const uint64_t o_codes = up256(sizeof(ExpertDesc));
   const uint64_t o_scales = up256(o_codes + e->code_bytes);
   const uint64_t o_zeros = up256(o_scales + 2 * e->n_groups);
-  const uint64_t o_rec = up256(o_zeros + 2 * e->n_groups);
+  const uint64_t o_meta = up256(o_zeros + 2 * e->n_groups);
+  const uint64_t o_rec = up256(o_meta + 4 * e->n_groups);
   const uint64_t total = o_rec + 4 * n;
   cudaError_t ce = cudaMalloc(&e->block, total);
   if (ce != cudaSuccess) {
@@ -410,6 +414,7 @@ int floe_gpu_expert_create(const floe_expert_host_view *v, floe_gpu_expert **out
   e->host_desc.scales = reinterpret_cast<const uint16_t *>(base + o_scales);
   e->host_desc.zeros = reinterpret_cast<const uint16_t *>(base + o_zeros);
   e->host_desc.records = reinterpret_cast<const __half *>(base + o_rec);
+  e->host_desc.meta = reinterpret_cast<const uint32_t *>(base + o_meta);
   e->host_desc.threshold = v->threshold;
 
   auto cleanup = [&](int rc) {
@@ -428,6 +433,13 @@ int floe_gpu_expert_create(const floe_expert_host_view *v, floe_gpu_expert **out
   cp(base + o_codes, v->codes, e->code_bytes);
   cp(base + o_scales, v->scales, 2 * e->n_groups);
   cp(base + o_zeros, v->zeros, 2 * e->n_groups);
+  if (err == cudaSuccess) {
+    floe_k::interleave_meta<<<1024, 256, 0, st>>>(
+        reinterpret_cast<const uint16_t *>(base + o_scales),
+        reinterpret_cast<const uint16_t *>(base + o_zeros), e->n_groups,
+        reinterpret_cast<uint32_t *>(base + o_meta));
+    err = cudaGetLastError();
+  }
   __half *rec = reinterpret_cast<__half *>(base + o_rec);
   if (v->records_f16) {
     cp(rec, v->records_f16, 4 * n);
@@ -513,7 +525,7 @@ int floe_gpu_workspace_create(uint32_t dh, uint32_t di, uint32_t slots,
   const uint64_t o_idx = o;   o = up256(o + 4 * sd);
   const uint64_t o_kv = o;    o = up256(o + 4 * sd);
   const uint64_t o_cnt = o;   o = up256(o + 4ull * MS * kMaxSeg);
-  const uint64_t o_mp = o;    o = up256(o + 4ull * 32 * ((dh + 7) / 8));
+  const uint64_t o_mp = o;    o = up256(o + 4ull * 32 * std::max<uint64_t>(1024, (dh + 7) / 8));
   const uint64_t o_md = o;    o = up256(o + 16);
   const uint64_t o_st = o;    o = up256(o + 16);
   const uint64_t o_sel = o;   o = up256(o + 4 * MS);
@@ -787,11 +799,30 @@ int floe_gpu_layer_forward(const floe_gpu_layer *l, floe_gpu_workspace *ws, cons
     m.weights = ws->weights;
     m.sel_trace = tr ? tr->experts_dev : nullptr;
     m.w_trace = tr ? tr->weights_dev : nullptr;
-    const dim3 grid((l->dh + rows_per_block - 1) / rows_per_block);
-    if (l->mix_f16)
-      floe_k::mixing_route<__half><<<grid, 256, smem, st>>>(m);
-    else
-      floe_k::mixing_route<float><<<grid, 256, smem, st>>>(m);
+    const uint32_t sm = (uint32_t)device_info().sm;
+    const uint32_t bulk_grid = std::min<uint32_t>(sm, l->dh);
+    const bool bulk = l->dh % 8 == 0 &&
+                      (l->dh + bulk_grid - 1) / bulk_grid <= floe_k::kMaxRowsPerCta;
+    if (bulk) {
+      constexpr int NS = 4;
+      const uint32_t row_bytes = l->dh * (l->mix_f16 ? 2u : 4u);
+      uint32_t rpc = 32768u / row_bytes;
+      rpc = rpc >= 8 ? 8 : rpc >= 4 ? 4 : rpc >= 2 ? 2 : 1;
+      const uint32_t bsmem = NS * floe_k::round_up128(rpc * row_bytes) + 4u * l->dh;
+      if (l->mix_f16) {
+        if (int rc = set_smem(floe_k::mixing_route_bulk<__half, NS>, bsmem)) return rc;
+        floe_k::mixing_route_bulk<__half, NS><<<bulk_grid, 256, bsmem, st>>>(m);
+      } else {
+        if (int rc = set_smem(floe_k::mixing_route_bulk<float, NS>, bsmem)) return rc;
+        floe_k::mixing_route_bulk<float, NS><<<bulk_grid, 256, bsmem, st>>>(m);
+      }
+    } else {
+      const dim3 grid((l->dh + rows_per_block - 1) / rows_per_block);
+      if (l->mix_f16)
+        floe_k::mixing_route<__half><<<grid, 256, smem, st>>>(m);
+      else
+        floe_k::mixing_route<float><<<grid, 256, smem, st>>>(m);
+    }
     CK_LAUNCH();
   }
   K1Launch k1{l->table, ws->sel, l->top_k, l->dh, l->di, l->bits, l->g, l->fast_k1, 0, 0.0f,

@@ -36,8 +36,9 @@ struct ExpertDesc {
   const uint16_t *scales;
   const uint16_t *zeros;
   const __half *records;  // [di][2*dh]
+  const uint32_t *meta;   // [di][dh/g] scale16 | zero16 << 16 (K1 fast path)
   float threshold;
-  uint32_t pad_[3];
+  uint32_t pad_;
 };
 
 // Kept-channel lists ("segments").  K1 runs on a (G1, slots) grid; CTA b of
@@ -322,6 +323,15 @@ __global__ void pack_records(const float *gate, const float *down, uint32_t dh,
   }
 }
 
+// Device metadata layout for the K1 fast path: one u32 per group holding the
+// f16 scale (low half) and f16 zero (high half) -> one 4-byte load per group.
+__global__ void interleave_meta(const uint16_t *scales, const uint16_t *zeros, uint64_t n,
+                                uint32_t *meta) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    meta[i] = (uint32_t)scales[i] | ((uint32_t)zeros[i] << 16);
+}
+
 __global__ void f32_to_f16_rn(const float *in, uint64_t n, __half *out) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x)
@@ -352,6 +362,31 @@ struct MixArgs {
 };
 
 __device__ inline void topk_small(const float *v, uint32_t n, uint32_t k, uint32_t *out);
+
+// route (model.cpp:83-93) after the logits: top_k, softmax over the selected
+// logits (la.cpp:37-46), outputs.  One thread.
+__device__ inline void route_finish(const float *logits, uint32_t E, uint32_t k, uint32_t *sel,
+                                    float *weights, uint32_t *sel_trace, float *w_trace) {
+  uint32_t sidx[32];
+  topk_small(logits, E, k, sidx);
+  float wv[32];
+  for (uint32_t i = 0; i < k; ++i) wv[i] = logits[sidx[i]];
+  float mx = wv[0];
+  for (uint32_t i = 1; i < k; ++i)
+    if (mx < wv[i]) mx = wv[i];
+  float sum = 0.0f;
+  for (uint32_t i = 0; i < k; ++i) {
+    wv[i] = expf(wv[i] - mx);
+    sum += wv[i];
+  }
+  for (uint32_t i = 0; i < k; ++i) wv[i] /= sum;
+  for (uint32_t i = 0; i < k; ++i) {
+    sel[i] = sidx[i];
+    weights[i] = wv[i];
+    if (sel_trace) sel_trace[i] = sidx[i];
+    if (w_trace) w_trace[i] = wv[i];
+  }
+}
 
 template <typename T>
 __global__ void __launch_bounds__(256) mixing_route(const MixArgs a) {
@@ -430,25 +465,7 @@ __global__ void __launch_bounds__(256) mixing_route(const MixArgs a) {
   __syncthreads();
   if (threadIdx.x == 0) {
     *a.done = 0;
-    uint32_t sidx[32];
-    topk_small(logits, a.E, a.k, sidx);
-    float wv[32];
-    for (uint32_t i = 0; i < a.k; ++i) wv[i] = logits[sidx[i]];
-    float mx = wv[0];  // softmax_inplace (la.cpp:37-46)
-    for (uint32_t i = 1; i < a.k; ++i)
-      if (mx < wv[i]) mx = wv[i];
-    float sum = 0.0f;
-    for (uint32_t i = 0; i < a.k; ++i) {
-      wv[i] = expf(wv[i] - mx);
-      sum += wv[i];
-    }
-    for (uint32_t i = 0; i < a.k; ++i) wv[i] /= sum;
-    for (uint32_t i = 0; i < a.k; ++i) {
-      a.sel[i] = sidx[i];
-      a.weights[i] = wv[i];
-      if (a.sel_trace) a.sel_trace[i] = sidx[i];
-      if (a.w_trace) a.w_trace[i] = wv[i];
-    }
+    route_finish(logits, a.E, a.k, a.sel, a.weights, a.sel_trace, a.w_trace);
   }
 }
 
