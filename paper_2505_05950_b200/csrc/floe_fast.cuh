@@ -1,7 +1,7 @@
 // floe_fast.cuh -- specialised sm_100a kernels for the Mixtral-shaped path
 // (INT2 codes, d_hidden in {2048, 4096}).  All three stream their weights with
 // 1-D bulk copies (cp.async.bulk, the TMA engine) into an NS-deep shared
-// memory ring tracked by mbarriers, so each SM keeps up to ~160 KB in flight
+// memory ring tracked by mbarriers, so each SM keeps up to ~190 KB in flight
 // without spending registers on loads, and nothing on an issue path waits on
 // a dependent global load.
 //
@@ -26,6 +26,22 @@ __host__ __device__ constexpr uint32_t k1_stage_bytes(uint32_t dh, uint32_t gpc)
   return round_up128(kK1Ch * dh / 4u) + round_up128(kK1Ch * gpc * 4u);
 }
 
+// f32 fallback for one channel's 64-element span when x holds inf/NaN (the
+// fixed-point limbs cannot represent them): the reference's own expression
+// float(code)*scale + zero, accumulated in element order.
+__device__ __noinline__ float k1_span_f32(const uint32_t *w, const uint32_t *meta, uint32_t g,
+                                          const float *xg) {
+  float acc = 0.0f;
+  for (int i = 0; i < 64; ++i) {
+    const uint32_t mz = meta[g >= 64 ? 0 : (uint32_t)i / g];
+    const float sc = __half2float(__ushort_as_half((uint16_t)(mz & 0xffffu)));
+    const float zr = __half2float(__ushort_as_half((uint16_t)(mz >> 16)));
+    const uint32_t code = (w[i / 16] >> (2 * (i % 16))) & 3u;
+    acc = fmaf(fmaf((float)code, sc, zr), xg[i], acc);
+  }
+  return acc;
+}
+
 // ---------------------------------------------------------------------------
 // K1: v[c] = sum_k deq(up[c,k]) x[k]; keep |v| >= t; compact kept channels.
 //
@@ -36,23 +52,23 @@ __host__ __device__ constexpr uint32_t k1_stage_bytes(uint32_t dh, uint32_t gpc)
 //   2-bit codes x four limb bytes per instruction), and
 //       v[c] = sum_g  s_g * (sum_k c_k X_k) / S  +  z_g * sum_k x_k ,
 //   i.e. the group-affine dequant c*s+z of dequantize_at (quant.cpp:104-109)
-//   folded out of the inner loop.  About 1.4 instructions per weight.
+//   folded out of the inner loop.  About 1.3 instructions per weight.
 //
 // Work split: CTA b owns channels [di*b/G1, di*(b+1)/G1) (balanced to one
 // channel), walked in sub-tiles of 16 channels, each ONE bulk copy of codes
 // plus one of interleaved metadata, NS sub-tiles in flight.  Thread t owns the
 // 64-element span (t % SPANS) of dh for every channel (x limbs stay in 48
-// registers) and channels q, q+CS, ... of each sub-tile (q = t / SPANS).
-//
-// Non-finite x (inf/NaN) cannot be represented in fixed point: the CTA then
-// takes an f32 per-element path with the reference's own expression.
-template <int SPANS, int NS>
+// registers) and channels q, q+CS, ... of each sub-tile (q = t / SPANS).  The
+// CS threads sharing a span split the limb preparation (one code word each)
+// and exchange it through shared memory.
+template <int SPANS, int GPT, int NS>
 __global__ void __launch_bounds__(256, 2) k1_int2(const K1Args a) {
   constexpr int TPB = 256;
   constexpr int NW = TPB / 32;
   constexpr int CH = kK1Ch;
-  constexpr int CS = TPB / SPANS;  // channel slots per CTA
+  constexpr int CS = TPB / SPANS;  // channel slots per CTA (threads per span)
   constexpr int CPT = CH / CS;     // channels per thread per sub-tile
+  constexpr int WPP = 4 / GPT;     // code words per group part
   static_assert(SPANS == 64 || SPANS == 32, "dh must be 4096 or 2048");
   constexpr uint32_t DH = SPANS * 64;
   constexpr uint32_t ROW = DH / 4;  // code bytes per channel
@@ -60,6 +76,8 @@ __global__ void __launch_bounds__(256, 2) k1_int2(const K1Args a) {
   __shared__ uint64_t full[NS];
   __shared__ float wsum[NW][CPT];
   __shared__ float red_max[NW];
+  __shared__ uint32_t limb_s[SPANS][4][12];  // [span][word][limb*4 + m]
+  __shared__ float xsum_s[SPANS][4];
 
   const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const uint32_t span = t % SPANS, q = t / SPANS;
@@ -90,25 +108,27 @@ __global__ void __launch_bounds__(256, 2) k1_int2(const K1Args a) {
   if (a.y_zero && blockIdx.x == 0 && slot == 0)
     for (uint32_t i = t; i < a.dh; i += TPB) a.y_zero[i] = 0.0f;
 
-  // ---- x: load this thread's 64-element span, block max|x| -> scale S ----
-  float xv[64];
+  // ---- x: word q of this span (16 elements) -> block max|x| -> limbs ----
+  const bool word_owner = q < 4;
+  float xw[16];
   {
-    const float4 *x4 = reinterpret_cast<const float4 *>(a.x + 64 * span);
+    const float4 *x4 = reinterpret_cast<const float4 *>(a.x + 64 * span + 16 * (q & 3));
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < 4; ++i) {
       const float4 f = x4[i];
-      xv[4 * i] = f.x;
-      xv[4 * i + 1] = f.y;
-      xv[4 * i + 2] = f.z;
-      xv[4 * i + 3] = f.w;
+      xw[4 * i] = f.x;
+      xw[4 * i + 1] = f.y;
+      xw[4 * i + 2] = f.z;
+      xw[4 * i + 3] = f.w;
     }
   }
   float m = 0.0f;
-#pragma unroll
-  for (int i = 0; i < 64; ++i) m = fmaxf(m, fabsf(xv[i]));  // NaN ignored by fmaxf
   bool finite = true;
 #pragma unroll
-  for (int i = 0; i < 64; ++i) finite = finite && isfinite(xv[i]);
+  for (int i = 0; i < 16; ++i) {
+    m = fmaxf(m, fabsf(xw[i]));
+    finite = finite && isfinite(xw[i]);
+  }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   const bool warp_finite = __all_sync(0xffffffffu, finite);
@@ -123,26 +143,18 @@ __global__ void __launch_bounds__(256, 2) k1_int2(const K1Args a) {
   }
   int ex = 0;
   frexpf(m, &ex);  // m < 2^ex
-  const float S = m > 0.0f ? ldexpf(1.0f, 22 - ex) : 1.0f;
-  const float invS = m > 0.0f ? ldexpf(1.0f, ex - 22) : 1.0f;
-
-  // limbs: lw[l][i][mm] packs limb l of elements 16i+mm+4b (b = 0..3), the
-  // byte order produced by (w >> 2mm) & 0x03030303 on code word i.
-  uint32_t lw[3][4][4];
-  constexpr int GPT_MAX = 4;  // group parts per span (g = 16)
-  float xpart[GPT_MAX];
-  const uint32_t parts = a.group_size >= 64 ? 1u : 64u / a.group_size;  // 1, 2 or 4
-  const uint32_t words_per_part = 4u / parts;
-#pragma unroll
-  for (int p = 0; p < GPT_MAX; ++p) xpart[p] = 0.0f;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  const float S = (m > 0.0f && all_finite) ? __int_as_float((127 + 22 - ex) << 23) : 1.0f;
+  const float invS = (m > 0.0f && all_finite) ? __int_as_float((127 - 22 + ex) << 23) : 1.0f;
+  if (word_owner) {
+    // limb l of elements mm + 4b (b = 0..3) in byte b: the byte order of
+    // (w >> 2mm) & 0x03030303 on this code word.
+    float s16 = 0.0f;
 #pragma unroll
     for (int mm = 0; mm < 4; ++mm) {
       uint32_t l0 = 0, l1 = 0, l2 = 0;
 #pragma unroll
       for (int b = 0; b < 4; ++b) {
-        const float xf = xv[16 * i + mm + 4 * b];
+        const float xf = xw[mm + 4 * b];
         const int X = all_finite ? __float2int_rn(xf * S) : 0;
         const int X0 = ((X + 128) & 255) - 128;
         const int R = (X - X0) >> 8;
@@ -152,13 +164,33 @@ __global__ void __launch_bounds__(256, 2) k1_int2(const K1Args a) {
         l1 |= (uint32_t)(X1 & 255) << (8 * b);
         l2 |= (uint32_t)(X2 & 255) << (8 * b);
       }
-      lw[0][i][mm] = l0;
-      lw[1][i][mm] = l1;
-      lw[2][i][mm] = l2;
+      limb_s[span][q][mm] = l0;
+      limb_s[span][q][4 + mm] = l1;
+      limb_s[span][q][8 + mm] = l2;
     }
-  }
 #pragma unroll
-  for (int i = 0; i < 64; ++i) xpart[(i / 16) / words_per_part] += xv[i];
+    for (int i = 0; i < 16; ++i) s16 += xw[i];
+    xsum_s[span][q] = s16;
+  }
+  __syncthreads();
+  uint32_t lw[4][12];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int k = 0; k < 12; k += 4) {
+      const uint4 v4 = *reinterpret_cast<const uint4 *>(&limb_s[span][i][k]);
+      lw[i][k] = v4.x;
+      lw[i][k + 1] = v4.y;
+      lw[i][k + 2] = v4.z;
+      lw[i][k + 3] = v4.w;
+    }
+  float xpart[GPT];
+#pragma unroll
+  for (int p = 0; p < GPT; ++p) {
+    xpart[p] = 0.0f;
+#pragma unroll
+    for (int i = p * WPP; i < (p + 1) * WPP; ++i) xpart[p] += xsum_s[span][i];
+  }
   const uint32_t g0 = (64u * span) / a.group_size;  // first group of this span
 
   uint32_t running = 0;
@@ -176,39 +208,30 @@ __global__ void __launch_bounds__(256, 2) k1_int2(const K1Args a) {
       if (j < nc) {
         const uint4 w4 = *reinterpret_cast<const uint4 *>(st + j * ROW + 16 * span);
         const uint32_t *meta = reinterpret_cast<const uint32_t *>(st + code_sz) + j * gpc + g0;
-        const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
         if (all_finite) {
+          const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
-          for (int p = 0; p < GPT_MAX; ++p) {
-            if ((uint32_t)p >= parts) break;
+          for (int p = 0; p < GPT; ++p) {
             int a0 = 0, a1 = 0, a2 = 0;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              if ((uint32_t)i / words_per_part != (uint32_t)p) continue;
+            for (int i = p * WPP; i < (p + 1) * WPP; ++i) {
 #pragma unroll
               for (int mm = 0; mm < 4; ++mm) {
                 const int cb = (int)((wv[i] >> (2 * mm)) & 0x03030303u);
-                a0 = __dp4a(cb, (int)lw[0][i][mm], a0);
-                a1 = __dp4a(cb, (int)lw[1][i][mm], a1);
-                a2 = __dp4a(cb, (int)lw[2][i][mm], a2);
+                a0 = __dp4a(cb, (int)lw[i][mm], a0);
+                a1 = __dp4a(cb, (int)lw[i][4 + mm], a1);
+                a2 = __dp4a(cb, (int)lw[i][8 + mm], a2);
               }
             }
             const int T = a2 * 65536 + a1 * 256 + a0;
-            const uint32_t mz = meta[p * (a.group_size >= 64 ? 0 : 1)];
+            const uint32_t mz = meta[p];
             const float sc = __half2float(__ushort_as_half((uint16_t)(mz & 0xffffu)));
             const float zr = __half2float(__ushort_as_half((uint16_t)(mz >> 16)));
             acc = fmaf(sc * invS, (float)T, fmaf(zr, xpart[p], acc));
           }
         } else {
-          // non-finite x: f32 per element, reference expression
-          const float *xg = a.x + 64 * span;
-          for (int i = 0; i < 64; ++i) {
-            const uint32_t mz = meta[(uint32_t)i / a.group_size * (a.group_size >= 64 ? 0 : 1)];
-            const float sc = __half2float(__ushort_as_half((uint16_t)(mz & 0xffffu)));
-            const float zr = __half2float(__ushort_as_half((uint16_t)(mz >> 16)));
-            const uint32_t code = (wv[i / 16] >> (2 * (i % 16))) & 3u;
-            acc = fmaf(fmaf((float)code, sc, zr), xg[i], acc);
-          }
+          const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
+          acc = k1_span_f32(wv, meta, a.group_size, a.x + 64 * span);
         }
       }
       part[r] = acc;
@@ -262,17 +285,20 @@ __global__ void __launch_bounds__(256, 2) k1_int2(const K1Args a) {
 // parallel with the segment scan; then all entries' (record address, v * w)
 // are resolved in one parallel round, so the issuing thread never waits on
 // global memory.  Each entry's 4*dh-byte record (gate row | down row, f16)
-// is ONE bulk copy into an NS-deep ring (NS*16 KB in flight per SM).
-// Thread t owns 16-byte chunks t and t+TPB of each half-record (elements
-// [8t, 8t+8) and [8(t+TPB), ...)): conflict-free 128-bit smem reads.
-constexpr uint32_t kK2Chunk = 512;  // entries resolved per preload round
+// is ONE bulk copy into an NS-deep ring (NS*16 KB in flight per SM), and R
+// records are consumed per block barrier (R independent dot chains, one
+// transposed warp reduction).  Thread t owns 16-byte chunks t and t+TPB of
+// each half-record (elements [8t, 8t+8) and [8(t+TPB), ...)): conflict-free
+// 128-bit smem reads, y kept in registers.
+constexpr uint32_t kK2Chunk = 512;  // entries resolved per preload round (multiple of R)
 
-template <int TPB, int NS>
+template <int TPB, int NS, int R>
 __global__ void __launch_bounds__(TPB, 1) k2_gate_down(const K2Args a) {
   constexpr int NW = TPB / 32;
+  static_assert(NS % R == 0 && (R == 1 || R == 2 || R == 4), "ring holds whole batches");
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t full[NS];
-  __shared__ float red[2][NW];
+  __shared__ float red[2][NW][R];
   __shared__ const __half *ent_rec[kK2Chunk];
   __shared__ float ent_scale[kK2Chunk];
   __shared__ const __half *slot_rec[kMaxSlots];
@@ -315,7 +341,8 @@ __global__ void __launch_bounds__(TPB, 1) k2_gate_down(const K2Args a) {
     for (int i = 0; i < 8; ++i) y2[i] = make_float2(0.0f, 0.0f);
   }
 
-  uint32_t it = 0;  // global iteration count (ring position / parity)
+  uint32_t it = 0;  // entries consumed so far (ring position)
+  uint32_t batch = 0;
   for (uint32_t cb = begin; cb < end; cb += kK2Chunk) {
     const uint32_t n = min(kK2Chunk, end - cb);
     __syncthreads();  // previous chunk's ent_* consumed; slot_* visible
@@ -330,49 +357,85 @@ __global__ void __launch_bounds__(TPB, 1) k2_gate_down(const K2Args a) {
       if (a.kept_out) a.kept_out[(size_t)slot * a.di + (p - prefix[slot * a.g1])] = c;
     }
     __syncthreads();
+    // `it` counts stage uses in order across chunks (every chunk but the
+    // last holds a whole number of batches), so stage = use % NS and the
+    // mbarrier parity = (use / NS) & 1 stay consistent.
     if (t == 0)
-      for (uint32_t qq = 0; qq < n && qq < (uint32_t)NS; ++qq) {
-        const uint32_t s = (it + qq) % NS;
+      for (uint32_t k = 0; k < n && k < (uint32_t)NS; ++k) {
+        const uint32_t s = (it + k) % NS;
         floe_ptx::mbar_arrive_expect_tx(&full[s], rec_bytes);
-        floe_ptx::bulk_g2s(smem + s * rec_bytes, ent_rec[qq], rec_bytes, &full[s]);
+        floe_ptx::bulk_g2s(smem + s * rec_bytes, ent_rec[k], rec_bytes, &full[s]);
       }
-    for (uint32_t qq = 0; qq < n; ++qq, ++it) {
-      const uint32_t s = it % NS;
-      floe_ptx::mbar_wait(&full[s], (it / NS) & 1u);
-      const uint4 *rec = reinterpret_cast<const uint4 *>(smem + s * rec_bytes);
-      const uint4 g0 = rec[t], g1 = rec[t + TPB];
-      const uint4 d0 = rec[2 * TPB + t], d1 = rec[3 * TPB + t];
-      float2 acc = make_float2(0.0f, 0.0f);
-      {
-        const __half2 *h0 = reinterpret_cast<const __half2 *>(&g0);
-        const __half2 *h1 = reinterpret_cast<const __half2 *>(&g1);
+    for (uint32_t q0 = 0; q0 < n; q0 += R, ++batch) {
+      uint4 gv[R][2], dv[R][2];
+      float gp[R];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          acc = __ffma2_rn(__half22float2(h0[j]), x2[j], acc);
-          acc = __ffma2_rn(__half22float2(h1[j]), x2[4 + j], acc);
+      for (int r = 0; r < R; ++r) {
+        const uint32_t qq = q0 + r;
+        gp[r] = 0.0f;
+        if (qq < n) {
+          const uint32_t s = (it + r) % NS;
+          floe_ptx::mbar_wait(&full[s], ((it + r) / NS) & 1u);
+          const uint4 *rec = reinterpret_cast<const uint4 *>(smem + s * rec_bytes);
+          gv[r][0] = rec[t];
+          gv[r][1] = rec[t + TPB];
+          dv[r][0] = rec[2 * TPB + t];
+          dv[r][1] = rec[3 * TPB + t];
+          const __half2 *h0 = reinterpret_cast<const __half2 *>(&gv[r][0]);
+          const __half2 *h1 = reinterpret_cast<const __half2 *>(&gv[r][1]);
+          float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            acc = __ffma2_rn(__half22float2(h0[j]), x2[j], acc);
+            acc = __ffma2_rn(__half22float2(h1[j]), x2[4 + j], acc);
+          }
+          gp[r] = acc.x + acc.y;
+        } else {
+          dv[r][0] = dv[r][1] = make_uint4(0, 0, 0, 0);
         }
       }
-      float gp = acc.x + acc.y;
+      // transposed warp reduction of R values
 #pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) gp += __shfl_xor_sync(0xffffffffu, gp, o);
-      if (lane == 0) red[it & 1][warp] = gp;
-      __syncthreads();  // red complete; stage s fully read
-      if (t == 0 && qq + NS < n) {
-        floe_ptx::mbar_arrive_expect_tx(&full[s], rec_bytes);
-        floe_ptx::bulk_g2s(smem + s * rec_bytes, ent_rec[qq + NS], rec_bytes, &full[s]);
+      for (int sft = 16, cnt = R / 2; cnt >= 1; sft >>= 1, cnt >>= 1) {
+        const bool upper = (lane & sft) != 0;
+#pragma unroll
+        for (int r = 0; r < cnt; ++r) {
+          const float send = upper ? gp[r] : gp[r + cnt];
+          const float keep = upper ? gp[r + cnt] : gp[r];
+          gp[r] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+        }
       }
-      float g = 0.0f;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) g += red[it & 1][w];
-      const float aco = silu_ref(g) * ent_scale[qq];
-      const float2 a2 = make_float2(aco, aco);
-      const __half2 *e0 = reinterpret_cast<const __half2 *>(&d0);
-      const __half2 *e1 = reinterpret_cast<const __half2 *>(&d1);
+      for (int sft = 32 / R / 2; sft >= 1; sft >>= 1)
+        gp[0] += __shfl_xor_sync(0xffffffffu, gp[0], sft);
+      if ((lane & (32 / R - 1)) == 0) red[batch & 1][warp][lane / (32 / R)] = gp[0];
+      __syncthreads();  // red complete; the batch's stages fully read
+      if (t == 0)
+        for (int r = 0; r < R; ++r) {
+          const uint32_t nq = q0 + r + NS;
+          if (nq < n) {
+            const uint32_t s = (it + r) % NS;
+            floe_ptx::mbar_arrive_expect_tx(&full[s], rec_bytes);
+            floe_ptx::bulk_g2s(smem + s * rec_bytes, ent_rec[nq], rec_bytes, &full[s]);
+          }
+        }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        y2[j] = __ffma2_rn(a2, __half22float2(e0[j]), y2[j]);
-        y2[4 + j] = __ffma2_rn(a2, __half22float2(e1[j]), y2[4 + j]);
+      for (int r = 0; r < R; ++r) {
+        if (q0 + r >= n) break;
+        float g = 0.0f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) g += red[batch & 1][w][r];
+        const float aco = silu_ref(g) * ent_scale[q0 + r];
+        const float2 a2 = make_float2(aco, aco);
+        const __half2 *e0 = reinterpret_cast<const __half2 *>(&dv[r][0]);
+        const __half2 *e1 = reinterpret_cast<const __half2 *>(&dv[r][1]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          y2[j] = __ffma2_rn(a2, __half22float2(e0[j]), y2[j]);
+          y2[4 + j] = __ffma2_rn(a2, __half22float2(e1[j]), y2[4 + j]);
+        }
       }
+      it += R;
     }
   }
   if (end > begin) {
@@ -387,30 +450,32 @@ __global__ void __launch_bounds__(TPB, 1) k2_gate_down(const K2Args a) {
 // ---------------------------------------------------------------------------
 // Block head: u = h + mixing.h; y = u; logits = router.u; top-k; softmax.
 //
-// One CTA per SM; CTA b owns rows [dh*b/G, dh*(b+1)/G), streamed in chunks of
-// RPC rows (32 KB) by bulk copy through an NS-deep ring, h bulk-copied once.
-// WPR = 8/RPC warps share a row (K-split, combined in smem).  Each CTA also
-// folds its rows into partial router logits; the last CTA (done counter,
-// reset in-kernel) sums the partials in a fixed order and routes.
+// One CTA per SM; CTA b owns rows [dh*b/G, dh*(b+1)/G), streamed in chunks
+// of RPC <= 8 rows (one row per warp) by bulk copy through an NS-deep ring;
+// h is bulk-copied once.  Each warp finishes its own row (u, y, and the
+// row's contribution to the router logits) -- one block barrier per chunk,
+// only to release the stage.  The last CTA (done counter, reset in-kernel)
+// sums the per-CTA partial logits in a fixed order and routes.
 // Deterministic: no float atomics.
 constexpr uint32_t kMaxRowsPerCta = 48;
+constexpr uint32_t kMixChunkBytes = 96 * 1024;  // bytes of rows per stage (cap)
+
+__host__ __device__ inline uint32_t mix_rows_per_chunk(uint32_t row_bytes) {
+  uint32_t r = kMixChunkBytes / row_bytes;
+  return r > 8 ? 8 : (r < 1 ? 1 : r);
+}
 
 template <typename T, int NS>
 __global__ void __launch_bounds__(256, 1) mixing_route_bulk(const MixArgs a) {
-  constexpr uint32_t CHUNK = 32768;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t full[NS + 1];  // [NS] = h
-  __shared__ float rsum[8];
-  __shared__ float usum[8];
-  __shared__ float pl[32];
+  __shared__ float plw[8][32];       // per-warp partial logits
   __shared__ float logits[32];
   __shared__ float rs[32 * kMaxRowsPerCta];  // router[e][this CTA's rows]
   __shared__ bool last;
   const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const uint32_t row_bytes = a.dh * (uint32_t)sizeof(T);
-  uint32_t rpc = CHUNK / row_bytes;  // rows per chunk (power of two, <= 8)
-  rpc = rpc >= 8 ? 8 : rpc >= 4 ? 4 : rpc >= 2 ? 2 : 1;
-  const uint32_t wpr = 8 / rpc;  // warps per row
+  const uint32_t rpc = mix_rows_per_chunk(row_bytes);
   const uint32_t r_lo = seg_begin(a.dh, blockIdx.x, gridDim.x);
   const uint32_t r_hi = seg_begin(a.dh, blockIdx.x + 1, gridDim.x);
   const uint32_t n_chunks = (r_hi - r_lo + rpc - 1) / rpc;
@@ -430,7 +495,6 @@ __global__ void __launch_bounds__(256, 1) mixing_route_bulk(const MixArgs a) {
       floe_ptx::bulk_g2s(smem + i * stage_sz, m + (size_t)r0 * a.dh, nr * row_bytes, &full[i]);
     }
   }
-  if (t < 32) pl[t] = 0.0f;
   // router slice for this CTA's rows, fetched while the bulk copies fly
   for (uint32_t i = t; i < a.E * kMaxRowsPerCta; i += 256) {
     const uint32_t e = i / kMaxRowsPerCta, lr = i % kMaxRowsPerCta;
@@ -439,17 +503,16 @@ __global__ void __launch_bounds__(256, 1) mixing_route_bulk(const MixArgs a) {
   __syncthreads();
   floe_ptx::mbar_wait(&full[NS], 0);
 
-  const uint32_t my_row = warp / wpr, my_part = warp % wpr;
-  const uint32_t k_lo = a.dh * my_part / wpr, k_hi = a.dh * (my_part + 1) / wpr;
   constexpr uint32_t EPL = 16 / sizeof(T);  // elements per 128-bit smem load
+  float pl = 0.0f;                          // lane e < E: this warp's partial logit e
   for (uint32_t ci = 0; ci < n_chunks; ++ci) {
     const uint32_t s = ci % NS;
-    floe_ptx::mbar_wait(&full[s], (ci / NS) & 1u);
     const uint32_t r0 = r_lo + ci * rpc, nr = min(rpc, r_hi - r0);
-    float acc = 0.0f;
-    if (my_row < nr) {
-      const T *rowp = reinterpret_cast<const T *>(smem + s * stage_sz) + (size_t)my_row * a.dh;
-      for (uint32_t k = k_lo + lane * EPL; k < k_hi; k += 32 * EPL) {
+    if (warp < nr) {
+      floe_ptx::mbar_wait(&full[s], (ci / NS) & 1u);
+      const T *rowp = reinterpret_cast<const T *>(smem + s * stage_sz) + (size_t)warp * a.dh;
+      float acc0 = 0.0f, acc1 = 0.0f;
+      for (uint32_t k = lane * EPL; k < a.dh; k += 32 * EPL) {
         const uint4 qv = *reinterpret_cast<const uint4 *>(rowp + k);
         const float4 h0 = *reinterpret_cast<const float4 *>(hs + k);
         if constexpr (sizeof(T) == 2) {
@@ -457,55 +520,53 @@ __global__ void __launch_bounds__(256, 1) mixing_route_bulk(const MixArgs a) {
           const __half2 *hh = reinterpret_cast<const __half2 *>(&qv);
           const float2 f0 = __half22float2(hh[0]), f1 = __half22float2(hh[1]);
           const float2 f2 = __half22float2(hh[2]), f3 = __half22float2(hh[3]);
-          acc = fmaf(f0.x, h0.x, acc);
-          acc = fmaf(f0.y, h0.y, acc);
-          acc = fmaf(f1.x, h0.z, acc);
-          acc = fmaf(f1.y, h0.w, acc);
-          acc = fmaf(f2.x, h1.x, acc);
-          acc = fmaf(f2.y, h1.y, acc);
-          acc = fmaf(f3.x, h1.z, acc);
-          acc = fmaf(f3.y, h1.w, acc);
+          acc0 = fmaf(f0.x, h0.x, acc0);
+          acc1 = fmaf(f0.y, h0.y, acc1);
+          acc0 = fmaf(f1.x, h0.z, acc0);
+          acc1 = fmaf(f1.y, h0.w, acc1);
+          acc0 = fmaf(f2.x, h1.x, acc0);
+          acc1 = fmaf(f2.y, h1.y, acc1);
+          acc0 = fmaf(f3.x, h1.z, acc0);
+          acc1 = fmaf(f3.y, h1.w, acc1);
         } else {
-          acc = fmaf(__uint_as_float(qv.x), h0.x, acc);
-          acc = fmaf(__uint_as_float(qv.y), h0.y, acc);
-          acc = fmaf(__uint_as_float(qv.z), h0.z, acc);
-          acc = fmaf(__uint_as_float(qv.w), h0.w, acc);
+          acc0 = fmaf(__uint_as_float(qv.x), h0.x, acc0);
+          acc1 = fmaf(__uint_as_float(qv.y), h0.y, acc1);
+          acc0 = fmaf(__uint_as_float(qv.z), h0.z, acc0);
+          acc1 = fmaf(__uint_as_float(qv.w), h0.w, acc1);
         }
       }
-    }
+      float acc = acc0 + acc1;
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) rsum[warp] = acc;
-    __syncthreads();  // rsum complete; stage s consumed
+      for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      const uint32_t row = r0 + warp;
+      const float uu = hs[row] + 1.0f * acc;  // drift_scale = 1 (model.cpp:151-152)
+      if (lane == 0) {
+        a.u[row] = uu;
+        a.y_init[row] = uu;
+        if (a.u_trace) a.u_trace[row] = uu;
+      }
+      if (lane < a.E) {
+        const uint32_t lr = row - r_lo;
+        const float w = lr < kMaxRowsPerCta ? rs[lane * kMaxRowsPerCta + lr]
+                                            : a.router[(size_t)lane * a.dh + row];
+        pl = fmaf(w, uu, pl);
+      }
+    }
+    __syncthreads();  // stage s consumed by every warp
     if (t == 0 && ci + NS < n_chunks) {
       const uint32_t r1 = r_lo + (ci + NS) * rpc, n1 = min(rpc, r_hi - r1);
       floe_ptx::mbar_arrive_expect_tx(&full[s], n1 * row_bytes);
       floe_ptx::bulk_g2s(smem + s * stage_sz, m + (size_t)r1 * a.dh, n1 * row_bytes, &full[s]);
     }
-    if (warp == 0 && lane < nr) {
-      float dot = 0.0f;
-      for (uint32_t p = 0; p < wpr; ++p) dot += rsum[lane * wpr + p];
-      const uint32_t row = r0 + lane;
-      const float uu = hs[row] + 1.0f * dot;  // drift_scale = 1 (model.cpp:151-152)
-      a.u[row] = uu;
-      a.y_init[row] = uu;
-      if (a.u_trace) a.u_trace[row] = uu;
-      usum[lane] = uu;
-    }
-    __syncwarp();
-    if (warp == 0 && lane < a.E) {  // router partial logits for these rows
-      float sacc = pl[lane];
-      for (uint32_t r = 0; r < nr; ++r) {
-        const uint32_t lr = r0 + r - r_lo;
-        const float w = lr < kMaxRowsPerCta ? rs[lane * kMaxRowsPerCta + lr]
-                                            : a.router[(size_t)lane * a.dh + r0 + r];
-        sacc += w * usum[r];
-      }
-      pl[lane] = sacc;
-    }
-    __syncthreads();
   }
-  if (t < a.E) a.partial[blockIdx.x * a.E + t] = pl[t];
+  plw[warp][lane] = pl;
+  __syncthreads();
+  if (t < a.E) {
+    float sacc = 0.0f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) sacc += plw[w][t];
+    a.partial[blockIdx.x * a.E + t] = sacc;
+  }
   __threadfence();
   __syncthreads();
   if (t == 0) last = atomicAdd(a.done, 1u) == gridDim.x - 1;

@@ -258,13 +258,22 @@ int launch_k1(const K1Launch &L, floe_gpu_workspace *ws, cudaStream_t st) {
     constexpr int NS = 4;
     const uint32_t gpc = L.dh / L.g;
     const uint32_t smem = NS * floe_k::k1_stage_bytes(L.dh, gpc);
+    const uint32_t gpt = L.g >= 64 ? 1u : 64u / L.g;  // group parts per 64-element span
+#define FLOE_K1(SP, GP)                                                 \
+  do {                                                                  \
+    if (int rc = set_smem(floe_k::k1_int2<SP, GP, NS>, smem)) return rc; \
+    floe_k::k1_int2<SP, GP, NS><<<grid, 256, smem, st>>>(a);            \
+  } while (0)
     if (L.dh == 4096) {
-      if (int rc = set_smem(floe_k::k1_int2<64, NS>, smem)) return rc;
-      floe_k::k1_int2<64, NS><<<grid, 256, smem, st>>>(a);
+      if (gpt == 1) FLOE_K1(64, 1);
+      else if (gpt == 2) FLOE_K1(64, 2);
+      else FLOE_K1(64, 4);
     } else {
-      if (int rc = set_smem(floe_k::k1_int2<32, NS>, smem)) return rc;
-      floe_k::k1_int2<32, NS><<<grid, 256, smem, st>>>(a);
+      if (gpt == 1) FLOE_K1(32, 1);
+      else if (gpt == 2) FLOE_K1(32, 2);
+      else FLOE_K1(32, 4);
     }
+#undef FLOE_K1
   } else {
     floe_k::k1_generic<<<grid, 256, 0, st>>>(a);
   }
@@ -312,15 +321,18 @@ int launch_k2(const K2Launch &L, floe_gpu_workspace *ws, cudaStream_t st) {
   StageScope prof(ws, kStageK2, st);
   if (L.fast && (tpb == 256 || tpb == 128)) {
     // one CTA per SM, 160 KB of records in flight per SM
-    constexpr int NS = 10;
-    const uint32_t smem = NS * 4u * L.dh + prefix_bytes;
+    // one CTA per SM, 192 KB of records in flight per SM, 4 records per barrier
+    constexpr int R = 4;
     if (tpb == 256) {
-      if (int rc = set_smem(floe_k::k2_gate_down<256, NS>, smem)) return rc;
-      floe_k::k2_gate_down<256, NS><<<sm, 256, smem, st>>>(a);
+      constexpr int NS = 12;
+      const uint32_t smem = NS * 4u * L.dh + prefix_bytes;
+      if (int rc = set_smem(floe_k::k2_gate_down<256, NS, R>, smem)) return rc;
+      floe_k::k2_gate_down<256, NS, R><<<sm, 256, smem, st>>>(a);
     } else {
-      if (int rc = set_smem(floe_k::k2_gate_down<128, 2 * NS>, smem + NS * 4u * L.dh))
-        return rc;
-      floe_k::k2_gate_down<128, 2 * NS><<<sm, 128, smem + NS * 4u * L.dh, st>>>(a);
+      constexpr int NS = 24;
+      const uint32_t smem = NS * 4u * L.dh + prefix_bytes;
+      if (int rc = set_smem(floe_k::k2_gate_down<128, NS, R>, smem)) return rc;
+      floe_k::k2_gate_down<128, NS, R><<<sm, 128, smem, st>>>(a);
     }
   } else {
     if (int rc = set_smem(floe_k::k2_generic, prefix_bytes)) return rc;
@@ -804,10 +816,9 @@ int floe_gpu_layer_forward(const floe_gpu_layer *l, floe_gpu_workspace *ws, cons
     const bool bulk = l->dh % 8 == 0 &&
                       (l->dh + bulk_grid - 1) / bulk_grid <= floe_k::kMaxRowsPerCta;
     if (bulk) {
-      constexpr int NS = 4;
+      constexpr int NS = 2;
       const uint32_t row_bytes = l->dh * (l->mix_f16 ? 2u : 4u);
-      uint32_t rpc = 32768u / row_bytes;
-      rpc = rpc >= 8 ? 8 : rpc >= 4 ? 4 : rpc >= 2 ? 2 : 1;
+      const uint32_t rpc = floe_k::mix_rows_per_chunk(row_bytes);
       const uint32_t bsmem = NS * floe_k::round_up128(rpc * row_bytes) + 4u * l->dh;
       if (l->mix_f16) {
         if (int rc = set_smem(floe_k::mixing_route_bulk<__half, NS>, bsmem)) return rc;

@@ -36,7 +36,7 @@ def main():
             if mode == "dirty":
                 buf.add_(1.0)
             elif mode == "clean":
-                torch.sum(buf, out=sink[0])
+                sink.copy_(buf.sum())
             evs[i][0].record(stream)
             fn(i)
             evs[i][1].record(stream)
