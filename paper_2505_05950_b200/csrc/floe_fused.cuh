@@ -1,0 +1,606 @@
+// floe_fused.cuh -- ONE persistent sm_100a kernel per decode step.
+//
+// A kernel launch on B200 carries several microseconds of fixed ramp cost
+// (profiles/r01_membench_cold_footprint.txt: an empty 148-CTA grid takes
+// ~3.5 us cold; a 34 MB stream ~10 us), comparable to the whole roofline time
+// of an expert-token (~10 us).  So the hot path runs as a single cooperative
+// grid, one CTA per SM, that walks the reference's block_forward in phases
+// separated by grid barriers (model.cpp:145-169):
+//
+//   A  (layer mode)  u = h + mixing.h; y = u; per-CTA partial router logits
+//      --- grid barrier ---
+//      every CTA sums the partials in the same fixed order and routes
+//      (route, model.cpp:83-93): identical top-k/softmax in all CTAs
+//   B  K1: v = qgemv_channels(up_e, u) for each selected expert over this
+//      CTA's channel range, |v| >= t, kept channels appended to the CTA's
+//      segment (quant.cpp:122-136, model.cpp:135)
+//      --- grid barrier ---
+//   C  K2: kept entries of all experts split evenly over CTAs; per entry
+//      silu(gate_c . u) * v_c * w_e * down_c accumulated in registers and
+//      reduced into y once (model.cpp:136-140, 162-166)
+//
+// All weight traffic is 1-D bulk copies (cp.async.bulk) through ONE shared
+// memory ring of NS stages that persists across phases; thread 0 refills a
+// stage after the block barrier that retires it.  The mbarrier parity of a
+// stage use is (use / NS) & 1 with `use` counted across all phases.
+#pragma once
+
+#include "floe_fast.cuh"
+
+namespace floe_k {
+
+struct FusedArgs {
+  // phase A (layer mode only)
+  const void *mixing;  // [dh][dh] f16 or f32
+  const float *h;      // [dh]
+  const float *router; // [E][dh]
+  uint32_t n_experts, top_k;
+  int has_mixing;
+  float *partial;  // [grid][32]
+  float *u_trace;
+  uint32_t *sel_trace;
+  float *w_trace;
+  uint32_t *sel_out;  // [slots] routing result for later consumers
+  float *w_out;
+  // shared
+  float *u;  // [dh] expert input (written in phase A in layer mode)
+  float *y;  // [dh] output
+  uint32_t dh, di, group_size, slots;
+  const ExpertDesc *table;
+  int use_threshold;
+  float threshold;
+  float *v_out;       // nullable [slots][di]
+  uint8_t *mask_out;  // nullable [slots][di]
+  uint32_t *kept_idx; // [slots][di]
+  float *kept_v;      // [slots][di]
+  uint32_t *seg_count;  // [slots][grid]
+  unsigned long long *bar;  // grid barrier counter (monotonic, never reset)
+  uint32_t *n_kept_out;
+  uint32_t *kept_out;
+  unsigned long long *stats;
+  uint32_t stage_bytes, ns;  // ring geometry
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Grid-wide barrier on a monotonic 64-bit counter (co-resident grid).
+__device__ __forceinline__ void grid_sync(unsigned long long *bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long g = gridDim.x;
+    const unsigned long long old = atomicAdd(bar, 1ull);
+    const unsigned long long target = (old / g + 1) * g;
+    while (ld_acquire_u64(bar) < target) __nanosleep(20);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// Ring of NS bulk-copy stages in dynamic shared memory.
+struct Ring {
+  uint8_t *base;
+  uint64_t *full;
+  uint32_t stage_bytes, ns;
+  uint32_t use;  // next stage use to be consumed (uniform across the CTA)
+  __device__ uint8_t *stage(uint32_t u) const { return base + (u % ns) * stage_bytes; }
+  __device__ uint64_t *bar(uint32_t u) const { return &full[u % ns]; }
+  __device__ void wait(uint32_t u) const { floe_ptx::mbar_wait(bar(u), (u / ns) & 1u); }
+};
+
+constexpr uint32_t kFusedMaxStages = 24;
+constexpr uint32_t kFusedRingBytes = 168 * 1024;
+
+// ---------------------------------------------------------------------------
+template <typename T, int SPANS, int GPT>
+__global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
+  constexpr int TPB = 256;
+  constexpr int NW = TPB / 32;
+  constexpr int CH = kK1Ch;
+  constexpr int CS = TPB / SPANS;
+  constexpr int CPT = CH / CS;
+  constexpr int WPP = 4 / GPT;
+  constexpr uint32_t DH = SPANS * 64;
+  constexpr uint32_t ROW = DH / 4;
+  constexpr int R = 4;  // K2 records per block barrier
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t full[kFusedMaxStages];
+  __shared__ uint64_t hbar;
+  __shared__ float part_s[NW][32];
+  __shared__ float u_s[kMaxRowsPerCta];
+  __shared__ float rs[32 * kMaxRowsPerCta];
+  __shared__ float logits[32];
+  __shared__ uint32_t sel_s[kMaxSlots];
+  __shared__ float w_s[kMaxSlots];
+  __shared__ const __half *rec_s[kMaxSlots];
+  __shared__ float thr_s[kMaxSlots];
+  __shared__ float red_max[NW];
+  __shared__ uint32_t limb_s[SPANS][4][12];
+  __shared__ float xsum_s[SPANS][4];
+  __shared__ float wsum[2][NW][CPT];
+  __shared__ float red[2][NW][R];
+  __shared__ const __half *ent_rec[kK2Chunk];
+  __shared__ float ent_scale[kK2Chunk];
+
+  const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint32_t G = gridDim.x, b = blockIdx.x;
+  Ring ring{smem, full, a.stage_bytes, a.ns, 0};
+  float *hs = reinterpret_cast<float *>(smem + a.ns * a.stage_bytes);  // [dh] (layer mode)
+
+  if (t == 0) {
+    for (uint32_t s = 0; s < a.ns; ++s) floe_ptx::mbar_init(&full[s], 1);
+    floe_ptx::mbar_init(&hbar, 1);
+    floe_ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  uint32_t issued = 0;  // stage uses issued so far (thread 0's view)
+
+  // =========================== phase A: mixing ===========================
+  if (a.has_mixing) {
+    const uint32_t row_bytes = DH * (uint32_t)sizeof(T);
+    const uint32_t rps = a.stage_bytes / row_bytes;  // rows per stage (1 or 2)
+    const uint32_t r_lo = seg_begin(DH, b, G), r_hi = seg_begin(DH, b + 1, G);
+    const uint32_t n_items = (r_hi - r_lo + rps - 1) / rps;
+    const T *m = static_cast<const T *>(a.mixing);
+    auto issue_rows = [&](uint32_t i) {  // item i -> use `issued`
+      const uint32_t r0 = r_lo + i * rps, nr = min(rps, r_hi - r0);
+      floe_ptx::mbar_arrive_expect_tx(ring.bar(issued), nr * row_bytes);
+      floe_ptx::bulk_g2s(ring.stage(issued), m + (size_t)r0 * DH, nr * row_bytes, ring.bar(issued));
+      ++issued;
+    };
+    if (t == 0) {
+      floe_ptx::mbar_arrive_expect_tx(&hbar, 4u * DH);
+      floe_ptx::bulk_g2s(hs, a.h, 4u * DH, &hbar);
+      for (uint32_t i = 0; i < n_items && i < a.ns; ++i) issue_rows(i);
+    }
+    for (uint32_t i = t; i < a.n_experts * kMaxRowsPerCta; i += TPB) {
+      const uint32_t e = i / kMaxRowsPerCta, lr = i % kMaxRowsPerCta;
+      if (r_lo + lr < r_hi) rs[i] = a.router[(size_t)e * DH + r_lo + lr];
+    }
+    floe_ptx::mbar_wait(&hbar, 0);
+    const uint32_t per_round = NW / rps;  // stages consumed per block barrier
+    constexpr uint32_t EPL = 16 / sizeof(T);
+    const uint32_t first_use = ring.use;
+    for (uint32_t i0 = 0; i0 < n_items; i0 += per_round) {
+      const uint32_t item = i0 + warp / rps, sub = warp % rps;
+      const uint32_t row = r_lo + item * rps + sub;
+      if (item < n_items && row < r_hi) {
+        const uint32_t u_idx = first_use + item;
+        ring.wait(u_idx);
+        const T *rowp = reinterpret_cast<const T *>(ring.stage(u_idx)) + (size_t)sub * DH;
+        float acc0 = 0.0f, acc1 = 0.0f;
+#pragma unroll 4
+        for (uint32_t k = lane * EPL; k < DH; k += 32 * EPL) {
+          const uint4 qv = *reinterpret_cast<const uint4 *>(rowp + k);
+          const float4 h0 = *reinterpret_cast<const float4 *>(hs + k);
+          if constexpr (sizeof(T) == 2) {
+            const float4 h1 = *reinterpret_cast<const float4 *>(hs + k + 4);
+            const __half2 *hh = reinterpret_cast<const __half2 *>(&qv);
+            const float2 f0 = __half22float2(hh[0]), f1 = __half22float2(hh[1]);
+            const float2 f2 = __half22float2(hh[2]), f3 = __half22float2(hh[3]);
+            acc0 = fmaf(f0.x, h0.x, acc0);
+            acc1 = fmaf(f0.y, h0.y, acc1);
+            acc0 = fmaf(f1.x, h0.z, acc0);
+            acc1 = fmaf(f1.y, h0.w, acc1);
+            acc0 = fmaf(f2.x, h1.x, acc0);
+            acc1 = fmaf(f2.y, h1.y, acc1);
+            acc0 = fmaf(f3.x, h1.z, acc0);
+            acc1 = fmaf(f3.y, h1.w, acc1);
+          } else {
+            acc0 = fmaf(__uint_as_float(qv.x), h0.x, acc0);
+            acc1 = fmaf(__uint_as_float(qv.y), h0.y, acc1);
+            acc0 = fmaf(__uint_as_float(qv.z), h0.z, acc0);
+            acc1 = fmaf(__uint_as_float(qv.w), h0.w, acc1);
+          }
+        }
+        float acc = acc0 + acc1;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        const float uu = hs[row] + 1.0f * acc;  // drift_scale = 1 (model.cpp:151-152)
+        if (lane == 0) {
+          a.u[row] = uu;
+          a.y[row] = uu;
+          if (a.u_trace) a.u_trace[row] = uu;
+          if (row - r_lo < kMaxRowsPerCta) u_s[row - r_lo] = uu;
+        }
+      }
+      __syncthreads();  // the round's stages are consumed
+      if (t == 0)
+        for (uint32_t k = 0; k < per_round; ++k) {
+          const uint32_t nxt = i0 + k + a.ns;
+          if (i0 + k < n_items && nxt < n_items) issue_rows(nxt);
+        }
+    }
+    ring.use = first_use + n_items;
+    // this CTA's share of router.u (fixed order: ascending rows)
+    if (warp == 0 && lane < a.n_experts) {
+      float s = 0.0f;
+      for (uint32_t r = r_lo; r < r_hi; ++r) {
+        const uint32_t lr = r - r_lo;
+        const float w = lr < kMaxRowsPerCta ? rs[lane * kMaxRowsPerCta + lr]
+                                            : a.router[(size_t)lane * DH + r];
+        const float uu = lr < kMaxRowsPerCta ? u_s[lr] : a.u[r];
+        s = fmaf(w, uu, s);
+      }
+      a.partial[b * 32 + lane] = s;
+    }
+    grid_sync(a.bar);
+    // route (model.cpp:83-93): every CTA sums the partials in the same order
+    for (uint32_t e = warp; e < a.n_experts; e += NW) {
+      float s = 0.0f;
+      for (uint32_t bb = lane; bb < G; bb += 32) s += __ldcg(&a.partial[bb * 32 + e]);
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) logits[e] = s;
+    }
+    __syncthreads();
+    if (t == 0) {
+      uint32_t sel[32];
+      float wv[32];
+      route_finish(logits, a.n_experts, a.top_k, sel, wv,
+                   b == 0 ? a.sel_trace : nullptr, b == 0 ? a.w_trace : nullptr);
+      for (uint32_t s = 0; s < a.slots; ++s) {
+        sel_s[s] = sel[s];
+        w_s[s] = wv[s];
+        if (b == 0 && a.sel_out) {
+          a.sel_out[s] = sel[s];
+          a.w_out[s] = wv[s];
+        }
+      }
+    }
+  } else {
+    if (t < a.slots) {
+      sel_s[t] = t;
+      w_s[t] = 1.0f;
+    }
+    if (b == 0)
+      for (uint32_t i = t; i < DH; i += TPB) a.y[i] = 0.0f;  // before barrier 2
+  }
+  __syncthreads();
+  if (t < a.slots) {
+    const ExpertDesc &d = a.table[sel_s[t]];
+    rec_s[t] = d.records;
+    thr_s[t] = a.use_threshold ? a.threshold : d.threshold;
+  }
+
+  // =========================== phase B: K1 ================================
+  {
+    const uint32_t span = t % SPANS, q = t / SPANS;
+    const uint32_t c_lo = seg_begin(a.di, b, G), c_hi = seg_begin(a.di, b + 1, G);
+    const uint32_t n_sub = (c_hi - c_lo + CH - 1) / CH;
+    const uint32_t n_items = n_sub * a.slots;
+    const uint32_t gpc = DH / a.group_size;
+    const uint32_t code_sz = round_up128(CH * ROW);
+    __syncthreads();  // sel_s / rec_s visible
+    auto issue_tile = [&](uint32_t i) {  // item i = (slot, sub-tile)
+      const uint32_t s = i / n_sub, k = i % n_sub;
+      const uint32_t c0 = c_lo + k * CH, nc = min((uint32_t)CH, c_hi - c0);
+      const ExpertDesc &d = a.table[sel_s[s]];
+      floe_ptx::mbar_arrive_expect_tx(ring.bar(issued), nc * (ROW + gpc * 4u));
+      floe_ptx::bulk_g2s(ring.stage(issued), d.codes + (size_t)c0 * ROW, nc * ROW, ring.bar(issued));
+      floe_ptx::bulk_g2s(ring.stage(issued) + code_sz, d.meta + (size_t)c0 * gpc, nc * gpc * 4u,
+                         ring.bar(issued));
+      ++issued;
+    };
+    const uint32_t first_use = ring.use;
+    if (t == 0)
+      for (uint32_t i = 0; i < n_items && i < a.ns; ++i) issue_tile(i);
+
+    // x limbs (word q of this span), shared by the CS threads of the span
+    const float *xg = a.u;
+    float xw[16];
+    {
+      const float4 *x4 = reinterpret_cast<const float4 *>(xg + 64 * span + 16 * (q & 3));
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float4 f = __ldcg(x4 + i);
+        xw[4 * i] = f.x;
+        xw[4 * i + 1] = f.y;
+        xw[4 * i + 2] = f.z;
+        xw[4 * i + 3] = f.w;
+      }
+    }
+    float mx = 0.0f;
+    bool finite = true;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      mx = fmaxf(mx, fabsf(xw[i]));
+      finite = finite && isfinite(xw[i]);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const bool warp_finite = __all_sync(0xffffffffu, finite);
+    if (lane == 0) red_max[warp] = warp_finite ? mx : -1.0f;
+    __syncthreads();
+    bool all_finite = true;
+    mx = 0.0f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+      all_finite = all_finite && red_max[w] >= 0.0f;
+      mx = fmaxf(mx, red_max[w]);
+    }
+    int ex = 0;
+    frexpf(mx, &ex);
+    const bool scaled = mx > 0.0f && all_finite;
+    const float S = scaled ? __int_as_float((127 + 22 - ex) << 23) : 1.0f;
+    const float invS = scaled ? __int_as_float((127 - 22 + ex) << 23) : 1.0f;
+    if (q < 4) {
+      float s16 = 0.0f;
+#pragma unroll
+      for (int mm = 0; mm < 4; ++mm) {
+        uint32_t l0 = 0, l1 = 0, l2 = 0;
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb) {
+          const int X = all_finite ? __float2int_rn(xw[mm + 4 * bb] * S) : 0;
+          const int X0 = ((X + 128) & 255) - 128;
+          const int Rr = (X - X0) >> 8;
+          const int X1 = ((Rr + 128) & 255) - 128;
+          const int X2 = (Rr - X1) >> 8;
+          l0 |= (uint32_t)(X0 & 255) << (8 * bb);
+          l1 |= (uint32_t)(X1 & 255) << (8 * bb);
+          l2 |= (uint32_t)(X2 & 255) << (8 * bb);
+        }
+        limb_s[span][q][mm] = l0;
+        limb_s[span][q][4 + mm] = l1;
+        limb_s[span][q][8 + mm] = l2;
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) s16 += xw[i];
+      xsum_s[span][q] = s16;
+    }
+    __syncthreads();
+    uint32_t lw[4][12];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int k = 0; k < 12; k += 4) {
+        const uint4 v4 = *reinterpret_cast<const uint4 *>(&limb_s[span][i][k]);
+        lw[i][k] = v4.x;
+        lw[i][k + 1] = v4.y;
+        lw[i][k + 2] = v4.z;
+        lw[i][k + 3] = v4.w;
+      }
+    float xpart[GPT];
+#pragma unroll
+    for (int p = 0; p < GPT; ++p) {
+      xpart[p] = 0.0f;
+#pragma unroll
+      for (int i = p * WPP; i < (p + 1) * WPP; ++i) xpart[p] += xsum_s[span][i];
+    }
+    const uint32_t g0 = (64u * span) / a.group_size;
+
+    uint32_t running = 0;  // warp 0: kept so far in the current slot's segment
+    for (uint32_t i = 0; i < n_items; ++i) {
+      const uint32_t s = i / n_sub, k = i % n_sub;
+      if (k == 0) running = 0;
+      const uint32_t u_idx = first_use + i;
+      ring.wait(u_idx);
+      const uint8_t *st = ring.stage(u_idx);
+      const uint32_t c0 = c_lo + k * CH;
+      const uint32_t nc = min((uint32_t)CH, c_hi - c0);
+      float part[CPT];
+#pragma unroll
+      for (int r = 0; r < CPT; ++r) {
+        const uint32_t j = q + CS * r;
+        float acc = 0.0f;
+        if (j < nc) {
+          const uint4 w4 = *reinterpret_cast<const uint4 *>(st + j * ROW + 16 * span);
+          const uint32_t *meta = reinterpret_cast<const uint32_t *>(st + code_sz) + j * gpc + g0;
+          const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
+          if (all_finite) {
+#pragma unroll
+            for (int p = 0; p < GPT; ++p) {
+              int a0 = 0, a1 = 0, a2 = 0;
+#pragma unroll
+              for (int ii = p * WPP; ii < (p + 1) * WPP; ++ii) {
+#pragma unroll
+                for (int mm = 0; mm < 4; ++mm) {
+                  const int cb = (int)((wv[ii] >> (2 * mm)) & 0x03030303u);
+                  a0 = __dp4a(cb, (int)lw[ii][mm], a0);
+                  a1 = __dp4a(cb, (int)lw[ii][4 + mm], a1);
+                  a2 = __dp4a(cb, (int)lw[ii][8 + mm], a2);
+                }
+              }
+              const int T = a2 * 65536 + a1 * 256 + a0;
+              const uint32_t mz = meta[p];
+              const float sc = __half2float(__ushort_as_half((uint16_t)(mz & 0xffffu)));
+              const float zr = __half2float(__ushort_as_half((uint16_t)(mz >> 16)));
+              acc = fmaf(sc * invS, (float)T, fmaf(zr, xpart[p], acc));
+            }
+          } else {
+            acc = k1_span_f32(wv, meta, a.group_size, xg + 64 * span);
+          }
+        }
+        part[r] = acc;
+      }
+#pragma unroll
+      for (int sft = 16, cnt = CPT / 2; cnt >= 1; sft >>= 1, cnt >>= 1) {
+        const bool upper = (lane & sft) != 0;
+#pragma unroll
+        for (int r = 0; r < cnt; ++r) {
+          const float send = upper ? part[r] : part[r + cnt];
+          const float keep = upper ? part[r + cnt] : part[r];
+          part[r] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+        }
+      }
+#pragma unroll
+      for (int sft = 32 / CPT / 2; sft >= 1; sft >>= 1)
+        part[0] += __shfl_xor_sync(0xffffffffu, part[0], sft);
+      if ((lane & (32 / CPT - 1)) == 0) wsum[i & 1][warp][lane / (32 / CPT)] = part[0];
+      __syncthreads();  // wsum[i&1] complete; stage retired
+      if (t == 0 && i + a.ns < n_items) issue_tile(i + a.ns);
+      if (warp == 0) {
+        const uint32_t j = lane;
+        float v = 0.0f;
+        if (j < (uint32_t)CH) {
+          const uint32_t qq = j % CS, rr = j / CS;
+#pragma unroll
+          for (int w = 0; w < SPANS / 32; ++w) v += wsum[i & 1][qq * (SPANS / 32) + w][rr];
+        }
+        const uint32_t c = c0 + j;
+        const bool valid = j < nc;
+        // model.cpp:135: `if (fabs(v) < t) continue;` -> ties and NaN are kept
+        const bool keep = valid && !(fabsf(v) < thr_s[s]);
+        const size_t off = (size_t)s * a.di + c;
+        if (valid) {
+          if (a.v_out) a.v_out[off] = v;
+          if (a.mask_out) a.mask_out[off] = keep ? 1 : 0;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+          const size_t o = (size_t)s * a.di + c_lo + running + __popc(bal & ((1u << lane) - 1));
+          a.kept_idx[o] = c;
+          a.kept_v[o] = v;
+        }
+        running += __popc(bal);
+        if (k + 1 == n_sub && lane == 0) a.seg_count[s * G + b] = running;
+      }
+    }
+    ring.use = first_use + n_items;
+  }
+  grid_sync(a.bar);
+
+  // =========================== phase C: K2 ================================
+  {
+    const uint32_t rec_bytes = 4u * DH;
+    const uint32_t nseg = a.slots * G;
+    uint32_t *prefix = reinterpret_cast<uint32_t *>(
+        smem + a.ns * a.stage_bytes + (a.has_mixing ? 4u * DH : 0u));
+    // seg_prefix reads seg_count written by other CTAs before the barrier
+    seg_prefix(a.seg_count, nseg, prefix);
+    if (b == 0) {
+      if (t < a.slots && a.n_kept_out) a.n_kept_out[t] = prefix[(t + 1) * G] - prefix[t * G];
+      if (t == 0 && a.stats) {
+        atomicAdd(&a.stats[0], 1ull);
+        atomicAdd(&a.stats[1], (unsigned long long)prefix[nseg]);
+      }
+    }
+    const uint32_t total = prefix[nseg];
+    const uint32_t begin = (uint32_t)(((uint64_t)total * b) / G);
+    const uint32_t end = (uint32_t)(((uint64_t)total * (b + 1)) / G);
+    constexpr int TPB2 = DH / 16;  // threads owning 16 elements each
+    float2 x2[8], y2[8];
+    const bool active = t < (uint32_t)TPB2;  // dh = 2048 uses half the CTA
+    {
+      const uint32_t tt = active ? t : 0;
+      const float4 *xa = reinterpret_cast<const float4 *>(a.u + 8 * tt);
+      const float4 *xb = reinterpret_cast<const float4 *>(a.u + 8 * (tt + TPB2));
+      const float4 q0 = __ldcg(xa), q1 = __ldcg(xa + 1), q2 = __ldcg(xb), q3 = __ldcg(xb + 1);
+      x2[0] = make_float2(q0.x, q0.y);
+      x2[1] = make_float2(q0.z, q0.w);
+      x2[2] = make_float2(q1.x, q1.y);
+      x2[3] = make_float2(q1.z, q1.w);
+      x2[4] = make_float2(q2.x, q2.y);
+      x2[5] = make_float2(q2.z, q2.w);
+      x2[6] = make_float2(q3.x, q3.y);
+      x2[7] = make_float2(q3.z, q3.w);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) y2[i] = make_float2(0.0f, 0.0f);
+    }
+    uint32_t batch = 0;
+    for (uint32_t cb = begin; cb < end; cb += kK2Chunk) {
+      const uint32_t n = min(kK2Chunk, end - cb);
+      __syncthreads();
+      for (uint32_t qq = t; qq < n; qq += TPB) {
+        const uint32_t p = cb + qq;
+        const uint32_t idx = seg_find(prefix, nseg, p);
+        const uint32_t s = idx / G, bb = idx % G;
+        const size_t o = (size_t)s * a.di + seg_begin(a.di, bb, G) + (p - prefix[idx]);
+        const uint32_t c = __ldcg(&a.kept_idx[o]);
+        ent_rec[qq] = rec_s[s] + (size_t)c * 2 * DH;
+        ent_scale[qq] = __ldcg(&a.kept_v[o]) * w_s[s];
+        if (a.kept_out) a.kept_out[(size_t)s * a.di + (p - prefix[s * G])] = c;
+      }
+      __syncthreads();
+      const uint32_t first_use = ring.use;
+      if (t == 0)
+        for (uint32_t k = 0; k < n && k < a.ns; ++k) {
+          floe_ptx::mbar_arrive_expect_tx(ring.bar(issued), rec_bytes);
+          floe_ptx::bulk_g2s(ring.stage(issued), ent_rec[k], rec_bytes, ring.bar(issued));
+          ++issued;
+        }
+      for (uint32_t q0 = 0; q0 < n; q0 += R, ++batch) {
+        uint4 dv[R][2];
+        float gp[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          gp[r] = 0.0f;
+          dv[r][0] = dv[r][1] = make_uint4(0, 0, 0, 0);
+          if (q0 + r < n) {
+            const uint32_t u_idx = first_use + q0 + r;
+            ring.wait(u_idx);
+            if (active) {
+              const uint4 *rec = reinterpret_cast<const uint4 *>(ring.stage(u_idx));
+              const uint4 g0 = rec[t], g1 = rec[t + TPB2];
+              dv[r][0] = rec[2 * TPB2 + t];
+              dv[r][1] = rec[3 * TPB2 + t];
+              const __half2 *h0 = reinterpret_cast<const __half2 *>(&g0);
+              const __half2 *h1 = reinterpret_cast<const __half2 *>(&g1);
+              float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                acc = __ffma2_rn(__half22float2(h0[j]), x2[j], acc);
+                acc = __ffma2_rn(__half22float2(h1[j]), x2[4 + j], acc);
+              }
+              gp[r] = acc.x + acc.y;
+            }
+          }
+        }
+#pragma unroll
+        for (int sft = 16, cnt = R / 2; cnt >= 1; sft >>= 1, cnt >>= 1) {
+          const bool upper = (lane & sft) != 0;
+#pragma unroll
+          for (int r = 0; r < cnt; ++r) {
+            const float send = upper ? gp[r] : gp[r + cnt];
+            const float keep = upper ? gp[r + cnt] : gp[r];
+            gp[r] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+          }
+        }
+#pragma unroll
+        for (int sft = 32 / R / 2; sft >= 1; sft >>= 1)
+          gp[0] += __shfl_xor_sync(0xffffffffu, gp[0], sft);
+        if ((lane & (32 / R - 1)) == 0) red[batch & 1][warp][lane / (32 / R)] = gp[0];
+        __syncthreads();  // batch stages retired
+        if (t == 0)
+          for (int r = 0; r < R; ++r) {
+            const uint32_t nq = q0 + r + a.ns;
+            if (q0 + r < n && nq < n) {
+              floe_ptx::mbar_arrive_expect_tx(ring.bar(issued), rec_bytes);
+              floe_ptx::bulk_g2s(ring.stage(issued), ent_rec[nq], rec_bytes, ring.bar(issued));
+              ++issued;
+            }
+          }
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (q0 + r >= n) break;
+          float g = 0.0f;
+#pragma unroll
+          for (int w = 0; w < NW; ++w) g += red[batch & 1][w][r];
+          const float aco = silu_ref(g) * ent_scale[q0 + r];
+          const float2 a2 = make_float2(aco, aco);
+          const __half2 *e0 = reinterpret_cast<const __half2 *>(&dv[r][0]);
+          const __half2 *e1 = reinterpret_cast<const __half2 *>(&dv[r][1]);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            y2[j] = __ffma2_rn(a2, __half22float2(e0[j]), y2[j]);
+            y2[4 + j] = __ffma2_rn(a2, __half22float2(e1[j]), y2[4 + j]);
+          }
+        }
+      }
+      ring.use = first_use + n;
+    }
+    if (end > begin && active) {
+      float *ya = a.y + 8 * t, *yb = a.y + 8 * (t + TPB2);
+      red_add_v4(ya, y2[0].x, y2[0].y, y2[1].x, y2[1].y);
+      red_add_v4(ya + 4, y2[2].x, y2[2].y, y2[3].x, y2[3].y);
+      red_add_v4(yb, y2[4].x, y2[4].y, y2[5].x, y2[5].y);
+      red_add_v4(yb + 4, y2[6].x, y2[6].y, y2[7].x, y2[7].y);
+    }
+  }
+}
+
+}  // namespace floe_k

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -16,7 +17,7 @@
 #include <vector>
 
 #include "../../include/floe_gpu.h"
-#include "floe_fast.cuh"
+#include "floe_fused.cuh"
 #include "floe_gen.cuh"
 
 using floe_k::ExpertDesc;
@@ -133,6 +134,7 @@ struct floe_gpu_workspace {
   float *mix_partial = nullptr;   // [dh/8][32] partial router logits
   uint32_t *mix_done = nullptr;
   unsigned long long *stats = nullptr;
+  unsigned long long *bar = nullptr;  // fused kernel's grid barrier (monotonic)
   uint32_t *sel = nullptr;
   float *weights = nullptr, *u = nullptr, *x = nullptr, *y = nullptr, *v = nullptr;
   uint8_t *mask = nullptr;
@@ -342,6 +344,119 @@ int launch_k2(const K2Launch &L, floe_gpu_workspace *ws, cudaStream_t st) {
   return FLOE_OK;
 }
 
+// Path selection: the fused persistent kernel (default) or the split
+// K1/K2 launches (FLOE_GPU_PATH=split, kept for A/B measurements).
+bool fused_enabled() {
+  static const bool on = [] {
+    const char *p = std::getenv("FLOE_GPU_PATH");
+    return !(p && std::strcmp(p, "split") == 0);
+  }();
+  return on;
+}
+
+struct FusedLaunch {
+  // layer mode (mixing != nullptr) or single-expert mode
+  const void *mixing;
+  bool mix_f16;
+  const float *h, *router;
+  uint32_t n_experts, top_k;
+  const floe_gpu_layer_trace *trace;
+  // experts
+  const ExpertDesc *table;
+  uint32_t slots, dh, di, g;
+  int use_thr;
+  float thr;
+  float *u, *y, *v_out;
+  uint8_t *mask_out;
+  uint32_t *n_kept_out, *kept_out;
+};
+
+int launch_fused(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) {
+  const uint32_t sm = (uint32_t)device_info().sm;
+  floe_k::FusedArgs a{};
+  a.mixing = L.mixing;
+  a.h = L.h;
+  a.router = L.router;
+  a.n_experts = L.n_experts;
+  a.top_k = L.top_k;
+  a.has_mixing = L.mixing != nullptr;
+  a.partial = ws->mix_partial;
+  a.u_trace = L.trace ? L.trace->block_input_dev : nullptr;
+  a.sel_trace = L.trace ? L.trace->experts_dev : nullptr;
+  a.w_trace = L.trace ? L.trace->weights_dev : nullptr;
+  a.sel_out = ws->sel;
+  a.w_out = ws->weights;
+  a.u = L.u;
+  a.y = L.y;
+  a.dh = L.dh;
+  a.di = L.di;
+  a.group_size = L.g;
+  a.slots = L.slots;
+  a.table = L.table;
+  a.use_threshold = L.use_thr;
+  a.threshold = L.thr;
+  a.v_out = L.v_out;
+  a.mask_out = L.mask_out ? L.mask_out : (L.trace ? L.trace->masks_dev : nullptr);
+  a.kept_idx = ws->kept_idx;
+  a.kept_v = ws->kept_v;
+  a.seg_count = ws->seg_count;
+  a.bar = ws->bar;
+  a.n_kept_out = L.n_kept_out;
+  a.kept_out = L.kept_out;
+  a.stats = ws->stats;
+  ws->g1 = sm;
+  // ring geometry: one stage holds a K1 sub-tile, a 16 KB record or mixing rows
+  const uint32_t gpc = L.dh / L.g;
+  uint32_t stage = std::max<uint32_t>(floe_k::k1_stage_bytes(L.dh, gpc), 4u * L.dh);
+  if (a.has_mixing) stage = std::max<uint32_t>(stage, L.dh * (L.mix_f16 ? 2u : 4u));
+  stage = floe_k::round_up128(stage);
+  const uint32_t ns = std::min<uint32_t>(floe_k::kFusedMaxStages, floe_k::kFusedRingBytes / stage);
+  if (ns < 2) return fail(FLOE_ERR_UNSUPPORTED, "fused path: stage of %u B too large", stage);
+  a.stage_bytes = stage;
+  a.ns = ns;
+  const uint32_t smem = ns * stage + (a.has_mixing ? 4u * L.dh : 0u) + 4u * (L.slots * sm + 1);
+  const uint32_t gpt = L.g >= 64 ? 1u : 64u / L.g;
+  void *kargs[] = {&a};
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(sm);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // grid barriers need co-residency
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  StageScope prof(ws, kStageK2, st);
+  cudaError_t e = cudaSuccess;
+#define FLOE_FUSED(TT, SP, GP)                                                           \
+  do {                                                                                   \
+    auto *fn = floe_k::floe_fused<TT, SP, GP>;                                           \
+    if (int rc = set_smem(fn, smem)) return rc;                                          \
+    e = cudaLaunchKernelExC(&cfg, reinterpret_cast<const void *>(fn), kargs);           \
+  } while (0)
+#define FLOE_FUSED_GPT(TT, SP)            \
+  do {                                    \
+    if (gpt == 1) FLOE_FUSED(TT, SP, 1);  \
+    else if (gpt == 2) FLOE_FUSED(TT, SP, 2); \
+    else FLOE_FUSED(TT, SP, 4);           \
+  } while (0)
+  const bool f32mix = a.has_mixing && !L.mix_f16;
+  if (L.dh == 4096) {
+    if (f32mix) FLOE_FUSED_GPT(float, 64);
+    else FLOE_FUSED_GPT(__half, 64);
+  } else {
+    if (f32mix) FLOE_FUSED_GPT(float, 32);
+    else FLOE_FUSED_GPT(__half, 32);
+  }
+#undef FLOE_FUSED_GPT
+#undef FLOE_FUSED
+  if (e != cudaSuccess)
+    return fail(FLOE_ERR_CUDA, "fused launch failed: %s", cudaGetErrorString(e));
+  CK_LAUNCH();
+  return FLOE_OK;
+}
+
 int check_ws(const char *fn, const floe_gpu_workspace *ws, uint32_t dh, uint32_t di,
              uint32_t slots) {
   if (!ws) return fail(FLOE_ERR_INVALID, "%s: null workspace", fn);
@@ -539,7 +654,7 @@ int floe_gpu_workspace_create(uint32_t dh, uint32_t di, uint32_t slots,
   const uint64_t o_cnt = o;   o = up256(o + 4ull * MS * kMaxSeg);
   const uint64_t o_mp = o;    o = up256(o + 4ull * 32 * std::max<uint64_t>(1024, (dh + 7) / 8));
   const uint64_t o_md = o;    o = up256(o + 16);
-  const uint64_t o_st = o;    o = up256(o + 16);
+  const uint64_t o_st = o;    o = up256(o + 32);  // stats[2], grid barrier counter
   const uint64_t o_sel = o;   o = up256(o + 4 * MS);
   const uint64_t o_w = o;     o = up256(o + 4 * MS);
   const uint64_t o_u = o;     o = up256(o + 4ull * dh);
@@ -559,6 +674,7 @@ int floe_gpu_workspace_create(uint32_t dh, uint32_t di, uint32_t slots,
   w->mix_partial = reinterpret_cast<float *>(b + o_mp);
   w->mix_done = reinterpret_cast<uint32_t *>(b + o_md);
   w->stats = reinterpret_cast<unsigned long long *>(b + o_st);
+  w->bar = w->stats + 2;
   w->sel = reinterpret_cast<uint32_t *>(b + o_sel);
   w->weights = reinterpret_cast<float *>(b + o_w);
   w->u = reinterpret_cast<float *>(b + o_u);
@@ -648,6 +764,21 @@ int floe_gpu_expert_forward_sparse(const floe_gpu_expert *e, floe_gpu_workspace 
                                    uint32_t *n_kept_out, floe_stream_t stream) {
   if (!e || !x || !y) return fail(FLOE_ERR_INVALID, "expert_forward_sparse: null argument");
   if (int rc = check_ws("expert_forward_sparse", ws, e->dh, e->di, 1)) return rc;
+  if (e->fast_k1 && e->fast_k2 && fused_enabled()) {
+    FusedLaunch f{};
+    f.table = e->dev_desc;
+    f.slots = 1;
+    f.dh = e->dh;
+    f.di = e->di;
+    f.g = e->g;
+    f.u = const_cast<float *>(x);
+    f.y = y;
+    f.v_out = v_out;
+    f.mask_out = mask_out;
+    f.n_kept_out = n_kept_out;
+    f.kept_out = kept_out;
+    return launch_fused(f, ws, S(stream));
+  }
   K1Launch k1{e->dev_desc, nullptr, 1, e->dh, e->di, e->bits, e->g, e->fast_k1, 0, 0.0f,
               x, v_out, mask_out, nullptr, nullptr, y};
   if (int rc = launch_k1(k1, ws, S(stream))) return rc;
@@ -789,6 +920,24 @@ int floe_gpu_layer_forward(const floe_gpu_layer *l, floe_gpu_workspace *ws, cons
   if (!l || !h || !y) return fail(FLOE_ERR_INVALID, "layer_forward: null argument");
   if (int rc = check_ws("layer_forward", ws, l->dh, l->di, l->top_k)) return rc;
   cudaStream_t st = S(stream);
+  if (l->fast_k1 && l->fast_k2 && fused_enabled() && l->E <= 32) {
+    FusedLaunch f{};
+    f.mixing = l->mixing;
+    f.mix_f16 = l->mix_f16;
+    f.h = h;
+    f.router = l->router;
+    f.n_experts = l->E;
+    f.top_k = l->top_k;
+    f.trace = tr;
+    f.table = l->table;
+    f.slots = l->top_k;
+    f.dh = l->dh;
+    f.di = l->di;
+    f.g = l->g;
+    f.u = ws->u;
+    f.y = y;
+    return launch_fused(f, ws, st);
+  }
   const uint32_t rows_per_block = 8;
   const size_t smem = 4ull * l->dh;
   float *u_tr = tr ? tr->block_input_dev : nullptr;
