@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(256, 2) k1_int2(const K1Args a) {
   __shared__ uint64_t full[NS];
   __shared__ float wsum[NW][CPT];
   __shared__ float red_max[NW];
-  __shared__ uint32_t limb_s[SPANS][4][12];  // [span][word][limb*4 + m]
+  __shared__ __align__(16) uint32_t limb_s[SPANS][4][12];  // [span][word][limb*4 + m], read as uint4
   __shared__ float xsum_s[SPANS][4];
 
   const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;

@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
   __shared__ const __half *rec_s[kMaxSlots];
   __shared__ float thr_s[kMaxSlots];
   __shared__ float red_max[NW];
-  __shared__ uint32_t limb_s[SPANS][4][12];
+  __shared__ __align__(16) uint32_t limb_s[SPANS][4][12];  // read as uint4
   __shared__ float xsum_s[SPANS][4];
   __shared__ float wsum[2][NW][CPT];
   __shared__ float red[2][NW][R];
