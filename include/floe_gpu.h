@@ -221,6 +221,13 @@ int floe_gpu_workspace_set_profiling(floe_gpu_workspace *ws, int enable);
 int floe_gpu_workspace_read_profile(floe_gpu_workspace *ws, double *ms,
                                     uint64_t *launches);
 
+/* Diagnostics: per-CTA %globaltimer marks of the fused kernel's phases
+ * (0 start, 1 mixing done, 2 routed, 3 K1 done, 4 after barrier, 5 K2 done),
+ * 8 u64 slots per CTA.  read copies min(cap, grid*8) values and synchronises. */
+int floe_gpu_workspace_set_phase_trace(floe_gpu_workspace *ws, int enable);
+int floe_gpu_workspace_read_phase_trace(floe_gpu_workspace *ws, uint64_t *out, uint32_t cap,
+                                        uint32_t *grid);
+
 /* ------------------------------------------------------- synthetic model */
 /* Reference random streams on the device (rng.cpp:12-64): out[i] =
  * sigma * (float)normal_i.  sharded = 1 reproduces gen_model's fill_gaussian

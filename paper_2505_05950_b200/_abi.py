@@ -85,7 +85,9 @@ _SIGS = {
     "floe_gpu_workspace_read_counters": (ct.c_int, [_P, _P, _P, _P]),
     "floe_gpu_workspace_set_profiling": (ct.c_int, [_P, ct.c_int]),
     "floe_gpu_workspace_read_profile": (ct.c_int, [_P, _P, _P]),
-    "floe_gpu_gen_normals": (ct.c_int, [ct.c_uint64, ct.c_uint64, ct.c_uint64, _F, ct.c_int, _P,
+    "floe_gpu_workspace_set_phase_trace": (ct.c_int, [_P, ct.c_int]),
+    "floe_gpu_workspace_read_phase_trace": (ct.c_int, [_P, _P, _U32, _P]),
+    "floe_gpu_gen_normals":(ct.c_int, [ct.c_uint64, ct.c_uint64, ct.c_uint64, _F, ct.c_int, _P,
                                         _P]),
     "floe_gpu_quantize": (ct.c_int, [_P, ct.c_uint64, _U32, _U32, _P, _P, _P, _P]),
     "floe_gpu_predictor_create": (ct.c_int, [_U32, _U32, _U32, _P, _P, ct.POINTER(_P)]),
@@ -200,6 +202,17 @@ class Workspace:
 
     def set_profiling(self, enable: bool):
         _check(lib().floe_gpu_workspace_set_profiling(self.handle, 1 if enable else 0))
+
+    def set_phase_trace(self, enable: bool):
+        _check(lib().floe_gpu_workspace_set_phase_trace(self.handle, 1 if enable else 0))
+
+    def read_phase_trace(self) -> np.ndarray:
+        """[grid, 8] %globaltimer ns marks of the fused kernel's last call."""
+        out = np.zeros(8 * 1024, np.uint64)
+        grid = ct.c_uint32()
+        _check(lib().floe_gpu_workspace_read_phase_trace(self.handle, out.ctypes.data, out.size,
+                                                         ct.byref(grid)))
+        return out[: 8 * grid.value].reshape(grid.value, 8)
 
     def read_profile(self) -> dict:
         ms = (ct.c_double * 4)()

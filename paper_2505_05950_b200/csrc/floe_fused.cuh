@@ -59,7 +59,18 @@ struct FusedArgs {
   uint32_t *kept_out;
   unsigned long long *stats;
   uint32_t stage_bytes, ns;  // ring geometry
+  unsigned long long *phase_ns;  // nullable [grid][8]: %globaltimer at phase marks
 };
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void mark(const FusedArgs &a, int k) {
+  if (a.phase_ns && threadIdx.x == 0) a.phase_ns[blockIdx.x * 8 + k] = global_ns();
+}
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
   unsigned long long v;
@@ -130,6 +141,7 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
   const uint32_t G = gridDim.x, b = blockIdx.x;
   Ring ring{smem, full, a.stage_bytes, a.ns, 0};
   float *hs = reinterpret_cast<float *>(smem + a.ns * a.stage_bytes);  // [dh] (layer mode)
+  mark(a, 0);
 
   if (t == 0) {
     for (uint32_t s = 0; s < a.ns; ++s) floe_ptx::mbar_init(&full[s], 1);
@@ -228,6 +240,7 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
       }
       a.partial[b * 32 + lane] = s;
     }
+    mark(a, 1);
     grid_sync(a.bar);
     // route (model.cpp:83-93): every CTA sums the partials in the same order
     for (uint32_t e = warp; e < a.n_experts; e += NW) {
@@ -267,6 +280,7 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
     thr_s[t] = a.use_threshold ? a.threshold : d.threshold;
   }
 
+  mark(a, 2);
   // =========================== phase B: K1 ================================
   {
     const uint32_t span = t % SPANS, q = t / SPANS;
@@ -462,9 +476,11 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
     }
     ring.use = first_use + n_items;
   }
+  mark(a, 3);
   grid_sync(a.bar);
 
   // =========================== phase C: K2 ================================
+  mark(a, 4);
   {
     const uint32_t rec_bytes = 4u * DH;
     const uint32_t nseg = a.slots * G;
@@ -593,6 +609,7 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
       }
       ring.use = first_use + n;
     }
+    mark(a, 5);
     if (end > begin && active) {
       float *ya = a.y + 8 * t, *yb = a.y + 8 * (t + TPB2);
       red_add_v4(ya, y2[0].x, y2[0].y, y2[1].x, y2[1].y);

@@ -135,6 +135,7 @@ struct floe_gpu_workspace {
   uint32_t *mix_done = nullptr;
   unsigned long long *stats = nullptr;
   unsigned long long *bar = nullptr;  // fused kernel's grid barrier (monotonic)
+  unsigned long long *phase_ns = nullptr;  // diagnostics: [grid][8] phase marks
   uint32_t *sel = nullptr;
   float *weights = nullptr, *u = nullptr, *x = nullptr, *y = nullptr, *v = nullptr;
   uint8_t *mask = nullptr;
@@ -404,6 +405,7 @@ int launch_fused(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) 
   a.n_kept_out = L.n_kept_out;
   a.kept_out = L.kept_out;
   a.stats = ws->stats;
+  a.phase_ns = ws->phase_ns;
   ws->g1 = sm;
   // ring geometry: one stage holds a K1 sub-tile, a 16 KB record or mixing rows
   const uint32_t gpc = L.dh / L.g;
@@ -710,6 +712,7 @@ int floe_gpu_workspace_destroy(floe_gpu_workspace *w) {
   if (w->hv) cudaFreeHost(w->hv);
   if (w->hmask) cudaFreeHost(w->hmask);
   if (w->hstats) cudaFreeHost(w->hstats);
+  if (w->phase_ns) cudaFree(w->phase_ns);
   delete w;
   return FLOE_OK;
 }
@@ -727,6 +730,29 @@ int floe_gpu_workspace_read_counters(floe_gpu_workspace *w, uint64_t *calls,
   CK(cudaStreamSynchronize(S(stream)));
   if (calls) *calls = w->hstats[0];
   if (kept_total) *kept_total = w->hstats[1];
+  return FLOE_OK;
+}
+
+int floe_gpu_workspace_set_phase_trace(floe_gpu_workspace *w, int enable) {
+  if (!w) return fail(FLOE_ERR_INVALID, "workspace_set_phase_trace: null workspace");
+  if (enable && !w->phase_ns) {
+    CK(cudaMalloc(&w->phase_ns, 8ull * 8 * device_info().sm));
+    CK(cudaMemset(w->phase_ns, 0, 8ull * 8 * device_info().sm));
+  } else if (!enable && w->phase_ns) {
+    cudaFree(w->phase_ns);
+    w->phase_ns = nullptr;
+  }
+  return FLOE_OK;
+}
+
+int floe_gpu_workspace_read_phase_trace(floe_gpu_workspace *w, uint64_t *out, uint32_t cap,
+                                        uint32_t *grid) {
+  if (!w || !out) return fail(FLOE_ERR_INVALID, "workspace_read_phase_trace: null argument");
+  const uint32_t n = std::min<uint32_t>(cap, 8u * device_info().sm);
+  if (grid) *grid = device_info().sm;
+  if (!w->phase_ns) return fail(FLOE_ERR_INVALID, "workspace_read_phase_trace: tracing is off");
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(out, w->phase_ns, 8ull * n, cudaMemcpyDeviceToHost));
   return FLOE_OK;
 }
 
