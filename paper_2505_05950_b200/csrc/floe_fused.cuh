@@ -20,9 +20,9 @@
 //      reduced into y once (model.cpp:136-140, 162-166)
 //
 // All weight traffic is 1-D bulk copies (cp.async.bulk) through ONE shared
-// memory ring of NS stages that persists across phases; thread 0 refills a
-// stage after the block barrier that retires it.  The mbarrier parity of a
-// stage use is (use / NS) & 1 with `use` counted across all phases.
+// memory ring that persists across phases and is re-carved per phase (16 KB
+// stages for mixing rows and gate|down records, K1-tile stages for phase B);
+// thread 0 refills a stage after the block barrier that retires it.
 #pragma once
 
 #include "floe_fast.cuh"
@@ -58,7 +58,7 @@ struct FusedArgs {
   uint32_t *n_kept_out;
   uint32_t *kept_out;
   unsigned long long *stats;
-  uint32_t stage_bytes, ns;  // ring geometry
+  uint32_t ring_bytes;           // shared-memory ring size
   unsigned long long *phase_ns;  // nullable [grid][8]: %globaltimer at phase marks
 };
 
@@ -92,19 +92,40 @@ __device__ __forceinline__ void grid_sync(unsigned long long *bar) {
   __syncthreads();
 }
 
-// Ring of NS bulk-copy stages in dynamic shared memory.
+constexpr uint32_t kFusedMaxStages = 24;
+constexpr uint32_t kFusedRingBytes = 168 * 1024;
+constexpr int kMaxGridPerWarp = 8;  // grid <= 256 CTAs
+
+// Ring of bulk-copy stages in dynamic shared memory.  `issued` is thread 0's
+// count of copies issued; uses are consumed in issue order.
 struct Ring {
   uint8_t *base;
   uint64_t *full;
   uint32_t stage_bytes, ns;
-  uint32_t use;  // next stage use to be consumed (uniform across the CTA)
   __device__ uint8_t *stage(uint32_t u) const { return base + (u % ns) * stage_bytes; }
   __device__ uint64_t *bar(uint32_t u) const { return &full[u % ns]; }
   __device__ void wait(uint32_t u) const { floe_ptx::mbar_wait(bar(u), (u / ns) & 1u); }
+  __device__ void issue(uint32_t u, const void *src, uint32_t bytes) const {
+    floe_ptx::mbar_arrive_expect_tx(bar(u), bytes);
+    floe_ptx::bulk_g2s(stage(u), src, bytes, bar(u));
+  }
 };
 
-constexpr uint32_t kFusedMaxStages = 24;
-constexpr uint32_t kFusedRingBytes = 168 * 1024;
+// Re-carve the ring (all previous copies consumed): fresh barriers.
+__device__ __forceinline__ Ring ring_make(uint8_t *base, uint64_t *full, uint32_t stage_bytes,
+                                          uint32_t ring_bytes, bool reinit) {
+  Ring r{base, full, stage_bytes, min(kFusedMaxStages, ring_bytes / stage_bytes)};
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < kFusedMaxStages; ++s) {
+      if (reinit) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(floe_ptx::smem_u32(&full[s])) : "memory");
+      floe_ptx::mbar_init(&full[s], 1);
+    }
+    floe_ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  return r;
+}
 
 // ---------------------------------------------------------------------------
 template <typename T, int SPANS, int GPT>
@@ -117,11 +138,11 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
   constexpr int WPP = 4 / GPT;
   constexpr uint32_t DH = SPANS * 64;
   constexpr uint32_t ROW = DH / 4;
-  constexpr int R = 4;  // K2 records per block barrier
+  constexpr uint32_t REC = 4 * DH;  // gate|down record bytes
+  constexpr int R = 4;              // K2 records per batch
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t full[kFusedMaxStages];
   __shared__ uint64_t hbar;
-  __shared__ float part_s[NW][32];
   __shared__ float u_s[kMaxRowsPerCta];
   __shared__ float rs[32 * kMaxRowsPerCta];
   __shared__ float logits[32];
@@ -129,61 +150,59 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
   __shared__ float w_s[kMaxSlots];
   __shared__ const __half *rec_s[kMaxSlots];
   __shared__ float thr_s[kMaxSlots];
+  __shared__ ExpertDesc table_s[32];
   __shared__ float red_max[NW];
   __shared__ __align__(16) uint32_t limb_s[SPANS][4][12];  // read as uint4
   __shared__ float xsum_s[SPANS][4];
   __shared__ float wsum[2][NW][CPT];
-  __shared__ float red[2][NW][R];
+  __shared__ float red[NW][R];
+  __shared__ float aco_s[2][R];
   __shared__ const __half *ent_rec[kK2Chunk];
   __shared__ float ent_scale[kK2Chunk];
 
   const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const uint32_t G = gridDim.x, b = blockIdx.x;
-  Ring ring{smem, full, a.stage_bytes, a.ns, 0};
-  float *hs = reinterpret_cast<float *>(smem + a.ns * a.stage_bytes);  // [dh] (layer mode)
+  float *hs = reinterpret_cast<float *>(smem + a.ring_bytes);  // [dh] (layer mode)
   mark(a, 0);
 
   if (t == 0) {
-    for (uint32_t s = 0; s < a.ns; ++s) floe_ptx::mbar_init(&full[s], 1);
     floe_ptx::mbar_init(&hbar, 1);
     floe_ptx::fence_barrier_init();
   }
-  __syncthreads();
-  uint32_t issued = 0;  // stage uses issued so far (thread 0's view)
+  // expert descriptors of the whole layer, fetched once (hidden behind phase A)
+  const uint32_t n_table = a.has_mixing ? a.n_experts : a.slots;
+  if (t < n_table) table_s[t] = a.table[t];
+  Ring ring = ring_make(smem, full, REC, a.ring_bytes, false);
 
   // =========================== phase A: mixing ===========================
   if (a.has_mixing) {
     const uint32_t row_bytes = DH * (uint32_t)sizeof(T);
-    const uint32_t rps = a.stage_bytes / row_bytes;  // rows per stage (1 or 2)
+    const uint32_t rps = REC / row_bytes;  // rows per stage (2 for f16, 1 for f32)
     const uint32_t r_lo = seg_begin(DH, b, G), r_hi = seg_begin(DH, b + 1, G);
     const uint32_t n_items = (r_hi - r_lo + rps - 1) / rps;
     const T *m = static_cast<const T *>(a.mixing);
-    auto issue_rows = [&](uint32_t i) {  // item i -> use `issued`
+    const uint32_t per_round = min(NW / rps, ring.ns / 2);  // stages per block barrier
+    auto issue_rows = [&](uint32_t i) {
       const uint32_t r0 = r_lo + i * rps, nr = min(rps, r_hi - r0);
-      floe_ptx::mbar_arrive_expect_tx(ring.bar(issued), nr * row_bytes);
-      floe_ptx::bulk_g2s(ring.stage(issued), m + (size_t)r0 * DH, nr * row_bytes, ring.bar(issued));
-      ++issued;
+      ring.issue(i, m + (size_t)r0 * DH, nr * row_bytes);
     };
     if (t == 0) {
       floe_ptx::mbar_arrive_expect_tx(&hbar, 4u * DH);
       floe_ptx::bulk_g2s(hs, a.h, 4u * DH, &hbar);
-      for (uint32_t i = 0; i < n_items && i < a.ns; ++i) issue_rows(i);
+      for (uint32_t i = 0; i < n_items && i < ring.ns; ++i) issue_rows(i);
     }
     for (uint32_t i = t; i < a.n_experts * kMaxRowsPerCta; i += TPB) {
       const uint32_t e = i / kMaxRowsPerCta, lr = i % kMaxRowsPerCta;
       if (r_lo + lr < r_hi) rs[i] = a.router[(size_t)e * DH + r_lo + lr];
     }
     floe_ptx::mbar_wait(&hbar, 0);
-    const uint32_t per_round = NW / rps;  // stages consumed per block barrier
     constexpr uint32_t EPL = 16 / sizeof(T);
-    const uint32_t first_use = ring.use;
     for (uint32_t i0 = 0; i0 < n_items; i0 += per_round) {
       const uint32_t item = i0 + warp / rps, sub = warp % rps;
       const uint32_t row = r_lo + item * rps + sub;
-      if (item < n_items && row < r_hi) {
-        const uint32_t u_idx = first_use + item;
-        ring.wait(u_idx);
-        const T *rowp = reinterpret_cast<const T *>(ring.stage(u_idx)) + (size_t)sub * DH;
+      if (warp / rps < per_round && item < n_items && row < r_hi) {
+        ring.wait(item);
+        const T *rowp = reinterpret_cast<const T *>(ring.stage(item)) + (size_t)sub * DH;
         float acc0 = 0.0f, acc1 = 0.0f;
 #pragma unroll 4
         for (uint32_t k = lane * EPL; k < DH; k += 32 * EPL) {
@@ -223,11 +242,10 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
       __syncthreads();  // the round's stages are consumed
       if (t == 0)
         for (uint32_t k = 0; k < per_round; ++k) {
-          const uint32_t nxt = i0 + k + a.ns;
+          const uint32_t nxt = i0 + k + ring.ns;
           if (i0 + k < n_items && nxt < n_items) issue_rows(nxt);
         }
     }
-    ring.use = first_use + n_items;
     // this CTA's share of router.u (fixed order: ascending rows)
     if (warp == 0 && lane < a.n_experts) {
       float s = 0.0f;
@@ -244,8 +262,15 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
     grid_sync(a.bar);
     // route (model.cpp:83-93): every CTA sums the partials in the same order
     for (uint32_t e = warp; e < a.n_experts; e += NW) {
+      float pv[kMaxGridPerWarp];  // all loads in flight at once
+#pragma unroll
+      for (int j = 0; j < kMaxGridPerWarp; ++j) {
+        const uint32_t bb = lane + 32 * j;
+        pv[j] = bb < G ? __ldcg(&a.partial[bb * 32 + e]) : 0.0f;
+      }
       float s = 0.0f;
-      for (uint32_t bb = lane; bb < G; bb += 32) s += __ldcg(&a.partial[bb * 32 + e]);
+#pragma unroll
+      for (int j = 0; j < kMaxGridPerWarp; ++j) s += pv[j];
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if (lane == 0) logits[e] = s;
@@ -275,7 +300,7 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
   }
   __syncthreads();
   if (t < a.slots) {
-    const ExpertDesc &d = a.table[sel_s[t]];
+    const ExpertDesc &d = table_s[sel_s[t]];
     rec_s[t] = d.records;
     thr_s[t] = a.use_threshold ? a.threshold : d.threshold;
   }
@@ -289,20 +314,18 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
     const uint32_t n_items = n_sub * a.slots;
     const uint32_t gpc = DH / a.group_size;
     const uint32_t code_sz = round_up128(CH * ROW);
-    __syncthreads();  // sel_s / rec_s visible
+    ring = ring_make(smem, full, k1_stage_bytes(DH, gpc), a.ring_bytes, true);
     auto issue_tile = [&](uint32_t i) {  // item i = (slot, sub-tile)
       const uint32_t s = i / n_sub, k = i % n_sub;
       const uint32_t c0 = c_lo + k * CH, nc = min((uint32_t)CH, c_hi - c0);
-      const ExpertDesc &d = a.table[sel_s[s]];
-      floe_ptx::mbar_arrive_expect_tx(ring.bar(issued), nc * (ROW + gpc * 4u));
-      floe_ptx::bulk_g2s(ring.stage(issued), d.codes + (size_t)c0 * ROW, nc * ROW, ring.bar(issued));
-      floe_ptx::bulk_g2s(ring.stage(issued) + code_sz, d.meta + (size_t)c0 * gpc, nc * gpc * 4u,
-                         ring.bar(issued));
-      ++issued;
+      const ExpertDesc &d = table_s[sel_s[s]];
+      floe_ptx::mbar_arrive_expect_tx(ring.bar(i), nc * (ROW + gpc * 4u));
+      floe_ptx::bulk_g2s(ring.stage(i), d.codes + (size_t)c0 * ROW, nc * ROW, ring.bar(i));
+      floe_ptx::bulk_g2s(ring.stage(i) + code_sz, d.meta + (size_t)c0 * gpc, nc * gpc * 4u,
+                         ring.bar(i));
     };
-    const uint32_t first_use = ring.use;
     if (t == 0)
-      for (uint32_t i = 0; i < n_items && i < a.ns; ++i) issue_tile(i);
+      for (uint32_t i = 0; i < n_items && i < ring.ns; ++i) issue_tile(i);
 
     // x limbs (word q of this span), shared by the CS threads of the span
     const float *xg = a.u;
@@ -391,45 +414,50 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
     for (uint32_t i = 0; i < n_items; ++i) {
       const uint32_t s = i / n_sub, k = i % n_sub;
       if (k == 0) running = 0;
-      const uint32_t u_idx = first_use + i;
-      ring.wait(u_idx);
-      const uint8_t *st = ring.stage(u_idx);
+      ring.wait(i);
+      const uint8_t *st = ring.stage(i);
       const uint32_t c0 = c_lo + k * CH;
       const uint32_t nc = min((uint32_t)CH, c_hi - c0);
       float part[CPT];
+      if (all_finite) {
+        // channels past nc read stale stage bytes: their partials are never used
 #pragma unroll
-      for (int r = 0; r < CPT; ++r) {
-        const uint32_t j = q + CS * r;
-        float acc = 0.0f;
-        if (j < nc) {
+        for (int r = 0; r < CPT; ++r) {
+          const uint32_t j = q + CS * r;
           const uint4 w4 = *reinterpret_cast<const uint4 *>(st + j * ROW + 16 * span);
           const uint32_t *meta = reinterpret_cast<const uint32_t *>(st + code_sz) + j * gpc + g0;
           const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
-          if (all_finite) {
+          float acc = 0.0f;
 #pragma unroll
-            for (int p = 0; p < GPT; ++p) {
-              int a0 = 0, a1 = 0, a2 = 0;
+          for (int p = 0; p < GPT; ++p) {
+            int a0 = 0, a1 = 0, a2 = 0;
 #pragma unroll
-              for (int ii = p * WPP; ii < (p + 1) * WPP; ++ii) {
+            for (int ii = p * WPP; ii < (p + 1) * WPP; ++ii) {
 #pragma unroll
-                for (int mm = 0; mm < 4; ++mm) {
-                  const int cb = (int)((wv[ii] >> (2 * mm)) & 0x03030303u);
-                  a0 = __dp4a(cb, (int)lw[ii][mm], a0);
-                  a1 = __dp4a(cb, (int)lw[ii][4 + mm], a1);
-                  a2 = __dp4a(cb, (int)lw[ii][8 + mm], a2);
-                }
+              for (int mm = 0; mm < 4; ++mm) {
+                const int cb = (int)((wv[ii] >> (2 * mm)) & 0x03030303u);
+                a0 = __dp4a(cb, (int)lw[ii][mm], a0);
+                a1 = __dp4a(cb, (int)lw[ii][4 + mm], a1);
+                a2 = __dp4a(cb, (int)lw[ii][8 + mm], a2);
               }
-              const int T = a2 * 65536 + a1 * 256 + a0;
-              const uint32_t mz = meta[p];
-              const float sc = __half2float(__ushort_as_half((uint16_t)(mz & 0xffffu)));
-              const float zr = __half2float(__ushort_as_half((uint16_t)(mz >> 16)));
-              acc = fmaf(sc * invS, (float)T, fmaf(zr, xpart[p], acc));
             }
-          } else {
-            acc = k1_span_f32(wv, meta, a.group_size, xg + 64 * span);
+            const int Tt = a2 * 65536 + a1 * 256 + a0;
+            const uint32_t mz = meta[p];
+            const float sc = __half2float(__ushort_as_half((uint16_t)(mz & 0xffffu)));
+            const float zr = __half2float(__ushort_as_half((uint16_t)(mz >> 16)));
+            acc = fmaf(sc * invS, (float)Tt, fmaf(zr, xpart[p], acc));
           }
+          part[r] = acc;
         }
-        part[r] = acc;
+      } else {
+#pragma unroll
+        for (int r = 0; r < CPT; ++r) {
+          const uint32_t j = q + CS * r;
+          const uint4 w4 = *reinterpret_cast<const uint4 *>(st + j * ROW + 16 * span);
+          const uint32_t *meta = reinterpret_cast<const uint32_t *>(st + code_sz) + j * gpc + g0;
+          const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
+          part[r] = j < nc ? k1_span_f32(wv, meta, a.group_size, xg + 64 * span) : 0.0f;
+        }
       }
 #pragma unroll
       for (int sft = 16, cnt = CPT / 2; cnt >= 1; sft >>= 1, cnt >>= 1) {
@@ -446,7 +474,7 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
         part[0] += __shfl_xor_sync(0xffffffffu, part[0], sft);
       if ((lane & (32 / CPT - 1)) == 0) wsum[i & 1][warp][lane / (32 / CPT)] = part[0];
       __syncthreads();  // wsum[i&1] complete; stage retired
-      if (t == 0 && i + a.ns < n_items) issue_tile(i + a.ns);
+      if (t == 0 && i + ring.ns < n_items) issue_tile(i + ring.ns);
       if (warp == 0) {
         const uint32_t j = lane;
         float v = 0.0f;
@@ -474,7 +502,6 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
         if (k + 1 == n_sub && lane == 0) a.seg_count[s * G + b] = running;
       }
     }
-    ring.use = first_use + n_items;
   }
   mark(a, 3);
   grid_sync(a.bar);
@@ -482,10 +509,10 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
   // =========================== phase C: K2 ================================
   mark(a, 4);
   {
-    const uint32_t rec_bytes = 4u * DH;
     const uint32_t nseg = a.slots * G;
-    uint32_t *prefix = reinterpret_cast<uint32_t *>(
-        smem + a.ns * a.stage_bytes + (a.has_mixing ? 4u * DH : 0u));
+    uint32_t *prefix = reinterpret_cast<uint32_t *>(smem + a.ring_bytes +
+                                                    (a.has_mixing ? 4u * DH : 0u));
+    ring = ring_make(smem, full, REC, a.ring_bytes, true);
     // seg_prefix reads seg_count written by other CTAs before the barrier
     seg_prefix(a.seg_count, nseg, prefix);
     if (b == 0) {
@@ -518,6 +545,7 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
       for (int i = 0; i < 8; ++i) y2[i] = make_float2(0.0f, 0.0f);
     }
     uint32_t batch = 0;
+    uint32_t use0 = 0;  // stage uses before this chunk
     for (uint32_t cb = begin; cb < end; cb += kK2Chunk) {
       const uint32_t n = min(kK2Chunk, end - cb);
       __syncthreads();
@@ -532,13 +560,8 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
         if (a.kept_out) a.kept_out[(size_t)s * a.di + (p - prefix[s * G])] = c;
       }
       __syncthreads();
-      const uint32_t first_use = ring.use;
       if (t == 0)
-        for (uint32_t k = 0; k < n && k < a.ns; ++k) {
-          floe_ptx::mbar_arrive_expect_tx(ring.bar(issued), rec_bytes);
-          floe_ptx::bulk_g2s(ring.stage(issued), ent_rec[k], rec_bytes, ring.bar(issued));
-          ++issued;
-        }
+        for (uint32_t k = 0; k < n && k < ring.ns; ++k) ring.issue(use0 + k, ent_rec[k], REC);
       for (uint32_t q0 = 0; q0 < n; q0 += R, ++batch) {
         uint4 dv[R][2];
         float gp[R];
@@ -547,7 +570,7 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
           gp[r] = 0.0f;
           dv[r][0] = dv[r][1] = make_uint4(0, 0, 0, 0);
           if (q0 + r < n) {
-            const uint32_t u_idx = first_use + q0 + r;
+            const uint32_t u_idx = use0 + q0 + r;
             ring.wait(u_idx);
             if (active) {
               const uint4 *rec = reinterpret_cast<const uint4 *>(ring.stage(u_idx));
@@ -566,6 +589,7 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
             }
           }
         }
+        // transposed warp reduction of R values: lanes 8r hold record r's warp sum
 #pragma unroll
         for (int sft = 16, cnt = R / 2; cnt >= 1; sft >>= 1, cnt >>= 1) {
           const bool upper = (lane & sft) != 0;
@@ -579,24 +603,25 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
 #pragma unroll
         for (int sft = 32 / R / 2; sft >= 1; sft >>= 1)
           gp[0] += __shfl_xor_sync(0xffffffffu, gp[0], sft);
-        if ((lane & (32 / R - 1)) == 0) red[batch & 1][warp][lane / (32 / R)] = gp[0];
-        __syncthreads();  // batch stages retired
+        if ((lane & (32 / R - 1)) == 0) red[warp][lane / (32 / R)] = gp[0];
+        __syncthreads();  // red complete; the batch's stages are read
         if (t == 0)
           for (int r = 0; r < R; ++r) {
-            const uint32_t nq = q0 + r + a.ns;
-            if (q0 + r < n && nq < n) {
-              floe_ptx::mbar_arrive_expect_tx(ring.bar(issued), rec_bytes);
-              floe_ptx::bulk_g2s(ring.stage(issued), ent_rec[nq], rec_bytes, ring.bar(issued));
-              ++issued;
-            }
+            const uint32_t nq = q0 + r + ring.ns;
+            if (q0 + r < n && nq < n) ring.issue(use0 + nq, ent_rec[nq], REC);
           }
+        // warp r finishes record r once: block sum, silu, scale
+        if (warp < (uint32_t)R && q0 + warp < n) {
+          float g = lane < (uint32_t)NW ? red[lane][warp] : 0.0f;
+#pragma unroll
+          for (int o = 4; o >= 1; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+          if (lane == 0) aco_s[batch & 1][warp] = silu_ref(g) * ent_scale[q0 + warp];
+        }
+        __syncthreads();  // aco_s visible
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if (q0 + r >= n) break;
-          float g = 0.0f;
-#pragma unroll
-          for (int w = 0; w < NW; ++w) g += red[batch & 1][w][r];
-          const float aco = silu_ref(g) * ent_scale[q0 + r];
+          const float aco = aco_s[batch & 1][r];
           const float2 a2 = make_float2(aco, aco);
           const __half2 *e0 = reinterpret_cast<const __half2 *>(&dv[r][0]);
           const __half2 *e1 = reinterpret_cast<const __half2 *>(&dv[r][1]);
@@ -607,7 +632,7 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
           }
         }
       }
-      ring.use = first_use + n;
+      use0 += n;
     }
     mark(a, 5);
     if (end > begin && active) {

@@ -407,16 +407,14 @@ int launch_fused(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) 
   a.stats = ws->stats;
   a.phase_ns = ws->phase_ns;
   ws->g1 = sm;
-  // ring geometry: one stage holds a K1 sub-tile, a 16 KB record or mixing rows
+  // one shared-memory ring, re-carved per phase: 4*dh-byte stages for mixing
+  // rows and gate|down records, K1-tile stages for the up projection
   const uint32_t gpc = L.dh / L.g;
-  uint32_t stage = std::max<uint32_t>(floe_k::k1_stage_bytes(L.dh, gpc), 4u * L.dh);
-  if (a.has_mixing) stage = std::max<uint32_t>(stage, L.dh * (L.mix_f16 ? 2u : 4u));
-  stage = floe_k::round_up128(stage);
-  const uint32_t ns = std::min<uint32_t>(floe_k::kFusedMaxStages, floe_k::kFusedRingBytes / stage);
-  if (ns < 2) return fail(FLOE_ERR_UNSUPPORTED, "fused path: stage of %u B too large", stage);
-  a.stage_bytes = stage;
-  a.ns = ns;
-  const uint32_t smem = ns * stage + (a.has_mixing ? 4u * L.dh : 0u) + 4u * (L.slots * sm + 1);
+  const uint32_t ring = floe_k::kFusedRingBytes;
+  if (ring / floe_k::k1_stage_bytes(L.dh, gpc) < 2 || ring / (4u * L.dh) < 4)
+    return fail(FLOE_ERR_UNSUPPORTED, "fused path: stages too large for the ring");
+  a.ring_bytes = ring;
+  const uint32_t smem = ring + (a.has_mixing ? 4u * L.dh : 0u) + 4u * (L.slots * sm + 1);
   const uint32_t gpt = L.g >= 64 ? 1u : 64u / L.g;
   void *kargs[] = {&a};
   cudaLaunchConfig_t cfg{};

@@ -7,6 +7,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <algorithm>
 #include <vector>
 
 #include "../paper_2505_05950_b200/csrc/floe_ptx.cuh"
@@ -40,6 +41,49 @@ __global__ void __launch_bounds__(256, 1) bulk_stream(const uint8_t *src, uint64
       floe_ptx::bulk_g2s(smem + (size_t)s * chunk, base + (size_t)(i + NS) * chunk, chunk,
                          &full[s]);
     }
+  }
+  if (acc == 0x12345678u) *sink = acc;
+}
+
+// Records of `rec` bytes at scattered offsets (like kept gate|down records),
+// ring of NS stages refilled R at a time after a block barrier (K2's shape).
+template <int NS, int R>
+__global__ void __launch_bounds__(256, 1) bulk_records(const uint8_t *src, const uint32_t *idx,
+                                                       uint32_t n_total, uint32_t rec,
+                                                       uint32_t *sink) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t full[NS];
+  const uint32_t begin = (uint32_t)((uint64_t)n_total * blockIdx.x / gridDim.x);
+  const uint32_t end = (uint32_t)((uint64_t)n_total * (blockIdx.x + 1) / gridDim.x);
+  const uint32_t n = end - begin;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) floe_ptx::mbar_init(&full[s], 1);
+    floe_ptx::fence_barrier_init();
+    for (uint32_t i = 0; i < n && i < (uint32_t)NS; ++i) {
+      floe_ptx::mbar_arrive_expect_tx(&full[i], rec);
+      floe_ptx::bulk_g2s(smem + (size_t)i * rec, src + (size_t)idx[begin + i] * rec, rec, &full[i]);
+    }
+  }
+  __syncthreads();
+  uint32_t acc = 0;
+  for (uint32_t i0 = 0; i0 < n; i0 += R) {
+    for (int r = 0; r < R && i0 + r < n; ++r) {
+      const uint32_t i = i0 + r, s = i % NS;
+      floe_ptx::mbar_wait(&full[s], (i / NS) & 1u);
+      const uint4 *p = reinterpret_cast<const uint4 *>(smem + (size_t)s * rec);
+      for (uint32_t k = threadIdx.x; k < rec / 16; k += 256) acc ^= p[k].x;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int r = 0; r < R; ++r) {
+        const uint32_t i = i0 + r, nx = i + NS;
+        if (i < n && nx < n) {
+          const uint32_t s = i % NS;
+          floe_ptx::mbar_arrive_expect_tx(&full[s], rec);
+          floe_ptx::bulk_g2s(smem + (size_t)s * rec, src + (size_t)idx[begin + nx] * rec, rec,
+                             &full[s]);
+        }
+      }
   }
   if (acc == 0x12345678u) *sink = acc;
 }
@@ -157,6 +201,41 @@ int main() {
     }
     float us0 = cold([&] { ldg_stream<8><<<sm, 256>>>((const uint4 *)buf, 0, sink); });
     printf("empty launch (cold): %.2f us\n", us0);
+  }
+  // K2-shaped traffic: 5760 scattered 16 KB records out of 2 x 14336 (94 MB)
+  {
+    mode = 1;
+    const uint32_t rec = 16384, pool = 2 * 14336, n = 5760;
+    std::vector<uint32_t> hidx(n);
+    uint64_t st = 12345;
+    std::vector<uint8_t> used(pool, 0);
+    for (uint32_t i = 0; i < n;) {
+      st = st * 6364136223846793005ull + 1442695040888963407ull;
+      const uint32_t c = (uint32_t)((st >> 33) % pool);
+      if (!used[c]) {
+        used[c] = 1;
+        hidx[i++] = c;
+      }
+    }
+    std::vector<uint32_t> sorted = hidx;
+    std::sort(sorted.begin(), sorted.end());
+    uint32_t *didx;
+    cudaMalloc(&didx, 4ull * n);
+    for (int variant = 0; variant < 2; ++variant) {
+      cudaMemcpy(didx, variant ? sorted.data() : hidx.data(), 4ull * n, cudaMemcpyHostToDevice);
+      auto runk = [&](auto kern, int ns, int r) {
+        const uint32_t smem = ns * rec;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        float us = cold([&] { kern<<<sm, 256, smem>>>(buf, didx, n, rec, sink); });
+        printf("records %s NS=%2d R=%d: %7.2f us (%6.1f GB/s) err=%s\n",
+               variant ? "sorted " : "random ", ns, r, us, (double)n * rec / (us * 1e-6) / 1e9,
+               cudaGetErrorString(cudaGetLastError()));
+      };
+      runk(bulk_records<8, 1>, 8, 1);
+      runk(bulk_records<8, 4>, 8, 4);
+      runk(bulk_records<12, 4>, 12, 4);
+      runk(bulk_records<12, 1>, 12, 1);
+    }
   }
   return 0;
 }
