@@ -60,6 +60,7 @@ struct FusedArgs {
   unsigned long long *stats;
   uint32_t ring_bytes;           // shared-memory ring size
   unsigned long long *phase_ns;  // nullable [grid][8]: %globaltimer at phase marks
+  uint32_t debug;                // diagnostics: bit0 skip K1 math, bit1 skip K2 math
 };
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -419,7 +420,10 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
       const uint32_t c0 = c_lo + k * CH;
       const uint32_t nc = min((uint32_t)CH, c_hi - c0);
       float part[CPT];
-      if (all_finite) {
+      if (a.debug & 1u) {
+#pragma unroll
+        for (int r = 0; r < CPT; ++r) part[r] = 0.0f;
+      } else if (all_finite) {
         // channels past nc read stale stage bytes: their partials are never used
 #pragma unroll
         for (int r = 0; r < CPT; ++r) {
@@ -572,7 +576,7 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
           if (q0 + r < n) {
             const uint32_t u_idx = use0 + q0 + r;
             ring.wait(u_idx);
-            if (active) {
+            if (active && !(a.debug & 2u)) {
               const uint4 *rec = reinterpret_cast<const uint4 *>(ring.stage(u_idx));
               const uint4 g0 = rec[t], g1 = rec[t + TPB2];
               dv[r][0] = rec[2 * TPB2 + t];

@@ -406,6 +406,13 @@ int launch_fused(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) 
   a.kept_out = L.kept_out;
   a.stats = ws->stats;
   a.phase_ns = ws->phase_ns;
+  {
+    static const uint32_t dbg = [] {
+      const char *d = std::getenv("FLOE_DEBUG_FLAGS");
+      return d ? (uint32_t)std::atoi(d) : 0u;
+    }();
+    a.debug = dbg;
+  }
   ws->g1 = sm;
   // one shared-memory ring, re-carved per phase: 4*dh-byte stages for mixing
   // rows and gate|down records, K1-tile stages for the up projection
