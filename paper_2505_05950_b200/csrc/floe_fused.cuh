@@ -69,8 +69,11 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
+constexpr int kTraceSlots = 64;  // per CTA: 0..7 phase marks, 8.. record arrivals
+
 __device__ __forceinline__ void mark(const FusedArgs &a, int k) {
-  if (a.phase_ns && threadIdx.x == 0) a.phase_ns[blockIdx.x * 8 + k] = global_ns();
+  if (a.phase_ns && threadIdx.x == 0 && k < kTraceSlots)
+    a.phase_ns[blockIdx.x * kTraceSlots + k] = global_ns();
 }
 
 __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p) {
@@ -576,6 +579,7 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
           if (q0 + r < n) {
             const uint32_t u_idx = use0 + q0 + r;
             ring.wait(u_idx);
+            if (u_idx < (uint32_t)(kTraceSlots - 8)) mark(a, 8 + (int)u_idx);
             if (active && !(a.debug & 2u)) {
               const uint4 *rec = reinterpret_cast<const uint4 *>(ring.stage(u_idx));
               const uint4 g0 = rec[t], g1 = rec[t + TPB2];

@@ -741,8 +741,8 @@ int floe_gpu_workspace_read_counters(floe_gpu_workspace *w, uint64_t *calls,
 int floe_gpu_workspace_set_phase_trace(floe_gpu_workspace *w, int enable) {
   if (!w) return fail(FLOE_ERR_INVALID, "workspace_set_phase_trace: null workspace");
   if (enable && !w->phase_ns) {
-    CK(cudaMalloc(&w->phase_ns, 8ull * 8 * device_info().sm));
-    CK(cudaMemset(w->phase_ns, 0, 8ull * 8 * device_info().sm));
+    CK(cudaMalloc(&w->phase_ns, 8ull * floe_k::kTraceSlots * device_info().sm));
+    CK(cudaMemset(w->phase_ns, 0, 8ull * floe_k::kTraceSlots * device_info().sm));
   } else if (!enable && w->phase_ns) {
     cudaFree(w->phase_ns);
     w->phase_ns = nullptr;
@@ -753,7 +753,7 @@ int floe_gpu_workspace_set_phase_trace(floe_gpu_workspace *w, int enable) {
 int floe_gpu_workspace_read_phase_trace(floe_gpu_workspace *w, uint64_t *out, uint32_t cap,
                                         uint32_t *grid) {
   if (!w || !out) return fail(FLOE_ERR_INVALID, "workspace_read_phase_trace: null argument");
-  const uint32_t n = std::min<uint32_t>(cap, 8u * device_info().sm);
+  const uint32_t n = std::min<uint32_t>(cap, (uint32_t)floe_k::kTraceSlots * device_info().sm);
   if (grid) *grid = device_info().sm;
   if (!w->phase_ns) return fail(FLOE_ERR_INVALID, "workspace_read_phase_trace: tracing is off");
   CK(cudaDeviceSynchronize());

@@ -25,6 +25,13 @@ def summarize(tag, traces, marks):
         print(f"   {name:28s} mean {d.mean():7.2f}  min {d.min():7.2f}  max {d.max():7.2f} us")
     end = (T[:, :, 5].max(1) - t0[:, 0]) / 1e3
     print(f"   first start -> last phase-C end: {end.mean():7.2f} us")
+    # phase-C record arrivals (after each wait) relative to phase-C start, CTA 0 and 100
+    for cta in (0, 100):
+        arr = T[-1, cta, 8:]
+        base = T[-1, cta, 4]
+        rel = [(x - base) / 1e3 for x in arr if x > base]
+        print(f"   CTA {cta:3d} phase-C record arrivals (us): " +
+              " ".join(f"{v:.1f}" for v in rel[:40]))
 
 
 def main():
