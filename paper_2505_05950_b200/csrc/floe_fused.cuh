@@ -120,11 +120,12 @@ __device__ __forceinline__ Ring ring_make(uint8_t *base, uint64_t *full, uint32_
                                           uint32_t ring_bytes, bool reinit) {
   Ring r{base, full, stage_bytes, min(kFusedMaxStages, ring_bytes / stage_bytes)};
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (uint32_t s = 0; s < kFusedMaxStages; ++s) {
-      if (reinit) asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(floe_ptx::smem_u32(&full[s])) : "memory");
-      floe_ptx::mbar_init(&full[s], 1);
-    }
+  if (threadIdx.x < kFusedMaxStages) {  // one barrier per thread
+    const uint32_t s = threadIdx.x;
+    if (reinit)
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(floe_ptx::smem_u32(&full[s]))
+                   : "memory");
+    floe_ptx::mbar_init(&full[s], 1);
     floe_ptx::fence_barrier_init();
   }
   __syncthreads();
@@ -163,6 +164,8 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
   __shared__ float aco_s[2][R];
   __shared__ const __half *ent_rec[kK2Chunk];
   __shared__ float ent_scale[kK2Chunk];
+  __shared__ uint32_t own_cnt_s[kMaxSlots];
+  __shared__ uint32_t plan_s[4];  // T, own_b, d_b, D_b
 
   const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const uint32_t G = gridDim.x, b = blockIdx.x;
@@ -506,35 +509,53 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
           a.kept_v[o] = v;
         }
         running += __popc(bal);
-        if (k + 1 == n_sub && lane == 0) a.seg_count[s * G + b] = running;
+        if (k + 1 == n_sub && lane == 0) {
+          a.seg_count[s * G + b] = running;
+          own_cnt_s[s] = running;
+        }
       }
     }
   }
-  mark(a, 3);
-  grid_sync(a.bar);
 
   // =========================== phase C: K2 ================================
-  mark(a, 4);
+  // Own-first balanced assignment.  Target per CTA t_b = T*(b+1)/G - T*b/G
+  // kept entries; CTA b keeps own_b = min(n_b, t_b, kK2Chunk) of its OWN
+  // entries (so their records can be prefetched BEFORE the barrier) and
+  // fills the deficit t_b - own_b from the pool of every CTA's surplus, in a
+  // fixed global order.  Stage uses: [0, E0) own items (prefetched first P,
+  // processed iff < own_b), then pool items in chunks.
   {
-    const uint32_t nseg = a.slots * G;
-    uint32_t *prefix = reinterpret_cast<uint32_t *>(smem + a.ring_bytes +
-                                                    (a.has_mixing ? 4u * DH : 0u));
-    ring = ring_make(smem, full, REC, a.ring_bytes, true);
-    // seg_prefix reads seg_count written by other CTAs before the barrier
-    seg_prefix(a.seg_count, nseg, prefix);
-    if (b == 0) {
-      if (t < a.slots && a.n_kept_out) a.n_kept_out[t] = prefix[(t + 1) * G] - prefix[t * G];
-      if (t == 0 && a.stats) {
-        atomicAdd(&a.stats[0], 1ull);
-        atomicAdd(&a.stats[1], (unsigned long long)prefix[nseg]);
-      }
-    }
-    const uint32_t total = prefix[nseg];
-    const uint32_t begin = (uint32_t)(((uint64_t)total * b) / G);
-    const uint32_t end = (uint32_t)(((uint64_t)total * (b + 1)) / G);
     constexpr int TPB2 = DH / 16;  // threads owning 16 elements each
-    float2 x2[8], y2[8];
     const bool active = t < (uint32_t)TPB2;  // dh = 2048 uses half the CTA
+    __syncthreads();  // own_cnt_s complete, last K1 stage retired
+    ring = ring_make(smem, full, REC, a.ring_bytes, true);
+    uint32_t n_own = 0;
+    for (uint32_t s = 0; s < a.slots; ++s) n_own += own_cnt_s[s];
+    const uint32_t c_lo = seg_begin(a.di, b, G);
+    const uint32_t n_res = min(n_own, kK2Chunk);
+    // own entry j -> (slot, position in the slot's segment)
+    auto own_entry = [&](uint32_t j, uint32_t &s_out, size_t &o_out) {
+      uint32_t s = 0;
+      while (s + 1 < a.slots && j >= own_cnt_s[s]) {
+        j -= own_cnt_s[s];
+        ++s;
+      }
+      s_out = s;
+      o_out = (size_t)s * a.di + c_lo + j;
+    };
+    for (uint32_t j = t; j < n_res; j += TPB) {
+      uint32_t s;
+      size_t o;
+      own_entry(j, s, o);
+      const uint32_t c = __ldcg(&a.kept_idx[o]);
+      ent_rec[j] = rec_s[s] + (size_t)c * 2 * DH;
+      ent_scale[j] = __ldcg(&a.kept_v[o]) * w_s[s];
+    }
+    __syncthreads();
+    const uint32_t P = min(n_res, ring.ns);  // speculative prefetch, before the barrier
+    if (t == 0)
+      for (uint32_t k = 0; k < P; ++k) ring.issue(k, ent_rec[k], REC);
+    float2 x2[8], y2[8];
     {
       const uint32_t tt = active ? t : 0;
       const float4 *xa = reinterpret_cast<const float4 *>(a.u + 8 * tt);
@@ -551,24 +572,87 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) y2[i] = make_float2(0.0f, 0.0f);
     }
-    uint32_t batch = 0;
-    uint32_t use0 = 0;  // stage uses before this chunk
-    for (uint32_t cb = begin; cb < end; cb += kK2Chunk) {
-      const uint32_t n = min(kK2Chunk, end - cb);
-      __syncthreads();
-      for (uint32_t qq = t; qq < n; qq += TPB) {
-        const uint32_t p = cb + qq;
-        const uint32_t idx = seg_find(prefix, nseg, p);
-        const uint32_t s = idx / G, bb = idx % G;
-        const size_t o = (size_t)s * a.di + seg_begin(a.di, bb, G) + (p - prefix[idx]);
-        const uint32_t c = __ldcg(&a.kept_idx[o]);
-        ent_rec[qq] = rec_s[s] + (size_t)c * 2 * DH;
-        ent_scale[qq] = __ldcg(&a.kept_v[o]) * w_s[s];
-        if (a.kept_out) a.kept_out[(size_t)s * a.di + (p - prefix[s * G])] = c;
+    mark(a, 3);
+    grid_sync(a.bar);
+    mark(a, 4);
+
+    // ---- the plan: per-CTA totals n_bb, targets, surplus/deficit prefixes
+    uint32_t *S = reinterpret_cast<uint32_t *>(smem + a.ring_bytes +
+                                               (a.has_mixing ? 4u * DH : 0u));  // [G+1]
+    uint32_t *D = S + (G + 1);                                                  // [G+1]
+    uint32_t *NB = D + (G + 1);                                                 // [G]
+    uint32_t *SU = NB + G;                                                      // [G]
+    for (uint32_t bb = t; bb < G; bb += TPB) {
+      uint32_t n = 0;
+      for (uint32_t s = 0; s < a.slots; ++s) n += __ldcg(&a.seg_count[s * G + bb]);
+      NB[bb] = n;
+    }
+    __syncthreads();
+    seg_prefix(NB, G, S);  // S[bb] = sum_{<bb} n  (reused below)
+    const uint32_t T = S[G];
+    auto plan = [&](uint32_t bb, uint32_t &own, uint32_t &sur, uint32_t &def) {
+      const uint32_t tb = (uint32_t)(((uint64_t)T * (bb + 1)) / G - ((uint64_t)T * bb) / G);
+      const uint32_t n = NB[bb];
+      own = min(min(n, tb), kK2Chunk);
+      sur = n - own;
+      def = tb - own;
+    };
+    __syncthreads();
+    for (uint32_t bb = t; bb < G; bb += TPB) {
+      uint32_t own, sur, def;
+      plan(bb, own, sur, def);
+      D[bb] = def;  // deficits (prefix-summed below)
+      SU[bb] = sur;
+    }
+    __syncthreads();
+    // prefix of deficits into D (in place via S as scratch is not possible):
+    seg_prefix(D, G, S);  // S = deficit prefix
+    __syncthreads();
+    for (uint32_t bb = t; bb <= G; bb += TPB) D[bb] = S[bb];
+    __syncthreads();
+    seg_prefix(SU, G, S);  // S = surplus prefix
+    if (t == 0) {
+      uint32_t own, sur, def;
+      plan(b, own, sur, def);
+      plan_s[0] = T;
+      plan_s[1] = own;
+      plan_s[2] = def;
+      plan_s[3] = D[b];
+    }
+    __syncthreads();
+    const uint32_t own_b = plan_s[1], d_b = plan_s[2], D_b = plan_s[3];
+    if (b == 0) {
+      if (t == 0 && a.stats) {
+        atomicAdd(&a.stats[0], 1ull);
+        atomicAdd(&a.stats[1], (unsigned long long)T);
       }
-      __syncthreads();
+      if (warp < a.slots && a.n_kept_out) {
+        uint32_t n = 0;
+        for (uint32_t bb = lane; bb < G; bb += 32) n += __ldcg(&a.seg_count[warp * G + bb]);
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+        if (lane == 0) a.n_kept_out[warp] = n;
+      }
+    }
+    if (a.kept_out && warp < a.slots) {
+      // own segment's ids -> ascending per-slot position (prefix over lower CTAs)
+      uint32_t base = 0;
+      for (uint32_t bb = lane; bb < b; bb += 32) base += __ldcg(&a.seg_count[warp * G + bb]);
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) base += __shfl_xor_sync(0xffffffffu, base, o);
+      const uint32_t cnt = own_cnt_s[warp];
+      for (uint32_t j = lane; j < cnt; j += 32)
+        a.kept_out[(size_t)warp * a.di + base + j] =
+            __ldcg(&a.kept_idx[(size_t)warp * a.di + c_lo + j]);
+    }
+
+    // ---- consume a run of n items at stage uses [ub, ub+n) from ent[eb..]
+    uint32_t batch = 0;
+    auto run_items = [&](uint32_t ub, uint32_t n, uint32_t eb, uint32_t proc_end,
+                         uint32_t pre_issued) {
       if (t == 0)
-        for (uint32_t k = 0; k < n && k < ring.ns; ++k) ring.issue(use0 + k, ent_rec[k], REC);
+        for (uint32_t k = pre_issued; k < n && k < ring.ns; ++k)
+          ring.issue(ub + k, ent_rec[eb + k], REC);
       for (uint32_t q0 = 0; q0 < n; q0 += R, ++batch) {
         uint4 dv[R][2];
         float gp[R];
@@ -576,11 +660,12 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
         for (int r = 0; r < R; ++r) {
           gp[r] = 0.0f;
           dv[r][0] = dv[r][1] = make_uint4(0, 0, 0, 0);
-          if (q0 + r < n) {
-            const uint32_t u_idx = use0 + q0 + r;
+          const uint32_t k = q0 + r;
+          if (k < n) {
+            const uint32_t u_idx = ub + k;
             ring.wait(u_idx);
             if (u_idx < (uint32_t)(kTraceSlots - 8)) mark(a, 8 + (int)u_idx);
-            if (active && !(a.debug & 2u)) {
+            if (active && k < proc_end && !(a.debug & 2u)) {
               const uint4 *rec = reinterpret_cast<const uint4 *>(ring.stage(u_idx));
               const uint4 g0 = rec[t], g1 = rec[t + TPB2];
               dv[r][0] = rec[2 * TPB2 + t];
@@ -616,19 +701,20 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
         if (t == 0)
           for (int r = 0; r < R; ++r) {
             const uint32_t nq = q0 + r + ring.ns;
-            if (q0 + r < n && nq < n) ring.issue(use0 + nq, ent_rec[nq], REC);
+            if (q0 + r < n && nq < n) ring.issue(ub + nq, ent_rec[eb + nq], REC);
           }
         // warp r finishes record r once: block sum, silu, scale
-        if (warp < (uint32_t)R && q0 + warp < n) {
+        if (warp < (uint32_t)R && q0 + warp < n && q0 + warp < proc_end) {
           float g = lane < (uint32_t)NW ? red[lane][warp] : 0.0f;
 #pragma unroll
           for (int o = 4; o >= 1; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
-          if (lane == 0) aco_s[batch & 1][warp] = silu_ref(g) * ent_scale[q0 + warp];
+          if (lane == 0) aco_s[batch & 1][warp] = silu_ref(g) * ent_scale[eb + q0 + warp];
         }
         __syncthreads();  // aco_s visible
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          if (q0 + r >= n) break;
+          const uint32_t k = q0 + r;
+          if (k >= n || k >= proc_end) break;
           const float aco = aco_s[batch & 1][r];
           const float2 a2 = make_float2(aco, aco);
           const __half2 *e0 = reinterpret_cast<const __half2 *>(&dv[r][0]);
@@ -640,10 +726,38 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
           }
         }
       }
-      use0 += n;
+    };
+    // own items: [0, E0), processed iff < own_b (prefetched surplus is drained)
+    const uint32_t E0 = max(P, own_b);
+    run_items(0, E0, 0, own_b, P);
+    // pool items in chunks of kK2Chunk
+    uint32_t ub = E0;
+    for (uint32_t q = 0; q < d_b; q += kK2Chunk) {
+      const uint32_t n = min(kK2Chunk, d_b - q);
+      __syncthreads();  // ent_* free
+      for (uint32_t k = t; k < n; k += TPB) {
+        const uint32_t pi = D_b + q + k;        // pool index
+        const uint32_t bb = seg_find(S, G, pi);  // source CTA
+        uint32_t own_src, sur_src, def_src;
+        plan(bb, own_src, sur_src, def_src);
+        uint32_t j = own_src + (pi - S[bb]);  // entry in bb's own list
+        uint32_t s = 0;
+        for (; s + 1 < a.slots; ++s) {
+          const uint32_t cs = __ldcg(&a.seg_count[s * G + bb]);
+          if (j < cs) break;
+          j -= cs;
+        }
+        const size_t o = (size_t)s * a.di + seg_begin(a.di, bb, G) + j;
+        const uint32_t c = __ldcg(&a.kept_idx[o]);
+        ent_rec[k] = rec_s[s] + (size_t)c * 2 * DH;
+        ent_scale[k] = __ldcg(&a.kept_v[o]) * w_s[s];
+      }
+      __syncthreads();
+      run_items(ub, n, 0, n, 0);
+      ub += n;
     }
     mark(a, 5);
-    if (end > begin && active) {
+    if (own_b + d_b > 0 && active) {
       float *ya = a.y + 8 * t, *yb = a.y + 8 * (t + TPB2);
       red_add_v4(ya, y2[0].x, y2[0].y, y2[1].x, y2[1].y);
       red_add_v4(ya + 4, y2[2].x, y2[2].y, y2[3].x, y2[3].y);

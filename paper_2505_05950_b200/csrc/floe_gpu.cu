@@ -421,7 +421,7 @@ int launch_fused(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) 
   if (ring / floe_k::k1_stage_bytes(L.dh, gpc) < 2 || ring / (4u * L.dh) < 4)
     return fail(FLOE_ERR_UNSUPPORTED, "fused path: stages too large for the ring");
   a.ring_bytes = ring;
-  const uint32_t smem = ring + (a.has_mixing ? 4u * L.dh : 0u) + 4u * (L.slots * sm + 1);
+  const uint32_t smem = ring + (a.has_mixing ? 4u * L.dh : 0u) + 4u * (4 * sm + 2);  // plan arrays
   const uint32_t gpt = L.g >= 64 ? 1u : 64u / L.g;
   void *kargs[] = {&a};
   cudaLaunchConfig_t cfg{};
