@@ -90,7 +90,12 @@ __device__ __forceinline__ void grid_sync(unsigned long long *bar) {
     const unsigned long long g = gridDim.x;
     const unsigned long long old = atomicAdd(bar, 1ull);
     const unsigned long long target = (old / g + 1) * g;
-    while (ld_acquire_u64(bar) < target) __nanosleep(20);
+    const unsigned long long t0 = global_ns();
+    for (uint32_t it = 1; ld_acquire_u64(bar) < target; ++it) {
+      __nanosleep(20);
+      if ((it & 1023u) == 0 && global_ns() - t0 > floe_ptx::kWatchdogNs)
+        floe_ptx::watchdog_fire("grid barrier", (uint32_t)(target / g), (uint32_t)(old % g));
+    }
     __threadfence();
   }
   __syncthreads();
@@ -105,10 +110,10 @@ constexpr int kMaxGridPerWarp = 8;  // grid <= 256 CTAs
 struct Ring {
   uint8_t *base;
   uint64_t *full;
-  uint32_t stage_bytes, ns;
+  uint32_t stage_bytes, ns, tag;  // tag: phase id for the watchdog
   __device__ uint8_t *stage(uint32_t u) const { return base + (u % ns) * stage_bytes; }
   __device__ uint64_t *bar(uint32_t u) const { return &full[u % ns]; }
-  __device__ void wait(uint32_t u) const { floe_ptx::mbar_wait(bar(u), (u / ns) & 1u); }
+  __device__ void wait(uint32_t u) const { floe_ptx::mbar_wait(bar(u), (u / ns) & 1u, tag | u); }
   __device__ void issue(uint32_t u, const void *src, uint32_t bytes) const {
     floe_ptx::mbar_arrive_expect_tx(bar(u), bytes);
     floe_ptx::bulk_g2s(stage(u), src, bytes, bar(u));
@@ -117,8 +122,8 @@ struct Ring {
 
 // Re-carve the ring (all previous copies consumed): fresh barriers.
 __device__ __forceinline__ Ring ring_make(uint8_t *base, uint64_t *full, uint32_t stage_bytes,
-                                          uint32_t ring_bytes, bool reinit) {
-  Ring r{base, full, stage_bytes, min(kFusedMaxStages, ring_bytes / stage_bytes)};
+                                          uint32_t ring_bytes, bool reinit, uint32_t tag) {
+  Ring r{base, full, stage_bytes, min(kFusedMaxStages, ring_bytes / stage_bytes), tag};
   __syncthreads();
   if (threadIdx.x < kFusedMaxStages) {  // one barrier per thread
     const uint32_t s = threadIdx.x;
@@ -179,7 +184,7 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
   // expert descriptors of the whole layer, fetched once (hidden behind phase A)
   const uint32_t n_table = a.has_mixing ? a.n_experts : a.slots;
   if (t < n_table) table_s[t] = a.table[t];
-  Ring ring = ring_make(smem, full, REC, a.ring_bytes, false);
+  Ring ring = ring_make(smem, full, REC, a.ring_bytes, false, 1u << 24);
 
   // =========================== phase A: mixing ===========================
   if (a.has_mixing) {
@@ -321,7 +326,7 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
     const uint32_t n_items = n_sub * a.slots;
     const uint32_t gpc = DH / a.group_size;
     const uint32_t code_sz = round_up128(CH * ROW);
-    ring = ring_make(smem, full, k1_stage_bytes(DH, gpc), a.ring_bytes, true);
+    ring = ring_make(smem, full, k1_stage_bytes(DH, gpc), a.ring_bytes, true, 2u << 24);
     auto issue_tile = [&](uint32_t i) {  // item i = (slot, sub-tile)
       const uint32_t s = i / n_sub, k = i % n_sub;
       const uint32_t c0 = c_lo + k * CH, nc = min((uint32_t)CH, c_hi - c0);
@@ -528,7 +533,7 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
     constexpr int TPB2 = DH / 16;  // threads owning 16 elements each
     const bool active = t < (uint32_t)TPB2;  // dh = 2048 uses half the CTA
     __syncthreads();  // own_cnt_s complete, last K1 stage retired
-    ring = ring_make(smem, full, REC, a.ring_bytes, true);
+    ring = ring_make(smem, full, REC, a.ring_bytes, true, 3u << 24);
     uint32_t n_own = 0;
     for (uint32_t s = 0; s < a.slots; ++s) n_own += own_cnt_s[s];
     const uint32_t c_lo = seg_begin(a.di, b, G);

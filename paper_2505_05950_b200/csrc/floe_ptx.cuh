@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 
 namespace floe_ptx {
 
@@ -50,8 +51,29 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
   return ok != 0;
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) {
+// Watchdog: a wait that has not completed after kWatchdogNs is a protocol
+// bug (a copy never issued, a barrier count mismatch).  Report the site and
+// trap so the launch fails loudly instead of hanging the device.
+constexpr unsigned long long kWatchdogNs = 4000000000ull;
+
+__device__ __forceinline__ unsigned long long now_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __noinline__ void watchdog_fire(const char *what, uint32_t tag, uint32_t parity) {
+  printf("floe watchdog: %s stuck (cta %u thread %u tag %u parity %u)\n", what, blockIdx.x,
+         threadIdx.x, tag, parity);
+  __trap();
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity, uint32_t tag = 0) {
+  if (mbar_try_wait(bar, parity)) return;
+  const unsigned long long t0 = now_ns();
+  for (uint32_t it = 1;; ++it) {
+    if (mbar_try_wait(bar, parity)) return;
+    if ((it & 1023u) == 0 && now_ns() - t0 > kWatchdogNs) watchdog_fire("mbarrier", tag, parity);
   }
 }
 

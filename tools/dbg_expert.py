@@ -8,6 +8,7 @@ q = O.quantize(u, 2, 64); v = O.qgemv_channels(q, dh, x); t = O.calibrate_thresh
 e = fb.GpuExpert(dh, di, 2, 64, q.codes, q.scales, q.zeros, gate=g, down=d, threshold=t)
 ws = fb.Workspace(dh, di)
 xd = torch.from_numpy(x).cuda()
+print("start", flush=True)
 for outputs in (False, True):
     kw = {}
     if outputs:
