@@ -105,36 +105,50 @@ constexpr uint32_t kFusedMaxStages = 24;
 constexpr uint32_t kFusedRingBytes = 168 * 1024;
 constexpr int kMaxGridPerWarp = 8;  // grid <= 256 CTAs
 
-// Ring of bulk-copy stages in dynamic shared memory.  `issued` is thread 0's
-// count of copies issued; uses are consumed in issue order.
+// Ring of bulk-copy stages in dynamic shared memory.  The kFusedMaxStages
+// mbarriers are initialised ONCE per launch; each phase re-carves the ring
+// with its own stage size and continues every barrier's phase sequence:
+// `par` bit s is the parity of barrier s's completed phases when the current
+// carving started, so use u waits for parity (u / ns + par_s) & 1.
 struct Ring {
   uint8_t *base;
   uint64_t *full;
-  uint32_t stage_bytes, ns, tag;  // tag: phase id for the watchdog
+  uint32_t stage_bytes, ns, tag, par;  // tag: phase id for the watchdog
   __device__ uint8_t *stage(uint32_t u) const { return base + (u % ns) * stage_bytes; }
   __device__ uint64_t *bar(uint32_t u) const { return &full[u % ns]; }
-  __device__ void wait(uint32_t u) const { floe_ptx::mbar_wait(bar(u), (u / ns) & 1u, tag | u); }
+  __device__ void wait(uint32_t u) const {
+    floe_ptx::mbar_wait(bar(u), ((u / ns) + (par >> (u % ns))) & 1u, tag | u);
+  }
   __device__ void issue(uint32_t u, const void *src, uint32_t bytes) const {
     floe_ptx::mbar_arrive_expect_tx(bar(u), bytes);
     floe_ptx::bulk_g2s(stage(u), src, bytes, bar(u));
   }
 };
 
-// Re-carve the ring (all previous copies consumed): fresh barriers.
-__device__ __forceinline__ Ring ring_make(uint8_t *base, uint64_t *full, uint32_t stage_bytes,
-                                          uint32_t ring_bytes, bool reinit, uint32_t tag) {
-  Ring r{base, full, stage_bytes, min(kFusedMaxStages, ring_bytes / stage_bytes), tag};
-  __syncthreads();
-  if (threadIdx.x < kFusedMaxStages) {  // one barrier per thread
-    const uint32_t s = threadIdx.x;
-    if (reinit)
-      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(floe_ptx::smem_u32(&full[s]))
-                   : "memory");
-    floe_ptx::mbar_init(&full[s], 1);
+__device__ __forceinline__ uint32_t ring_ns(uint32_t stage_bytes, uint32_t ring_bytes) {
+  return min(kFusedMaxStages, ring_bytes / stage_bytes);
+}
+
+// First carving: initialise the barriers.
+__device__ __forceinline__ Ring ring_init(uint8_t *base, uint64_t *full, uint32_t stage_bytes,
+                                          uint32_t ring_bytes, uint32_t tag) {
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < kFusedMaxStages; ++s) floe_ptx::mbar_init(&full[s], 1);
     floe_ptx::fence_barrier_init();
   }
   __syncthreads();
-  return r;
+  return Ring{base, full, stage_bytes, ring_ns(stage_bytes, ring_bytes), tag, 0u};
+}
+
+// Re-carve after the previous carving's `used` stage uses were all issued and
+// waited (block-uniform count): no barrier re-initialisation.
+__device__ __forceinline__ Ring ring_next(const Ring &prev, uint32_t used, uint32_t stage_bytes,
+                                          uint32_t ring_bytes, uint32_t tag) {
+  uint32_t par = prev.par;
+  for (uint32_t s = 0; s < prev.ns && s < used; ++s)
+    par ^= (((used - 1 - s) / prev.ns + 1) & 1u) << s;
+  __syncthreads();  // previous stages fully read before they are refilled
+  return Ring{prev.base, prev.full, stage_bytes, ring_ns(stage_bytes, ring_bytes), tag, par};
 }
 
 // ---------------------------------------------------------------------------
@@ -184,7 +198,8 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
   // expert descriptors of the whole layer, fetched once (hidden behind phase A)
   const uint32_t n_table = a.has_mixing ? a.n_experts : a.slots;
   if (t < n_table) table_s[t] = a.table[t];
-  Ring ring = ring_make(smem, full, REC, a.ring_bytes, false, 1u << 24);
+  Ring ring = ring_init(smem, full, REC, a.ring_bytes, 1u << 24);
+  uint32_t ring_used = 0;  // stage uses of the current carving
 
   // =========================== phase A: mixing ===========================
   if (a.has_mixing) {
@@ -192,6 +207,7 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
     const uint32_t rps = REC / row_bytes;  // rows per stage (2 for f16, 1 for f32)
     const uint32_t r_lo = seg_begin(DH, b, G), r_hi = seg_begin(DH, b + 1, G);
     const uint32_t n_items = (r_hi - r_lo + rps - 1) / rps;
+    ring_used = n_items;
     const T *m = static_cast<const T *>(a.mixing);
     const uint32_t per_round = min(NW / rps, ring.ns / 2);  // stages per block barrier
     auto issue_rows = [&](uint32_t i) {
@@ -326,7 +342,8 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
     const uint32_t n_items = n_sub * a.slots;
     const uint32_t gpc = DH / a.group_size;
     const uint32_t code_sz = round_up128(CH * ROW);
-    ring = ring_make(smem, full, k1_stage_bytes(DH, gpc), a.ring_bytes, true, 2u << 24);
+    ring = ring_next(ring, ring_used, k1_stage_bytes(DH, gpc), a.ring_bytes, 2u << 24);
+    ring_used = n_items;
     auto issue_tile = [&](uint32_t i) {  // item i = (slot, sub-tile)
       const uint32_t s = i / n_sub, k = i % n_sub;
       const uint32_t c0 = c_lo + k * CH, nc = min((uint32_t)CH, c_hi - c0);
@@ -533,7 +550,7 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
     constexpr int TPB2 = DH / 16;  // threads owning 16 elements each
     const bool active = t < (uint32_t)TPB2;  // dh = 2048 uses half the CTA
     __syncthreads();  // own_cnt_s complete, last K1 stage retired
-    ring = ring_make(smem, full, REC, a.ring_bytes, true, 3u << 24);
+    ring = ring_next(ring, ring_used, REC, a.ring_bytes, 3u << 24);
     uint32_t n_own = 0;
     for (uint32_t s = 0; s < a.slots; ++s) n_own += own_cnt_s[s];
     const uint32_t c_lo = seg_begin(a.di, b, G);
