@@ -340,6 +340,10 @@ __global__ void __launch_bounds__(256, 1) floe_fused(const FusedArgs a) {
     const uint32_t c_lo = seg_begin(a.di, b, G), c_hi = seg_begin(a.di, b + 1, G);
     const uint32_t n_sub = (c_hi - c_lo + CH - 1) / CH;
     const uint32_t n_items = n_sub * a.slots;
+    if (n_sub == 0 && t < a.slots) {  // di < grid: an empty segment still publishes its count
+      a.seg_count[t * G + b] = 0;
+      own_cnt_s[t] = 0;
+    }
     const uint32_t gpc = DH / a.group_size;
     const uint32_t code_sz = round_up128(CH * ROW);
     ring = ring_next(ring, ring_used, k1_stage_bytes(DH, gpc), a.ring_bytes, 2u << 24);

@@ -275,3 +275,16 @@ def test_acceptance_check1_gpu(fb, torch):
         out0 = run(fb, torch, e, ws, x, 256)
         dense = O.expert_forward_dense(64, 256, gate, O.dequantize(q), down, x)
         assert O.rel_l2(out0["y"], dense) <= 1e-3
+
+
+@pytest.mark.parametrize("dh", [2048, 4096])
+def test_small_di_after_large_di_shared_workspace(fb, torch, dh):
+    """di < grid leaves CTAs without channels; their segment counts must be
+    rewritten every call, not inherited from an earlier, larger call."""
+    ws = fb.Workspace(dh, 4096)
+    for di in (4096, 64, 100, 4096, 37 * 16):
+        c = Case(dh, di, 7 + di, 8)
+        out = run(fb, torch, c.upload(fb), ws, c.x, di)
+        diff = check_v_mask(c, out)
+        if len(diff) == 0:
+            assert O.rel_l2(out["y"], c.ref_y()) <= Y_REF_TOL
