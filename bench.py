@@ -262,6 +262,9 @@ def run_ours(args, rank, world, local):
         "k1_up_threshold": TOPK * (CODE_BYTES + META_BYTES) + 4 * DH,
         "k2_gate_down": kept_per_step * REC_BYTES + 2 * 4 * DH,
     }
+    layer_bytes = sum(stage_bytes.values())
+    stage_bytes["fused"] = layer_bytes  # whole layer in one launch
+    prof = {k: p for k, p in prof.items() if p["launches"] > 0}
     stage = {}
     for k, p in prof.items():
         avg_ms = p["ms"] / max(p["launches"], 1)
@@ -281,7 +284,6 @@ def run_ours(args, rank, world, local):
                 "frac": round(d["gbs"] / hbm_peak, 4) if d["gbs"] else None,
                 "traffic": traffic, "algorithmic_bytes_per_launch": d["bytes"],
                 "avg_launch_us": d["avg_us"]}
-    layer_bytes = sum(stage_bytes.values())
     step_mean_ms = my_ms / args.steps
 
     # ---------------- config 1: single expert (expert_ffn) ----------------
@@ -325,7 +327,7 @@ def run_ours(args, rank, world, local):
         "stages": stage,
         "expert_ffn": expert_ffn,
         "e2e": e2e,
-        "gpu_launches": 4 * args.steps,
+        "gpu_launches": sum(p["launches"] for p in prof.values()),
         "clocks": clocks,
         "wall_s_timed_region": round(wall_s, 4),
         "setup_s": round(setup_s, 2),
@@ -364,20 +366,24 @@ def run_expert(fb, torch, args, flush, stream, hbm_peak):
     ws.read_profile()
     time_steps(torch, step, args.steps, flush, stream)
     prof = ws.read_profile()
-    k1 = prof["k1_up_threshold"]["ms"] / max(prof["k1_up_threshold"]["launches"], 1)
-    k2 = prof["k2_gate_down"]["ms"] / max(prof["k2_gate_down"]["launches"], 1)
     bytes_tok = CODE_BYTES + META_BYTES + n_kept * REC_BYTES + 8 * DH
     mean_ms = sum(ms) / len(ms)
     gbs = bytes_tok / (mean_ms * 1e-3) / 1e9
+    kernels = {}
+    for k, p in prof.items():
+        if p["launches"]:
+            avg = p["ms"] / p["launches"]
+            b = {"k1_up_threshold": CODE_BYTES + META_BYTES + 4 * DH,
+                 "k2_gate_down": n_kept * REC_BYTES + 8 * DH, "fused": bytes_tok}.get(k)
+            kernels[k] = {"avg_us": round(avg * 1e3, 3),
+                          "gbs": round(b / (avg * 1e-3) / 1e9, 1) if b and avg > 0 else None}
     return {"workload": "config1: seeded_expert(4096,14336,99), INT2 g64, k=0.8, batch 1",
             "value": round(1e3 / mean_ms, 1), "unit": "expert-tokens/s",
             "us_per_expert_token": round(mean_ms * 1e3, 3), "kept": n_kept,
             "threshold": round(t, 6), "bytes_per_expert_token": bytes_tok,
             "achieved": round(gbs, 1), "peak": hbm_peak, "unit_bw": "GB/s",
             "frac": round(gbs / hbm_peak, 4),
-            "k1_us": round(k1 * 1e3, 3), "k2_us": round(k2 * 1e3, 3),
-            "k1_gbs": round((CODE_BYTES + META_BYTES + 4 * DH) / (k1 * 1e-3) / 1e9, 1),
-            "k2_gbs": round((n_kept * REC_BYTES + 8 * DH) / (k2 * 1e-3) / 1e9, 1)}
+            "kernels": kernels}
 
 
 # ------------------------------------------------------------------ reference arm

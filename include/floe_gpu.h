@@ -216,7 +216,8 @@ int floe_gpu_workspace_read_counters(floe_gpu_workspace *ws, uint64_t *calls,
 /* Per-stage CUDA-event timing: when enabled, forward calls record an event
  * before and after every kernel on the launching stream and accumulate the
  * elapsed device time per stage.  Stages: 0 mixing, 1 route, 2 K1 (up GEMV +
- * threshold), 3 K2 (gate/down).  read synchronises; ms[4], launches[4]. */
+ * threshold), 3 K2 (gate/down), 4 the fused persistent kernel (whole
+ * expert/layer call in one launch).  read synchronises; ms[5], launches[5]. */
 int floe_gpu_workspace_set_profiling(floe_gpu_workspace *ws, int enable);
 int floe_gpu_workspace_read_profile(floe_gpu_workspace *ws, double *ms,
                                     uint64_t *launches);

@@ -189,7 +189,7 @@ class Workspace:
 
     __del__ = close
 
-    STAGES = ("mixing", "route", "k1_up_threshold", "k2_gate_down")
+    STAGES = ("mixing", "route", "k1_up_threshold", "k2_gate_down", "fused")
 
     def reset_counters(self, stream=None):
         _check(lib().floe_gpu_workspace_reset_counters(self.handle, _stream(stream)))
@@ -215,8 +215,8 @@ class Workspace:
         return out[: 64 * grid.value].reshape(grid.value, 64)
 
     def read_profile(self) -> dict:
-        ms = (ct.c_double * 4)()
-        n = (ct.c_uint64 * 4)()
+        ms = (ct.c_double * 5)()
+        n = (ct.c_uint64 * 5)()
         _check(lib().floe_gpu_workspace_read_profile(self.handle, ms, n))
         return {k: dict(ms=ms[i], launches=n[i]) for i, k in enumerate(self.STAGES)}
 

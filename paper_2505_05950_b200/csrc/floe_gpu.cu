@@ -122,7 +122,7 @@ struct floe_gpu_expert {
   bool fast_k1 = false, fast_k2 = false;
 };
 
-enum { kStageMixing = 0, kStageRoute = 1, kStageK1 = 2, kStageK2 = 3, kStages = 4 };
+enum { kStageMixing = 0, kStageRoute = 1, kStageK1 = 2, kStageK2 = 3, kStageFused = 4, kStages = 5 };
 
 struct floe_gpu_workspace {
   uint32_t dh = 0, di = 0, slots = 0;
@@ -151,8 +151,8 @@ struct floe_gpu_workspace {
     cudaEvent_t a, b;
   };
   std::vector<Pending> pending;
-  double ms[kStages] = {0, 0, 0, 0};
-  uint64_t launches[kStages] = {0, 0, 0, 0};
+  double ms[kStages] = {};
+  uint64_t launches[kStages] = {};
 };
 
 struct floe_gpu_layer {
@@ -434,7 +434,7 @@ int launch_fused(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) 
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  StageScope prof(ws, kStageK2, st);
+  StageScope prof(ws, kStageFused, st);
   cudaError_t e = cudaSuccess;
 #define FLOE_FUSED(TT, SP, GP)                                                           \
   do {                                                                                   \
