@@ -17,8 +17,8 @@
 #include <vector>
 
 #include "../../include/floe_gpu.h"
-#include "floe_fused.cuh"
 #include "floe_gen.cuh"
+#include "floe_v2.cuh"
 
 using floe_k::ExpertDesc;
 using floe_k::K1Args;
@@ -96,11 +96,10 @@ bool bits_ok(uint32_t b) { return b == 1 || b == 2 || b == 3 || b == 4 || b == 8
 
 uint64_t packed_code_bytes(uint64_t n, uint32_t bits) { return (n * bits + 7) / 8; }
 
-// Specialised kernels: thread t of a TPB-thread CTA owns x[16t, 16t+16).
-int fast_tpb(uint32_t dh) {
-  if (dh == 4096) return 256;
-  if (dh == 2048) return 128;
-  return 0;
+// The sm_100a fast path (floe_v2.cuh): INT2 codes, d_hidden 2048 or 4096,
+// quantisation groups made of whole 64-element spans.
+bool fast_shape(uint32_t dh, uint32_t bits, uint32_t g) {
+  return bits == 2 && (dh == 4096 || dh == 2048) && g % 64 == 0 && dh % g == 0;
 }
 
 cudaStream_t S(floe_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -119,7 +118,7 @@ struct floe_gpu_expert {
   void *block = nullptr;  // one device allocation for everything
   ExpertDesc host_desc{};
   ExpertDesc *dev_desc = nullptr;
-  bool fast_k1 = false, fast_k2 = false;
+  bool fast = false;  // tile-fragment layout + fused kernel
 };
 
 enum { kStageMixing = 0, kStageRoute = 1, kStageK1 = 2, kStageK2 = 3, kStageFused = 4, kStages = 5 };
@@ -157,7 +156,7 @@ struct floe_gpu_workspace {
 
 struct floe_gpu_layer {
   uint32_t dh = 0, di = 0, E = 0, top_k = 0, bits = 0, g = 0;
-  bool mix_f16 = false, fast_k1 = false, fast_k2 = false;
+  bool mix_f16 = false, fast = false;
   float *router = nullptr;
   void *mixing = nullptr;
   ExpertDesc *table = nullptr;
@@ -216,24 +215,15 @@ struct K1Launch {
   const ExpertDesc *table;
   const uint32_t *sel;
   uint32_t slots, dh, di, bits, g;
-  bool fast;
   int use_thr;
   float thr;
   const float *x;
   float *v_out;
   uint8_t *mask_out;
-  uint32_t *kept_out, *n_kept_out;
   float *y_zero;
 };
 
-// Segments per slot of a K1 launch (= its grid.x); bounded by kMaxSeg.
-uint32_t k1_grid(uint32_t di, uint32_t slots, bool fast) {
-  const uint32_t sm = (uint32_t)device_info().sm;
-  const uint32_t want = fast ? std::max<uint32_t>(1, (2u * sm) / slots)
-                             : std::max<uint32_t>(1, std::min<uint32_t>((di + 63) / 64, 4u * sm));
-  return std::min<uint32_t>({want, (di + 15) / 16 ? (di + 15) / 16 : 1u, kMaxSeg});
-}
-
+// Generic-path K1 (any bits / group / d_hidden): segments per slot = grid.x.
 int launch_k1(const K1Launch &L, floe_gpu_workspace *ws, cudaStream_t st) {
   K1Args a{};
   a.table = L.table;
@@ -251,35 +241,12 @@ int launch_k1(const K1Launch &L, floe_gpu_workspace *ws, cudaStream_t st) {
   a.kept_v = ws->kept_v;
   a.seg_count = ws->seg_count;
   a.y_zero = L.y_zero;
-  const int tpb = fast_tpb(L.dh);
-  const bool fast = L.fast && (tpb == 256 || tpb == 128);
-  const uint32_t g1 = k1_grid(L.di, L.slots, fast);
+  const uint32_t sm = (uint32_t)device_info().sm;
+  const uint32_t g1 = std::min<uint32_t>(
+      {std::max<uint32_t>(1, std::min<uint32_t>((L.di + 63) / 64, 4u * sm)), kMaxSeg});
   ws->g1 = g1;
   StageScope prof(ws, kStageK1, st);
-  dim3 grid(g1, L.slots);
-  if (fast) {
-    constexpr int NS = 4;
-    const uint32_t gpc = L.dh / L.g;
-    const uint32_t smem = NS * floe_k::k1_stage_bytes(L.dh, gpc);
-    const uint32_t gpt = L.g >= 64 ? 1u : 64u / L.g;  // group parts per 64-element span
-#define FLOE_K1(SP, GP)                                                 \
-  do {                                                                  \
-    if (int rc = set_smem(floe_k::k1_int2<SP, GP, NS>, smem)) return rc; \
-    floe_k::k1_int2<SP, GP, NS><<<grid, 256, smem, st>>>(a);            \
-  } while (0)
-    if (L.dh == 4096) {
-      if (gpt == 1) FLOE_K1(64, 1);
-      else if (gpt == 2) FLOE_K1(64, 2);
-      else FLOE_K1(64, 4);
-    } else {
-      if (gpt == 1) FLOE_K1(32, 1);
-      else if (gpt == 2) FLOE_K1(32, 2);
-      else FLOE_K1(32, 4);
-    }
-#undef FLOE_K1
-  } else {
-    floe_k::k1_generic<<<grid, 256, 0, st>>>(a);
-  }
+  floe_k::k1_generic<<<dim3(g1, L.slots), 256, 0, st>>>(a);
   CK_LAUNCH();
   return FLOE_OK;
 }
@@ -289,7 +256,6 @@ struct K2Launch {
   const uint32_t *sel;
   const float *weights;
   uint32_t slots, dh, di;
-  bool fast;
   const float *x;
   float *y;  // nullptr: finalize only (n_kept / kept ids of a K1-only call)
   uint32_t *n_kept_out, *kept_out;
@@ -313,48 +279,16 @@ int launch_k2(const K2Launch &L, floe_gpu_workspace *ws, cudaStream_t st) {
   a.kept_out = L.kept_out;
   a.stats = L.y ? ws->stats : nullptr;
   const int sm = device_info().sm;
-  const int tpb = fast_tpb(L.dh);
   const uint32_t prefix_bytes = 4u * (L.slots * ws->g1 + 1);
-  if (!L.y) {  // finalize a K1-only call
-    if (!L.n_kept_out && !L.kept_out) return FLOE_OK;
-    floe_k::k2_generic<<<sm, 128, prefix_bytes, st>>>(a);
-    CK_LAUNCH();
-    return FLOE_OK;
-  }
+  if (!L.y && !L.n_kept_out && !L.kept_out) return FLOE_OK;
   StageScope prof(ws, kStageK2, st);
-  if (L.fast && (tpb == 256 || tpb == 128)) {
-    // one CTA per SM, 160 KB of records in flight per SM
-    // one CTA per SM, 192 KB of records in flight per SM, 4 records per barrier
-    constexpr int R = 4;
-    if (tpb == 256) {
-      constexpr int NS = 12;
-      const uint32_t smem = NS * 4u * L.dh + prefix_bytes;
-      if (int rc = set_smem(floe_k::k2_gate_down<256, NS, R>, smem)) return rc;
-      floe_k::k2_gate_down<256, NS, R><<<sm, 256, smem, st>>>(a);
-    } else {
-      constexpr int NS = 24;
-      const uint32_t smem = NS * 4u * L.dh + prefix_bytes;
-      if (int rc = set_smem(floe_k::k2_gate_down<128, NS, R>, smem)) return rc;
-      floe_k::k2_gate_down<128, NS, R><<<sm, 128, smem, st>>>(a);
-    }
-  } else {
-    if (int rc = set_smem(floe_k::k2_generic, prefix_bytes)) return rc;
-    floe_k::k2_generic<<<4 * sm, 128, prefix_bytes, st>>>(a);
-  }
+  if (int rc = set_smem(floe_k::k2_generic, prefix_bytes)) return rc;
+  floe_k::k2_generic<<<(L.y ? 4 : 1) * sm, 128, prefix_bytes, st>>>(a);
   CK_LAUNCH();
   return FLOE_OK;
 }
 
-// Path selection: the fused persistent kernel (default) or the split
-// K1/K2 launches (FLOE_GPU_PATH=split, kept for A/B measurements).
-bool fused_enabled() {
-  static const bool on = [] {
-    const char *p = std::getenv("FLOE_GPU_PATH");
-    return !(p && std::strcmp(p, "split") == 0);
-  }();
-  return on;
-}
-
+// The fast path: one cooperative persistent launch of floe_v2::fused.
 struct FusedLaunch {
   // layer mode (mixing != nullptr) or single-expert mode
   const void *mixing;
@@ -364,69 +298,83 @@ struct FusedLaunch {
   const floe_gpu_layer_trace *trace;
   // experts
   const ExpertDesc *table;
-  uint32_t slots, dh, di, g;
+  uint32_t slots, dh, di;
+  bool k1_only;
   int use_thr;
   float thr;
+  const float *x;
   float *u, *y, *v_out;
   uint8_t *mask_out;
   uint32_t *n_kept_out, *kept_out;
 };
 
-int launch_fused(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) {
-  const uint32_t sm = (uint32_t)device_info().sm;
-  floe_k::FusedArgs a{};
+template <int DH>
+int launch_v2_dh(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) {
+  namespace V = floe_v2;
+  const uint32_t G = std::min<uint32_t>((uint32_t)device_info().sm, V::kMaxGrid);
+  const uint32_t tps = V::tiles_per_expert(L.di);
+  const uint32_t NT = L.slots * tps;
+  const uint32_t max_tiles = std::max<uint32_t>(1, (NT + G - 1) / G);
+  static int optin = [] {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0);
+    return v;
+  }();
+  static size_t static_smem = [] {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, V::fused<DH>);
+    return fa.sharedSizeBytes;
+  }();
+  const uint32_t other = V::smem_layout(DH, 0, max_tiles, G).total;
+  const int64_t budget = (int64_t)optin - (int64_t)static_smem - (int64_t)other - 1024;
+  // stages: a multiple of the consumer warp count (stage ownership in phases A/B)
+  const uint32_t ns = (uint32_t)std::min<int64_t>(V::kMaxStages, budget / V::tile_bytes(DH)) /
+                      V::kConsumerWarps * V::kConsumerWarps;
+  if (ns < (uint32_t)V::kConsumerWarps)
+    return fail(FLOE_ERR_UNSUPPORTED, "fused path: shared memory too small for the ring");
+  const uint32_t smem = V::smem_layout(DH, ns, max_tiles, G).total;
+
+  V::FusedArgs a{};
+  a.has_mixing = L.mixing != nullptr;
+  a.k1_only = L.k1_only;
   a.mixing = L.mixing;
+  a.mix_f16 = L.mix_f16;
   a.h = L.h;
   a.router = L.router;
   a.n_experts = L.n_experts;
   a.top_k = L.top_k;
-  a.has_mixing = L.mixing != nullptr;
   a.partial = ws->mix_partial;
   a.u_trace = L.trace ? L.trace->block_input_dev : nullptr;
   a.sel_trace = L.trace ? L.trace->experts_dev : nullptr;
   a.w_trace = L.trace ? L.trace->weights_dev : nullptr;
   a.sel_out = ws->sel;
   a.w_out = ws->weights;
+  a.x = L.x;
   a.u = L.u;
   a.y = L.y;
-  a.dh = L.dh;
   a.di = L.di;
-  a.group_size = L.g;
   a.slots = L.slots;
   a.table = L.table;
   a.use_threshold = L.use_thr;
   a.threshold = L.thr;
   a.v_out = L.v_out;
   a.mask_out = L.mask_out ? L.mask_out : (L.trace ? L.trace->masks_dev : nullptr);
-  a.kept_idx = ws->kept_idx;
+  a.kept_f = ws->kept_idx;
   a.kept_v = ws->kept_v;
   a.seg_count = ws->seg_count;
   a.bar = ws->bar;
   a.n_kept_out = L.n_kept_out;
   a.kept_out = L.kept_out;
-  a.stats = ws->stats;
+  a.stats = L.k1_only ? nullptr : ws->stats;
   a.phase_ns = ws->phase_ns;
-  {
-    static const uint32_t dbg = [] {
-      const char *d = std::getenv("FLOE_DEBUG_FLAGS");
-      return d ? (uint32_t)std::atoi(d) : 0u;
-    }();
-    a.debug = dbg;
-  }
-  ws->g1 = sm;
-  // one shared-memory ring, re-carved per phase: 4*dh-byte stages for mixing
-  // rows and gate|down records, K1-tile stages for the up projection
-  const uint32_t gpc = L.dh / L.g;
-  const uint32_t ring = floe_k::kFusedRingBytes;
-  if (ring / floe_k::k1_stage_bytes(L.dh, gpc) < 2 || ring / (4u * L.dh) < 4)
-    return fail(FLOE_ERR_UNSUPPORTED, "fused path: stages too large for the ring");
-  a.ring_bytes = ring;
-  const uint32_t smem = ring + (a.has_mixing ? 4u * L.dh : 0u) + 4u * (4 * sm + 2);  // plan arrays
-  const uint32_t gpt = L.g >= 64 ? 1u : 64u / L.g;
+  a.ns = ns;
+  a.max_tiles = max_tiles;
+
+  if (int rc = set_smem(V::fused<DH>, smem)) return rc;
   void *kargs[] = {&a};
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(sm);
-  cfg.blockDim = dim3(256);
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(V::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -435,33 +383,20 @@ int launch_fused(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   StageScope prof(ws, kStageFused, st);
-  cudaError_t e = cudaSuccess;
-#define FLOE_FUSED(TT, SP, GP)                                                           \
-  do {                                                                                   \
-    auto *fn = floe_k::floe_fused<TT, SP, GP>;                                           \
-    if (int rc = set_smem(fn, smem)) return rc;                                          \
-    e = cudaLaunchKernelExC(&cfg, reinterpret_cast<const void *>(fn), kargs);           \
-  } while (0)
-#define FLOE_FUSED_GPT(TT, SP)            \
-  do {                                    \
-    if (gpt == 1) FLOE_FUSED(TT, SP, 1);  \
-    else if (gpt == 2) FLOE_FUSED(TT, SP, 2); \
-    else FLOE_FUSED(TT, SP, 4);           \
-  } while (0)
-  const bool f32mix = a.has_mixing && !L.mix_f16;
-  if (L.dh == 4096) {
-    if (f32mix) FLOE_FUSED_GPT(float, 64);
-    else FLOE_FUSED_GPT(__half, 64);
-  } else {
-    if (f32mix) FLOE_FUSED_GPT(float, 32);
-    else FLOE_FUSED_GPT(__half, 32);
-  }
-#undef FLOE_FUSED_GPT
-#undef FLOE_FUSED
+  const cudaError_t e =
+      cudaLaunchKernelExC(&cfg, reinterpret_cast<const void *>(V::fused<DH>), kargs);
   if (e != cudaSuccess)
     return fail(FLOE_ERR_CUDA, "fused launch failed: %s", cudaGetErrorString(e));
   CK_LAUNCH();
   return FLOE_OK;
+}
+
+int launch_v2(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) {
+  if (L.slots > (uint32_t)floe_k::kMaxSlots || (L.mixing && L.n_experts > 32))
+    return fail(FLOE_ERR_UNSUPPORTED, "fused path: at most 32 experts and 8 slots");
+  if (L.dh == 4096) return launch_v2_dh<4096>(L, ws, st);
+  if (L.dh == 2048) return launch_v2_dh<2048>(L, ws, st);
+  return fail(FLOE_ERR_UNSUPPORTED, "fused path: d_hidden %u", L.dh);
 }
 
 int check_ws(const char *fn, const floe_gpu_workspace *ws, uint32_t dh, uint32_t di,
@@ -521,20 +456,16 @@ int floe_gpu_expert_create(const floe_expert_host_view *v, floe_gpu_expert **out
   e->threshold = v->threshold;
   e->code_bytes = packed_code_bytes(n, v->bits);
   e->n_groups = n / v->group_size;
-  const int tpb = fast_tpb(e->dh);
-  // K1 fast path: a thread's 64-element span holds whole groups or lies in
-  // one group, and per-channel metadata rows are 16-byte multiples.
-  const bool g_ok = e->g % 64 == 0 || (e->g % 16 == 0 && 64 % e->g == 0);
-  e->fast_k1 = tpb && e->bits == 2 && g_ok && e->dh % e->g == 0 && (e->dh / e->g) % 4 == 0;
-  e->fast_k2 = tpb != 0;
+  e->fast = fast_shape(e->dh, e->bits, e->g);
 
   // One allocation, 256-B aligned sections:
-  //   [desc][codes][scales][zeros][meta = scale|zero<<16][records]
+  //   fast:    [desc][tiles: ceil(di/16) x 5*dh B][records]
+  //   generic: [desc][codes][scales][zeros][records]
   const uint64_t o_codes = up256(sizeof(ExpertDesc));
+  const uint64_t tile_total = (uint64_t)floe_v2::tiles_per_expert(e->di) * floe_v2::tile_bytes(e->dh);
   const uint64_t o_scales = up256(o_codes + e->code_bytes);
   const uint64_t o_zeros = up256(o_scales + 2 * e->n_groups);
-  const uint64_t o_meta = up256(o_zeros + 2 * e->n_groups);
-  const uint64_t o_rec = up256(o_meta + 4 * e->n_groups);
+  const uint64_t o_rec = e->fast ? up256(o_codes + tile_total) : up256(o_zeros + 2 * e->n_groups);
   const uint64_t total = o_rec + 4 * n;
   cudaError_t ce = cudaMalloc(&e->block, total);
   if (ce != cudaSuccess) {
@@ -544,11 +475,14 @@ int floe_gpu_expert_create(const floe_expert_host_view *v, floe_gpu_expert **out
   }
   char *base = static_cast<char *>(e->block);
   e->dev_desc = reinterpret_cast<ExpertDesc *>(base);
-  e->host_desc.codes = reinterpret_cast<const uint8_t *>(base + o_codes);
-  e->host_desc.scales = reinterpret_cast<const uint16_t *>(base + o_scales);
-  e->host_desc.zeros = reinterpret_cast<const uint16_t *>(base + o_zeros);
+  if (e->fast) {
+    e->host_desc.tiles = reinterpret_cast<const uint32_t *>(base + o_codes);
+  } else {
+    e->host_desc.codes = reinterpret_cast<const uint8_t *>(base + o_codes);
+    e->host_desc.scales = reinterpret_cast<const uint16_t *>(base + o_scales);
+    e->host_desc.zeros = reinterpret_cast<const uint16_t *>(base + o_zeros);
+  }
   e->host_desc.records = reinterpret_cast<const __half *>(base + o_rec);
-  e->host_desc.meta = reinterpret_cast<const uint32_t *>(base + o_meta);
   e->host_desc.threshold = v->threshold;
 
   auto cleanup = [&](int rc) {
@@ -564,15 +498,38 @@ int floe_gpu_expert_create(const floe_expert_host_view *v, floe_gpu_expert **out
     if (err == cudaSuccess) err = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st);
   };
   cp(e->dev_desc, &e->host_desc, sizeof(ExpertDesc));
-  cp(base + o_codes, v->codes, e->code_bytes);
-  cp(base + o_scales, v->scales, 2 * e->n_groups);
-  cp(base + o_zeros, v->zeros, 2 * e->n_groups);
-  if (err == cudaSuccess) {
-    floe_k::interleave_meta<<<1024, 256, 0, st>>>(
-        reinterpret_cast<const uint16_t *>(base + o_scales),
-        reinterpret_cast<const uint16_t *>(base + o_zeros), e->n_groups,
-        reinterpret_cast<uint32_t *>(base + o_meta));
-    err = cudaGetLastError();
+  if (e->fast) {
+    // stage the reference arrays on the device (unless they are there), then
+    // build the tile-fragment layout
+    const uint8_t *dc = v->codes;
+    const uint16_t *dsc = v->scales, *dz = v->zeros;
+    void *tmp = nullptr;
+    if (!on_device && err == cudaSuccess) {
+      const uint64_t tb = up256(e->code_bytes) + 2 * up256(2 * e->n_groups);
+      err = cudaMalloc(&tmp, tb);
+      if (err == cudaSuccess) {
+        char *tc = static_cast<char *>(tmp);
+        cp(tc, v->codes, e->code_bytes);
+        cp(tc + up256(e->code_bytes), v->scales, 2 * e->n_groups);
+        cp(tc + up256(e->code_bytes) + up256(2 * e->n_groups), v->zeros, 2 * e->n_groups);
+        dc = reinterpret_cast<const uint8_t *>(tc);
+        dsc = reinterpret_cast<const uint16_t *>(tc + up256(e->code_bytes));
+        dz = reinterpret_cast<const uint16_t *>(tc + up256(e->code_bytes) + up256(2 * e->n_groups));
+      }
+    }
+    if (err == cudaSuccess) {
+      floe_v2::tile_up<<<1024, 256, 0, st>>>(dc, dsc, dz, e->dh, e->di, e->g,
+                                             reinterpret_cast<uint32_t *>(base + o_codes));
+      err = cudaGetLastError();
+    }
+    if (tmp) {
+      if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+      cudaFree(tmp);
+    }
+  } else {
+    cp(base + o_codes, v->codes, e->code_bytes);
+    cp(base + o_scales, v->scales, 2 * e->n_groups);
+    cp(base + o_zeros, v->zeros, 2 * e->n_groups);
   }
   __half *rec = reinterpret_cast<__half *>(base + o_rec);
   if (v->records_f16) {
@@ -627,7 +584,7 @@ int floe_gpu_expert_info(const floe_gpu_expert *e, floe_expert_info *info) {
   info->code_bytes = e->code_bytes;
   info->meta_bytes = 4 * e->n_groups;
   info->record_bytes = 4ull * e->dh;
-  info->fast_path = e->fast_k1 && e->fast_k2;
+  info->fast_path = e->fast ? 1 : 0;
   return FLOE_OK;
 }
 
@@ -741,8 +698,8 @@ int floe_gpu_workspace_read_counters(floe_gpu_workspace *w, uint64_t *calls,
 int floe_gpu_workspace_set_phase_trace(floe_gpu_workspace *w, int enable) {
   if (!w) return fail(FLOE_ERR_INVALID, "workspace_set_phase_trace: null workspace");
   if (enable && !w->phase_ns) {
-    CK(cudaMalloc(&w->phase_ns, 8ull * floe_k::kTraceSlots * device_info().sm));
-    CK(cudaMemset(w->phase_ns, 0, 8ull * floe_k::kTraceSlots * device_info().sm));
+    CK(cudaMalloc(&w->phase_ns, 8ull * floe_v2::kTraceSlots * device_info().sm));
+    CK(cudaMemset(w->phase_ns, 0, 8ull * floe_v2::kTraceSlots * device_info().sm));
   } else if (!enable && w->phase_ns) {
     cudaFree(w->phase_ns);
     w->phase_ns = nullptr;
@@ -753,7 +710,7 @@ int floe_gpu_workspace_set_phase_trace(floe_gpu_workspace *w, int enable) {
 int floe_gpu_workspace_read_phase_trace(floe_gpu_workspace *w, uint64_t *out, uint32_t cap,
                                         uint32_t *grid) {
   if (!w || !out) return fail(FLOE_ERR_INVALID, "workspace_read_phase_trace: null argument");
-  const uint32_t n = std::min<uint32_t>(cap, (uint32_t)floe_k::kTraceSlots * device_info().sm);
+  const uint32_t n = std::min<uint32_t>(cap, (uint32_t)floe_v2::kTraceSlots * device_info().sm);
   if (grid) *grid = device_info().sm;
   if (!w->phase_ns) return fail(FLOE_ERR_INVALID, "workspace_read_phase_trace: tracing is off");
   CK(cudaDeviceSynchronize());
@@ -795,26 +752,24 @@ int floe_gpu_expert_forward_sparse(const floe_gpu_expert *e, floe_gpu_workspace 
                                    uint32_t *n_kept_out, floe_stream_t stream) {
   if (!e || !x || !y) return fail(FLOE_ERR_INVALID, "expert_forward_sparse: null argument");
   if (int rc = check_ws("expert_forward_sparse", ws, e->dh, e->di, 1)) return rc;
-  if (e->fast_k1 && e->fast_k2 && fused_enabled()) {
+  if (e->fast) {
     FusedLaunch f{};
     f.table = e->dev_desc;
     f.slots = 1;
     f.dh = e->dh;
     f.di = e->di;
-    f.g = e->g;
-    f.u = const_cast<float *>(x);
+    f.x = x;
     f.y = y;
     f.v_out = v_out;
     f.mask_out = mask_out;
     f.n_kept_out = n_kept_out;
     f.kept_out = kept_out;
-    return launch_fused(f, ws, S(stream));
+    return launch_v2(f, ws, S(stream));
   }
-  K1Launch k1{e->dev_desc, nullptr, 1, e->dh, e->di, e->bits, e->g, e->fast_k1, 0, 0.0f,
-              x, v_out, mask_out, nullptr, nullptr, y};
+  K1Launch k1{e->dev_desc, nullptr, 1, e->dh, e->di, e->bits, e->g, 0, 0.0f,
+              x, v_out, mask_out, y};
   if (int rc = launch_k1(k1, ws, S(stream))) return rc;
-  K2Launch k2{e->dev_desc, nullptr, nullptr, 1, e->dh, e->di, e->fast_k2, x, y,
-              n_kept_out, kept_out};
+  K2Launch k2{e->dev_desc, nullptr, nullptr, 1, e->dh, e->di, x, y, n_kept_out, kept_out};
   return launch_k2(k2, ws, S(stream));
 }
 
@@ -845,16 +800,33 @@ int floe_gpu_qgemv_channels(const floe_gpu_expert *e, floe_gpu_workspace *ws,
                             const float *x, float *v_out, floe_stream_t stream) {
   if (!e || !x || !v_out) return fail(FLOE_ERR_INVALID, "qgemv_channels: null argument");
   if (int rc = check_ws("qgemv_channels", ws, e->dh, e->di, 1)) return rc;
-  K1Launch k1{e->dev_desc, nullptr, 1, e->dh, e->di, e->bits, e->g, e->fast_k1, 1,
-              __builtin_inff(), x, v_out, nullptr, nullptr, nullptr, nullptr};
+  if (e->fast) {
+    FusedLaunch f{};
+    f.table = e->dev_desc;
+    f.slots = 1;
+    f.dh = e->dh;
+    f.di = e->di;
+    f.k1_only = true;
+    f.use_thr = 1;
+    f.thr = __builtin_inff();  // nothing kept: v only
+    f.x = x;
+    f.v_out = v_out;
+    return launch_v2(f, ws, S(stream));
+  }
+  K1Launch k1{e->dev_desc, nullptr, 1, e->dh, e->di, e->bits, e->g, 1,
+              __builtin_inff(), x, v_out, nullptr, nullptr};
   return launch_k1(k1, ws, S(stream));
 }
 
 int floe_gpu_dequantize_up(const floe_gpu_expert *e, float *out, floe_stream_t stream) {
   if (!e || !out) return fail(FLOE_ERR_INVALID, "dequantize: null argument");
   const uint64_t n = (uint64_t)e->dh * e->di;
-  floe_k::dequant_up<<<4 * device_info().sm, 256, 0, S(stream)>>>(e->dev_desc, n, e->bits,
-                                                                   e->g, out);
+  if (e->fast)
+    floe_v2::dequant_tiled<<<4 * device_info().sm, 256, 0, S(stream)>>>(e->host_desc.tiles, e->dh,
+                                                                        e->di, out);
+  else
+    floe_k::dequant_up<<<4 * device_info().sm, 256, 0, S(stream)>>>(e->dev_desc, n, e->bits,
+                                                                     e->g, out);
   CK_LAUNCH();
   return FLOE_OK;
 }
@@ -864,10 +836,25 @@ int floe_gpu_predict_mask(const floe_gpu_expert *next, floe_gpu_workspace *ws,
                           uint32_t *kept_out, uint32_t *n_kept_out, floe_stream_t stream) {
   if (!next || !x_prev) return fail(FLOE_ERR_INVALID, "predict_mask: null argument");
   if (int rc = check_ws("predict_mask", ws, next->dh, next->di, 1)) return rc;
-  K1Launch k1{next->dev_desc, nullptr, 1, next->dh, next->di, next->bits, next->g,
-              next->fast_k1, 1, t, x_prev, nullptr, mask_out, nullptr, nullptr, nullptr};
+  if (next->fast) {
+    FusedLaunch f{};
+    f.table = next->dev_desc;
+    f.slots = 1;
+    f.dh = next->dh;
+    f.di = next->di;
+    f.k1_only = true;
+    f.use_thr = 1;
+    f.thr = t;
+    f.x = x_prev;
+    f.mask_out = mask_out;
+    f.kept_out = kept_out;
+    f.n_kept_out = n_kept_out;
+    return launch_v2(f, ws, S(stream));
+  }
+  K1Launch k1{next->dev_desc, nullptr, 1, next->dh, next->di, next->bits, next->g, 1, t,
+              x_prev, nullptr, mask_out, nullptr};
   if (int rc = launch_k1(k1, ws, S(stream))) return rc;
-  K2Launch fin{next->dev_desc, nullptr, nullptr, 1, next->dh, next->di, false, x_prev, nullptr,
+  K2Launch fin{next->dev_desc, nullptr, nullptr, 1, next->dh, next->di, x_prev, nullptr,
                n_kept_out, kept_out};
   return launch_k2(fin, ws, S(stream));
 }
@@ -902,8 +889,7 @@ int floe_gpu_layer_create(const floe_layer_host_view *v, floe_gpu_layer **out) {
   l->bits = e0->bits;
   l->g = e0->g;
   l->mix_f16 = v->mixing_f16 != 0;
-  l->fast_k1 = e0->fast_k1;
-  l->fast_k2 = e0->fast_k2;
+  l->fast = e0->fast;
   const uint64_t dh = l->dh;
   std::vector<ExpertDesc> table(l->E);
   for (uint32_t i = 0; i < l->E; ++i) table[i] = v->experts[i]->host_desc;
@@ -951,7 +937,7 @@ int floe_gpu_layer_forward(const floe_gpu_layer *l, floe_gpu_workspace *ws, cons
   if (!l || !h || !y) return fail(FLOE_ERR_INVALID, "layer_forward: null argument");
   if (int rc = check_ws("layer_forward", ws, l->dh, l->di, l->top_k)) return rc;
   cudaStream_t st = S(stream);
-  if (l->fast_k1 && l->fast_k2 && fused_enabled() && l->E <= 32) {
+  if (l->fast && l->E <= 32) {
     FusedLaunch f{};
     f.mixing = l->mixing;
     f.mix_f16 = l->mix_f16;
@@ -964,13 +950,11 @@ int floe_gpu_layer_forward(const floe_gpu_layer *l, floe_gpu_workspace *ws, cons
     f.slots = l->top_k;
     f.dh = l->dh;
     f.di = l->di;
-    f.g = l->g;
+    f.x = ws->u;
     f.u = ws->u;
     f.y = y;
-    return launch_fused(f, ws, st);
+    return launch_v2(f, ws, st);
   }
-  const uint32_t rows_per_block = 8;
-  const size_t smem = 4ull * l->dh;
   float *u_tr = tr ? tr->block_input_dev : nullptr;
   {
     // mixing GEMV + residual + router logits + top-k + softmax in one launch
@@ -991,36 +975,23 @@ int floe_gpu_layer_forward(const floe_gpu_layer *l, floe_gpu_workspace *ws, cons
     m.weights = ws->weights;
     m.sel_trace = tr ? tr->experts_dev : nullptr;
     m.w_trace = tr ? tr->weights_dev : nullptr;
-    const uint32_t sm = (uint32_t)device_info().sm;
-    const uint32_t bulk_grid = std::min<uint32_t>(sm, l->dh);
-    const bool bulk = l->dh % 8 == 0 &&
-                      (l->dh + bulk_grid - 1) / bulk_grid <= floe_k::kMaxRowsPerCta;
-    if (bulk) {
-      constexpr int NS = 2;
-      const uint32_t row_bytes = l->dh * (l->mix_f16 ? 2u : 4u);
-      const uint32_t rpc = floe_k::mix_rows_per_chunk(row_bytes);
-      const uint32_t bsmem = NS * floe_k::round_up128(rpc * row_bytes) + 4u * l->dh;
-      if (l->mix_f16) {
-        if (int rc = set_smem(floe_k::mixing_route_bulk<__half, NS>, bsmem)) return rc;
-        floe_k::mixing_route_bulk<__half, NS><<<bulk_grid, 256, bsmem, st>>>(m);
-      } else {
-        if (int rc = set_smem(floe_k::mixing_route_bulk<float, NS>, bsmem)) return rc;
-        floe_k::mixing_route_bulk<float, NS><<<bulk_grid, 256, bsmem, st>>>(m);
-      }
-    } else {
-      const dim3 grid((l->dh + rows_per_block - 1) / rows_per_block);
-      if (l->mix_f16)
-        floe_k::mixing_route<__half><<<grid, 256, smem, st>>>(m);
-      else
-        floe_k::mixing_route<float><<<grid, 256, smem, st>>>(m);
+    const dim3 grid((l->dh + 7) / 8);
+    const size_t smem = 4ull * l->dh;
+    if (smem > 48 * 1024) {
+      if (int rc = set_smem(l->mix_f16 ? (void (*)(floe_k::MixArgs))floe_k::mixing_route<__half>
+                                       : floe_k::mixing_route<float>, (uint32_t)smem))
+        return rc;
     }
+    if (l->mix_f16)
+      floe_k::mixing_route<__half><<<grid, 256, smem, st>>>(m);
+    else
+      floe_k::mixing_route<float><<<grid, 256, smem, st>>>(m);
     CK_LAUNCH();
   }
-  K1Launch k1{l->table, ws->sel, l->top_k, l->dh, l->di, l->bits, l->g, l->fast_k1, 0, 0.0f,
-              ws->u, nullptr, tr ? tr->masks_dev : nullptr, nullptr, nullptr, nullptr};
+  K1Launch k1{l->table, ws->sel, l->top_k, l->dh, l->di, l->bits, l->g, 0, 0.0f,
+              ws->u, nullptr, tr ? tr->masks_dev : nullptr, nullptr};
   if (int rc = launch_k1(k1, ws, st)) return rc;
-  K2Launch k2{l->table, ws->sel, ws->weights, l->top_k, l->dh, l->di, l->fast_k2, ws->u, y,
-              nullptr, nullptr};
+  K2Launch k2{l->table, ws->sel, ws->weights, l->top_k, l->dh, l->di, ws->u, y, nullptr, nullptr};
   return launch_k2(k2, ws, st);
 }
 

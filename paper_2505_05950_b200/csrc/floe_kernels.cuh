@@ -6,21 +6,19 @@
 //     keep c iff !(|v[c]| < t)                                  core/src/model.cpp:135
 //     y += silu(gate_c . x) * v[c] * down_c  (kept c only)      core/src/model.cpp:136-140
 //
-// Kernels
-//   K1  k1_int2<TPB,NS>    (floe_fast.cuh) fused INT2 group-dequant GEMV +
-//                          |v|>=t epilogue + compaction, bulk-copy staged
-//   K1g k1_generic         same contract for any bits / group size / d_hidden
-//   K2  k2_gate_down<TPB,NS> (floe_fast.cuh) channel-sparse gate dot + SwiGLU +
-//                          down accumulation over bulk-copied channel records
-//   K2g k2_generic         same contract for any d_hidden
+// Kernels (the INT2 fast path lives in floe_v2.cuh; these serve every other
+// shape: any bits, any group size, any d_hidden)
+//   K1g k1_generic         dequant GEMV + |v|>=t epilogue + compaction
+//   K2g k2_generic         channel-sparse gate dot + SwiGLU + down accumulation
 //   dequant_up             bit-exact f32 dequantisation (debug / parity)
 //   mixing_gemv, route_topk, predict_experts_k   layer glue (model.cpp:83-93,145-169)
 //
-// HBM layout of one expert:
+// HBM layout of one generic-path expert:
 //   codes    u8 [di][dh*bits/8]  unchanged reference packing (LE in byte)
 //   scales   u16[di][dh/g]       f16 bits, unchanged
 //   zeros    u16[di][dh/g]       f16 bits, unchanged
 //   records  f16[di][2][dh]      gate row c | down row c  (pack_compact wire format)
+// Fast-path experts replace codes/scales/zeros by the tile-fragment layout.
 #pragma once
 
 #include <cuda_fp16.h>
@@ -32,13 +30,13 @@ constexpr int kMaxSlots = 8;
 
 // Device-side descriptor of one resident expert.
 struct ExpertDesc {
-  const uint8_t *codes;
-  const uint16_t *scales;
-  const uint16_t *zeros;
-  const __half *records;  // [di][2*dh]
-  const uint32_t *meta;   // [di][dh/g] scale16 | zero16 << 16 (K1 fast path)
+  const uint8_t *codes;    // generic path: reference packing (null on the fast path)
+  const uint16_t *scales;  // generic path
+  const uint16_t *zeros;   // generic path
+  const __half *records;   // [di][2*dh]
+  const uint32_t *tiles;   // fast path: tile-fragment up projection (floe_v2.cuh)
   float threshold;
-  uint32_t pad_;
+  uint32_t pad_[3];
 };
 
 // Kept-channel lists ("segments").  K1 runs on a (G1, slots) grid; CTA b of

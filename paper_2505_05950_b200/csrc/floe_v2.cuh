@@ -1,0 +1,1012 @@
+// floe_v2.cuh -- the sm_100a fast path: ONE warp-specialised persistent
+// kernel per decode step over a tile-fragment HBM layout of the INT2 up
+// projection, with the up-projection GEMV on the tensor cores (exact integer
+// IMMA).
+//
+// Reference (paths relative to /root/reference/proj/):
+//   block_forward / route        core/src/model.cpp:145-169, 83-93   (phase A)
+//   qgemv_channels + threshold   core/src/quant.cpp:122-136, model.cpp:135 (phase B)
+//   gate dot + silu + down       core/src/model.cpp:136-140, la.cpp:25-31 (phase C)
+//
+// ---------------------------------------------------------------------------
+// Up projection as an exact integer tensor-core product.
+//
+//   v[c] = sum_s  scale[c,s] * sum_{k in span s} code[c,k] * x[k]  +  zero[c,s] * sum_{k in s} x[k]
+//
+// (the group-affine dequant code*scale+zero of dequantize_at, quant.cpp:104-109,
+// folded out of the inner sum; s runs over 64-element spans, each inside one
+// quantisation group because g % 64 == 0).  x is scaled once per call by
+// S = 2^(22-E) (max|x| < 2^E) to a 23-bit integer X = X0 + 256 X1 + 65536 X2
+// with signed 8-bit limbs, and sum code*X is computed EXACTLY with
+// mma.sync m16n8k32 s8.s8.s32 (IMMA): A = 16 channels x 32 codes (0..3 as s8),
+// B = 32 x-positions x 8 columns, columns 0..2 = the three limbs.  One IMMA
+// covers 512 weights; two cover a 64-element span of 16 channels.  The limb
+// columns land in lanes tig=0 (limbs 0,1) and tig=1 (limb 2) of each quad, so
+// each lane scales its own columns (mult = 1/S or 65536/S) and a final quad
+// reduction sums them -- no shuffles in the inner loop.
+//
+// Tile-fragment HBM layout of one expert's up projection (built at upload by
+// tile_up; bit-exact dequant from it is checked by dequant_tiled):
+//   tile t = channels [16t, 16t+16) (zero-padded past d_intermediate), 5*DH bytes:
+//   codes [pair p < DH/128][lane < 32][4 x u32]    = 4*DH bytes
+//         lane = 4*g + tig; the 4 words are word `tig` (codes 16tig..16tig+15)
+//         of (row g, span 2p), (row g+8, span 2p), (row g, span 2p+1), (row g+8, span 2p+1)
+//   meta  [pair p][g < 8][4 x u32]                 = DH bytes
+//         scale16 | zero16 << 16 of the group of the same four (row, span)
+// so every lane reads its IMMA A-fragments with one conflict-free LDS.128 per
+// two spans.  Extracting 2-bit codes to s8: (w >> 2m) & 0x03030303 gives bytes
+// = codes 16tig + 4b + m, which fixes the logical k order; the B table (x limbs)
+// is built in the same order once per call.
+#pragma once
+
+#include "floe_kernels.cuh"
+#include "floe_ptx.cuh"
+
+namespace floe_v2 {
+
+using floe_k::ExpertDesc;
+using floe_k::h2f;
+
+constexpr int kTileCh = 16;
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumers = 32 * kConsumerWarps;   // 256
+constexpr int kThreads = kConsumers + 32;         // + 1 producer warp
+constexpr int kMaxStages = 24;  // ring stages: a multiple of kConsumerWarps (see phase B)
+constexpr int kMaxGrid = 256;                     // plan scans: one value per consumer
+constexpr int kR = 4;                             // phase-C records per consumer barrier
+constexpr int kMaxRowsPerCta = 32;                // phase-A router slice in smem
+
+__host__ __device__ constexpr uint32_t tile_bytes(uint32_t dh) { return 5u * dh; }
+__host__ __device__ constexpr uint32_t xtab_bytes(uint32_t dh) { return (dh / 128u) * 2u * 16u * 16u; }
+__host__ __device__ inline uint32_t tiles_per_expert(uint32_t di) { return (di + kTileCh - 1) / kTileCh; }
+
+// ------------------------------------------------------------ layout kernels
+// Reference codes/scales/zeros (device) -> tile-fragment layout.
+__global__ void tile_up(const uint8_t *codes, const uint16_t *scales, const uint16_t *zeros,
+                        uint32_t dh, uint32_t di, uint32_t gsize, uint32_t *out) {
+  const uint32_t tb = tile_bytes(dh) / 4;  // u32 per tile
+  const uint32_t code_w = dh;              // u32 of codes per tile (4*dh bytes)
+  const uint64_t n = (uint64_t)tiles_per_expert(di) * tb;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t t = (uint32_t)(i / tb), q = (uint32_t)(i % tb);
+    uint32_t row, span, word;
+    const bool is_code = q < code_w;
+    if (is_code) {
+      const uint32_t k = q & 3, lane = (q >> 2) & 31, p = q >> 7;
+      row = (lane >> 2) + 8 * (k & 1);
+      span = 2 * p + (k >> 1);
+      word = lane & 3;
+    } else {
+      const uint32_t m = q - code_w;
+      const uint32_t k = m & 3, g = (m >> 2) & 7, p = m >> 5;
+      row = g + 8 * (k & 1);
+      span = 2 * p + (k >> 1);
+      word = 0;
+    }
+    const uint32_t c = t * kTileCh + row;
+    uint32_t val = 0;
+    if (c < di) {
+      const uint64_t e0 = (uint64_t)c * dh + 64u * span;  // first element of the span
+      if (is_code) {
+        val = *reinterpret_cast<const uint32_t *>(codes + e0 / 4 + 4u * word);
+      } else {
+        const uint64_t grp = e0 / gsize;
+        val = (uint32_t)scales[grp] | ((uint32_t)zeros[grp] << 16);
+      }
+    }
+    out[i] = val;
+  }
+}
+
+// dequantize (quant.cpp:104-120) from the tile layout: bit-exact (one fmaf of
+// an exact product, like the reference's mul-then-add).
+__global__ void dequant_tiled(const uint32_t *tiles, uint32_t dh, uint32_t di, float *out) {
+  const uint64_t n = (uint64_t)dh * di;
+  const uint32_t tb = tile_bytes(dh) / 4;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = (uint32_t)(i / dh), kk = (uint32_t)(i % dh);
+    const uint32_t t = c / kTileCh, row = c % kTileCh, span = kk / 64, e = kk % 64;
+    const uint32_t p = span / 2, kidx = (span & 1) * 2 + (row >= 8);
+    const uint32_t lane = 4 * (row & 7) + e / 16;
+    const uint32_t *tile = tiles + (uint64_t)t * tb;
+    const uint32_t w = tile[(p * 32 + lane) * 4 + kidx];
+    const uint32_t m = tile[dh + (p * 8 + (row & 7)) * 4 + kidx];
+    const uint32_t code = (w >> (2 * (e % 16))) & 3u;
+    out[i] = fmaf((float)code, h2f((uint16_t)(m & 0xffffu)), h2f((uint16_t)(m >> 16)));
+  }
+}
+
+// --------------------------------------------------------------- K1 tile math
+__device__ __forceinline__ void imma16832(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                          uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// One 64-element span of 16 channels: wa/wb = this lane's code word of rows
+// g / g+8, xb = the lane's B fragments (limb column groupID) for the span's two
+// IMMAs, mg/mg8 = scale|zero of rows g / g+8.
+__device__ __forceinline__ void span_step(float2 &acc, uint32_t wa, uint32_t wb, uint4 xb,
+                                          uint32_t mg, uint32_t mg8, float zxs, float mult) {
+  constexpr uint32_t M = 0x03030303u;
+  int c[4] = {0, 0, 0, 0};
+  imma16832(c, wa & M, wb & M, (wa >> 2) & M, (wb >> 2) & M, xb.x, xb.y);
+  imma16832(c, (wa >> 4) & M, (wb >> 4) & M, (wa >> 6) & M, (wb >> 6) & M, xb.z, xb.w);
+  const float tg = (float)(c[0] + 256 * c[1]);   // exact: |.| < 2^23
+  const float tg8 = (float)(c[2] + 256 * c[3]);
+  acc.x = fmaf(h2f((uint16_t)(mg & 0xffffu)) * mult, tg, fmaf(h2f((uint16_t)(mg >> 16)), zxs, acc.x));
+  acc.y = fmaf(h2f((uint16_t)(mg8 & 0xffffu)) * mult, tg8, fmaf(h2f((uint16_t)(mg8 >> 16)), zxs, acc.y));
+}
+
+// v of rows (g, g+8) of one tile in stage memory; all four lanes of a quad
+// return the same pair.
+template <int DH>
+__device__ __forceinline__ float2 k1_tile(const uint8_t *stage, const uint8_t *xtab,
+                                          const float *xs, float mult, float zx, uint32_t lane) {
+  constexpr int PAIRS = DH / 128;
+  const uint4 *cw = reinterpret_cast<const uint4 *>(stage) + lane;
+  const uint4 *mw = reinterpret_cast<const uint4 *>(stage + 4 * DH) + (lane >> 2);
+  const uint4 *xw = reinterpret_cast<const uint4 *>(xtab) + (lane < 12 ? lane : 12);
+  float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll 4
+  for (int p = 0; p < PAIRS; ++p) {
+    const uint4 c4 = cw[p * 32];
+    const uint4 m4 = mw[p * 8];
+    const uint4 x0 = xw[p * 32], x1 = xw[p * 32 + 16];
+    const float2 xsp = *reinterpret_cast<const float2 *>(xs + 2 * p);
+    span_step(acc, c4.x, c4.y, x0, m4.x, m4.y, xsp.x * zx, mult);
+    span_step(acc, c4.z, c4.w, x1, m4.z, m4.w, xsp.y * zx, mult);
+  }
+  acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
+  acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
+  acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
+  acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
+  return acc;
+}
+
+// Non-finite x (inf/NaN cannot be limb-encoded): the reference's own f32
+// expression float(code)*scale + zero per element, so NaN/inf propagate exactly
+// as in qgemv_channels.  xf = x in shared memory.
+template <int DH>
+__device__ __noinline__ float2 k1_tile_f32(const uint8_t *stage, const float *xf, uint32_t lane) {
+  const uint32_t *cw = reinterpret_cast<const uint32_t *>(stage);
+  const uint32_t *mw = reinterpret_cast<const uint32_t *>(stage + 4 * DH);
+  const uint32_t g = lane >> 2, tig = lane & 3;
+  float2 acc = make_float2(0.0f, 0.0f);
+  for (uint32_t span = 0; span < DH / 64; ++span) {
+    const uint32_t p = span / 2, hi = span & 1;
+    for (uint32_t r = 0; r < 2; ++r) {
+      const uint32_t kidx = hi * 2 + r;
+      const uint32_t w = cw[(p * 32 + lane) * 4 + kidx];
+      const uint32_t m = mw[(p * 8 + g) * 4 + kidx];
+      const float sc = h2f((uint16_t)(m & 0xffffu)), zr = h2f((uint16_t)(m >> 16));
+      float s = 0.0f;
+      for (uint32_t q = 0; q < 16; ++q)
+        s = fmaf(fmaf((float)((w >> (2 * q)) & 3u), sc, zr), xf[64 * span + 16 * tig + q], s);
+      if (r == 0) acc.x += s;
+      else acc.y += s;
+    }
+  }
+  acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 1);
+  acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 1);
+  acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 2);
+  acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 2);
+  return acc;
+}
+
+// ----------------------------------------------------------------- utilities
+// Named barriers.  __syncwarp() first: an inline-asm barrier is not a
+// reconvergence point for the compiler, and a warp arriving diverged would be
+// counted twice.
+__device__ __forceinline__ void cbar() {
+  __syncwarp();
+  asm volatile("barrier.sync 1, 256;" ::: "memory");
+}
+__device__ __forceinline__ void abar() {
+  __syncwarp();
+  asm volatile("barrier.sync 2, 288;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive1(uint64_t *bar) { floe_ptx::mbar_arrive(bar); }
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+constexpr int kTraceSlots = 64;
+
+// Grid barrier on a monotonic counter; called by consumer thread 0 only,
+// between two consumer barriers.
+__device__ __forceinline__ void grid_arrive_wait(unsigned long long *bar, uint32_t G) {
+  __threadfence();
+  const unsigned long long old = atomicAdd(bar, 1ull);
+  const unsigned long long target = (old / G + 1) * G;
+  const unsigned long long t0 = gtime();
+  for (uint32_t it = 1;; ++it) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
+    if (v >= target) break;
+    if ((it & 255u) == 0 && gtime() - t0 > floe_ptx::kWatchdogNs)
+      floe_ptx::watchdog_fire("grid barrier", (uint32_t)(target / G), (uint32_t)(old % G));
+  }
+  __threadfence();
+}
+
+// Exclusive scan over the 256 consumer threads (one value each); returns the
+// prefix, writes the total to *total.  Uses ws[8] shared scratch; contains
+// two consumer barriers.
+__device__ __forceinline__ uint32_t cscan(uint32_t v, uint32_t *ws, uint32_t *total) {
+  const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  uint32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= (uint32_t)o) inc += y;
+  }
+  if (lane == 31) ws[warp] = inc;
+  cbar();
+  uint32_t base = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < kConsumerWarps; ++w) {
+    const uint32_t x = ws[w];
+    if (w < (int)warp) base += x;
+    tot += x;
+  }
+  cbar();
+  *total = tot;
+  return base + inc - v;
+}
+
+// -------------------------------------------------------------- the kernel
+struct FusedArgs {
+  int has_mixing;  // layer mode (phase A) vs single-expert mode
+  int k1_only;     // qgemv_channels / predict_mask: no phase C
+  // phase A
+  const void *mixing;  // [DH][DH] f16 or f32
+  int mix_f16;
+  const float *h;
+  const float *router;  // [E][DH]
+  uint32_t n_experts, top_k;
+  float *partial;  // [G][32]
+  float *u_trace;
+  uint32_t *sel_trace;
+  float *w_trace;
+  uint32_t *sel_out;
+  float *w_out;
+  // expert input/outputs
+  const float *x;  // expert mode input (layer mode: x = u)
+  float *u;        // layer mode: block input u (written in phase A)
+  float *y;        // output (nullable when k1_only)
+  uint32_t di, slots;
+  const ExpertDesc *table;  // layer: [E]; expert mode: [slots]
+  int use_threshold;
+  float threshold;
+  float *v_out;       // nullable [slots][di]
+  uint8_t *mask_out;  // nullable [slots][di]
+  uint32_t *kept_f;   // [slots*di] per-CTA compacted lists (flattened channel ids)
+  float *kept_v;
+  uint32_t *seg_count;  // [slots][G]
+  unsigned long long *bar;
+  uint32_t *n_kept_out;  // nullable [slots]
+  uint32_t *kept_out;    // nullable [slots][di], ascending-by-CTA order
+  unsigned long long *stats;
+  unsigned long long *phase_ns;  // nullable [G][kTraceSlots]
+  uint32_t ns;        // ring stages
+  uint32_t max_tiles; // per-CTA tile capacity of the smem emit buffer
+};
+
+// Dynamic shared memory layout (bytes), host and device agree.
+struct SmemLayout {
+  uint32_t ring, uni, xs, emit_f, emit_v, tile_cnt, plan, scale, total;
+};
+
+__host__ __device__ inline SmemLayout smem_layout(uint32_t dh, uint32_t ns, uint32_t max_tiles,
+                                                  uint32_t G) {
+  SmemLayout L;
+  uint32_t o = 0;
+  L.ring = o;     o += ns * tile_bytes(dh);
+  L.uni = o;      o += (4u * dh > xtab_bytes(dh) ? 4u * dh : xtab_bytes(dh));  // h | x f32 | xtab
+  L.xs = o;       o += 4u * (dh / 64);
+  L.emit_f = o;   o += 4u * kTileCh * max_tiles;
+  L.emit_v = o;   o += 4u * kTileCh * max_tiles;
+  L.tile_cnt = o; o += 4u * max_tiles + 16;
+  L.plan = o;     o += 4u * 3 * (G + 1);
+  L.scale = o;    o += 4u * ns;
+  L.total = (o + 127u) & ~127u;
+  return L;
+}
+
+__device__ __forceinline__ void mark(const FusedArgs &a, int k) {
+  if (a.phase_ns && (threadIdx.x == 0) && k < kTraceSlots)
+    a.phase_ns[blockIdx.x * kTraceSlots + k] = gtime();
+}
+
+// Tile i of the launch (tile-granular split of slots x tiles_per_expert over
+// the grid): slot, tile within expert, channel count, flattened position.
+struct TileRef {
+  uint32_t slot, t, nc, f0;
+};
+__device__ __forceinline__ TileRef tile_ref(uint32_t i, uint32_t tps, uint32_t di) {
+  TileRef r;
+  r.slot = i / tps;
+  r.t = i % tps;
+  r.nc = min((uint32_t)kTileCh, di - r.t * kTileCh);
+  r.f0 = r.slot * di + r.t * kTileCh;
+  return r;
+}
+
+template <int DH>
+__global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
+  constexpr uint32_t TILE_B = tile_bytes(DH);
+  constexpr uint32_t REC_B = 4 * DH;
+  constexpr uint32_t SPANS = DH / 64;
+  constexpr int TPB2 = DH / 16;  // phase-C threads owning 16 elements each
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
+  __shared__ uint64_t hbar;
+  __shared__ float rs[32 * kMaxRowsPerCta];
+  __shared__ float plw[kConsumerWarps][32];
+  __shared__ float logits[32];
+  __shared__ uint32_t sel_s[floe_k::kMaxSlots];
+  __shared__ float w_s[floe_k::kMaxSlots];
+  __shared__ const __half *rec_s[floe_k::kMaxSlots];
+  __shared__ const uint8_t *tiles_s[floe_k::kMaxSlots];
+  __shared__ float thr_s[floe_k::kMaxSlots];
+  __shared__ uint32_t ws8[kConsumerWarps];
+  __shared__ float redmax[kConsumerWarps];
+  __shared__ float red[kConsumerWarps][kR];
+  __shared__ float aco_s[2][kR];
+  __shared__ uint32_t pv[8];  // plan values: 0 T, 1 own_b, 2 d_b, 3 D_b, 4 n_own, 5 P, 6 all_finite
+  __shared__ uint32_t slot_cnt[floe_k::kMaxSlots];
+
+  const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const uint32_t G = gridDim.x, b = blockIdx.x;
+  const bool producer = warp == kConsumerWarps;
+  const SmemLayout L = smem_layout(DH, a.ns, a.max_tiles, G);
+  uint8_t *ring = smem + L.ring;
+  float *hs = reinterpret_cast<float *>(smem + L.uni);  // phase A: h; phase B: x (f32) or xtab
+  uint8_t *xtab = smem + L.uni;
+  float *xs = reinterpret_cast<float *>(smem + L.xs);
+  uint32_t *emit_f = reinterpret_cast<uint32_t *>(smem + L.emit_f);
+  float *emit_v = reinterpret_cast<float *>(smem + L.emit_v);
+  uint32_t *tile_cnt = reinterpret_cast<uint32_t *>(smem + L.tile_cnt);
+  uint32_t *NB = reinterpret_cast<uint32_t *>(smem + L.plan);  // [G+1] per-CTA counts
+  uint32_t *SUp = NB + (G + 1);                                // [G+1] surplus prefix
+  uint32_t *TBp = SUp + (G + 1);                               // [G+1] unused spare
+  float *stage_scale = reinterpret_cast<float *>(smem + L.scale);
+  (void)TBp;
+  const uint32_t ns = a.ns;
+
+  auto stage = [&](uint32_t u) { return ring + (u % ns) * TILE_B; };
+  auto wait_full = [&](uint32_t u) {
+    floe_ptx::mbar_wait(&full[u % ns], (u / ns) & 1u, (1u << 28) | u);
+  };
+  // producer side: stage use u may be (re)filled once use u - ns is released
+  auto wait_empty = [&](uint32_t u) {
+    if (u >= ns) floe_ptx::mbar_wait(&empty[u % ns], ((u / ns) + 1) & 1u, (2u << 28) | u);
+  };
+  auto issue = [&](uint32_t u, const void *src, uint32_t bytes) {
+    floe_ptx::mbar_arrive_expect_tx(&full[u % ns], bytes);
+    floe_ptx::bulk_g2s(stage(u), src, bytes, &full[u % ns]);
+  };
+
+  mark(a, 0);
+  if (t == 0) {
+    for (uint32_t s = 0; s < ns; ++s) {
+      floe_ptx::mbar_init(&full[s], 1);
+      floe_ptx::mbar_init(&empty[s], 1);
+    }
+    floe_ptx::mbar_init(&hbar, 1);
+    floe_ptx::fence_barrier_init();
+  }
+  __syncthreads();
+
+  // ---- geometry
+  const uint32_t tps = tiles_per_expert(a.di);
+  const uint32_t NT = a.slots * tps;
+  const uint32_t tile_lo = (uint32_t)(((uint64_t)NT * b) / G);
+  const uint32_t nB = (uint32_t)(((uint64_t)NT * (b + 1)) / G) - tile_lo;
+  const uint32_t rpi = a.mix_f16 ? 2u : 1u;  // mixing rows per stage
+  const uint32_t r_lo = floe_k::seg_begin(DH, b, G), r_hi = floe_k::seg_begin(DH, b + 1, G);
+  const uint32_t nA = a.has_mixing ? (r_hi - r_lo + rpi - 1) / rpi : 0u;
+  const uint32_t uB = nA, uC = nA + nB;
+
+  if (producer) {
+    // =================== producer warp ===================
+    if (a.has_mixing && lane == 0) {
+      floe_ptx::mbar_arrive_expect_tx(&hbar, 4u * DH);
+      floe_ptx::bulk_g2s(hs, a.h, 4u * DH, &hbar);
+      const uint32_t row_bytes = DH * (a.mix_f16 ? 2u : 4u);
+      const uint8_t *m = static_cast<const uint8_t *>(a.mixing);
+      for (uint32_t i = 0; i < nA; ++i) {
+        const uint32_t r0 = r_lo + i * rpi, nr = min(rpi, r_hi - r0);
+        wait_empty(i);
+        issue(i, m + (size_t)r0 * row_bytes, nr * row_bytes);
+      }
+    }
+    __syncwarp();
+    abar();  // ALL#1: routing known
+    if (lane == 0)
+      for (uint32_t j = 0; j < nB; ++j) {
+        const TileRef tr = tile_ref(tile_lo + j, tps, a.di);
+        wait_empty(uB + j);
+        issue(uB + j, tiles_s[tr.slot] + (size_t)tr.t * TILE_B, TILE_B);
+      }
+    __syncwarp();
+    abar();  // ALL#2: K1 done, own list in smem
+    if (a.k1_only) {
+      abar();  // ALL#3
+      return;
+    }
+    // speculative prefetch of own records (before the plan is known)
+    uint32_t P = 0;
+    if (lane == 0) {
+      uint32_t j = 0, r = 0;
+      const uint32_t n_own = pv[4];
+      P = min(n_own, ns);
+      for (uint32_t k = 0; k < P; ++k) {
+        while (r >= tile_cnt[j]) {
+          ++j;
+          r = 0;
+        }
+        const uint32_t f = emit_f[kTileCh * j + r];
+        const uint32_t s = f / a.di, c = f % a.di;
+        const uint32_t u = uC + k;
+        wait_empty(u);
+        stage_scale[u % ns] = emit_v[kTileCh * j + r] * w_s[s];
+        issue(u, rec_s[s] + (size_t)c * 2 * DH, REC_B);
+        ++r;
+      }
+      pv[5] = P;
+    }
+    __syncwarp();
+    abar();  // ALL#3: plan known
+    const uint32_t own_b = pv[1], d_b = pv[2], D_b = pv[3], T = pv[0];
+    P = pv[5];
+    if (lane == 0) {  // remaining own records
+      uint32_t j = 0, r = 0;
+      for (uint32_t k = 0; k < own_b; ++k) {
+        while (r >= tile_cnt[j]) {
+          ++j;
+          r = 0;
+        }
+        if (k >= P) {
+          const uint32_t f = emit_f[kTileCh * j + r];
+          const uint32_t s = f / a.di, c = f % a.di;
+          const uint32_t u = uC + k;
+          wait_empty(u);
+          stage_scale[u % ns] = emit_v[kTileCh * j + r] * w_s[s];
+          issue(u, rec_s[s] + (size_t)c * 2 * DH, REC_B);
+        }
+        ++r;
+      }
+    }
+    __syncwarp();
+    // pool records: 32 resolved in parallel, issued by lane 0
+    const uint32_t E0 = max(P, own_b);
+    for (uint32_t q = 0; q < d_b; q += 32) {
+      const uint32_t pi = D_b + q + lane;
+      const __half *src = nullptr;
+      float scale = 0.0f;
+      if (q + lane < d_b) {
+        uint32_t lo = 0, hi = G;  // SUp[lo] <= pi < SUp[hi]
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (SUp[mid] <= pi) lo = mid;
+          else hi = mid;
+        }
+        const uint32_t bb = lo;
+        const uint32_t tb = (uint32_t)(((uint64_t)T * (bb + 1)) / G - ((uint64_t)T * bb) / G);
+        const uint32_t own_bb = min(NB[bb], tb);
+        const uint32_t first_tile = (uint32_t)(((uint64_t)NT * bb) / G);
+        const TileRef tr = tile_ref(first_tile, tps, a.di);
+        const uint32_t pos = tr.f0 + own_bb + (pi - SUp[bb]);
+        const uint32_t f = __ldcg(&a.kept_f[pos]);
+        const float v = __ldcg(&a.kept_v[pos]);
+        const uint32_t s = f / a.di, c = f % a.di;
+        src = rec_s[s] + (size_t)c * 2 * DH;
+        scale = v * w_s[s];
+      }
+      const uint32_t nq = min(32u, d_b - q);
+      for (uint32_t k = 0; k < nq; ++k) {
+        const unsigned long long sp =
+            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(src), k);
+        const float sc = __shfl_sync(0xffffffffu, scale, k);
+        if (lane == 0) {
+          const uint32_t u = uC + E0 + q + k;
+          wait_empty(u);
+          stage_scale[u % ns] = sc;
+          issue(u, reinterpret_cast<const void *>(sp), REC_B);
+        }
+        __syncwarp();
+      }
+    }
+    return;
+  }
+
+  // =================== consumer warps (threads 0..255) ===================
+  // expert descriptors, router slice
+  __shared__ ExpertDesc table_s[32];
+  const uint32_t n_table = a.has_mixing ? a.n_experts : a.slots;
+  if (t < n_table) table_s[t] = a.table[t];
+  const uint32_t nrows = r_hi - r_lo;
+  const bool rs_ok = a.has_mixing && nrows <= (uint32_t)kMaxRowsPerCta;
+  if (rs_ok)
+    for (uint32_t i = t; i < a.n_experts * kMaxRowsPerCta; i += kConsumers) {
+      const uint32_t e = i / kMaxRowsPerCta, lr = i % kMaxRowsPerCta;
+      if (lr < nrows) rs[i] = a.router[(size_t)e * DH + r_lo + lr];
+    }
+  cbar();
+
+  // ============================ phase A: mixing ============================
+  if (a.has_mixing) {
+    floe_ptx::mbar_wait(&hbar, 0, 3u << 28);
+    float pl = 0.0f;  // lane e < E: this warp's partial logit e
+    for (uint32_t i = warp; i < nA; i += kConsumerWarps) {
+      wait_full(i);
+      const uint32_t r0 = r_lo + i * rpi, nr = min(rpi, r_hi - r0);
+      float acc0 = 0.0f, acc1 = 0.0f;
+      if (a.mix_f16) {
+        const __half *row0 = reinterpret_cast<const __half *>(stage(i));
+        const __half *row1 = row0 + DH;
+        const bool two = nr > 1;
+#pragma unroll 4
+        for (uint32_t k = lane * 8; k < DH; k += 256) {
+          const float4 h0 = *reinterpret_cast<const float4 *>(hs + k);
+          const float4 h1 = *reinterpret_cast<const float4 *>(hs + k + 4);
+          const uint4 q0 = *reinterpret_cast<const uint4 *>(row0 + k);
+          const __half2 *p0 = reinterpret_cast<const __half2 *>(&q0);
+          float2 f;
+          f = __half22float2(p0[0]); acc0 = fmaf(f.x, h0.x, acc0); acc0 = fmaf(f.y, h0.y, acc0);
+          f = __half22float2(p0[1]); acc0 = fmaf(f.x, h0.z, acc0); acc0 = fmaf(f.y, h0.w, acc0);
+          f = __half22float2(p0[2]); acc0 = fmaf(f.x, h1.x, acc0); acc0 = fmaf(f.y, h1.y, acc0);
+          f = __half22float2(p0[3]); acc0 = fmaf(f.x, h1.z, acc0); acc0 = fmaf(f.y, h1.w, acc0);
+          if (two) {
+            const uint4 q1 = *reinterpret_cast<const uint4 *>(row1 + k);
+            const __half2 *p1 = reinterpret_cast<const __half2 *>(&q1);
+            f = __half22float2(p1[0]); acc1 = fmaf(f.x, h0.x, acc1); acc1 = fmaf(f.y, h0.y, acc1);
+            f = __half22float2(p1[1]); acc1 = fmaf(f.x, h0.z, acc1); acc1 = fmaf(f.y, h0.w, acc1);
+            f = __half22float2(p1[2]); acc1 = fmaf(f.x, h1.x, acc1); acc1 = fmaf(f.y, h1.y, acc1);
+            f = __half22float2(p1[3]); acc1 = fmaf(f.x, h1.z, acc1); acc1 = fmaf(f.y, h1.w, acc1);
+          }
+        }
+      } else {
+        const float *row0 = reinterpret_cast<const float *>(stage(i));
+#pragma unroll 4
+        for (uint32_t k = lane * 4; k < DH; k += 128) {
+          const float4 h0 = *reinterpret_cast<const float4 *>(hs + k);
+          const float4 q0 = *reinterpret_cast<const float4 *>(row0 + k);
+          acc0 = fmaf(q0.x, h0.x, acc0);
+          acc0 = fmaf(q0.y, h0.y, acc0);
+          acc0 = fmaf(q0.z, h0.z, acc0);
+          acc0 = fmaf(q0.w, h0.w, acc0);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        acc0 += __shfl_xor_sync(0xffffffffu, acc0, o);
+        acc1 += __shfl_xor_sync(0xffffffffu, acc1, o);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive1(&empty[i % ns]);  // stage fully read
+      for (uint32_t rr = 0; rr < nr; ++rr) {
+        const uint32_t row = r0 + rr;
+        const float uu = hs[row] + 1.0f * (rr ? acc1 : acc0);  // drift_scale 1 (model.cpp:151-152)
+        if (lane == 0) {
+          a.u[row] = uu;
+          a.y[row] = uu;
+          if (a.u_trace) a.u_trace[row] = uu;
+        }
+        if (lane < a.n_experts) {
+          const float w = rs_ok ? rs[lane * kMaxRowsPerCta + (row - r_lo)]
+                                : a.router[(size_t)lane * DH + row];
+          pl = fmaf(w, uu, pl);
+        }
+      }
+    }
+    plw[warp][lane] = pl;
+    cbar();
+    if (t < a.n_experts) {
+      float s = 0.0f;
+#pragma unroll
+      for (int w = 0; w < kConsumerWarps; ++w) s += plw[w][t];
+      a.partial[b * 32 + t] = s;
+    }
+    mark(a, 1);
+    cbar();
+    if (t == 0) grid_arrive_wait(a.bar, G);
+    cbar();
+    // route (model.cpp:83-93): every CTA sums the partials in the same order
+    for (uint32_t e = warp; e < a.n_experts; e += kConsumerWarps) {
+      float s = 0.0f;
+      for (uint32_t bb = lane; bb < G; bb += 32) s += __ldcg(&a.partial[bb * 32 + e]);
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) logits[e] = s;
+    }
+    cbar();
+    if (t == 0) {
+      uint32_t sel[32];
+      float wv[32];
+      floe_k::route_finish(logits, a.n_experts, a.top_k, sel, wv, b == 0 ? a.sel_trace : nullptr,
+                           b == 0 ? a.w_trace : nullptr);
+      for (uint32_t s = 0; s < a.slots; ++s) {
+        sel_s[s] = sel[s];
+        w_s[s] = wv[s];
+        if (b == 0 && a.sel_out) {
+          a.sel_out[s] = sel[s];
+          a.w_out[s] = wv[s];
+        }
+      }
+    }
+  } else {
+    if (t < a.slots) {
+      sel_s[t] = t;
+      w_s[t] = 1.0f;
+    }
+    if (b == 0 && a.y && !a.k1_only)
+      for (uint32_t i = t; i < DH; i += kConsumers) a.y[i] = 0.0f;  // before barrier 2
+  }
+  cbar();
+  if (t < a.slots) {
+    const ExpertDesc &d = table_s[sel_s[t]];
+    rec_s[t] = d.records;
+    tiles_s[t] = reinterpret_cast<const uint8_t *>(d.tiles);
+    thr_s[t] = a.use_threshold ? a.threshold : d.threshold;
+    slot_cnt[t] = 0;
+  }
+  mark(a, 2);
+  abar();  // ALL#1: the producer starts streaming K1 tiles
+
+  // ============================ phase B: K1 ================================
+  const float *xg = a.has_mixing ? a.u : a.x;
+  // x -> max|x| -> limbs (B fragments) + span sums
+  float mult = 0.0f, zx = 0.0f;
+  bool all_finite;
+  {
+    float xv[16];
+    const bool act = t < SPANS * 4;
+    const uint32_t span = t >> 2, tig = t & 3;
+    const float4 *x4 = reinterpret_cast<const float4 *>(xg + (act ? 64 * span + 16 * tig : 0));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float4 f = __ldcg(x4 + i);
+      xv[4 * i] = f.x;
+      xv[4 * i + 1] = f.y;
+      xv[4 * i + 2] = f.z;
+      xv[4 * i + 3] = f.w;
+    }
+    float mx = 0.0f;
+    bool fin = true;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      mx = fmaxf(mx, fabsf(xv[i]));
+      fin = fin && isfinite(xv[i]);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const bool wfin = __all_sync(0xffffffffu, fin);
+    if (lane == 0) redmax[warp] = wfin ? mx : -1.0f;
+    cbar();
+    all_finite = true;
+    mx = 0.0f;
+#pragma unroll
+    for (int w = 0; w < kConsumerWarps; ++w) {
+      all_finite = all_finite && redmax[w] >= 0.0f;
+      mx = fmaxf(mx, redmax[w]);
+    }
+    int ex = 0;
+    frexpf(mx, &ex);  // mx < 2^ex
+    const bool scaled = mx > 0.0f && all_finite;
+    const float S = scaled ? __int_as_float((127 + 22 - ex) << 23) : 1.0f;
+    const float invS = scaled ? __int_as_float((127 - 22 + ex) << 23) : 1.0f;
+    const uint32_t mytig = lane & 3;
+    mult = mytig == 0 ? invS : (mytig == 1 ? 65536.0f * invS : 0.0f);
+    zx = mytig == 0 ? 1.0f : 0.0f;
+    if (act) {
+      if (all_finite) {
+        int X[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) X[i] = __float2int_rn(xv[i] * S);
+        const uint32_t p = span >> 1, sodd = span & 1;
+        uint4 *xt = reinterpret_cast<uint4 *>(xtab) + (p * 2 + sodd) * 16;
+#pragma unroll
+        for (int n = 0; n < 3; ++n) {
+          uint32_t wd[4];  // (m, j) = (0,0), (0,1), (1,0), (1,1)
+#pragma unroll
+          for (int mj = 0; mj < 4; ++mj) {
+            const int m = mj >> 1, j = mj & 1;
+            uint32_t w = 0;
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) {
+              const int v = X[4 * bb + 2 * m + j];
+              const int l0 = ((v + 128) & 255) - 128;
+              const int r1 = (v - l0) >> 8;
+              const int l1 = ((r1 + 128) & 255) - 128;
+              const int l2 = (r1 - l1) >> 8;
+              const int l = n == 0 ? l0 : (n == 1 ? l1 : l2);
+              w |= (uint32_t)(l & 255) << (8 * bb);
+            }
+            wd[mj] = w;
+          }
+          xt[4 * n + tig] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+        }
+        xt[12 + tig] = make_uint4(0, 0, 0, 0);  // columns 3..7 (lanes >= 12) read zeros
+      } else {
+        float *xf = hs + 64 * span + 16 * tig;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) xf[i] = xv[i];
+      }
+    }
+    float s16 = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s16 += xv[i];
+    s16 += __shfl_xor_sync(0xffffffffu, s16, 1);
+    s16 += __shfl_xor_sync(0xffffffffu, s16, 2);
+    if (act && tig == 0) xs[span] = s16;
+  }
+  cbar();
+
+  // tile j (stage use uB + j) belongs to warp (uB + j) % 8: with ns a multiple
+  // of 8, every stage is consumed by ONE warp in phases A and B, so a warp
+  // never waits on a stage whose previous fill it has not consumed itself
+  // (mbarrier parity waits cannot tell phase k from phase k+2).
+  for (uint32_t j = (warp + kConsumerWarps - uB % kConsumerWarps) % kConsumerWarps; j < nB;
+       j += kConsumerWarps) {
+    const uint32_t u = uB + j;
+    const TileRef tr = tile_ref(tile_lo + j, tps, a.di);
+    wait_full(u);
+    const float2 v2 = all_finite ? k1_tile<DH>(stage(u), xtab, xs, mult, zx, lane)
+                                 : k1_tile_f32<DH>(stage(u), hs, lane);
+    __syncwarp();
+    if (lane == 0) mbar_arrive1(&empty[u % ns]);
+    const uint32_t g = lane >> 2;
+    const bool q0 = (lane & 3) == 0;
+    const float thr = thr_s[tr.slot];
+    // model.cpp:135: `if (fabs(v) < t) continue;` -> ties and NaN are kept
+    const bool va = q0 && g < tr.nc, vb = q0 && g + 8 < tr.nc;
+    const bool ka = va && !(fabsf(v2.x) < thr), kb = vb && !(fabsf(v2.y) < thr);
+    const size_t o = (size_t)tr.f0;
+    if (a.v_out) {
+      if (va) a.v_out[o + g] = v2.x;
+      if (vb) a.v_out[o + g + 8] = v2.y;
+    }
+    if (a.mask_out) {
+      if (va) a.mask_out[o + g] = ka ? 1 : 0;
+      if (vb) a.mask_out[o + g + 8] = kb ? 1 : 0;
+    }
+    const uint32_t ba = __ballot_sync(0xffffffffu, ka), bbal = __ballot_sync(0xffffffffu, kb);
+    const uint32_t lt = (1u << lane) - 1;
+    const uint32_t na = __popc(ba);
+    if (ka) {
+      emit_f[kTileCh * j + __popc(ba & lt)] = tr.f0 + g;
+      emit_v[kTileCh * j + __popc(ba & lt)] = v2.x;
+    }
+    if (kb) {
+      emit_f[kTileCh * j + na + __popc(bbal & lt)] = tr.f0 + g + 8;
+      emit_v[kTileCh * j + na + __popc(bbal & lt)] = v2.y;
+    }
+    if (lane == 0) tile_cnt[j] = na + __popc(bbal);
+  }
+  mark(a, 3);
+  cbar();
+  // own-list totals (warp 0), per-slot counts
+  if (warp == 0) {
+    uint32_t n = 0;
+    for (uint32_t j = lane; j < nB; j += 32) {
+      n += tile_cnt[j];
+      atomicAdd(&slot_cnt[tile_ref(tile_lo + j, tps, a.di).slot], tile_cnt[j]);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+    if (lane == 0) pv[4] = n;
+  }
+  cbar();
+  abar();  // ALL#2: the producer prefetches own records
+
+  // publish: compacted own list at the CTA's flattened start, per-slot counts
+  const uint32_t F_b = nB ? tile_ref(tile_lo, tps, a.di).f0 : 0u;
+  {
+    // tile prefix by warp 0 (nB <= max_tiles), then copy by all warps
+    uint32_t *tpref = reinterpret_cast<uint32_t *>(ws8);  // reuse: only when nB <= 8
+    (void)tpref;
+    uint32_t base = 0;
+    for (uint32_t j = 0; j < nB; ++j) {
+      const uint32_t cnt = tile_cnt[j];
+      if ((j % kConsumerWarps) == warp && lane < cnt) {
+        a.kept_f[F_b + base + lane] = emit_f[kTileCh * j + lane];
+        a.kept_v[F_b + base + lane] = emit_v[kTileCh * j + lane];
+      }
+      base += cnt;
+    }
+    for (uint32_t s = t; s < a.slots; s += kConsumers) a.seg_count[s * G + b] = slot_cnt[s];
+  }
+  cbar();
+  if (t == 0) grid_arrive_wait(a.bar, G);
+  cbar();
+  mark(a, 4);
+
+  // ------------------------------ the plan ---------------------------------
+  // n_bb per CTA; targets t_bb = T(bb+1)/G - T bb/G; own_bb = min(n_bb, t_bb);
+  // surplus entries own_bb..n_bb-1 of every CTA form the pool, handed out to
+  // deficits t_bb - own_bb in CTA order.
+  uint32_t nb_t = 0;
+  if (t < G)
+    for (uint32_t s = 0; s < a.slots; ++s) nb_t += __ldcg(&a.seg_count[s * G + t]);
+  uint32_t T;
+  const uint32_t npre = cscan(nb_t, ws8, &T);
+  (void)npre;
+  uint32_t sur = 0, def = 0;
+  if (t < G) {
+    NB[t] = nb_t;
+    const uint32_t tb = (uint32_t)(((uint64_t)T * (t + 1)) / G - ((uint64_t)T * t) / G);
+    const uint32_t own = min(nb_t, tb);
+    sur = nb_t - own;
+    def = tb - own;
+  }
+  uint32_t SUT, DT;
+  const uint32_t su_pre = cscan(sur, ws8, &SUT);
+  const uint32_t d_pre = cscan(def, ws8, &DT);
+  if (t < G) SUp[t] = su_pre;
+  if (t == 0) SUp[G] = SUT;
+  if (t == b) {
+    pv[0] = T;
+    pv[1] = nb_t - sur;  // own_b
+    pv[2] = def;         // d_b
+    pv[3] = d_pre;       // D_b
+  }
+  if (b == 0) {
+    if (t == 0 && a.stats) {
+      atomicAdd(&a.stats[0], 1ull);
+      atomicAdd(&a.stats[1], (unsigned long long)T);
+    }
+    if (a.n_kept_out && warp < a.slots) {
+      uint32_t n = 0;
+      for (uint32_t bb = lane; bb < G; bb += 32) n += __ldcg(&a.seg_count[warp * G + bb]);
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+      if (lane == 0) a.n_kept_out[warp] = n;
+    }
+  }
+  if (a.kept_out && warp < a.slots) {
+    // own entries of slot `warp` -> kept_out[slot][prefix over lower CTAs + j]
+    uint32_t base = 0;
+    for (uint32_t bb = lane; bb < b; bb += 32) base += __ldcg(&a.seg_count[warp * G + bb]);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) base += __shfl_xor_sync(0xffffffffu, base, o);
+    uint32_t k = 0;
+    for (uint32_t j = 0; j < nB; ++j) {
+      const TileRef tr = tile_ref(tile_lo + j, tps, a.di);
+      const uint32_t cnt = tile_cnt[j];
+      if (tr.slot == warp) {
+        if (lane < cnt) a.kept_out[(size_t)warp * a.di + base + k + lane] = emit_f[kTileCh * j + lane] - warp * a.di;
+        k += cnt;
+      }
+    }
+  }
+  cbar();
+  abar();  // ALL#3: the producer streams the rest
+  if (a.k1_only) return;
+
+  // ============================ phase C: K2 ================================
+  const uint32_t own_b = pv[1], d_b = pv[2], P = pv[5];
+  const uint32_t E0 = max(P, own_b);
+  const uint32_t n_items = E0 + d_b;
+  const bool active = t < (uint32_t)TPB2;
+  float2 x2[8], y2[8];
+  {
+    const uint32_t tt = active ? t : 0;
+    const float4 *xa = reinterpret_cast<const float4 *>(xg + 8 * tt);
+    const float4 *xb = reinterpret_cast<const float4 *>(xg + 8 * (tt + TPB2));
+    const float4 q0 = __ldcg(xa), q1 = __ldcg(xa + 1), q2 = __ldcg(xb), q3 = __ldcg(xb + 1);
+    x2[0] = make_float2(q0.x, q0.y);
+    x2[1] = make_float2(q0.z, q0.w);
+    x2[2] = make_float2(q1.x, q1.y);
+    x2[3] = make_float2(q1.z, q1.w);
+    x2[4] = make_float2(q2.x, q2.y);
+    x2[5] = make_float2(q2.z, q2.w);
+    x2[6] = make_float2(q3.x, q3.y);
+    x2[7] = make_float2(q3.z, q3.w);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) y2[i] = make_float2(0.0f, 0.0f);
+  }
+  uint32_t batch = 0;
+  uint32_t processed = 0;
+  for (uint32_t q0 = 0; q0 < n_items; q0 += kR, ++batch) {
+    uint4 dv[kR][2];
+    float gp[kR], sc[kR];
+    bool proc[kR];
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      gp[r] = 0.0f;
+      sc[r] = 0.0f;
+      dv[r][0] = dv[r][1] = make_uint4(0, 0, 0, 0);
+      const uint32_t k = q0 + r;
+      proc[r] = k < n_items && (k >= E0 || k < own_b);
+      if (k < n_items) {
+        const uint32_t u = uC + k;
+        wait_full(u);
+        sc[r] = stage_scale[u % ns];
+        if (active && proc[r]) {
+          const uint4 *rec = reinterpret_cast<const uint4 *>(stage(u));
+          const uint4 g0 = rec[t], g1 = rec[t + TPB2];
+          dv[r][0] = rec[2 * TPB2 + t];
+          dv[r][1] = rec[3 * TPB2 + t];
+          const __half2 *h0 = reinterpret_cast<const __half2 *>(&g0);
+          const __half2 *h1 = reinterpret_cast<const __half2 *>(&g1);
+          float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            acc = __ffma2_rn(__half22float2(h0[jj]), x2[jj], acc);
+            acc = __ffma2_rn(__half22float2(h1[jj]), x2[4 + jj], acc);
+          }
+          gp[r] = acc.x + acc.y;
+        }
+      }
+    }
+    // transposed warp reduction of kR values: lanes 8r hold record r's warp sum
+#pragma unroll
+    for (int sft = 16, cnt = kR / 2; cnt >= 1; sft >>= 1, cnt >>= 1) {
+      const bool upper = (lane & sft) != 0;
+#pragma unroll
+      for (int r = 0; r < cnt; ++r) {
+        const float send = upper ? gp[r] : gp[r + cnt];
+        const float keep = upper ? gp[r + cnt] : gp[r];
+        gp[r] = keep + __shfl_xor_sync(0xffffffffu, send, sft);
+      }
+    }
+#pragma unroll
+    for (int sft = 32 / kR / 2; sft >= 1; sft >>= 1)
+      gp[0] += __shfl_xor_sync(0xffffffffu, gp[0], sft);
+    if ((lane & (32 / kR - 1)) == 0) red[warp][lane / (32 / kR)] = gp[0];
+    cbar();  // red complete; the batch's stages are fully read
+    if (t == 0)
+      for (int r = 0; r < kR; ++r)
+        if (q0 + r < n_items) mbar_arrive1(&empty[(uC + q0 + r) % ns]);
+    if (warp < (uint32_t)kR) {
+      float g = lane < (uint32_t)kConsumerWarps ? red[lane][warp] : 0.0f;
+#pragma unroll
+      for (int o = 4; o >= 1; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+      float scw = sc[0];
+#pragma unroll
+      for (int r = 1; r < kR; ++r)
+        if ((uint32_t)r == warp) scw = sc[r];
+      bool pw = proc[0];
+#pragma unroll
+      for (int r = 1; r < kR; ++r)
+        if ((uint32_t)r == warp) pw = proc[r];
+      if (lane == 0) aco_s[batch & 1][warp] = pw ? floe_k::silu_ref(g) * scw : 0.0f;
+    }
+    cbar();  // aco_s visible
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      if (!proc[r]) continue;
+      ++processed;
+      const float aco = aco_s[batch & 1][r];
+      const float2 a2 = make_float2(aco, aco);
+      const __half2 *e0 = reinterpret_cast<const __half2 *>(&dv[r][0]);
+      const __half2 *e1 = reinterpret_cast<const __half2 *>(&dv[r][1]);
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        y2[jj] = __ffma2_rn(a2, __half22float2(e0[jj]), y2[jj]);
+        y2[4 + jj] = __ffma2_rn(a2, __half22float2(e1[jj]), y2[4 + jj]);
+      }
+    }
+  }
+  mark(a, 5);
+  if (processed > 0 && active) {
+    float *ya = a.y + 8 * t, *yb = a.y + 8 * (t + TPB2);
+    floe_k::red_add_v4(ya, y2[0].x, y2[0].y, y2[1].x, y2[1].y);
+    floe_k::red_add_v4(ya + 4, y2[2].x, y2[2].y, y2[3].x, y2[3].y);
+    floe_k::red_add_v4(yb, y2[4].x, y2[4].y, y2[5].x, y2[5].y);
+    floe_k::red_add_v4(yb + 4, y2[6].x, y2[6].y, y2[7].x, y2[7].y);
+  }
+}
+
+}  // namespace floe_v2
