@@ -15,6 +15,8 @@ import numpy as np
 
 _HERE = Path(__file__).resolve().parent
 _LIB_PATH = _HERE / "libfloe_b200.so"
+if os.environ.get("FLOE_LIB"):  # A/B builds of the same ABI (tools/, never the default)
+    _LIB_PATH = Path(os.environ["FLOE_LIB"]).resolve()
 
 FLOE_OK = 0
 _STATUS = {1: "FLOE_ERR_INVALID", 2: "FLOE_ERR_CUDA", 3: "FLOE_ERR_OOM", 4: "FLOE_ERR_UNSUPPORTED"}

@@ -329,8 +329,8 @@ int launch_v2_dh(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) 
   const int64_t budget = (int64_t)optin - (int64_t)static_smem - (int64_t)other - 1024;
   // stages: a multiple of the consumer warp count (stage ownership in phases A/B)
   const uint32_t ns = (uint32_t)std::min<int64_t>(V::kMaxStages, budget / V::tile_bytes(DH)) /
-                      V::kConsumerWarps * V::kConsumerWarps;
-  if (ns < (uint32_t)V::kConsumerWarps)
+                      V::kPairs * V::kPairs;
+  if (ns < (uint32_t)V::kPairs)
     return fail(FLOE_ERR_UNSUPPORTED, "fused path: shared memory too small for the ring");
   const uint32_t smem = V::smem_layout(DH, ns, max_tiles, G).total;
 
@@ -369,6 +369,11 @@ int launch_v2_dh(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) 
   a.phase_ns = ws->phase_ns;
   a.ns = ns;
   a.max_tiles = max_tiles;
+  static const uint32_t dbg = [] {
+    const char *d = std::getenv("FLOE_DEBUG_FLAGS");
+    return d ? (uint32_t)std::atoi(d) : 0u;
+  }();
+  a.debug = dbg;
 
   if (int rc = set_smem(V::fused<DH>, smem)) return rc;
   void *kargs[] = {&a};
@@ -377,11 +382,19 @@ int launch_v2_dh(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) 
   cfg.blockDim = dim3(V::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;  // grid barriers need co-residency
   attr[0].val.cooperative = 1;
+  // programmatic dependent launch: back-to-back calls overlap the next
+  // grid's prologue and weight prefetch with this one's drain
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  static const bool pdl_env = [] {
+    const char *p = std::getenv("FLOE_PDL");
+    return !(p && std::strcmp(p, "0") == 0);
+  }();
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = (pdl_env && !ws->profiling) ? 2 : 1;
   StageScope prof(ws, kStageFused, st);
   const cudaError_t e =
       cudaLaunchKernelExC(&cfg, reinterpret_cast<const void *>(V::fused<DH>), kargs);
@@ -446,6 +459,9 @@ int floe_gpu_expert_create(const floe_expert_host_view *v, floe_gpu_expert **out
     return fail(FLOE_ERR_INVALID,
                 "expert_create: give exactly one of gate_f32+down_f32 or records_f16");
   const bool on_device = (v->flags & FLOE_VIEW_DEVICE) != 0;
+  // Device-resident inputs may still be in flight on the caller's streams
+  // (e.g. quantize just launched): creation is not a hot path, so wait.
+  if (on_device) CK(cudaDeviceSynchronize());
 
   auto *e = new (std::nothrow) floe_gpu_expert();
   if (!e) return fail(FLOE_ERR_OOM, "expert_create: host allocation failed");
@@ -715,6 +731,7 @@ int floe_gpu_workspace_read_phase_trace(floe_gpu_workspace *w, uint64_t *out, ui
   if (!w->phase_ns) return fail(FLOE_ERR_INVALID, "workspace_read_phase_trace: tracing is off");
   CK(cudaDeviceSynchronize());
   CK(cudaMemcpy(out, w->phase_ns, 8ull * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemset(w->phase_ns, 0, 8ull * floe_v2::kTraceSlots * device_info().sm));  // fresh marks
   return FLOE_OK;
 }
 
@@ -882,6 +899,10 @@ int floe_gpu_layer_create(const floe_layer_host_view *v, floe_gpu_layer **out) {
   }
   auto *l = new (std::nothrow) floe_gpu_layer();
   if (!l) return fail(FLOE_ERR_OOM, "layer_create: host allocation failed");
+  if (cudaDeviceSynchronize() != cudaSuccess) {  // router/mixing may be device tensors in flight
+    delete l;
+    return fail(FLOE_ERR_CUDA, "layer_create: device synchronisation failed");
+  }
   l->dh = v->d_hidden;
   l->di = e0->di;
   l->E = v->n_experts;

@@ -39,6 +39,8 @@
 // is built in the same order once per call.
 #pragma once
 
+#include <type_traits>
+
 #include "floe_kernels.cuh"
 #include "floe_ptx.cuh"
 
@@ -48,12 +50,17 @@ using floe_k::ExpertDesc;
 using floe_k::h2f;
 
 constexpr int kTileCh = 16;
-constexpr int kConsumerWarps = 8;
-constexpr int kConsumers = 32 * kConsumerWarps;   // 256
+constexpr int kConsumerWarps = 16;
+constexpr int kConsumers = 32 * kConsumerWarps;   // 512
 constexpr int kThreads = kConsumers + 32;         // + 1 producer warp
-constexpr int kMaxStages = 24;  // ring stages: a multiple of kConsumerWarps (see phase B)
+constexpr int kPairs = kConsumerWarps / 2;        // stage owners in phases A/B: warps p, p+8
+constexpr int kMaxStages = 24;  // ring stages: a multiple of kPairs (see phase B)
+constexpr int kMaxStagesC = 24; // phase-C ring (records), carved over ring + staging area
 constexpr int kMaxGrid = 256;                     // plan scans: one value per consumer
-constexpr int kR = 4;                             // phase-C records per consumer barrier
+#ifndef FLOE_KR
+#define FLOE_KR 2
+#endif
+constexpr int kR = FLOE_KR;                             // phase-C records per consumer barrier
 constexpr int kMaxRowsPerCta = 32;                // phase-A router slice in smem
 
 __host__ __device__ constexpr uint32_t tile_bytes(uint32_t dh) { return 5u * dh; }
@@ -146,10 +153,16 @@ __device__ __forceinline__ void span_step(float2 &acc, uint32_t wa, uint32_t wb,
 // return the same pair.
 template <int DH>
 __device__ __forceinline__ float2 k1_tile(const uint8_t *stage, const uint8_t *xtab,
-                                          const float *xs, float mult, float zx, uint32_t lane) {
-  constexpr int PAIRS = DH / 128;
+                                          const float *xs, float mult, float zx, uint32_t lane,
+                                          uint32_t half) {
+  constexpr int PAIRS = DH / 256;  // span pairs of this half of the tile
+  stage += half * PAIRS * 32 * 16;
+  const uint32_t moff = half * PAIRS * 8 * 16;
+  xtab += half * PAIRS * 32 * 16;
+  xs += half * PAIRS * 2;
   const uint4 *cw = reinterpret_cast<const uint4 *>(stage) + lane;
-  const uint4 *mw = reinterpret_cast<const uint4 *>(stage + 4 * DH) + (lane >> 2);
+  const uint4 *mw = reinterpret_cast<const uint4 *>(stage + 4 * DH - half * PAIRS * 32 * 16 + moff) +
+                    (lane >> 2);
   const uint4 *xw = reinterpret_cast<const uint4 *>(xtab) + (lane < 12 ? lane : 12);
   float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll 4
@@ -172,12 +185,13 @@ __device__ __forceinline__ float2 k1_tile(const uint8_t *stage, const uint8_t *x
 // expression float(code)*scale + zero per element, so NaN/inf propagate exactly
 // as in qgemv_channels.  xf = x in shared memory.
 template <int DH>
-__device__ __noinline__ float2 k1_tile_f32(const uint8_t *stage, const float *xf, uint32_t lane) {
+__device__ __noinline__ float2 k1_tile_f32(const uint8_t *stage, const float *xf, uint32_t lane,
+                                           uint32_t half) {
   const uint32_t *cw = reinterpret_cast<const uint32_t *>(stage);
   const uint32_t *mw = reinterpret_cast<const uint32_t *>(stage + 4 * DH);
   const uint32_t g = lane >> 2, tig = lane & 3;
   float2 acc = make_float2(0.0f, 0.0f);
-  for (uint32_t span = 0; span < DH / 64; ++span) {
+  for (uint32_t span = half * DH / 128; span < (half + 1) * DH / 128; ++span) {
     const uint32_t p = span / 2, hi = span & 1;
     for (uint32_t r = 0; r < 2; ++r) {
       const uint32_t kidx = hi * 2 + r;
@@ -202,16 +216,33 @@ __device__ __noinline__ float2 k1_tile_f32(const uint8_t *stage, const float *xf
 // Named barriers.  __syncwarp() first: an inline-asm barrier is not a
 // reconvergence point for the compiler, and a warp arriving diverged would be
 // counted twice.
-__device__ __forceinline__ void cbar() {
+__device__ __forceinline__ void cbar() {  // consumers
   __syncwarp();
-  asm volatile("barrier.sync 1, 256;" ::: "memory");
+  asm volatile("barrier.sync 1, %0;" ::"n"(kConsumers) : "memory");
 }
-__device__ __forceinline__ void abar() {
+__device__ __forceinline__ void abar() {  // consumers + producer
   __syncwarp();
-  asm volatile("barrier.sync 2, 288;" ::: "memory");
+  asm volatile("barrier.sync 2, %0;" ::"n"(kThreads) : "memory");
+}
+__device__ __forceinline__ void pbar(uint32_t pair) {  // the two warps of a pair
+  __syncwarp();
+  asm volatile("barrier.sync %0, 64;" ::"r"(3 + pair) : "memory");
+}
+__device__ __forceinline__ void gbar(uint32_t grp) {  // phase C: one 8-warp record group
+  __syncwarp();
+  asm volatile("barrier.sync %0, 256;" ::"r"(11 + grp) : "memory");
 }
 
 __device__ __forceinline__ void mbar_arrive1(uint64_t *bar) { floe_ptx::mbar_arrive(bar); }
+
+// Programmatic dependent launch: the next fused launch on the stream may start
+// its prologue (barrier init, weight prefetch) while this grid drains; it
+// waits for this grid's completion before touching anything this grid
+// writes or reads (workspace, h/x, y).
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
@@ -238,9 +269,9 @@ __device__ __forceinline__ void grid_arrive_wait(unsigned long long *bar, uint32
   __threadfence();
 }
 
-// Exclusive scan over the 256 consumer threads (one value each); returns the
-// prefix, writes the total to *total.  Uses ws[8] shared scratch; contains
-// two consumer barriers.
+// Exclusive scan over the consumer threads (one value each); returns the
+// prefix, writes the total to *total.  Uses ws[kConsumerWarps] shared
+// scratch; contains two consumer barriers.
 __device__ __forceinline__ uint32_t cscan(uint32_t v, uint32_t *ws, uint32_t *total) {
   const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
   uint32_t inc = v;
@@ -299,11 +330,12 @@ struct FusedArgs {
   unsigned long long *phase_ns;  // nullable [G][kTraceSlots]
   uint32_t ns;        // ring stages
   uint32_t max_tiles; // per-CTA tile capacity of the smem emit buffer
+  uint32_t debug;     // diagnostics (FLOE_DEBUG_FLAGS): bit 1 = phase C waits only, no math
 };
 
 // Dynamic shared memory layout (bytes), host and device agree.
 struct SmemLayout {
-  uint32_t ring, uni, xs, emit_f, emit_v, tile_cnt, plan, scale, total;
+  uint32_t ring, uni, xs, emit_f, emit_v, tile_cnt, plan, scale, isrc, iscale, total;
 };
 
 __host__ __device__ inline SmemLayout smem_layout(uint32_t dh, uint32_t ns, uint32_t max_tiles,
@@ -317,13 +349,18 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t dh, uint32_t ns, uint
   L.emit_v = o;   o += 4u * kTileCh * max_tiles;
   L.tile_cnt = o; o += 4u * max_tiles + 16;
   L.plan = o;     o += 4u * 3 * (G + 1);
-  L.scale = o;    o += 4u * ns;
+  L.scale = o;    o += 0;  // (phase-C scales live in static shared memory)
+  o = (o + 7u) & ~7u;
+  L.isrc = o;     o += 8u * kTileCh * max_tiles;  // own records: source address
+  L.iscale = o;   o += 4u * kTileCh * max_tiles;  //              v * routing weight
   L.total = (o + 127u) & ~127u;
   return L;
 }
 
+// Phase trace (diagnostics): %globaltimer at fixed points, consumer thread 0
+// (marks 0..13) and producer lane 0 (marks 16..23).
 __device__ __forceinline__ void mark(const FusedArgs &a, int k) {
-  if (a.phase_ns && (threadIdx.x == 0) && k < kTraceSlots)
+  if (a.phase_ns && (threadIdx.x == 0 || threadIdx.x == kConsumers) && k < kTraceSlots)
     a.phase_ns[blockIdx.x * kTraceSlots + k] = gtime();
 }
 
@@ -346,9 +383,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   constexpr uint32_t TILE_B = tile_bytes(DH);
   constexpr uint32_t REC_B = 4 * DH;
   constexpr uint32_t SPANS = DH / 64;
-  constexpr int TPB2 = DH / 16;  // phase-C threads owning 16 elements each
+  static_assert(DH == 4096 || DH == 2048, "d_hidden 4096 or 2048");
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
+  __shared__ uint64_t fullC[kMaxStagesC], emptyC[kMaxStagesC];
+  __shared__ float stage_scale[kMaxStagesC];
   __shared__ uint64_t hbar;
   __shared__ float rs[32 * kMaxRowsPerCta];
   __shared__ float plw[kConsumerWarps][32];
@@ -359,9 +398,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   __shared__ const uint8_t *tiles_s[floe_k::kMaxSlots];
   __shared__ float thr_s[floe_k::kMaxSlots];
   __shared__ uint32_t ws8[kConsumerWarps];
+  __shared__ float2 xch[kPairs][2][8];  // phase B: upper-half partials of a pair's tile
   __shared__ float redmax[kConsumerWarps];
-  __shared__ float red[kConsumerWarps][kR];
-  __shared__ float aco_s[2][kR];
+  __shared__ float red[2][2][8][kR];  // [group][batch parity][warp][record]
   __shared__ uint32_t pv[8];  // plan values: 0 T, 1 own_b, 2 d_b, 3 D_b, 4 n_own, 5 P, 6 all_finite
   __shared__ uint32_t slot_cnt[floe_k::kMaxSlots];
 
@@ -376,10 +415,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   uint32_t *emit_f = reinterpret_cast<uint32_t *>(smem + L.emit_f);
   float *emit_v = reinterpret_cast<float *>(smem + L.emit_v);
   uint32_t *tile_cnt = reinterpret_cast<uint32_t *>(smem + L.tile_cnt);
+  const __half **isrc = reinterpret_cast<const __half **>(smem + L.isrc);
+  float *iscale = reinterpret_cast<float *>(smem + L.iscale);
   uint32_t *NB = reinterpret_cast<uint32_t *>(smem + L.plan);  // [G+1] per-CTA counts
   uint32_t *SUp = NB + (G + 1);                                // [G+1] surplus prefix
   uint32_t *TBp = SUp + (G + 1);                               // [G+1] unused spare
-  float *stage_scale = reinterpret_cast<float *>(smem + L.scale);
   (void)TBp;
   const uint32_t ns = a.ns;
 
@@ -395,15 +435,40 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
     floe_ptx::mbar_arrive_expect_tx(&full[u % ns], bytes);
     floe_ptx::bulk_g2s(stage(u), src, bytes, &full[u % ns]);
   };
+  // Phase C re-carves the ring plus the x-table area (both free once every K1
+  // tile is consumed) into 4*DH-byte record stages with their own barriers:
+  // 11 records (176 KB) in flight at d_hidden 4096 instead of 8.
+  const uint32_t nsC = min((uint32_t)kMaxStagesC, (L.xs - L.ring) / REC_B);
+  auto stageC = [&](uint32_t k) { return ring + (k % nsC) * REC_B; };
+  auto wait_fullC = [&](uint32_t k) {
+    floe_ptx::mbar_wait(&fullC[k % nsC], (k / nsC) & 1u, (4u << 28) | k);
+  };
+  auto wait_emptyC = [&](uint32_t k) {
+    if (k >= nsC) floe_ptx::mbar_wait(&emptyC[k % nsC], ((k / nsC) + 1) & 1u, (5u << 28) | k);
+  };
+  auto issueC = [&](uint32_t k, const void *src, float scale) {
+    wait_emptyC(k);
+    if (k < 16) mark(a, 48 + (int)k);
+    stage_scale[k % nsC] = scale;
+    floe_ptx::mbar_arrive_expect_tx(&fullC[k % nsC], REC_B);
+    floe_ptx::bulk_g2s(stageC(k), src, REC_B, &fullC[k % nsC]);
+  };
 
   mark(a, 0);
   if (t == 0) {
     for (uint32_t s = 0; s < ns; ++s) {
       floe_ptx::mbar_init(&full[s], 1);
-      floe_ptx::mbar_init(&empty[s], 1);
+      // released by all 16 consumer warps: count 8 from each warp of the
+      // owning pair (phases A/B), 1 from every warp (phase C)
+      floe_ptx::mbar_init(&empty[s], kConsumerWarps);
+    }
+    for (uint32_t s = 0; s < nsC; ++s) {
+      floe_ptx::mbar_init(&fullC[s], 1);
+      floe_ptx::mbar_init(&emptyC[s], 8);  // the 8 warps of the record's group
     }
     floe_ptx::mbar_init(&hbar, 1);
     floe_ptx::fence_barrier_init();
+    pdl_launch_dependents();
   }
   __syncthreads();
 
@@ -420,18 +485,31 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   if (producer) {
     // =================== producer warp ===================
     if (a.has_mixing && lane == 0) {
-      floe_ptx::mbar_arrive_expect_tx(&hbar, 4u * DH);
-      floe_ptx::bulk_g2s(hs, a.h, 4u * DH, &hbar);
       const uint32_t row_bytes = DH * (a.mix_f16 ? 2u : 4u);
       const uint8_t *m = static_cast<const uint8_t *>(a.mixing);
+      // mixing rows are read-only weights: the first two stream in before the
+      // previous grid has finished (PDL); h (the previous layer's output)
+      // goes right after them so it is not queued behind the whole ring
+      const uint32_t early = min(nA, 2u);
       for (uint32_t i = 0; i < nA; ++i) {
+        if (i == early) {
+          pdl_wait();
+          floe_ptx::mbar_arrive_expect_tx(&hbar, 4u * DH);
+          floe_ptx::bulk_g2s(hs, a.h, 4u * DH, &hbar);
+        }
         const uint32_t r0 = r_lo + i * rpi, nr = min(rpi, r_hi - r0);
         wait_empty(i);
         issue(i, m + (size_t)r0 * row_bytes, nr * row_bytes);
       }
+      if (nA <= early) {
+        pdl_wait();
+        floe_ptx::mbar_arrive_expect_tx(&hbar, 4u * DH);
+        floe_ptx::bulk_g2s(hs, a.h, 4u * DH, &hbar);
+      }
     }
     __syncwarp();
     abar();  // ALL#1: routing known
+    mark(a, 16);
     if (lane == 0)
       for (uint32_t j = 0; j < nB; ++j) {
         const TileRef tr = tile_ref(tile_lo + j, tps, a.di);
@@ -447,47 +525,21 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
     // speculative prefetch of own records (before the plan is known)
     uint32_t P = 0;
     if (lane == 0) {
-      uint32_t j = 0, r = 0;
       const uint32_t n_own = pv[4];
-      P = min(n_own, ns);
-      for (uint32_t k = 0; k < P; ++k) {
-        while (r >= tile_cnt[j]) {
-          ++j;
-          r = 0;
-        }
-        const uint32_t f = emit_f[kTileCh * j + r];
-        const uint32_t s = f / a.di, c = f % a.di;
-        const uint32_t u = uC + k;
-        wait_empty(u);
-        stage_scale[u % ns] = emit_v[kTileCh * j + r] * w_s[s];
-        issue(u, rec_s[s] + (size_t)c * 2 * DH, REC_B);
-        ++r;
-      }
+      P = min(n_own, nsC);
+      for (uint32_t k = 0; k < P; ++k) issueC(k, isrc[k], iscale[k]);
       pv[5] = P;
     }
     __syncwarp();
+    mark(a, 17);
     abar();  // ALL#3: plan known
+    mark(a, 18);
     const uint32_t own_b = pv[1], d_b = pv[2], D_b = pv[3], T = pv[0];
     P = pv[5];
-    if (lane == 0) {  // remaining own records
-      uint32_t j = 0, r = 0;
-      for (uint32_t k = 0; k < own_b; ++k) {
-        while (r >= tile_cnt[j]) {
-          ++j;
-          r = 0;
-        }
-        if (k >= P) {
-          const uint32_t f = emit_f[kTileCh * j + r];
-          const uint32_t s = f / a.di, c = f % a.di;
-          const uint32_t u = uC + k;
-          wait_empty(u);
-          stage_scale[u % ns] = emit_v[kTileCh * j + r] * w_s[s];
-          issue(u, rec_s[s] + (size_t)c * 2 * DH, REC_B);
-        }
-        ++r;
-      }
-    }
+    if (lane == 0)  // remaining own records
+      for (uint32_t k = P; k < own_b; ++k) issueC(k, isrc[k], iscale[k]);
     __syncwarp();
+    mark(a, 19);
     // pool records: 32 resolved in parallel, issued by lane 0
     const uint32_t E0 = max(P, own_b);
     for (uint32_t q = 0; q < d_b; q += 32) {
@@ -519,14 +571,12 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
             __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(src), k);
         const float sc = __shfl_sync(0xffffffffu, scale, k);
         if (lane == 0) {
-          const uint32_t u = uC + E0 + q + k;
-          wait_empty(u);
-          stage_scale[u % ns] = sc;
-          issue(u, reinterpret_cast<const void *>(sp), REC_B);
+          issueC(E0 + q + k, reinterpret_cast<const void *>(sp), sc);
         }
         __syncwarp();
       }
     }
+    mark(a, 20);
     return;
   }
 
@@ -542,62 +592,55 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
       const uint32_t e = i / kMaxRowsPerCta, lr = i % kMaxRowsPerCta;
       if (lr < nrows) rs[i] = a.router[(size_t)e * DH + r_lo + lr];
     }
+  pdl_wait();  // from here on: workspace, inputs and outputs shared with the previous grid
   cbar();
 
   // ============================ phase A: mixing ============================
   if (a.has_mixing) {
     floe_ptx::mbar_wait(&hbar, 0, 3u << 28);
     float pl = 0.0f;  // lane e < E: this warp's partial logit e
-    for (uint32_t i = warp; i < nA; i += kConsumerWarps) {
+    const uint32_t pair = warp % kPairs, sub = warp / kPairs;
+    // item i (stage use i) belongs to pair i % 8; warp `sub` of the pair takes
+    // row `sub` of the item (f16: 2 rows per stage; f32: 1 row, sub 1 idles)
+    for (uint32_t i = pair; i < nA; i += kPairs) {
       wait_full(i);
       const uint32_t r0 = r_lo + i * rpi, nr = min(rpi, r_hi - r0);
+      const bool mine = sub < nr;
       float acc0 = 0.0f, acc1 = 0.0f;
-      if (a.mix_f16) {
-        const __half *row0 = reinterpret_cast<const __half *>(stage(i));
-        const __half *row1 = row0 + DH;
-        const bool two = nr > 1;
+      if (mine && a.mix_f16) {
+        const __half *row = reinterpret_cast<const __half *>(stage(i)) + sub * DH;
 #pragma unroll 4
         for (uint32_t k = lane * 8; k < DH; k += 256) {
           const float4 h0 = *reinterpret_cast<const float4 *>(hs + k);
           const float4 h1 = *reinterpret_cast<const float4 *>(hs + k + 4);
-          const uint4 q0 = *reinterpret_cast<const uint4 *>(row0 + k);
+          const uint4 q0 = *reinterpret_cast<const uint4 *>(row + k);
           const __half2 *p0 = reinterpret_cast<const __half2 *>(&q0);
           float2 f;
-          f = __half22float2(p0[0]); acc0 = fmaf(f.x, h0.x, acc0); acc0 = fmaf(f.y, h0.y, acc0);
-          f = __half22float2(p0[1]); acc0 = fmaf(f.x, h0.z, acc0); acc0 = fmaf(f.y, h0.w, acc0);
-          f = __half22float2(p0[2]); acc0 = fmaf(f.x, h1.x, acc0); acc0 = fmaf(f.y, h1.y, acc0);
-          f = __half22float2(p0[3]); acc0 = fmaf(f.x, h1.z, acc0); acc0 = fmaf(f.y, h1.w, acc0);
-          if (two) {
-            const uint4 q1 = *reinterpret_cast<const uint4 *>(row1 + k);
-            const __half2 *p1 = reinterpret_cast<const __half2 *>(&q1);
-            f = __half22float2(p1[0]); acc1 = fmaf(f.x, h0.x, acc1); acc1 = fmaf(f.y, h0.y, acc1);
-            f = __half22float2(p1[1]); acc1 = fmaf(f.x, h0.z, acc1); acc1 = fmaf(f.y, h0.w, acc1);
-            f = __half22float2(p1[2]); acc1 = fmaf(f.x, h1.x, acc1); acc1 = fmaf(f.y, h1.y, acc1);
-            f = __half22float2(p1[3]); acc1 = fmaf(f.x, h1.z, acc1); acc1 = fmaf(f.y, h1.w, acc1);
-          }
+          f = __half22float2(p0[0]); acc0 = fmaf(f.x, h0.x, acc0); acc1 = fmaf(f.y, h0.y, acc1);
+          f = __half22float2(p0[1]); acc0 = fmaf(f.x, h0.z, acc0); acc1 = fmaf(f.y, h0.w, acc1);
+          f = __half22float2(p0[2]); acc0 = fmaf(f.x, h1.x, acc0); acc1 = fmaf(f.y, h1.y, acc1);
+          f = __half22float2(p0[3]); acc0 = fmaf(f.x, h1.z, acc0); acc1 = fmaf(f.y, h1.w, acc1);
         }
-      } else {
-        const float *row0 = reinterpret_cast<const float *>(stage(i));
+      } else if (mine) {
+        const float *row = reinterpret_cast<const float *>(stage(i));
 #pragma unroll 4
         for (uint32_t k = lane * 4; k < DH; k += 128) {
           const float4 h0 = *reinterpret_cast<const float4 *>(hs + k);
-          const float4 q0 = *reinterpret_cast<const float4 *>(row0 + k);
+          const float4 q0 = *reinterpret_cast<const float4 *>(row + k);
           acc0 = fmaf(q0.x, h0.x, acc0);
-          acc0 = fmaf(q0.y, h0.y, acc0);
+          acc1 = fmaf(q0.y, h0.y, acc1);
           acc0 = fmaf(q0.z, h0.z, acc0);
-          acc0 = fmaf(q0.w, h0.w, acc0);
+          acc1 = fmaf(q0.w, h0.w, acc1);
         }
       }
+      float acc = acc0 + acc1;
 #pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) {
-        acc0 += __shfl_xor_sync(0xffffffffu, acc0, o);
-        acc1 += __shfl_xor_sync(0xffffffffu, acc1, o);
-      }
+      for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       __syncwarp();
-      if (lane == 0) mbar_arrive1(&empty[i % ns]);  // stage fully read
-      for (uint32_t rr = 0; rr < nr; ++rr) {
-        const uint32_t row = r0 + rr;
-        const float uu = hs[row] + 1.0f * (rr ? acc1 : acc0);  // drift_scale 1 (model.cpp:151-152)
+      if (lane == 0) floe_ptx::mbar_arrive_cnt(&empty[i % ns], kPairs);  // done with the stage
+      if (mine) {
+        const uint32_t row = r0 + sub;
+        const float uu = hs[row] + 1.0f * acc;  // drift_scale 1 (model.cpp:151-152)
         if (lane == 0) {
           a.u[row] = uu;
           a.y[row] = uu;
@@ -616,32 +659,74 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
       float s = 0.0f;
 #pragma unroll
       for (int w = 0; w < kConsumerWarps; ++w) s += plw[w][t];
-      a.partial[b * 32 + t] = s;
+      a.partial[t * kMaxGrid + b] = s;  // [expert][CTA]: coalesced reads below
     }
     mark(a, 1);
     cbar();
     if (t == 0) grid_arrive_wait(a.bar, G);
     cbar();
+    mark(a, 6);
     // route (model.cpp:83-93): every CTA sums the partials in the same order
     for (uint32_t e = warp; e < a.n_experts; e += kConsumerWarps) {
+      float pv8[kMaxGrid / 32];  // all loads in flight at once
+#pragma unroll
+      for (int j = 0; j < kMaxGrid / 32; ++j) {
+        const uint32_t bb = lane + 32 * j;
+        pv8[j] = bb < G ? __ldcg(&a.partial[e * kMaxGrid + bb]) : 0.0f;
+      }
       float s = 0.0f;
-      for (uint32_t bb = lane; bb < G; bb += 32) s += __ldcg(&a.partial[bb * 32 + e]);
+#pragma unroll
+      for (int j = 0; j < kMaxGrid / 32; ++j) s += pv8[j];
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if (lane == 0) logits[e] = s;
     }
     cbar();
-    if (t == 0) {
-      uint32_t sel[32];
-      float wv[32];
-      floe_k::route_finish(logits, a.n_experts, a.top_k, sel, wv, b == 0 ? a.sel_trace : nullptr,
-                           b == 0 ? a.w_trace : nullptr);
-      for (uint32_t s = 0; s < a.slots; ++s) {
-        sel_s[s] = sel[s];
-        w_s[s] = wv[s];
-        if (b == 0 && a.sel_out) {
-          a.sel_out[s] = sel[s];
-          a.w_out[s] = wv[s];
+    if (warp == 0) {
+      // top_k (la.cpp:48-61: ties to the lower index, output ascending) as k
+      // warp arg-max rounds; softmax over the selected logits (la.cpp:37-46)
+      const float lg = lane < a.n_experts ? logits[lane] : -__int_as_float(0x7f800000);
+      uint32_t taken = 0;
+      for (uint32_t r = 0; r < a.top_k; ++r) {
+        float bv = (taken >> lane) & 1u || lane >= a.n_experts ? -__int_as_float(0x7f800000) : lg;
+        uint32_t bi = lane < a.n_experts && !((taken >> lane) & 1u) ? lane : 64u;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+          const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ov > bv || (ov == bv && oi < bi)) {
+            bv = ov;
+            bi = oi;
+          }
+        }
+        taken |= 1u << bi;
+      }
+      if (lane == 0) {
+        float mx = -__int_as_float(0x7f800000), wv[floe_k::kMaxSlots];
+        uint32_t sl[floe_k::kMaxSlots], n = 0;
+        for (uint32_t m = taken; m; m &= m - 1) {
+          sl[n] = __ffs(m) - 1;
+          wv[n] = logits[sl[n]];
+          if (n == 0 || mx < wv[n]) mx = wv[n];
+          ++n;
+        }
+        float sum = 0.0f;
+        for (uint32_t i = 0; i < n; ++i) {
+          wv[i] = expf(wv[i] - mx);
+          sum += wv[i];
+        }
+        for (uint32_t i = 0; i < n; ++i) {
+          const float w = wv[i] / sum;
+          sel_s[i] = sl[i];
+          w_s[i] = w;
+          if (b == 0) {
+            if (a.sel_out) {
+              a.sel_out[i] = sl[i];
+              a.w_out[i] = w;
+            }
+            if (a.sel_trace) a.sel_trace[i] = sl[i];
+            if (a.w_trace) a.w_trace[i] = w;
+          }
         }
       }
     }
@@ -753,81 +838,89 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   }
   cbar();
 
-  // tile j (stage use uB + j) belongs to warp (uB + j) % 8: with ns a multiple
-  // of 8, every stage is consumed by ONE warp in phases A and B, so a warp
+  // tile j (stage use uB + j) belongs to pair (uB + j) % 8: with ns a multiple
+  // of 8, every stage is consumed by ONE pair in phases A and B, so a warp
   // never waits on a stage whose previous fill it has not consumed itself
-  // (mbarrier parity waits cannot tell phase k from phase k+2).
-  for (uint32_t j = (warp + kConsumerWarps - uB % kConsumerWarps) % kConsumerWarps; j < nB;
-       j += kConsumerWarps) {
-    const uint32_t u = uB + j;
-    const TileRef tr = tile_ref(tile_lo + j, tps, a.di);
-    wait_full(u);
-    const float2 v2 = all_finite ? k1_tile<DH>(stage(u), xtab, xs, mult, zx, lane)
-                                 : k1_tile_f32<DH>(stage(u), hs, lane);
-    __syncwarp();
-    if (lane == 0) mbar_arrive1(&empty[u % ns]);
-    const uint32_t g = lane >> 2;
-    const bool q0 = (lane & 3) == 0;
-    const float thr = thr_s[tr.slot];
-    // model.cpp:135: `if (fabs(v) < t) continue;` -> ties and NaN are kept
-    const bool va = q0 && g < tr.nc, vb = q0 && g + 8 < tr.nc;
-    const bool ka = va && !(fabsf(v2.x) < thr), kb = vb && !(fabsf(v2.y) < thr);
-    const size_t o = (size_t)tr.f0;
-    if (a.v_out) {
-      if (va) a.v_out[o + g] = v2.x;
-      if (vb) a.v_out[o + g + 8] = v2.y;
+  // (mbarrier parity waits cannot tell phase k from phase k+2).  Warp `sub`
+  // of the pair computes span half `sub`; the upper half's partials go
+  // through xch (double-buffered by the pair's tile parity) to the lower warp,
+  // which thresholds and emits.
+  {
+    const uint32_t pair = warp % kPairs, sub = warp / kPairs;
+    uint32_t n = 0;  // tiles this pair has done
+    for (uint32_t j = (pair + kPairs - uB % kPairs) % kPairs; j < nB; j += kPairs, ++n) {
+      const uint32_t u = uB + j;
+      const TileRef tr = tile_ref(tile_lo + j, tps, a.di);
+      wait_full(u);
+      if (n == 0 && warp == 0) mark(a, 7);
+      float2 v2 = all_finite ? k1_tile<DH>(stage(u), xtab, xs, mult, zx, lane, sub)
+                             : k1_tile_f32<DH>(stage(u), hs, lane, sub);
+      __syncwarp();
+      if (lane == 0) floe_ptx::mbar_arrive_cnt(&empty[u % ns], kPairs);
+      if (sub == 1 && (lane & 3) == 0) xch[pair][n & 1][lane >> 2] = v2;
+      pbar(pair);
+      if (sub == 1) continue;
+      const float2 o2 = xch[pair][n & 1][lane >> 2];
+      v2.x += o2.x;
+      v2.y += o2.y;
+      const uint32_t g = lane >> 2;
+      const bool q0 = (lane & 3) == 0;
+      const float thr = thr_s[tr.slot];
+      // model.cpp:135: `if (fabs(v) < t) continue;` -> ties and NaN are kept
+      const bool va = q0 && g < tr.nc, vb = q0 && g + 8 < tr.nc;
+      const bool ka = va && !(fabsf(v2.x) < thr), kb = vb && !(fabsf(v2.y) < thr);
+      const size_t o = (size_t)tr.f0;
+      if (a.v_out) {
+        if (va) a.v_out[o + g] = v2.x;
+        if (vb) a.v_out[o + g + 8] = v2.y;
+      }
+      if (a.mask_out) {
+        if (va) a.mask_out[o + g] = ka ? 1 : 0;
+        if (vb) a.mask_out[o + g + 8] = kb ? 1 : 0;
+      }
+      const uint32_t ba = __ballot_sync(0xffffffffu, ka), bbal = __ballot_sync(0xffffffffu, kb);
+      const uint32_t lt = (1u << lane) - 1;
+      const uint32_t na = __popc(ba);
+      if (ka) {
+        emit_f[kTileCh * j + __popc(ba & lt)] = tr.f0 + g;
+        emit_v[kTileCh * j + __popc(ba & lt)] = v2.x;
+      }
+      if (kb) {
+        emit_f[kTileCh * j + na + __popc(bbal & lt)] = tr.f0 + g + 8;
+        emit_v[kTileCh * j + na + __popc(bbal & lt)] = v2.y;
+      }
+      if (lane == 0) tile_cnt[j] = na + __popc(bbal);
     }
-    if (a.mask_out) {
-      if (va) a.mask_out[o + g] = ka ? 1 : 0;
-      if (vb) a.mask_out[o + g + 8] = kb ? 1 : 0;
-    }
-    const uint32_t ba = __ballot_sync(0xffffffffu, ka), bbal = __ballot_sync(0xffffffffu, kb);
-    const uint32_t lt = (1u << lane) - 1;
-    const uint32_t na = __popc(ba);
-    if (ka) {
-      emit_f[kTileCh * j + __popc(ba & lt)] = tr.f0 + g;
-      emit_v[kTileCh * j + __popc(ba & lt)] = v2.x;
-    }
-    if (kb) {
-      emit_f[kTileCh * j + na + __popc(bbal & lt)] = tr.f0 + g + 8;
-      emit_v[kTileCh * j + na + __popc(bbal & lt)] = v2.y;
-    }
-    if (lane == 0) tile_cnt[j] = na + __popc(bbal);
   }
   mark(a, 3);
   cbar();
-  // own-list totals (warp 0), per-slot counts
-  if (warp == 0) {
-    uint32_t n = 0;
-    for (uint32_t j = lane; j < nB; j += 32) {
-      n += tile_cnt[j];
-      atomicAdd(&slot_cnt[tile_ref(tile_lo + j, tps, a.di).slot], tile_cnt[j]);
-    }
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
-    if (lane == 0) pv[4] = n;
-  }
-  cbar();
-  abar();  // ALL#2: the producer prefetches own records
-
-  // publish: compacted own list at the CTA's flattened start, per-slot counts
+  // own list: totals, per-slot counts, the producer's issue list (record
+  // address, v * routing weight) in emission order, and the compacted list at
+  // the CTA's flattened start for the other CTAs (pool)
   const uint32_t F_b = nB ? tile_ref(tile_lo, tps, a.di).f0 : 0u;
   {
-    // tile prefix by warp 0 (nB <= max_tiles), then copy by all warps
-    uint32_t *tpref = reinterpret_cast<uint32_t *>(ws8);  // reuse: only when nB <= 8
-    (void)tpref;
     uint32_t base = 0;
     for (uint32_t j = 0; j < nB; ++j) {
       const uint32_t cnt = tile_cnt[j];
       if ((j % kConsumerWarps) == warp && lane < cnt) {
-        a.kept_f[F_b + base + lane] = emit_f[kTileCh * j + lane];
-        a.kept_v[F_b + base + lane] = emit_v[kTileCh * j + lane];
+        const TileRef tr = tile_ref(tile_lo + j, tps, a.di);
+        const uint32_t f = emit_f[kTileCh * j + lane];
+        const float v = emit_v[kTileCh * j + lane];
+        isrc[base + lane] = rec_s[tr.slot] + (size_t)(f - tr.slot * a.di) * 2 * DH;
+        iscale[base + lane] = v * w_s[tr.slot];
+        a.kept_f[F_b + base + lane] = f;
+        a.kept_v[F_b + base + lane] = v;
+        if (lane == 0) atomicAdd(&slot_cnt[tr.slot], cnt);
       }
       base += cnt;
     }
-    for (uint32_t s = t; s < a.slots; s += kConsumers) a.seg_count[s * G + b] = slot_cnt[s];
+    if (t == 0) pv[4] = base;
   }
   cbar();
+  abar();  // ALL#2: the producer prefetches own records
+  for (uint32_t s = t; s < a.slots; s += kConsumers) a.seg_count[s * G + b] = slot_cnt[s];
+  cbar();
+  mark(a, 8);
   if (t == 0) grid_arrive_wait(a.bar, G);
   cbar();
   mark(a, 4);
@@ -891,6 +984,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
     }
   }
   cbar();
+  mark(a, 9);
   abar();  // ALL#3: the producer streams the rest
   if (a.k1_only) return;
 
@@ -898,58 +992,72 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   const uint32_t own_b = pv[1], d_b = pv[2], P = pv[5];
   const uint32_t E0 = max(P, own_b);
   const uint32_t n_items = E0 + d_b;
-  const bool active = t < (uint32_t)TPB2;
-  float2 x2[8], y2[8];
+  // Two groups of 8 warps take alternate records (group g: items g, g+2, ...)
+  // so each record costs the bookkeeping of 8 warps, not 16; thread gt of a
+  // group owns elements [EPT2 gt, EPT2 gt + EPT2) of both record halves.
+  constexpr int EPT2 = DH / 256;  // 16 (d_hidden 4096) or 8
+  using Vec = typename std::conditional<EPT2 == 16, uint4, uint2>::type;  // EPT2/2 halves
+  const uint32_t grp = warp / 8, gw = warp % 8, gt = t % 256;
+  float2 x2[EPT2 / 2], y2[EPT2 / 2];
   {
-    const uint32_t tt = active ? t : 0;
-    const float4 *xa = reinterpret_cast<const float4 *>(xg + 8 * tt);
-    const float4 *xb = reinterpret_cast<const float4 *>(xg + 8 * (tt + TPB2));
-    const float4 q0 = __ldcg(xa), q1 = __ldcg(xa + 1), q2 = __ldcg(xb), q3 = __ldcg(xb + 1);
-    x2[0] = make_float2(q0.x, q0.y);
-    x2[1] = make_float2(q0.z, q0.w);
-    x2[2] = make_float2(q1.x, q1.y);
-    x2[3] = make_float2(q1.z, q1.w);
-    x2[4] = make_float2(q2.x, q2.y);
-    x2[5] = make_float2(q2.z, q2.w);
-    x2[6] = make_float2(q3.x, q3.y);
-    x2[7] = make_float2(q3.z, q3.w);
+    const float4 *xa = reinterpret_cast<const float4 *>(xg + EPT2 * gt);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) y2[i] = make_float2(0.0f, 0.0f);
+    for (int i = 0; i < EPT2 / 4; ++i) {
+      const float4 q = __ldcg(xa + i);
+      x2[2 * i] = make_float2(q.x, q.y);
+      x2[2 * i + 1] = make_float2(q.z, q.w);
+    }
+#pragma unroll
+    for (int i = 0; i < EPT2 / 2; ++i) y2[i] = make_float2(0.0f, 0.0f);
   }
-  uint32_t batch = 0;
-  uint32_t processed = 0;
-  for (uint32_t q0 = 0; q0 < n_items; q0 += kR, ++batch) {
-    uint4 dv[kR][2];
+  const uint32_t n_mine = n_items > grp ? (n_items - grp + 1) / 2 : 0u;
+  uint32_t stg = grp % nsC, ph = 0;  // ring position of item k = grp + 2i (no divisions)
+  uint32_t batch = 0, processed = 0;
+  for (uint32_t i0 = 0; i0 < n_mine; i0 += kR, ++batch) {
+    if (batch < 6 && grp == 0) mark(a, 24 + 4 * (int)batch);  // batch start
+    Vec dv[kR][2];
     float gp[kR], sc[kR];
     bool proc[kR];
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
       gp[r] = 0.0f;
       sc[r] = 0.0f;
-      dv[r][0] = dv[r][1] = make_uint4(0, 0, 0, 0);
-      const uint32_t k = q0 + r;
-      proc[r] = k < n_items && (k >= E0 || k < own_b);
-      if (k < n_items) {
-        const uint32_t u = uC + k;
-        wait_full(u);
-        sc[r] = stage_scale[u % ns];
-        if (active && proc[r]) {
-          const uint4 *rec = reinterpret_cast<const uint4 *>(stage(u));
-          const uint4 g0 = rec[t], g1 = rec[t + TPB2];
-          dv[r][0] = rec[2 * TPB2 + t];
-          dv[r][1] = rec[3 * TPB2 + t];
+      dv[r][0] = dv[r][1] = Vec{};
+      const uint32_t k = grp + 2 * (i0 + r);
+      proc[r] = i0 + r < n_mine && (k >= E0 || k < own_b);
+      if (i0 + r < n_mine) {
+        floe_ptx::mbar_wait(&fullC[stg], ph, (4u << 28) | k);
+        if (k == 0) mark(a, 10);
+        sc[r] = stage_scale[stg];
+        Vec g0{}, g1{};
+        if (proc[r] && !(a.debug & 2u)) {
+          const Vec *rec = reinterpret_cast<const Vec *>(ring + stg * REC_B);
+          g0 = rec[2 * gt];
+          g1 = rec[2 * gt + 1];
+          dv[r][0] = rec[512 + 2 * gt];
+          dv[r][1] = rec[512 + 2 * gt + 1];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive1(&emptyC[stg]);  // this warp's slice is in registers
+        if (proc[r]) {
           const __half2 *h0 = reinterpret_cast<const __half2 *>(&g0);
           const __half2 *h1 = reinterpret_cast<const __half2 *>(&g1);
           float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
+          for (int jj = 0; jj < EPT2 / 4; ++jj) {
             acc = __ffma2_rn(__half22float2(h0[jj]), x2[jj], acc);
-            acc = __ffma2_rn(__half22float2(h1[jj]), x2[4 + jj], acc);
+            acc = __ffma2_rn(__half22float2(h1[jj]), x2[EPT2 / 4 + jj], acc);
           }
           gp[r] = acc.x + acc.y;
         }
+        stg += 2;
+        if (stg >= nsC) {
+          stg -= nsC;
+          ph ^= 1u;
+        }
       }
     }
+    if (batch < 6 && grp == 0) mark(a, 25 + 4 * (int)batch);  // batch data in registers
     // transposed warp reduction of kR values: lanes 8r hold record r's warp sum
 #pragma unroll
     for (int sft = 16, cnt = kR / 2; cnt >= 1; sft >>= 1, cnt >>= 1) {
@@ -964,48 +1072,46 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
 #pragma unroll
     for (int sft = 32 / kR / 2; sft >= 1; sft >>= 1)
       gp[0] += __shfl_xor_sync(0xffffffffu, gp[0], sft);
-    if ((lane & (32 / kR - 1)) == 0) red[warp][lane / (32 / kR)] = gp[0];
-    cbar();  // red complete; the batch's stages are fully read
-    if (t == 0)
-      for (int r = 0; r < kR; ++r)
-        if (q0 + r < n_items) mbar_arrive1(&empty[(uC + q0 + r) % ns]);
-    if (warp < (uint32_t)kR) {
-      float g = lane < (uint32_t)kConsumerWarps ? red[lane][warp] : 0.0f;
+    if ((lane & (32 / kR - 1)) == 0) red[grp][batch & 1][gw][lane / (32 / kR)] = gp[0];
+    gbar(grp);  // the group's partials for this batch (double-buffered: one barrier)
+    if (batch < 6 && grp == 0) mark(a, 26 + 4 * (int)batch);
+    // lane l: record r = l / 8, warp partial l % 8 -> lanes 8r finish record r
+    // (block sum in a fixed order, silu, scale) and broadcast its coefficient
+    float g = red[grp][batch & 1][lane % 8][min(lane / 8, (uint32_t)kR - 1)];
+    g += __shfl_xor_sync(0xffffffffu, g, 4);
+    g += __shfl_xor_sync(0xffffffffu, g, 2);
+    g += __shfl_xor_sync(0xffffffffu, g, 1);
+    float scl = sc[0];
+    bool pl = proc[0];
 #pragma unroll
-      for (int o = 4; o >= 1; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
-      float scw = sc[0];
-#pragma unroll
-      for (int r = 1; r < kR; ++r)
-        if ((uint32_t)r == warp) scw = sc[r];
-      bool pw = proc[0];
-#pragma unroll
-      for (int r = 1; r < kR; ++r)
-        if ((uint32_t)r == warp) pw = proc[r];
-      if (lane == 0) aco_s[batch & 1][warp] = pw ? floe_k::silu_ref(g) * scw : 0.0f;
-    }
-    cbar();  // aco_s visible
+    for (int r = 1; r < kR; ++r)
+      if (lane / 8 == (uint32_t)r) {
+        scl = sc[r];
+        pl = proc[r];
+      }
+    const float myaco = pl ? floe_k::silu_ref(g) * scl : 0.0f;
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
+      const float aco = __shfl_sync(0xffffffffu, myaco, 8 * r);
       if (!proc[r]) continue;
       ++processed;
-      const float aco = aco_s[batch & 1][r];
       const float2 a2 = make_float2(aco, aco);
       const __half2 *e0 = reinterpret_cast<const __half2 *>(&dv[r][0]);
       const __half2 *e1 = reinterpret_cast<const __half2 *>(&dv[r][1]);
 #pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {
+      for (int jj = 0; jj < EPT2 / 4; ++jj) {
         y2[jj] = __ffma2_rn(a2, __half22float2(e0[jj]), y2[jj]);
-        y2[4 + jj] = __ffma2_rn(a2, __half22float2(e1[jj]), y2[4 + jj]);
+        y2[EPT2 / 4 + jj] = __ffma2_rn(a2, __half22float2(e1[jj]), y2[EPT2 / 4 + jj]);
       }
     }
+    if (batch < 6 && grp == 0) mark(a, 27 + 4 * (int)batch);  // batch done
   }
   mark(a, 5);
-  if (processed > 0 && active) {
-    float *ya = a.y + 8 * t, *yb = a.y + 8 * (t + TPB2);
-    floe_k::red_add_v4(ya, y2[0].x, y2[0].y, y2[1].x, y2[1].y);
-    floe_k::red_add_v4(ya + 4, y2[2].x, y2[2].y, y2[3].x, y2[3].y);
-    floe_k::red_add_v4(yb, y2[4].x, y2[4].y, y2[5].x, y2[5].y);
-    floe_k::red_add_v4(yb + 4, y2[6].x, y2[6].y, y2[7].x, y2[7].y);
+  if (processed > 0) {
+    float *yo = a.y + EPT2 * gt;
+#pragma unroll
+    for (int i = 0; i < EPT2 / 4; ++i)
+      floe_k::red_add_v4(yo + 4 * i, y2[2 * i].x, y2[2 * i].y, y2[2 * i + 1].x, y2[2 * i + 1].y);
   }
 }
 

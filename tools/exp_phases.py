@@ -1,8 +1,6 @@
-"""Per-phase timing of the fused kernel via in-kernel %globaltimer marks.
-
-Prints, for layer mode and single-expert mode, the distribution over CTAs of
-each phase's duration (us) and the launch skew, averaged over several steps.
-"""
+"""Per-phase timing of the fused kernel via in-kernel %globaltimer marks
+(floe_v2.cuh mark()): distribution over CTAs of each interval, averaged over
+several flushed steps, for layer mode and single-expert mode."""
 import sys
 from pathlib import Path
 
@@ -13,25 +11,31 @@ sys.path.insert(0, str(ROOT))
 
 import bench  # noqa: E402
 
+# consumer marks: 0 start, 1 phase A done, 6 barrier-1 passed, 2 routed, 7 first K1
+# tile landed, 3 K1 done, 8 published, 4 barrier-2 passed, 9 plan done, 10 first
+# record landed, 11 first pool record landed, 5 phase C done.
+# producer marks: 16 K1 issue start, 17 prefetch issued, 18 plan seen, 19 own
+# issued, 20 all issued.
+LAYER = [(0, 1, "A mixing"), (1, 6, "grid barrier 1"), (6, 2, "route"),
+         (2, 7, "first K1 tile lands"), (7, 3, "K1 tiles"), (3, 8, "publish"),
+         (8, 4, "grid barrier 2"), (4, 9, "plan"), (9, 10, "first record"),
+         (10, 11, "own records"), (11, 5, "pool records"), (16, 17, "P: K1 issue+prefetch"),
+         (18, 19, "P: own issue"), (19, 20, "P: pool issue")]
+EXPERT = [(0, 2, "start -> K1")] + LAYER[3:]
+
 
 def summarize(tag, traces, marks):
-    # traces: list of [G, 8] arrays
-    T = np.stack(traces).astype(np.int64)  # [steps, G, 8]
-    t0 = T[:, :, 0].min(axis=1, keepdims=True)
+    T = np.stack(traces).astype(np.int64)  # [steps, G, 64]
+    t0 = T[:, :, 0].min(axis=1)
     print(f"== {tag}: {T.shape[0]} steps, {T.shape[1]} CTAs")
-    print(f"   launch skew (max start - min start): {np.mean(T[:, :, 0].max(1) - T[:, :, 0].min(1)) / 1e3:7.2f} us")
     for (a, b, name) in marks:
-        d = (T[:, :, b] - T[:, :, a]) / 1e3
-        print(f"   {name:28s} mean {d.mean():7.2f}  min {d.min():7.2f}  max {d.max():7.2f} us")
-    end = (T[:, :, 5].max(1) - t0[:, 0]) / 1e3
+        ok = (T[:, :, a] > 0) & (T[:, :, b] > 0)
+        if not ok.any():
+            continue
+        d = ((T[:, :, b] - T[:, :, a]) / 1e3)[ok]
+        print(f"   {name:24s} mean {d.mean():7.2f}  min {d.min():7.2f}  max {d.max():7.2f} us")
+    end = (T[:, :, 5].max(1) - t0) / 1e3
     print(f"   first start -> last phase-C end: {end.mean():7.2f} us")
-    # phase-C record arrivals (after each wait) relative to phase-C start, CTA 0 and 100
-    for cta in (0, 100):
-        arr = T[-1, cta, 8:]
-        base = T[-1, cta, 4]
-        rel = [(x - base) / 1e3 for x in arr if x > base]
-        print(f"   CTA {cta:3d} phase-C record arrivals (us): " +
-              " ".join(f"{v:.1f}" for v in rel[:40]))
 
 
 def main():
@@ -39,37 +43,43 @@ def main():
 
     import paper_2505_05950_b200 as fb
     torch.cuda.set_device(0)
-    flush = torch.zeros(64 << 20, dtype=torch.float32, device="cuda")
-    sink = torch.zeros(1, device="cuda")
-    router, mixing, experts = bench.build_layer(fb, torch)
     ws = fb.Workspace(bench.DH, bench.DI, bench.TOPK)
-    bench.calibrate(fb, torch, router, mixing, experts, ws)
-    layer = fb.GpuLayer(router.cpu().numpy(), mixing.cpu().numpy(), experts, bench.TOPK)
+    layers, experts0 = [], []
+    for li in range(bench.N_LAYERS):  # distinct layers cycled: nothing L2-resident
+        router, mixing, experts = bench.build_layer(fb, torch, li)
+        bench.calibrate(fb, torch, router, mixing, experts, ws)
+        layers.append(fb.GpuLayer(router.cpu().numpy(), mixing.cpu().numpy(), experts,
+                                  bench.TOPK))
+        experts0.append(experts[0])
     toks = torch.stack([fb.gen_normals(1, (1 << 40) + t, bench.DH) for t in range(12)])
     y = torch.empty(bench.DH, device="cuda")
-    ws.set_phase_trace(True)
-    traces = []
-    for i in range(12):
-        sink.copy_(flush.sum())
-        fb.layer_forward(layer, toks[i], ws, out=y)
-        torch.cuda.synchronize()
-        if i >= 2:
-            traces.append(ws.read_phase_trace())
-    summarize("layer (clean L2)", traces,
-              [(0, 1, "A mixing"), (1, 2, "barrier1 + route"), (2, 3, "B K1 (2 experts)"),
-               (3, 4, "barrier2"), (4, 5, "C K2")])
     ws1 = fb.Workspace(bench.DH, bench.DI, 1)
-    ws1.set_phase_trace(True)
-    traces = []
-    for i in range(12):
-        sink.copy_(flush.sum())
-        fb.expert_forward_sparse(experts[0], toks[i], ws1, out=y)
-        torch.cuda.synchronize()
-        if i >= 2:
-            traces.append(ws1.read_phase_trace())
-    summarize("expert (clean L2)", traces,
-              [(0, 2, "start -> K1"), (2, 3, "B K1"), (3, 4, "barrier2"), (4, 5, "C K2")])
+    for name, w, run, marks in (
+            ("layer", ws, lambda i: fb.layer_forward(layers[i % 4], toks[i], ws, out=y), LAYER),
+            ("expert", ws1, lambda i: fb.expert_forward_sparse(experts0[i % 4], toks[i], ws1,
+                                                               out=y), EXPERT)):
+        w.set_phase_trace(True)
+        traces = []
+        for i in range(12):
+            run(i)
+            torch.cuda.synchronize()
+            if i >= 2:
+                traces.append(w.read_phase_trace())
+            else:
+                w.read_phase_trace()
+        summarize(name, traces, marks)
+        T = np.stack(traces).astype(np.int64)
+        for cta in (0, 37, 100):
+            tr = T[-1, cta]
+            base = tr[48]
+            iss = [(tr[48 + k] - base) / 1e3 for k in range(16) if tr[48 + k]]
+            bat = [tuple((tr[24 + 4 * i + j] - base) / 1e3 for j in range(4)) for i in range(6)
+                   if tr[24 + 4 * i]]
+            print(f"   CTA {cta}: issue " + " ".join(f"{v:.1f}" for v in iss))
+            print("          batches (start,ready,barrier,done) " +
+                  " ".join("(" + ",".join(f"{x:.2f}" for x in b4) + ")" for b4 in bat))
 
 
 if __name__ == "__main__":
     main()
+
