@@ -57,10 +57,26 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
   return ok != 0;
 }
 
+// Non-blocking probe of a phase (mbarrier.test_wait never suspends).
+__device__ __forceinline__ bool mbar_test_wait(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
 // Watchdog: a wait that has not completed after kWatchdogNs is a protocol
 // bug (a copy never issued, a barrier count mismatch).  Report the site and
 // trap so the launch fails loudly instead of hanging the device.
-constexpr unsigned long long kWatchdogNs = 4000000000ull;
+#ifndef FLOE_WATCHDOG_NS
+#define FLOE_WATCHDOG_NS 4000000000ull
+#endif
+constexpr unsigned long long kWatchdogNs = FLOE_WATCHDOG_NS;
 
 __device__ __forceinline__ unsigned long long now_ns() {
   unsigned long long t;

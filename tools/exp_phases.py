@@ -36,6 +36,16 @@ def summarize(tag, traces, marks):
         print(f"   {name:24s} mean {d.mean():7.2f}  min {d.min():7.2f}  max {d.max():7.2f} us")
     end = (T[:, :, 5].max(1) - t0) / 1e3
     print(f"   first start -> last phase-C end: {end.mean():7.2f} us")
+    names = {0: "start", 1: "A done", 6: "barrier1 out", 2: "routed", 7: "1st tile", 3: "K1 done",
+             8: "published", 18: "P: all published", 5: "C done"}
+    for m, nm in names.items():
+        v = T[:, :, m]
+        if not (v > 0).any():
+            continue
+        rel = (v - t0[:, None]) / 1e3
+        rel = rel[v > 0]
+        q = np.percentile(rel, [0, 10, 50, 90, 100])
+        print(f"   t[{nm:16s}] min {q[0]:6.2f} p10 {q[1]:6.2f} med {q[2]:6.2f} p90 {q[3]:6.2f} max {q[4]:6.2f}")
 
 
 def main():
