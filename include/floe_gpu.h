@@ -71,8 +71,10 @@ typedef struct floe_gpu_layer floe_gpu_layer;
 typedef struct floe_gpu_predictor floe_gpu_predictor;
 
 /* Host view of one compressed expert: the fields of floe::CompressedExpert
- * (core/include/floe/model.hpp:60-70) as raw arrays.  Exactly one of
- * {gate_f32 + down_f32} or {records_f16} must be given:
+ * (core/include/floe/model.hpp:60-70) as raw arrays.  At most one of
+ * {gate_f32 + down_f32} or {records_f16} may be given; with neither, the
+ * handle holds only the up projection (qgemv_channels / predict_mask /
+ * dequantize_up on a bare QuantizedTensor) and forward calls fail:
  *   gate_f32 / down_f32: f32 [d_intermediate][d_hidden] channel-major, as the
  *       reference stores them; converted to f16 on the device with IEEE RNE
  *       (identical to floe::f32_to_f16, core/src/io.cpp:19-51).
@@ -110,6 +112,13 @@ int floe_gpu_abi_version(void);
 /* Device properties of the current device; fails if it is not sm_100. */
 int floe_gpu_device_info(int *sm_count, int *cc_major, int *cc_minor,
                          size_t *total_mem);
+
+/* Device memory and copies for callers that do not link the CUDA runtime
+ * (the C++ value-type API, FFI bindings).  floe_gpu_copy is cudaMemcpyDefault
+ * on `stream` followed by a synchronisation of that stream. */
+int floe_gpu_device_malloc(void **ptr, size_t bytes);
+int floe_gpu_device_free(void *ptr);
+int floe_gpu_copy(void *dst, const void *src, size_t bytes, floe_stream_t stream);
 
 /* ---------------------------------------------------------------- experts */
 int floe_gpu_expert_create(const floe_expert_host_view *view,

@@ -67,6 +67,9 @@ _F = ct.c_float
 _SIGS = {
     "floe_gpu_last_error": (ct.c_char_p, []),
     "floe_gpu_abi_version": (ct.c_int, []),
+    "floe_gpu_device_malloc": (ct.c_int, [_P, ct.c_size_t]),
+    "floe_gpu_device_free": (ct.c_int, [_P]),
+    "floe_gpu_copy": (ct.c_int, [_P, _P, ct.c_size_t, _P]),
     "floe_gpu_device_info": (ct.c_int, [_P, _P, _P, _P]),
     "floe_gpu_expert_create": (ct.c_int, [ct.POINTER(ExpertHostView), ct.POINTER(_P)]),
     "floe_gpu_expert_destroy": (ct.c_int, [_P]),

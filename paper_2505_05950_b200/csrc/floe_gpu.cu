@@ -119,6 +119,7 @@ struct floe_gpu_expert {
   ExpertDesc host_desc{};
   ExpertDesc *dev_desc = nullptr;
   bool fast = false;  // tile-fragment layout + fused kernel
+  bool up_only = false;  // no gate/down records (qgemv_channels / predict_mask only)
 };
 
 enum { kStageMixing = 0, kStageRoute = 1, kStageK1 = 2, kStageK2 = 3, kStageFused = 4, kStages = 5 };
@@ -440,6 +441,29 @@ int floe_gpu_device_info(int *sm_count, int *cc_major, int *cc_minor, size_t *to
   return FLOE_OK;
 }
 
+int floe_gpu_device_malloc(void **ptr, size_t bytes) {
+  if (!ptr) return fail(FLOE_ERR_INVALID, "device_malloc: null argument");
+  *ptr = nullptr;
+  if (int rc = require_device("device_malloc")) return rc;
+  if (bytes == 0) return FLOE_OK;
+  CK(cudaMalloc(ptr, bytes));
+  return FLOE_OK;
+}
+
+int floe_gpu_device_free(void *ptr) {
+  if (ptr) CK(cudaFree(ptr));
+  return FLOE_OK;
+}
+
+int floe_gpu_copy(void *dst, const void *src, size_t bytes, floe_stream_t stream) {
+  if (bytes == 0) return FLOE_OK;
+  if (!dst || !src) return fail(FLOE_ERR_INVALID, "copy: null argument");
+  if (int rc = require_device("copy")) return rc;
+  CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, S(stream)));
+  CK(cudaStreamSynchronize(S(stream)));
+  return FLOE_OK;
+}
+
 // ---------------------------------------------------------------- experts --
 int floe_gpu_expert_create(const floe_expert_host_view *v, floe_gpu_expert **out) {
   if (!v || !out) return fail(FLOE_ERR_INVALID, "expert_create: null argument");
@@ -455,9 +479,12 @@ int floe_gpu_expert_create(const floe_expert_host_view *v, floe_gpu_expert **out
   if (!v->codes || !v->scales || !v->zeros)
     return fail(FLOE_ERR_INVALID, "expert_create: codes/scales/zeros required");
   const bool have_f32 = v->gate_f32 && v->down_f32;
-  if (have_f32 == (v->records_f16 != nullptr))
+  if (have_f32 && v->records_f16)
     return fail(FLOE_ERR_INVALID,
-                "expert_create: give exactly one of gate_f32+down_f32 or records_f16");
+                "expert_create: give at most one of gate_f32+down_f32 or records_f16");
+  if ((v->gate_f32 != nullptr) != (v->down_f32 != nullptr))
+    return fail(FLOE_ERR_INVALID, "expert_create: gate_f32 and down_f32 go together");
+  const bool up_only = !have_f32 && !v->records_f16;  // qgemv / predict_mask only
   const bool on_device = (v->flags & FLOE_VIEW_DEVICE) != 0;
   // Device-resident inputs may still be in flight on the caller's streams
   // (e.g. quantize just launched): creation is not a hot path, so wait.
@@ -482,7 +509,8 @@ int floe_gpu_expert_create(const floe_expert_host_view *v, floe_gpu_expert **out
   const uint64_t o_scales = up256(o_codes + e->code_bytes);
   const uint64_t o_zeros = up256(o_scales + 2 * e->n_groups);
   const uint64_t o_rec = e->fast ? up256(o_codes + tile_total) : up256(o_zeros + 2 * e->n_groups);
-  const uint64_t total = o_rec + 4 * n;
+  e->up_only = up_only;
+  const uint64_t total = o_rec + (up_only ? 0 : 4 * n);
   cudaError_t ce = cudaMalloc(&e->block, total);
   if (ce != cudaSuccess) {
     delete e;
@@ -498,7 +526,7 @@ int floe_gpu_expert_create(const floe_expert_host_view *v, floe_gpu_expert **out
     e->host_desc.scales = reinterpret_cast<const uint16_t *>(base + o_scales);
     e->host_desc.zeros = reinterpret_cast<const uint16_t *>(base + o_zeros);
   }
-  e->host_desc.records = reinterpret_cast<const __half *>(base + o_rec);
+  e->host_desc.records = up_only ? nullptr : reinterpret_cast<const __half *>(base + o_rec);
   e->host_desc.threshold = v->threshold;
 
   auto cleanup = [&](int rc) {
@@ -548,7 +576,9 @@ int floe_gpu_expert_create(const floe_expert_host_view *v, floe_gpu_expert **out
     cp(base + o_zeros, v->zeros, 2 * e->n_groups);
   }
   __half *rec = reinterpret_cast<__half *>(base + o_rec);
-  if (v->records_f16) {
+  if (up_only) {
+    // nothing to upload
+  } else if (v->records_f16) {
     cp(rec, v->records_f16, 4 * n);
   } else if (on_device) {
     if (err == cudaSuccess) {
@@ -768,6 +798,8 @@ int floe_gpu_expert_forward_sparse(const floe_gpu_expert *e, floe_gpu_workspace 
                                    uint8_t *mask_out, uint32_t *kept_out,
                                    uint32_t *n_kept_out, floe_stream_t stream) {
   if (!e || !x || !y) return fail(FLOE_ERR_INVALID, "expert_forward_sparse: null argument");
+  if (e->up_only)
+    return fail(FLOE_ERR_INVALID, "expert_forward_sparse: expert was created without gate/down");
   if (int rc = check_ws("expert_forward_sparse", ws, e->dh, e->di, 1)) return rc;
   if (e->fast) {
     FusedLaunch f{};
@@ -896,6 +928,7 @@ int floe_gpu_layer_create(const floe_layer_host_view *v, floe_gpu_layer **out) {
     const floe_gpu_expert *e = v->experts[i];
     if (!e || e->dh != v->d_hidden || e->di != e0->di || e->bits != e0->bits || e->g != e0->g)
       return fail(FLOE_ERR_INVALID, "layer_create: expert %u shape differs from the layer", i);
+    if (e->up_only) return fail(FLOE_ERR_INVALID, "layer_create: expert %u has no gate/down", i);
   }
   auto *l = new (std::nothrow) floe_gpu_layer();
   if (!l) return fail(FLOE_ERR_OOM, "layer_create: host allocation failed");

@@ -53,6 +53,7 @@ def test_sm100a_only_and_bulk_copy_in_sass():
                           text=True, check=True).stdout
     assert "UBLKCP" in sass  # cp.async.bulk (TMA engine) staging in K1/K2
     assert "FFMA2" in sass   # packed fp32x2 math (sm_100)
+    assert "IMMA.16832.S8.S8" in sass  # K1: exact integer tensor-core up projection
 
 
 def test_compute_fails_loudly_without_gpu():
