@@ -213,11 +213,11 @@ class Workspace:
 
     def read_phase_trace(self) -> np.ndarray:
         """[grid, 8] %globaltimer ns marks of the fused kernel's last call."""
-        out = np.zeros(64 * 1024, np.uint64)
+        out = np.zeros(96 * 1024, np.uint64)
         grid = ct.c_uint32()
         _check(lib().floe_gpu_workspace_read_phase_trace(self.handle, out.ctypes.data, out.size,
                                                          ct.byref(grid)))
-        return out[: 64 * grid.value].reshape(grid.value, 64)
+        return out[: 96 * grid.value].reshape(grid.value, 96)
 
     def read_profile(self) -> dict:
         ms = (ct.c_double * 5)()

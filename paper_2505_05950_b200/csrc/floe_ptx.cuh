@@ -45,14 +45,18 @@ __device__ __forceinline__ void mbar_arrive_cnt(uint64_t *bar, uint32_t count) {
                : "memory");
 }
 
+// try_wait with a suspend-time hint: a waiting thread sleeps (it is woken
+// when the phase completes) instead of re-polling, so spinning waiters --
+// notably the producer warp, which shares SMSP 0 with consumer warps -- do
+// not steal issue slots.
 __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(20000u)
       : "memory");
   return ok != 0;
 }

@@ -64,7 +64,7 @@ constexpr int kR = FLOE_KR;                             // phase-C records per c
 constexpr int kMaxRowsPerCta = 32;                // phase-A router slice in smem
 
 __host__ __device__ constexpr uint32_t tile_bytes(uint32_t dh) { return 5u * dh; }
-__host__ __device__ constexpr uint32_t xtab_bytes(uint32_t dh) { return (dh / 128u) * 2u * 16u * 16u; }
+__host__ __device__ constexpr uint32_t xtab_bytes(uint32_t dh) { return (dh / 128u) * 2u * 32u * 16u; }
 __host__ __device__ inline uint32_t tiles_per_expert(uint32_t di) { return (di + kTileCh - 1) / kTileCh; }
 
 // ------------------------------------------------------------ layout kernels
@@ -135,18 +135,31 @@ __device__ __forceinline__ void imma16832(int (&c)[4], uint32_t a0, uint32_t a1,
 }
 
 // One 64-element span of 16 channels: wa/wb = this lane's code word of rows
-// g / g+8, xb = the lane's B fragments (limb column groupID) for the span's two
+// g / g+8, xb = the lane's B fragments (column groupID) for the span's two
 // IMMAs, mg/mg8 = scale|zero of rows g / g+8.
+//
+// Code extraction in two classes, without per-class shifts: bits 0-1 of each
+// byte (`& 0x03030303`, class x1: codes 4b+0 / 4b+2) and bits 2-3 left in
+// place (`& 0x0C0C0C0C`, class x4: 4 * codes 4b+1 / 4b+3), one shift by 4
+// for the second IMMA -- 5 ops per code word instead of 7.  The classes sit
+// in the k-halves of each IMMA; the B columns separate them (columns 0,1,4
+// carry limbs 0,1,2 of the class-x1 elements and are zero on class-x4 rows,
+// columns 2,3,6 the converse), so lane tig of a quad holds one class and
+// limb pair and scales it by its own constant `mult` (1, 1/4, 65536, 16384
+// times 1/S).
 __device__ __forceinline__ void span_step(float2 &acc, uint32_t wa, uint32_t wb, uint4 xb,
                                           uint32_t mg, uint32_t mg8, float zxs, float mult) {
-  constexpr uint32_t M = 0x03030303u;
+  constexpr uint32_t M1 = 0x03030303u, M4 = 0x0C0C0C0Cu;
   int c[4] = {0, 0, 0, 0};
-  imma16832(c, wa & M, wb & M, (wa >> 2) & M, (wb >> 2) & M, xb.x, xb.y);
-  imma16832(c, (wa >> 4) & M, (wb >> 4) & M, (wa >> 6) & M, (wb >> 6) & M, xb.z, xb.w);
-  const float tg = (float)(c[0] + 256 * c[1]);   // exact: |.| < 2^23
-  const float tg8 = (float)(c[2] + 256 * c[3]);
-  acc.x = fmaf(h2f((uint16_t)(mg & 0xffffu)) * mult, tg, fmaf(h2f((uint16_t)(mg >> 16)), zxs, acc.x));
-  acc.y = fmaf(h2f((uint16_t)(mg8 & 0xffffu)) * mult, tg8, fmaf(h2f((uint16_t)(mg8 >> 16)), zxs, acc.y));
+  imma16832(c, wa & M1, wb & M1, wa & M4, wb & M4, xb.x, xb.y);
+  const uint32_t wa4 = wa >> 4, wb4 = wb >> 4;
+  imma16832(c, wa4 & M1, wb4 & M1, wa4 & M4, wb4 & M4, xb.z, xb.w);
+  // exact in f32: |c0 + 256 c1| < 2^24 for every class/limb pair
+  const float2 t2 = make_float2((float)(c[0] + 256 * c[1]), (float)(c[2] + 256 * c[3]));
+  const float2 s2 = __fmul2_rn(make_float2(h2f((uint16_t)(mg & 0xffffu)), h2f((uint16_t)(mg8 & 0xffffu))),
+                               make_float2(mult, mult));
+  const float2 z2 = make_float2(h2f((uint16_t)(mg >> 16)), h2f((uint16_t)(mg8 >> 16)));
+  acc = __ffma2_rn(s2, t2, __ffma2_rn(z2, make_float2(zxs, zxs), acc));
 }
 
 // v of rows (g, g+8) of one tile in stage memory; all four lanes of a quad
@@ -158,18 +171,18 @@ __device__ __forceinline__ float2 k1_tile(const uint8_t *stage, const uint8_t *x
   constexpr int PAIRS = DH / 256;  // span pairs of this half of the tile
   stage += half * PAIRS * 32 * 16;
   const uint32_t moff = half * PAIRS * 8 * 16;
-  xtab += half * PAIRS * 32 * 16;
+  xtab += half * PAIRS * 64 * 16;
   xs += half * PAIRS * 2;
   const uint4 *cw = reinterpret_cast<const uint4 *>(stage) + lane;
   const uint4 *mw = reinterpret_cast<const uint4 *>(stage + 4 * DH - half * PAIRS * 32 * 16 + moff) +
                     (lane >> 2);
-  const uint4 *xw = reinterpret_cast<const uint4 *>(xtab) + (lane < 12 ? lane : 12);
+  const uint4 *xw = reinterpret_cast<const uint4 *>(xtab) + lane;
   float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll 4
   for (int p = 0; p < PAIRS; ++p) {
     const uint4 c4 = cw[p * 32];
     const uint4 m4 = mw[p * 8];
-    const uint4 x0 = xw[p * 32], x1 = xw[p * 32 + 16];
+    const uint4 x0 = xw[p * 64], x1 = xw[p * 64 + 32];
     const float2 xsp = *reinterpret_cast<const float2 *>(xs + 2 * p);
     span_step(acc, c4.x, c4.y, x0, m4.x, m4.y, xsp.x * zx, mult);
     span_step(acc, c4.z, c4.w, x1, m4.z, m4.w, xsp.y * zx, mult);
@@ -250,7 +263,7 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 
-constexpr int kTraceSlots = 64;
+constexpr int kTraceSlots = 96;
 
 // Grid barrier on a monotonic counter; called by consumer thread 0 only,
 // between two consumer barriers.
@@ -423,6 +436,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   (void)TBp;
   const uint32_t ns = a.ns;
 
+  // Streamed weights (read once per call) go through L2 as evict-first, so the
+  // ~165 MB per layer do not evict the kernel's code, the routing partials and
+  // the published lists (cold instruction fetches from DRAM showed up as
+  // ~2.5 us stalls at phase transitions in 40% of the CTAs).
+  const uint64_t l2_stream = floe_ptx::policy_evict_first();
   auto stage = [&](uint32_t u) { return ring + (u % ns) * TILE_B; };
   auto wait_full = [&](uint32_t u) {
     floe_ptx::mbar_wait(&full[u % ns], (u / ns) & 1u, (1u << 28) | u);
@@ -433,7 +451,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   };
   auto issue = [&](uint32_t u, const void *src, uint32_t bytes) {
     floe_ptx::mbar_arrive_expect_tx(&full[u % ns], bytes);
-    floe_ptx::bulk_g2s(stage(u), src, bytes, &full[u % ns]);
+    floe_ptx::bulk_g2s_hint(stage(u), src, bytes, &full[u % ns], l2_stream);
   };
   // Phase C re-carves the ring plus the x-table area (both free once every K1
   // tile is consumed) into 4*DH-byte record stages with their own barriers:
@@ -451,10 +469,15 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
     if (k < 16) mark(a, 48 + (int)k);
     stage_scale[k % nsC] = scale;
     floe_ptx::mbar_arrive_expect_tx(&fullC[k % nsC], REC_B);
-    floe_ptx::bulk_g2s(stageC(k), src, REC_B, &fullC[k % nsC]);
+    floe_ptx::bulk_g2s_hint(stageC(k), src, REC_B, &fullC[k % nsC], l2_stream);
   };
 
   mark(a, 0);
+  if (a.phase_ns && t == 0) {  // diagnostics: which SM runs this CTA
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    a.phase_ns[blockIdx.x * kTraceSlots + 64] = smid;
+  }
   if (t == 0) {
     for (uint32_t s = 0; s < ns; ++s) {
       floe_ptx::mbar_init(&full[s], 1);
@@ -681,16 +704,22 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
       for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if (lane == 0) logits[e] = s;
     }
+    if (t == 0) mark(a, 12);  // warp 0's partial sums loaded
     cbar();
-    if (warp == 0) {
+    mark(a, 13);              // all warps' partial sums loaded
+    mark(a, 65);              // (diagnostic: back-to-back marks)
+    if (warp == 1) {  // (not warp 0: it shares SMSP 0 with the producer warp)
       // top_k (la.cpp:48-61: ties to the lower index, output ascending) as k
       // warp arg-max rounds; softmax over the selected logits (la.cpp:37-46)
+      __syncwarp();  // converged: otherwise the shuffles take the BRA.DIV slow path
       const float lg = lane < a.n_experts ? logits[lane] : -__int_as_float(0x7f800000);
       uint32_t taken = 0;
+#pragma unroll 1
       for (uint32_t r = 0; r < a.top_k; ++r) {
-        float bv = (taken >> lane) & 1u || lane >= a.n_experts ? -__int_as_float(0x7f800000) : lg;
-        uint32_t bi = lane < a.n_experts && !((taken >> lane) & 1u) ? lane : 64u;
-#pragma unroll
+        const bool cand = lane < a.n_experts && !((taken >> lane) & 1u);
+        float bv = cand ? lg : -__int_as_float(0x7f800000);
+        uint32_t bi = cand ? lane : 64u;
+#pragma unroll 1
         for (int o = 16; o >= 1; o >>= 1) {
           const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
           const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
@@ -701,32 +730,30 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
         }
         taken |= 1u << bi;
       }
-      if (lane == 0) {
-        float mx = -__int_as_float(0x7f800000), wv[floe_k::kMaxSlots];
-        uint32_t sl[floe_k::kMaxSlots], n = 0;
-        for (uint32_t m = taken; m; m &= m - 1) {
-          sl[n] = __ffs(m) - 1;
-          wv[n] = logits[sl[n]];
-          if (n == 0 || mx < wv[n]) mx = wv[n];
-          ++n;
-        }
-        float sum = 0.0f;
-        for (uint32_t i = 0; i < n; ++i) {
-          wv[i] = expf(wv[i] - mx);
-          sum += wv[i];
-        }
-        for (uint32_t i = 0; i < n; ++i) {
-          const float w = wv[i] / sum;
-          sel_s[i] = sl[i];
-          w_s[i] = w;
-          if (b == 0) {
-            if (a.sel_out) {
-              a.sel_out[i] = sl[i];
-              a.w_out[i] = w;
-            }
-            if (a.sel_trace) a.sel_trace[i] = sl[i];
-            if (a.w_trace) a.w_trace[i] = w;
+      if (lane == 0 && a.phase_ns) a.phase_ns[blockIdx.x * kTraceSlots + 14] = gtime();
+      // softmax over the selected logits in registers (no local-memory arrays:
+      // a cold stack line costs a DRAM round trip on the routing critical path).
+      // mx first, then the sum in ascending expert order, as la.cpp:37-46.
+      const bool mine = (taken >> lane) & 1u;
+      float mx = mine ? lg : -__int_as_float(0x7f800000);
+#pragma unroll 1
+      for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const float ex = mine ? expf(lg - mx) : 0.0f;
+      float sum = 0.0f;
+      for (uint32_t m = taken; m; m &= m - 1) sum += __shfl_sync(0xffffffffu, ex, __ffs(m) - 1);
+      if (mine) {
+        const uint32_t i = __popc(taken & ((1u << lane) - 1));  // rank = ascending position
+        const float w = ex / sum;
+        sel_s[i] = lane;
+        w_s[i] = w;
+        if (i == 0) mark(a, 15);
+        if (b == 0) {
+          if (a.sel_out) {
+            a.sel_out[i] = lane;
+            a.w_out[i] = w;
           }
+          if (a.sel_trace) a.sel_trace[i] = lane;
+          if (a.w_trace) a.w_trace[i] = w;
         }
       }
     }
@@ -792,7 +819,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
     const float S = scaled ? __int_as_float((127 + 22 - ex) << 23) : 1.0f;
     const float invS = scaled ? __int_as_float((127 - 22 + ex) << 23) : 1.0f;
     const uint32_t mytig = lane & 3;
-    mult = mytig == 0 ? invS : (mytig == 1 ? 65536.0f * invS : 0.0f);
+    // column pair of this lane (see span_step): (c1L0,c1L1) (c4L0,c4L1) (c1L2,-) (c4L2,-)
+    mult = mytig == 0 ? invS : (mytig == 1 ? 0.25f * invS : (mytig == 2 ? 65536.0f * invS : 16384.0f * invS));
     zx = mytig == 0 ? 1.0f : 0.0f;
     if (act) {
       if (all_finite) {
@@ -800,29 +828,37 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) X[i] = __float2int_rn(xv[i] * S);
         const uint32_t p = span >> 1, sodd = span & 1;
-        uint4 *xt = reinterpret_cast<uint4 *>(xtab) + (p * 2 + sodd) * 16;
+        uint4 *xt = reinterpret_cast<uint4 *>(xtab) + (p * 2 + sodd) * 32;
+        // limb bytes of the 16 elements: lb[l][i] for element i
+        uint32_t lw[3][4][2];  // [limb][m][j]: element 4b + 2m + j, byte b
 #pragma unroll
-        for (int n = 0; n < 3; ++n) {
-          uint32_t wd[4];  // (m, j) = (0,0), (0,1), (1,0), (1,1)
+        for (int l = 0; l < 3; ++l)
 #pragma unroll
-          for (int mj = 0; mj < 4; ++mj) {
-            const int m = mj >> 1, j = mj & 1;
-            uint32_t w = 0;
+          for (int m = 0; m < 2; ++m)
 #pragma unroll
-            for (int bb = 0; bb < 4; ++bb) {
-              const int v = X[4 * bb + 2 * m + j];
-              const int l0 = ((v + 128) & 255) - 128;
-              const int r1 = (v - l0) >> 8;
-              const int l1 = ((r1 + 128) & 255) - 128;
-              const int l2 = (r1 - l1) >> 8;
-              const int l = n == 0 ? l0 : (n == 1 ? l1 : l2);
-              w |= (uint32_t)(l & 255) << (8 * bb);
-            }
-            wd[mj] = w;
-          }
-          xt[4 * n + tig] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+            for (int j = 0; j < 2; ++j) lw[l][m][j] = 0;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int v = X[i];
+          const int l0 = ((v + 128) & 255) - 128;
+          const int r1 = (v - l0) >> 8;
+          const int l1 = ((r1 + 128) & 255) - 128;
+          const int l2 = (r1 - l1) >> 8;
+          const int bb = i >> 2, m = (i >> 1) & 1, j = i & 1;
+          lw[0][m][j] |= (uint32_t)(l0 & 255) << (8 * bb);
+          lw[1][m][j] |= (uint32_t)(l1 & 255) << (8 * bb);
+          lw[2][m][j] |= (uint32_t)(l2 & 255) << (8 * bb);
         }
-        xt[12 + tig] = make_uint4(0, 0, 0, 0);  // columns 3..7 (lanes >= 12) read zeros
+        // column n -> (class, limb): 0 (x1,L0) 1 (x1,L1) 2 (x4,L0) 3 (x4,L1)
+        // 4 (x1,L2) 6 (x4,L2); 5, 7 zero.  Class x1 rides in b0 (j = 0, the
+        // even elements), class x4 in b1 (j = 1, the odd elements).
+#pragma unroll
+        for (int n = 0; n < 8; ++n) {
+          const int lim = n == 0 || n == 2 ? 0 : (n == 1 || n == 3 ? 1 : 2);
+          const bool c1 = n == 0 || n == 1 || n == 4, c4 = n == 2 || n == 3 || n == 6;
+          xt[4 * n + tig] = make_uint4(c1 ? lw[lim][0][0] : 0u, c4 ? lw[lim][0][1] : 0u,
+                                       c1 ? lw[lim][1][0] : 0u, c4 ? lw[lim][1][1] : 0u);
+        }
       } else {
         float *xf = hs + 64 * span + 16 * tig;
 #pragma unroll

@@ -36,7 +36,9 @@ def summarize(tag, traces, marks):
         print(f"   {name:24s} mean {d.mean():7.2f}  min {d.min():7.2f}  max {d.max():7.2f} us")
     end = (T[:, :, 5].max(1) - t0) / 1e3
     print(f"   first start -> last phase-C end: {end.mean():7.2f} us")
-    names = {0: "start", 1: "A done", 6: "barrier1 out", 2: "routed", 7: "1st tile", 3: "K1 done",
+    names = {0: "start", 1: "A done", 6: "barrier1 out", 12: "partials (w0)", 13: "partials (all)",
+             14: "top-k done", 15: "softmax done",
+             2: "routed", 7: "1st tile", 3: "K1 done",
              8: "published", 18: "P: all published", 5: "C done"}
     for m, nm in names.items():
         v = T[:, :, m]
@@ -79,6 +81,18 @@ def main():
                 w.read_phase_trace()
         summarize(name, traces, marks)
         T = np.stack(traces).astype(np.int64)
+        if name == "layer":
+            d0 = (T[:, :, 65] - T[:, :, 13]) / 1e3
+            print("   back-to-back marks histogram (us):", np.histogram(d0, bins=[0, 0.5, 1, 1.5, 2, 3, 4, 6, 10])[0].tolist())
+            d = (T[:, :, 14] - T[:, :, 65]) / 1e3
+            print("   top-k interval histogram (us):", np.histogram(d, bins=[0, 0.5, 1, 1.5, 2, 3, 4, 6, 10])[0].tolist())
+            smid = T[-1, :, 64]
+            slow = d[-1] > 1.5
+            print("   slow CTAs' SMs (last step):", sorted(smid[slow].tolist()))
+            print("   fast CTAs' SMs (last step):", sorted(smid[~slow].tolist())[:60])
+            for st in range(T.shape[0]):
+                print("   step", st, "slow count", int((d[st] > 1.5).sum()), "slow SMs even/odd:",
+                      int((smid[d[st] > 1.5] % 2 == 0).sum()), int((smid[d[st] > 1.5] % 2 == 1).sum()))
         for cta in (0, 37, 100):
             tr = T[-1, cta]
             base = tr[48]
@@ -93,3 +107,9 @@ def main():
 if __name__ == "__main__":
     main()
 
+
+
+def slow_ctas(T, a, b, thr_us=1.5):
+    """CTAs whose interval a->b exceeds thr_us in the last trace, with %smid."""
+    d = (T[-1, :, b] - T[-1, :, a]) / 1e3
+    return [(int(i), round(float(d[i]), 2)) for i in np.nonzero(d > thr_us)[0]]
