@@ -96,6 +96,9 @@ typedef struct floe_expert_host_view {
 } floe_expert_host_view;
 
 #define FLOE_VIEW_DEVICE 1u
+/* keep the gate|down records host-resident (pinned, mapped): the kernels
+ * read the kept channels' records directly over PCIe (SURVEY config 3) */
+#define FLOE_VIEW_HOST_RECORDS 2u
 
 typedef struct floe_expert_info {
   uint32_t d_hidden, d_intermediate, bits, group_size;
@@ -127,6 +130,15 @@ int floe_gpu_expert_destroy(floe_gpu_expert *e);
 int floe_gpu_expert_info(const floe_gpu_expert *e, floe_expert_info *info);
 /* Thresholds are per expert (ThresholdTable, core/src/model.cpp:237). */
 int floe_gpu_expert_set_threshold(floe_gpu_expert *e, float threshold);
+
+/* Placement of an expert's gate|down records: resident = 1 -> HBM,
+ * 0 -> pinned host memory read in place over PCIe by the kernels.  Stream
+ * ordered on `stream` (copy, descriptor switch in the expert and in every
+ * layer holding it, release of the old copy).  The host copy, once made, is
+ * kept for later promotions.  Mirrors ExpertCache residency
+ * (core/src/offload.cpp:89-159) at expert granularity. */
+int floe_gpu_expert_set_resident(floe_gpu_expert *e, int resident, floe_stream_t stream);
+int floe_gpu_expert_residency(const floe_gpu_expert *e, int *resident, uint64_t *device_bytes);
 
 /* -------------------------------------------------------------- workspace */
 /* Scratch for calls on experts of at most d_intermediate channels and

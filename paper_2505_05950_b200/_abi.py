@@ -40,6 +40,7 @@ class ExpertHostView(ct.Structure):
 
 
 FLOE_VIEW_DEVICE = 1
+FLOE_VIEW_HOST_RECORDS = 2
 
 
 class ExpertInfo(ct.Structure):
@@ -68,6 +69,8 @@ _SIGS = {
     "floe_gpu_last_error": (ct.c_char_p, []),
     "floe_gpu_abi_version": (ct.c_int, []),
     "floe_gpu_device_malloc": (ct.c_int, [_P, ct.c_size_t]),
+    "floe_gpu_expert_set_resident": (ct.c_int, [_P, ct.c_int, _P]),
+    "floe_gpu_expert_residency": (ct.c_int, [_P, _P, _P]),
     "floe_gpu_device_free": (ct.c_int, [_P]),
     "floe_gpu_copy": (ct.c_int, [_P, _P, ct.c_size_t, _P]),
     "floe_gpu_device_info": (ct.c_int, [_P, _P, _P, _P]),
@@ -235,7 +238,7 @@ class GpuExpert:
     """
 
     def __init__(self, d_hidden, d_intermediate, bits, group_size, codes, scales, zeros,
-                 gate=None, down=None, records=None, threshold=0.0):
+                 gate=None, down=None, records=None, threshold=0.0, host_records=False):
         keep = []
         on_device = not isinstance(codes, np.ndarray)  # torch CUDA tensors
 
@@ -254,7 +257,8 @@ class GpuExpert:
                            host(codes, np.uint8), host(scales, np.uint16), host(zeros, np.uint16),
                            host(gate, np.float32), host(down, np.float32),
                            host(records, np.uint16), float(threshold),
-                           FLOE_VIEW_DEVICE if on_device else 0)
+                           (FLOE_VIEW_DEVICE if on_device else 0)
+                           | (FLOE_VIEW_HOST_RECORDS if host_records else 0))
         h = ct.c_void_p()
         _check(lib().floe_gpu_expert_create(ct.byref(v), ct.byref(h)))
         self.handle = h.value
@@ -276,6 +280,17 @@ class GpuExpert:
     @property
     def threshold(self) -> float:
         return self.info()["threshold"]
+
+    def set_resident(self, resident: bool, stream=None):
+        """Move the gate|down records to HBM (True) or keep them host-resident
+        (False; the kernels read them over PCIe).  Stream-ordered."""
+        _check(lib().floe_gpu_expert_set_resident(self.handle, 1 if resident else 0,
+                                                  _stream(stream)))
+
+    def residency(self) -> dict:
+        r, nb = ct.c_int(), ct.c_uint64()
+        _check(lib().floe_gpu_expert_residency(self.handle, ct.byref(r), ct.byref(nb)))
+        return dict(resident=bool(r.value), device_bytes=nb.value)
 
     def set_threshold(self, t: float):
         _check(lib().floe_gpu_expert_set_threshold(self.handle, float(t)))

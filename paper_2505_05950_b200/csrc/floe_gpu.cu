@@ -120,6 +120,12 @@ struct floe_gpu_expert {
   ExpertDesc *dev_desc = nullptr;
   bool fast = false;  // tile-fragment layout + fused kernel
   bool up_only = false;  // no gate/down records (qgemv_channels / predict_mask only)
+  // gate|down records: in HBM (rec_dev) or host-resident in pinned, mapped
+  // memory (rec_host) that the kernels read directly over PCIe
+  __half *rec_dev = nullptr;
+  __half *rec_host = nullptr;
+  bool resident = true;
+  std::vector<ExpertDesc *> tables;  // device layer-table entries copying host_desc
 };
 
 enum { kStageMixing = 0, kStageRoute = 1, kStageK1 = 2, kStageK2 = 3, kStageFused = 4, kStages = 5 };
@@ -510,7 +516,7 @@ int floe_gpu_expert_create(const floe_expert_host_view *v, floe_gpu_expert **out
   const uint64_t o_zeros = up256(o_scales + 2 * e->n_groups);
   const uint64_t o_rec = e->fast ? up256(o_codes + tile_total) : up256(o_zeros + 2 * e->n_groups);
   e->up_only = up_only;
-  const uint64_t total = o_rec + (up_only ? 0 : 4 * n);
+  const uint64_t total = o_rec;  // records live in their own allocation (residency)
   cudaError_t ce = cudaMalloc(&e->block, total);
   if (ce != cudaSuccess) {
     delete e;
@@ -526,11 +532,21 @@ int floe_gpu_expert_create(const floe_expert_host_view *v, floe_gpu_expert **out
     e->host_desc.scales = reinterpret_cast<const uint16_t *>(base + o_scales);
     e->host_desc.zeros = reinterpret_cast<const uint16_t *>(base + o_zeros);
   }
-  e->host_desc.records = up_only ? nullptr : reinterpret_cast<const __half *>(base + o_rec);
+  if (!up_only) {
+    ce = cudaMalloc(reinterpret_cast<void **>(&e->rec_dev), 4 * n);
+    if (ce != cudaSuccess) {
+      cudaFree(e->block);
+      delete e;
+      return fail(FLOE_ERR_OOM, "expert_create: cudaMalloc(records, %llu) failed: %s",
+                  (unsigned long long)(4 * n), cudaGetErrorString(ce));
+    }
+  }
+  e->host_desc.records = e->rec_dev;
   e->host_desc.threshold = v->threshold;
 
   auto cleanup = [&](int rc) {
     cudaFree(e->block);
+    if (e->rec_dev) cudaFree(e->rec_dev);
     delete e;
     return rc;
   };
@@ -575,7 +591,7 @@ int floe_gpu_expert_create(const floe_expert_host_view *v, floe_gpu_expert **out
     cp(base + o_scales, v->scales, 2 * e->n_groups);
     cp(base + o_zeros, v->zeros, 2 * e->n_groups);
   }
-  __half *rec = reinterpret_cast<__half *>(base + o_rec);
+  __half *rec = e->rec_dev;
   if (up_only) {
     // nothing to upload
   } else if (v->records_f16) {
@@ -610,12 +626,69 @@ int floe_gpu_expert_create(const floe_expert_host_view *v, floe_gpu_expert **out
     return cleanup(fail(FLOE_ERR_CUDA, "expert_create: upload failed: %s",
                         cudaGetErrorString(err)));
   *out = e;
+  if ((v->flags & FLOE_VIEW_HOST_RECORDS) && !up_only) {
+    if (int rc = floe_gpu_expert_set_resident(e, 0, nullptr)) {
+      *out = nullptr;
+      floe_gpu_expert_destroy(e);
+      return rc;
+    }
+    if (cudaDeviceSynchronize() != cudaSuccess)
+      return fail(FLOE_ERR_CUDA, "expert_create: host-resident demotion failed");
+  }
+  return FLOE_OK;
+}
+
+// Residency of the gate|down records (the host-resident decode of SURVEY
+// config 3; ExpertCache entries of core/src/offload.cpp:89-159 at expert
+// granularity).  Stream-ordered: the copy, the descriptor switch (expert and
+// every layer table holding it) and the release of the old copy all run on
+// `stream`, so kernels on `stream` see either placement consistently.
+int floe_gpu_expert_set_resident(floe_gpu_expert *e, int resident, floe_stream_t stream) {
+  if (!e) return fail(FLOE_ERR_INVALID, "expert_set_resident: null expert");
+  if (e->up_only) return fail(FLOE_ERR_INVALID, "expert_set_resident: expert has no gate/down");
+  const bool want = resident != 0;
+  if (want == e->resident) return FLOE_OK;
+  cudaStream_t st = S(stream);
+  const uint64_t bytes = 4ull * e->dh * e->di;
+  if (!want) {
+    if (!e->rec_host) {
+      CK(cudaHostAlloc(reinterpret_cast<void **>(&e->rec_host), bytes,
+                       cudaHostAllocMapped | cudaHostAllocPortable));
+      CK(cudaMemcpyAsync(e->rec_host, e->rec_dev, bytes, cudaMemcpyDeviceToHost, st));
+    }
+    void *dptr = nullptr;
+    CK(cudaHostGetDevicePointer(&dptr, e->rec_host, 0));
+    e->host_desc.records = static_cast<const __half *>(dptr);
+  } else {
+    CK(cudaMallocAsync(reinterpret_cast<void **>(&e->rec_dev), bytes, st));
+    CK(cudaMemcpyAsync(e->rec_dev, e->rec_host, bytes, cudaMemcpyHostToDevice, st));
+    e->host_desc.records = e->rec_dev;
+  }
+  CK(cudaMemcpyAsync(e->dev_desc, &e->host_desc, sizeof(ExpertDesc), cudaMemcpyHostToDevice, st));
+  for (ExpertDesc *t : e->tables)
+    CK(cudaMemcpyAsync(t, &e->host_desc, sizeof(ExpertDesc), cudaMemcpyHostToDevice, st));
+  if (!want) {
+    CK(cudaFreeAsync(e->rec_dev, st));
+    e->rec_dev = nullptr;
+  }
+  e->resident = want;
+  return FLOE_OK;
+}
+
+int floe_gpu_expert_residency(const floe_gpu_expert *e, int *resident, uint64_t *device_bytes) {
+  if (!e) return fail(FLOE_ERR_INVALID, "expert_residency: null expert");
+  if (resident) *resident = e->resident ? 1 : 0;
+  if (device_bytes)
+    *device_bytes = (e->resident && !e->up_only) ? 4ull * e->dh * e->di : 0ull;
   return FLOE_OK;
 }
 
 int floe_gpu_expert_destroy(floe_gpu_expert *e) {
   if (!e) return FLOE_OK;
+  cudaDeviceSynchronize();  // stream-ordered residency changes may be in flight
   cudaFree(e->block);
+  if (e->rec_dev) cudaFree(e->rec_dev);
+  if (e->rec_host) cudaFreeHost(e->rec_host);
   delete e;
   return FLOE_OK;
 }
@@ -954,6 +1027,8 @@ int floe_gpu_layer_create(const floe_layer_host_view *v, floe_gpu_layer **out) {
     ce = cudaMemcpy(l->router, v->router, 4ull * l->E * dh, cudaMemcpyDefault);
   if (ce == cudaSuccess)
     ce = cudaMemcpy(l->table, table.data(), sizeof(ExpertDesc) * l->E, cudaMemcpyHostToDevice);
+  if (ce == cudaSuccess)
+    for (uint32_t i = 0; i < l->E; ++i) v->experts[i]->tables.push_back(l->table + i);
   if (ce == cudaSuccess) {
     if (!l->mix_f16) {
       ce = cudaMemcpy(l->mixing, v->mixing, 4ull * dh * dh, cudaMemcpyDefault);

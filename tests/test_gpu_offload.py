@@ -1,0 +1,74 @@
+"""Host-resident gate|down records (SURVEY config 3, ExpertCache residency of
+core/src/offload.cpp:89-159 at expert granularity): the kernels read the kept
+channels' records in place from pinned host memory over PCIe; promotion to
+HBM and demotion are stream-ordered and switch every layer table holding the
+expert.  Outputs must not depend on where the records live."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    assert torch.cuda.is_available()
+    return torch
+
+
+@pytest.fixture(scope="module")
+def fb(torch):
+    import paper_2505_05950_b200 as fb
+    return fb
+
+
+@pytest.mark.parametrize("dh,di,bits,g", [(4096, 2048, 2, 64), (2048, 512, 2, 64), (64, 256, 8, 64)])
+def test_expert_forward_independent_of_residency(fb, torch, dh, di, bits, g):
+    gate, up, down = O.seeded_expert(dh, di, 5)
+    x = O.seeded_input(dh, 6)
+    q = O.quantize(up, bits, g)
+    t = O.calibrate_threshold(np.abs(O.qgemv_channels(q, dh, x)), 0.8)
+    dev = fb.GpuExpert(dh, di, bits, g, q.codes, q.scales, q.zeros, gate=gate, down=down,
+                       threshold=t)
+    host = fb.GpuExpert(dh, di, bits, g, q.codes, q.scales, q.zeros, gate=gate, down=down,
+                        threshold=t, host_records=True)
+    assert host.residency() == dict(resident=False, device_bytes=0)
+    ws = fb.Workspace(dh, di)
+    xd = torch.from_numpy(x).cuda()
+    y_dev = fb.expert_forward_sparse(dev, xd, ws).cpu().numpy()
+    y_host = fb.expert_forward_sparse(host, xd, ws).cpu().numpy()
+    assert O.rel_l2(y_host, y_dev) <= 1e-6
+    # promote, demote, promote: same result each time
+    for r in (True, False, True):
+        host.set_resident(r)
+        assert host.residency()["resident"] == r
+        y = fb.expert_forward_sparse(host, xd, ws).cpu().numpy()
+        assert O.rel_l2(y, y_dev) <= 1e-6
+
+
+def test_layer_tables_follow_residency(fb, torch):
+    dh, di, E, K = 2048, 512, 4, 2
+    rng = np.random.default_rng(3)
+    experts, hosted = [], []
+    for e in range(E):
+        gate, up, down = O.seeded_expert(dh, di, 40 + e)
+        q = O.quantize(up, 2, 64)
+        experts.append(fb.GpuExpert(dh, di, 2, 64, q.codes, q.scales, q.zeros, gate=gate,
+                                    down=down, threshold=1.0))
+        hosted.append(fb.GpuExpert(dh, di, 2, 64, q.codes, q.scales, q.zeros, gate=gate,
+                                   down=down, threshold=1.0, host_records=True))
+    router = (rng.standard_normal((E, dh)) / 45).astype(np.float32)
+    mixing = (rng.standard_normal((dh, dh)) / 45).astype(np.float32)
+    la = fb.GpuLayer(router, mixing, experts, K)
+    lb = fb.GpuLayer(router, mixing, hosted, K)
+    ws = fb.Workspace(dh, di, K)
+    for t in range(3):
+        h = torch.from_numpy(O.token_input(1, t, dh)).cuda()
+        ya = fb.layer_forward(la, h, ws).cpu().numpy()
+        yb = fb.layer_forward(lb, h, ws).cpu().numpy()
+        assert O.rel_l2(yb, ya) <= 1e-6
+        hosted[t % E].set_resident(True)  # the layer table switches with the expert
+        yc = fb.layer_forward(lb, h, ws).cpu().numpy()
+        assert O.rel_l2(yc, ya) <= 1e-6

@@ -86,6 +86,12 @@ def main():
             print("   back-to-back marks histogram (us):", np.histogram(d0, bins=[0, 0.5, 1, 1.5, 2, 3, 4, 6, 10])[0].tolist())
             d = (T[:, :, 14] - T[:, :, 65]) / 1e3
             print("   top-k interval histogram (us):", np.histogram(d, bins=[0, 0.5, 1, 1.5, 2, 3, 4, 6, 10])[0].tolist())
+            cdone = (T[-1, :, 5] - T[-1, :, 0].min()) / 1e3
+            order = np.argsort(cdone)[::-1][:8]
+            print("   slowest phase-C CTAs (cta, C done us, own, deficit, P, plan->done us):",
+                  [(int(c), round(float(cdone[c]), 1), int(T[-1, c, 66]), int(T[-1, c, 67]),
+                    int(T[-1, c, 68]), round(float((T[-1, c, 5] - T[-1, c, 9]) / 1e3), 1)) for c in order])
+            print("   own+deficit spread:", int((T[-1, :, 66] + T[-1, :, 67]).min()), int((T[-1, :, 66] + T[-1, :, 67]).max()))
             smid = T[-1, :, 64]
             slow = d[-1] > 1.5
             print("   slow CTAs' SMs (last step):", sorted(smid[slow].tolist()))
