@@ -226,6 +226,31 @@ int floe_gpu_layer_forward_host(const floe_gpu_layer *l, floe_gpu_workspace *ws,
                                 const float *h_host, float *y_host,
                                 floe_stream_t stream);
 
+/* ------------------------------------------------ host-resident decode */
+/* Config 3 of SURVEY.md: a stack of layers whose experts' gate|down records
+ * stay in pinned host memory (the kernels read kept channels of non-resident
+ * experts over PCIe), with an LRU of whole experts in HBM under
+ * `vram_budget` bytes, promoted from the routing of earlier tokens by copies
+ * on a side stream (the reference's simulate_decode / ExpertCache,
+ * core/src/offload.cpp:89-159,299-464, as a real engine).  decode runs one
+ * token through every layer (h_dev -> y_dev) on `stream`. */
+typedef struct floe_gpu_offload floe_gpu_offload;
+typedef struct floe_offload_stats {
+  uint64_t tokens;
+  uint64_t records_from_hbm;     /* kept channel records served from resident experts */
+  uint64_t records_over_pcie;    /* ... read in place from pinned host memory        */
+  uint64_t record_bytes;         /* bytes per record (4 * d_hidden)                   */
+  uint64_t up_bytes_per_expert;  /* codes + f16 meta, always resident in HBM          */
+  uint64_t promotions, evictions, bytes_promoted;
+  uint64_t device_record_bytes;  /* records resident in HBM now                       */
+} floe_offload_stats;
+int floe_gpu_offload_create(floe_gpu_layer *const *layers, uint32_t n_layers,
+                            uint64_t vram_budget, floe_gpu_offload **out);
+int floe_gpu_offload_destroy(floe_gpu_offload *o);
+int floe_gpu_offload_decode(floe_gpu_offload *o, floe_gpu_workspace *ws, const float *h_dev,
+                            float *y_dev, floe_stream_t stream);
+int floe_gpu_offload_stats(floe_gpu_offload *o, floe_offload_stats *out, floe_stream_t stream);
+
 /* ----------------------------------------------------- counters / profile */
 /* Device-side running totals kept by a workspace: calls (K1 launches) and
  * kept channels summed over all slots -- the byte-accounting identity

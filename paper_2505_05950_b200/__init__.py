@@ -16,6 +16,7 @@ from ._abi import (  # noqa: F401
     GpuExpert,
     GpuLayer,
     GpuPredictor,
+    Offload,
     Workspace,
     abi_version,
     dequantize,
@@ -33,7 +34,7 @@ from ._abi import (  # noqa: F401
     quantize,
 )
 
-__all__ = ["FloeError", "GpuExpert", "GpuLayer", "GpuPredictor", "Workspace",
+__all__ = ["FloeError", "GpuExpert", "GpuLayer", "GpuPredictor", "Offload", "Workspace",
            "abi_version", "dequantize", "device_info", "expert_forward_sparse",
            "exported_symbols", "layer_forward", "lib", "library_path", "predict_experts",
            "predict_mask", "qgemv_channels", "gen_normals", "layer_forward_host",

@@ -69,6 +69,10 @@ _SIGS = {
     "floe_gpu_last_error": (ct.c_char_p, []),
     "floe_gpu_abi_version": (ct.c_int, []),
     "floe_gpu_device_malloc": (ct.c_int, [_P, ct.c_size_t]),
+    "floe_gpu_offload_create": (ct.c_int, [_P, _U32, ct.c_uint64, _P]),
+    "floe_gpu_offload_destroy": (ct.c_int, [_P]),
+    "floe_gpu_offload_decode": (ct.c_int, [_P, _P, _P, _P, _P]),
+    "floe_gpu_offload_stats": (ct.c_int, [_P, _P, _P]),
     "floe_gpu_expert_set_resident": (ct.c_int, [_P, ct.c_int, _P]),
     "floe_gpu_expert_residency": (ct.c_int, [_P, _P, _P]),
     "floe_gpu_device_free": (ct.c_int, [_P]),
@@ -479,3 +483,46 @@ def quantize(x, bits: int, group_size: int, stream=None):
     _check(lib().floe_gpu_quantize(x.data_ptr(), n, bits, group_size, codes.data_ptr(),
                                    scales.data_ptr(), zeros.data_ptr(), _stream(stream)))
     return codes, scales, zeros
+
+
+class OffloadStats(ct.Structure):
+    _fields_ = [("tokens", ct.c_uint64), ("records_from_hbm", ct.c_uint64),
+                ("records_over_pcie", ct.c_uint64), ("record_bytes", ct.c_uint64),
+                ("up_bytes_per_expert", ct.c_uint64), ("promotions", ct.c_uint64),
+                ("evictions", ct.c_uint64), ("bytes_promoted", ct.c_uint64),
+                ("device_record_bytes", ct.c_uint64)]
+
+
+class Offload:
+    """Host-resident decode engine (floe_gpu_offload; SURVEY config 3): the
+    layers' experts keep their gate|down records in pinned host memory, an LRU
+    of whole experts lives in HBM under `vram_budget` bytes."""
+
+    def __init__(self, layers, vram_budget: int):
+        arr = (ct.c_void_p * len(layers))(*[l.handle for l in layers])
+        h = ct.c_void_p()
+        _check(lib().floe_gpu_offload_create(arr, len(layers), int(vram_budget), ct.byref(h)))
+        self.handle = h.value
+        self.layers = layers
+        self.d_hidden = layers[0].d_hidden
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().floe_gpu_offload_destroy(self.handle)
+            self.handle = None
+
+    __del__ = close
+
+    def decode(self, h, ws: Workspace, out=None, stream=None):
+        """One token through every layer (h -> y), stream-ordered."""
+        torch = _torch()
+        h = _dev_f32(h, self.d_hidden, "offload_decode")
+        y = torch.empty(self.d_hidden, dtype=torch.float32, device=h.device) if out is None else out
+        _check(lib().floe_gpu_offload_decode(self.handle, ws.handle, h.data_ptr(), y.data_ptr(),
+                                             _stream(stream)))
+        return y
+
+    def stats(self, stream=None) -> dict:
+        st = OffloadStats()
+        _check(lib().floe_gpu_offload_stats(self.handle, ct.byref(st), _stream(stream)))
+        return {f: getattr(st, f) for f, _ in OffloadStats._fields_}

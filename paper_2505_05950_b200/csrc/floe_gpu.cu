@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <new>
 #include <string>
@@ -167,6 +168,7 @@ struct floe_gpu_layer {
   float *router = nullptr;
   void *mixing = nullptr;
   ExpertDesc *table = nullptr;
+  std::vector<floe_gpu_expert *> experts;  // borrowed (offload engine)
 };
 
 struct floe_gpu_predictor {
@@ -1028,7 +1030,10 @@ int floe_gpu_layer_create(const floe_layer_host_view *v, floe_gpu_layer **out) {
   if (ce == cudaSuccess)
     ce = cudaMemcpy(l->table, table.data(), sizeof(ExpertDesc) * l->E, cudaMemcpyHostToDevice);
   if (ce == cudaSuccess)
-    for (uint32_t i = 0; i < l->E; ++i) v->experts[i]->tables.push_back(l->table + i);
+    for (uint32_t i = 0; i < l->E; ++i) {
+      v->experts[i]->tables.push_back(l->table + i);
+      l->experts.push_back(v->experts[i]);
+    }
   if (ce == cudaSuccess) {
     if (!l->mix_f16) {
       ce = cudaMemcpy(l->mixing, v->mixing, 4ull * dh * dh, cudaMemcpyDefault);
@@ -1137,6 +1142,241 @@ int floe_gpu_layer_forward_host(const floe_gpu_layer *l, floe_gpu_workspace *ws,
   std::memcpy(y_host, ws->hy, 4ull * l->dh);
   return FLOE_OK;
 }
+
+// ----------------------------------------------------------- offload engine --
+// Host-resident decode (SURVEY config 3; the reference's simulate_decode /
+// ExpertCache, core/src/offload.cpp:89-159,299-464, made real).  Every
+// expert's gate|down records live in pinned host memory; the fused kernel
+// reads the kept channels of non-resident experts in place over PCIe (the
+// simulator's "sync" bytes, fetched on demand at exactly channel
+// granularity, no host round trip).  An LRU of whole experts under a VRAM
+// budget holds recently routed experts in HBM: the routing of token t
+// (read back asynchronously) promotes missing experts with copies on a side
+// stream; a promoted copy is switched in, and an evicted one switched out and
+// freed, on the decode stream between tokens, so every kernel sees one
+// consistent placement and the byte accounting is exact.
+namespace {
+__global__ void offload_account(const uint32_t *seg_count, uint32_t G, uint32_t slots,
+                                const uint32_t *sel, const uint8_t *resident,
+                                unsigned long long *acc /* [2]: from HBM, over PCIe */) {
+  const uint32_t lane = threadIdx.x;
+  for (uint32_t s = 0; s < slots; ++s) {
+    uint32_t n = 0;
+    for (uint32_t b = lane; b < G; b += 32) n += seg_count[s * G + b];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+    if (lane == 0) atomicAdd(&acc[resident[sel[s]] ? 0 : 1], (unsigned long long)n);
+  }
+}
+}  // namespace
+
+struct floe_gpu_offload {
+  std::vector<floe_gpu_layer *> layers;
+  uint32_t L = 0, E = 0, K = 0, dh = 0;
+  uint64_t budget = 0, rec_bytes = 0, committed = 0;  // bytes of HBM copies (ready + in flight)
+  enum State : uint8_t { kHost = 0, kCopying = 1, kResident = 2 };
+  std::vector<uint8_t> state;                 // [L*E]
+  std::vector<__half *> pending;              // [L*E] device copy in flight
+  std::vector<cudaEvent_t> copy_done;         // [L*E]
+  std::vector<uint64_t> last_use;             // [L*E] token of last routing
+  uint8_t *resident_dev = nullptr;            // [L*E] for the byte accounting
+  std::vector<uint8_t> resident_host;
+  uint32_t *sel_dev = nullptr;                // [L][K] routing of the last token
+  uint32_t *sel_host = nullptr;               // pinned
+  float *buf = nullptr;                       // 2 x dh ping-pong
+  unsigned long long *acc = nullptr;          // [2] kept records from HBM / over PCIe
+  cudaEvent_t sel_ready = nullptr;
+  bool sel_pending = false;
+  cudaStream_t side = nullptr;
+  uint64_t tokens = 0, promotions = 0, evictions = 0, bytes_promoted = 0;
+  uint64_t up_bytes = 0;
+};
+
+namespace {
+int offload_switch(floe_gpu_offload *o, uint32_t i, bool to_hbm, cudaStream_t st) {
+  floe_gpu_expert *e = o->layers[i / o->E]->experts[i % o->E];
+  if (to_hbm) {
+    e->rec_dev = o->pending[i];
+    o->pending[i] = nullptr;
+    e->host_desc.records = e->rec_dev;
+  } else {
+    void *dptr = nullptr;
+    CK(cudaHostGetDevicePointer(&dptr, e->rec_host, 0));
+    e->host_desc.records = static_cast<const __half *>(dptr);
+  }
+  CK(cudaMemcpyAsync(e->dev_desc, &e->host_desc, sizeof(ExpertDesc), cudaMemcpyHostToDevice, st));
+  for (ExpertDesc *t : e->tables)
+    CK(cudaMemcpyAsync(t, &e->host_desc, sizeof(ExpertDesc), cudaMemcpyHostToDevice, st));
+  if (!to_hbm) {  // kernels already enqueued on st may still read the old copy: free after them
+    CK(cudaFreeAsync(e->rec_dev, st));
+    e->rec_dev = nullptr;
+  }
+  e->resident = to_hbm;
+  o->resident_host[i] = to_hbm ? 1 : 0;
+  CK(cudaMemcpyAsync(o->resident_dev + i, &o->resident_host[i], 1, cudaMemcpyHostToDevice, st));
+  return FLOE_OK;
+}
+
+// Between tokens: switch in finished copies; read the previous token's routing
+// (if it is done) and promote its missing experts, evicting least recently
+// used ones to stay under the budget.
+int offload_policy(floe_gpu_offload *o, cudaStream_t st) {
+  const uint32_t N = o->L * o->E;
+  for (uint32_t i = 0; i < N; ++i)
+    if (o->state[i] == floe_gpu_offload::kCopying && cudaEventQuery(o->copy_done[i]) == cudaSuccess) {
+      if (int rc = offload_switch(o, i, true, st)) return rc;
+      o->state[i] = floe_gpu_offload::kResident;
+    }
+  if (!o->sel_pending || cudaEventQuery(o->sel_ready) != cudaSuccess) return FLOE_OK;
+  o->sel_pending = false;
+  std::vector<uint32_t> want;
+  for (uint32_t l = 0; l < o->L; ++l)
+    for (uint32_t k = 0; k < o->K; ++k) {
+      const uint32_t i = l * o->E + o->sel_host[l * o->K + k];
+      o->last_use[i] = o->tokens;
+      if (o->state[i] == floe_gpu_offload::kHost) want.push_back(i);
+    }
+  for (uint32_t i : want) {
+    while (o->committed + o->rec_bytes > o->budget) {  // evict the LRU resident expert
+      int64_t victim = -1;
+      for (uint32_t j = 0; j < N; ++j)
+        if (o->state[j] == floe_gpu_offload::kResident &&
+            (victim < 0 || o->last_use[j] < o->last_use[victim]))
+          victim = j;
+      if (victim < 0 || o->last_use[victim] >= o->tokens) break;  // nothing evictable
+      if (int rc = offload_switch(o, (uint32_t)victim, false, st)) return rc;
+      o->state[victim] = floe_gpu_offload::kHost;
+      o->committed -= o->rec_bytes;
+      ++o->evictions;
+    }
+    if (o->committed + o->rec_bytes > o->budget) break;
+    floe_gpu_expert *e = o->layers[i / o->E]->experts[i % o->E];
+    CK(cudaMallocAsync(reinterpret_cast<void **>(&o->pending[i]), o->rec_bytes, o->side));
+    CK(cudaMemcpyAsync(o->pending[i], e->rec_host, o->rec_bytes, cudaMemcpyHostToDevice, o->side));
+    CK(cudaEventRecord(o->copy_done[i], o->side));
+    o->state[i] = floe_gpu_offload::kCopying;
+    o->committed += o->rec_bytes;
+    o->bytes_promoted += o->rec_bytes;
+    ++o->promotions;
+  }
+  return FLOE_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int floe_gpu_offload_create(floe_gpu_layer *const *layers, uint32_t n_layers,
+                            uint64_t vram_budget, floe_gpu_offload **out) {
+  if (!layers || !out || n_layers == 0) return fail(FLOE_ERR_INVALID, "offload_create: bad arguments");
+  *out = nullptr;
+  if (int rc = require_device("offload_create")) return rc;
+  auto o = std::make_unique<floe_gpu_offload>();
+  for (uint32_t l = 0; l < n_layers; ++l) {
+    const floe_gpu_layer *ly = layers[l];
+    if (!ly || ly->dh != layers[0]->dh || ly->E != layers[0]->E || ly->top_k != layers[0]->top_k ||
+        ly->di != layers[0]->di)
+      return fail(FLOE_ERR_INVALID, "offload_create: layer %u shape differs", l);
+    o->layers.push_back(const_cast<floe_gpu_layer *>(ly));
+  }
+  o->L = n_layers;
+  o->E = layers[0]->E;
+  o->K = layers[0]->top_k;
+  o->dh = layers[0]->dh;
+  o->budget = vram_budget;
+  o->rec_bytes = 4ull * o->dh * layers[0]->di;
+  const uint32_t N = o->L * o->E;
+  o->state.assign(N, floe_gpu_offload::kHost);
+  o->pending.assign(N, nullptr);
+  o->copy_done.assign(N, nullptr);
+  o->last_use.assign(N, 0);
+  o->resident_host.assign(N, 0);
+  CK(cudaStreamCreateWithFlags(&o->side, cudaStreamNonBlocking));
+  for (auto &ev : o->copy_done) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&o->sel_ready, cudaEventDisableTiming));
+  CK(cudaMalloc(&o->resident_dev, N));
+  CK(cudaMalloc(&o->sel_dev, 4ull * o->L * o->K));
+  CK(cudaMallocHost(&o->sel_host, 4ull * o->L * o->K));
+  CK(cudaMalloc(&o->buf, 8ull * o->dh));
+  CK(cudaMalloc(&o->acc, 16));
+  CK(cudaMemset(o->acc, 0, 16));
+  // every expert starts host-resident (records in pinned host memory)
+  for (uint32_t i = 0; i < N; ++i) {
+    floe_gpu_expert *e = o->layers[i / o->E]->experts[i % o->E];
+    if (e->up_only) return fail(FLOE_ERR_INVALID, "offload_create: expert without gate/down");
+    if (e->resident)
+      if (int rc = floe_gpu_expert_set_resident(e, 0, nullptr)) return rc;
+    o->up_bytes = e->code_bytes + 4 * e->n_groups;
+  }
+  CK(cudaMemset(o->resident_dev, 0, N));
+  CK(cudaDeviceSynchronize());
+  *out = o.release();
+  return FLOE_OK;
+}
+
+int floe_gpu_offload_destroy(floe_gpu_offload *o) {
+  if (!o) return FLOE_OK;
+  cudaDeviceSynchronize();
+  for (uint32_t i = 0; i < o->L * o->E; ++i) {
+    if (o->pending[i]) cudaFree(o->pending[i]);
+    if (o->copy_done[i]) cudaEventDestroy(o->copy_done[i]);
+  }
+  if (o->sel_ready) cudaEventDestroy(o->sel_ready);
+  if (o->side) cudaStreamDestroy(o->side);
+  cudaFree(o->resident_dev);
+  cudaFree(o->sel_dev);
+  cudaFreeHost(o->sel_host);
+  cudaFree(o->buf);
+  cudaFree(o->acc);
+  delete o;
+  return FLOE_OK;
+}
+
+int floe_gpu_offload_decode(floe_gpu_offload *o, floe_gpu_workspace *ws, const float *h_dev,
+                            float *y_dev, floe_stream_t stream) {
+  if (!o || !ws || !h_dev || !y_dev) return fail(FLOE_ERR_INVALID, "offload_decode: null argument");
+  cudaStream_t st = S(stream);
+  if (int rc = offload_policy(o, st)) return rc;
+  const float *in = h_dev;
+  for (uint32_t l = 0; l < o->L; ++l) {
+    float *outp = l + 1 == o->L ? y_dev : o->buf + (l & 1) * o->dh;
+    floe_gpu_layer_trace tr{nullptr, o->sel_dev + l * o->K, nullptr, nullptr};
+    if (int rc = floe_gpu_layer_forward(o->layers[l], ws, in, outp, &tr, stream)) return rc;
+    offload_account<<<1, 32, 0, st>>>(ws->seg_count, (uint32_t)device_info().sm, o->K,
+                                      o->sel_dev + l * o->K, o->resident_dev + l * o->E, o->acc);
+    CK_LAUNCH();
+    in = outp;
+  }
+  if (!o->sel_pending) {
+    CK(cudaMemcpyAsync(o->sel_host, o->sel_dev, 4ull * o->L * o->K, cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(o->sel_ready, st));
+    o->sel_pending = true;
+  }
+  ++o->tokens;
+  return FLOE_OK;
+}
+
+int floe_gpu_offload_stats(floe_gpu_offload *o, floe_offload_stats *out, floe_stream_t stream) {
+  if (!o || !out) return fail(FLOE_ERR_INVALID, "offload_stats: null argument");
+  unsigned long long acc[2];
+  CK(cudaStreamSynchronize(S(stream)));
+  CK(cudaMemcpy(acc, o->acc, 16, cudaMemcpyDeviceToHost));
+  std::memset(out, 0, sizeof *out);
+  out->tokens = o->tokens;
+  out->records_from_hbm = acc[0];
+  out->records_over_pcie = acc[1];
+  out->record_bytes = 4ull * o->dh;
+  out->up_bytes_per_expert = o->up_bytes;
+  out->promotions = o->promotions;
+  out->evictions = o->evictions;
+  out->bytes_promoted = o->bytes_promoted;
+  uint64_t dev = 0;
+  for (uint32_t i = 0; i < o->L * o->E; ++i)
+    if (o->state[i] == floe_gpu_offload::kResident) dev += o->rec_bytes;
+  out->device_record_bytes = dev;
+  return FLOE_OK;
+}
+
+}  // extern "C"
 
 // ------------------------------------------------------- synthetic model ---
 int floe_gpu_gen_normals(uint64_t seed, uint64_t stream_id, uint64_t n, float sigma,

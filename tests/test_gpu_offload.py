@@ -72,3 +72,52 @@ def test_layer_tables_follow_residency(fb, torch):
         hosted[t % E].set_resident(True)  # the layer table switches with the expert
         yc = fb.layer_forward(lb, h, ws).cpu().numpy()
         assert O.rel_l2(yc, ya) <= 1e-6
+
+
+def _stack(fb, L, E, K, dh, di, host):
+    rng = np.random.default_rng(11)
+    layers = []
+    for l in range(L):
+        ex = []
+        for e in range(E):
+            gate, up, down = O.seeded_expert(dh, di, 100 * l + e)
+            q = O.quantize(up, 2, 64)
+            ex.append(fb.GpuExpert(dh, di, 2, 64, q.codes, q.scales, q.zeros, gate=gate,
+                                   down=down, threshold=1.0, host_records=host))
+        router = (rng.standard_normal((E, dh)) / 45).astype(np.float32)
+        mixing = (rng.standard_normal((dh, dh)) / 45).astype(np.float32)
+        layers.append(fb.GpuLayer(router, mixing, ex, K))
+    return layers
+
+
+@pytest.mark.parametrize("budget_experts", [0, 3, 100])
+def test_offload_decode_matches_resident_chain(fb, torch, budget_experts):
+    """decode through host-resident layers == the chain of layer_forward calls
+    on HBM-resident copies, for any VRAM budget; the record accounting covers
+    every kept channel exactly once."""
+    L, E, K, dh, di = 3, 4, 2, 2048, 512
+    ref_layers = _stack(fb, L, E, K, dh, di, host=False)
+    host_layers = _stack(fb, L, E, K, dh, di, host=True)
+    off = fb.Offload(host_layers, budget_experts * 4 * dh * di)
+    ws = fb.Workspace(dh, di, K)
+    ws_ref = fb.Workspace(dh, di, K)
+    ws_ref.reset_counters()
+    for t in range(6):
+        h = torch.from_numpy(O.token_input(2, t, dh)).cuda()
+        y = off.decode(h, ws)
+        r = h
+        for L_ in ref_layers:
+            r = fb.layer_forward(L_, r, ws_ref)
+        torch.cuda.synchronize()
+        assert O.rel_l2(y.cpu().numpy(), r.cpu().numpy()) <= 1e-5
+    st = off.stats()
+    kept = ws_ref.read_counters()["kept"]
+    assert st["tokens"] == 6
+    assert st["records_from_hbm"] + st["records_over_pcie"] == kept
+    if budget_experts == 0:
+        assert st["records_from_hbm"] == 0 and st["promotions"] == 0
+    if budget_experts == 100:
+        assert st["promotions"] > 0 and st["evictions"] == 0
+        assert st["records_from_hbm"] > 0
+    assert st["device_record_bytes"] <= budget_experts * 4 * dh * di
+    off.close()
