@@ -249,6 +249,11 @@ int floe_gpu_offload_create(floe_gpu_layer *const *layers, uint32_t n_layers,
 int floe_gpu_offload_destroy(floe_gpu_offload *o);
 int floe_gpu_offload_decode(floe_gpu_offload *o, floe_gpu_workspace *ws, const float *h_dev,
                             float *y_dev, floe_stream_t stream);
+/* decode_replay: every layer l reads its own block input h_dev[l*d_hidden ..]
+ * and writes y_dev[l*d_hidden ..] (replay of recorded hidden states,
+ * predictor.cpp:60-85) -- same placement policy and accounting as decode. */
+int floe_gpu_offload_decode_replay(floe_gpu_offload *o, floe_gpu_workspace *ws,
+                                   const float *h_dev, float *y_dev, floe_stream_t stream);
 int floe_gpu_offload_stats(floe_gpu_offload *o, floe_offload_stats *out, floe_stream_t stream);
 
 /* ----------------------------------------------------- counters / profile */

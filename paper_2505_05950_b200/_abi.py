@@ -72,6 +72,7 @@ _SIGS = {
     "floe_gpu_offload_create": (ct.c_int, [_P, _U32, ct.c_uint64, _P]),
     "floe_gpu_offload_destroy": (ct.c_int, [_P]),
     "floe_gpu_offload_decode": (ct.c_int, [_P, _P, _P, _P, _P]),
+    "floe_gpu_offload_decode_replay": (ct.c_int, [_P, _P, _P, _P, _P]),
     "floe_gpu_offload_stats": (ct.c_int, [_P, _P, _P]),
     "floe_gpu_expert_set_resident": (ct.c_int, [_P, ct.c_int, _P]),
     "floe_gpu_expert_residency": (ct.c_int, [_P, _P, _P]),
@@ -520,6 +521,18 @@ class Offload:
         y = torch.empty(self.d_hidden, dtype=torch.float32, device=h.device) if out is None else out
         _check(lib().floe_gpu_offload_decode(self.handle, ws.handle, h.data_ptr(), y.data_ptr(),
                                              _stream(stream)))
+        return y
+
+    def decode_replay(self, h, ws: Workspace, out=None, stream=None):
+        """One token, each layer on its own recorded block input: h [L, dh] -> y [L, dh]."""
+        torch = _torch()
+        L = len(self.layers)
+        if tuple(h.shape) != (L, self.d_hidden) or h.dtype != torch.float32 or not h.is_cuda:
+            raise FloeError("offload_decode_replay: h must be a cuda float32 [layers, d_hidden]")
+        h = h.contiguous()
+        y = torch.empty_like(h) if out is None else out
+        _check(lib().floe_gpu_offload_decode_replay(self.handle, ws.handle, h.data_ptr(),
+                                                    y.data_ptr(), _stream(stream)))
         return y
 
     def stats(self, stream=None) -> dict:

@@ -315,6 +315,7 @@ struct FusedLaunch {
   float *u, *y, *v_out;
   uint8_t *mask_out;
   uint32_t *n_kept_out, *kept_out;
+  unsigned long long *place_acc;  // nullable: offload engine's HBM / PCIe record counts
 };
 
 template <int DH>
@@ -375,6 +376,7 @@ int launch_v2_dh(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) 
   a.n_kept_out = L.n_kept_out;
   a.kept_out = L.kept_out;
   a.stats = L.k1_only ? nullptr : ws->stats;
+  a.place_acc = L.place_acc;
   a.phase_ns = ws->phase_ns;
   a.ns = ns;
   a.max_tiles = max_tiles;
@@ -544,6 +546,7 @@ int floe_gpu_expert_create(const floe_expert_host_view *v, floe_gpu_expert **out
     }
   }
   e->host_desc.records = e->rec_dev;
+  e->host_desc.host_records = 0;
   e->host_desc.threshold = v->threshold;
 
   auto cleanup = [&](int rc) {
@@ -661,10 +664,12 @@ int floe_gpu_expert_set_resident(floe_gpu_expert *e, int resident, floe_stream_t
     void *dptr = nullptr;
     CK(cudaHostGetDevicePointer(&dptr, e->rec_host, 0));
     e->host_desc.records = static_cast<const __half *>(dptr);
+    e->host_desc.host_records = 1;
   } else {
     CK(cudaMallocAsync(reinterpret_cast<void **>(&e->rec_dev), bytes, st));
     CK(cudaMemcpyAsync(e->rec_dev, e->rec_host, bytes, cudaMemcpyHostToDevice, st));
     e->host_desc.records = e->rec_dev;
+    e->host_desc.host_records = 0;
   }
   CK(cudaMemcpyAsync(e->dev_desc, &e->host_desc, sizeof(ExpertDesc), cudaMemcpyHostToDevice, st));
   for (ExpertDesc *t : e->tables)
@@ -1066,12 +1071,28 @@ int floe_gpu_layer_destroy(floe_gpu_layer *l) {
   return FLOE_OK;
 }
 
+namespace {
+// place_acc (nullable, fast path only): the fused kernel adds each slot's kept
+// record count to [0] (records in HBM) or [1] (pinned host records over PCIe).
+int layer_forward_impl(const floe_gpu_layer *l, floe_gpu_workspace *ws, const float *h, float *y,
+                       const floe_gpu_layer_trace *tr, unsigned long long *place_acc,
+                       cudaStream_t st);
+}  // namespace
+
 int floe_gpu_layer_forward(const floe_gpu_layer *l, floe_gpu_workspace *ws, const float *h,
                            float *y, const floe_gpu_layer_trace *tr, floe_stream_t stream) {
   if (!l || !h || !y) return fail(FLOE_ERR_INVALID, "layer_forward: null argument");
   if (int rc = check_ws("layer_forward", ws, l->dh, l->di, l->top_k)) return rc;
-  cudaStream_t st = S(stream);
-  if (l->fast && l->E <= 32) {
+  return layer_forward_impl(l, ws, h, y, tr, nullptr, S(stream));
+}
+
+namespace {
+bool layer_fused(const floe_gpu_layer *l) { return l->fast && l->E <= 32; }
+
+int layer_forward_impl(const floe_gpu_layer *l, floe_gpu_workspace *ws, const float *h, float *y,
+                       const floe_gpu_layer_trace *tr, unsigned long long *place_acc,
+                       cudaStream_t st) {
+  if (layer_fused(l)) {
     FusedLaunch f{};
     f.mixing = l->mixing;
     f.mix_f16 = l->mix_f16;
@@ -1087,6 +1108,7 @@ int floe_gpu_layer_forward(const floe_gpu_layer *l, floe_gpu_workspace *ws, cons
     f.x = ws->u;
     f.u = ws->u;
     f.y = y;
+    f.place_acc = place_acc;
     return launch_v2(f, ws, st);
   }
   float *u_tr = tr ? tr->block_input_dev : nullptr;
@@ -1128,6 +1150,7 @@ int floe_gpu_layer_forward(const floe_gpu_layer *l, floe_gpu_workspace *ws, cons
   K2Launch k2{l->table, ws->sel, ws->weights, l->top_k, l->dh, l->di, ws->u, y, nullptr, nullptr};
   return launch_k2(k2, ws, st);
 }
+}  // namespace
 
 int floe_gpu_layer_forward_host(const floe_gpu_layer *l, floe_gpu_workspace *ws,
                                 const float *h_host, float *y_host, floe_stream_t stream) {
@@ -1179,6 +1202,7 @@ struct floe_gpu_offload {
   std::vector<__half *> pending;              // [L*E] device copy in flight
   std::vector<cudaEvent_t> copy_done;         // [L*E]
   std::vector<uint64_t> last_use;             // [L*E] token of last routing
+  std::vector<float> freq;                    // [L*E] decayed routing count
   uint8_t *resident_dev = nullptr;            // [L*E] for the byte accounting
   std::vector<uint8_t> resident_host;
   uint32_t *sel_dev = nullptr;                // [L][K] routing of the last token
@@ -1199,10 +1223,12 @@ int offload_switch(floe_gpu_offload *o, uint32_t i, bool to_hbm, cudaStream_t st
     e->rec_dev = o->pending[i];
     o->pending[i] = nullptr;
     e->host_desc.records = e->rec_dev;
+    e->host_desc.host_records = 0;
   } else {
     void *dptr = nullptr;
     CK(cudaHostGetDevicePointer(&dptr, e->rec_host, 0));
     e->host_desc.records = static_cast<const __half *>(dptr);
+    e->host_desc.host_records = 1;
   }
   CK(cudaMemcpyAsync(e->dev_desc, &e->host_desc, sizeof(ExpertDesc), cudaMemcpyHostToDevice, st));
   for (ExpertDesc *t : e->tables)
@@ -1218,8 +1244,12 @@ int offload_switch(floe_gpu_offload *o, uint32_t i, bool to_hbm, cudaStream_t st
 }
 
 // Between tokens: switch in finished copies; read the previous token's routing
-// (if it is done) and promote its missing experts, evicting least recently
-// used ones to stay under the budget.
+// (if it is done) and promote its missing experts into free budget, or in
+// place of a resident expert routed clearly less often (ExpertCache's LRU,
+// offload.cpp:89-159, with frequency-aware admission: see below).
+constexpr float kFreqDecay = 0.98f;   // per token: a ~50-token memory of routing counts
+constexpr float kAdmitMargin = 3.0f;  // extra routings (decayed) to displace a resident expert
+
 int offload_policy(floe_gpu_offload *o, cudaStream_t st) {
   const uint32_t N = o->L * o->E;
   for (uint32_t i = 0; i < N; ++i)
@@ -1230,20 +1260,29 @@ int offload_policy(floe_gpu_offload *o, cudaStream_t st) {
   if (!o->sel_pending || cudaEventQuery(o->sel_ready) != cudaSuccess) return FLOE_OK;
   o->sel_pending = false;
   std::vector<uint32_t> want;
+  for (float &f : o->freq) f *= kFreqDecay;
   for (uint32_t l = 0; l < o->L; ++l)
     for (uint32_t k = 0; k < o->K; ++k) {
       const uint32_t i = l * o->E + o->sel_host[l * o->K + k];
       o->last_use[i] = o->tokens;
+      o->freq[i] += 1.0f;
       if (o->state[i] == floe_gpu_offload::kHost) want.push_back(i);
     }
   for (uint32_t i : want) {
-    while (o->committed + o->rec_bytes > o->budget) {  // evict the LRU resident expert
+    while (o->committed + o->rec_bytes > o->budget) {  // the budget is full: pick a victim
+      // least frequently routed resident expert, ties to the least recently used
       int64_t victim = -1;
       for (uint32_t j = 0; j < N; ++j)
         if (o->state[j] == floe_gpu_offload::kResident &&
-            (victim < 0 || o->last_use[j] < o->last_use[victim]))
+            (victim < 0 || o->freq[j] < o->freq[victim] ||
+             (o->freq[j] == o->freq[victim] && o->last_use[j] < o->last_use[victim])))
           victim = j;
       if (victim < 0 || o->last_use[victim] >= o->tokens) break;  // nothing evictable
+      // Admission: a promotion moves the whole record block (~1/keep-fraction
+      // times what one routing reads in place), so replace a resident expert
+      // only for one routed clearly more often; otherwise a budget smaller
+      // than the working set thrashes and pays more PCIe than it saves.
+      if (o->freq[i] < o->freq[victim] + kAdmitMargin) break;
       if (int rc = offload_switch(o, (uint32_t)victim, false, st)) return rc;
       o->state[victim] = floe_gpu_offload::kHost;
       o->committed -= o->rec_bytes;
@@ -1289,6 +1328,7 @@ int floe_gpu_offload_create(floe_gpu_layer *const *layers, uint32_t n_layers,
   o->pending.assign(N, nullptr);
   o->copy_done.assign(N, nullptr);
   o->last_use.assign(N, 0);
+  o->freq.assign(N, 0.0f);
   o->resident_host.assign(N, 0);
   CK(cudaStreamCreateWithFlags(&o->side, cudaStreamNonBlocking));
   for (auto &ev : o->copy_done) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -1331,19 +1371,33 @@ int floe_gpu_offload_destroy(floe_gpu_offload *o) {
   return FLOE_OK;
 }
 
-int floe_gpu_offload_decode(floe_gpu_offload *o, floe_gpu_workspace *ws, const float *h_dev,
-                            float *y_dev, floe_stream_t stream) {
-  if (!o || !ws || !h_dev || !y_dev) return fail(FLOE_ERR_INVALID, "offload_decode: null argument");
-  cudaStream_t st = S(stream);
+namespace {
+// One token through every layer.  replay == false: the layers chain
+// (h -> layer 0 -> ... -> y, as predictor.cpp:66-83 drives layer_forward).
+// replay == true: layer l reads its own recorded block input h[l] and writes
+// y[l] (the traces the reference pairs with routing decisions,
+// predictor.cpp:60-85), so a benchmark can hold every layer at its calibrated
+// sparsity instead of following a random-weight stack's growing activations.
+int offload_token(floe_gpu_offload *o, floe_gpu_workspace *ws, const float *h_dev, float *y_dev,
+                  bool replay, cudaStream_t st) {
   if (int rc = offload_policy(o, st)) return rc;
   const float *in = h_dev;
   for (uint32_t l = 0; l < o->L; ++l) {
-    float *outp = l + 1 == o->L ? y_dev : o->buf + (l & 1) * o->dh;
+    float *outp = replay ? y_dev + (size_t)l * o->dh
+                         : (l + 1 == o->L ? y_dev : o->buf + (l & 1) * o->dh);
+    if (replay) in = h_dev + (size_t)l * o->dh;
     floe_gpu_layer_trace tr{nullptr, o->sel_dev + l * o->K, nullptr, nullptr};
-    if (int rc = floe_gpu_layer_forward(o->layers[l], ws, in, outp, &tr, stream)) return rc;
-    offload_account<<<1, 32, 0, st>>>(ws->seg_count, (uint32_t)device_info().sm, o->K,
-                                      o->sel_dev + l * o->K, o->resident_dev + l * o->E, o->acc);
-    CK_LAUNCH();
+    const floe_gpu_layer *ly = o->layers[l];
+    if (int rc = check_ws("offload_decode", ws, ly->dh, ly->di, ly->top_k)) return rc;
+    if (layer_fused(ly)) {  // the fused kernel does the record accounting itself
+      if (int rc = layer_forward_impl(ly, ws, in, outp, &tr, o->acc, st)) return rc;
+    } else {
+      if (int rc = layer_forward_impl(ly, ws, in, outp, &tr, nullptr, st)) return rc;
+      offload_account<<<1, 32, 0, st>>>(ws->seg_count, (uint32_t)device_info().sm, o->K,
+                                        o->sel_dev + l * o->K, o->resident_dev + l * o->E,
+                                        o->acc);
+      CK_LAUNCH();
+    }
     in = outp;
   }
   if (!o->sel_pending) {
@@ -1353,6 +1407,20 @@ int floe_gpu_offload_decode(floe_gpu_offload *o, floe_gpu_workspace *ws, const f
   }
   ++o->tokens;
   return FLOE_OK;
+}
+}  // namespace
+
+int floe_gpu_offload_decode(floe_gpu_offload *o, floe_gpu_workspace *ws, const float *h_dev,
+                            float *y_dev, floe_stream_t stream) {
+  if (!o || !ws || !h_dev || !y_dev) return fail(FLOE_ERR_INVALID, "offload_decode: null argument");
+  return offload_token(o, ws, h_dev, y_dev, false, S(stream));
+}
+
+int floe_gpu_offload_decode_replay(floe_gpu_offload *o, floe_gpu_workspace *ws,
+                                   const float *h_dev, float *y_dev, floe_stream_t stream) {
+  if (!o || !ws || !h_dev || !y_dev)
+    return fail(FLOE_ERR_INVALID, "offload_decode_replay: null argument");
+  return offload_token(o, ws, h_dev, y_dev, true, S(stream));
 }
 
 int floe_gpu_offload_stats(floe_gpu_offload *o, floe_offload_stats *out, floe_stream_t stream) {

@@ -36,7 +36,8 @@ struct ExpertDesc {
   const __half *records;   // [di][2*dh]
   const uint32_t *tiles;   // fast path: tile-fragment up projection (floe_v2.cuh)
   float threshold;
-  uint32_t pad_[3];
+  uint32_t host_records;   // records read in place from pinned host memory (over PCIe)
+  uint32_t pad_[2];
 };
 
 // Kept-channel lists ("segments").  K1 runs on a (G1, slots) grid; CTA b of
@@ -359,6 +360,25 @@ struct MixArgs {
   float *w_trace;
 };
 
+// Total order for top_k: larger value first, ties (incl. -0 == +0) to the
+// lower index, as la.cpp:52-55.  The reference's comparator is not a strict
+// weak order once a NaN is present; here a NaN ranks below every number
+// (-inf included), so every lane and thread agrees on an in-range selection
+// for any input.  Key = (class|ordered value) << 8 | (255 - index); 0 never
+// occurs for a real candidate.
+__device__ __forceinline__ unsigned long long topk_key(float v, uint32_t i) {
+  uint32_t hi;
+  if (isnan(v)) {
+    hi = 0u;
+  } else {
+    const uint32_t u = __float_as_uint(v == 0.0f ? 0.0f : v);
+    hi = 1u + ((u >> 31) ? ~u : (u | 0x80000000u));  // -inf -> 0x00800000
+  }
+  return ((unsigned long long)hi << 8) | (255u - i);
+}
+__device__ __forceinline__ uint32_t topk_index(unsigned long long key) {
+  return 255u - (uint32_t)(key & 255u);
+}
 __device__ inline void topk_small(const float *v, uint32_t n, uint32_t k, uint32_t *out);
 
 // route (model.cpp:83-93) after the logits: top_k, softmax over the selected
@@ -472,13 +492,12 @@ __device__ inline void topk_small(const float *v, uint32_t n, uint32_t k,
                                   uint32_t *out) {
   uint32_t taken = 0;  // n <= 32
   for (uint32_t r = 0; r < k; ++r) {
-    int best = -1;
-    for (uint32_t i = 0; i < n; ++i) {
-      if (taken & (1u << i)) continue;
-      if (best < 0 || v[i] > v[best] || (v[i] == v[best] && (int)i < best)) best = (int)i;
-    }
-    taken |= 1u << best;
-    out[r] = (uint32_t)best;
+    unsigned long long best = 0;
+    for (uint32_t i = 0; i < n; ++i)
+      if (!(taken & (1u << i))) best = max(best, topk_key(v[i], i));
+    const uint32_t bi = topk_index(best);
+    taken |= 1u << bi;
+    out[r] = bi;
   }
   for (uint32_t i = 1; i < k; ++i)
     for (uint32_t j = i; j > 0 && out[j - 1] > out[j]; --j) {

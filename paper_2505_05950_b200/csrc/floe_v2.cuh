@@ -340,6 +340,7 @@ struct FusedArgs {
   uint32_t *n_kept_out;  // nullable [slots]
   uint32_t *kept_out;    // nullable [slots][di], ascending-by-CTA order
   unsigned long long *stats;
+  unsigned long long *place_acc;  // nullable [2]: kept records read from HBM / over PCIe
   unsigned long long *phase_ns;  // nullable [G][kTraceSlots]
   uint32_t ns;        // ring stages
   uint32_t max_tiles; // per-CTA tile capacity of the smem emit buffer
@@ -713,22 +714,15 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
       // warp arg-max rounds; softmax over the selected logits (la.cpp:37-46)
       __syncwarp();  // converged: otherwise the shuffles take the BRA.DIV slow path
       const float lg = lane < a.n_experts ? logits[lane] : -__int_as_float(0x7f800000);
+      const unsigned long long mykey = floe_k::topk_key(lg, lane);  // NaN-safe total order
       uint32_t taken = 0;
 #pragma unroll 1
       for (uint32_t r = 0; r < a.top_k; ++r) {
         const bool cand = lane < a.n_experts && !((taken >> lane) & 1u);
-        float bv = cand ? lg : -__int_as_float(0x7f800000);
-        uint32_t bi = cand ? lane : 64u;
+        unsigned long long bk = cand ? mykey : 0ull;
 #pragma unroll 1
-        for (int o = 16; o >= 1; o >>= 1) {
-          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-          const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ov > bv || (ov == bv && oi < bi)) {
-            bv = ov;
-            bi = oi;
-          }
-        }
-        taken |= 1u << bi;
+        for (int o = 16; o >= 1; o >>= 1) bk = max(bk, __shfl_xor_sync(0xffffffffu, bk, o));
+        taken |= 1u << floe_k::topk_index(bk);
       }
       if (lane == 0 && a.phase_ns) a.phase_ns[blockIdx.x * kTraceSlots + 14] = gtime();
       // softmax over the selected logits in registers (no local-memory arrays:
@@ -995,12 +989,15 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
       atomicAdd(&a.stats[0], 1ull);
       atomicAdd(&a.stats[1], (unsigned long long)T);
     }
-    if (a.n_kept_out && warp < a.slots) {
+    if ((a.n_kept_out || a.place_acc) && warp < a.slots) {
       uint32_t n = 0;
       for (uint32_t bb = lane; bb < G; bb += 32) n += __ldcg(&a.seg_count[warp * G + bb]);
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
-      if (lane == 0) a.n_kept_out[warp] = n;
+      if (lane == 0 && a.n_kept_out) a.n_kept_out[warp] = n;
+      if (lane == 0 && a.place_acc)  // where this slot's kept records are read from
+        atomicAdd(&a.place_acc[table_s[sel_s[warp]].host_records ? 1 : 0],
+                  (unsigned long long)n);
     }
   }
   if (a.kept_out && warp < a.slots) {

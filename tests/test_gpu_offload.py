@@ -121,3 +121,53 @@ def test_offload_decode_matches_resident_chain(fb, torch, budget_experts):
         assert st["records_from_hbm"] > 0
     assert st["device_record_bytes"] <= budget_experts * 4 * dh * di
     off.close()
+
+
+def test_offload_decode_replay_matches_layer_forward(fb, torch):
+    """decode_replay: layer l on its own recorded block input == layer_forward."""
+    L, E, K, dh, di = 3, 4, 2, 2048, 512
+    ref_layers = _stack(fb, L, E, K, dh, di, host=False)
+    off = fb.Offload(_stack(fb, L, E, K, dh, di, host=True), 2 * 4 * dh * di)
+    ws, ws_ref = fb.Workspace(dh, di, K), fb.Workspace(dh, di, K)
+    for t in range(4):
+        h = torch.stack([torch.from_numpy(O.token_input(7 + l, t, dh)) for l in range(L)]).cuda()
+        y = off.decode_replay(h, ws)
+        for l in range(L):
+            r = fb.layer_forward(ref_layers[l], h[l], ws_ref)
+            assert O.rel_l2(y[l].cpu().numpy(), r.cpu().numpy()) <= 1e-5
+    with pytest.raises(fb.FloeError):
+        off.decode_replay(h[0], ws)
+    off.close()
+
+
+@pytest.mark.parametrize("dh,di", [(4096, 2048), (2048, 512), (256, 256)])
+@pytest.mark.parametrize("bad", ["inf", "nan"])
+def test_layer_forward_nonfinite_input_terminates(fb, torch, dh, di, bad):
+    """A non-finite block input (a random-weight stack chained far enough
+    overflows) must give an in-range routing and a non-finite output, never a
+    hang or a fault.  The reference's top_k comparator (la.cpp:52-55) is not a
+    strict weak order with NaNs; here NaN ranks below every number."""
+    E, K = 4, 2
+    ex = []
+    for e in range(E):
+        gate, up, down = O.seeded_expert(dh, di, 300 + e)
+        q = O.quantize(up, 2, 64)
+        ex.append(fb.GpuExpert(dh, di, 2, 64, q.codes, q.scales, q.zeros, gate=gate, down=down,
+                               threshold=1.0))
+    rng = np.random.default_rng(5)
+    router = (rng.standard_normal((E, dh)) / np.sqrt(dh)).astype(np.float32)
+    mixing = (rng.standard_normal((dh, dh)) / np.sqrt(dh)).astype(np.float32)
+    layer = fb.GpuLayer(router, mixing, ex, K)
+    ws = fb.Workspace(dh, di, K)
+    h = torch.from_numpy(O.token_input(1, 0, dh)).cuda()
+    h[dh // 3] = float(bad)
+    r = fb.layer_forward(layer, h, ws, traced=True)
+    torch.cuda.synchronize()
+    sel = r["experts"].cpu().numpy()
+    assert ((sel >= 0) & (sel < E)).all() and len(set(sel.tolist())) == K
+    assert list(sel) == sorted(sel)
+    assert not torch.isfinite(r["out"]).all()
+    # the device is still healthy: a finite input afterwards gives the normal result
+    h2 = torch.from_numpy(O.token_input(1, 1, dh)).cuda()
+    y2 = fb.layer_forward(layer, h2, ws).cpu().numpy()
+    assert np.isfinite(y2).all()
