@@ -373,6 +373,11 @@ int launch_v2_dh(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) 
   a.kept_v = ws->kept_v;
   a.seg_count = ws->seg_count;
   a.bar = ws->bar;
+  static const uint32_t early_env = [] {
+    const char *p = std::getenv("FLOE_EARLY");
+    return p ? (uint32_t)std::atoi(p) : 2u;
+  }();
+  a.early = std::min<uint32_t>(early_env, ns);
   a.n_kept_out = L.n_kept_out;
   a.kept_out = L.kept_out;
   a.stats = L.k1_only ? nullptr : ws->stats;

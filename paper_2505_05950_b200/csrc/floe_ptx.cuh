@@ -121,6 +121,11 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   return p;
 }
 
+// Fire-and-forget bulk prefetch of global memory into L2 (no smem, no barrier).
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes,
                                               uint64_t *bar, uint64_t policy) {
   asm volatile(

@@ -345,6 +345,7 @@ struct FusedArgs {
   uint32_t ns;        // ring stages
   uint32_t max_tiles; // per-CTA tile capacity of the smem emit buffer
   uint32_t debug;     // diagnostics (FLOE_DEBUG_FLAGS): bit 1 = phase C waits only, no math
+  uint32_t early;     // mixing stages issued before griddepcontrol.wait (PDL overlap)
 };
 
 // Dynamic shared memory layout (bytes), host and device agree.
@@ -411,6 +412,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   __shared__ const __half *rec_s[floe_k::kMaxSlots];
   __shared__ const uint8_t *tiles_s[floe_k::kMaxSlots];
   __shared__ float thr_s[floe_k::kMaxSlots];
+  __shared__ uint32_t rhost_s[floe_k::kMaxSlots];  // records in pinned host memory
   __shared__ uint32_t ws8[kConsumerWarps];
   __shared__ float2 xch[kPairs][2][8];  // phase B: upper-half partials of a pair's tile
   __shared__ float redmax[kConsumerWarps];
@@ -514,7 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
       // mixing rows are read-only weights: the first two stream in before the
       // previous grid has finished (PDL); h (the previous layer's output)
       // goes right after them so it is not queued behind the whole ring
-      const uint32_t early = min(nA, 2u);
+      const uint32_t early = min(nA, a.early);
       for (uint32_t i = 0; i < nA; ++i) {
         if (i == early) {
           pdl_wait();
@@ -553,6 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
       P = min(n_own, nsC);
       for (uint32_t k = 0; k < P; ++k) issueC(k, isrc[k], iscale[k]);
       pv[5] = P;
+
     }
     __syncwarp();
     mark(a, 17);
@@ -763,6 +766,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   if (t < a.slots) {
     const ExpertDesc &d = table_s[sel_s[t]];
     rec_s[t] = d.records;
+    rhost_s[t] = d.host_records;
     tiles_s[t] = reinterpret_cast<const uint8_t *>(d.tiles);
     thr_s[t] = a.use_threshold ? a.threshold : d.threshold;
     slot_cnt[t] = 0;
