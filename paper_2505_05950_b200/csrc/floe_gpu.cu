@@ -167,6 +167,7 @@ struct floe_gpu_layer {
   bool mix_f16 = false, fast = false;
   float *router = nullptr;
   void *mixing = nullptr;
+  float *router_pred = nullptr;  // fused path: router + router * mixing (speculative K1)
   ExpertDesc *table = nullptr;
   std::vector<floe_gpu_expert *> experts;  // borrowed (offload engine)
 };
@@ -302,7 +303,7 @@ struct FusedLaunch {
   // layer mode (mixing != nullptr) or single-expert mode
   const void *mixing;
   bool mix_f16;
-  const float *h, *router;
+  const float *h, *router, *router_pred;
   uint32_t n_experts, top_k;
   const floe_gpu_layer_trace *trace;
   // experts
@@ -351,6 +352,7 @@ int launch_v2_dh(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) 
   a.mix_f16 = L.mix_f16;
   a.h = L.h;
   a.router = L.router;
+  a.router_pred = L.router_pred;
   a.n_experts = L.n_experts;
   a.top_k = L.top_k;
   a.partial = ws->mix_partial;
@@ -1059,6 +1061,28 @@ int floe_gpu_layer_create(const floe_layer_host_view *v, floe_gpu_layer **out) {
       if (tmp) cudaFree(tmp);
     }
   }
+  // Predicted routing for the fused kernel's speculative K1 stream:
+  // router * (h + mixing h) = (router + router * mixing) h, with the mixing
+  // weights exactly as the kernel reads them.  Only a prediction: the kernel
+  // still routes on the exact logits and discards a wrong speculation.
+  static const bool spec_env = [] {
+    const char *p = std::getenv("FLOE_SPEC");
+    return !(p && std::strcmp(p, "0") == 0);
+  }();
+  if (ce == cudaSuccess && spec_env && l->fast && l->E <= 32) {
+    ce = cudaMalloc(&l->router_pred, 4ull * l->E * dh);
+    if (ce == cudaSuccess) {
+      const uint32_t blocks = (dh + 127) / 128;
+      if (l->mix_f16)
+        floe_k::router_pred<__half><<<blocks, 128>>>(l->router, static_cast<const __half *>(l->mixing),
+                                                      l->E, dh, l->router_pred);
+      else
+        floe_k::router_pred<float><<<blocks, 128>>>(l->router, static_cast<const float *>(l->mixing),
+                                                     l->E, dh, l->router_pred);
+      ce = cudaGetLastError();
+      if (ce == cudaSuccess) ce = cudaDeviceSynchronize();
+    }
+  }
   if (ce != cudaSuccess) {
     floe_gpu_layer_destroy(l);
     return fail(FLOE_ERR_OOM, "layer_create: %s", cudaGetErrorString(ce));
@@ -1071,6 +1095,7 @@ int floe_gpu_layer_destroy(floe_gpu_layer *l) {
   if (!l) return FLOE_OK;
   if (l->router) cudaFree(l->router);
   if (l->mixing) cudaFree(l->mixing);
+  if (l->router_pred) cudaFree(l->router_pred);
   if (l->table) cudaFree(l->table);
   delete l;
   return FLOE_OK;
@@ -1103,6 +1128,7 @@ int layer_forward_impl(const floe_gpu_layer *l, floe_gpu_workspace *ws, const fl
     f.mix_f16 = l->mix_f16;
     f.h = h;
     f.router = l->router;
+    f.router_pred = l->router_pred;
     f.n_experts = l->E;
     f.top_k = l->top_k;
     f.trace = tr;

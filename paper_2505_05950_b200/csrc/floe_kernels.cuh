@@ -553,4 +553,25 @@ __global__ void __launch_bounds__(256) route_topk(const float *__restrict__ w,
   }
 }
 
+// router_pred = router + router * mixing ([E][dh], E <= 32), the fused
+// kernel's routing predictor.  Thread j owns column j; setup only.
+template <typename MT>
+__global__ void router_pred(const float *__restrict__ router, const MT *__restrict__ mixing,
+                            uint32_t E, uint32_t dh, float *__restrict__ out) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= dh) return;
+  float acc[32];
+#pragma unroll
+  for (int e = 0; e < 32; ++e) acc[e] = 0.0f;
+  for (uint32_t i = 0; i < dh; ++i) {
+    const float m = static_cast<float>(mixing[(size_t)i * dh + j]);
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+      if ((uint32_t)e < E) acc[e] = fmaf(router[(size_t)e * dh + i], m, acc[e]);
+  }
+#pragma unroll
+  for (int e = 0; e < 32; ++e)
+    if ((uint32_t)e < E) out[(size_t)e * dh + j] = router[(size_t)e * dh + j] + acc[e];
+}
+
 }  // namespace floe_k

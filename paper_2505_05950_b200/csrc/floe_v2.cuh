@@ -316,6 +316,9 @@ struct FusedArgs {
   int mix_f16;
   const float *h;
   const float *router;  // [E][DH]
+  // nullable [E][DH]: router + router * mixing, so predicted logits =
+  // router_pred * h need no mixing GEMV (speculative K1 streaming, below)
+  const float *router_pred;
   uint32_t n_experts, top_k;
   float *partial;  // [G][32]
   float *u_trace;
@@ -344,7 +347,8 @@ struct FusedArgs {
   unsigned long long *phase_ns;  // nullable [G][kTraceSlots]
   uint32_t ns;        // ring stages
   uint32_t max_tiles; // per-CTA tile capacity of the smem emit buffer
-  uint32_t debug;     // diagnostics (FLOE_DEBUG_FLAGS): bit 1 = phase C waits only, no math
+  uint32_t debug;     // diagnostics (FLOE_DEBUG_FLAGS): bit 1 = phase C waits only, no math;
+                      // bit 3 = invert the routing prediction (misprediction path)
   uint32_t early;     // mixing stages issued before griddepcontrol.wait (PDL overlap)
 };
 
@@ -393,6 +397,23 @@ __device__ __forceinline__ TileRef tile_ref(uint32_t i, uint32_t tps, uint32_t d
   return r;
 }
 
+// top_k as k warp arg-max rounds over lanes < E holding one logit each
+// (la.cpp:48-61; NaN-safe total order, floe_k::topk_key); returns the
+// selection as a lane mask (ascending order = rank of the set bits).
+__device__ __forceinline__ uint32_t warp_topk(float lg, uint32_t lane, uint32_t E, uint32_t K) {
+  const unsigned long long mykey = floe_k::topk_key(lg, lane);
+  uint32_t taken = 0;
+#pragma unroll 1
+  for (uint32_t r = 0; r < K; ++r) {
+    const bool cand = lane < E && !((taken >> lane) & 1u);
+    unsigned long long bk = cand ? mykey : 0ull;
+#pragma unroll 1
+    for (int o = 16; o >= 1; o >>= 1) bk = max(bk, __shfl_xor_sync(0xffffffffu, bk, o));
+    taken |= 1u << floe_k::topk_index(bk);
+  }
+  return taken;
+}
+
 template <int DH>
 __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   constexpr uint32_t TILE_B = tile_bytes(DH);
@@ -404,6 +425,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   __shared__ uint64_t fullC[kMaxStagesC], emptyC[kMaxStagesC];
   __shared__ float stage_scale[kMaxStagesC];
   __shared__ uint64_t hbar;
+  __shared__ uint64_t predbar;                      // predicted routing published
+  __shared__ const uint8_t *ptiles_s[floe_k::kMaxSlots];
+  __shared__ uint32_t psel_s[floe_k::kMaxSlots];
+  __shared__ float plog[32];
+  __shared__ uint32_t spec_ok, ptaken_s;
   __shared__ float rs[32 * kMaxRowsPerCta];
   __shared__ float plw[kConsumerWarps][32];
   __shared__ float logits[32];
@@ -493,6 +519,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
       floe_ptx::mbar_init(&emptyC[s], 8);  // the 8 warps of the record's group
     }
     floe_ptx::mbar_init(&hbar, 1);
+    floe_ptx::mbar_init(&predbar, 1);
+    spec_ok = 1u;
     floe_ptx::fence_barrier_init();
     pdl_launch_dependents();
   }
@@ -506,7 +534,14 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   const uint32_t rpi = a.mix_f16 ? 2u : 1u;  // mixing rows per stage
   const uint32_t r_lo = floe_k::seg_begin(DH, b, G), r_hi = floe_k::seg_begin(DH, b + 1, G);
   const uint32_t nA = a.has_mixing ? (r_hi - r_lo + rpi - 1) / rpi : 0u;
-  const uint32_t uB = nA, uC = nA + nB;
+  const uint32_t uB = nA;
+  // Speculative K1: with a predicted routing (router_pred * h, known long
+  // before the mixing GEMV ends) the producer streams the first S K1 tiles
+  // of the predicted experts right behind the mixing rows, so the ring is
+  // full when the exact routing lands.  A misprediction costs S wasted
+  // stages: they are consumed unread and every tile is streamed again.
+  const bool spec = a.has_mixing && a.router_pred != nullptr;
+  const uint32_t S = spec ? min(nB, a.ns) : 0u;
 
   if (producer) {
     // =================== producer warp ===================
@@ -533,15 +568,26 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
         floe_ptx::bulk_g2s(hs, a.h, 4u * DH, &hbar);
       }
     }
+    if (spec && lane == 0) {
+      floe_ptx::mbar_wait(&predbar, 0, 6u << 28);
+      for (uint32_t j = 0; j < S; ++j) {  // waits on phase-A releases only
+        const TileRef tr = tile_ref(tile_lo + j, tps, a.di);
+        wait_empty(uB + j);
+        issue(uB + j, ptiles_s[tr.slot] + (size_t)tr.t * TILE_B, TILE_B);
+      }
+    }
     __syncwarp();
     abar();  // ALL#1: routing known
     mark(a, 16);
-    if (lane == 0)
-      for (uint32_t j = 0; j < nB; ++j) {
+    if (lane == 0) {
+      const bool ok = spec_ok != 0u;
+      const uint32_t shift = ok ? 0u : S;  // ring uses taken by discarded stages
+      for (uint32_t j = ok ? S : 0u; j < nB; ++j) {
         const TileRef tr = tile_ref(tile_lo + j, tps, a.di);
-        wait_empty(uB + j);
-        issue(uB + j, tiles_s[tr.slot] + (size_t)tr.t * TILE_B, TILE_B);
+        wait_empty(uB + shift + j);
+        issue(uB + shift + j, tiles_s[tr.slot] + (size_t)tr.t * TILE_B, TILE_B);
       }
+    }
     __syncwarp();
     abar();  // ALL#2: K1 done, own list in smem
     if (a.k1_only) {
@@ -625,6 +671,43 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   // ============================ phase A: mixing ============================
   if (a.has_mixing) {
     floe_ptx::mbar_wait(&hbar, 0, 3u << 28);
+    if (spec) {
+      // predicted logits router_pred * h (one warp per expert)
+      for (uint32_t e = warp; e < a.n_experts; e += kConsumerWarps) {
+        const float4 *rp = reinterpret_cast<const float4 *>(a.router_pred + (size_t)e * DH);
+        float p0 = 0.0f, p1 = 0.0f;
+#pragma unroll 8
+        for (uint32_t k = lane; k < DH / 4; k += 32) {
+          const float4 w = __ldg(rp + k);
+          const float4 hv = *reinterpret_cast<const float4 *>(hs + 4 * k);
+          p0 = fmaf(w.x, hv.x, p0);
+          p1 = fmaf(w.y, hv.y, p1);
+          p0 = fmaf(w.z, hv.z, p0);
+          p1 = fmaf(w.w, hv.w, p1);
+        }
+        float pe = p0 + p1;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) pe += __shfl_xor_sync(0xffffffffu, pe, o);
+        if (lane == 0) plog[e] = pe;
+      }
+      cbar();
+      if (warp == 1) {
+        __syncwarp();
+        float lg = lane < a.n_experts ? plog[lane] : 0.0f;
+        if (a.debug & 8u) lg = -lg;  // test hook: force a misprediction
+        const uint32_t taken = warp_topk(lg, lane, a.n_experts, a.top_k);
+        if ((taken >> lane) & 1u) {
+          const uint32_t i = __popc(taken & ((1u << lane) - 1));
+          psel_s[i] = lane;
+          ptiles_s[i] = reinterpret_cast<const uint8_t *>(table_s[lane].tiles);
+        }
+        __syncwarp();
+        if (lane == 0) {
+          ptaken_s = taken;
+          floe_ptx::mbar_arrive(&predbar);
+        }
+      }
+    }
     float pl = 0.0f;  // lane e < E: this warp's partial logit e
     const uint32_t pair = warp % kPairs, sub = warp / kPairs;
     // item i (stage use i) belongs to pair i % 8; warp `sub` of the pair takes
@@ -717,16 +800,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
       // warp arg-max rounds; softmax over the selected logits (la.cpp:37-46)
       __syncwarp();  // converged: otherwise the shuffles take the BRA.DIV slow path
       const float lg = lane < a.n_experts ? logits[lane] : -__int_as_float(0x7f800000);
-      const unsigned long long mykey = floe_k::topk_key(lg, lane);  // NaN-safe total order
-      uint32_t taken = 0;
-#pragma unroll 1
-      for (uint32_t r = 0; r < a.top_k; ++r) {
-        const bool cand = lane < a.n_experts && !((taken >> lane) & 1u);
-        unsigned long long bk = cand ? mykey : 0ull;
-#pragma unroll 1
-        for (int o = 16; o >= 1; o >>= 1) bk = max(bk, __shfl_xor_sync(0xffffffffu, bk, o));
-        taken |= 1u << floe_k::topk_index(bk);
-      }
+      const uint32_t taken = warp_topk(lg, lane, a.n_experts, a.top_k);
+      if (spec && lane == 0) spec_ok = taken == ptaken_s ? 1u : 0u;  // read by all after ALL#1
       if (lane == 0 && a.phase_ns) a.phase_ns[blockIdx.x * kTraceSlots + 14] = gtime();
       // softmax over the selected logits in registers (no local-memory arrays:
       // a cold stack line costs a DRAM round trip on the routing critical path).
@@ -881,9 +956,18 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   // which thresholds and emits.
   {
     const uint32_t pair = warp % kPairs, sub = warp / kPairs;
+    // a misprediction: the S speculative stages are consumed unread (each by
+    // its owning pair) and the tiles follow at ring uses uB + S ...
+    const uint32_t skip = spec_ok ? 0u : S;
+    for (uint32_t j = (pair + kPairs - uB % kPairs) % kPairs; j < skip; j += kPairs) {
+      wait_full(uB + j);
+      __syncwarp();
+      if (lane == 0) floe_ptx::mbar_arrive_cnt(&empty[(uB + j) % ns], kPairs);
+    }
+    const uint32_t uB2 = uB + skip;
     uint32_t n = 0;  // tiles this pair has done
-    for (uint32_t j = (pair + kPairs - uB % kPairs) % kPairs; j < nB; j += kPairs, ++n) {
-      const uint32_t u = uB + j;
+    for (uint32_t j = (pair + kPairs - uB2 % kPairs) % kPairs; j < nB; j += kPairs, ++n) {
+      const uint32_t u = uB2 + j;
       const TileRef tr = tile_ref(tile_lo + j, tps, a.di);
       wait_full(u);
       if (n == 0 && warp == 0) mark(a, 7);
