@@ -668,6 +668,107 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   pdl_wait();  // from here on: workspace, inputs and outputs shared with the previous grid
   cbar();
 
+  // ---- K1 operand setup: x -> max|x| -> limbs (IMMA B fragments) + span
+  // sums.  It runs on warps 8..15 while warps 0..7 route (layer mode), so it
+  // is off the critical path between grid barrier 1 and the first K1 tile.
+  const float *xg = a.has_mixing ? a.u : a.x;
+  const bool setup_warp = warp >= kConsumerWarps / 2;
+  const uint32_t ts = t - kConsumers / 2;  // setup thread index (warps 8..15)
+  const bool act = setup_warp && ts < SPANS * 4;
+  const uint32_t span = ts >> 2, tig = ts & 3;
+  float xv[16];
+  auto setup1 = [&]() {  // load x, this warp's max|x| and finiteness
+    const float4 *x4 = reinterpret_cast<const float4 *>(xg + (act ? 64 * span + 16 * tig : 0));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float4 f = __ldcg(x4 + i);
+      xv[4 * i] = f.x;
+      xv[4 * i + 1] = f.y;
+      xv[4 * i + 2] = f.z;
+      xv[4 * i + 3] = f.w;
+    }
+    float mx = 0.0f;
+    bool fin = true;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      mx = fmaxf(mx, fabsf(xv[i]));
+      fin = fin && isfinite(xv[i]);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const bool wfin = __all_sync(0xffffffffu, fin);
+    if (lane == 0) redmax[warp] = wfin ? mx : -1.0f;
+  };
+  // global max|x| over the setup warps -> scale S = 2^(22 - e), max|x| < 2^e
+  auto x_scale = [&](bool &fin_all, float &S, float &invS) {
+    fin_all = true;
+    float mx = 0.0f;
+#pragma unroll
+    for (int w = kConsumerWarps / 2; w < kConsumerWarps; ++w) {
+      fin_all = fin_all && redmax[w] >= 0.0f;
+      mx = fmaxf(mx, redmax[w]);
+    }
+    int ex = 0;
+    frexpf(mx, &ex);  // mx < 2^ex
+    const bool scaled = mx > 0.0f && fin_all;
+    S = scaled ? __int_as_float((127 + 22 - ex) << 23) : 1.0f;
+    invS = scaled ? __int_as_float((127 - 22 + ex) << 23) : 1.0f;
+  };
+  auto setup2 = [&]() {  // limbs -> xtab (or the f32 copy), span sums -> xs
+    bool fin_all;
+    float S, invS;
+    x_scale(fin_all, S, invS);
+      if (act) {
+        if (fin_all) {
+          int X[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) X[i] = __float2int_rn(xv[i] * S);
+          const uint32_t p = span >> 1, sodd = span & 1;
+          uint4 *xt = reinterpret_cast<uint4 *>(xtab) + (p * 2 + sodd) * 32;
+          // limb bytes of the 16 elements: lb[l][i] for element i
+          uint32_t lw[3][4][2];  // [limb][m][j]: element 4b + 2m + j, byte b
+#pragma unroll
+          for (int l = 0; l < 3; ++l)
+#pragma unroll
+            for (int m = 0; m < 2; ++m)
+#pragma unroll
+              for (int j = 0; j < 2; ++j) lw[l][m][j] = 0;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int v = X[i];
+            const int l0 = ((v + 128) & 255) - 128;
+            const int r1 = (v - l0) >> 8;
+            const int l1 = ((r1 + 128) & 255) - 128;
+            const int l2 = (r1 - l1) >> 8;
+            const int bb = i >> 2, m = (i >> 1) & 1, j = i & 1;
+            lw[0][m][j] |= (uint32_t)(l0 & 255) << (8 * bb);
+            lw[1][m][j] |= (uint32_t)(l1 & 255) << (8 * bb);
+            lw[2][m][j] |= (uint32_t)(l2 & 255) << (8 * bb);
+          }
+          // column n -> (class, limb): 0 (x1,L0) 1 (x1,L1) 2 (x4,L0) 3 (x4,L1)
+          // 4 (x1,L2) 6 (x4,L2); 5, 7 zero.  Class x1 rides in b0 (j = 0, the
+          // even elements), class x4 in b1 (j = 1, the odd elements).
+#pragma unroll
+          for (int n = 0; n < 8; ++n) {
+            const int lim = n == 0 || n == 2 ? 0 : (n == 1 || n == 3 ? 1 : 2);
+            const bool c1 = n == 0 || n == 1 || n == 4, c4 = n == 2 || n == 3 || n == 6;
+            xt[4 * n + tig] = make_uint4(c1 ? lw[lim][0][0] : 0u, c4 ? lw[lim][0][1] : 0u,
+                                         c1 ? lw[lim][1][0] : 0u, c4 ? lw[lim][1][1] : 0u);
+          }
+        } else {
+          float *xf = hs + 64 * span + 16 * tig;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) xf[i] = xv[i];
+        }
+      }
+    float s16 = 0.0f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) s16 += xv[i];
+    s16 += __shfl_xor_sync(0xffffffffu, s16, 1);
+    s16 += __shfl_xor_sync(0xffffffffu, s16, 2);
+    if (act && tig == 0) xs[span] = s16;
+  };
+
   // ============================ phase A: mixing ============================
   if (a.has_mixing) {
     floe_ptx::mbar_wait(&hbar, 0, 3u << 28);
@@ -777,7 +878,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
     cbar();
     mark(a, 6);
     // route (model.cpp:83-93): every CTA sums the partials in the same order
-    for (uint32_t e = warp; e < a.n_experts; e += kConsumerWarps) {
+    if (setup_warp) setup1();
+    else
+    for (uint32_t e = warp; e < a.n_experts; e += kConsumerWarps / 2) {
       float pv8[kMaxGrid / 32];  // all loads in flight at once
 #pragma unroll
       for (int j = 0; j < kMaxGrid / 32; ++j) {
@@ -795,13 +898,17 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
     cbar();
     mark(a, 13);              // all warps' partial sums loaded
     mark(a, 65);              // (diagnostic: back-to-back marks)
+    if (setup_warp) setup2();
     if (warp == 1) {  // (not warp 0: it shares SMSP 0 with the producer warp)
       // top_k (la.cpp:48-61: ties to the lower index, output ascending) as k
       // warp arg-max rounds; softmax over the selected logits (la.cpp:37-46)
       __syncwarp();  // converged: otherwise the shuffles take the BRA.DIV slow path
       const float lg = lane < a.n_experts ? logits[lane] : -__int_as_float(0x7f800000);
       const uint32_t taken = warp_topk(lg, lane, a.n_experts, a.top_k);
-      if (spec && lane == 0) spec_ok = taken == ptaken_s ? 1u : 0u;  // read by all after ALL#1
+      if (spec && lane == 0) {
+        spec_ok = taken == ptaken_s ? 1u : 0u;  // read by all after ALL#1
+        if (a.phase_ns) a.phase_ns[blockIdx.x * kTraceSlots + 71] = spec_ok + 1u;
+      }
       if (lane == 0 && a.phase_ns) a.phase_ns[blockIdx.x * kTraceSlots + 14] = gtime();
       // softmax over the selected logits in registers (no local-memory arrays:
       // a cold stack line costs a DRAM round trip on the routing critical path).
@@ -838,6 +945,17 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
       for (uint32_t i = t; i < DH; i += kConsumers) a.y[i] = 0.0f;  // before barrier 2
   }
   cbar();
+  // every consumer warp: the K1 epilogue multipliers of its lane
+  float mult, zx;
+  bool all_finite;
+  auto k1_multipliers = [&]() {
+    float S, invS;
+    x_scale(all_finite, S, invS);
+    const uint32_t mytig = lane & 3;
+    // column pair of this lane (see span_step): (c1L0,c1L1) (c4L0,c4L1) (c1L2,-) (c4L2,-)
+    mult = mytig == 0 ? invS : (mytig == 1 ? 0.25f * invS : (mytig == 2 ? 65536.0f * invS : 16384.0f * invS));
+    zx = mytig == 0 ? 1.0f : 0.0f;
+  };
   if (t < a.slots) {
     const ExpertDesc &d = table_s[sel_s[t]];
     rec_s[t] = d.records;
@@ -848,105 +966,15 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   }
   mark(a, 2);
   abar();  // ALL#1: the producer starts streaming K1 tiles
+  if (!a.has_mixing) {  // expert mode: the setup runs while the first tiles stream in
+    if (setup_warp) setup1();
+    cbar();
+    if (setup_warp) setup2();
+    cbar();
+  }
+  k1_multipliers();
 
   // ============================ phase B: K1 ================================
-  const float *xg = a.has_mixing ? a.u : a.x;
-  // x -> max|x| -> limbs (B fragments) + span sums
-  float mult = 0.0f, zx = 0.0f;
-  bool all_finite;
-  {
-    float xv[16];
-    const bool act = t < SPANS * 4;
-    const uint32_t span = t >> 2, tig = t & 3;
-    const float4 *x4 = reinterpret_cast<const float4 *>(xg + (act ? 64 * span + 16 * tig : 0));
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const float4 f = __ldcg(x4 + i);
-      xv[4 * i] = f.x;
-      xv[4 * i + 1] = f.y;
-      xv[4 * i + 2] = f.z;
-      xv[4 * i + 3] = f.w;
-    }
-    float mx = 0.0f;
-    bool fin = true;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      mx = fmaxf(mx, fabsf(xv[i]));
-      fin = fin && isfinite(xv[i]);
-    }
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    const bool wfin = __all_sync(0xffffffffu, fin);
-    if (lane == 0) redmax[warp] = wfin ? mx : -1.0f;
-    cbar();
-    all_finite = true;
-    mx = 0.0f;
-#pragma unroll
-    for (int w = 0; w < kConsumerWarps; ++w) {
-      all_finite = all_finite && redmax[w] >= 0.0f;
-      mx = fmaxf(mx, redmax[w]);
-    }
-    int ex = 0;
-    frexpf(mx, &ex);  // mx < 2^ex
-    const bool scaled = mx > 0.0f && all_finite;
-    const float S = scaled ? __int_as_float((127 + 22 - ex) << 23) : 1.0f;
-    const float invS = scaled ? __int_as_float((127 - 22 + ex) << 23) : 1.0f;
-    const uint32_t mytig = lane & 3;
-    // column pair of this lane (see span_step): (c1L0,c1L1) (c4L0,c4L1) (c1L2,-) (c4L2,-)
-    mult = mytig == 0 ? invS : (mytig == 1 ? 0.25f * invS : (mytig == 2 ? 65536.0f * invS : 16384.0f * invS));
-    zx = mytig == 0 ? 1.0f : 0.0f;
-    if (act) {
-      if (all_finite) {
-        int X[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) X[i] = __float2int_rn(xv[i] * S);
-        const uint32_t p = span >> 1, sodd = span & 1;
-        uint4 *xt = reinterpret_cast<uint4 *>(xtab) + (p * 2 + sodd) * 32;
-        // limb bytes of the 16 elements: lb[l][i] for element i
-        uint32_t lw[3][4][2];  // [limb][m][j]: element 4b + 2m + j, byte b
-#pragma unroll
-        for (int l = 0; l < 3; ++l)
-#pragma unroll
-          for (int m = 0; m < 2; ++m)
-#pragma unroll
-            for (int j = 0; j < 2; ++j) lw[l][m][j] = 0;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int v = X[i];
-          const int l0 = ((v + 128) & 255) - 128;
-          const int r1 = (v - l0) >> 8;
-          const int l1 = ((r1 + 128) & 255) - 128;
-          const int l2 = (r1 - l1) >> 8;
-          const int bb = i >> 2, m = (i >> 1) & 1, j = i & 1;
-          lw[0][m][j] |= (uint32_t)(l0 & 255) << (8 * bb);
-          lw[1][m][j] |= (uint32_t)(l1 & 255) << (8 * bb);
-          lw[2][m][j] |= (uint32_t)(l2 & 255) << (8 * bb);
-        }
-        // column n -> (class, limb): 0 (x1,L0) 1 (x1,L1) 2 (x4,L0) 3 (x4,L1)
-        // 4 (x1,L2) 6 (x4,L2); 5, 7 zero.  Class x1 rides in b0 (j = 0, the
-        // even elements), class x4 in b1 (j = 1, the odd elements).
-#pragma unroll
-        for (int n = 0; n < 8; ++n) {
-          const int lim = n == 0 || n == 2 ? 0 : (n == 1 || n == 3 ? 1 : 2);
-          const bool c1 = n == 0 || n == 1 || n == 4, c4 = n == 2 || n == 3 || n == 6;
-          xt[4 * n + tig] = make_uint4(c1 ? lw[lim][0][0] : 0u, c4 ? lw[lim][0][1] : 0u,
-                                       c1 ? lw[lim][1][0] : 0u, c4 ? lw[lim][1][1] : 0u);
-        }
-      } else {
-        float *xf = hs + 64 * span + 16 * tig;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) xf[i] = xv[i];
-      }
-    }
-    float s16 = 0.0f;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) s16 += xv[i];
-    s16 += __shfl_xor_sync(0xffffffffu, s16, 1);
-    s16 += __shfl_xor_sync(0xffffffffu, s16, 2);
-    if (act && tig == 0) xs[span] = s16;
-  }
-  cbar();
-
   // tile j (stage use uB + j) belongs to pair (uB + j) % 8: with ns a multiple
   // of 8, every stage is consumed by ONE pair in phases A and B, so a warp
   // never waits on a stage whose previous fill it has not consumed itself

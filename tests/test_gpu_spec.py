@@ -1,4 +1,4 @@
-"""Speculative K1 streaming in the fused layer kernel: the producer streams the
+"""Speculative K1 streaming in the fused layer kernel (opt-in, FLOE_SPEC=1): the producer streams the
 first K1 tiles of the experts predicted by router_pred * h (router_pred =
 router + router * mixing) before the exact routing exists.  The result must not
 depend on the prediction: a correct speculation, a forced misprediction
@@ -71,8 +71,8 @@ def _subprocess(tmp_path, name, env_extra):
 
 
 def test_speculation_never_changes_results(tmp_path):
-    spec = _subprocess(tmp_path, "spec", {})
-    miss = _subprocess(tmp_path, "miss", {"FLOE_DEBUG_FLAGS": "8"})
+    spec = _subprocess(tmp_path, "spec", {"FLOE_SPEC": "1"})
+    miss = _subprocess(tmp_path, "miss", {"FLOE_SPEC": "1", "FLOE_DEBUG_FLAGS": "8"})
     none = _subprocess(tmp_path, "none", {"FLOE_SPEC": "0"})
     for key in spec:
         for other in (miss, none):
@@ -83,7 +83,7 @@ def test_speculation_never_changes_results(tmp_path):
 
 
 def test_speculative_layer_matches_oracle(tmp_path):
-    spec = _subprocess(tmp_path, "spec2", {})
+    spec = _subprocess(tmp_path, "spec2", {"FLOE_SPEC": "1"})
     for si, (dh, di, E, K) in enumerate(SHAPES):
         L = _layer(dh, di, E, K)
         L.mixing = L.mixing.astype(np.float16).astype(np.float32)  # the device reads f16 mixing

@@ -91,6 +91,9 @@ def main():
             print("   slowest phase-C CTAs (cta, C done us, own, deficit, P, plan->done us):",
                   [(int(c), round(float(cdone[c]), 1), int(T[-1, c, 66]), int(T[-1, c, 67]),
                     int(T[-1, c, 68]), round(float((T[-1, c, 5] - T[-1, c, 9]) / 1e3), 1)) for c in order])
+            so = T[:, :, 71]
+            if (so > 0).any():
+                print("   speculation: ok", int((so == 2).sum()), "mispredicted", int((so == 1).sum()))
             print("   own+deficit spread:", int((T[-1, :, 66] + T[-1, :, 67]).min()), int((T[-1, :, 66] + T[-1, :, 67]).max()))
             smid = T[-1, :, 64]
             slow = d[-1] > 1.5
