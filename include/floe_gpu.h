@@ -42,6 +42,11 @@
  *     by two streams at the same time.
  *   - There is no CPU fallback: without a usable sm_100 device every compute
  *     call fails with FLOE_ERR_CUDA.
+ *   - The fast path is one persistent grid (one CTA per SM) with grid-wide
+ *     barriers, launched with programmatic dependent launch so consecutive
+ *     calls overlap.  Do not run fast-path calls on two streams at the same
+ *     time (their grids would compete for SMs; a barrier watchdog traps after
+ *     4 s), or set FLOE_COOP=1 to launch cooperatively (no launch overlap).
  */
 #ifndef FLOE_GPU_H
 #define FLOE_GPU_H

@@ -411,8 +411,25 @@ int launch_v2_dh(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) 
     const char *p = std::getenv("FLOE_PDL");
     return !(p && std::strcmp(p, "0") == 0);
   }();
-  cfg.attrs = attr;
-  cfg.numAttrs = (pdl_env && !ws->profiling) ? 2 : 1;
+  // Cooperative launch guarantees the co-residency the grid barriers need,
+  // but the driver then does not overlap a launch with its predecessor (PDL
+  // is ignored: 55.3 vs 52.5 us per layer, 32.8 vs 29.3 us per expert).
+  // Without it the grid (one CTA per SM, G <= SMs, ~200 KB smem each) is
+  // still co-resident: a PDL dependent only launches once EVERY CTA of its
+  // primary has executed griddepcontrol.launch_dependents (issued at kernel
+  // start), so a fused grid never competes for SMs with its successor.  What
+  // the driver no longer rules out is another grid-barrier kernel holding SMs
+  // concurrently (two fused launches on two streams, or an MPS SM limit):
+  // there the barrier watchdog traps instead of hanging.  FLOE_COOP=1, or an
+  // MPS client with an active-thread limit, keeps the cooperative launch.
+  static const bool coop_env = [] {
+    const char *p = std::getenv("FLOE_COOP");
+    if (p) return std::strcmp(p, "0") != 0;
+    return std::getenv("CUDA_MPS_ACTIVE_THREAD_PERCENTAGE") != nullptr;
+  }();
+  const bool use_pdl = pdl_env && !ws->profiling;
+  cfg.attrs = coop_env ? attr : attr + 1;
+  cfg.numAttrs = coop_env ? (use_pdl ? 2 : 1) : (use_pdl ? 1 : 0);
   StageScope prof(ws, kStageFused, st);
   const cudaError_t e =
       cudaLaunchKernelExC(&cfg, reinterpret_cast<const void *>(V::fused<DH>), kargs);
