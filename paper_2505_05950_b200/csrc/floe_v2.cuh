@@ -282,6 +282,25 @@ __device__ __forceinline__ void grid_arrive_wait(unsigned long long *bar, uint32
   __threadfence();
 }
 
+// Split grid barrier: arrive (returns the target) ... wait.
+__device__ __forceinline__ unsigned long long grid_arrive(unsigned long long *bar, uint32_t G) {
+  __threadfence();
+  const unsigned long long old = atomicAdd(bar, 1ull);
+  return (old / G + 1) * G;
+}
+__device__ __forceinline__ void grid_wait(unsigned long long *bar, unsigned long long target,
+                                          uint32_t G) {
+  const unsigned long long t0 = gtime();
+  for (uint32_t it = 1;; ++it) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
+    if (v >= target) break;
+    if ((it & 255u) == 0 && gtime() - t0 > floe_ptx::kWatchdogNs)
+      floe_ptx::watchdog_fire("grid barrier", (uint32_t)(target / G), 0u);
+  }
+  __threadfence();
+}
+
 // Exclusive scan over the consumer threads (one value each); returns the
 // prefix, writes the total to *total.  Uses ws[kConsumerWarps] shared
 // scratch; contains two consumer barriers.
@@ -628,7 +647,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
         }
         const uint32_t bb = lo;
         const uint32_t tb = (uint32_t)(((uint64_t)T * (bb + 1)) / G - ((uint64_t)T * bb) / G);
-        const uint32_t own_bb = min(NB[bb], tb);
+        const uint32_t own_bb = max(min(NB[bb], nsC), min(NB[bb], tb));
         const uint32_t first_tile = (uint32_t)(((uint64_t)NT * bb) / G);
         const TileRef tr = tile_ref(first_tile, tps, a.di);
         const uint32_t pos = tr.f0 + own_bb + (pi - SUp[bb]);
@@ -1067,80 +1086,13 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   for (uint32_t s = t; s < a.slots; s += kConsumers) a.seg_count[s * G + b] = slot_cnt[s];
   cbar();
   mark(a, 8);
-  if (t == 0) grid_arrive_wait(a.bar, G);
-  cbar();
-  mark(a, 4);
-
-  // ------------------------------ the plan ---------------------------------
-  // n_bb per CTA; targets t_bb = T(bb+1)/G - T bb/G; own_bb = min(n_bb, t_bb);
-  // surplus entries own_bb..n_bb-1 of every CTA form the pool, handed out to
-  // deficits t_bb - own_bb in CTA order.
-  uint32_t nb_t = 0;
-  if (t < G)
-    for (uint32_t s = 0; s < a.slots; ++s) nb_t += __ldcg(&a.seg_count[s * G + t]);
-  uint32_t T;
-  const uint32_t npre = cscan(nb_t, ws8, &T);
-  (void)npre;
-  uint32_t sur = 0, def = 0;
-  if (t < G) {
-    NB[t] = nb_t;
-    const uint32_t tb = (uint32_t)(((uint64_t)T * (t + 1)) / G - ((uint64_t)T * t) / G);
-    const uint32_t own = min(nb_t, tb);
-    sur = nb_t - own;
-    def = tb - own;
-  }
-  uint32_t SUT, DT;
-  const uint32_t su_pre = cscan(sur, ws8, &SUT);
-  const uint32_t d_pre = cscan(def, ws8, &DT);
-  if (t < G) SUp[t] = su_pre;
-  if (t == 0) SUp[G] = SUT;
-  if (t == b) {
-    pv[0] = T;
-    pv[1] = nb_t - sur;  // own_b
-    pv[2] = def;         // d_b
-    pv[3] = d_pre;       // D_b
-  }
-  if (b == 0) {
-    if (t == 0 && a.stats) {
-      atomicAdd(&a.stats[0], 1ull);
-      atomicAdd(&a.stats[1], (unsigned long long)T);
-    }
-    if ((a.n_kept_out || a.place_acc) && warp < a.slots) {
-      uint32_t n = 0;
-      for (uint32_t bb = lane; bb < G; bb += 32) n += __ldcg(&a.seg_count[warp * G + bb]);
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
-      if (lane == 0 && a.n_kept_out) a.n_kept_out[warp] = n;
-      if (lane == 0 && a.place_acc)  // where this slot's kept records are read from
-        atomicAdd(&a.place_acc[table_s[sel_s[warp]].host_records ? 1 : 0],
-                  (unsigned long long)n);
-    }
-  }
-  if (a.kept_out && warp < a.slots) {
-    // own entries of slot `warp` -> kept_out[slot][prefix over lower CTAs + j]
-    uint32_t base = 0;
-    for (uint32_t bb = lane; bb < b; bb += 32) base += __ldcg(&a.seg_count[warp * G + bb]);
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) base += __shfl_xor_sync(0xffffffffu, base, o);
-    uint32_t k = 0;
-    for (uint32_t j = 0; j < nB; ++j) {
-      const TileRef tr = tile_ref(tile_lo + j, tps, a.di);
-      const uint32_t cnt = tile_cnt[j];
-      if (tr.slot == warp) {
-        if (lane < cnt) a.kept_out[(size_t)warp * a.di + base + k + lane] = emit_f[kTileCh * j + lane] - warp * a.di;
-        k += cnt;
-      }
-    }
-  }
-  cbar();
-  mark(a, 9);
-  abar();  // ALL#3: the producer streams the rest
-  if (a.k1_only) return;
+  unsigned long long bar_target = 0;
+  if (t == 0) bar_target = grid_arrive(a.bar, G);
 
   // ============================ phase C: K2 ================================
-  const uint32_t own_b = pv[1], d_b = pv[2], P = pv[5];
-  const uint32_t E0 = max(P, own_b);
-  const uint32_t n_items = E0 + d_b;
+  // Ring items: the first P own records (prefetched before the barrier and
+  // owned whatever the plan says), then the rest of the own share, then pool
+  // records.  The first P are processed while the grid barrier completes.
   // Two groups of 8 warps take alternate records (group g: items g, g+2, ...)
   // so each record costs the bookkeeping of 8 warps, not 16; thread gt of a
   // group owns elements [EPT2 gt, EPT2 gt + EPT2) of both record halves.
@@ -1159,10 +1111,11 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
 #pragma unroll
     for (int i = 0; i < EPT2 / 2; ++i) y2[i] = make_float2(0.0f, 0.0f);
   }
-  const uint32_t n_mine = n_items > grp ? (n_items - grp + 1) / 2 : 0u;
+  const uint32_t P = a.k1_only ? 0u : min(pv[4], nsC);
   uint32_t stg = grp % nsC, ph = 0;  // ring position of item k = grp + 2i (no divisions)
   uint32_t batch = 0, processed = 0;
-  for (uint32_t i0 = 0; i0 < n_mine; i0 += kR, ++batch) {
+  auto run_items = [&](uint32_t i_begin, uint32_t i_end) {
+  for (uint32_t i0 = i_begin; i0 < i_end; i0 += kR, ++batch) {
     if (batch < 6 && grp == 0) mark(a, 24 + 4 * (int)batch);  // batch start
     Vec dv[kR][2];
     float gp[kR], sc[kR];
@@ -1173,8 +1126,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
       sc[r] = 0.0f;
       dv[r][0] = dv[r][1] = Vec{};
       const uint32_t k = grp + 2 * (i0 + r);
-      proc[r] = i0 + r < n_mine && (k >= E0 || k < own_b);
-      if (i0 + r < n_mine) {
+      proc[r] = i0 + r < i_end;
+      if (proc[r]) {
         floe_ptx::mbar_wait(&fullC[stg], ph, (4u << 28) | k);
         if (k == 0) mark(a, 10);
         sc[r] = stage_scale[stg];
@@ -1255,6 +1208,86 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
     }
     if (batch < 6 && grp == 0) mark(a, 27 + 4 * (int)batch);  // batch done
   }
+  };
+  const uint32_t n1 = P > grp ? (P - grp + 1) / 2 : 0u;  // this group's items < P
+  run_items(0, n1);
+  mark(a, 21);
+  if (t == 0) grid_wait(a.bar, bar_target, G);
+  cbar();
+  mark(a, 4);
+  // ------------------------------ the plan ---------------------------------
+  // n_bb per CTA; targets t_bb = T(bb+1)/G - T bb/G; every CTA keeps its
+  // first min(n_bb, nsC) entries (already streamed and processed) and up to
+  // its target: own_bb = max(min(n_bb, nsC), min(n_bb, t_bb)); the surplus
+  // entries own_bb..n_bb-1 of every CTA form the pool, handed out to the
+  // deficits t_bb - own_bb in CTA order until it runs out.
+  uint32_t nb_t = 0;
+  if (t < G)
+    for (uint32_t s = 0; s < a.slots; ++s) nb_t += __ldcg(&a.seg_count[s * G + t]);
+  uint32_t T;
+  const uint32_t npre = cscan(nb_t, ws8, &T);
+  (void)npre;
+  uint32_t sur = 0, def = 0;
+  if (t < G) {
+    NB[t] = nb_t;
+    const uint32_t tb = (uint32_t)(((uint64_t)T * (t + 1)) / G - ((uint64_t)T * t) / G);
+    const uint32_t own = max(min(nb_t, nsC), min(nb_t, tb));
+    sur = nb_t - own;
+    def = tb > own ? tb - own : 0u;
+  }
+  uint32_t SUT, DT;
+  const uint32_t su_pre = cscan(sur, ws8, &SUT);
+  const uint32_t d_pre = cscan(def, ws8, &DT);
+  if (t < G) SUp[t] = su_pre;
+  if (t == 0) SUp[G] = SUT;
+  if (t == b) {
+    pv[0] = T;
+    pv[1] = nb_t - sur;                                // own_b
+    pv[2] = d_pre < SUT ? min(def, SUT - d_pre) : 0u;  // d_b (the pool may run out)
+    pv[3] = d_pre;                                     // D_b
+  }
+  if (b == 0) {
+    if (t == 0 && a.stats) {
+      atomicAdd(&a.stats[0], 1ull);
+      atomicAdd(&a.stats[1], (unsigned long long)T);
+    }
+    if ((a.n_kept_out || a.place_acc) && warp < a.slots) {
+      uint32_t n = 0;
+      for (uint32_t bb = lane; bb < G; bb += 32) n += __ldcg(&a.seg_count[warp * G + bb]);
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+      if (lane == 0 && a.n_kept_out) a.n_kept_out[warp] = n;
+      if (lane == 0 && a.place_acc)  // where this slot's kept records are read from
+        atomicAdd(&a.place_acc[table_s[sel_s[warp]].host_records ? 1 : 0],
+                  (unsigned long long)n);
+    }
+  }
+  if (a.kept_out && warp < a.slots) {
+    // own entries of slot `warp` -> kept_out[slot][prefix over lower CTAs + j]
+    uint32_t base = 0;
+    for (uint32_t bb = lane; bb < b; bb += 32) base += __ldcg(&a.seg_count[warp * G + bb]);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) base += __shfl_xor_sync(0xffffffffu, base, o);
+    uint32_t k = 0;
+    for (uint32_t j = 0; j < nB; ++j) {
+      const TileRef tr = tile_ref(tile_lo + j, tps, a.di);
+      const uint32_t cnt = tile_cnt[j];
+      if (tr.slot == warp) {
+        if (lane < cnt) a.kept_out[(size_t)warp * a.di + base + k + lane] = emit_f[kTileCh * j + lane] - warp * a.di;
+        k += cnt;
+      }
+    }
+  }
+  cbar();
+  mark(a, 9);
+  abar();  // ALL#3: the producer streams the rest
+  if (a.k1_only) return;
+
+  // ---- phase C, segment 2: the rest of the own share, then pool records
+  const uint32_t own_b = pv[1], d_b = pv[2];
+  const uint32_t n_items = own_b + d_b;  // own_b >= P by construction of the plan
+  const uint32_t n_mine = n_items > grp ? (n_items - grp + 1) / 2 : 0u;
+  run_items(n1, n_mine);
   mark(a, 5);
   if (processed > 0) {
     float *yo = a.y + EPT2 * gt;
