@@ -181,6 +181,14 @@ int floe_gpu_qgemv_channels(const floe_gpu_expert *e, floe_gpu_workspace *ws,
                             const float *x_dev, float *v_dev,
                             floe_stream_t stream);
 
+/* Batched up projection (SURVEY config 4): v_dev[t][c] = qgemv_channels(up_q,
+ * d_hidden, x_dev[t]) for n_tokens <= 64 tokens, x_dev [n_tokens][d_hidden],
+ * v_dev [n_tokens][d_intermediate].  One pass over the codes on the tcgen05
+ * tensor cores (exact integer group sums); fast-layout experts only
+ * (FLOE_ERR_UNSUPPORTED otherwise).  A token with a non-finite x gets NaN. */
+int floe_gpu_qgemv_channels_batched(const floe_gpu_expert *e, const float *x_dev,
+                                    uint32_t n_tokens, float *v_dev, floe_stream_t stream);
+
 /* out = dequantize(up_q) in f32, bit-exact with floe::dequantize. */
 int floe_gpu_dequantize_up(const floe_gpu_expert *e, float *out_dev,
                            floe_stream_t stream);

@@ -88,6 +88,7 @@ _SIGS = {
     "floe_gpu_expert_forward_sparse": (ct.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "floe_gpu_expert_forward_sparse_host": (ct.c_int, [_P, _P, _P, _P, _P, _P, _P]),
     "floe_gpu_qgemv_channels": (ct.c_int, [_P, _P, _P, _P, _P]),
+    "floe_gpu_qgemv_channels_batched": (ct.c_int, [_P, _P, ct.c_uint32, _P, _P]),
     "floe_gpu_dequantize_up": (ct.c_int, [_P, _P, _P]),
     "floe_gpu_predict_mask": (ct.c_int, [_P, _P, _P, _F, _P, _P, _P, _P]),
     "floe_gpu_layer_create": (ct.c_int, [ct.POINTER(LayerHostView), ct.POINTER(_P)]),
@@ -345,6 +346,19 @@ def qgemv_channels(e: GpuExpert, x, ws: Workspace, stream=None):
     v = torch.empty(e.d_intermediate, dtype=torch.float32, device=x.device)
     _check(lib().floe_gpu_qgemv_channels(e.handle, ws.handle, x.data_ptr(), v.data_ptr(),
                                          _stream(stream)))
+    return v
+
+
+def qgemv_channels_batched(e: GpuExpert, x, stream=None):
+    """qgemv_channels for a batch of tokens: x [B, d_hidden] -> v [B, d_intermediate]
+    (tcgen05 tensor cores, exact integer group sums; B <= 64)."""
+    torch = _torch()
+    if x.dim() != 2 or x.shape[1] != e.d_hidden or x.dtype != torch.float32 or not x.is_cuda:
+        raise FloeError("qgemv_channels_batched: x must be a cuda float32 [B, d_hidden]")
+    x = x.contiguous()
+    v = torch.empty((x.shape[0], e.d_intermediate), dtype=torch.float32, device=x.device)
+    _check(lib().floe_gpu_qgemv_channels_batched(e.handle, x.data_ptr(), x.shape[0], v.data_ptr(),
+                                                 _stream(stream)))
     return v
 
 

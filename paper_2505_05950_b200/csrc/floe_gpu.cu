@@ -20,6 +20,7 @@
 #include "../../include/floe_gpu.h"
 #include "floe_gen.cuh"
 #include "floe_v2.cuh"
+#include "floe_tc.cuh"
 
 using floe_k::ExpertDesc;
 using floe_k::K1Args;
@@ -969,6 +970,58 @@ int floe_gpu_qgemv_channels(const floe_gpu_expert *e, floe_gpu_workspace *ws,
   K1Launch k1{e->dev_desc, nullptr, 1, e->dh, e->di, e->bits, e->g, 1,
               __builtin_inff(), x, v_out, nullptr, nullptr};
   return launch_k1(k1, ws, S(stream));
+}
+
+}  // extern "C"
+namespace {
+template <int DH>
+int launch_batched(const floe_tc::BatchedArgs &a, cudaStream_t st) {
+  const floe_tc::BatchedSmem L = floe_tc::batched_smem(DH, a.B);
+  if (int rc = set_smem(floe_tc::k1_batched<DH>, L.total)) return rc;
+  const uint32_t blocks = (a.di + floe_tc::kRows - 1) / floe_tc::kRows;
+  floe_tc::k1_batched<DH><<<blocks, floe_tc::kThreads, L.total, st>>>(a);
+  CK_LAUNCH();
+  return FLOE_OK;
+}
+}  // namespace
+extern "C" {
+
+int floe_gpu_qgemv_channels_batched(const floe_gpu_expert *e, const float *x, uint32_t n_tokens,
+                                    float *v_out, floe_stream_t stream) {
+  if (!e || !x || !v_out) return fail(FLOE_ERR_INVALID, "qgemv_channels_batched: null argument");
+  if (n_tokens == 0) return FLOE_OK;
+  if (n_tokens > (uint32_t)floe_tc::kMaxTokens)
+    return fail(FLOE_ERR_INVALID, "qgemv_channels_batched: at most %d tokens", floe_tc::kMaxTokens);
+  if (!e->fast)
+    return fail(FLOE_ERR_UNSUPPORTED,
+                "qgemv_channels_batched: needs the tile layout (bits 2, d_hidden 2048/4096, g %% 64 == 0)");
+  if (int rc = require_device("qgemv_channels_batched")) return rc;
+  cudaStream_t st = S(stream);
+  const uint32_t Bp = floe_tc::padded_tokens(n_tokens), spans = e->dh / 64;
+  const size_t xl_bytes = (size_t)spans * floe_tc::xl_span_bytes(n_tokens);
+  const size_t xs_bytes = 4ull * spans * Bp;
+  uint8_t *scratch = nullptr;  // S | invS | xs | xl (stream-ordered)
+  const size_t o_inv = 256, o_xs = 512, o_xl = (o_xs + xs_bytes + 1023) & ~size_t(1023);
+  CK(cudaMallocAsync(reinterpret_cast<void **>(&scratch), o_xl + xl_bytes, st));
+  float *Sv = reinterpret_cast<float *>(scratch), *invS = reinterpret_cast<float *>(scratch + o_inv);
+  float *xs = reinterpret_cast<float *>(scratch + o_xs);
+  uint8_t *xl = scratch + o_xl;
+  floe_tc::token_scale<<<n_tokens, 256, 0, st>>>(x, e->dh, invS, Sv);
+  CK_LAUNCH();
+  floe_tc::token_limbs<<<spans, 256, 0, st>>>(x, e->dh, n_tokens, Sv, xl, xs);
+  CK_LAUNCH();
+  floe_tc::BatchedArgs a{};
+  a.tiles = e->host_desc.tiles;
+  a.dh = e->dh;
+  a.di = e->di;
+  a.B = n_tokens;
+  a.xl = xl;
+  a.xs = xs;
+  a.invS = invS;
+  a.v = v_out;
+  const int rc = e->dh == 4096 ? launch_batched<4096>(a, st) : launch_batched<2048>(a, st);
+  CK(cudaFreeAsync(scratch, st));
+  return rc;
 }
 
 int floe_gpu_dequantize_up(const floe_gpu_expert *e, float *out, floe_stream_t stream) {
