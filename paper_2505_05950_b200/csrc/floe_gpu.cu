@@ -979,7 +979,7 @@ int launch_batched(const floe_tc::BatchedArgs &a, cudaStream_t st) {
   const floe_tc::BatchedSmem L = floe_tc::batched_smem(DH, a.B);
   if (int rc = set_smem(floe_tc::k1_batched<DH>, L.total)) return rc;
   const uint32_t blocks = (a.di + floe_tc::kRows - 1) / floe_tc::kRows;
-  floe_tc::k1_batched<DH><<<blocks, floe_tc::kThreads, L.total, st>>>(a);
+  floe_tc::k1_batched<DH><<<blocks, floe_tc::kBThreads, L.total, st>>>(a);
   CK_LAUNCH();
   return FLOE_OK;
 }
@@ -1000,6 +1000,16 @@ int floe_gpu_qgemv_channels_batched(const floe_gpu_expert *e, const float *x, ui
   const uint32_t Bp = floe_tc::padded_tokens(n_tokens), spans = e->dh / 64;
   const size_t xl_bytes = (size_t)spans * floe_tc::xl_span_bytes(n_tokens);
   const size_t xs_bytes = 4ull * spans * Bp;
+  static const bool pool_ready = [] {  // keep freed stream-ordered memory cached
+    cudaMemPool_t pool;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    return true;
+  }();
+  (void)pool_ready;
   uint8_t *scratch = nullptr;  // S | invS | xs | xl (stream-ordered)
   const size_t o_inv = 256, o_xs = 512, o_xl = (o_xs + xs_bytes + 1023) & ~size_t(1023);
   CK(cudaMallocAsync(reinterpret_cast<void **>(&scratch), o_xl + xl_bytes, st));
@@ -1019,8 +1029,26 @@ int floe_gpu_qgemv_channels_batched(const floe_gpu_expert *e, const float *x, ui
   a.xs = xs;
   a.invS = invS;
   a.v = v_out;
+  static const bool tc_trace = std::getenv("FLOE_TC_TRACE") != nullptr;
+  const uint32_t blocks = (e->di + floe_tc::kRows - 1) / floe_tc::kRows;
+  if (tc_trace) CK(cudaMalloc(&a.trace, 8ull * 32 * blocks));
+  if (tc_trace) CK(cudaMemset(a.trace, 0, 8ull * 32 * blocks));
   const int rc = e->dh == 4096 ? launch_batched<4096>(a, st) : launch_batched<2048>(a, st);
   CK(cudaFreeAsync(scratch, st));
+  if (tc_trace && rc == FLOE_OK) {  // diagnostics: per-CTA marks relative to the first start
+    std::vector<unsigned long long> h(32ull * blocks);
+    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpy(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost));
+    unsigned long long t0 = ~0ull;
+    for (uint32_t b = 0; b < blocks; ++b) t0 = std::min(t0, h[32ull * b]);
+    for (uint32_t b : {0u, blocks / 2, blocks - 1}) {
+      std::fprintf(stderr, "[tc] B=%u cta %u:", n_tokens, b);
+      for (int k = 0; k < 32; ++k)
+        if (h[32ull * b + k]) std::fprintf(stderr, " %d:%.2f", k, (h[32ull * b + k] - t0) / 1e3);
+      std::fprintf(stderr, "\n");
+    }
+    cudaFree(a.trace);
+  }
   return rc;
 }
 

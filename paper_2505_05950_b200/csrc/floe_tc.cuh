@@ -23,10 +23,11 @@
 //       m = 0..3, so K position 4m + b of a 16-byte chunk holds element
 //       16*chunk + 4b + m -- a fixed permutation of K that B follows too;
 //   B = limbs, row n = l * Bp + t (limb l of token t, Bp = B rounded up to 16).
-// One CTA per 128-channel block; a 3-stage ring of span pairs (codes, meta,
-// limbs) arrives by bulk copies; thread 0 issues copies and MMAs; all 128
-// threads unpack, and drain TMEM (thread = channel row) once per batch of
-// spans that fills the 512 TMEM columns.
+// One CTA per 128-channel block.  A producer warp streams span pairs by bulk
+// copies (an 8-deep ring of codes+meta, 2-4 operand stages of limbs) and
+// issues the MMAs; 16 consumer warps unpack codes into the A operand and drain
+// TMEM (thread = channel row, 16 tokens) once per batch of spans that fills
+// the 512 TMEM columns.
 #pragma once
 
 #include <cuda_fp16.h>
@@ -36,9 +37,7 @@
 
 namespace floe_tc {
 
-constexpr int kThreads = 128;
 constexpr int kRows = 128;      // channels per CTA (MMA M)
-constexpr int kStages = 3;      // ring of span pairs
 constexpr int kMaxTokens = 64;
 
 __host__ __device__ constexpr uint32_t padded_tokens(uint32_t B) { return (B + 15u) / 16u * 16u; }
@@ -61,10 +60,11 @@ __global__ void __launch_bounds__(256) token_scale(const float *__restrict__ x, 
   __shared__ int bad[8];
   float mx = 0.0f;
   int nf = 0;
-  for (uint32_t k = threadIdx.x; k < dh; k += blockDim.x) {
-    const float v = x[(size_t)t * dh + k];
-    mx = fmaxf(mx, fabsf(v));
-    nf |= !isfinite(v);
+  const float4 *x4 = reinterpret_cast<const float4 *>(x + (size_t)t * dh);
+  for (uint32_t k = threadIdx.x; k < dh / 4u; k += blockDim.x) {
+    const float4 v = x4[k];
+    mx = fmaxf(fmaxf(mx, fmaxf(fabsf(v.x), fabsf(v.y))), fmaxf(fabsf(v.z), fabsf(v.w)));
+    nf |= !isfinite(v.x) | !isfinite(v.y) | !isfinite(v.z) | !isfinite(v.w);
   }
   for (int o = 16; o >= 1; o >>= 1) {
     mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -118,12 +118,18 @@ __global__ void __launch_bounds__(256) token_limbs(const float *__restrict__ x, 
     out[kmaj_off(1u * Bp + t, kp)] = (uint8_t)(l1 & 255);
     out[kmaj_off(2u * Bp + t, kp)] = (uint8_t)(l2 & 255);
   }
-  // span sums in f32, ascending (the zero term: zero * sum_k x_k)
-  for (uint32_t t = threadIdx.x; t < Bp; t += blockDim.x) {
+  // span sums in f32 (the zero term: zero * sum_k x_k): one warp per token,
+  // two elements per lane, butterfly reduction
+  for (uint32_t t = threadIdx.x >> 5; t < Bp; t += blockDim.x >> 5) {
+    const uint32_t ln = threadIdx.x & 31u;
     float s = 0.0f;
-    if (t < B)
-      for (uint32_t e = 0; e < 64u; ++e) s += x[(size_t)t * dh + 64u * span + e];
-    xs[(size_t)span * Bp + t] = s;
+    if (t < B) {
+      const float2 v2 = *reinterpret_cast<const float2 *>(x + (size_t)t * dh + 64u * span + 2u * ln);
+      s = v2.x + v2.y;
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (ln == 0) xs[(size_t)span * Bp + t] = s;
   }
 }
 
@@ -135,48 +141,64 @@ struct BatchedArgs {
   const float *xs;        // [spans][Bp]
   const float *invS;      // [Bp]
   float *v;               // [B][di]
+  unsigned long long *trace;  // nullable [blocks][32] %globaltimer marks (diagnostics)
 };
+__device__ __forceinline__ void tmark(const BatchedArgs &a, int k) {
+  if (a.trace) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    a.trace[blockIdx.x * 32u + (uint32_t)k] = g;
+  }
+}
+
+// Roles: warps 0..15 consume (unpack, epilogue), warp 16 lane 0 produces
+// (bulk copies) and issues the MMAs.  Epilogue: warp w reads TMEM lane
+// quadrant w % 4 (its 32 channel rows) for token chunk w / 4 (16 tokens).
+constexpr int kConsumerWarps = 16;
+constexpr int kBThreads = 32 * (kConsumerWarps + 1);
+constexpr int kPS = 4;   // packed ring stages
+constexpr int kPPS = 4;  // span pairs per packed stage: per tile one 2 KB codes + one 512 B meta copy
 
 struct BatchedSmem {
-  uint32_t stage_bytes, codes, meta, xlb, a, meta_batch, xs, vacc, total;
+  uint32_t nos, pstage, ostage, p, o, meta_batch, xs, total;
 };
 __host__ __device__ inline BatchedSmem batched_smem(uint32_t dh, uint32_t B) {
   BatchedSmem L;
   const uint32_t Bp = padded_tokens(B), N = 3u * Bp;
   const uint32_t SB = (512u / N) & ~1u;  // spans per TMEM batch (even)
-  // per stage: codes 8 tiles x 512 B, meta 8 x 128 B, limbs 2 spans, A 2 x 8 KB
-  L.codes = 0;
-  L.meta = 4096;
-  L.xlb = 4096 + 1024;
-  L.a = (L.xlb + 2u * N * 64u + 1023u) & ~1023u;
-  L.stage_bytes = L.a + 2u * 8192u;
-  uint32_t o = kStages * L.stage_bytes;
-  L.meta_batch = o;  o += SB * kRows * 4u;
-  L.xs = o;          o += (dh / 64u) * Bp * 4u;
-  L.vacc = o;        o += Bp * kRows * 4u;
+  L.nos = N <= 96u ? 4u : 2u;  // operand stages (A + limbs of a pair)
+  L.pstage = kPPS * 5120u;
+  L.ostage = (16384u + 2u * N * 64u + 1023u) & ~1023u;
+  uint32_t o = 0;
+  L.o = o;            o += L.nos * L.ostage;  // 1024-aligned operand stages first
+  L.p = o;            o += kPS * L.pstage;
+  L.meta_batch = o;   o += SB * 128u * 4u;
+  L.xs = o;           o += (dh / 64u) * Bp * 4u;
   L.total = o;
-  (void)dh;
   return L;
 }
 
 template <int DH>
-__global__ void __launch_bounds__(kThreads, 1) k1_batched(const BatchedArgs a) {
-  constexpr uint32_t SPANS = DH / 64, PAIRS = DH / 128;
+__global__ void __launch_bounds__(kBThreads, 1) k1_batched(const BatchedArgs a) {
+  constexpr uint32_t PAIRS = DH / 128;
   constexpr uint32_t TILE_W = 5u * DH / 4u;  // u32 per tile
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[kStages], mdone[kStages];
+  __shared__ __align__(8) uint64_t pfull[kPS], pempty[kPS];
+  __shared__ __align__(8) uint64_t xfull[4], aready[4], mdone[4], tfree;
   __shared__ uint32_t tmem_base;
   __shared__ float invS_s[kMaxTokens];
   const uint32_t t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  if (t == 0) tmark(a, 0);
   const uint32_t B = a.B, Bp = padded_tokens(B), N = 3u * Bp;
   const uint32_t SB = (512u / N) & ~1u;
   const BatchedSmem L = batched_smem(DH, B);
-  const uint32_t blk = blockIdx.x, tiles_total = (a.di + 15u) / 16u;
-  const uint32_t tile0 = blk * 8u;
-  auto stage_ptr = [&](uint32_t s) { return smem + s * L.stage_bytes; };
+  const uint32_t NOS = L.nos;
+  const uint32_t blk = blockIdx.x, tiles_total = (a.di + 15u) / 16u, tile0 = blk * 8u;
+  const uint32_t ntiles = tile0 < tiles_total ? min(8u, tiles_total - tile0) : 0u;
+  auto pst = [&](uint32_t s) { return smem + L.p + s * L.pstage; };
+  auto ost = [&](uint32_t o) { return smem + L.o + o * L.ostage; };
   uint32_t *meta_batch = reinterpret_cast<uint32_t *>(smem + L.meta_batch);
   float *xs_s = reinterpret_cast<float *>(smem + L.xs);
-  float *vacc = reinterpret_cast<float *>(smem + L.vacc);
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
@@ -184,147 +206,243 @@ __global__ void __launch_bounds__(kThreads, 1) k1_batched(const BatchedArgs a) {
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (t == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      floe_ptx::mbar_init(&full[s], 1);
-      floe_ptx::mbar_init(&mdone[s], 1);
+    for (int s = 0; s < kPS; ++s) {
+      floe_ptx::mbar_init(&pfull[s], 1);
+      floe_ptx::mbar_init(&pempty[s], kConsumerWarps);
     }
+    for (int o = 0; o < 4; ++o) {
+      floe_ptx::mbar_init(&xfull[o], 1);
+      floe_ptx::mbar_init(&aready[o], kConsumerWarps);
+      floe_ptx::mbar_init(&mdone[o], 1);
+    }
+    floe_ptx::mbar_init(&tfree, kConsumerWarps);
     floe_ptx::fence_barrier_init();
   }
-  for (uint32_t i = t; i < Bp; i += kThreads) invS_s[i] = i < B ? a.invS[i] : 0.0f;
-  for (uint32_t i = t; i < SPANS * Bp; i += kThreads) xs_s[i] = a.xs[i];
-  for (uint32_t i = t; i < Bp * kRows; i += kThreads) vacc[i] = 0.0f;
-  // tiles past the expert's end: their codes are zero in the whole ring
-  const uint32_t ntiles = tile0 < tiles_total ? min(8u, tiles_total - tile0) : 0u;
-  if (ntiles < 8u)
-    for (uint32_t s = 0; s < kStages; ++s)
-      for (uint32_t i = t; i < 5120u / 4u; i += kThreads)
-        reinterpret_cast<uint32_t *>(stage_ptr(s))[i] = 0u;
+  for (uint32_t i = t; i < Bp; i += kBThreads) invS_s[i] = i < B ? a.invS[i] : 0.0f;
+  for (uint32_t i = t; i < (DH / 64u) * Bp; i += kBThreads) xs_s[i] = a.xs[i];
+  if (ntiles < 8u)  // tiles past the expert's end: zero codes/meta in the whole ring
+    for (uint32_t i = t; i < kPS * L.pstage / 4u; i += kBThreads)
+      reinterpret_cast<uint32_t *>(smem + L.p)[i] = 0u;
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base;
+  if (t == 0) tmark(a, 1);
 
-  // producer: pair p -> stage p % kStages
-  auto issue = [&](uint32_t p) {
-    const uint32_t s = p % kStages;
-    uint8_t *st = stage_ptr(s);
-    const uint32_t xlb = 2u * N * 64u;
-    floe_ptx::mbar_arrive_expect_tx(&full[s], ntiles * (512u + 128u) + xlb);
-    for (uint32_t j = 0; j < ntiles; ++j) {
-      const uint32_t *tile = a.tiles + (size_t)(tile0 + j) * TILE_W;
-      floe_ptx::bulk_g2s(st + L.codes + 512u * j, tile + p * 128u, 512u, &full[s]);
-      floe_ptx::bulk_g2s(st + L.meta + 128u * j, tile + DH + p * 32u, 128u, &full[s]);
-    }
-    floe_ptx::bulk_g2s(st + L.xlb, a.xl + (size_t)(2u * p) * N * 64u, xlb, &full[s]);
-  };
-  if (t == 0)
-    for (uint32_t p = 0; p < min((uint32_t)kStages, PAIRS); ++p) issue(p);
-
-  // instruction descriptor: D s32, A u8, B s8, K-major both, N, M = 128
-  const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((N >> 3) << 17) | ((uint32_t)(kRows >> 4) << 24);
-  auto desc = [](uint32_t saddr) -> uint64_t {
-    return (uint64_t)((saddr >> 4) & 0x3fffu) | ((uint64_t)(128u >> 4) << 16) |
-           ((uint64_t)(512u >> 4) << 32) | ((uint64_t)1 << 46);
-  };
-
-  const uint32_t row = t;  // TMEM lane / channel row of this thread in the epilogue
-  uint32_t batch_begin = 0;  // first span of the current TMEM batch
-  for (uint32_t p = 0; p < PAIRS; ++p) {
-    const uint32_t s = p % kStages;
-    uint8_t *st = stage_ptr(s);
-    floe_ptx::mbar_wait(&full[s], (p / kStages) & 1u, (7u << 28) | p);
-    // unpack: 8 tiles x 32 lanes x 4 words -> A (2 spans x 128 rows x 64 B)
-    {
-      const uint32_t *cw = reinterpret_cast<const uint32_t *>(st + L.codes);
-      uint8_t *A = st + L.a;
-#pragma unroll 2
-      for (uint32_t i = t; i < 8u * 128u; i += kThreads) {
-        const uint32_t j = i >> 7, q = i & 127u;          // tile, word in the pair
-        const uint32_t k = q & 3u, ln = q >> 2;           // word slot, lane
-        const uint32_t r = 16u * j + (ln >> 2) + 8u * (k & 1u), sp = k >> 1, chunk = ln & 3u;
-        const uint32_t w = cw[i];
-        const uint4 o = make_uint4(w & 0x03030303u, (w >> 2) & 0x03030303u,
-                                   (w >> 4) & 0x03030303u, (w >> 6) & 0x03030303u);
-        *reinterpret_cast<uint4 *>(A + sp * 8192u + kmaj_off(r, 16u * chunk)) = o;
-      }
-      // meta of the two spans -> this TMEM batch's table [span][row]
-      const uint32_t *mw = reinterpret_cast<const uint32_t *>(st + L.meta);
-      for (uint32_t i = t; i < 8u * 32u; i += kThreads) {
-        const uint32_t j = i >> 5, q = i & 31u, k = q & 3u, g = q >> 2;
-        const uint32_t r = 16u * j + g + 8u * (k & 1u), sp = k >> 1;
-        meta_batch[(2u * p + sp - batch_begin) * kRows + r] = mw[i];
-      }
-    }
-    asm volatile("fence.proxy.async.shared::cta;");  // generic writes -> tensor-core reads
-    __syncthreads();
-    if (t == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      for (uint32_t sp = 0; sp < 2; ++sp) {
-        const uint32_t col = (2u * p + sp - batch_begin) * N;
-        const uint32_t a0 = floe_ptx::smem_u32(st + L.a + sp * 8192u);
-        const uint32_t b0 = floe_ptx::smem_u32(st + L.xlb + sp * N * 64u);
-        for (uint32_t kh = 0; kh < 2; ++kh) {  // K = 64: two K=32 instructions
-          const uint64_t da = desc(a0 + kh * 256u), db = desc(b0 + kh * 256u);
-          const uint32_t acc = kh;
-          asm volatile(
-              "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, q;\n\t}" ::"r"(tmem + col),
-              "l"(da), "l"(db), "r"(idesc), "r"(acc));
+  if (warp == kConsumerWarps) {
+    // ======================= producer / MMA issuer =======================
+    if (lane == 0) {
+      // packed stage q = span pairs kPPS*q ..: per tile the codes (kPPS x 512 B)
+      // and meta (kPPS x 128 B) of those pairs are contiguous in the tile
+      auto issue_packed = [&](uint32_t q) {
+        const uint32_t s = q % kPS, p0 = q * kPPS;
+        uint8_t *st = pst(s);
+        floe_ptx::mbar_arrive_expect_tx(&pfull[s], ntiles * kPPS * (512u + 128u));
+        for (uint32_t j = 0; j < ntiles; ++j) {
+          const uint32_t *tile = a.tiles + (size_t)(tile0 + j) * TILE_W;
+          floe_ptx::bulk_g2s(st + kPPS * 512u * j, tile + p0 * 128u, kPPS * 512u, &pfull[s]);
+          floe_ptx::bulk_g2s(st + kPPS * 4096u + kPPS * 128u * j, tile + DH + p0 * 32u,
+                             kPPS * 128u, &pfull[s]);
         }
-      }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          floe_ptx::smem_u32(&mdone[s])));
-      // refill this stage once its MMAs have read it
-      if (p + kStages < PAIRS) {
-        floe_ptx::mbar_wait(&mdone[s], (p / kStages) & 1u, (8u << 28) | p);
-        issue(p + kStages);
-      }
-    }
-    const uint32_t span_end = 2u * p + 2u;
-    if (span_end - batch_begin == SB || p + 1 == PAIRS) {
-      // drain TMEM: wait for this pair's MMAs (commit covers all earlier ones)
-      if (!(t == 0 && p + kStages < PAIRS))  // (thread 0 waited above)
-        floe_ptx::mbar_wait(&mdone[s], (p / kStages) & 1u, (9u << 28) | p);
-      asm volatile("tcgen05.fence::after_thread_sync;");
-      for (uint32_t sp = batch_begin; sp < span_end; ++sp) {
-        const uint32_t mv = meta_batch[(sp - batch_begin) * kRows + row];
-        const float scale = __half2float(__ushort_as_half((unsigned short)(mv & 0xffffu)));
-        const float zero = __half2float(__ushort_as_half((unsigned short)(mv >> 16)));
-        const uint32_t col0 = (sp - batch_begin) * N;
-        for (uint32_t tc = 0; tc < Bp; tc += 16u) {
-          uint32_t c[3][16];
-#pragma unroll
-          for (int l = 0; l < 3; ++l) {
-            const uint32_t addr = tmem + ((warp * 32u) << 16) + col0 + (uint32_t)l * Bp + tc;
+      };
+      auto issue_xl = [&](uint32_t p) {
+        const uint32_t o = p % NOS;
+        floe_ptx::mbar_arrive_expect_tx(&xfull[o], 2u * N * 64u);
+        floe_ptx::bulk_g2s(ost(o) + 16384u, a.xl + (size_t)(2u * p) * N * 64u, 2u * N * 64u,
+                           &xfull[o]);
+      };
+      constexpr uint32_t QS = PAIRS / kPPS;  // packed stages in all
+      for (uint32_t q = 0; q < min((uint32_t)kPS, QS); ++q) issue_packed(q);
+      for (uint32_t q = 0; q < min(NOS, PAIRS); ++q) issue_xl(q);
+      const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((N >> 3) << 17) |
+                             ((uint32_t)(128 >> 4) << 24);
+      auto desc = [](uint32_t saddr) -> uint64_t {
+        return (uint64_t)((saddr >> 4) & 0x3fffu) | ((uint64_t)(128u >> 4) << 16) |
+               ((uint64_t)(512u >> 4) << 32) | ((uint64_t)1 << 46);
+      };
+      uint32_t batch = 0, batch_begin = 0;
+      for (uint32_t p = 0; p < PAIRS; ++p) {
+        const uint32_t o = p % NOS;
+        if (2u * p == batch_begin + SB) {  // a new TMEM batch: wait for the epilogue
+          floe_ptx::mbar_wait(&tfree, batch & 1u, (10u << 28) | p);
+          ++batch;
+          batch_begin = 2u * p;
+        }
+        if (p == 8) tmark(a, 22);
+        floe_ptx::mbar_wait(&aready[o], (p / NOS) & 1u, (11u << 28) | p);
+        if (p == 0) tmark(a, 2);
+        if (p == 8) tmark(a, 23);
+        floe_ptx::mbar_wait(&xfull[o], (p / NOS) & 1u, (12u << 28) | p);
+        if (p == 0) tmark(a, 3);
+        if (p == 8) tmark(a, 24);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        for (uint32_t sp = 0; sp < 2; ++sp) {
+          const uint32_t col = (2u * p + sp - batch_begin) * N;
+          const uint32_t a0 = floe_ptx::smem_u32(ost(o) + sp * 8192u);
+          const uint32_t b0 = floe_ptx::smem_u32(ost(o) + 16384u + sp * N * 64u);
+          for (uint32_t kh = 0; kh < 2; ++kh) {
+            const uint64_t da = desc(a0 + kh * 256u), db = desc(b0 + kh * 256u);
             asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                : "=r"(c[l][0]), "=r"(c[l][1]), "=r"(c[l][2]), "=r"(c[l][3]), "=r"(c[l][4]),
-                  "=r"(c[l][5]), "=r"(c[l][6]), "=r"(c[l][7]), "=r"(c[l][8]), "=r"(c[l][9]),
-                  "=r"(c[l][10]), "=r"(c[l][11]), "=r"(c[l][12]), "=r"(c[l][13]), "=r"(c[l][14]),
-                  "=r"(c[l][15])
-                : "r"(addr));
-          }
-          asm volatile("tcgen05.wait::ld.sync.aligned;");
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const uint32_t tok = tc + (uint32_t)i;
-            const int isum = (int)c[0][i] + 256 * (int)c[1][i] + 65536 * (int)c[2][i];  // exact
-            float &acc = vacc[tok * kRows + row];
-            acc = fmaf(scale * invS_s[tok], (float)isum, fmaf(zero, xs_s[sp * Bp + tok], acc));
+                "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, q;\n\t}" ::"r"(tmem + col),
+                "l"(da), "l"(db), "r"(idesc), "r"(kh));
           }
         }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            floe_ptx::smem_u32(&mdone[o])));
+        if (p == 8) tmark(a, 25);
+        // refills: the packed stage of pair p is free once unpacked (aready
+        // implies it); the limbs of pair p-1 once its MMAs are done
+        if (p % kPPS == kPPS - 1 && p / kPPS + kPS < QS) {  // stage p/kPPS fully unpacked
+          const uint32_t q = p / kPPS;
+          floe_ptx::mbar_wait(&pempty[q % kPS], (q / kPS) & 1u, (13u << 28) | p);
+          issue_packed(q + kPS);
+        }
+        // refill the limbs of pair p-lag's operand stage; lag 2 (when the ring
+        // allows) waits on MMAs issued two pairs ago, not on the ones just issued
+        const uint32_t lag = NOS > 2u ? 2u : 1u;
+        if (p >= lag && p - lag + NOS < PAIRS) {
+          floe_ptx::mbar_wait(&mdone[(p - lag) % NOS], ((p - lag) / NOS) & 1u, (14u << 28) | p);
+          issue_xl(p - lag + NOS);
+        }
+        if (p == 8) tmark(a, 26);
       }
-      asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncthreads();  // TMEM may be overwritten by the next batch's MMAs
-      batch_begin = span_end;
+    }
+    __syncwarp();
+  } else {
+    // ============================ consumers =============================
+    // epilogue role: TMEM lane quadrant, token chunk of 16, and (when there
+    // are fewer than 4 token chunks) which of the batch's spans, so that all
+    // 16 warps drain TMEM for any batch size
+    const uint32_t nchunk = Bp / 16u, spg = 4u / nchunk;  // span groups per chunk
+    const uint32_t quad = warp & 3u, wg = warp >> 2;
+    const uint32_t tchunk = wg % nchunk, sphase = wg / nchunk;
+    const uint32_t row = 32u * quad + lane;
+    const bool ep = sphase < spg;
+    float acc1[16], acc2[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc1[i] = acc2[i] = 0.0f;
+    uint32_t batch = 0, batch_begin = 0;
+    for (uint32_t p = 0; p < PAIRS; ++p) {
+      const uint32_t q = p / kPPS, pp = p % kPPS, s = q % kPS, o = p % NOS;
+      if (t == 0 && p == 8) tmark(a, 19);
+      floe_ptx::mbar_wait(&pfull[s], (q / kPS) & 1u, (15u << 28) | p);
+      if (t == 0 && p == 8) tmark(a, 27);
+      if (p >= NOS)  // A[o] free: MMAs of pair p - NOS done
+        floe_ptx::mbar_wait(&mdone[o], ((p / NOS) - 1u) & 1u, (16u << 28) | p);
+      if (t == 0 && p == 8) tmark(a, 28);
+      {
+        const uint32_t *cw = reinterpret_cast<const uint32_t *>(pst(s) + pp * 512u);
+        uint8_t *A = ost(o);
+        if (t < 8u * 32u) {  // thread = (tile j, lane ln): its 4 code words
+          const uint32_t j = t >> 5, ln = t & 31u, g = ln >> 2, chunk = ln & 3u;
+          const uint4 w4 = *reinterpret_cast<const uint4 *>(cw + j * (kPPS * 128u) + 4u * ln);
+          const uint32_t ws[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+          for (uint32_t k = 0; k < 4; ++k) {  // slot k: row g + 8(k&1), span k>>1
+            const uint32_t w = ws[k], r = 16u * j + g + 8u * (k & 1u);
+            const uint4 ov = make_uint4(w & 0x03030303u, (w >> 2) & 0x03030303u,
+                                        (w >> 4) & 0x03030303u, (w >> 6) & 0x03030303u);
+            *reinterpret_cast<uint4 *>(A + (k >> 1) * 8192u + kmaj_off(r, 16u * chunk)) = ov;
+          }
+        }
+        const uint32_t *mw = reinterpret_cast<const uint32_t *>(pst(s) + kPPS * 4096u + pp * 128u);
+        if (t >= 8u * 32u && t < 16u * 32u) {
+          const uint32_t tm = t - 8u * 32u;
+          const uint32_t j = tm >> 5, mq = tm & 31u, k = mq & 3u, g = mq >> 2;
+          const uint32_t r = 16u * j + g + 8u * (k & 1u), sp = k >> 1;
+          meta_batch[(2u * p + sp - batch_begin) * 128u + r] = mw[j * (kPPS * 32u) + mq];
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;");  // generic writes -> tensor-core reads
+      __syncwarp();
+      if (lane == 0) {
+        if (pp == kPPS - 1) floe_ptx::mbar_arrive(&pempty[s]);
+        floe_ptx::mbar_arrive(&aready[o]);
+      }
+      if (t == 0 && p == 8) tmark(a, 29);
+      const uint32_t span_end = 2u * p + 2u;
+      if (span_end - batch_begin == SB || p + 1 == PAIRS) {
+        // all MMAs of the batch are done when pair p's commit fires
+        if (t == 0 && batch < 12) tmark(a, 4 + 2 * (int)batch);
+        floe_ptx::mbar_wait(&mdone[o], (p / NOS) & 1u, (17u << 28) | p);
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps));  // meta_batch complete
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (ep) {
+          for (uint32_t sp = batch_begin + sphase; sp < span_end; sp += spg) {
+            const uint32_t mv = meta_batch[(sp - batch_begin) * 128u + row];
+            const float scale = __half2float(__ushort_as_half((unsigned short)(mv & 0xffffu)));
+            const float zero = __half2float(__ushort_as_half((unsigned short)(mv >> 16)));
+            const uint32_t col0 = (sp - batch_begin) * N + 16u * tchunk;
+            uint32_t c[3][16];
+#pragma unroll
+            for (int l = 0; l < 3; ++l) {
+              const uint32_t addr = tmem + ((32u * quad) << 16) + col0 + (uint32_t)l * Bp;
+              asm volatile(
+                  "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                  : "=r"(c[l][0]), "=r"(c[l][1]), "=r"(c[l][2]), "=r"(c[l][3]), "=r"(c[l][4]),
+                    "=r"(c[l][5]), "=r"(c[l][6]), "=r"(c[l][7]), "=r"(c[l][8]), "=r"(c[l][9]),
+                    "=r"(c[l][10]), "=r"(c[l][11]), "=r"(c[l][12]), "=r"(c[l][13]), "=r"(c[l][14]),
+                    "=r"(c[l][15])
+                  : "r"(addr));
+            }
+            asm volatile("tcgen05.wait::ld.sync.aligned;");
+            const float4 *xsv = reinterpret_cast<const float4 *>(xs_s + sp * Bp + 16u * tchunk);
+#pragma unroll
+            for (int i4 = 0; i4 < 4; ++i4) {
+              const float4 z = xsv[i4];
+              const float zz[4] = {z.x, z.y, z.z, z.w};
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const int i = 4 * i4 + u;
+                const int isum = (int)c[0][i] + 256 * (int)c[1][i] + 65536 * (int)c[2][i];  // exact
+                acc1[i] = fmaf(scale, (float)isum, acc1[i]);
+                acc2[i] = fmaf(zero, zz[u], acc2[i]);
+              }
+            }
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (t == 0 && batch < 12) tmark(a, 5 + 2 * (int)batch);
+        if (lane == 0) floe_ptx::mbar_arrive(&tfree);  // TMEM and meta_batch reusable
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps));  // meta_batch reuse
+        ++batch;
+        batch_begin = span_end;
+      }
+    }
+    // combine the span groups' partials (through the packed ring, free now),
+    // then v = invS * sum_g scale*isum + sum_g zero*xs (invS a power of two)
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps));
+    float *red = reinterpret_cast<float *>(smem + L.p);  // [wg][row][32]
+    if (ep && sphase > 0)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        red[(wg * 128u + row) * 32u + i] = acc1[i];
+        red[(wg * 128u + row) * 32u + 16 + i] = acc2[i];
+      }
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps));
+    const uint32_t c = blk * 128u + row;
+    if (ep && sphase == 0) {
+      for (uint32_t ph = 1; ph < spg; ++ph) {
+        const uint32_t og = ph * nchunk + tchunk;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          acc1[i] += red[(og * 128u + row) * 32u + i];
+          acc2[i] += red[(og * 128u + row) * 32u + 16 + i];
+        }
+      }
+      if (c < a.di)
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const uint32_t tok = 16u * tchunk + (uint32_t)i;
+          if (tok < B) a.v[(size_t)tok * a.di + c] = fmaf(invS_s[tok], acc1[i], acc2[i]);
+        }
     }
   }
-  // v[t][c] for the block's channels
-  const uint32_t c = blk * kRows + row;
-  if (c < a.di)
-    for (uint32_t tok = 0; tok < B; ++tok) a.v[(size_t)tok * a.di + c] = vacc[tok * kRows + row];
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+  if (t == 0) tmark(a, 30);
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
