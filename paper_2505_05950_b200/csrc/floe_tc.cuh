@@ -151,11 +151,11 @@ __device__ __forceinline__ void tmark(const BatchedArgs &a, int k) {
   }
 }
 
-// Roles: warps 0..15 consume (unpack, epilogue), warp 16 lane 0 produces
-// (bulk copies) and issues the MMAs.  Epilogue: warp w reads TMEM lane
+// Roles: warps 0..15 consume (unpack, epilogue), warp 16 lane 0 issues the
+// MMAs, warp 17 lane 0 issues the bulk copies (so neither waits on the other).  Epilogue: warp w reads TMEM lane
 // quadrant w % 4 (its 32 channel rows) for token chunk w / 4 (16 tokens).
 constexpr int kConsumerWarps = 16;
-constexpr int kBThreads = 32 * (kConsumerWarps + 1);
+constexpr int kBThreads = 32 * (kConsumerWarps + 2);  // + MMA warp + copy warp
 constexpr int kPS = 4;   // packed ring stages
 constexpr int kPPS = 4;  // span pairs per packed stage: per tile one 2 KB codes + one 512 B meta copy
 
@@ -229,31 +229,48 @@ __global__ void __launch_bounds__(kBThreads, 1) k1_batched(const BatchedArgs a) 
   const uint32_t tmem = tmem_base;
   if (t == 0) tmark(a, 1);
 
-  if (warp == kConsumerWarps) {
-    // ======================= producer / MMA issuer =======================
+  // packed stage q = span pairs kPPS*q ..: per tile the codes (kPPS x 512 B)
+  // and meta (kPPS x 128 B) of those pairs are contiguous in the tile
+  auto issue_packed = [&](uint32_t q) {
+    const uint32_t s = q % kPS, p0 = q * kPPS;
+    uint8_t *st = pst(s);
+    floe_ptx::mbar_arrive_expect_tx(&pfull[s], ntiles * kPPS * (512u + 128u));
+    for (uint32_t j = 0; j < ntiles; ++j) {
+      const uint32_t *tile = a.tiles + (size_t)(tile0 + j) * TILE_W;
+      floe_ptx::bulk_g2s(st + kPPS * 512u * j, tile + p0 * 128u, kPPS * 512u, &pfull[s]);
+      floe_ptx::bulk_g2s(st + kPPS * 4096u + kPPS * 128u * j, tile + DH + p0 * 32u, kPPS * 128u,
+                         &pfull[s]);
+    }
+  };
+  auto issue_xl = [&](uint32_t p) {
+    const uint32_t o = p % NOS;
+    floe_ptx::mbar_arrive_expect_tx(&xfull[o], 2u * N * 64u);
+    floe_ptx::bulk_g2s(ost(o) + 16384u, a.xl + (size_t)(2u * p) * N * 64u, 2u * N * 64u,
+                       &xfull[o]);
+  };
+  constexpr uint32_t QS = PAIRS / kPPS;  // packed stages in all
+
+  if (warp == kConsumerWarps + 1) {
+    // ============================= copy warp =============================
     if (lane == 0) {
-      // packed stage q = span pairs kPPS*q ..: per tile the codes (kPPS x 512 B)
-      // and meta (kPPS x 128 B) of those pairs are contiguous in the tile
-      auto issue_packed = [&](uint32_t q) {
-        const uint32_t s = q % kPS, p0 = q * kPPS;
-        uint8_t *st = pst(s);
-        floe_ptx::mbar_arrive_expect_tx(&pfull[s], ntiles * kPPS * (512u + 128u));
-        for (uint32_t j = 0; j < ntiles; ++j) {
-          const uint32_t *tile = a.tiles + (size_t)(tile0 + j) * TILE_W;
-          floe_ptx::bulk_g2s(st + kPPS * 512u * j, tile + p0 * 128u, kPPS * 512u, &pfull[s]);
-          floe_ptx::bulk_g2s(st + kPPS * 4096u + kPPS * 128u * j, tile + DH + p0 * 32u,
-                             kPPS * 128u, &pfull[s]);
-        }
-      };
-      auto issue_xl = [&](uint32_t p) {
-        const uint32_t o = p % NOS;
-        floe_ptx::mbar_arrive_expect_tx(&xfull[o], 2u * N * 64u);
-        floe_ptx::bulk_g2s(ost(o) + 16384u, a.xl + (size_t)(2u * p) * N * 64u, 2u * N * 64u,
-                           &xfull[o]);
-      };
-      constexpr uint32_t QS = PAIRS / kPPS;  // packed stages in all
       for (uint32_t q = 0; q < min((uint32_t)kPS, QS); ++q) issue_packed(q);
       for (uint32_t q = 0; q < min(NOS, PAIRS); ++q) issue_xl(q);
+      for (uint32_t p = 0; p < PAIRS; ++p) {
+        if (p % kPPS == kPPS - 1 && p / kPPS + kPS < QS) {  // stage p/kPPS fully unpacked
+          const uint32_t q = p / kPPS;
+          floe_ptx::mbar_wait(&pempty[q % kPS], (q / kPS) & 1u, (13u << 28) | p);
+          issue_packed(q + kPS);
+        }
+        if (p + NOS < PAIRS) {  // pair p's MMAs done: its operand stage takes pair p + NOS
+          floe_ptx::mbar_wait(&mdone[p % NOS], (p / NOS) & 1u, (14u << 28) | p);
+          issue_xl(p + NOS);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == kConsumerWarps) {
+    // ============================= MMA warp ==============================
+    if (lane == 0) {
       const uint32_t idesc = (2u << 4) | (0u << 7) | (1u << 10) | ((N >> 3) << 17) |
                              ((uint32_t)(128 >> 4) << 24);
       auto desc = [](uint32_t saddr) -> uint64_t {
@@ -291,21 +308,6 @@ __global__ void __launch_bounds__(kBThreads, 1) k1_batched(const BatchedArgs a) 
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
             floe_ptx::smem_u32(&mdone[o])));
         if (p == 8) tmark(a, 25);
-        // refills: the packed stage of pair p is free once unpacked (aready
-        // implies it); the limbs of pair p-1 once its MMAs are done
-        if (p % kPPS == kPPS - 1 && p / kPPS + kPS < QS) {  // stage p/kPPS fully unpacked
-          const uint32_t q = p / kPPS;
-          floe_ptx::mbar_wait(&pempty[q % kPS], (q / kPS) & 1u, (13u << 28) | p);
-          issue_packed(q + kPS);
-        }
-        // refill the limbs of pair p-lag's operand stage; lag 2 (when the ring
-        // allows) waits on MMAs issued two pairs ago, not on the ones just issued
-        const uint32_t lag = NOS > 2u ? 2u : 1u;
-        if (p >= lag && p - lag + NOS < PAIRS) {
-          floe_ptx::mbar_wait(&mdone[(p - lag) % NOS], ((p - lag) / NOS) & 1u, (14u << 28) | p);
-          issue_xl(p - lag + NOS);
-        }
-        if (p == 8) tmark(a, 26);
       }
     }
     __syncwarp();
