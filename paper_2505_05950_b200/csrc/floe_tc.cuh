@@ -23,11 +23,11 @@
 //       m = 0..3, so K position 4m + b of a 16-byte chunk holds element
 //       16*chunk + 4b + m -- a fixed permutation of K that B follows too;
 //   B = limbs, row n = l * Bp + t (limb l of token t, Bp = B rounded up to 16).
-// One CTA per 128-channel block.  A producer warp streams span pairs by bulk
-// copies (an 8-deep ring of codes+meta, 2-4 operand stages of limbs) and
-// issues the MMAs; 16 consumer warps unpack codes into the A operand and drain
-// TMEM (thread = channel row, 16 tokens) once per batch of spans that fills
-// the 512 TMEM columns.
+// One CTA per 128-channel block.  A copy warp streams span pairs by bulk
+// copies (a ring of 4-pair codes+meta stages, 2-4 operand stages of limbs), an
+// MMA warp issues the MMAs, and 16 consumer warps unpack codes into the A
+// operand and drain TMEM (thread = channel row, 16 tokens) once per batch of
+// spans that fills the 512 TMEM columns.
 #pragma once
 
 #include <cuda_fp16.h>
