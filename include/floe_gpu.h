@@ -189,6 +189,17 @@ int floe_gpu_qgemv_channels(const floe_gpu_expert *e, floe_gpu_workspace *ws,
 int floe_gpu_qgemv_channels_batched(const floe_gpu_expert *e, const float *x_dev,
                                     uint32_t n_tokens, float *v_dev, floe_stream_t stream);
 
+/* Batched expert_forward_sparse (SURVEY config 4): y_dev[t] =
+ * expert_forward_sparse(e, x_dev[t]) for n_tokens <= 64 tokens (model.cpp:128-142;
+ * each token keeps its own channels, !(|v| < threshold)).  The up projection
+ * runs once for the batch on the tensor cores, and the gate/down records of the
+ * union of kept channels are read once.  x_dev [n][d_hidden], y_dev
+ * [n][d_hidden], v_dev nullable [n][d_intermediate].  Fast-layout experts with
+ * gate/down records only. */
+int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x_dev,
+                                    uint32_t n_tokens, float *y_dev, float *v_dev,
+                                    floe_stream_t stream);
+
 /* out = dequantize(up_q) in f32, bit-exact with floe::dequantize. */
 int floe_gpu_dequantize_up(const floe_gpu_expert *e, float *out_dev,
                            floe_stream_t stream);

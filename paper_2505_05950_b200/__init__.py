@@ -32,11 +32,12 @@ from ._abi import (  # noqa: F401
     predict_mask,
     qgemv_channels,
     qgemv_channels_batched,
+    expert_forward_batched,
     quantize,
 )
 
 __all__ = ["FloeError", "GpuExpert", "GpuLayer", "GpuPredictor", "Offload", "Workspace",
            "abi_version", "dequantize", "device_info", "expert_forward_sparse",
            "exported_symbols", "layer_forward", "lib", "library_path", "predict_experts",
-           "predict_mask", "qgemv_channels", "qgemv_channels_batched", "gen_normals", "layer_forward_host",
+           "predict_mask", "qgemv_channels", "qgemv_channels_batched", "expert_forward_batched", "gen_normals", "layer_forward_host",
            "quantize"]

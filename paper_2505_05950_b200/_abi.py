@@ -89,6 +89,7 @@ _SIGS = {
     "floe_gpu_expert_forward_sparse_host": (ct.c_int, [_P, _P, _P, _P, _P, _P, _P]),
     "floe_gpu_qgemv_channels": (ct.c_int, [_P, _P, _P, _P, _P]),
     "floe_gpu_qgemv_channels_batched": (ct.c_int, [_P, _P, ct.c_uint32, _P, _P]),
+    "floe_gpu_expert_forward_batched": (ct.c_int, [_P, _P, ct.c_uint32, _P, _P, _P]),
     "floe_gpu_dequantize_up": (ct.c_int, [_P, _P, _P]),
     "floe_gpu_predict_mask": (ct.c_int, [_P, _P, _P, _F, _P, _P, _P, _P]),
     "floe_gpu_layer_create": (ct.c_int, [ct.POINTER(LayerHostView), ct.POINTER(_P)]),
@@ -360,6 +361,19 @@ def qgemv_channels_batched(e: GpuExpert, x, stream=None):
     _check(lib().floe_gpu_qgemv_channels_batched(e.handle, x.data_ptr(), x.shape[0], v.data_ptr(),
                                                  _stream(stream)))
     return v
+
+
+def expert_forward_batched(e: GpuExpert, x, *, v=None, stream=None):
+    """expert_forward_sparse for a batch of tokens: x [B, d_hidden] -> y [B, d_hidden]
+    (batched up projection on tcgen05, union gate/down records read once; B <= 64)."""
+    torch = _torch()
+    if x.dim() != 2 or x.shape[1] != e.d_hidden or x.dtype != torch.float32 or not x.is_cuda:
+        raise FloeError("expert_forward_batched: x must be a cuda float32 [B, d_hidden]")
+    x = x.contiguous()
+    y = torch.empty_like(x)
+    _check(lib().floe_gpu_expert_forward_batched(e.handle, x.data_ptr(), x.shape[0], y.data_ptr(),
+                                                 _ptr(v), _stream(stream)))
+    return y
 
 
 def dequantize(e: GpuExpert, stream=None):

@@ -1052,6 +1052,67 @@ int floe_gpu_qgemv_channels_batched(const floe_gpu_expert *e, const float *x, ui
   return rc;
 }
 
+int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x, uint32_t n_tokens,
+                                    float *y_out, float *v_out, floe_stream_t stream) {
+  if (!e || !x || !y_out) return fail(FLOE_ERR_INVALID, "expert_forward_batched: null argument");
+  if (n_tokens == 0) return FLOE_OK;
+  if (e->up_only)
+    return fail(FLOE_ERR_INVALID, "expert_forward_batched: expert has no gate/down records");
+  if (!e->fast)
+    return fail(FLOE_ERR_UNSUPPORTED, "expert_forward_batched: needs the tile layout");
+  if (n_tokens > (uint32_t)floe_tc::kMaxTokens)
+    return fail(FLOE_ERR_INVALID, "expert_forward_batched: at most %d tokens", floe_tc::kMaxTokens);
+  cudaStream_t st = S(stream);
+  const uint32_t B = n_tokens, di = e->di, dh = e->dh;
+  // scratch: count | v [B][di] | uc [di] | um [di] | A [di][B]
+  const size_t o_v = 256, o_uc = o_v + ((4ull * B * di + 255) & ~size_t(255));
+  const size_t o_um = o_uc + ((4ull * di + 255) & ~size_t(255));
+  const size_t o_a = o_um + 8ull * di, total = o_a + 4ull * di * B;
+  uint8_t *scratch = nullptr;
+  CK(cudaMallocAsync(reinterpret_cast<void **>(&scratch), total, st));
+  uint32_t *count = reinterpret_cast<uint32_t *>(scratch);
+  float *v = v_out ? v_out : reinterpret_cast<float *>(scratch + o_v);
+  uint32_t *uc = reinterpret_cast<uint32_t *>(scratch + o_uc);
+  unsigned long long *um = reinterpret_cast<unsigned long long *>(scratch + o_um);
+  float *A = reinterpret_cast<float *>(scratch + o_a);
+  int rc = floe_gpu_qgemv_channels_batched(e, x, B, v, stream);
+  if (rc == FLOE_OK) {
+    CK(cudaMemsetAsync(count, 0, 4, st));
+    floe_tc::union_masks<<<(di + 255) / 256, 256, 0, st>>>(v, B, di, e->host_desc.threshold, count,
+                                                           uc, um);
+    CK_LAUNCH();
+    const __half *rec = e->host_desc.records;
+    const uint32_t csm = 4u * floe_tc::kCoefTokens * dh;
+    const int sm = device_info().sm;
+    if (dh == 4096) {
+      rc = set_smem(floe_tc::coeffs<4096>, csm);
+      if (rc == FLOE_OK) {
+        floe_tc::coeffs<4096><<<2 * sm, 256, csm, st>>>(rec, x, v, B, di, count, uc, um, A);
+        CK(cudaMemsetAsync(y_out, 0, 4ull * B * dh, st));
+        const uint32_t dsm = 4u * floe_tc::kDownRowCap * B;
+        rc = set_smem(floe_tc::down_accum<4096>, dsm);
+        if (rc == FLOE_OK)
+          floe_tc::down_accum<4096><<<dim3(4096 / 1024, floe_tc::kDownRowChunks), 256, dsm, st>>>(
+              rec, B, count, uc, A, y_out);
+      }
+    } else {
+      rc = set_smem(floe_tc::coeffs<2048>, csm);
+      if (rc == FLOE_OK) {
+        floe_tc::coeffs<2048><<<2 * sm, 256, csm, st>>>(rec, x, v, B, di, count, uc, um, A);
+        CK(cudaMemsetAsync(y_out, 0, 4ull * B * dh, st));
+        const uint32_t dsm = 4u * floe_tc::kDownRowCap * B;
+        rc = set_smem(floe_tc::down_accum<2048>, dsm);
+        if (rc == FLOE_OK)
+          floe_tc::down_accum<2048><<<dim3(2048 / 1024, floe_tc::kDownRowChunks), 256, dsm, st>>>(
+              rec, B, count, uc, A, y_out);
+      }
+    }
+    if (rc == FLOE_OK) CK_LAUNCH();
+  }
+  CK(cudaFreeAsync(scratch, st));
+  return rc;
+}
+
 int floe_gpu_dequantize_up(const floe_gpu_expert *e, float *out, floe_stream_t stream) {
   if (!e || !out) return fail(FLOE_ERR_INVALID, "dequantize: null argument");
   const uint64_t n = (uint64_t)e->dh * e->di;

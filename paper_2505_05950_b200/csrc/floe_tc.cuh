@@ -33,6 +33,7 @@
 #include <cuda_fp16.h>
 #include <cstdint>
 
+#include "floe_kernels.cuh"
 #include "floe_ptx.cuh"
 
 namespace floe_tc {
@@ -447,6 +448,170 @@ __global__ void __launch_bounds__(kBThreads, 1) k1_batched(const BatchedArgs a) 
   if (t == 0) tmark(a, 30);
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// ------------------------------------------------------- batched gate/down
+// expert_forward_sparse (model.cpp:128-142) for B tokens after the batched up
+// projection: token t keeps channel c iff !(|v[t][c]| < t_e) (model.cpp:135:
+// ties and NaN kept); the union of kept channels is read once.
+//   union_masks: per channel a token bitmask; kept channels appended to a list
+//   coeffs:      A[u][t] = silu(gate_c . x_t) * v[t][c] for the tokens keeping c
+//                (la.cpp:25-31), one warp per union channel, x in shared memory
+//   down_accum:  y[t][j] = sum_u A[u][t] * down_c[j], CTAs over (1024-column
+//                chunk, union-row chunk), partial sums added into y
+constexpr int kCoefTokens = 8;  // tokens per shared-memory pass of coeffs
+
+__global__ void __launch_bounds__(256) union_masks(const float *__restrict__ v, uint32_t B,
+                                                   uint32_t di, float thr,
+                                                   uint32_t *__restrict__ count,
+                                                   uint32_t *__restrict__ uc,
+                                                   unsigned long long *__restrict__ um) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= di) return;
+  unsigned long long m = 0;
+  for (uint32_t t = 0; t < B; ++t)
+    if (!(fabsf(v[(size_t)t * di + c]) < thr)) m |= 1ull << t;
+  if (m) {
+    const uint32_t i = atomicAdd(count, 1u);
+    uc[i] = c;
+    um[i] = m;
+  }
+}
+
+template <int DH>
+__global__ void __launch_bounds__(256) coeffs(const __half *__restrict__ records,
+                                              const float *__restrict__ x, const float *__restrict__ v,
+                                              uint32_t B, uint32_t di,
+                                              const uint32_t *__restrict__ count,
+                                              const uint32_t *__restrict__ uc,
+                                              const unsigned long long *__restrict__ um,
+                                              float *__restrict__ A /* [n][B] */) {
+  extern __shared__ __align__(16) float xs[];  // [kCoefTokens][DH]
+  const uint32_t n = *count, lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  for (uint32_t t0 = 0; t0 < B; t0 += kCoefTokens) {
+    const uint32_t tb = min((uint32_t)kCoefTokens, B - t0);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < tb * DH / 4u; i += blockDim.x)
+      reinterpret_cast<float4 *>(xs)[i] = reinterpret_cast<const float4 *>(x + (size_t)t0 * DH)[i];
+    __syncthreads();
+    for (uint32_t u = blockIdx.x * 8u + warp; u < n; u += gridDim.x * 8u) {
+      const uint32_t c = uc[u];
+      const unsigned long long m = (um[u] >> t0) & ((tb < 64u ? (1ull << tb) : 0ull) - 1ull);
+      if (!m) {  // no token of this group keeps channel c
+        if (lane < tb) A[(size_t)u * B + t0 + lane] = 0.0f;
+        continue;
+      }
+      // gate row c: DH halves, lane-strided 8-half chunks
+      const uint4 *g4 = reinterpret_cast<const uint4 *>(records + (size_t)c * 2 * DH);
+      uint4 gr[DH / 256];
+#pragma unroll
+      for (int i = 0; i < DH / 256; ++i) gr[i] = __ldg(g4 + lane + 32 * i);
+      for (unsigned long long mm = m; mm; mm &= mm - 1) {
+        const uint32_t tt = (uint32_t)__ffsll((long long)mm) - 1u;
+        const float *xt = xs + (size_t)tt * DH;
+        float acc = 0.0f;
+#pragma unroll
+        for (int i = 0; i < DH / 256; ++i) {
+          const __half2 *h2 = reinterpret_cast<const __half2 *>(&gr[i]);
+          const float4 xa = *reinterpret_cast<const float4 *>(xt + 8 * (lane + 32 * i));
+          const float4 xb = *reinterpret_cast<const float4 *>(xt + 8 * (lane + 32 * i) + 4);
+          float2 f;
+          f = __half22float2(h2[0]); acc = fmaf(f.x, xa.x, acc); acc = fmaf(f.y, xa.y, acc);
+          f = __half22float2(h2[1]); acc = fmaf(f.x, xa.z, acc); acc = fmaf(f.y, xa.w, acc);
+          f = __half22float2(h2[2]); acc = fmaf(f.x, xb.x, acc); acc = fmaf(f.y, xb.y, acc);
+          f = __half22float2(h2[3]); acc = fmaf(f.x, xb.z, acc); acc = fmaf(f.y, xb.w, acc);
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) {
+          const uint32_t t = t0 + tt;
+          const float z = acc;
+          A[(size_t)u * B + t] = z / (1.0f + expf(-z)) * v[(size_t)t * di + c];  // silu(g) * v
+        }
+      }
+      if (lane < tb && !((m >> lane) & 1ull)) A[(size_t)u * B + t0 + lane] = 0.0f;
+    }
+  }
+}
+
+// Grid (DH / 1024 column chunks) x (row chunks): each CTA reads 2 KB of each of
+// its union rows' down halves (a warp: 256 contiguous bytes), thread = 4
+// columns x 16 tokens in registers, token groups of 16 in turn; partial sums
+// are added into y (zeroed by the caller) with vector reductions.
+constexpr int kDownRowChunks = 37;
+constexpr uint32_t kDownRowCap = 400;  // rows per chunk staged in shared memory
+
+template <int DH>
+__global__ void __launch_bounds__(256) down_accum(const __half *__restrict__ records,
+                                                  uint32_t B, const uint32_t *__restrict__ count,
+                                                  const uint32_t *__restrict__ uc,
+                                                  const float *__restrict__ A, float *__restrict__ y) {
+  const uint32_t n = *count;
+  const uint32_t r0 = (uint32_t)(((uint64_t)n * blockIdx.y) / gridDim.y);
+  const uint32_t r1 = (uint32_t)(((uint64_t)n * (blockIdx.y + 1)) / gridDim.y);
+  const uint32_t col = blockIdx.x * 1024u + 4u * threadIdx.x;
+  // the chunk's channel ids and coefficients up front (shared memory): the
+  // record loads do not wait on them and the coefficients are broadcast reads
+  __shared__ uint32_t ucs[1024];
+  extern __shared__ float As[];  // [min(r1 - r0, kDownRowCap)][B]
+  const uint32_t nr = min(r1 - r0, 1024u);
+  const uint32_t na = min(r1 - r0, kDownRowCap);
+  for (uint32_t i = threadIdx.x; i < nr; i += blockDim.x) ucs[i] = uc[r0 + i];
+  for (uint32_t i = threadIdx.x; i < na * B; i += blockDim.x) As[i] = A[(size_t)r0 * B + i];
+  __syncthreads();
+  auto coef = [&](uint32_t u, uint32_t t) {
+    return u - r0 < na ? As[(u - r0) * B + t] : __ldg(A + (size_t)u * B + t);
+  };
+  auto chan = [&](uint32_t u) { return u - r0 < nr ? ucs[u - r0] : uc[u]; };
+  for (uint32_t tg = 0; tg < B; tg += 16u) {
+    const uint32_t nt = min(16u, B - tg);
+    float acc[16][4];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.0f;
+    uint32_t u = r0;
+    for (; u + 8u <= r1; u += 8u) {  // eight rows' loads in flight
+      uint2 d[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        d[k] = __ldg(reinterpret_cast<const uint2 *>(records + (size_t)chan(u + k) * 2 * DH + DH + col));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float2 d01 = __half22float2(*reinterpret_cast<const __half2 *>(&d[k].x));
+        const float2 d23 = __half22float2(*reinterpret_cast<const __half2 *>(&d[k].y));
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          if ((uint32_t)t < nt) {
+            const float a = coef(u + k, tg + t);
+            acc[t][0] = fmaf(a, d01.x, acc[t][0]);
+            acc[t][1] = fmaf(a, d01.y, acc[t][1]);
+            acc[t][2] = fmaf(a, d23.x, acc[t][2]);
+            acc[t][3] = fmaf(a, d23.y, acc[t][3]);
+          }
+        }
+      }
+    }
+    for (; u < r1; ++u) {
+      const uint2 d = __ldg(reinterpret_cast<const uint2 *>(records + (size_t)chan(u) * 2 * DH + DH + col));
+      const float2 d01 = __half22float2(*reinterpret_cast<const __half2 *>(&d.x));
+      const float2 d23 = __half22float2(*reinterpret_cast<const __half2 *>(&d.y));
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        if ((uint32_t)t < nt) {
+          const float a = coef(u, tg + t);
+          acc[t][0] = fmaf(a, d01.x, acc[t][0]);
+          acc[t][1] = fmaf(a, d01.y, acc[t][1]);
+          acc[t][2] = fmaf(a, d23.x, acc[t][2]);
+          acc[t][3] = fmaf(a, d23.y, acc[t][3]);
+        }
+      }
+    }
+    if (r1 > r0)
+#pragma unroll
+      for (int t = 0; t < 16; ++t)
+        if ((uint32_t)t < nt)
+          floe_k::red_add_v4(y + (size_t)(tg + t) * DH + col, acc[t][0], acc[t][1], acc[t][2],
+                             acc[t][3]);
+  }
 }
 
 }  // namespace floe_tc

@@ -99,3 +99,59 @@ def test_batched_argument_errors(fb, torch, mixtral):
     generic = fb.GpuExpert(64, 256, 8, 64, q.codes, q.scales, q.zeros)
     with pytest.raises(fb.FloeError, match="tile layout"):
         fb.qgemv_channels_batched(generic, torch.zeros((2, 64), device="cuda"))
+
+
+# ------------------------------------------------ batched expert forward
+@pytest.fixture(scope="module")
+def mixtral_full(fb):
+    dh, di = 4096, 14336
+    gate, up, down = O.seeded_expert(dh, di, 99)
+    q = O.quantize(up, 2, 64)
+    x0 = O.seeded_input(dh, 100)
+    t = O.calibrate_threshold(np.abs(O.qgemv_channels(q, dh, x0)), 0.8)
+    e = fb.GpuExpert(dh, di, 2, 64, q.codes, q.scales, q.zeros, gate=gate, down=down, threshold=t)
+    return O.Expert(dh, di, q, gate, down, t), e
+
+
+@pytest.mark.parametrize("B", [1, 7, 16, 64])
+def test_expert_forward_batched_matches_per_token(fb, torch, mixtral_full, B):
+    """Each token of the batch == the single-token fused path on the same
+    token (same masks up to exact ties), and == the reference within 1e-2."""
+    ref_e, e = mixtral_full
+    X = np.stack([O.seeded_input(4096, 100 + t) for t in range(B)])
+    xd = torch.from_numpy(X).cuda()
+    v = torch.empty((B, 14336), dtype=torch.float32, device="cuda")
+    Y = fb.expert_forward_batched(e, xd, v=v).cpu().numpy()
+    ws = fb.Workspace(4096, 14336)
+    for t in (range(B) if B <= 16 else [0, 5, 31, 63]):
+        y1 = fb.expert_forward_sparse(e, xd[t], ws).cpu().numpy()
+        assert O.rel_l2(Y[t], y1) <= 1e-4, t
+        if t < 3:
+            assert O.rel_l2(Y[t], O.expert_forward_sparse(ref_e, X[t])) <= 1e-2
+    V = v.cpu().numpy()
+    _check(ref_e.up_q, 4096, X, V, [0, B - 1])
+
+
+def test_expert_forward_batched_small_and_edge(fb, torch):
+    """Ragged shape, a threshold that keeps nothing for some tokens, and a
+    token with a non-finite input (its NaN v keeps every channel, as the
+    reference's `fabs(v) < t` test does) next to finite ones."""
+    dh, di = 2048, 520
+    gate, up, down = O.seeded_expert(dh, di, 11)
+    q = O.quantize(up, 2, 64)
+    X = np.stack([O.token_input(1, t, dh) * (0.05 if t == 1 else 1.0) for t in range(5)])
+    t_hi = O.calibrate_threshold(np.abs(O.qgemv_channels(q, dh, X[0])), 0.9)
+    e = fb.GpuExpert(dh, di, 2, 64, q.codes, q.scales, q.zeros, gate=gate, down=down,
+                     threshold=t_hi)
+    ref_e = O.Expert(dh, di, q, gate, down, t_hi)
+    X[3, 9] = np.nan
+    Y = fb.expert_forward_batched(e, torch.from_numpy(X).cuda()).cpu().numpy()
+    ws = fb.Workspace(dh, di)
+    for t in (0, 1, 2, 4):
+        y1 = fb.expert_forward_sparse(e, torch.from_numpy(X[t]).cuda(), ws).cpu().numpy()
+        if np.linalg.norm(y1) == 0:
+            assert np.all(Y[t] == 0)
+        else:
+            assert O.rel_l2(Y[t], y1) <= 1e-4
+        assert O.rel_l2(Y[t], O.expert_forward_sparse(ref_e, X[t])) <= 1e-2 or np.linalg.norm(y1) == 0
+    assert np.all(np.isnan(Y[3]))
