@@ -390,8 +390,21 @@ def run_expert(fb, torch, args, stream, hbm_peak):
                  "k2_gate_down": n_kept * REC_BYTES + 8 * DH, "fused": bytes_tok}.get(k)
             kernels[k] = {"avg_us": round(avg * 1e3, 3),
                           "gbs": round(b / (avg * 1e-3) / 1e9, 1) if b and avg > 0 else None}
+    # config 4 (started): 16 tokens at once through the batched expert forward
+    # (tcgen05 up projection + union gate/down) on the same experts
+    B4 = 16
+    X4 = torch.stack([fb.gen_normals(1, (1 << 40) + t, DH) for t in range(B4)])
+    step4 = lambda i: fb.expert_forward_batched(exs[i % N_EXPERTS_C1], X4)  # noqa: E731
+    n4 = max(4, args.steps // 8)
+    time_region(torch, step4, 3, stream)
+    ms4 = time_region(torch, step4, n4, stream) / n4
+    batched = {"workload": "config4 (expert level): 16 tokens, batched expert_forward_sparse",
+               "tokens": B4, "us_per_call": round(ms4 * 1e3, 2),
+               "value": round(B4 / (ms4 * 1e-3), 1), "unit": "expert-tokens/s",
+               "vs_batch1_value": round(B4 / (ms4 * 1e-3) / (1e3 / mean_ms), 3)}
     return {"workload": (f"config1: seeded_expert(4096,14336,99+j), j<{N_EXPERTS_C1} cycled, "
                          "seeded_input(4096,100), INT2 g64, k=0.8, batch 1"),
+            "batched_16": batched,
             "value": round(1e3 / mean_ms, 1), "unit": "expert-tokens/s",
             "us_per_expert_token": round(mean_ms * 1e3, 3), "kept": n_kept,
             "threshold": round(ths[0], 6), "bytes_per_expert_token": bytes_tok,
