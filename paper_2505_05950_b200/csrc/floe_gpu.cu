@@ -1082,28 +1082,29 @@ int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x, ui
                                                            uc, um);
     CK_LAUNCH();
     const __half *rec = e->host_desc.records;
-    const uint32_t csm = 4u * floe_tc::kCoefTokens * dh;
     const int sm = device_info().sm;
     if (dh == 4096) {
-      rc = set_smem(floe_tc::coeffs<4096>, csm);
-      if (rc == FLOE_OK) {
-        floe_tc::coeffs<4096><<<2 * sm, 256, csm, st>>>(rec, x, v, B, di, count, uc, um, A);
+      {
+        floe_tc::coeffs<4096><<<4 * sm, 256, 0, st>>>(rec, x, v, B, di, count, uc, um, A);
         CK(cudaMemsetAsync(y_out, 0, 4ull * B * dh, st));
-        const uint32_t dsm = 4u * floe_tc::kDownRowCap * B;
+        // row chunks of <= kDownRowCap union rows (the union is at most di)
+        const uint32_t chunks = (di + floe_tc::kDownRowCap - 1) / floe_tc::kDownRowCap;
+        const uint32_t dsm = 4u * floe_tc::kDownRowCap * ((B + 3u) & ~3u);
         rc = set_smem(floe_tc::down_accum<4096>, dsm);
         if (rc == FLOE_OK)
-          floe_tc::down_accum<4096><<<dim3(4096 / 1024, floe_tc::kDownRowChunks), 256, dsm, st>>>(
+          floe_tc::down_accum<4096><<<dim3(4096 / 1024, chunks), 256, dsm, st>>>(
               rec, B, count, uc, A, y_out);
       }
     } else {
-      rc = set_smem(floe_tc::coeffs<2048>, csm);
-      if (rc == FLOE_OK) {
-        floe_tc::coeffs<2048><<<2 * sm, 256, csm, st>>>(rec, x, v, B, di, count, uc, um, A);
+      {
+        floe_tc::coeffs<2048><<<4 * sm, 256, 0, st>>>(rec, x, v, B, di, count, uc, um, A);
         CK(cudaMemsetAsync(y_out, 0, 4ull * B * dh, st));
-        const uint32_t dsm = 4u * floe_tc::kDownRowCap * B;
+        // row chunks of <= kDownRowCap union rows (the union is at most di)
+        const uint32_t chunks = (di + floe_tc::kDownRowCap - 1) / floe_tc::kDownRowCap;
+        const uint32_t dsm = 4u * floe_tc::kDownRowCap * ((B + 3u) & ~3u);
         rc = set_smem(floe_tc::down_accum<2048>, dsm);
         if (rc == FLOE_OK)
-          floe_tc::down_accum<2048><<<dim3(2048 / 1024, floe_tc::kDownRowChunks), 256, dsm, st>>>(
+          floe_tc::down_accum<2048><<<dim3(2048 / 1024, chunks), 256, dsm, st>>>(
               rec, B, count, uc, A, y_out);
       }
     }

@@ -456,10 +456,9 @@ __global__ void __launch_bounds__(kBThreads, 1) k1_batched(const BatchedArgs a) 
 // ties and NaN kept); the union of kept channels is read once.
 //   union_masks: per channel a token bitmask; kept channels appended to a list
 //   coeffs:      A[u][t] = silu(gate_c . x_t) * v[t][c] for the tokens keeping c
-//                (la.cpp:25-31), one warp per union channel, x in shared memory
+//                (la.cpp:25-31), one warp per union channel, x from L2
 //   down_accum:  y[t][j] = sum_u A[u][t] * down_c[j], CTAs over (1024-column
 //                chunk, union-row chunk), partial sums added into y
-constexpr int kCoefTokens = 8;  // tokens per shared-memory pass of coeffs
 
 __global__ void __launch_bounds__(256) union_masks(const float *__restrict__ v, uint32_t B,
                                                    uint32_t di, float thr,
@@ -486,50 +485,39 @@ __global__ void __launch_bounds__(256) coeffs(const __half *__restrict__ records
                                               const uint32_t *__restrict__ uc,
                                               const unsigned long long *__restrict__ um,
                                               float *__restrict__ A /* [n][B] */) {
-  extern __shared__ __align__(16) float xs[];  // [kCoefTokens][DH]
+  // one warp per union channel, one pass: the gate row stays in registers and
+  // each keeping token's x streams from L2 (x is B x 16 KB, shared by all SMs)
   const uint32_t n = *count, lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  for (uint32_t t0 = 0; t0 < B; t0 += kCoefTokens) {
-    const uint32_t tb = min((uint32_t)kCoefTokens, B - t0);
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < tb * DH / 4u; i += blockDim.x)
-      reinterpret_cast<float4 *>(xs)[i] = reinterpret_cast<const float4 *>(x + (size_t)t0 * DH)[i];
-    __syncthreads();
-    for (uint32_t u = blockIdx.x * 8u + warp; u < n; u += gridDim.x * 8u) {
-      const uint32_t c = uc[u];
-      const unsigned long long m = (um[u] >> t0) & ((tb < 64u ? (1ull << tb) : 0ull) - 1ull);
-      if (!m) {  // no token of this group keeps channel c
-        if (lane < tb) A[(size_t)u * B + t0 + lane] = 0.0f;
-        continue;
+  for (uint32_t u = blockIdx.x * 8u + warp; u < n; u += gridDim.x * 8u) {
+    const uint32_t c = uc[u];
+    const unsigned long long m = um[u];
+    const uint4 *g4 = reinterpret_cast<const uint4 *>(records + (size_t)c * 2 * DH);
+    uint4 gr[DH / 256];
+#pragma unroll
+    for (int i = 0; i < DH / 256; ++i) gr[i] = __ldg(g4 + lane + 32 * i);
+    for (uint32_t t = lane; t < B; t += 32u)
+      if (!((m >> t) & 1ull)) A[(size_t)u * B + t] = 0.0f;
+    for (unsigned long long mm = m; mm; mm &= mm - 1) {
+      const uint32_t tt = (uint32_t)__ffsll((long long)mm) - 1u;
+      const float4 *xt = reinterpret_cast<const float4 *>(x + (size_t)tt * DH);
+      float acc = 0.0f;
+#pragma unroll
+      for (int i = 0; i < DH / 256; ++i) {
+        const __half2 *h2 = reinterpret_cast<const __half2 *>(&gr[i]);
+        const float4 xa = __ldg(xt + 2 * (lane + 32 * i));
+        const float4 xb = __ldg(xt + 2 * (lane + 32 * i) + 1);
+        float2 f;
+        f = __half22float2(h2[0]); acc = fmaf(f.x, xa.x, acc); acc = fmaf(f.y, xa.y, acc);
+        f = __half22float2(h2[1]); acc = fmaf(f.x, xa.z, acc); acc = fmaf(f.y, xa.w, acc);
+        f = __half22float2(h2[2]); acc = fmaf(f.x, xb.x, acc); acc = fmaf(f.y, xb.y, acc);
+        f = __half22float2(h2[3]); acc = fmaf(f.x, xb.z, acc); acc = fmaf(f.y, xb.w, acc);
       }
-      // gate row c: DH halves, lane-strided 8-half chunks
-      const uint4 *g4 = reinterpret_cast<const uint4 *>(records + (size_t)c * 2 * DH);
-      uint4 gr[DH / 256];
 #pragma unroll
-      for (int i = 0; i < DH / 256; ++i) gr[i] = __ldg(g4 + lane + 32 * i);
-      for (unsigned long long mm = m; mm; mm &= mm - 1) {
-        const uint32_t tt = (uint32_t)__ffsll((long long)mm) - 1u;
-        const float *xt = xs + (size_t)tt * DH;
-        float acc = 0.0f;
-#pragma unroll
-        for (int i = 0; i < DH / 256; ++i) {
-          const __half2 *h2 = reinterpret_cast<const __half2 *>(&gr[i]);
-          const float4 xa = *reinterpret_cast<const float4 *>(xt + 8 * (lane + 32 * i));
-          const float4 xb = *reinterpret_cast<const float4 *>(xt + 8 * (lane + 32 * i) + 4);
-          float2 f;
-          f = __half22float2(h2[0]); acc = fmaf(f.x, xa.x, acc); acc = fmaf(f.y, xa.y, acc);
-          f = __half22float2(h2[1]); acc = fmaf(f.x, xa.z, acc); acc = fmaf(f.y, xa.w, acc);
-          f = __half22float2(h2[2]); acc = fmaf(f.x, xb.x, acc); acc = fmaf(f.y, xb.y, acc);
-          f = __half22float2(h2[3]); acc = fmaf(f.x, xb.z, acc); acc = fmaf(f.y, xb.w, acc);
-        }
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) {
-          const uint32_t t = t0 + tt;
-          const float z = acc;
-          A[(size_t)u * B + t] = z / (1.0f + expf(-z)) * v[(size_t)t * di + c];  // silu(g) * v
-        }
+      for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) {
+        const float z = acc;
+        A[(size_t)u * B + tt] = z / (1.0f + expf(-z)) * v[(size_t)tt * di + c];  // silu(g) * v
       }
-      if (lane < tb && !((m >> lane) & 1ull)) A[(size_t)u * B + t0 + lane] = 0.0f;
     }
   }
 }
@@ -538,8 +526,7 @@ __global__ void __launch_bounds__(256) coeffs(const __half *__restrict__ records
 // its union rows' down halves (a warp: 256 contiguous bytes), thread = 4
 // columns x 16 tokens in registers, token groups of 16 in turn; partial sums
 // are added into y (zeroed by the caller) with vector reductions.
-constexpr int kDownRowChunks = 37;
-constexpr uint32_t kDownRowCap = 400;  // rows per chunk staged in shared memory
+constexpr uint32_t kDownRowCap = 128;  // union rows per CTA (staged in shared memory)
 
 template <int DH>
 __global__ void __launch_bounds__(256) down_accum(const __half *__restrict__ records,
@@ -550,67 +537,59 @@ __global__ void __launch_bounds__(256) down_accum(const __half *__restrict__ rec
   const uint32_t r0 = (uint32_t)(((uint64_t)n * blockIdx.y) / gridDim.y);
   const uint32_t r1 = (uint32_t)(((uint64_t)n * (blockIdx.y + 1)) / gridDim.y);
   const uint32_t col = blockIdx.x * 1024u + 4u * threadIdx.x;
-  // the chunk's channel ids and coefficients up front (shared memory): the
-  // record loads do not wait on them and the coefficients are broadcast reads
-  __shared__ uint32_t ucs[1024];
-  extern __shared__ float As[];  // [min(r1 - r0, kDownRowCap)][B]
-  const uint32_t nr = min(r1 - r0, 1024u);
-  const uint32_t na = min(r1 - r0, kDownRowCap);
+  // the chunk's channel ids and coefficients (row stride padded to 4 tokens)
+  // in shared memory: record loads do not wait on them, coefficients are
+  // broadcast 16-byte reads
+  __shared__ uint32_t ucs[kDownRowCap];
+  extern __shared__ __align__(16) float As[];  // [r1 - r0][B4]
+  const uint32_t B4 = (B + 3u) & ~3u;
+  const uint32_t nr = r1 - r0;  // <= kDownRowCap (host sizes the grid for it)
   for (uint32_t i = threadIdx.x; i < nr; i += blockDim.x) ucs[i] = uc[r0 + i];
-  for (uint32_t i = threadIdx.x; i < na * B; i += blockDim.x) As[i] = A[(size_t)r0 * B + i];
+  for (uint32_t i = threadIdx.x; i < nr * B4; i += blockDim.x) {
+    const uint32_t r = i / B4, t = i % B4;
+    As[i] = t < B ? A[(size_t)(r0 + r) * B + t] : 0.0f;
+  }
   __syncthreads();
-  auto coef = [&](uint32_t u, uint32_t t) {
-    return u - r0 < na ? As[(u - r0) * B + t] : __ldg(A + (size_t)u * B + t);
-  };
-  auto chan = [&](uint32_t u) { return u - r0 < nr ? ucs[u - r0] : uc[u]; };
-  for (uint32_t tg = 0; tg < B; tg += 16u) {
-    const uint32_t nt = min(16u, B - tg);
-    float acc[16][4];
+  for (uint32_t tg = 0; tg < B4; tg += 16u) {
+    const uint32_t nq = min(4u, (B4 - tg) / 4u);  // token quads in this group
+    float2 acc[16][2];
 #pragma unroll
-    for (int t = 0; t < 16; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.0f;
-    uint32_t u = r0;
-    for (; u + 8u <= r1; u += 8u) {  // eight rows' loads in flight
-      uint2 d[8];
+    for (int t = 0; t < 16; ++t) acc[t][0] = acc[t][1] = make_float2(0.0f, 0.0f);
+    auto row = [&](uint32_t r, uint2 d) {
+      const float2 d01 = __half22float2(*reinterpret_cast<const __half2 *>(&d.x));
+      const float2 d23 = __half22float2(*reinterpret_cast<const __half2 *>(&d.y));
+      const float4 *aq = reinterpret_cast<const float4 *>(As + (size_t)r * B4 + tg);
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        d[k] = __ldg(reinterpret_cast<const uint2 *>(records + (size_t)chan(u + k) * 2 * DH + DH + col));
+      for (int q = 0; q < 4; ++q) {
+        if ((uint32_t)q < nq) {
+          const float4 a4 = aq[q];
+          const float av[4] = {a4.x, a4.y, a4.z, a4.w};
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const float2 d01 = __half22float2(*reinterpret_cast<const __half2 *>(&d[k].x));
-        const float2 d23 = __half22float2(*reinterpret_cast<const __half2 *>(&d[k].y));
-#pragma unroll
-        for (int t = 0; t < 16; ++t) {
-          if ((uint32_t)t < nt) {
-            const float a = coef(u + k, tg + t);
-            acc[t][0] = fmaf(a, d01.x, acc[t][0]);
-            acc[t][1] = fmaf(a, d01.y, acc[t][1]);
-            acc[t][2] = fmaf(a, d23.x, acc[t][2]);
-            acc[t][3] = fmaf(a, d23.y, acc[t][3]);
+          for (int k = 0; k < 4; ++k) {
+            const float2 a2 = make_float2(av[k], av[k]);
+            acc[4 * q + k][0] = __ffma2_rn(a2, d01, acc[4 * q + k][0]);
+            acc[4 * q + k][1] = __ffma2_rn(a2, d23, acc[4 * q + k][1]);
           }
         }
       }
-    }
-    for (; u < r1; ++u) {
-      const uint2 d = __ldg(reinterpret_cast<const uint2 *>(records + (size_t)chan(u) * 2 * DH + DH + col));
-      const float2 d01 = __half22float2(*reinterpret_cast<const __half2 *>(&d.x));
-      const float2 d23 = __half22float2(*reinterpret_cast<const __half2 *>(&d.y));
+    };
+    uint32_t r = 0;
+    for (; r + 8u <= nr; r += 8u) {  // eight rows' loads in flight
+      uint2 d[8];
 #pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        if ((uint32_t)t < nt) {
-          const float a = coef(u, tg + t);
-          acc[t][0] = fmaf(a, d01.x, acc[t][0]);
-          acc[t][1] = fmaf(a, d01.y, acc[t][1]);
-          acc[t][2] = fmaf(a, d23.x, acc[t][2]);
-          acc[t][3] = fmaf(a, d23.y, acc[t][3]);
-        }
-      }
+      for (int k = 0; k < 8; ++k)
+        d[k] = __ldg(reinterpret_cast<const uint2 *>(records + (size_t)ucs[r + k] * 2 * DH + DH + col));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) row(r + k, d[k]);
     }
-    if (r1 > r0)
+    for (; r < nr; ++r)
+      row(r, __ldg(reinterpret_cast<const uint2 *>(records + (size_t)ucs[r] * 2 * DH + DH + col)));
+    if (nr > 0)
 #pragma unroll
       for (int t = 0; t < 16; ++t)
-        if ((uint32_t)t < nt)
-          floe_k::red_add_v4(y + (size_t)(tg + t) * DH + col, acc[t][0], acc[t][1], acc[t][2],
-                             acc[t][3]);
+        if (tg + (uint32_t)t < B)
+          floe_k::red_add_v4(y + (size_t)(tg + t) * DH + col, acc[t][0].x, acc[t][0].y,
+                             acc[t][1].x, acc[t][1].y);
   }
 }
 
