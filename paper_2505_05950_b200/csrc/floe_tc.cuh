@@ -160,16 +160,21 @@ constexpr int kBThreads = 32 * (kConsumerWarps + 2);  // + MMA warp + copy warp
 constexpr int kPS = 4;   // packed ring stages
 constexpr int kPPS = 4;  // span pairs per packed stage: per tile one 2 KB codes + one 512 B meta copy
 
+// Span pairs are handled in groups of ppg (2 while the 4 spans' accumulators
+// fit TMEM twice over, else 1): one unpack/arrive, one limb copy, one MMA
+// batch and one commit per group.
 struct BatchedSmem {
-  uint32_t nos, pstage, ostage, p, o, meta_batch, xs, total;
+  uint32_t ppg, sb, nos, pstage, ostage, p, o, meta_batch, xs, total;
 };
 __host__ __device__ inline BatchedSmem batched_smem(uint32_t dh, uint32_t B) {
   BatchedSmem L;
   const uint32_t Bp = padded_tokens(B), N = 3u * Bp;
-  const uint32_t SB = (512u / N) & ~1u;  // spans per TMEM batch (even)
-  L.nos = N <= 96u ? 4u : 2u;  // operand stages (A + limbs of a pair)
+  L.ppg = N <= 96u ? 2u : 1u;
+  L.sb = (512u / N) / (2u * L.ppg) * (2u * L.ppg);  // spans per TMEM batch (whole groups)
+  const uint32_t SB = L.sb;
+  L.nos = N <= 48u ? 3u : 2u;  // operand stages (A + limbs of a group)
   L.pstage = kPPS * 5120u;
-  L.ostage = (16384u + 2u * N * 64u + 1023u) & ~1023u;
+  L.ostage = (L.ppg * 16384u + L.ppg * 2u * N * 64u + 1023u) & ~1023u;
   uint32_t o = 0;
   L.o = o;            o += L.nos * L.ostage;  // 1024-aligned operand stages first
   L.p = o;            o += kPS * L.pstage;
@@ -185,14 +190,14 @@ __global__ void __launch_bounds__(kBThreads, 1) k1_batched(const BatchedArgs a) 
   constexpr uint32_t TILE_W = 5u * DH / 4u;  // u32 per tile
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t pfull[kPS], pempty[kPS];
-  __shared__ __align__(8) uint64_t xfull[4], aready[4], mdone[4], tfree;
+  __shared__ __align__(8) uint64_t xfull[3], aready[3], mdone[3], tfree;
   __shared__ uint32_t tmem_base;
   __shared__ float invS_s[kMaxTokens];
   const uint32_t t = threadIdx.x, warp = t >> 5, lane = t & 31;
   if (t == 0) tmark(a, 0);
   const uint32_t B = a.B, Bp = padded_tokens(B), N = 3u * Bp;
-  const uint32_t SB = (512u / N) & ~1u;
   const BatchedSmem L = batched_smem(DH, B);
+  const uint32_t SB = L.sb, PPG = L.ppg, NG = PAIRS / PPG;
   const uint32_t NOS = L.nos;
   const uint32_t blk = blockIdx.x, tiles_total = (a.di + 15u) / 16u, tile0 = blk * 8u;
   const uint32_t ntiles = tile0 < tiles_total ? min(8u, tiles_total - tile0) : 0u;
@@ -211,7 +216,7 @@ __global__ void __launch_bounds__(kBThreads, 1) k1_batched(const BatchedArgs a) 
       floe_ptx::mbar_init(&pfull[s], 1);
       floe_ptx::mbar_init(&pempty[s], kConsumerWarps);
     }
-    for (int o = 0; o < 4; ++o) {
+    for (int o = 0; o < 3; ++o) {
       floe_ptx::mbar_init(&xfull[o], 1);
       floe_ptx::mbar_init(&aready[o], kConsumerWarps);
       floe_ptx::mbar_init(&mdone[o], 1);
@@ -243,10 +248,10 @@ __global__ void __launch_bounds__(kBThreads, 1) k1_batched(const BatchedArgs a) 
                          &pfull[s]);
     }
   };
-  auto issue_xl = [&](uint32_t p) {
-    const uint32_t o = p % NOS;
-    floe_ptx::mbar_arrive_expect_tx(&xfull[o], 2u * N * 64u);
-    floe_ptx::bulk_g2s(ost(o) + 16384u, a.xl + (size_t)(2u * p) * N * 64u, 2u * N * 64u,
+  auto issue_xl = [&](uint32_t g) {  // limbs of group g's 2*PPG spans (contiguous)
+    const uint32_t o = g % NOS, bytes = PPG * 2u * N * 64u;
+    floe_ptx::mbar_arrive_expect_tx(&xfull[o], bytes);
+    floe_ptx::bulk_g2s(ost(o) + PPG * 16384u, a.xl + (size_t)(2u * PPG * g) * N * 64u, bytes,
                        &xfull[o]);
   };
   constexpr uint32_t QS = PAIRS / kPPS;  // packed stages in all
@@ -255,16 +260,17 @@ __global__ void __launch_bounds__(kBThreads, 1) k1_batched(const BatchedArgs a) 
     // ============================= copy warp =============================
     if (lane == 0) {
       for (uint32_t q = 0; q < min((uint32_t)kPS, QS); ++q) issue_packed(q);
-      for (uint32_t q = 0; q < min(NOS, PAIRS); ++q) issue_xl(q);
-      for (uint32_t p = 0; p < PAIRS; ++p) {
-        if (p % kPPS == kPPS - 1 && p / kPPS + kPS < QS) {  // stage p/kPPS fully unpacked
-          const uint32_t q = p / kPPS;
-          floe_ptx::mbar_wait(&pempty[q % kPS], (q / kPS) & 1u, (13u << 28) | p);
+      for (uint32_t g = 0; g < min(NOS, NG); ++g) issue_xl(g);
+      for (uint32_t g = 0; g < NG; ++g) {
+        const uint32_t plast = PPG * g + PPG - 1u;
+        if (plast % kPPS == kPPS - 1 && plast / kPPS + kPS < QS) {  // stage fully unpacked
+          const uint32_t q = plast / kPPS;
+          floe_ptx::mbar_wait(&pempty[q % kPS], (q / kPS) & 1u, (13u << 28) | g);
           issue_packed(q + kPS);
         }
-        if (p + NOS < PAIRS) {  // pair p's MMAs done: its operand stage takes pair p + NOS
-          floe_ptx::mbar_wait(&mdone[p % NOS], (p / NOS) & 1u, (14u << 28) | p);
-          issue_xl(p + NOS);
+        if (g + NOS < NG) {  // group g's MMAs done: its operand stage takes group g + NOS
+          floe_ptx::mbar_wait(&mdone[g % NOS], (g / NOS) & 1u, (14u << 28) | g);
+          issue_xl(g + NOS);
         }
       }
     }
@@ -279,25 +285,25 @@ __global__ void __launch_bounds__(kBThreads, 1) k1_batched(const BatchedArgs a) 
                ((uint64_t)(512u >> 4) << 32) | ((uint64_t)1 << 46);
       };
       uint32_t batch = 0, batch_begin = 0;
-      for (uint32_t p = 0; p < PAIRS; ++p) {
-        const uint32_t o = p % NOS;
-        if (2u * p == batch_begin + SB) {  // a new TMEM batch: wait for the epilogue
-          floe_ptx::mbar_wait(&tfree, batch & 1u, (10u << 28) | p);
+      for (uint32_t g = 0; g < NG; ++g) {
+        const uint32_t o = g % NOS, s0 = 2u * PPG * g;  // first span of the group
+        if (s0 == batch_begin + SB) {  // a new TMEM batch: wait for the epilogue
+          floe_ptx::mbar_wait(&tfree, batch & 1u, (10u << 28) | g);
           ++batch;
-          batch_begin = 2u * p;
+          batch_begin = s0;
         }
-        if (p == 8) tmark(a, 22);
-        floe_ptx::mbar_wait(&aready[o], (p / NOS) & 1u, (11u << 28) | p);
-        if (p == 0) tmark(a, 2);
-        if (p == 8) tmark(a, 23);
-        floe_ptx::mbar_wait(&xfull[o], (p / NOS) & 1u, (12u << 28) | p);
-        if (p == 0) tmark(a, 3);
-        if (p == 8) tmark(a, 24);
+        if (g == 4) tmark(a, 22);
+        floe_ptx::mbar_wait(&aready[o], (g / NOS) & 1u, (11u << 28) | g);
+        if (g == 0) tmark(a, 2);
+        if (g == 4) tmark(a, 23);
+        floe_ptx::mbar_wait(&xfull[o], (g / NOS) & 1u, (12u << 28) | g);
+        if (g == 0) tmark(a, 3);
+        if (g == 4) tmark(a, 24);
         asm volatile("tcgen05.fence::after_thread_sync;");
-        for (uint32_t sp = 0; sp < 2; ++sp) {
-          const uint32_t col = (2u * p + sp - batch_begin) * N;
-          const uint32_t a0 = floe_ptx::smem_u32(ost(o) + sp * 8192u);
-          const uint32_t b0 = floe_ptx::smem_u32(ost(o) + 16384u + sp * N * 64u);
+        for (uint32_t sg = 0; sg < 2u * PPG; ++sg) {  // span within the group
+          const uint32_t col = (s0 + sg - batch_begin) * N;
+          const uint32_t a0 = floe_ptx::smem_u32(ost(o) + sg * 8192u);
+          const uint32_t b0 = floe_ptx::smem_u32(ost(o) + PPG * 16384u + sg * N * 64u);
           for (uint32_t kh = 0; kh < 2; ++kh) {
             const uint64_t da = desc(a0 + kh * 256u), db = desc(b0 + kh * 256u);
             asm volatile(
@@ -308,7 +314,7 @@ __global__ void __launch_bounds__(kBThreads, 1) k1_batched(const BatchedArgs a) 
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
             floe_ptx::smem_u32(&mdone[o])));
-        if (p == 8) tmark(a, 25);
+        if (g == 4) tmark(a, 25);
       }
     }
     __syncwarp();
@@ -326,49 +332,51 @@ __global__ void __launch_bounds__(kBThreads, 1) k1_batched(const BatchedArgs a) 
 #pragma unroll
     for (int i = 0; i < 16; ++i) acc1[i] = acc2[i] = 0.0f;
     uint32_t batch = 0, batch_begin = 0;
-    for (uint32_t p = 0; p < PAIRS; ++p) {
-      const uint32_t q = p / kPPS, pp = p % kPPS, s = q % kPS, o = p % NOS;
-      if (t == 0 && p == 8) tmark(a, 19);
-      floe_ptx::mbar_wait(&pfull[s], (q / kPS) & 1u, (15u << 28) | p);
-      if (t == 0 && p == 8) tmark(a, 27);
-      if (p >= NOS)  // A[o] free: MMAs of pair p - NOS done
-        floe_ptx::mbar_wait(&mdone[o], ((p / NOS) - 1u) & 1u, (16u << 28) | p);
-      if (t == 0 && p == 8) tmark(a, 28);
+    for (uint32_t g = 0; g < NG; ++g) {
+      const uint32_t p0 = PPG * g, q = p0 / kPPS, s = q % kPS, o = g % NOS;
+      if (t == 0 && g == 4) tmark(a, 19);
+      floe_ptx::mbar_wait(&pfull[s], (q / kPS) & 1u, (15u << 28) | g);  // (a group lies in one stage)
+      if (t == 0 && g == 4) tmark(a, 27);
+      if (g >= NOS)  // A[o] free: MMAs of group g - NOS done
+        floe_ptx::mbar_wait(&mdone[o], ((g / NOS) - 1u) & 1u, (16u << 28) | g);
+      if (t == 0 && g == 4) tmark(a, 28);
       {
-        const uint32_t *cw = reinterpret_cast<const uint32_t *>(pst(s) + pp * 512u);
         uint8_t *A = ost(o);
-        if (t < 8u * 32u) {  // thread = (tile j, lane ln): its 4 code words
-          const uint32_t j = t >> 5, ln = t & 31u, g = ln >> 2, chunk = ln & 3u;
+        if (t < PPG * 256u) {  // thread = (pair of the group, tile j, lane ln): 4 code words
+          const uint32_t pg = t >> 8, j = (t >> 5) & 7u, ln = t & 31u, g8 = ln >> 2, chunk = ln & 3u;
+          const uint32_t pp = (p0 + pg) % kPPS;
+          const uint32_t *cw = reinterpret_cast<const uint32_t *>(pst(s) + pp * 512u);
           const uint4 w4 = *reinterpret_cast<const uint4 *>(cw + j * (kPPS * 128u) + 4u * ln);
           const uint32_t ws[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
-          for (uint32_t k = 0; k < 4; ++k) {  // slot k: row g + 8(k&1), span k>>1
-            const uint32_t w = ws[k], r = 16u * j + g + 8u * (k & 1u);
+          for (uint32_t k = 0; k < 4; ++k) {  // slot k: row g8 + 8(k&1), span k>>1
+            const uint32_t w = ws[k], r = 16u * j + g8 + 8u * (k & 1u);
             const uint4 ov = make_uint4(w & 0x03030303u, (w >> 2) & 0x03030303u,
                                         (w >> 4) & 0x03030303u, (w >> 6) & 0x03030303u);
-            *reinterpret_cast<uint4 *>(A + (k >> 1) * 8192u + kmaj_off(r, 16u * chunk)) = ov;
+            *reinterpret_cast<uint4 *>(A + pg * 16384u + (k >> 1) * 8192u + kmaj_off(r, 16u * chunk)) = ov;
           }
         }
-        const uint32_t *mw = reinterpret_cast<const uint32_t *>(pst(s) + kPPS * 4096u + pp * 128u);
-        if (t >= 8u * 32u && t < 16u * 32u) {
-          const uint32_t tm = t - 8u * 32u;
-          const uint32_t j = tm >> 5, mq = tm & 31u, k = mq & 3u, g = mq >> 2;
-          const uint32_t r = 16u * j + g + 8u * (k & 1u), sp = k >> 1;
-          meta_batch[(2u * p + sp - batch_begin) * 128u + r] = mw[j * (kPPS * 32u) + mq];
+        for (uint32_t i = t; i < PPG * 256u; i += 32u * kConsumerWarps) {  // meta -> batch table
+          const uint32_t pg = i >> 8, tm = i & 255u;
+          const uint32_t pp = (p0 + pg) % kPPS;
+          const uint32_t *mw = reinterpret_cast<const uint32_t *>(pst(s) + kPPS * 4096u + pp * 128u);
+          const uint32_t j = tm >> 5, mq = tm & 31u, k = mq & 3u, g8 = mq >> 2;
+          const uint32_t r = 16u * j + g8 + 8u * (k & 1u), sp = k >> 1;
+          meta_batch[(2u * (p0 + pg) + sp - batch_begin) * 128u + r] = mw[j * (kPPS * 32u) + mq];
         }
       }
       asm volatile("fence.proxy.async.shared::cta;");  // generic writes -> tensor-core reads
       __syncwarp();
       if (lane == 0) {
-        if (pp == kPPS - 1) floe_ptx::mbar_arrive(&pempty[s]);
+        if ((p0 + PPG - 1u) % kPPS == kPPS - 1) floe_ptx::mbar_arrive(&pempty[s]);
         floe_ptx::mbar_arrive(&aready[o]);
       }
-      if (t == 0 && p == 8) tmark(a, 29);
-      const uint32_t span_end = 2u * p + 2u;
-      if (span_end - batch_begin == SB || p + 1 == PAIRS) {
-        // all MMAs of the batch are done when pair p's commit fires
+      if (t == 0 && g == 4) tmark(a, 29);
+      const uint32_t span_end = 2u * PPG * (g + 1u);
+      if (span_end - batch_begin == SB || g + 1 == NG) {
+        // all MMAs of the batch are done when group g's commit fires
         if (t == 0 && batch < 12) tmark(a, 4 + 2 * (int)batch);
-        floe_ptx::mbar_wait(&mdone[o], (p / NOS) & 1u, (17u << 28) | p);
+        floe_ptx::mbar_wait(&mdone[o], (g / NOS) & 1u, (17u << 28) | g);
         asm volatile("bar.sync 1, %0;" ::"n"(32 * kConsumerWarps));  // meta_batch complete
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (ep) {
