@@ -22,3 +22,9 @@ clean:
 	$(MAKE) -C oracle clean
 
 .PHONY: all oracle clean
+
+# Sanitizer build: same sources, a 600 s barrier watchdog (compute-sanitizer
+# slows the kernels by orders of magnitude), separate output used through
+# FLOE_LIB=tools/libfloe_b200_sanitize.so.
+tools/libfloe_b200_sanitize.so: $(SRCS) $(HDRS)
+	$(NVCC) $(NVFLAGS) -DFLOE_WATCHDOG_NS=600000000000ull -shared -cudart static -o $@ $(SRCS) 2> /dev/null
