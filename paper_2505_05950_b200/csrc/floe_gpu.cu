@@ -1064,10 +1064,12 @@ int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x, ui
     return fail(FLOE_ERR_INVALID, "expert_forward_batched: at most %d tokens", floe_tc::kMaxTokens);
   cudaStream_t st = S(stream);
   const uint32_t B = n_tokens, di = e->di, dh = e->dh;
-  // scratch: count | v [B][di] | uc [di] | um [di] | A [di][B]
+  // scratch: count | v [B][di] | uc [di] | um [di] | A [di][B] | x hi/lo table
   const size_t o_v = 256, o_uc = o_v + ((4ull * B * di + 255) & ~size_t(255));
   const size_t o_um = o_uc + ((4ull * di + 255) & ~size_t(255));
-  const size_t o_a = o_um + 8ull * di, total = o_a + 4ull * di * B;
+  const size_t o_a = o_um + 8ull * di;
+  const size_t o_xh = (o_a + 4ull * di * B + 1023) & ~size_t(1023);
+  const size_t total = o_xh + (size_t)(dh / 64) * floe_tc::gemm_n(B) * 128u;
   uint8_t *scratch = nullptr;
   CK(cudaMallocAsync(reinterpret_cast<void **>(&scratch), total, st));
   uint32_t *count = reinterpret_cast<uint32_t *>(scratch);
@@ -1075,6 +1077,15 @@ int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x, ui
   uint32_t *uc = reinterpret_cast<uint32_t *>(scratch + o_uc);
   unsigned long long *um = reinterpret_cast<unsigned long long *>(scratch + o_um);
   float *A = reinterpret_cast<float *>(scratch + o_a);
+  uint8_t *xh = scratch + o_xh;
+  // gate dots: a tcgen05 GEMM over 128-channel blocks pays off from about 16
+  // tokens (fixed cost ~40 us per block); fewer tokens use the CUDA-core warps.
+  // FLOE_GATE_TC=0/1 forces either.
+  static const int gate_env = [] {
+    const char *p = std::getenv("FLOE_GATE_TC");
+    return p ? std::atoi(p) : -1;
+  }();
+  const bool tc_gate = gate_env >= 0 ? gate_env != 0 : B > 16;
   int rc = floe_gpu_qgemv_channels_batched(e, x, B, v, stream);
   if (rc == FLOE_OK) {
     CK(cudaMemsetAsync(count, 0, 4, st));
@@ -1085,7 +1096,16 @@ int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x, ui
     const int sm = device_info().sm;
     if (dh == 4096) {
       {
-        floe_tc::coeffs<4096><<<4 * sm, 256, 0, st>>>(rec, x, v, B, di, count, uc, um, A);
+        if (tc_gate) {
+          floe_tc::x_hilo<<<4096 / 64, 256, 0, st>>>(x, 4096, B, xh);
+          const uint32_t gsm = floe_tc::kGemmStages * (16384u + floe_tc::gemm_n(B) * 128u);
+          rc = set_smem(floe_tc::gate_gemm<4096>, gsm);
+          if (rc == FLOE_OK)
+            floe_tc::gate_gemm<4096><<<(di + 127) / 128, 128, gsm, st>>>(rec, xh, v, B, di, count,
+                                                                       uc, um, A);
+        } else {
+          floe_tc::coeffs<4096><<<4 * sm, 256, 0, st>>>(rec, x, v, B, di, count, uc, um, A);
+        }
         CK(cudaMemsetAsync(y_out, 0, 4ull * B * dh, st));
         // row chunks of <= kDownRowCap union rows (the union is at most di)
         const uint32_t chunks = (di + floe_tc::kDownRowCap - 1) / floe_tc::kDownRowCap;
@@ -1097,7 +1117,16 @@ int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x, ui
       }
     } else {
       {
-        floe_tc::coeffs<2048><<<4 * sm, 256, 0, st>>>(rec, x, v, B, di, count, uc, um, A);
+        if (tc_gate) {
+          floe_tc::x_hilo<<<2048 / 64, 256, 0, st>>>(x, 2048, B, xh);
+          const uint32_t gsm = floe_tc::kGemmStages * (16384u + floe_tc::gemm_n(B) * 128u);
+          rc = set_smem(floe_tc::gate_gemm<2048>, gsm);
+          if (rc == FLOE_OK)
+            floe_tc::gate_gemm<2048><<<(di + 127) / 128, 128, gsm, st>>>(rec, xh, v, B, di, count,
+                                                                       uc, um, A);
+        } else {
+          floe_tc::coeffs<2048><<<4 * sm, 256, 0, st>>>(rec, x, v, B, di, count, uc, um, A);
+        }
         CK(cudaMemsetAsync(y_out, 0, 4ull * B * dh, st));
         // row chunks of <= kDownRowCap union rows (the union is at most di)
         const uint32_t chunks = (di + floe_tc::kDownRowCap - 1) / floe_tc::kDownRowCap;

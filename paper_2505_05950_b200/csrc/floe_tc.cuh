@@ -530,6 +530,154 @@ __global__ void __launch_bounds__(256) coeffs(const __half *__restrict__ records
   }
 }
 
+// ---------------------------------------------- gate GEMM on tcgen05 (f16)
+// G[u][t] = gate_{c_u} . x_t for 128 union channels per CTA as one tensor-core
+// GEMM: A = the channels' f16 gate rows (gathered with cp.async, K-major
+// SWIZZLE_NONE, LBO 128 B / SBO 1024 B), B = x split into f16 hi + lo (x =
+// hi + lo to ~22 bits, rows 2t and 2t+1), D f32 in TMEM; g = D[2t] + D[2t+1].
+// 64-element K chunks through a 4-stage ring; then A[u][t] = silu(g) * v.
+constexpr int kGemmStages = 4;
+
+__host__ __device__ constexpr uint32_t gemm_n(uint32_t B) { return 2u * ((B + 7u) / 8u * 8u); }
+
+__device__ __forceinline__ uint32_t kmaj_off128(uint32_t row, uint32_t kbyte) {
+  return (row & 7u) * 16u + (kbyte & 15u) + (kbyte >> 4) * 128u + (row >> 3) * 1024u;
+}
+
+// x -> hi/lo table [chunk][N rows][128 B] in the B-operand layout.  Grid: chunks.
+__global__ void __launch_bounds__(256) x_hilo(const float *__restrict__ x, uint32_t dh, uint32_t B,
+                                              uint8_t *__restrict__ xh) {
+  const uint32_t ch = blockIdx.x, N = gemm_n(B);
+  uint8_t *out = xh + (size_t)ch * N * 128u;
+  for (uint32_t i = threadIdx.x; i < (N / 2u) * 64u; i += blockDim.x) {
+    const uint32_t t = i / 64u, e = i % 64u;
+    __half hi = __float2half_rn(0.0f), lo = hi;
+    if (t < B) {
+      const float xv = x[(size_t)t * dh + 64u * ch + e];
+      hi = __float2half_rn(xv);
+      lo = __float2half_rn(xv - __half2float(hi));
+    }
+    *reinterpret_cast<__half *>(out + kmaj_off128(2u * t, 2u * e)) = hi;
+    *reinterpret_cast<__half *>(out + kmaj_off128(2u * t + 1u, 2u * e)) = lo;
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(floe_ptx::smem_u32(dst)), "l"(src)
+               : "memory");
+}
+
+template <int DH>
+__global__ void __launch_bounds__(128, 1) gate_gemm(const __half *__restrict__ records,
+                                                    const uint8_t *__restrict__ xh,
+                                                    const float *__restrict__ v, uint32_t B,
+                                                    uint32_t di, const uint32_t *__restrict__ count,
+                                                    const uint32_t *__restrict__ uc,
+                                                    const unsigned long long *__restrict__ um,
+                                                    float *__restrict__ A /* [n][B] */) {
+  constexpr uint32_t CHUNKS = DH / 64u;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t mdone[kGemmStages];
+  __shared__ uint32_t tmem_base;
+  __shared__ uint32_t ucs[128];
+  const uint32_t n = *count, u0 = blockIdx.x * 128u;
+  if (u0 >= n) return;
+  const uint32_t t = threadIdx.x, warp = t >> 5, lane = t & 31u;
+  const uint32_t N = gemm_n(B), nr = min(128u, n - u0);
+  const uint32_t stageA = 16384u, stage = stageA + N * 128u;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
+        floe_ptx::smem_u32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (t == 0) {
+    for (int s = 0; s < kGemmStages; ++s) floe_ptx::mbar_init(&mdone[s], 1);
+    floe_ptx::fence_barrier_init();
+  }
+  ucs[t] = t < nr ? uc[u0 + t] : uc[u0];  // rows past the union repeat a valid channel
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+  // chunk loads: A = 128 rows x 128 B (8 x 16 B per row), B = N rows x 128 B
+  auto load = [&](uint32_t c) {
+    uint8_t *st = smem + (c % kGemmStages) * stage;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t idx = t + 128u * (uint32_t)i, row = idx >> 3, kb = (idx & 7u) * 16u;
+      const uint8_t *src = reinterpret_cast<const uint8_t *>(records + (size_t)ucs[row] * 2 * DH) +
+                           128u * c + kb;
+      cp_async16(st + kmaj_off128(row, kb), src);
+    }
+    const uint8_t *xs = xh + (size_t)c * N * 128u;
+    for (uint32_t i = t; i < N * 8u; i += 128u) cp_async16(st + stageA + 16u * i, xs + 16u * i);
+  };
+  const uint32_t idesc = (1u << 4) | (0u << 7) | (0u << 10) | ((N >> 3) << 17) | ((128u >> 4) << 24);
+  auto desc = [](uint32_t saddr) -> uint64_t {
+    return (uint64_t)((saddr >> 4) & 0x3fffu) | ((uint64_t)(128u >> 4) << 16) |
+           ((uint64_t)(1024u >> 4) << 32) | ((uint64_t)1 << 46);
+  };
+  for (uint32_t c = 0; c < kGemmStages - 1; ++c) {
+    load(c);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (uint32_t c = 0; c < CHUNKS; ++c) {
+    // stage of chunk c + 3 was last read by the MMAs of chunk c - 1
+    if (c >= 1 && c + kGemmStages - 1 < CHUNKS)
+      floe_ptx::mbar_wait(&mdone[(c - 1) % kGemmStages], ((c - 1) / kGemmStages) & 1u, c);
+    if (c + kGemmStages - 1 < CHUNKS) load(c + kGemmStages - 1);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(kGemmStages - 1) : "memory");  // chunk c landed
+    asm volatile("fence.proxy.async.shared::cta;");
+    __syncthreads();
+    if (t == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t a0 = floe_ptx::smem_u32(smem + (c % kGemmStages) * stage);
+      const uint32_t b0 = a0 + stageA;
+#pragma unroll
+      for (uint32_t kk = 0; kk < 4; ++kk) {  // K = 16 halves (32 B) per instruction
+        const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
+        asm volatile(
+            "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, q;\n\t}" ::"r"(tmem),
+            "l"(desc(a0 + kk * 256u)), "l"(desc(b0 + kk * 256u)), "r"(idesc), "r"(acc));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          floe_ptx::smem_u32(&mdone[c % kGemmStages])));
+    }
+  }
+  floe_ptx::mbar_wait(&mdone[(CHUNKS - 1) % kGemmStages], ((CHUNKS - 1) / kGemmStages) & 1u, 999u);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  // epilogue: thread = union row; columns (2t, 2t+1) = x_t hi, lo
+  const uint32_t u = u0 + t;
+  const unsigned long long m = t < nr ? um[u] : 0ull;
+  const uint32_t c_ch = ucs[t];
+  for (uint32_t c0 = 0; c0 < N; c0 += 16u) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(tmem + ((warp * 32u) << 16) + c0));
+    asm volatile("tcgen05.wait::ld.sync.aligned;");
+    if (t < nr)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t tok = c0 / 2u + (uint32_t)i;
+        if (tok < B) {
+          const float z = __uint_as_float(r[2 * i]) + __uint_as_float(r[2 * i + 1]);
+          A[(size_t)u * B + tok] =
+              ((m >> tok) & 1ull) ? z / (1.0f + expf(-z)) * v[(size_t)tok * di + c_ch] : 0.0f;
+        }
+      }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+  (void)lane;
+}
+
 // Grid (DH / 1024 column chunks) x (row chunks): each CTA reads 2 KB of each of
 // its union rows' down halves (a warp: 256 contiguous bytes), thread = 4
 // columns x 16 tokens in registers, token groups of 16 in turn; partial sums

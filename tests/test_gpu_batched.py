@@ -155,3 +155,30 @@ def test_expert_forward_batched_small_and_edge(fb, torch):
             assert O.rel_l2(Y[t], y1) <= 1e-4
         assert O.rel_l2(Y[t], O.expert_forward_sparse(ref_e, X[t])) <= 1e-2 or np.linalg.norm(y1) == 0
     assert np.all(np.isnan(Y[3]))
+
+
+def test_gate_gemm_and_cuda_core_paths_agree(tmp_path):
+    """The gate dots of the batched forward run as a tcgen05 f16 GEMM (x split
+    into hi + lo halves) or on CUDA cores; both give the same outputs."""
+    import os
+    import subprocess
+    import sys
+    root = __import__("pathlib").Path(__file__).resolve().parents[1]
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, %r)\n"
+        "from oracle import oracle as O\n"
+        "import paper_2505_05950_b200 as fb\n"
+        "gate, up, down = O.seeded_expert(2048, 1040, 21)\n"
+        "q = O.quantize(up, 2, 64)\n"
+        "e = fb.GpuExpert(2048, 1040, 2, 64, q.codes, q.scales, q.zeros, gate=gate, down=down, threshold=1.0)\n"
+        "X = torch.from_numpy(np.stack([O.token_input(4, t, 2048) for t in range(24)])).cuda()\n"
+        "np.save(sys.argv[1], fb.expert_forward_batched(e, X).cpu().numpy())\n") % str(root)
+    outs = []
+    for flag in ("0", "1"):
+        f = tmp_path / f"y{flag}.npy"
+        r = subprocess.run([sys.executable, "-c", code, str(f)], cwd=root, capture_output=True,
+                           text=True, timeout=300, env=dict(os.environ, FLOE_GATE_TC=flag))
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(f))
+    for t in range(24):
+        assert O.rel_l2(outs[1][t], outs[0][t]) <= 1e-5, t
