@@ -1086,6 +1086,13 @@ int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x, ui
     return p ? std::atoi(p) : -1;
   }();
   const bool tc_gate = gate_env >= 0 ? gate_env != 0 : B > 16;
+  // down product: the tcgen05 GEMM (MN-major gathered down rows) is correct but
+  // not yet faster than the CUDA-core kernel (315 vs 221 us at B=16, 521 vs
+  // 502 at B=64): opt-in with FLOE_DOWN_TC=1
+  static const bool tc_down = [] {
+    const char *p = std::getenv("FLOE_DOWN_TC");
+    return p && std::strcmp(p, "1") == 0;
+  }();
   int rc = floe_gpu_qgemv_channels_batched(e, x, B, v, stream);
   if (rc == FLOE_OK) {
     CK(cudaMemsetAsync(count, 0, 4, st));
@@ -1109,11 +1116,21 @@ int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x, ui
         CK(cudaMemsetAsync(y_out, 0, 4ull * B * dh, st));
         // row chunks of <= kDownRowCap union rows (the union is at most di)
         const uint32_t chunks = (di + floe_tc::kDownRowCap - 1) / floe_tc::kDownRowCap;
-        const uint32_t dsm = 4u * floe_tc::kDownRowCap * ((B + 3u) & ~3u);
-        rc = set_smem(floe_tc::down_accum<4096>, dsm);
-        if (rc == FLOE_OK)
-          floe_tc::down_accum<4096><<<dim3(4096 / 1024, chunks), 256, dsm, st>>>(
-              rec, B, count, uc, A, y_out);
+        if (tc_down) {
+          const uint32_t gsm = floe_tc::kDownStages * (128u * floe_tc::kDownKChunk * 2u +
+                                                       floe_tc::kDownKChunk * 256u * 2u);
+          rc = set_smem(floe_tc::down_gemm<4096>, gsm);
+          if (rc == FLOE_OK)
+            floe_tc::down_gemm<4096><<<dim3(4096 / 256, (di + floe_tc::kDownKRange - 1) /
+                                                           floe_tc::kDownKRange),
+                                        128, gsm, st>>>(rec, B, count, uc, A, y_out);
+        } else {
+          const uint32_t dsm = 4u * floe_tc::kDownRowCap * ((B + 3u) & ~3u);
+          rc = set_smem(floe_tc::down_accum<4096>, dsm);
+          if (rc == FLOE_OK)
+            floe_tc::down_accum<4096><<<dim3(4096 / 1024, chunks), 256, dsm, st>>>(
+                rec, B, count, uc, A, y_out);
+        }
       }
     } else {
       {
@@ -1130,11 +1147,21 @@ int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x, ui
         CK(cudaMemsetAsync(y_out, 0, 4ull * B * dh, st));
         // row chunks of <= kDownRowCap union rows (the union is at most di)
         const uint32_t chunks = (di + floe_tc::kDownRowCap - 1) / floe_tc::kDownRowCap;
-        const uint32_t dsm = 4u * floe_tc::kDownRowCap * ((B + 3u) & ~3u);
-        rc = set_smem(floe_tc::down_accum<2048>, dsm);
-        if (rc == FLOE_OK)
-          floe_tc::down_accum<2048><<<dim3(2048 / 1024, chunks), 256, dsm, st>>>(
-              rec, B, count, uc, A, y_out);
+        if (tc_down) {
+          const uint32_t gsm = floe_tc::kDownStages * (128u * floe_tc::kDownKChunk * 2u +
+                                                       floe_tc::kDownKChunk * 256u * 2u);
+          rc = set_smem(floe_tc::down_gemm<2048>, gsm);
+          if (rc == FLOE_OK)
+            floe_tc::down_gemm<2048><<<dim3(2048 / 256, (di + floe_tc::kDownKRange - 1) /
+                                                           floe_tc::kDownKRange),
+                                        128, gsm, st>>>(rec, B, count, uc, A, y_out);
+        } else {
+          const uint32_t dsm = 4u * floe_tc::kDownRowCap * ((B + 3u) & ~3u);
+          rc = set_smem(floe_tc::down_accum<2048>, dsm);
+          if (rc == FLOE_OK)
+            floe_tc::down_accum<2048><<<dim3(2048 / 1024, chunks), 256, dsm, st>>>(
+                rec, B, count, uc, A, y_out);
+        }
       }
     }
     if (rc == FLOE_OK) CK_LAUNCH();

@@ -678,6 +678,144 @@ __global__ void __launch_bounds__(128, 1) gate_gemm(const __half *__restrict__ r
   (void)lane;
 }
 
+// ---------------------------------------------- down GEMM on tcgen05 (f16)
+// Y[t][m] = sum_u A[u][t] * down_{c_u}[m] for a 256-wide slice of m and a range
+// of kDownKRange union channels per CTA: M = 2 rows per token (the f32
+// coefficient split into f16 hi + lo, zero rows past 2B), N = 256 (d_hidden
+// slice), K = channels.  A (K-major) is built from the coefficients; B is the
+// gathered f16 down rows, N-contiguous per channel = the MN-major operand
+// (validated by tools/umma_f16_mn_test.cu: core matrices 8 k x 16 B of n,
+// n-adjacent 128 B apart; descriptor LBO = k-core stride, SBO = 128 B).
+// Partial sums of the channel range are added into y.
+constexpr uint32_t kDownKRange = 1024;  // union channels per CTA
+constexpr uint32_t kDownKChunk = 64;    // channels per pipeline stage
+constexpr int kDownStages = 3;
+
+template <int DH>
+__global__ void __launch_bounds__(128, 1) down_gemm(const __half *__restrict__ records,
+                                                    uint32_t B, const uint32_t *__restrict__ count,
+                                                    const uint32_t *__restrict__ uc,
+                                                    const float *__restrict__ A, float *__restrict__ y) {
+  constexpr uint32_t NS = 256;  // d_hidden columns per CTA
+  constexpr uint32_t SA = 128u * kDownKChunk * 2u;   // 16 KB: 128 rows x 64 k f16
+  constexpr uint32_t SBB = kDownKChunk * NS * 2u;    // 32 KB: 64 k x 256 n f16
+  constexpr uint32_t ST = SA + SBB;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t mdone[kDownStages];
+  __shared__ uint32_t tmem_base;
+  const uint32_t n = *count, k0 = blockIdx.y * kDownKRange;
+  if (k0 >= n) return;
+  const uint32_t m0 = blockIdx.x * NS, t = threadIdx.x, warp = t >> 5, lane = t & 31u;
+  const uint32_t nk = min(kDownKRange, n - k0), nch = (nk + kDownKChunk - 1) / kDownKChunk;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+        floe_ptx::smem_u32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (t == 0) {
+    for (int s2 = 0; s2 < kDownStages; ++s2) floe_ptx::mbar_init(&mdone[s2], 1);
+    floe_ptx::fence_barrier_init();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+  // stage c: B = down rows (cp.async gather), A = coefficient hi/lo rows
+  auto load = [&](uint32_t c) {
+    uint8_t *st = smem + (c % kDownStages) * ST;
+    const uint32_t kc0 = k0 + c * kDownKChunk;
+    // B: 64 channels x 32 pieces of 16 B (8 n each)
+    for (uint32_t i = t; i < kDownKChunk * 32u; i += 128u) {
+      const uint32_t kk = i >> 5, piece = i & 31u;
+      uint8_t *dst = st + SA + (kk & 7u) * 16u + piece * 128u + (kk >> 3) * (NS / 8u * 128u);
+      if (kc0 + kk < k0 + nk) {
+        const uint8_t *src = reinterpret_cast<const uint8_t *>(records + (size_t)uc[kc0 + kk] * 2 * DH +
+                                                               DH + m0) + 16u * piece;
+        cp_async16(dst, src);
+      } else {
+        *reinterpret_cast<uint4 *>(dst) = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+    // A: rows 2t (hi), 2t+1 (lo) for t < B; k = channel in chunk
+    for (uint32_t i = t; i < 128u * kDownKChunk; i += 128u) {
+      const uint32_t row = i / kDownKChunk, kk = i % kDownKChunk, tok = row >> 1;
+      float a = 0.0f;
+      if (tok < B && kc0 + kk < k0 + nk) a = A[(size_t)(kc0 + kk) * B + tok];
+      const __half hi = __float2half_rn(a);
+      const __half val = (row & 1u) ? __float2half_rn(a - __half2float(hi)) : hi;
+      *reinterpret_cast<__half *>(st + kmaj_off128(row, 2u * kk)) = val;
+    }
+  };
+  const uint32_t idesc = (1u << 4) | (1u << 16) | ((NS >> 3) << 17) | ((128u >> 4) << 24);
+  auto descA = [](uint32_t saddr) -> uint64_t {
+    return (uint64_t)((saddr >> 4) & 0x3fffu) | ((uint64_t)(128u >> 4) << 16) |
+           ((uint64_t)(1024u >> 4) << 32) | ((uint64_t)1 << 46);
+  };
+  auto descB = [](uint32_t saddr) -> uint64_t {
+    return (uint64_t)((saddr >> 4) & 0x3fffu) | ((uint64_t)((NS / 8u * 128u) >> 4) << 16) |
+           ((uint64_t)(128u >> 4) << 32) | ((uint64_t)1 << 46);
+  };
+  for (uint32_t c = 0; c < kDownStages - 1; ++c) {  // (empty groups keep the count uniform)
+    if (c < nch) load(c);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (uint32_t c = 0; c < nch; ++c) {
+    if (c + kDownStages - 1 < nch) {
+      if (c >= 1)  // stage of chunk c + 2 was last read by the MMAs of chunk c - 1
+        floe_ptx::mbar_wait(&mdone[(c - 1) % kDownStages], ((c - 1) / kDownStages) & 1u, c);
+      load(c + kDownStages - 1);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(kDownStages - 1) : "memory");
+    asm volatile("fence.proxy.async.shared::cta;");
+    __syncthreads();
+    if (t == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t a0 = floe_ptx::smem_u32(smem + (c % kDownStages) * ST), b0 = a0 + SA;
+#pragma unroll
+      for (uint32_t kk = 0; kk < kDownKChunk / 16u; ++kk) {
+        const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
+        asm volatile(
+            "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, q;\n\t}" ::"r"(tmem),
+            "l"(descA(a0 + kk * 256u)), "l"(descB(b0 + kk * 2u * (NS / 8u * 128u))), "r"(idesc),
+            "r"(acc));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          floe_ptx::smem_u32(&mdone[c % kDownStages])));
+    }
+  }
+  floe_ptx::mbar_wait(&mdone[(nch - 1) % kDownStages], ((nch - 1) / kDownStages) & 1u, 998u);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  // epilogue: TMEM lane = row 2t + h; the hi and lo rows are adjacent lanes
+  const uint32_t row = warp * 32u + lane, tok = row >> 1;
+  if (warp * 16u < B) {  // this warp holds tokens 16 warp .. 16 warp + 15
+    for (uint32_t c0 = 0; c0 < NS; c0 += 16u) {
+      uint32_t r[16];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+            "=r"(r[14]), "=r"(r[15])
+          : "r"(tmem + ((warp * 32u) << 16) + c0));
+      asm volatile("tcgen05.wait::ld.sync.aligned;");
+      float f[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float mine = __uint_as_float(r[i]);
+        f[i] = mine + __shfl_xor_sync(0xffffffffu, mine, 1);  // hi + lo
+      }
+      if (!(row & 1u) && tok < B)
+#pragma unroll
+        for (int i = 0; i < 16; i += 4)
+          floe_k::red_add_v4(y + (size_t)tok * DH + m0 + c0 + i, f[i], f[i + 1], f[i + 2], f[i + 3]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
 // Grid (DH / 1024 column chunks) x (row chunks): each CTA reads 2 KB of each of
 // its union rows' down halves (a warp: 256 contiguous bytes), thread = 4
 // columns x 16 tokens in registers, token groups of 16 in turn; partial sums

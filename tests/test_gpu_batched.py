@@ -158,8 +158,9 @@ def test_expert_forward_batched_small_and_edge(fb, torch):
 
 
 def test_gate_gemm_and_cuda_core_paths_agree(tmp_path):
-    """The gate dots of the batched forward run as a tcgen05 f16 GEMM (x split
-    into hi + lo halves) or on CUDA cores; both give the same outputs."""
+    """The gate dots and the down product of the batched forward run as tcgen05
+    f16 GEMMs (x / the coefficients split into hi + lo halves) or on CUDA
+    cores; all four combinations give the same outputs."""
     import os
     import subprocess
     import sys
@@ -174,11 +175,13 @@ def test_gate_gemm_and_cuda_core_paths_agree(tmp_path):
         "X = torch.from_numpy(np.stack([O.token_input(4, t, 2048) for t in range(24)])).cuda()\n"
         "np.save(sys.argv[1], fb.expert_forward_batched(e, X).cpu().numpy())\n") % str(root)
     outs = []
-    for flag in ("0", "1"):
-        f = tmp_path / f"y{flag}.npy"
+    for gate, down in (("0", "0"), ("1", "0"), ("0", "1"), ("1", "1")):
+        f = tmp_path / f"y{gate}{down}.npy"
         r = subprocess.run([sys.executable, "-c", code, str(f)], cwd=root, capture_output=True,
-                           text=True, timeout=300, env=dict(os.environ, FLOE_GATE_TC=flag))
+                           text=True, timeout=300,
+                           env=dict(os.environ, FLOE_GATE_TC=gate, FLOE_DOWN_TC=down))
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(np.load(f))
-    for t in range(24):
-        assert O.rel_l2(outs[1][t], outs[0][t]) <= 1e-5, t
+    for o in outs[1:]:
+        for t in range(24):
+            assert O.rel_l2(o[t], outs[0][t]) <= 1e-5, t
