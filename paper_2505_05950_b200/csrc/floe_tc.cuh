@@ -719,6 +719,13 @@ __global__ void __launch_bounds__(128, 1) down_gemm(const __half *__restrict__ r
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
+  // zero the A rows past 2B in every stage once (never written afterwards)
+  for (uint32_t s2 = 0; s2 < (uint32_t)kDownStages; ++s2)
+    for (uint32_t i = t; i < (128u - 2u * B) * kDownKChunk; i += 128u) {
+      const uint32_t row = 2u * B + i / kDownKChunk, kk = i % kDownKChunk;
+      *reinterpret_cast<__half *>(smem + s2 * ST + kmaj_off128(row, 2u * kk)) = __float2half_rn(0.0f);
+    }
+  __syncthreads();
   const uint32_t tmem = tmem_base;
   // stage c: B = down rows (cp.async gather), A = coefficient hi/lo rows
   auto load = [&](uint32_t c) {
@@ -736,14 +743,14 @@ __global__ void __launch_bounds__(128, 1) down_gemm(const __half *__restrict__ r
         *reinterpret_cast<uint4 *>(dst) = make_uint4(0u, 0u, 0u, 0u);
       }
     }
-    // A: rows 2t (hi), 2t+1 (lo) for t < B; k = channel in chunk
-    for (uint32_t i = t; i < 128u * kDownKChunk; i += 128u) {
-      const uint32_t row = i / kDownKChunk, kk = i % kDownKChunk, tok = row >> 1;
-      float a = 0.0f;
-      if (tok < B && kc0 + kk < k0 + nk) a = A[(size_t)(kc0 + kk) * B + tok];
-      const __half hi = __float2half_rn(a);
-      const __half val = (row & 1u) ? __float2half_rn(a - __half2float(hi)) : hi;
-      *reinterpret_cast<__half *>(st + kmaj_off128(row, 2u * kk)) = val;
+    // A: rows 2t (hi), 2t+1 (lo) for t < B (rows past 2B stay zero from the
+    // start); coefficients read token-contiguous
+    for (uint32_t i = t; i < kDownKChunk * B; i += 128u) {
+      const uint32_t kk = i / B, tok = i % B;
+      const float a = kc0 + kk < k0 + nk ? A[(size_t)kc0 * B + i] : 0.0f;
+      const __half hi = __float2half_rn(a), lo = __float2half_rn(a - __half2float(hi));
+      *reinterpret_cast<__half *>(st + kmaj_off128(2u * tok, 2u * kk)) = hi;
+      *reinterpret_cast<__half *>(st + kmaj_off128(2u * tok + 1u, 2u * kk)) = lo;
     }
   };
   const uint32_t idesc = (1u << 4) | (1u << 16) | ((NS >> 3) << 17) | ((128u >> 4) << 24);
