@@ -1069,7 +1069,8 @@ int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x, ui
   const size_t o_um = o_uc + ((4ull * di + 255) & ~size_t(255));
   const size_t o_a = o_um + 8ull * di;
   const size_t o_xh = (o_a + 4ull * di * B + 1023) & ~size_t(1023);
-  const size_t total = o_xh + (size_t)(dh / 64) * floe_tc::gemm_n(B) * 128u;
+  const size_t o_g = o_xh + (((size_t)(dh / 64) * floe_tc::gemm_n(B) * 128u + 255) & ~size_t(255));
+  const size_t total = o_g + 4ull * di * B;  // G: split-K partial gate dots
   uint8_t *scratch = nullptr;
   CK(cudaMallocAsync(reinterpret_cast<void **>(&scratch), total, st));
   uint32_t *count = reinterpret_cast<uint32_t *>(scratch);
@@ -1078,14 +1079,16 @@ int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x, ui
   unsigned long long *um = reinterpret_cast<unsigned long long *>(scratch + o_um);
   float *A = reinterpret_cast<float *>(scratch + o_a);
   uint8_t *xh = scratch + o_xh;
-  // gate dots: a tcgen05 GEMM over 128-channel blocks pays off from about 16
-  // tokens (fixed cost ~40 us per block); fewer tokens use the CUDA-core warps.
+  float *Gp = reinterpret_cast<float *>(scratch + o_g);
+  constexpr uint32_t kGateSplit = 4;  // K parts of the gate GEMM (CTAs = 4 x 128-row blocks)
+  // gate dots: a tcgen05 GEMM (128-channel blocks, K split in 4) pays off from
+  // about 16 tokens; fewer tokens use the CUDA-core warps.
   // FLOE_GATE_TC=0/1 forces either.
   static const int gate_env = [] {
     const char *p = std::getenv("FLOE_GATE_TC");
     return p ? std::atoi(p) : -1;
   }();
-  const bool tc_gate = gate_env >= 0 ? gate_env != 0 : B > 16;
+  const bool tc_gate = gate_env >= 0 ? gate_env != 0 : B >= 16;
   // down product: the tcgen05 GEMM (MN-major gathered down rows) wins from
   // about 64 tokens (451 vs 502 us at B=64; 272 vs 221 at B=16);
   // FLOE_DOWN_TC=0/1 forces either
@@ -1109,8 +1112,12 @@ int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x, ui
           const uint32_t gsm = floe_tc::kGemmStages * (16384u + floe_tc::gemm_n(B) * 128u);
           rc = set_smem(floe_tc::gate_gemm<4096>, gsm);
           if (rc == FLOE_OK)
-            floe_tc::gate_gemm<4096><<<(di + 127) / 128, 128, gsm, st>>>(rec, xh, v, B, di, count,
-                                                                       uc, um, A);
+          {
+            CK(cudaMemsetAsync(Gp, 0, 4ull * di * B, st));
+            floe_tc::gate_gemm<4096><<<dim3((di + 127) / 128, kGateSplit), 128, gsm, st>>>(
+                rec, xh, v, B, di, count, uc, um, A, Gp);
+            floe_tc::gate_finish<<<4 * sm, 256, 0, st>>>(Gp, v, B, di, count, uc, um, A);
+          }
         } else {
           floe_tc::coeffs<4096><<<4 * sm, 256, 0, st>>>(rec, x, v, B, di, count, uc, um, A);
         }
@@ -1140,8 +1147,12 @@ int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x, ui
           const uint32_t gsm = floe_tc::kGemmStages * (16384u + floe_tc::gemm_n(B) * 128u);
           rc = set_smem(floe_tc::gate_gemm<2048>, gsm);
           if (rc == FLOE_OK)
-            floe_tc::gate_gemm<2048><<<(di + 127) / 128, 128, gsm, st>>>(rec, xh, v, B, di, count,
-                                                                       uc, um, A);
+          {
+            CK(cudaMemsetAsync(Gp, 0, 4ull * di * B, st));
+            floe_tc::gate_gemm<2048><<<dim3((di + 127) / 128, kGateSplit), 128, gsm, st>>>(
+                rec, xh, v, B, di, count, uc, um, A, Gp);
+            floe_tc::gate_finish<<<4 * sm, 256, 0, st>>>(Gp, v, B, di, count, uc, um, A);
+          }
         } else {
           floe_tc::coeffs<2048><<<4 * sm, 256, 0, st>>>(rec, x, v, B, di, count, uc, um, A);
         }

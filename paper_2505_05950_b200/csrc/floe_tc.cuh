@@ -574,8 +574,13 @@ __global__ void __launch_bounds__(128, 1) gate_gemm(const __half *__restrict__ r
                                                     uint32_t di, const uint32_t *__restrict__ count,
                                                     const uint32_t *__restrict__ uc,
                                                     const unsigned long long *__restrict__ um,
-                                                    float *__restrict__ A /* [n][B] */) {
+                                                    float *__restrict__ A /* [n][B] */,
+                                                    float *__restrict__ G /* split K: [n][B] */) {
+  // K (d_hidden) split over gridDim.y CTAs: each adds its partial dot into G,
+  // gate_finish applies silu * v; with one part the epilogue does it directly
   constexpr uint32_t CHUNKS = DH / 64u;
+  const uint32_t c_lo = CHUNKS * blockIdx.y / gridDim.y, c_hi = CHUNKS * (blockIdx.y + 1) / gridDim.y;
+  const uint32_t NCH = c_hi - c_lo;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t mdone[kGemmStages];
   __shared__ uint32_t tmem_base;
@@ -600,8 +605,9 @@ __global__ void __launch_bounds__(128, 1) gate_gemm(const __half *__restrict__ r
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base;
   // chunk loads: A = 128 rows x 128 B (8 x 16 B per row), B = N rows x 128 B
-  auto load = [&](uint32_t c) {
-    uint8_t *st = smem + (c % kGemmStages) * stage;
+  auto load = [&](uint32_t j) {  // local chunk j = global chunk c_lo + j
+    const uint32_t c = c_lo + j;
+    uint8_t *st = smem + (j % kGemmStages) * stage;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint32_t idx = t + 128u * (uint32_t)i, row = idx >> 3, kb = (idx & 7u) * 16u;
@@ -618,14 +624,14 @@ __global__ void __launch_bounds__(128, 1) gate_gemm(const __half *__restrict__ r
            ((uint64_t)(1024u >> 4) << 32) | ((uint64_t)1 << 46);
   };
   for (uint32_t c = 0; c < kGemmStages - 1; ++c) {
-    load(c);
+    if (c < NCH) load(c);
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  for (uint32_t c = 0; c < CHUNKS; ++c) {
+  for (uint32_t c = 0; c < NCH; ++c) {
     // stage of chunk c + 3 was last read by the MMAs of chunk c - 1
-    if (c >= 1 && c + kGemmStages - 1 < CHUNKS)
+    if (c >= 1 && c + kGemmStages - 1 < NCH)
       floe_ptx::mbar_wait(&mdone[(c - 1) % kGemmStages], ((c - 1) / kGemmStages) & 1u, c);
-    if (c + kGemmStages - 1 < CHUNKS) load(c + kGemmStages - 1);
+    if (c + kGemmStages - 1 < NCH) load(c + kGemmStages - 1);
     asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_group %0;" ::"n"(kGemmStages - 1) : "memory");  // chunk c landed
     asm volatile("fence.proxy.async.shared::cta;");
@@ -646,7 +652,7 @@ __global__ void __launch_bounds__(128, 1) gate_gemm(const __half *__restrict__ r
           floe_ptx::smem_u32(&mdone[c % kGemmStages])));
     }
   }
-  floe_ptx::mbar_wait(&mdone[(CHUNKS - 1) % kGemmStages], ((CHUNKS - 1) / kGemmStages) & 1u, 999u);
+  floe_ptx::mbar_wait(&mdone[(NCH - 1) % kGemmStages], ((NCH - 1) / kGemmStages) & 1u, 999u);
   asm volatile("tcgen05.fence::after_thread_sync;");
   // epilogue: thread = union row; columns (2t, 2t+1) = x_t hi, lo
   const uint32_t u = u0 + t;
@@ -667,8 +673,11 @@ __global__ void __launch_bounds__(128, 1) gate_gemm(const __half *__restrict__ r
         const uint32_t tok = c0 / 2u + (uint32_t)i;
         if (tok < B) {
           const float z = __uint_as_float(r[2 * i]) + __uint_as_float(r[2 * i + 1]);
-          A[(size_t)u * B + tok] =
-              ((m >> tok) & 1ull) ? z / (1.0f + expf(-z)) * v[(size_t)tok * di + c_ch] : 0.0f;
+          if (gridDim.y > 1)
+            atomicAdd(G + (size_t)u * B + tok, z);
+          else
+            A[(size_t)u * B + tok] =
+                ((m >> tok) & 1ull) ? z / (1.0f + expf(-z)) * v[(size_t)tok * di + c_ch] : 0.0f;
         }
       }
   }
@@ -676,6 +685,21 @@ __global__ void __launch_bounds__(128, 1) gate_gemm(const __half *__restrict__ r
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
   (void)lane;
+}
+
+// A[u][t] = silu(G[u][t]) * v[t][c_u] for the tokens keeping c_u, else 0.
+__global__ void __launch_bounds__(256) gate_finish(const float *__restrict__ G,
+                                                   const float *__restrict__ v, uint32_t B,
+                                                   uint32_t di, const uint32_t *__restrict__ count,
+                                                   const uint32_t *__restrict__ uc,
+                                                   const unsigned long long *__restrict__ um,
+                                                   float *__restrict__ A) {
+  const uint32_t n = *count;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n * B; i += gridDim.x * blockDim.x) {
+    const uint32_t u = i / B, tok = i % B;
+    const float z = G[i];
+    A[i] = ((um[u] >> tok) & 1ull) ? z / (1.0f + expf(-z)) * v[(size_t)tok * di + uc[u]] : 0.0f;
+  }
 }
 
 // ---------------------------------------------- down GEMM on tcgen05 (f16)
