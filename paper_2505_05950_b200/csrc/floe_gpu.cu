@@ -1089,14 +1089,14 @@ int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x, ui
     return p ? std::atoi(p) : -1;
   }();
   const bool tc_gate = gate_env >= 0 ? gate_env != 0 : B >= 16;
-  // down product: the tcgen05 GEMM (MN-major gathered down rows) wins from
-  // about 64 tokens (451 vs 502 us at B=64; 272 vs 221 at B=16);
-  // FLOE_DOWN_TC=0/1 forces either
+  // down product: the tcgen05 GEMM (MN-major gathered down rows, 256-channel
+  // ranges per CTA) wins from about 16 tokens (207 vs 215 us at B=16, 358 vs
+  // 451 at B=64); FLOE_DOWN_TC=0/1 forces either
   static const int down_env = [] {
     const char *p = std::getenv("FLOE_DOWN_TC");
     return p ? std::atoi(p) : -1;
   }();
-  const bool tc_down = down_env >= 0 ? down_env != 0 : B > 32;
+  const bool tc_down = down_env >= 0 ? down_env != 0 : B >= 16;
   int rc = floe_gpu_qgemv_channels_batched(e, x, B, v, stream);
   if (rc == FLOE_OK) {
     CK(cudaMemsetAsync(count, 0, 4, st));

@@ -711,9 +711,9 @@ __global__ void __launch_bounds__(256) gate_finish(const float *__restrict__ G,
 // (validated by tools/umma_f16_mn_test.cu: core matrices 8 k x 16 B of n,
 // n-adjacent 128 B apart; descriptor LBO = k-core stride, SBO = 128 B).
 // Partial sums of the channel range are added into y.
-constexpr uint32_t kDownKRange = 1024;  // union channels per CTA
+constexpr uint32_t kDownKRange = 256;   // union channels per CTA
 constexpr uint32_t kDownKChunk = 64;    // channels per pipeline stage
-constexpr int kDownStages = 3;
+constexpr int kDownStages = 2;
 
 template <int DH>
 __global__ void __launch_bounds__(128, 1) down_gemm(const __half *__restrict__ records,
