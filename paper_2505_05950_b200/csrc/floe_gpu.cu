@@ -1080,8 +1080,10 @@ int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x, ui
   float *A = reinterpret_cast<float *>(scratch + o_a);
   uint8_t *xh = scratch + o_xh;
   float *Gp = reinterpret_cast<float *>(scratch + o_g);
-  constexpr uint32_t kGateSplit = 4;  // K parts of the gate GEMM (CTAs = 4 x 128-row blocks)
-  // gate dots: a tcgen05 GEMM (128-channel blocks, K split in 4) pays off from
+  // K parts of the gate GEMM per 128-channel block: more CTAs in flight at
+  // small batches, fewer partial-sum atomics at large ones
+  const uint32_t kGateSplit = B <= 16 ? 8u : 4u;
+  // gate dots: a tcgen05 GEMM (128-channel blocks, K split in 4-8) pays off from
   // about 16 tokens; fewer tokens use the CUDA-core warps.
   // FLOE_GATE_TC=0/1 forces either.
   static const int gate_env = [] {
