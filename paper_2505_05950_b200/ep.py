@@ -1,0 +1,102 @@
+"""Expert-parallel MoE layer: the experts of
+a layer are sharded over the ranks of a process group (rank r owns experts
+[r*E/W, (r+1)*E/W)); every rank routes its own tokens, dispatches (token,
+expert) pairs to the owning ranks with an all-to-all, runs its experts on what
+it received, and gets the outputs back with the reverse all-to-all; the
+combine happens on the source rank.
+
+Per token the arithmetic is the reference's block (model.cpp:145-169):
+  u = h + mixing h;  logits = router u;  top_k (ties to the lower index,
+  selection in ascending expert order, la.cpp:48-61);  w = softmax of the
+  selected logits (la.cpp:37-46);  y = u + sum_j w_j expert_j(u) in ascending
+  expert order.
+The mixing and router products for a token batch are plain GEMMs (torch,
+i.e. cuBLAS on the device); the experts run through `expert_fn` -- on the GPU
+`batched_expert_fn`, the tcgen05 batched expert forward.  The collectives are
+NCCL over NVLink on GPUs (gloo in the CPU tests).  Fusing dispatch/combine
+with the expert kernels over peer memory is the next step; this module is the
+reference-semantics baseline for it.
+"""
+from __future__ import annotations
+
+from typing import Callable, Optional
+
+
+def route_topk(torch, logits, k: int):
+    """top_k with ties to the lower index, selection in ascending expert
+    order, softmax over the selected logits (la.cpp:37-61)."""
+    order = torch.sort(-logits, dim=1, stable=True).indices[:, :k]
+    sel = torch.sort(order, dim=1).values
+    lg = torch.gather(logits, 1, sel)
+    mx = lg.max(dim=1, keepdim=True).values
+    ex = torch.exp(lg - mx)
+    return sel, ex / ex.sum(dim=1, keepdim=True)
+
+
+def _a2a(torch, dist, group, x, out_splits, in_splits):
+    out = x.new_empty((sum(out_splits),) + tuple(x.shape[1:]))
+    dist.all_to_all_single(out, x.contiguous(), out_splits, in_splits, group=group)
+    return out
+
+
+def ep_moe_layer(h, router, mixing, top_k: int, expert_fn: Callable, n_experts: int,
+                 group=None):
+    """One expert-parallel MoE layer over this rank's tokens h [T, dh].
+
+    expert_fn(e, X [n, dh]) -> Y [n, dh] runs local expert e (global index).
+    Returns y [T, dh] and the routing (sel [T, k], w [T, k])."""
+    import torch
+    import torch.distributed as dist
+
+    dist_on = dist.is_available() and dist.is_initialized()
+    world = dist.get_world_size(group) if dist_on else 1
+    if n_experts % world:
+        raise ValueError("ep_moe_layer: experts must divide evenly over the ranks")
+    per_rank = n_experts // world
+    u = h + h @ mixing.t()                      # block input (model.cpp:150-152)
+    sel, w = route_topk(torch, u @ router.t(), top_k)
+    T = h.shape[0]
+    pair_tok = torch.arange(T, device=h.device).repeat_interleave(top_k)
+    pair_exp = sel.reshape(-1)
+    dest = pair_exp // per_rank
+    order = torch.sort(dest, stable=True).indices        # pairs grouped by owner
+    send = torch.bincount(dest, minlength=world)
+    x_send = u[pair_tok[order]]
+    e_send = pair_exp[order]
+    if world > 1:
+        recv = torch.empty_like(send)
+        dist.all_to_all_single(recv, send, group=group)  # counts
+        s_list, r_list = send.tolist(), recv.tolist()
+        x_recv = _a2a(torch, dist, group, x_send, r_list, s_list)
+        e_recv = _a2a(torch, dist, group, e_send, r_list, s_list)
+    else:
+        x_recv, e_recv = x_send, e_send
+    out = torch.empty_like(x_recv)
+    for e in torch.unique(e_recv).tolist():
+        idx = (e_recv == e).nonzero(as_tuple=True)[0]
+        out[idx] = expert_fn(int(e), x_recv[idx])
+    back = _a2a(torch, dist, group, out, s_list, r_list) if world > 1 else out
+    contrib = torch.empty_like(back)
+    contrib[order] = back
+    contrib = contrib.view(T, top_k, -1)
+    y = u.clone()
+    for j in range(top_k):                      # ascending expert order (model.cpp:160-166)
+        y = y + w[:, j:j + 1] * contrib[:, j]
+    return y, sel, w
+
+
+def batched_expert_fn(experts, first_expert: int = 0, chunk: int = 64):
+    """expert_fn over GpuExpert objects on this rank: the batched expert
+    forward (tcgen05 up projection + union gate/down) in chunks of <= 64
+    tokens.  experts[i] is global expert first_expert + i."""
+    from . import _abi
+
+    def fn(e: int, X):
+        ex = experts[e - first_expert]
+        if X.shape[0] == 0:
+            return X.clone()
+        parts = [_abi.expert_forward_batched(ex, X[i:i + chunk]) for i in range(0, X.shape[0], chunk)]
+        import torch
+        return torch.cat(parts, dim=0)
+
+    return fn
