@@ -71,10 +71,19 @@ def ep_moe_layer(h, router, mixing, top_k: int, expert_fn: Callable, n_experts: 
         e_recv = _a2a(torch, dist, group, e_send, r_list, s_list)
     else:
         x_recv, e_recv = x_send, e_send
+    # group the received rows by expert (one host sync for the counts), run
+    # each local expert on a contiguous slice, scatter back
+    perm = torch.sort(e_recv, stable=True).indices
+    x_sorted = x_recv[perm]
+    counts = torch.bincount(e_recv, minlength=n_experts).tolist()
+    out_sorted = torch.empty_like(x_sorted)
+    off = 0
+    for e, c in enumerate(counts):
+        if c:
+            out_sorted[off:off + c] = expert_fn(e, x_sorted[off:off + c])
+            off += c
     out = torch.empty_like(x_recv)
-    for e in torch.unique(e_recv).tolist():
-        idx = (e_recv == e).nonzero(as_tuple=True)[0]
-        out[idx] = expert_fn(int(e), x_recv[idx])
+    out[perm] = out_sorted
     back = _a2a(torch, dist, group, out, s_list, r_list) if world > 1 else out
     contrib = torch.empty_like(back)
     contrib[order] = back
