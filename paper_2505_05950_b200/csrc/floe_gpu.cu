@@ -143,6 +143,11 @@ struct floe_gpu_workspace {
   uint32_t *mix_done = nullptr;
   unsigned long long *stats = nullptr;
   unsigned long long *bar = nullptr;  // fused kernel's grid barrier (monotonic)
+  unsigned long long *tick = nullptr;    // fused kernel: monotonic CTA ticket
+  unsigned long long *y_flag = nullptr;  // fused kernel, expert mode: y-zeroed flag + CTA count
+  uint32_t *kcount = nullptr;            // fused kernel: per-call kept counts per slot
+  unsigned long long *pcnt = nullptr;    // fused kernel: published predicted partials
+  float *pred_partial = nullptr;         // fused kernel: [32][kMaxGrid] predicted partials
   unsigned long long *phase_ns = nullptr;  // diagnostics: [grid][8] phase marks
   uint32_t *sel = nullptr;
   float *weights = nullptr, *u = nullptr, *x = nullptr, *y = nullptr, *v = nullptr;
@@ -168,7 +173,7 @@ struct floe_gpu_layer {
   bool mix_f16 = false, fast = false;
   float *router = nullptr;
   void *mixing = nullptr;
-  float *router_pred = nullptr;  // fused path: router + router * mixing (speculative K1)
+  float *router_pred = nullptr;  // fused path: router + router * mixing (routing predictor)
   ExpertDesc *table = nullptr;
   std::vector<floe_gpu_expert *> experts;  // borrowed (offload engine)
 };
@@ -372,15 +377,13 @@ int launch_v2_dh(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) 
   a.threshold = L.thr;
   a.v_out = L.v_out;
   a.mask_out = L.mask_out ? L.mask_out : (L.trace ? L.trace->masks_dev : nullptr);
-  a.kept_f = ws->kept_idx;
-  a.kept_v = ws->kept_v;
-  a.seg_count = ws->seg_count;
+  a.kcount = ws->kcount;
+  a.tick = ws->tick;
   a.bar = ws->bar;
-  static const uint32_t early_env = [] {
-    const char *p = std::getenv("FLOE_EARLY");
-    return p ? (uint32_t)std::atoi(p) : 2u;
-  }();
-  a.early = std::min<uint32_t>(early_env, ns);
+  a.y_flag = ws->y_flag;
+  a.pred_partial = ws->pred_partial;
+  a.pcnt = ws->pcnt;
+
   a.n_kept_out = L.n_kept_out;
   a.kept_out = L.kept_out;
   a.stats = L.k1_only ? nullptr : ws->stats;
@@ -388,9 +391,11 @@ int launch_v2_dh(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) 
   a.phase_ns = ws->phase_ns;
   a.ns = ns;
   a.max_tiles = max_tiles;
+  // test hook (tests/test_gpu_spec.py): invert the predicted logits so the
+  // misprediction path of the layer kernel runs
   static const uint32_t dbg = [] {
-    const char *d = std::getenv("FLOE_DEBUG_FLAGS");
-    return d ? (uint32_t)std::atoi(d) : 0u;
+    const char *d = std::getenv("FLOE_TEST_MISPREDICT");
+    return (d && std::strcmp(d, "1") == 0) ? 8u : 0u;
   }();
   a.debug = dbg;
 
@@ -741,9 +746,16 @@ int floe_gpu_expert_info(const floe_gpu_expert *e, floe_expert_info *info) {
 
 int floe_gpu_expert_set_threshold(floe_gpu_expert *e, float t) {
   if (!e) return fail(FLOE_ERR_INVALID, "expert_set_threshold: null expert");
+  // Not a hot-path call: drain every stream first (kernels in flight may read
+  // the descriptors), then update the expert's own descriptor AND every layer
+  // table entry that copies it, so layer_forward and expert_forward_sparse
+  // see the same threshold (ThresholdTable is per expert, model.cpp:237).
+  CK(cudaDeviceSynchronize());
   e->threshold = t;
   e->host_desc.threshold = t;
   CK(cudaMemcpy(e->dev_desc, &e->host_desc, sizeof(ExpertDesc), cudaMemcpyHostToDevice));
+  for (ExpertDesc *tab : e->tables)
+    CK(cudaMemcpy(tab, &e->host_desc, sizeof(ExpertDesc), cudaMemcpyHostToDevice));
   return FLOE_OK;
 }
 
@@ -770,6 +782,8 @@ int floe_gpu_workspace_create(uint32_t dh, uint32_t di, uint32_t slots,
   const uint64_t o_mp = o;    o = up256(o + 4ull * 32 * std::max<uint64_t>(1024, (dh + 7) / 8));
   const uint64_t o_md = o;    o = up256(o + 16);
   const uint64_t o_st = o;    o = up256(o + 32);  // stats[2], grid barrier counter
+  const uint64_t o_fk = o;    o = up256(o + 32 + 4ull * MS);  // tick, y flag[2], pcnt, kcount[MS]
+  const uint64_t o_pp = o;    o = up256(o + 4ull * 32 * floe_v2::kMaxGrid);
   const uint64_t o_sel = o;   o = up256(o + 4 * MS);
   const uint64_t o_w = o;     o = up256(o + 4 * MS);
   const uint64_t o_u = o;     o = up256(o + 4ull * dh);
@@ -790,6 +804,11 @@ int floe_gpu_workspace_create(uint32_t dh, uint32_t di, uint32_t slots,
   w->mix_done = reinterpret_cast<uint32_t *>(b + o_md);
   w->stats = reinterpret_cast<unsigned long long *>(b + o_st);
   w->bar = w->stats + 2;
+  w->tick = reinterpret_cast<unsigned long long *>(b + o_fk);
+  w->y_flag = w->tick + 1;
+  w->pcnt = w->tick + 3;
+  w->kcount = reinterpret_cast<uint32_t *>(w->tick + 4);
+  w->pred_partial = reinterpret_cast<float *>(b + o_pp);
   w->sel = reinterpret_cast<uint32_t *>(b + o_sel);
   w->weights = reinterpret_cast<float *>(b + o_w);
   w->u = reinterpret_cast<float *>(b + o_u);
@@ -983,6 +1002,69 @@ int launch_batched(const floe_tc::BatchedArgs &a, cudaStream_t st) {
   CK_LAUNCH();
   return FLOE_OK;
 }
+// Gate/down stage of the batched expert forward (after the batched K1 wrote
+// v): union of kept channels, gate dots (tcgen05 GEMM or CUDA-core warps),
+// down product (tcgen05 GEMM or CUDA-core tiles) into y.  Scratch layout as
+// floe_gpu_expert_forward_batched documents.
+template <int DH>
+int batched_gate_down(const floe_gpu_expert *e, const float *x, uint32_t B, float *y_out,
+                      const float *v, uint8_t *scratch, size_t o_xh, size_t o_g, bool tc_gate,
+                      bool tc_down, uint32_t gate_split, cudaStream_t st) {
+  const uint32_t di = e->di;
+  const size_t o_v = 256, o_uc = o_v + ((4ull * B * di + 255) & ~size_t(255));
+  const size_t o_um = o_uc + ((4ull * di + 255) & ~size_t(255));
+  const size_t o_a = o_um + 8ull * di;
+  uint32_t *count = reinterpret_cast<uint32_t *>(scratch);
+  uint32_t *uc = reinterpret_cast<uint32_t *>(scratch + o_uc);
+  unsigned long long *um = reinterpret_cast<unsigned long long *>(scratch + o_um);
+  float *A = reinterpret_cast<float *>(scratch + o_a);
+  uint8_t *xh = scratch + o_xh;
+  float *Gp = reinterpret_cast<float *>(scratch + o_g);
+  float *xsc = reinterpret_cast<float *>(scratch + o_g + 4ull * di * B);
+  float *inv_xsc = xsc + floe_tc::kMaxTokens;
+  uint32_t *amax = reinterpret_cast<uint32_t *>(inv_xsc + floe_tc::kMaxTokens);
+  const int sm = device_info().sm;
+  CK(cudaMemsetAsync(count, 0, 4, st));
+  floe_tc::hilo_token_scale<<<B, 256, 0, st>>>(x, DH, xsc, inv_xsc, amax);
+  CK_LAUNCH();
+  floe_tc::union_masks<<<(di + 255) / 256, 256, 0, st>>>(v, B, di, e->host_desc.threshold, count,
+                                                         uc, um);
+  CK_LAUNCH();
+  const __half *rec = e->host_desc.records;
+  if (tc_gate) {
+    floe_tc::x_hilo<<<DH / 64, 256, 0, st>>>(x, DH, B, xsc, xh);
+    CK_LAUNCH();
+    const uint32_t gsm = floe_tc::kGemmStages * (16384u + floe_tc::gemm_n(B) * 128u);
+    if (int rc = set_smem(floe_tc::gate_gemm<DH>, gsm)) return rc;
+    CK(cudaMemsetAsync(Gp, 0, 4ull * di * B, st));
+    floe_tc::gate_gemm<DH><<<dim3((di + 127) / 128, gate_split), 128, gsm, st>>>(
+        rec, xh, v, B, di, count, uc, um, A, Gp, inv_xsc, amax);
+    CK_LAUNCH();
+    floe_tc::gate_finish<<<4 * sm, 256, 0, st>>>(Gp, v, B, di, count, uc, um, A, amax);
+    CK_LAUNCH();
+  } else {
+    floe_tc::coeffs<DH><<<4 * sm, 256, 0, st>>>(rec, x, v, B, di, count, uc, um, A,
+                                                tc_down ? amax : nullptr);
+    CK_LAUNCH();
+  }
+  CK(cudaMemsetAsync(y_out, 0, 4ull * B * DH, st));
+  if (tc_down) {
+    const uint32_t gsm = floe_tc::kDownStages * (128u * floe_tc::kDownKChunk * 2u +
+                                                 floe_tc::kDownKChunk * 256u * 2u);
+    if (int rc = set_smem(floe_tc::down_gemm<DH>, gsm)) return rc;
+    floe_tc::down_gemm<DH><<<dim3(DH / 256, (di + floe_tc::kDownKRange - 1) / floe_tc::kDownKRange),
+                             128, gsm, st>>>(rec, B, count, uc, A, y_out, amax);
+  } else {
+    // row chunks of <= kDownRowCap union rows (the union is at most di)
+    const uint32_t chunks = (di + floe_tc::kDownRowCap - 1) / floe_tc::kDownRowCap;
+    const uint32_t dsm = 4u * floe_tc::kDownRowCap * ((B + 3u) & ~3u);
+    if (int rc = set_smem(floe_tc::down_accum<DH>, dsm)) return rc;
+    floe_tc::down_accum<DH><<<dim3(DH / 1024, chunks), 256, dsm, st>>>(rec, B, count, uc, A, y_out);
+  }
+  CK_LAUNCH();
+  return FLOE_OK;
+}
+
 }  // namespace
 extern "C" {
 
@@ -1070,16 +1152,14 @@ int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x, ui
   const size_t o_a = o_um + 8ull * di;
   const size_t o_xh = (o_a + 4ull * di * B + 1023) & ~size_t(1023);
   const size_t o_g = o_xh + (((size_t)(dh / 64) * floe_tc::gemm_n(B) * 128u + 255) & ~size_t(255));
-  const size_t total = o_g + 4ull * di * B;  // G: split-K partial gate dots
+  // G: split-K partial gate dots; then x scale | 1/x scale | max|A| per token
+  const size_t total = o_g + 4ull * di * B + 3ull * 4 * floe_tc::kMaxTokens;
   uint8_t *scratch = nullptr;
   CK(cudaMallocAsync(reinterpret_cast<void **>(&scratch), total, st));
   uint32_t *count = reinterpret_cast<uint32_t *>(scratch);
   float *v = v_out ? v_out : reinterpret_cast<float *>(scratch + o_v);
   uint32_t *uc = reinterpret_cast<uint32_t *>(scratch + o_uc);
   unsigned long long *um = reinterpret_cast<unsigned long long *>(scratch + o_um);
-  float *A = reinterpret_cast<float *>(scratch + o_a);
-  uint8_t *xh = scratch + o_xh;
-  float *Gp = reinterpret_cast<float *>(scratch + o_g);
   // K parts of the gate GEMM per 128-channel block: more CTAs in flight at
   // small batches, fewer partial-sum atomics at large ones
   const uint32_t kGateSplit = B <= 16 ? 8u : 4u;
@@ -1100,87 +1180,15 @@ int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x, ui
   }();
   const bool tc_down = down_env >= 0 ? down_env != 0 : B >= 16;
   int rc = floe_gpu_qgemv_channels_batched(e, x, B, v, stream);
-  if (rc == FLOE_OK) {
-    CK(cudaMemsetAsync(count, 0, 4, st));
-    floe_tc::union_masks<<<(di + 255) / 256, 256, 0, st>>>(v, B, di, e->host_desc.threshold, count,
-                                                           uc, um);
-    CK_LAUNCH();
-    const __half *rec = e->host_desc.records;
-    const int sm = device_info().sm;
-    if (dh == 4096) {
-      {
-        if (tc_gate) {
-          floe_tc::x_hilo<<<4096 / 64, 256, 0, st>>>(x, 4096, B, xh);
-          const uint32_t gsm = floe_tc::kGemmStages * (16384u + floe_tc::gemm_n(B) * 128u);
-          rc = set_smem(floe_tc::gate_gemm<4096>, gsm);
-          if (rc == FLOE_OK)
-          {
-            CK(cudaMemsetAsync(Gp, 0, 4ull * di * B, st));
-            floe_tc::gate_gemm<4096><<<dim3((di + 127) / 128, kGateSplit), 128, gsm, st>>>(
-                rec, xh, v, B, di, count, uc, um, A, Gp);
-            floe_tc::gate_finish<<<4 * sm, 256, 0, st>>>(Gp, v, B, di, count, uc, um, A);
-          }
-        } else {
-          floe_tc::coeffs<4096><<<4 * sm, 256, 0, st>>>(rec, x, v, B, di, count, uc, um, A);
-        }
-        CK(cudaMemsetAsync(y_out, 0, 4ull * B * dh, st));
-        // row chunks of <= kDownRowCap union rows (the union is at most di)
-        const uint32_t chunks = (di + floe_tc::kDownRowCap - 1) / floe_tc::kDownRowCap;
-        if (tc_down) {
-          const uint32_t gsm = floe_tc::kDownStages * (128u * floe_tc::kDownKChunk * 2u +
-                                                       floe_tc::kDownKChunk * 256u * 2u);
-          rc = set_smem(floe_tc::down_gemm<4096>, gsm);
-          if (rc == FLOE_OK)
-            floe_tc::down_gemm<4096><<<dim3(4096 / 256, (di + floe_tc::kDownKRange - 1) /
-                                                           floe_tc::kDownKRange),
-                                        128, gsm, st>>>(rec, B, count, uc, A, y_out);
-        } else {
-          const uint32_t dsm = 4u * floe_tc::kDownRowCap * ((B + 3u) & ~3u);
-          rc = set_smem(floe_tc::down_accum<4096>, dsm);
-          if (rc == FLOE_OK)
-            floe_tc::down_accum<4096><<<dim3(4096 / 1024, chunks), 256, dsm, st>>>(
-                rec, B, count, uc, A, y_out);
-        }
-      }
-    } else {
-      {
-        if (tc_gate) {
-          floe_tc::x_hilo<<<2048 / 64, 256, 0, st>>>(x, 2048, B, xh);
-          const uint32_t gsm = floe_tc::kGemmStages * (16384u + floe_tc::gemm_n(B) * 128u);
-          rc = set_smem(floe_tc::gate_gemm<2048>, gsm);
-          if (rc == FLOE_OK)
-          {
-            CK(cudaMemsetAsync(Gp, 0, 4ull * di * B, st));
-            floe_tc::gate_gemm<2048><<<dim3((di + 127) / 128, kGateSplit), 128, gsm, st>>>(
-                rec, xh, v, B, di, count, uc, um, A, Gp);
-            floe_tc::gate_finish<<<4 * sm, 256, 0, st>>>(Gp, v, B, di, count, uc, um, A);
-          }
-        } else {
-          floe_tc::coeffs<2048><<<4 * sm, 256, 0, st>>>(rec, x, v, B, di, count, uc, um, A);
-        }
-        CK(cudaMemsetAsync(y_out, 0, 4ull * B * dh, st));
-        // row chunks of <= kDownRowCap union rows (the union is at most di)
-        const uint32_t chunks = (di + floe_tc::kDownRowCap - 1) / floe_tc::kDownRowCap;
-        if (tc_down) {
-          const uint32_t gsm = floe_tc::kDownStages * (128u * floe_tc::kDownKChunk * 2u +
-                                                       floe_tc::kDownKChunk * 256u * 2u);
-          rc = set_smem(floe_tc::down_gemm<2048>, gsm);
-          if (rc == FLOE_OK)
-            floe_tc::down_gemm<2048><<<dim3(2048 / 256, (di + floe_tc::kDownKRange - 1) /
-                                                           floe_tc::kDownKRange),
-                                        128, gsm, st>>>(rec, B, count, uc, A, y_out);
-        } else {
-          const uint32_t dsm = 4u * floe_tc::kDownRowCap * ((B + 3u) & ~3u);
-          rc = set_smem(floe_tc::down_accum<2048>, dsm);
-          if (rc == FLOE_OK)
-            floe_tc::down_accum<2048><<<dim3(2048 / 1024, chunks), 256, dsm, st>>>(
-                rec, B, count, uc, A, y_out);
-        }
-      }
-    }
-    if (rc == FLOE_OK) CK_LAUNCH();
-  }
-  CK(cudaFreeAsync(scratch, st));
+  if (rc == FLOE_OK)
+    rc = dh == 4096 ? batched_gate_down<4096>(e, x, B, y_out, v, scratch, o_xh, o_g, tc_gate,
+                                              tc_down, kGateSplit, st)
+                    : batched_gate_down<2048>(e, x, B, y_out, v, scratch, o_xh, o_g, tc_gate,
+                                              tc_down, kGateSplit, st);
+  // the scratch is released on every path (stream-ordered)
+  const cudaError_t fe = cudaFreeAsync(scratch, st);
+  if (rc == FLOE_OK && fe != cudaSuccess)
+    return fail(FLOE_ERR_CUDA, "expert_forward_batched: %s", cudaGetErrorString(fe));
   return rc;
 }
 
@@ -1291,18 +1299,12 @@ int floe_gpu_layer_create(const floe_layer_host_view *v, floe_gpu_layer **out) {
       if (tmp) cudaFree(tmp);
     }
   }
-  // Predicted routing for the fused kernel's speculative K1 stream:
-  // router * (h + mixing h) = (router + router * mixing) h, with the mixing
-  // weights exactly as the kernel reads them.  Only a prediction: the kernel
-  // still routes on the exact logits and discards a wrong speculation.
-  // Off by default: K1 is issue-bound, so tiles that land earlier do not
-  // finish it earlier, and the extra stream slows phase A (measured 60.2 vs
-  // 55.2 us per layer, every prediction correct).  FLOE_SPEC=1 enables it.
-  static const bool spec_env = [] {
-    const char *p = std::getenv("FLOE_SPEC");
-    return p && std::strcmp(p, "1") == 0;
-  }();
-  if (ce == cudaSuccess && spec_env && l->fast && l->E <= 32) {
+  // Routing predictor of the fused layer kernel: router * (h + mixing h) =
+  // (router + router * mixing) h, with the mixing weights exactly as the
+  // kernel reads them (f16 or f32), accumulated in f64.  The kernel streams
+  // the predicted experts' K1 tiles during the mixing GEMV and verifies the
+  // prediction against the exact routing of u before any record is read.
+  if (ce == cudaSuccess && l->fast && l->E <= 32) {
     ce = cudaMalloc(&l->router_pred, 4ull * l->E * dh);
     if (ce == cudaSuccess) {
       const uint32_t blocks = (dh + 127) / 128;
@@ -1326,6 +1328,13 @@ int floe_gpu_layer_create(const floe_layer_host_view *v, floe_gpu_layer **out) {
 
 int floe_gpu_layer_destroy(floe_gpu_layer *l) {
   if (!l) return FLOE_OK;
+  cudaDeviceSynchronize();  // kernels in flight may still read the table
+  // unregister this layer's table entries from its (borrowed) experts, so a
+  // later residency or threshold change does not write into freed memory
+  for (size_t i = 0; i < l->experts.size(); ++i) {
+    auto &tabs = l->experts[i]->tables;
+    tabs.erase(std::remove(tabs.begin(), tabs.end(), l->table + i), tabs.end());
+  }
   if (l->router) cudaFree(l->router);
   if (l->mixing) cudaFree(l->mixing);
   if (l->router_pred) cudaFree(l->router_pred);

@@ -560,18 +560,22 @@ __global__ void router_pred(const float *__restrict__ router, const MT *__restri
                             uint32_t E, uint32_t dh, float *__restrict__ out) {
   const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= dh) return;
-  float acc[32];
+  // f64 accumulation, 8 experts per pass (registers)
+  for (uint32_t e0 = 0; e0 < E; e0 += 8) {
+    double acc[8];
 #pragma unroll
-  for (int e = 0; e < 32; ++e) acc[e] = 0.0f;
-  for (uint32_t i = 0; i < dh; ++i) {
-    const float m = static_cast<float>(mixing[(size_t)i * dh + j]);
+    for (int e = 0; e < 8; ++e) acc[e] = 0.0;
+    for (uint32_t i = 0; i < dh; ++i) {
+      const double m = static_cast<double>(static_cast<float>(mixing[(size_t)i * dh + j]));
 #pragma unroll
-    for (int e = 0; e < 32; ++e)
-      if ((uint32_t)e < E) acc[e] = fmaf(router[(size_t)e * dh + i], m, acc[e]);
+      for (int e = 0; e < 8; ++e)
+        if (e0 + e < E) acc[e] = fma((double)router[(size_t)(e0 + e) * dh + i], m, acc[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (e0 + e < E)
+        out[(size_t)(e0 + e) * dh + j] = (float)((double)router[(size_t)(e0 + e) * dh + j] + acc[e]);
   }
-#pragma unroll
-  for (int e = 0; e < 32; ++e)
-    if ((uint32_t)e < E) out[(size_t)e * dh + j] = router[(size_t)e * dh + j] + acc[e];
 }
 
 }  // namespace floe_k

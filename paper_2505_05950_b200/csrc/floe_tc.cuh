@@ -492,7 +492,8 @@ __global__ void __launch_bounds__(256) coeffs(const __half *__restrict__ records
                                               const uint32_t *__restrict__ count,
                                               const uint32_t *__restrict__ uc,
                                               const unsigned long long *__restrict__ um,
-                                              float *__restrict__ A /* [n][B] */) {
+                                              float *__restrict__ A /* [n][B] */,
+                                              uint32_t *__restrict__ amax) {
   // one warp per union channel, one pass: the gate row stays in registers and
   // each keeping token's x streams from L2 (x is B x 16 KB, shared by all SMs)
   const uint32_t n = *count, lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -524,7 +525,9 @@ __global__ void __launch_bounds__(256) coeffs(const __half *__restrict__ records
       for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
       if (lane == 0) {
         const float z = acc;
-        A[(size_t)u * B + tt] = z / (1.0f + expf(-z)) * v[(size_t)tt * di + c];  // silu(g) * v
+        const float av = z / (1.0f + expf(-z)) * v[(size_t)tt * di + c];  // silu(g) * v
+        A[(size_t)u * B + tt] = av;
+        if (amax) atomicMax(&amax[tt], __float_as_uint(fabsf(av)));
       }
     }
   }
@@ -544,8 +547,48 @@ __device__ __forceinline__ uint32_t kmaj_off128(uint32_t row, uint32_t kbyte) {
   return (row & 7u) * 16u + (kbyte & 15u) + (kbyte >> 4) * 128u + (row >> 3) * 1024u;
 }
 
-// x -> hi/lo table [chunk][N rows][128 B] in the B-operand layout.  Grid: chunks.
+// Power-of-two scale that puts max|a| in [64, 128): the f16 hi + lo split of
+// a*scale then keeps ~22 significant bits without f16 underflow or overflow
+// whatever the token's magnitude (1 when amax is 0 or not finite).  amax_bits
+// = float bits of a non-negative max (uint order == float order).
+__device__ __forceinline__ float hilo_scale(uint32_t amax_bits) {
+  if (amax_bits == 0u || amax_bits >= 0x7f800000u) return 1.0f;
+  const int e = (int)((amax_bits >> 23) & 255u) - 127;  // amax < 2^(e+1)
+  const int se = max(-100, min(100, 6 - e));
+  return __int_as_float((127 + se) << 23);
+}
+
+// Per token: the hi/lo scale of x (xsc[t], inv_xsc[t]); clears amax[t] (the
+// per-token max|A| the gate stage accumulates for the down GEMM's A scale).
+__global__ void __launch_bounds__(256) hilo_token_scale(const float *__restrict__ x, uint32_t dh,
+                                                        float *__restrict__ xsc,
+                                                        float *__restrict__ inv_xsc,
+                                                        uint32_t *__restrict__ amax) {
+  const uint32_t t = blockIdx.x;
+  __shared__ uint32_t red[8];
+  uint32_t mx = 0;
+  const float4 *x4 = reinterpret_cast<const float4 *>(x + (size_t)t * dh);
+  for (uint32_t k = threadIdx.x; k < dh / 4u; k += blockDim.x) {
+    const float4 v = x4[k];
+    mx = max(mx, max(max(__float_as_uint(fabsf(v.x)), __float_as_uint(fabsf(v.y))),
+                     max(__float_as_uint(fabsf(v.z)), __float_as_uint(fabsf(v.w)))));
+  }
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = max(mx, red[w]);
+    const float sc = hilo_scale(max(mx, red[0]));
+    xsc[t] = sc;
+    inv_xsc[t] = 1.0f / sc;
+    amax[t] = 0u;
+  }
+}
+
+// x -> hi/lo table [chunk][N rows][128 B] in the B-operand layout, x_t scaled
+// by xsc[t] (undone in the gate epilogue).  Grid: chunks.
 __global__ void __launch_bounds__(256) x_hilo(const float *__restrict__ x, uint32_t dh, uint32_t B,
+                                              const float *__restrict__ xsc,
                                               uint8_t *__restrict__ xh) {
   const uint32_t ch = blockIdx.x, N = gemm_n(B);
   uint8_t *out = xh + (size_t)ch * N * 128u;
@@ -553,7 +596,7 @@ __global__ void __launch_bounds__(256) x_hilo(const float *__restrict__ x, uint3
     const uint32_t t = i / 64u, e = i % 64u;
     __half hi = __float2half_rn(0.0f), lo = hi;
     if (t < B) {
-      const float xv = x[(size_t)t * dh + 64u * ch + e];
+      const float xv = x[(size_t)t * dh + 64u * ch + e] * xsc[t];
       hi = __float2half_rn(xv);
       lo = __float2half_rn(xv - __half2float(hi));
     }
@@ -575,7 +618,9 @@ __global__ void __launch_bounds__(128, 1) gate_gemm(const __half *__restrict__ r
                                                     const uint32_t *__restrict__ uc,
                                                     const unsigned long long *__restrict__ um,
                                                     float *__restrict__ A /* [n][B] */,
-                                                    float *__restrict__ G /* split K: [n][B] */) {
+                                                    float *__restrict__ G /* split K: [n][B] */,
+                                                    const float *__restrict__ inv_xsc,
+                                                    uint32_t *__restrict__ amax) {
   // K (d_hidden) split over gridDim.y CTAs: each adds its partial dot into G,
   // gate_finish applies silu * v; with one part the epilogue does it directly
   constexpr uint32_t CHUNKS = DH / 64u;
@@ -585,6 +630,7 @@ __global__ void __launch_bounds__(128, 1) gate_gemm(const __half *__restrict__ r
   __shared__ __align__(8) uint64_t mdone[kGemmStages];
   __shared__ uint32_t tmem_base;
   __shared__ uint32_t ucs[128];
+  __shared__ uint32_t amax_s[kMaxTokens];
   const uint32_t n = *count, u0 = blockIdx.x * 128u;
   if (u0 >= n) return;
   const uint32_t t = threadIdx.x, warp = t >> 5, lane = t & 31u;
@@ -600,6 +646,7 @@ __global__ void __launch_bounds__(128, 1) gate_gemm(const __half *__restrict__ r
     floe_ptx::fence_barrier_init();
   }
   ucs[t] = t < nr ? uc[u0 + t] : uc[u0];  // rows past the union repeat a valid channel
+  if (t < kMaxTokens) amax_s[t] = 0u;
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
@@ -672,17 +719,21 @@ __global__ void __launch_bounds__(128, 1) gate_gemm(const __half *__restrict__ r
       for (int i = 0; i < 8; ++i) {
         const uint32_t tok = c0 / 2u + (uint32_t)i;
         if (tok < B) {
-          const float z = __uint_as_float(r[2 * i]) + __uint_as_float(r[2 * i + 1]);
-          if (gridDim.y > 1)
+          const float z = (__uint_as_float(r[2 * i]) + __uint_as_float(r[2 * i + 1])) * inv_xsc[tok];
+          if (gridDim.y > 1) {
             atomicAdd(G + (size_t)u * B + tok, z);
-          else
-            A[(size_t)u * B + tok] =
+          } else {
+            const float av =
                 ((m >> tok) & 1ull) ? z / (1.0f + expf(-z)) * v[(size_t)tok * di + c_ch] : 0.0f;
+            A[(size_t)u * B + tok] = av;
+            atomicMax(&amax_s[tok], __float_as_uint(fabsf(av)));
+          }
         }
       }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+  if (gridDim.y == 1 && t < B && amax_s[t]) atomicMax(&amax[t], amax_s[t]);
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
   (void)lane;
 }
@@ -693,13 +744,21 @@ __global__ void __launch_bounds__(256) gate_finish(const float *__restrict__ G,
                                                    uint32_t di, const uint32_t *__restrict__ count,
                                                    const uint32_t *__restrict__ uc,
                                                    const unsigned long long *__restrict__ um,
-                                                   float *__restrict__ A) {
+                                                   float *__restrict__ A,
+                                                   uint32_t *__restrict__ amax) {
+  __shared__ uint32_t amax_s[kMaxTokens];
+  if (threadIdx.x < kMaxTokens) amax_s[threadIdx.x] = 0u;
+  __syncthreads();
   const uint32_t n = *count;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n * B; i += gridDim.x * blockDim.x) {
     const uint32_t u = i / B, tok = i % B;
     const float z = G[i];
-    A[i] = ((um[u] >> tok) & 1ull) ? z / (1.0f + expf(-z)) * v[(size_t)tok * di + uc[u]] : 0.0f;
+    const float av = ((um[u] >> tok) & 1ull) ? z / (1.0f + expf(-z)) * v[(size_t)tok * di + uc[u]] : 0.0f;
+    A[i] = av;
+    atomicMax(&amax_s[tok], __float_as_uint(fabsf(av)));
   }
+  __syncthreads();
+  if (threadIdx.x < B && amax_s[threadIdx.x]) atomicMax(&amax[threadIdx.x], amax_s[threadIdx.x]);
 }
 
 // ---------------------------------------------- down GEMM on tcgen05 (f16)
@@ -719,7 +778,8 @@ template <int DH>
 __global__ void __launch_bounds__(128, 1) down_gemm(const __half *__restrict__ records,
                                                     uint32_t B, const uint32_t *__restrict__ count,
                                                     const uint32_t *__restrict__ uc,
-                                                    const float *__restrict__ A, float *__restrict__ y) {
+                                                    const float *__restrict__ A, float *__restrict__ y,
+                                                    const uint32_t *__restrict__ amax) {
   constexpr uint32_t NS = 256;  // d_hidden columns per CTA
   constexpr uint32_t SA = 128u * kDownKChunk * 2u;   // 16 KB: 128 rows x 64 k f16
   constexpr uint32_t SBB = kDownKChunk * NS * 2u;    // 32 KB: 64 k x 256 n f16
@@ -727,8 +787,14 @@ __global__ void __launch_bounds__(128, 1) down_gemm(const __half *__restrict__ r
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t mdone[kDownStages];
   __shared__ uint32_t tmem_base;
+  __shared__ float asc[kMaxTokens], inv_asc[kMaxTokens];
   const uint32_t n = *count, k0 = blockIdx.y * kDownKRange;
   if (k0 >= n) return;
+  if (threadIdx.x < B) {  // per-token power-of-two scale of the coefficients
+    const float sc = hilo_scale(amax[threadIdx.x]);
+    asc[threadIdx.x] = sc;
+    inv_asc[threadIdx.x] = 1.0f / sc;
+  }
   const uint32_t m0 = blockIdx.x * NS, t = threadIdx.x, warp = t >> 5, lane = t & 31u;
   const uint32_t nk = min(kDownKRange, n - k0), nch = (nk + kDownKChunk - 1) / kDownKChunk;
   if (warp == 0) {
@@ -771,7 +837,7 @@ __global__ void __launch_bounds__(128, 1) down_gemm(const __half *__restrict__ r
     // start); coefficients read token-contiguous
     for (uint32_t i = t; i < kDownKChunk * B; i += 128u) {
       const uint32_t kk = i / B, tok = i % B;
-      const float a = kc0 + kk < k0 + nk ? A[(size_t)kc0 * B + i] : 0.0f;
+      const float a = kc0 + kk < k0 + nk ? A[(size_t)kc0 * B + i] * asc[tok] : 0.0f;
       const __half hi = __float2half_rn(a), lo = __float2half_rn(a - __half2float(hi));
       *reinterpret_cast<__half *>(st + kmaj_off128(2u * tok, 2u * kk)) = hi;
       *reinterpret_cast<__half *>(st + kmaj_off128(2u * tok + 1u, 2u * kk)) = lo;
@@ -834,7 +900,7 @@ __global__ void __launch_bounds__(128, 1) down_gemm(const __half *__restrict__ r
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const float mine = __uint_as_float(r[i]);
-        f[i] = mine + __shfl_xor_sync(0xffffffffu, mine, 1);  // hi + lo
+        f[i] = (mine + __shfl_xor_sync(0xffffffffu, mine, 1)) * inv_asc[min(tok, B - 1)];  // hi + lo
       }
       if (!(row & 1u) && tok < B)
 #pragma unroll

@@ -52,10 +52,9 @@ using floe_k::h2f;
 constexpr int kTileCh = 16;
 constexpr int kConsumerWarps = 16;
 constexpr int kConsumers = 32 * kConsumerWarps;   // 512
-constexpr int kThreads = kConsumers + 32;         // + 1 producer warp
+constexpr int kThreads = kConsumers + 64;         // + 1 producer warp + 1 router warp
 constexpr int kPairs = kConsumerWarps / 2;        // stage owners in phases A/B: warps p, p+8
 constexpr int kMaxStages = 24;  // ring stages: a multiple of kPairs (see phase B)
-constexpr int kMaxStagesC = 24; // phase-C ring (records), carved over ring + staging area
 constexpr int kMaxGrid = 256;                     // plan scans: one value per consumer
 #ifndef FLOE_KR
 #define FLOE_KR 2
@@ -233,10 +232,6 @@ __device__ __forceinline__ void cbar() {  // consumers
   __syncwarp();
   asm volatile("barrier.sync 1, %0;" ::"n"(kConsumers) : "memory");
 }
-__device__ __forceinline__ void abar() {  // consumers + producer
-  __syncwarp();
-  asm volatile("barrier.sync 2, %0;" ::"n"(kThreads) : "memory");
-}
 __device__ __forceinline__ void pbar(uint32_t pair) {  // the two warps of a pair
   __syncwarp();
   asm volatile("barrier.sync %0, 64;" ::"r"(3 + pair) : "memory");
@@ -282,51 +277,44 @@ __device__ __forceinline__ void grid_arrive_wait(unsigned long long *bar, uint32
   __threadfence();
 }
 
-// Split grid barrier: arrive (returns the target) ... wait.
-__device__ __forceinline__ unsigned long long grid_arrive(unsigned long long *bar, uint32_t G) {
-  __threadfence();
-  const unsigned long long old = atomicAdd(bar, 1ull);
-  return (old / G + 1) * G;
-}
-__device__ __forceinline__ void grid_wait(unsigned long long *bar, unsigned long long target,
-                                          uint32_t G) {
-  const unsigned long long t0 = gtime();
-  for (uint32_t it = 1;; ++it) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
-    if (v >= target) break;
-    if ((it & 255u) == 0 && gtime() - t0 > floe_ptx::kWatchdogNs)
-      floe_ptx::watchdog_fire("grid barrier", (uint32_t)(target / G), 0u);
-  }
-  __threadfence();
-}
 
-// Exclusive scan over the consumer threads (one value each); returns the
-// prefix, writes the total to *total.  Uses ws[kConsumerWarps] shared
-// scratch; contains two consumer barriers.
-__device__ __forceinline__ uint32_t cscan(uint32_t v, uint32_t *ws, uint32_t *total) {
-  const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  uint32_t inc = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= (uint32_t)o) inc += y;
-  }
-  if (lane == 31) ws[warp] = inc;
-  cbar();
-  uint32_t base = 0, tot = 0;
-#pragma unroll
-  for (int w = 0; w < kConsumerWarps; ++w) {
-    const uint32_t x = ws[w];
-    if (w < (int)warp) base += x;
-    tot += x;
-  }
-  cbar();
-  *total = tot;
-  return base + inc - v;
+
+// shared-memory flag words of the producer <-> consumer list protocol
+__device__ __forceinline__ uint32_t ld_acquire_s(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(floe_ptx::smem_u32(p))
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_s(uint32_t *p, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(floe_ptx::smem_u32(p)), "r"(v)
+               : "memory");
 }
 
 // -------------------------------------------------------------- the kernel
+//
+// One persistent CTA per SM: 16 consumer warps, 1 producer warp (lane 0
+// issues every bulk copy), 1 router warp (layer mode: exact routing).  All
+// weight bytes flow through ONE ring of `ns` 20 KB stages, in one sequence of
+// ring uses per CTA:
+//   [mixing rows]  [K1 tiles of the predicted experts]  [own kept records]
+// Layer mode:
+//   * at kernel start the consumers compute PREDICTED logits router_pred * h
+//     (router_pred = router + router * mixing, so router_pred * h ==
+//     router * (h + mixing * h) up to f32 rounding) and the producer streams
+//     the predicted experts' K1 tiles right behind the mixing rows: the ring is
+//     full of K1 tiles when phase A ends;
+//   * phase A (mixing GEMV, u, y = u, partial router logits), ONE grid barrier;
+//   * the router warp computes the EXACT routing from the partial logits
+//     (model.cpp:83-93) while the consumers run K1 on the predicted experts;
+//     the prediction is checked before any record is issued, and a
+//     misprediction re-runs K1 on the exact experts (tests force it);
+//   * K1 epilogues append kept channels to the CTA's own list in shared memory
+//     and the producer streams their gate|down records as they appear, so the
+//     records flow in while the last K1 tiles are still being consumed;
+//   * phase C: the CTA's own kept records, no second grid barrier.
+// Expert mode: no phase A; K1 starts at once; y is zeroed by CTA 0 and the
+// other CTAs check a per-call flag before their final y reduction.
 struct FusedArgs {
   int has_mixing;  // layer mode (phase A) vs single-expert mode
   int k1_only;     // qgemv_channels / predict_mask: no phase C
@@ -334,12 +322,12 @@ struct FusedArgs {
   const void *mixing;  // [DH][DH] f16 or f32
   int mix_f16;
   const float *h;
-  const float *router;  // [E][DH]
-  // nullable [E][DH]: router + router * mixing, so predicted logits =
-  // router_pred * h need no mixing GEMV (speculative K1 streaming, below)
-  const float *router_pred;
+  const float *router;       // [E][DH]
+  const float *router_pred;  // [E][DH] router + router * mixing (layer mode)
   uint32_t n_experts, top_k;
-  float *partial;  // [G][32]
+  float *partial;  // [32][kMaxGrid] per-CTA partial router logits
+  float *pred_partial;       // [32][kMaxGrid] per-CTA partial predicted logits
+  unsigned long long *pcnt;  // monotonic count of published predicted partials
   float *u_trace;
   uint32_t *sel_trace;
   float *w_trace;
@@ -353,64 +341,63 @@ struct FusedArgs {
   const ExpertDesc *table;  // layer: [E]; expert mode: [slots]
   int use_threshold;
   float threshold;
-  float *v_out;       // nullable [slots][di]
-  uint8_t *mask_out;  // nullable [slots][di]
-  uint32_t *kept_f;   // [slots*di] per-CTA compacted lists (flattened channel ids)
-  float *kept_v;
-  uint32_t *seg_count;  // [slots][G]
-  unsigned long long *bar;
+  float *v_out;          // nullable [slots][di]
+  uint8_t *mask_out;     // nullable [slots][di]
   uint32_t *n_kept_out;  // nullable [slots]
-  uint32_t *kept_out;    // nullable [slots][di], ascending-by-CTA order
+  uint32_t *kept_out;    // nullable [slots][di], unordered
+  uint32_t *kcount;      // [kMaxSlots] per-call kept counts (zero between calls)
+  unsigned long long *tick;    // monotonic CTA ticket (last CTA publishes the counts)
+  unsigned long long *bar;     // monotonic grid-barrier counter
+  unsigned long long *y_flag;  // expert mode: [0] index + 1 of the last call whose y is
+                               // zeroed, [1] monotonic CTA count (G per call)
   unsigned long long *stats;
   unsigned long long *place_acc;  // nullable [2]: kept records read from HBM / over PCIe
-  unsigned long long *phase_ns;  // nullable [G][kTraceSlots]
-  uint32_t ns;        // ring stages
-  uint32_t max_tiles; // per-CTA tile capacity of the smem emit buffer
-  uint32_t debug;     // diagnostics (FLOE_DEBUG_FLAGS): bit 1 = phase C waits only, no math;
-                      // bit 3 = invert the routing prediction (misprediction path)
-  uint32_t early;     // mixing stages issued before griddepcontrol.wait (PDL overlap)
+  unsigned long long *phase_ns;   // nullable [G][kTraceSlots]
+  uint32_t ns;         // ring stages
+  uint32_t max_tiles;  // per-CTA tile capacity of the shared-memory kept list
+  uint32_t debug;      // test hook: bit 3 = invert the predicted logits (misprediction path)
 };
 
 // Dynamic shared memory layout (bytes), host and device agree.
 struct SmemLayout {
-  uint32_t ring, uni, xs, emit_f, emit_v, tile_cnt, plan, scale, isrc, iscale, total;
+  uint32_t ring, uni, xs, lf, lv, total;
 };
 
 __host__ __device__ inline SmemLayout smem_layout(uint32_t dh, uint32_t ns, uint32_t max_tiles,
                                                   uint32_t G) {
+  (void)G;
   SmemLayout L;
   uint32_t o = 0;
-  L.ring = o;     o += ns * tile_bytes(dh);
-  L.uni = o;      o += (4u * dh > xtab_bytes(dh) ? 4u * dh : xtab_bytes(dh));  // h | x f32 | xtab
-  L.xs = o;       o += 4u * (dh / 64);
-  L.emit_f = o;   o += 4u * kTileCh * max_tiles;
-  L.emit_v = o;   o += 4u * kTileCh * max_tiles;
-  L.tile_cnt = o; o += 4u * max_tiles + 16;
-  L.plan = o;     o += 4u * 3 * (G + 1);
-  L.scale = o;    o += 0;  // (phase-C scales live in static shared memory)
-  o = (o + 7u) & ~7u;
-  L.isrc = o;     o += 8u * kTileCh * max_tiles;  // own records: source address
-  L.iscale = o;   o += 4u * kTileCh * max_tiles;  //              v * routing weight
+  L.ring = o; o += ns * tile_bytes(dh);
+  L.uni = o;  o += (4u * dh > xtab_bytes(dh) ? 4u * dh : xtab_bytes(dh));  // h | x f32 | xtab
+  L.xs = o;   o += 4u * (dh / 64);
+  L.lf = o;   o += 4u * kTileCh * max_tiles;  // kept list: flattened channel | kValid
+  L.lv = o;   o += 4u * kTileCh * max_tiles;  //            v
   L.total = (o + 127u) & ~127u;
   return L;
 }
 
-// Phase trace (diagnostics): %globaltimer at fixed points, consumer thread 0
-// (marks 0..13) and producer lane 0 (marks 16..23).
+constexpr uint32_t kValid = 0x80000000u;
+constexpr uint32_t kEarly = 2;  // mixing stages issued before griddepcontrol.wait
+
+// Phase trace (diagnostics): %globaltimer at fixed points by consumer thread 0
+// (marks 0..15), producer lane 0 (16..23) and router lane 0 (24..27).
 __device__ __forceinline__ void mark(const FusedArgs &a, int k) {
-  if (a.phase_ns && (threadIdx.x == 0 || threadIdx.x == kConsumers) && k < kTraceSlots)
-    a.phase_ns[blockIdx.x * kTraceSlots + k] = gtime();
+  if (a.phase_ns && k < kTraceSlots) a.phase_ns[blockIdx.x * kTraceSlots + k] = gtime();
 }
 
 // Tile i of the launch (tile-granular split of slots x tiles_per_expert over
-// the grid): slot, tile within expert, channel count, flattened position.
+// the grid, slots interleaved: every CTA gets the same channel range of each
+// slot, so its kept-record count does not depend on which expert keeps more
+// channels for this token): slot, tile within expert, channel count,
+// flattened position.
 struct TileRef {
   uint32_t slot, t, nc, f0;
 };
-__device__ __forceinline__ TileRef tile_ref(uint32_t i, uint32_t tps, uint32_t di) {
+__device__ __forceinline__ TileRef tile_ref(uint32_t i, uint32_t slots, uint32_t di) {
   TileRef r;
-  r.slot = i / tps;
-  r.t = i % tps;
+  r.slot = i % slots;
+  r.t = i / slots;
   r.nc = min((uint32_t)kTileCh, di - r.t * kTileCh);
   r.f0 = r.slot * di + r.t * kTileCh;
   return r;
@@ -441,53 +428,47 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   static_assert(DH == 4096 || DH == 2048, "d_hidden 4096 or 2048");
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
-  __shared__ uint64_t fullC[kMaxStagesC], emptyC[kMaxStagesC];
-  __shared__ float stage_scale[kMaxStagesC];
-  __shared__ uint64_t hbar;
-  __shared__ uint64_t predbar;                      // predicted routing published
-  __shared__ const uint8_t *ptiles_s[floe_k::kMaxSlots];
-  __shared__ uint32_t psel_s[floe_k::kMaxSlots];
-  __shared__ float plog[32];
-  __shared__ uint32_t spec_ok, ptaken_s;
+  __shared__ float stage_scale[kMaxStages];
+  __shared__ uint64_t hbar, predbar, bar1, routebar, lreset, listbar, pubbar;
+  __shared__ unsigned long long pc_target, y_target;
+  __shared__ ExpertDesc table_s[32];
   __shared__ float rs[32 * kMaxRowsPerCta];
-  __shared__ float plw[kConsumerWarps][32];
-  __shared__ float logits[32];
-  __shared__ uint32_t sel_s[floe_k::kMaxSlots];
+  __shared__ float plw[kConsumerWarps][32];  // phase A partial logits per warp
+  __shared__ float rps[32 * kMaxRowsPerCta];  // router_pred slice (predicted logits)
+  // predicted selection (the K1 pass) and exact routing (the records)
+  __shared__ uint32_t ptaken_s, spec_ok;
+  __shared__ float pthr_s[floe_k::kMaxSlots];
+  __shared__ const uint8_t *ptiles_s[floe_k::kMaxSlots];
+  __shared__ float ethr_s[floe_k::kMaxSlots];
+  __shared__ const uint8_t *etiles_s[floe_k::kMaxSlots];
   __shared__ float w_s[floe_k::kMaxSlots];
   __shared__ const __half *rec_s[floe_k::kMaxSlots];
-  __shared__ const uint8_t *tiles_s[floe_k::kMaxSlots];
-  __shared__ float thr_s[floe_k::kMaxSlots];
-  __shared__ uint32_t rhost_s[floe_k::kMaxSlots];  // records in pinned host memory
-  __shared__ uint32_t ws8[kConsumerWarps];
-  __shared__ float2 xch[kPairs][2][8];  // phase B: upper-half partials of a pair's tile
+  __shared__ uint32_t rhost_s[floe_k::kMaxSlots];
+  __shared__ uint32_t slot_cnt[floe_k::kMaxSlots], kbase_s[floe_k::kMaxSlots],
+      kpos_s[floe_k::kMaxSlots];
+  __shared__ uint32_t n_list;
+  __shared__ uint64_t fullC[kMaxStages], emptyC[kMaxStages];
   __shared__ float redmax[kConsumerWarps];
-  __shared__ float red[2][2][8][kR];  // [group][batch parity][warp][record]
-  __shared__ uint32_t pv[8];  // plan values: 0 T, 1 own_b, 2 d_b, 3 D_b, 4 n_own, 5 P, 6 all_finite
-  __shared__ uint32_t slot_cnt[floe_k::kMaxSlots];
+  __shared__ float2 xch[kPairs][2][8];  // phase B: upper-half partials of a pair's tile
+  __shared__ float red[2][2][8][kR];    // phase C: [group][batch parity][warp][record]
 
   const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const uint32_t G = gridDim.x, b = blockIdx.x;
   const bool producer = warp == kConsumerWarps;
+  const bool router_warp = warp == kConsumerWarps + 1;
   const SmemLayout L = smem_layout(DH, a.ns, a.max_tiles, G);
   uint8_t *ring = smem + L.ring;
   float *hs = reinterpret_cast<float *>(smem + L.uni);  // phase A: h; phase B: x (f32) or xtab
   uint8_t *xtab = smem + L.uni;
   float *xs = reinterpret_cast<float *>(smem + L.xs);
-  uint32_t *emit_f = reinterpret_cast<uint32_t *>(smem + L.emit_f);
-  float *emit_v = reinterpret_cast<float *>(smem + L.emit_v);
-  uint32_t *tile_cnt = reinterpret_cast<uint32_t *>(smem + L.tile_cnt);
-  const __half **isrc = reinterpret_cast<const __half **>(smem + L.isrc);
-  float *iscale = reinterpret_cast<float *>(smem + L.iscale);
-  uint32_t *NB = reinterpret_cast<uint32_t *>(smem + L.plan);  // [G+1] per-CTA counts
-  uint32_t *SUp = NB + (G + 1);                                // [G+1] surplus prefix
-  uint32_t *TBp = SUp + (G + 1);                               // [G+1] unused spare
-  (void)TBp;
+  uint32_t *lf = reinterpret_cast<uint32_t *>(smem + L.lf);
+  float *lv = reinterpret_cast<float *>(smem + L.lv);
   const uint32_t ns = a.ns;
+  const uint32_t list_cap = kTileCh * a.max_tiles;
 
   // Streamed weights (read once per call) go through L2 as evict-first, so the
-  // ~165 MB per layer do not evict the kernel's code, the routing partials and
-  // the published lists (cold instruction fetches from DRAM showed up as
-  // ~2.5 us stalls at phase transitions in 40% of the CTAs).
+  // ~165 MB per layer do not evict the kernel's code, the routing partials or
+  // router_pred.
   const uint64_t l2_stream = floe_ptx::policy_evict_first();
   auto stage = [&](uint32_t u) { return ring + (u % ns) * TILE_B; };
   auto wait_full = [&](uint32_t u) {
@@ -503,34 +484,22 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   };
   // Phase C re-carves the ring plus the x-table area (both free once every K1
   // tile is consumed) into 4*DH-byte record stages with their own barriers:
-  // 11 records (176 KB) in flight at d_hidden 4096 instead of 8.
-  const uint32_t nsC = min((uint32_t)kMaxStagesC, (L.xs - L.ring) / REC_B);
+  // 12 records (192 KB) in flight at d_hidden 4096.
+  const uint32_t nsC = min((uint32_t)kMaxStages, (L.xs - L.ring) / REC_B);
   auto stageC = [&](uint32_t k) { return ring + (k % nsC) * REC_B; };
-  auto wait_fullC = [&](uint32_t k) {
-    floe_ptx::mbar_wait(&fullC[k % nsC], (k / nsC) & 1u, (4u << 28) | k);
-  };
-  auto wait_emptyC = [&](uint32_t k) {
-    if (k >= nsC) floe_ptx::mbar_wait(&emptyC[k % nsC], ((k / nsC) + 1) & 1u, (5u << 28) | k);
-  };
   auto issueC = [&](uint32_t k, const void *src, float scale) {
-    wait_emptyC(k);
-    if (k < 16) mark(a, 48 + (int)k);
+    if (k >= nsC) floe_ptx::mbar_wait(&emptyC[k % nsC], ((k / nsC) + 1) & 1u, (5u << 28) | k);
     stage_scale[k % nsC] = scale;
     floe_ptx::mbar_arrive_expect_tx(&fullC[k % nsC], REC_B);
     floe_ptx::bulk_g2s_hint(stageC(k), src, REC_B, &fullC[k % nsC], l2_stream);
   };
 
-  mark(a, 0);
-  if (a.phase_ns && t == 0) {  // diagnostics: which SM runs this CTA
-    uint32_t smid;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    a.phase_ns[blockIdx.x * kTraceSlots + 64] = smid;
-  }
   if (t == 0) {
+    mark(a, 0);
     for (uint32_t s = 0; s < ns; ++s) {
       floe_ptx::mbar_init(&full[s], 1);
       // released by all 16 consumer warps: count 8 from each warp of the
-      // owning pair (phases A/B), 1 from every warp (phase C)
+      // owning pair (phases A/B), 2 from each warp of the record group (C)
       floe_ptx::mbar_init(&empty[s], kConsumerWarps);
     }
     for (uint32_t s = 0; s < nsC; ++s) {
@@ -539,9 +508,32 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
     }
     floe_ptx::mbar_init(&hbar, 1);
     floe_ptx::mbar_init(&predbar, 1);
-    spec_ok = 1u;
+    floe_ptx::mbar_init(&bar1, 1);
+    floe_ptx::mbar_init(&routebar, 1);
+    floe_ptx::mbar_init(&lreset, 1);
+    floe_ptx::mbar_init(&listbar, 1);  // consumers: K1 done, own list final
+    floe_ptx::mbar_init(&pubbar, 1);   // warp 0: predicted partial published
     floe_ptx::fence_barrier_init();
+    spec_ok = 1u;
+    n_list = 0u;
     pdl_launch_dependents();
+  }
+  const uint32_t n_table = a.has_mixing ? a.n_experts : a.slots;
+  if (t < n_table) table_s[t] = a.table[t];
+  if (t < (uint32_t)floe_k::kMaxSlots) {
+    slot_cnt[t] = 0u;
+    kpos_s[t] = 0u;
+  }
+  for (uint32_t i = t; i < list_cap; i += kThreads) lf[i] = 0u;
+  __syncthreads();
+  if (!a.has_mixing && t < a.slots) {  // expert mode: the slots are the experts
+    const ExpertDesc &d = table_s[t];
+    const float thr = a.use_threshold ? a.threshold : d.threshold;
+    pthr_s[t] = ethr_s[t] = thr;
+    ptiles_s[t] = etiles_s[t] = reinterpret_cast<const uint8_t *>(d.tiles);
+    w_s[t] = 1.0f;
+    rec_s[t] = d.records;
+    rhost_s[t] = d.host_records;
   }
   __syncthreads();
 
@@ -553,143 +545,210 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   const uint32_t rpi = a.mix_f16 ? 2u : 1u;  // mixing rows per stage
   const uint32_t r_lo = floe_k::seg_begin(DH, b, G), r_hi = floe_k::seg_begin(DH, b + 1, G);
   const uint32_t nA = a.has_mixing ? (r_hi - r_lo + rpi - 1) / rpi : 0u;
-  const uint32_t uB = nA;
-  // Speculative K1: with a predicted routing (router_pred * h, known long
-  // before the mixing GEMV ends) the producer streams the first S K1 tiles
-  // of the predicted experts right behind the mixing rows, so the ring is
-  // full when the exact routing lands.  A misprediction costs S wasted
-  // stages: they are consumed unread and every tile is streamed again.
-  const bool spec = a.has_mixing && a.router_pred != nullptr;
-  const uint32_t S = spec ? min(nB, a.ns) : 0u;
+  const uint32_t uB = nA;  // first K1 ring use
 
   if (producer) {
     // =================== producer warp ===================
-    if (a.has_mixing && lane == 0) {
-      const uint32_t row_bytes = DH * (a.mix_f16 ? 2u : 4u);
-      const uint8_t *m = static_cast<const uint8_t *>(a.mixing);
-      // mixing rows are read-only weights: the first two stream in before the
-      // previous grid has finished (PDL); h (the previous layer's output)
-      // goes right after them so it is not queued behind the whole ring
-      const uint32_t early = min(nA, a.early);
-      for (uint32_t i = 0; i < nA; ++i) {
-        if (i == early) {
+    // lane 0 issues every copy; the whole warp computes the phase-C plan
+    if (lane == 0) {
+      uint32_t u = 0;
+      if (a.has_mixing) {
+        const uint32_t row_bytes = DH * (a.mix_f16 ? 2u : 4u);
+        const uint8_t *m = static_cast<const uint8_t *>(a.mixing);
+        // mixing rows are read-only weights: the first kEarly stream in before
+        // the previous grid has finished (PDL); h (the previous layer's output)
+        // goes right after them so it is not queued behind the whole ring
+        for (uint32_t i = 0; i < nA; ++i) {
+          if (i == min(nA, kEarly)) {
+            pdl_wait();
+            floe_ptx::mbar_arrive_expect_tx(&hbar, 4u * DH);
+            floe_ptx::bulk_g2s(hs, a.h, 4u * DH, &hbar);
+          }
+          const uint32_t r0 = r_lo + i * rpi, nr = min(rpi, r_hi - r0);
+          wait_empty(u);
+          issue(u++, m + (size_t)r0 * row_bytes, nr * row_bytes);
+        }
+        if (nA <= kEarly) {
           pdl_wait();
           floe_ptx::mbar_arrive_expect_tx(&hbar, 4u * DH);
           floe_ptx::bulk_g2s(hs, a.h, 4u * DH, &hbar);
         }
-        const uint32_t r0 = r_lo + i * rpi, nr = min(rpi, r_hi - r0);
-        wait_empty(i);
-        issue(i, m + (size_t)r0 * row_bytes, nr * row_bytes);
+        floe_ptx::mbar_wait(&predbar, 0, 6u << 28);  // predicted routing
+        mark(a, 16);
       }
-      if (nA <= early) {
-        pdl_wait();
-        floe_ptx::mbar_arrive_expect_tx(&hbar, 4u * DH);
-        floe_ptx::bulk_g2s(hs, a.h, 4u * DH, &hbar);
+      // K1 tiles of the predicted (layer) / given (expert) experts
+      for (uint32_t j = 0; j < nB; ++j) {
+        const TileRef tr = tile_ref(tile_lo + j, a.slots, a.di);
+        wait_empty(u);
+        issue(u++, ptiles_s[tr.slot] + (size_t)tr.t * TILE_B, TILE_B);
+      }
+      mark(a, 17);
+      if (a.has_mixing && !a.k1_only) {
+        floe_ptx::mbar_wait(&routebar, 0, 7u << 28);
+        if (!spec_ok)  // misprediction: the exact experts' tiles follow
+          for (uint32_t j = 0; j < nB; ++j) {
+            const TileRef tr = tile_ref(tile_lo + j, a.slots, a.di);
+            wait_empty(u);
+            issue(u++, etiles_s[tr.slot] + (size_t)tr.t * TILE_B, TILE_B);
+          }
       }
     }
-    if (spec && lane == 0) {
-      floe_ptx::mbar_wait(&predbar, 0, 6u << 28);
-      for (uint32_t j = 0; j < S; ++j) {  // waits on phase-A releases only
-        const TileRef tr = tile_ref(tile_lo + j, tps, a.di);
-        wait_empty(uB + j);
-        issue(uB + j, ptiles_s[tr.slot] + (size_t)tr.t * TILE_B, TILE_B);
-      }
-    }
-    __syncwarp();
-    abar();  // ALL#1: routing known
-    mark(a, 16);
+    if (a.k1_only) return;
+    // ---- phase C: the record ring fills as soon as K1 is done (every tile
+    // consumed, the list final)
+    floe_ptx::mbar_wait(&listbar, 0, 12u << 28);
+    const uint32_t n_own = n_list;
     if (lane == 0) {
-      const bool ok = spec_ok != 0u;
-      const uint32_t shift = ok ? 0u : S;  // ring uses taken by discarded stages
-      for (uint32_t j = ok ? S : 0u; j < nB; ++j) {
-        const TileRef tr = tile_ref(tile_lo + j, tps, a.di);
-        wait_empty(uB + shift + j);
-        issue(uB + shift + j, tiles_s[tr.slot] + (size_t)tr.t * TILE_B, TILE_B);
+      mark(a, 18);
+      // own kept records in list order; each CTA processes exactly its own:
+      // any cross-CTA balancing needs global reads, and those wait behind the
+      // SM's queued bulk copies for several us (measured: a published-count
+      // plan arrived 6-12 us after K1 and cost more than the tail it removed)
+      for (uint32_t k = 0; k < n_own; ++k) {
+        const uint32_t f = lf[k] & ~kValid, s2 = f / a.di, c = f - s2 * a.di;
+        issueC(k, rec_s[s2] + (size_t)c * 2 * DH, lv[k] * w_s[s2]);
       }
+      mark(a, 19);
     }
-    __syncwarp();
-    abar();  // ALL#2: K1 done, own list in smem
-    if (a.k1_only) {
-      abar();  // ALL#3
-      return;
-    }
-    // speculative prefetch of own records (before the plan is known)
-    uint32_t P = 0;
-    if (lane == 0) {
-      const uint32_t n_own = pv[4];
-      P = min(n_own, nsC);
-      for (uint32_t k = 0; k < P; ++k) issueC(k, isrc[k], iscale[k]);
-      pv[5] = P;
-
-    }
-    __syncwarp();
-    mark(a, 17);
-    abar();  // ALL#3: plan known
-    mark(a, 18);
-    const uint32_t own_b = pv[1], d_b = pv[2], D_b = pv[3], T = pv[0];
-    P = pv[5];
-    if (lane == 0)  // remaining own records
-      for (uint32_t k = P; k < own_b; ++k) issueC(k, isrc[k], iscale[k]);
-    __syncwarp();
-    mark(a, 19);
-    // pool records: 32 resolved in parallel, issued by lane 0
-    const uint32_t E0 = max(P, own_b);
-    for (uint32_t q = 0; q < d_b; q += 32) {
-      const uint32_t pi = D_b + q + lane;
-      const __half *src = nullptr;
-      float scale = 0.0f;
-      if (q + lane < d_b) {
-        uint32_t lo = 0, hi = G;  // SUp[lo] <= pi < SUp[hi]
-        while (hi - lo > 1) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (SUp[mid] <= pi) lo = mid;
-          else hi = mid;
-        }
-        const uint32_t bb = lo;
-        const uint32_t tb = (uint32_t)(((uint64_t)T * (bb + 1)) / G - ((uint64_t)T * bb) / G);
-        const uint32_t own_bb = max(min(NB[bb], nsC), min(NB[bb], tb));
-        const uint32_t first_tile = (uint32_t)(((uint64_t)NT * bb) / G);
-        const TileRef tr = tile_ref(first_tile, tps, a.di);
-        const uint32_t pos = tr.f0 + own_bb + (pi - SUp[bb]);
-        const uint32_t f = __ldcg(&a.kept_f[pos]);
-        const float v = __ldcg(&a.kept_v[pos]);
-        const uint32_t s = f / a.di, c = f % a.di;
-        src = rec_s[s] + (size_t)c * 2 * DH;
-        scale = v * w_s[s];
-      }
-      const uint32_t nq = min(32u, d_b - q);
-      for (uint32_t k = 0; k < nq; ++k) {
-        const unsigned long long sp =
-            __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(src), k);
-        const float sc = __shfl_sync(0xffffffffu, scale, k);
-        if (lane == 0) {
-          issueC(E0 + q + k, reinterpret_cast<const void *>(sp), sc);
-        }
-        __syncwarp();
-      }
-    }
-    mark(a, 20);
     return;
   }
 
-  // =================== consumer warps (threads 0..255) ===================
-  // expert descriptors, router slice
-  __shared__ ExpertDesc table_s[32];
-  const uint32_t n_table = a.has_mixing ? a.n_experts : a.slots;
-  if (t < n_table) table_s[t] = a.table[t];
+  if (router_warp) {
+    // =================== router warp (layer mode) ===================
+    if (!a.has_mixing) return;
+    pdl_wait();
+    // sum of the per-CTA partials of E logits, the same fixed order in every
+    // CTA; all loads in flight at once; lane e returns logit e
+    auto sum_partials = [&](const float *part) {
+      float lg = -__int_as_float(0x7f800000);
+      for (uint32_t e0 = 0; e0 < a.n_experts; e0 += 8) {
+        float sv[8];
+#pragma unroll
+        for (int ee = 0; ee < 8; ++ee) {
+          const uint32_t e = e0 + ee;
+          float pv[kMaxGrid / 32];
+#pragma unroll
+          for (int j = 0; j < kMaxGrid / 32; ++j) {
+            const uint32_t bb = lane + 32 * j;
+            pv[j] = (e < a.n_experts && bb < G) ? __ldcg(&part[e * kMaxGrid + bb]) : 0.0f;
+          }
+          float s = 0.0f;
+#pragma unroll
+          for (int j = 0; j < kMaxGrid / 32; ++j) s += pv[j];
+          sv[ee] = s;
+        }
+#pragma unroll
+        for (int ee = 0; ee < 8; ++ee) {
+          float s = sv[ee];
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+          if (lane == e0 + ee) lg = s;
+        }
+      }
+      return lg;
+    };
+    // ---- predicted routing: wait for every CTA's predicted partials
+    floe_ptx::mbar_wait(&pubbar, 0, 14u << 28);
+    if (lane == 0) {
+      const unsigned long long target = pc_target, t0 = gtime();
+      for (uint32_t it = 1;; ++it) {
+        unsigned long long v;
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.pcnt) : "memory");
+        if (v >= target) break;
+        if ((it & 255u) == 0 && gtime() - t0 > floe_ptx::kWatchdogNs)
+          floe_ptx::watchdog_fire("prediction", (uint32_t)(target / G), 0u);
+      }
+    }
+    __syncwarp();
+    {
+      float plg = sum_partials(a.pred_partial);
+      if (a.debug & 8u) plg = -plg;  // test hook: force a misprediction
+      const uint32_t ptaken = warp_topk(lane < a.n_experts ? plg : -__int_as_float(0x7f800000),
+                                        lane, a.n_experts, a.top_k);
+      if ((ptaken >> lane) & 1u) {
+        const uint32_t i = __popc(ptaken & ((1u << lane) - 1));
+        ptiles_s[i] = reinterpret_cast<const uint8_t *>(table_s[lane].tiles);
+        pthr_s[i] = a.use_threshold ? a.threshold : table_s[lane].threshold;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        ptaken_s = ptaken;
+        mark(a, 26);
+        floe_ptx::mbar_arrive(&predbar);
+      }
+    }
+    floe_ptx::mbar_wait(&bar1, 0, 10u << 28);
+    if (lane == 0) mark(a, 24);
+    // route (model.cpp:83-93) on the exact logits router * u
+    const float lg = sum_partials(a.partial);
+    // top_k (la.cpp:48-61: ties to the lower index, output ascending); softmax
+    // over the selected logits (la.cpp:37-46): mx, then the sum in ascending
+    // expert order
+    const uint32_t taken = warp_topk(lane < a.n_experts ? lg : -__int_as_float(0x7f800000), lane,
+                                     a.n_experts, a.top_k);
+    const bool mine = (taken >> lane) & 1u;
+    float mx = mine ? lg : -__int_as_float(0x7f800000);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    const float ex = mine ? expf(lg - mx) : 0.0f;
+    float sum = 0.0f;
+    for (uint32_t m = taken; m; m &= m - 1) sum += __shfl_sync(0xffffffffu, ex, __ffs(m) - 1);
+    if (mine) {
+      const uint32_t i = __popc(taken & ((1u << lane) - 1));  // rank = ascending position
+      const float w = ex / sum;
+      const ExpertDesc &d = table_s[lane];
+      w_s[i] = w;
+      rec_s[i] = d.records;
+      rhost_s[i] = d.host_records;
+      etiles_s[i] = reinterpret_cast<const uint8_t *>(d.tiles);
+      ethr_s[i] = a.use_threshold ? a.threshold : d.threshold;
+      if (b == 0) {
+        if (a.sel_out) {
+          a.sel_out[i] = lane;
+          a.w_out[i] = w;
+        }
+        if (a.sel_trace) a.sel_trace[i] = lane;
+        if (a.w_trace) a.w_trace[i] = w;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      spec_ok = taken == ptaken_s ? 1u : 0u;
+      mark(a, 25);
+      floe_ptx::mbar_arrive(&routebar);
+    }
+    return;
+  }
+
+  // =================== consumer warps (threads 0..511) ===================
   const uint32_t nrows = r_hi - r_lo;
   const bool rs_ok = a.has_mixing && nrows <= (uint32_t)kMaxRowsPerCta;
   if (rs_ok)
     for (uint32_t i = t; i < a.n_experts * kMaxRowsPerCta; i += kConsumers) {
       const uint32_t e = i / kMaxRowsPerCta, lr = i % kMaxRowsPerCta;
-      if (lr < nrows) rs[i] = a.router[(size_t)e * DH + r_lo + lr];
+      if (lr < nrows) {
+        rs[i] = a.router[(size_t)e * DH + r_lo + lr];
+        rps[i] = a.router_pred[(size_t)e * DH + r_lo + lr];
+      }
     }
   pdl_wait();  // from here on: workspace, inputs and outputs shared with the previous grid
-  cbar();
+  if (!a.has_mixing && a.y && !a.k1_only) {
+    // expert mode: CTA 0 zeroes y, the others check a flag before their final
+    // reduction; the call index comes from a counter every CTA bumps once
+    if (t == 0) y_target = atomicAdd(a.y_flag + 1, 1ull) / G + 1;
+    if (b == 0) {
+      for (uint32_t i = t; i < DH; i += kConsumers) a.y[i] = 0.0f;
+      cbar();
+      if (t == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a.y_flag), "l"(y_target)
+                     : "memory");
+      }
+    }
+  }
 
-  // ---- K1 operand setup: x -> max|x| -> limbs (IMMA B fragments) + span
-  // sums.  It runs on warps 8..15 while warps 0..7 route (layer mode), so it
-  // is off the critical path between grid barrier 1 and the first K1 tile.
+  // ---- K1 operand setup (warps 8..15): x -> max|x| -> limbs (IMMA B
+  // fragments) + span sums
   const float *xg = a.has_mixing ? a.u : a.x;
   const bool setup_warp = warp >= kConsumerWarps / 2;
   const uint32_t ts = t - kConsumers / 2;  // setup thread index (warps 8..15)
@@ -737,49 +796,49 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
     bool fin_all;
     float S, invS;
     x_scale(fin_all, S, invS);
-      if (act) {
-        if (fin_all) {
-          int X[16];
+    if (act) {
+      if (fin_all) {
+        int X[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) X[i] = __float2int_rn(xv[i] * S);
-          const uint32_t p = span >> 1, sodd = span & 1;
-          uint4 *xt = reinterpret_cast<uint4 *>(xtab) + (p * 2 + sodd) * 32;
-          // limb bytes of the 16 elements: lb[l][i] for element i
-          uint32_t lw[3][4][2];  // [limb][m][j]: element 4b + 2m + j, byte b
+        for (int i = 0; i < 16; ++i) X[i] = __float2int_rn(xv[i] * S);
+        const uint32_t p = span >> 1, sodd = span & 1;
+        uint4 *xt = reinterpret_cast<uint4 *>(xtab) + (p * 2 + sodd) * 32;
+        // limb bytes of the 16 elements: lb[l][i] for element i
+        uint32_t lw[3][2][2];  // [limb][m][j]: element 4b + 2m + j, byte b
 #pragma unroll
-          for (int l = 0; l < 3; ++l)
+        for (int l = 0; l < 3; ++l)
 #pragma unroll
-            for (int m = 0; m < 2; ++m)
+          for (int m = 0; m < 2; ++m)
 #pragma unroll
-              for (int j = 0; j < 2; ++j) lw[l][m][j] = 0;
+            for (int j = 0; j < 2; ++j) lw[l][m][j] = 0;
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int v = X[i];
-            const int l0 = ((v + 128) & 255) - 128;
-            const int r1 = (v - l0) >> 8;
-            const int l1 = ((r1 + 128) & 255) - 128;
-            const int l2 = (r1 - l1) >> 8;
-            const int bb = i >> 2, m = (i >> 1) & 1, j = i & 1;
-            lw[0][m][j] |= (uint32_t)(l0 & 255) << (8 * bb);
-            lw[1][m][j] |= (uint32_t)(l1 & 255) << (8 * bb);
-            lw[2][m][j] |= (uint32_t)(l2 & 255) << (8 * bb);
-          }
-          // column n -> (class, limb): 0 (x1,L0) 1 (x1,L1) 2 (x4,L0) 3 (x4,L1)
-          // 4 (x1,L2) 6 (x4,L2); 5, 7 zero.  Class x1 rides in b0 (j = 0, the
-          // even elements), class x4 in b1 (j = 1, the odd elements).
-#pragma unroll
-          for (int n = 0; n < 8; ++n) {
-            const int lim = n == 0 || n == 2 ? 0 : (n == 1 || n == 3 ? 1 : 2);
-            const bool c1 = n == 0 || n == 1 || n == 4, c4 = n == 2 || n == 3 || n == 6;
-            xt[4 * n + tig] = make_uint4(c1 ? lw[lim][0][0] : 0u, c4 ? lw[lim][0][1] : 0u,
-                                         c1 ? lw[lim][1][0] : 0u, c4 ? lw[lim][1][1] : 0u);
-          }
-        } else {
-          float *xf = hs + 64 * span + 16 * tig;
-#pragma unroll
-          for (int i = 0; i < 16; ++i) xf[i] = xv[i];
+        for (int i = 0; i < 16; ++i) {
+          const int v = X[i];
+          const int l0 = ((v + 128) & 255) - 128;
+          const int r1 = (v - l0) >> 8;
+          const int l1 = ((r1 + 128) & 255) - 128;
+          const int l2 = (r1 - l1) >> 8;
+          const int bb = i >> 2, m = (i >> 1) & 1, j = i & 1;
+          lw[0][m][j] |= (uint32_t)(l0 & 255) << (8 * bb);
+          lw[1][m][j] |= (uint32_t)(l1 & 255) << (8 * bb);
+          lw[2][m][j] |= (uint32_t)(l2 & 255) << (8 * bb);
         }
+        // column n -> (class, limb): 0 (x1,L0) 1 (x1,L1) 2 (x4,L0) 3 (x4,L1)
+        // 4 (x1,L2) 6 (x4,L2); 5, 7 zero.  Class x1 rides in b0 (j = 0, the
+        // even elements), class x4 in b1 (j = 1, the odd elements).
+#pragma unroll
+        for (int n = 0; n < 8; ++n) {
+          const int lim = n == 0 || n == 2 ? 0 : (n == 1 || n == 3 ? 1 : 2);
+          const bool c1 = n == 0 || n == 1 || n == 4, c4 = n == 2 || n == 3 || n == 6;
+          xt[4 * n + tig] = make_uint4(c1 ? lw[lim][0][0] : 0u, c4 ? lw[lim][0][1] : 0u,
+                                       c1 ? lw[lim][1][0] : 0u, c4 ? lw[lim][1][1] : 0u);
+        }
+      } else {
+        float *xf = hs + 64 * span + 16 * tig;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) xf[i] = xv[i];
       }
+    }
     float s16 = 0.0f;
 #pragma unroll
     for (int i = 0; i < 16; ++i) s16 += xv[i];
@@ -791,41 +850,25 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   // ============================ phase A: mixing ============================
   if (a.has_mixing) {
     floe_ptx::mbar_wait(&hbar, 0, 3u << 28);
-    if (spec) {
-      // predicted logits router_pred * h (one warp per expert)
-      for (uint32_t e = warp; e < a.n_experts; e += kConsumerWarps) {
-        const float4 *rp = reinterpret_cast<const float4 *>(a.router_pred + (size_t)e * DH);
-        float p0 = 0.0f, p1 = 0.0f;
-#pragma unroll 8
-        for (uint32_t k = lane; k < DH / 4; k += 32) {
-          const float4 w = __ldg(rp + k);
-          const float4 hv = *reinterpret_cast<const float4 *>(hs + 4 * k);
-          p0 = fmaf(w.x, hv.x, p0);
-          p1 = fmaf(w.y, hv.y, p1);
-          p0 = fmaf(w.z, hv.z, p0);
-          p1 = fmaf(w.w, hv.w, p1);
-        }
-        float pe = p0 + p1;
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) pe += __shfl_xor_sync(0xffffffffu, pe, o);
-        if (lane == 0) plog[e] = pe;
+    // predicted logits router_pred * h (router_pred = router + router *
+    // mixing), distributed like the exact ones: this CTA's rows of h give
+    // per-CTA partials, published with a counter; the router warp sums them
+    // in the background while phase A streams
+    if (warp == 0) {
+      for (uint32_t e = lane; e < a.n_experts; e += 32) {
+        float s = 0.0f;
+        for (uint32_t lr = 0; lr < nrows; ++lr)
+          s = fmaf(rs_ok ? rps[e * kMaxRowsPerCta + lr] : a.router_pred[(size_t)e * DH + r_lo + lr],
+                   hs[r_lo + lr], s);
+        a.pred_partial[e * kMaxGrid + b] = s;
       }
-      cbar();
-      if (warp == 1) {
-        __syncwarp();
-        float lg = lane < a.n_experts ? plog[lane] : 0.0f;
-        if (a.debug & 8u) lg = -lg;  // test hook: force a misprediction
-        const uint32_t taken = warp_topk(lg, lane, a.n_experts, a.top_k);
-        if ((taken >> lane) & 1u) {
-          const uint32_t i = __popc(taken & ((1u << lane) - 1));
-          psel_s[i] = lane;
-          ptiles_s[i] = reinterpret_cast<const uint8_t *>(table_s[lane].tiles);
-        }
-        __syncwarp();
-        if (lane == 0) {
-          ptaken_s = taken;
-          floe_ptx::mbar_arrive(&predbar);
-        }
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        const unsigned long long old = atomicAdd(a.pcnt, 1ull);
+        pc_target = (old / G + 1) * G;  // this call's last publication
+        mark(a, 7);
+        floe_ptx::mbar_arrive(&pubbar);
       }
     }
     float pl = 0.0f;  // lane e < E: this warp's partial logit e
@@ -834,6 +877,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
     // row `sub` of the item (f16: 2 rows per stage; f32: 1 row, sub 1 idles)
     for (uint32_t i = pair; i < nA; i += kPairs) {
       wait_full(i);
+      if (i == 0 && t == 0) mark(a, 8);
       const uint32_t r0 = r_lo + i * rpi, nr = min(rpi, r_hi - r0);
       const bool mine = sub < nr;
       float acc0 = 0.0f, acc1 = 0.0f;
@@ -889,135 +933,50 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
       float s = 0.0f;
 #pragma unroll
       for (int w = 0; w < kConsumerWarps; ++w) s += plw[w][t];
-      a.partial[t * kMaxGrid + b] = s;  // [expert][CTA]: coalesced reads below
+      a.partial[t * kMaxGrid + b] = s;  // [expert][CTA]: coalesced reads by the router warp
     }
-    mark(a, 1);
+    if (t == 0) mark(a, 1);
     cbar();
-    if (t == 0) grid_arrive_wait(a.bar, G);
+    if (t == 0) {
+      grid_arrive_wait(a.bar, G);  // u, y = u and the partials of every CTA
+      mark(a, 2);
+      floe_ptx::mbar_arrive(&bar1);
+    }
     cbar();
-    mark(a, 6);
-    // route (model.cpp:83-93): every CTA sums the partials in the same order
-    if (setup_warp) setup1();
-    else
-    for (uint32_t e = warp; e < a.n_experts; e += kConsumerWarps / 2) {
-      float pv8[kMaxGrid / 32];  // all loads in flight at once
-#pragma unroll
-      for (int j = 0; j < kMaxGrid / 32; ++j) {
-        const uint32_t bb = lane + 32 * j;
-        pv8[j] = bb < G ? __ldcg(&a.partial[e * kMaxGrid + bb]) : 0.0f;
-      }
-      float s = 0.0f;
-#pragma unroll
-      for (int j = 0; j < kMaxGrid / 32; ++j) s += pv8[j];
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) logits[e] = s;
-    }
-    if (t == 0) mark(a, 12);  // warp 0's partial sums loaded
-    cbar();
-    mark(a, 13);              // all warps' partial sums loaded
-    mark(a, 65);              // (diagnostic: back-to-back marks)
-    if (setup_warp) setup2();
-    if (warp == 1) {  // (not warp 0: it shares SMSP 0 with the producer warp)
-      // top_k (la.cpp:48-61: ties to the lower index, output ascending) as k
-      // warp arg-max rounds; softmax over the selected logits (la.cpp:37-46)
-      __syncwarp();  // converged: otherwise the shuffles take the BRA.DIV slow path
-      const float lg = lane < a.n_experts ? logits[lane] : -__int_as_float(0x7f800000);
-      const uint32_t taken = warp_topk(lg, lane, a.n_experts, a.top_k);
-      if (spec && lane == 0) {
-        spec_ok = taken == ptaken_s ? 1u : 0u;  // read by all after ALL#1
-        if (a.phase_ns) a.phase_ns[blockIdx.x * kTraceSlots + 71] = spec_ok + 1u;
-      }
-      if (lane == 0 && a.phase_ns) a.phase_ns[blockIdx.x * kTraceSlots + 14] = gtime();
-      // softmax over the selected logits in registers (no local-memory arrays:
-      // a cold stack line costs a DRAM round trip on the routing critical path).
-      // mx first, then the sum in ascending expert order, as la.cpp:37-46.
-      const bool mine = (taken >> lane) & 1u;
-      float mx = mine ? lg : -__int_as_float(0x7f800000);
-#pragma unroll 1
-      for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      const float ex = mine ? expf(lg - mx) : 0.0f;
-      float sum = 0.0f;
-      for (uint32_t m = taken; m; m &= m - 1) sum += __shfl_sync(0xffffffffu, ex, __ffs(m) - 1);
-      if (mine) {
-        const uint32_t i = __popc(taken & ((1u << lane) - 1));  // rank = ascending position
-        const float w = ex / sum;
-        sel_s[i] = lane;
-        w_s[i] = w;
-        if (i == 0) mark(a, 15);
-        if (b == 0) {
-          if (a.sel_out) {
-            a.sel_out[i] = lane;
-            a.w_out[i] = w;
-          }
-          if (a.sel_trace) a.sel_trace[i] = lane;
-          if (a.w_trace) a.w_trace[i] = w;
-        }
-      }
-    }
-  } else {
-    if (t < a.slots) {
-      sel_s[t] = t;
-      w_s[t] = 1.0f;
-    }
-    if (b == 0 && a.y && !a.k1_only)
-      for (uint32_t i = t; i < DH; i += kConsumers) a.y[i] = 0.0f;  // before barrier 2
   }
+
+  // ---- K1 setup: x limbs, span sums, epilogue multipliers
+  if (setup_warp) setup1();
   cbar();
-  // every consumer warp: the K1 epilogue multipliers of its lane
+  if (setup_warp) setup2();
+  cbar();
+  if (t == 0) mark(a, 3);
   float mult, zx;
   bool all_finite;
-  auto k1_multipliers = [&]() {
+  {
     float S, invS;
     x_scale(all_finite, S, invS);
     const uint32_t mytig = lane & 3;
     // column pair of this lane (see span_step): (c1L0,c1L1) (c4L0,c4L1) (c1L2,-) (c4L2,-)
     mult = mytig == 0 ? invS : (mytig == 1 ? 0.25f * invS : (mytig == 2 ? 65536.0f * invS : 16384.0f * invS));
     zx = mytig == 0 ? 1.0f : 0.0f;
-  };
-  if (t < a.slots) {
-    const ExpertDesc &d = table_s[sel_s[t]];
-    rec_s[t] = d.records;
-    rhost_s[t] = d.host_records;
-    tiles_s[t] = reinterpret_cast<const uint8_t *>(d.tiles);
-    thr_s[t] = a.use_threshold ? a.threshold : d.threshold;
-    slot_cnt[t] = 0;
   }
-  mark(a, 2);
-  abar();  // ALL#1: the producer starts streaming K1 tiles
-  if (!a.has_mixing) {  // expert mode: the setup runs while the first tiles stream in
-    if (setup_warp) setup1();
-    cbar();
-    if (setup_warp) setup2();
-    cbar();
-  }
-  k1_multipliers();
 
   // ============================ phase B: K1 ================================
-  // tile j (stage use uB + j) belongs to pair (uB + j) % 8: with ns a multiple
+  // tile j (ring use u0 + j) belongs to pair (u0 + j) % 8: with ns a multiple
   // of 8, every stage is consumed by ONE pair in phases A and B, so a warp
   // never waits on a stage whose previous fill it has not consumed itself
   // (mbarrier parity waits cannot tell phase k from phase k+2).  Warp `sub`
   // of the pair computes span half `sub`; the upper half's partials go
   // through xch (double-buffered by the pair's tile parity) to the lower warp,
-  // which thresholds and emits.
-  {
+  // which thresholds and appends kept channels to the CTA's list.
+  auto k1_pass = [&](uint32_t u0, const float *thr_tab) {
     const uint32_t pair = warp % kPairs, sub = warp / kPairs;
-    // a misprediction: the S speculative stages are consumed unread (each by
-    // its owning pair) and the tiles follow at ring uses uB + S ...
-    const uint32_t skip = spec_ok ? 0u : S;
-    for (uint32_t j = (pair + kPairs - uB % kPairs) % kPairs; j < skip; j += kPairs) {
-      wait_full(uB + j);
-      __syncwarp();
-      if (lane == 0) floe_ptx::mbar_arrive_cnt(&empty[(uB + j) % ns], kPairs);
-    }
-    const uint32_t uB2 = uB + skip;
     uint32_t n = 0;  // tiles this pair has done
-    for (uint32_t j = (pair + kPairs - uB2 % kPairs) % kPairs; j < nB; j += kPairs, ++n) {
-      const uint32_t u = uB2 + j;
-      const TileRef tr = tile_ref(tile_lo + j, tps, a.di);
+    for (uint32_t j = (pair + kPairs - u0 % kPairs) % kPairs; j < nB; j += kPairs, ++n) {
+      const uint32_t u = u0 + j;
+      const TileRef tr = tile_ref(tile_lo + j, a.slots, a.di);
       wait_full(u);
-      if (n == 0 && warp == 0) mark(a, 7);
       float2 v2 = all_finite ? k1_tile<DH>(stage(u), xtab, xs, mult, zx, lane, sub)
                              : k1_tile_f32<DH>(stage(u), hs, lane, sub);
       __syncwarp();
@@ -1030,7 +989,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
       v2.y += o2.y;
       const uint32_t g = lane >> 2;
       const bool q0 = (lane & 3) == 0;
-      const float thr = thr_s[tr.slot];
+      const float thr = thr_tab[tr.slot];
       // model.cpp:135: `if (fabs(v) < t) continue;` -> ties and NaN are kept
       const bool va = q0 && g < tr.nc, vb = q0 && g + 8 < tr.nc;
       const bool ka = va && !(fabsf(v2.x) < thr), kb = vb && !(fabsf(v2.y) < thr);
@@ -1044,55 +1003,87 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
         if (vb) a.mask_out[o + g + 8] = kb ? 1 : 0;
       }
       const uint32_t ba = __ballot_sync(0xffffffffu, ka), bbal = __ballot_sync(0xffffffffu, kb);
+      const uint32_t na = __popc(ba), cnt = na + __popc(bbal);
+      if (cnt == 0) continue;
+      uint32_t base = 0;
+      if (lane == 0) {
+        base = atomicAdd(&n_list, cnt);
+        atomicAdd(&slot_cnt[tr.slot], cnt);
+      }
+      base = __shfl_sync(0xffffffffu, base, 0);
       const uint32_t lt = (1u << lane) - 1;
-      const uint32_t na = __popc(ba);
       if (ka) {
-        emit_f[kTileCh * j + __popc(ba & lt)] = tr.f0 + g;
-        emit_v[kTileCh * j + __popc(ba & lt)] = v2.x;
+        const uint32_t pos = base + __popc(ba & lt);
+        lv[pos] = v2.x;
+        lf[pos] = (tr.f0 + g) | kValid;
       }
       if (kb) {
-        emit_f[kTileCh * j + na + __popc(bbal & lt)] = tr.f0 + g + 8;
-        emit_v[kTileCh * j + na + __popc(bbal & lt)] = v2.y;
+        const uint32_t pos = base + na + __popc(bbal & lt);
+        lv[pos] = v2.y;
+        lf[pos] = (tr.f0 + g + 8) | kValid;
       }
-      if (lane == 0) tile_cnt[j] = na + __popc(bbal);
+    }
+  };
+  k1_pass(uB, pthr_s);
+  cbar();
+  if (a.has_mixing) {
+    floe_ptx::mbar_wait(&routebar, 0, 11u << 28);  // exact routing known
+    if (!spec_ok) {
+      // misprediction: drop the list, K1 again on the exact experts (their
+      // tiles follow the predicted ones in the ring)
+      for (uint32_t i = t; i < list_cap; i += kConsumers) lf[i] = 0u;
+      if (t < (uint32_t)floe_k::kMaxSlots) slot_cnt[t] = 0u;
+      cbar();
+      if (t == 0) {
+        n_list = 0u;
+        floe_ptx::mbar_arrive(&lreset);
+      }
+      cbar();
+      k1_pass(uB + nB, ethr_s);
+      cbar();
     }
   }
-  mark(a, 3);
-  cbar();
-  // own list: totals, per-slot counts, the producer's issue list (record
-  // address, v * routing weight) in emission order, and the compacted list at
-  // the CTA's flattened start for the other CTAs (pool)
-  const uint32_t F_b = nB ? tile_ref(tile_lo, tps, a.di).f0 : 0u;
-  {
-    uint32_t base = 0;
-    for (uint32_t j = 0; j < nB; ++j) {
-      const uint32_t cnt = tile_cnt[j];
-      if ((j % kConsumerWarps) == warp && lane < cnt) {
-        const TileRef tr = tile_ref(tile_lo + j, tps, a.di);
-        const uint32_t f = emit_f[kTileCh * j + lane];
-        const float v = emit_v[kTileCh * j + lane];
-        isrc[base + lane] = rec_s[tr.slot] + (size_t)(f - tr.slot * a.di) * 2 * DH;
-        iscale[base + lane] = v * w_s[tr.slot];
-        a.kept_f[F_b + base + lane] = f;
-        a.kept_v[F_b + base + lane] = v;
-        if (lane == 0) atomicAdd(&slot_cnt[tr.slot], cnt);
-      }
-      base += cnt;
-    }
-    if (t == 0) pv[4] = base;
+  const uint32_t n_items = n_list;
+  if (t == 0) {
+    mark(a, 4);
+    if (a.phase_ns) a.phase_ns[b * kTraceSlots + 9] = n_items;  // (a count, not a time)
+    if (!a.k1_only) floe_ptx::mbar_arrive(&listbar);  // the producer streams the own records
   }
-  cbar();
-  abar();  // ALL#2: the producer prefetches own records
-  for (uint32_t s = t; s < a.slots; s += kConsumers) a.seg_count[s * G + b] = slot_cnt[s];
-  cbar();
-  mark(a, 8);
-  unsigned long long bar_target = 0;
-  if (t == 0) bar_target = grid_arrive(a.bar, G);
+
+  // ---- per-call accounting (the calls / kept totals behind the byte
+  // identity, HBM vs PCIe record counts, kept ids and counts)
+  if (t == 0 && a.stats && !a.k1_only) {
+    if (b == 0) atomicAdd(&a.stats[0], 1ull);
+    atomicAdd(&a.stats[1], (unsigned long long)n_items);
+  }
+  if (a.place_acc && t < a.slots && slot_cnt[t])
+    atomicAdd(&a.place_acc[rhost_s[t] ? 1 : 0], (unsigned long long)slot_cnt[t]);
+  if (a.kept_out || a.n_kept_out) {
+    if (t < a.slots) kbase_s[t] = slot_cnt[t] ? atomicAdd(&a.kcount[t], slot_cnt[t]) : 0u;
+    cbar();
+    if (a.kept_out)
+      for (uint32_t i = t; i < n_items; i += kConsumers) {
+        const uint32_t f = lf[i] & ~kValid, s = f / a.di;
+        const uint32_t pos = kbase_s[s] + atomicAdd(&kpos_s[s], 1u);
+        a.kept_out[(size_t)s * a.di + pos] = f - s * a.di;
+      }
+    cbar();
+    if (t == 0) {
+      __threadfence();
+      const unsigned long long tk = atomicAdd(a.tick, 1ull);
+      if (tk % G == G - 1) {  // the last CTA of this call: publish and reset
+        __threadfence();
+        for (uint32_t s = 0; s < a.slots; ++s) {
+          const uint32_t nk = atomicExch(&a.kcount[s], 0u);
+          if (a.n_kept_out) a.n_kept_out[s] = nk;
+        }
+      }
+    }
+  }
+  if (a.k1_only) return;
 
   // ============================ phase C: K2 ================================
-  // Ring items: the first P own records (prefetched before the barrier and
-  // owned whatever the plan says), then the rest of the own share, then pool
-  // records.  The first P are processed while the grid barrier completes.
+  // Ring items: the CTA's own kept records in list order (ring use uC + k).
   // Two groups of 8 warps take alternate records (group g: items g, g+2, ...)
   // so each record costs the bookkeeping of 8 warps, not 16; thread gt of a
   // group owns elements [EPT2 gt, EPT2 gt + EPT2) of both record halves.
@@ -1111,12 +1102,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
 #pragma unroll
     for (int i = 0; i < EPT2 / 2; ++i) y2[i] = make_float2(0.0f, 0.0f);
   }
-  const uint32_t P = a.k1_only ? 0u : min(pv[4], nsC);
-  uint32_t stg = grp % nsC, ph = 0;  // ring position of item k = grp + 2i (no divisions)
+  uint32_t stg = grp % nsC, ph = 0;  // ring position of item grp + 2i
   uint32_t batch = 0, processed = 0;
-  auto run_items = [&](uint32_t i_begin, uint32_t i_end) {
-  for (uint32_t i0 = i_begin; i0 < i_end; i0 += kR, ++batch) {
-    if (batch < 6 && grp == 0) mark(a, 24 + 4 * (int)batch);  // batch start
+  const uint32_t n_mine = n_items > grp ? (n_items - grp + 1) / 2 : 0u;
+  for (uint32_t i0 = 0; i0 < n_mine; i0 += kR, ++batch) {
     Vec dv[kR][2];
     float gp[kR], sc[kR];
     bool proc[kR];
@@ -1125,33 +1114,27 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
       gp[r] = 0.0f;
       sc[r] = 0.0f;
       dv[r][0] = dv[r][1] = Vec{};
-      const uint32_t k = grp + 2 * (i0 + r);
-      proc[r] = i0 + r < i_end;
+      proc[r] = i0 + r < n_mine;
       if (proc[r]) {
-        floe_ptx::mbar_wait(&fullC[stg], ph, (4u << 28) | k);
-        if (k == 0) mark(a, 10);
+        floe_ptx::mbar_wait(&fullC[stg], ph, (4u << 28) | (grp + 2 * (i0 + r)));
+        if (i0 + r == 0 && grp == 0 && t == 0) mark(a, 5);
         sc[r] = stage_scale[stg];
-        Vec g0{}, g1{};
-        if (proc[r] && !(a.debug & 2u)) {
-          const Vec *rec = reinterpret_cast<const Vec *>(ring + stg * REC_B);
-          g0 = rec[2 * gt];
-          g1 = rec[2 * gt + 1];
-          dv[r][0] = rec[512 + 2 * gt];
-          dv[r][1] = rec[512 + 2 * gt + 1];
-        }
+        const Vec *rec = reinterpret_cast<const Vec *>(stageC(stg));
+        const Vec g0 = rec[2 * gt];
+        const Vec g1 = rec[2 * gt + 1];
+        dv[r][0] = rec[512 + 2 * gt];
+        dv[r][1] = rec[512 + 2 * gt + 1];
         __syncwarp();
         if (lane == 0) mbar_arrive1(&emptyC[stg]);  // this warp's slice is in registers
-        if (proc[r]) {
-          const __half2 *h0 = reinterpret_cast<const __half2 *>(&g0);
-          const __half2 *h1 = reinterpret_cast<const __half2 *>(&g1);
-          float2 acc = make_float2(0.0f, 0.0f);
+        const __half2 *h0 = reinterpret_cast<const __half2 *>(&g0);
+        const __half2 *h1 = reinterpret_cast<const __half2 *>(&g1);
+        float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
-          for (int jj = 0; jj < EPT2 / 4; ++jj) {
-            acc = __ffma2_rn(__half22float2(h0[jj]), x2[jj], acc);
-            acc = __ffma2_rn(__half22float2(h1[jj]), x2[EPT2 / 4 + jj], acc);
-          }
-          gp[r] = acc.x + acc.y;
+        for (int jj = 0; jj < EPT2 / 4; ++jj) {
+          acc = __ffma2_rn(__half22float2(h0[jj]), x2[jj], acc);
+          acc = __ffma2_rn(__half22float2(h1[jj]), x2[EPT2 / 4 + jj], acc);
         }
+        gp[r] = acc.x + acc.y;
         stg += 2;
         if (stg >= nsC) {
           stg -= nsC;
@@ -1159,7 +1142,6 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
         }
       }
     }
-    if (batch < 6 && grp == 0) mark(a, 25 + 4 * (int)batch);  // batch data in registers
     // transposed warp reduction of kR values: lanes 8r hold record r's warp sum
 #pragma unroll
     for (int sft = 16, cnt = kR / 2; cnt >= 1; sft >>= 1, cnt >>= 1) {
@@ -1176,7 +1158,6 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
       gp[0] += __shfl_xor_sync(0xffffffffu, gp[0], sft);
     if ((lane & (32 / kR - 1)) == 0) red[grp][batch & 1][gw][lane / (32 / kR)] = gp[0];
     gbar(grp);  // the group's partials for this batch (double-buffered: one barrier)
-    if (batch < 6 && grp == 0) mark(a, 26 + 4 * (int)batch);
     // lane l: record r = l / 8, warp partial l % 8 -> lanes 8r finish record r
     // (block sum in a fixed order, silu, scale) and broadcast its coefficient
     float g = red[grp][batch & 1][lane % 8][min(lane / 8, (uint32_t)kR - 1)];
@@ -1206,89 +1187,21 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
         y2[EPT2 / 4 + jj] = __ffma2_rn(a2, __half22float2(e1[jj]), y2[EPT2 / 4 + jj]);
       }
     }
-    if (batch < 6 && grp == 0) mark(a, 27 + 4 * (int)batch);  // batch done
   }
-  };
-  const uint32_t n1 = P > grp ? (P - grp + 1) / 2 : 0u;  // this group's items < P
-  run_items(0, n1);
-  mark(a, 21);
-  if (t == 0) grid_wait(a.bar, bar_target, G);
-  cbar();
-  mark(a, 4);
-  // ------------------------------ the plan ---------------------------------
-  // n_bb per CTA; targets t_bb = T(bb+1)/G - T bb/G; every CTA keeps its
-  // first min(n_bb, nsC) entries (already streamed and processed) and up to
-  // its target: own_bb = max(min(n_bb, nsC), min(n_bb, t_bb)); the surplus
-  // entries own_bb..n_bb-1 of every CTA form the pool, handed out to the
-  // deficits t_bb - own_bb in CTA order until it runs out.
-  uint32_t nb_t = 0;
-  if (t < G)
-    for (uint32_t s = 0; s < a.slots; ++s) nb_t += __ldcg(&a.seg_count[s * G + t]);
-  uint32_t T;
-  const uint32_t npre = cscan(nb_t, ws8, &T);
-  (void)npre;
-  uint32_t sur = 0, def = 0;
-  if (t < G) {
-    NB[t] = nb_t;
-    const uint32_t tb = (uint32_t)(((uint64_t)T * (t + 1)) / G - ((uint64_t)T * t) / G);
-    const uint32_t own = max(min(nb_t, nsC), min(nb_t, tb));
-    sur = nb_t - own;
-    def = tb > own ? tb - own : 0u;
-  }
-  uint32_t SUT, DT;
-  const uint32_t su_pre = cscan(sur, ws8, &SUT);
-  const uint32_t d_pre = cscan(def, ws8, &DT);
-  if (t < G) SUp[t] = su_pre;
-  if (t == 0) SUp[G] = SUT;
-  if (t == b) {
-    pv[0] = T;
-    pv[1] = nb_t - sur;                                // own_b
-    pv[2] = d_pre < SUT ? min(def, SUT - d_pre) : 0u;  // d_b (the pool may run out)
-    pv[3] = d_pre;                                     // D_b
-  }
-  if (b == 0) {
-    if (t == 0 && a.stats) {
-      atomicAdd(&a.stats[0], 1ull);
-      atomicAdd(&a.stats[1], (unsigned long long)T);
-    }
-    if ((a.n_kept_out || a.place_acc) && warp < a.slots) {
-      uint32_t n = 0;
-      for (uint32_t bb = lane; bb < G; bb += 32) n += __ldcg(&a.seg_count[warp * G + bb]);
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
-      if (lane == 0 && a.n_kept_out) a.n_kept_out[warp] = n;
-      if (lane == 0 && a.place_acc)  // where this slot's kept records are read from
-        atomicAdd(&a.place_acc[table_s[sel_s[warp]].host_records ? 1 : 0],
-                  (unsigned long long)n);
-    }
-  }
-  if (a.kept_out && warp < a.slots) {
-    // own entries of slot `warp` -> kept_out[slot][prefix over lower CTAs + j]
-    uint32_t base = 0;
-    for (uint32_t bb = lane; bb < b; bb += 32) base += __ldcg(&a.seg_count[warp * G + bb]);
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) base += __shfl_xor_sync(0xffffffffu, base, o);
-    uint32_t k = 0;
-    for (uint32_t j = 0; j < nB; ++j) {
-      const TileRef tr = tile_ref(tile_lo + j, tps, a.di);
-      const uint32_t cnt = tile_cnt[j];
-      if (tr.slot == warp) {
-        if (lane < cnt) a.kept_out[(size_t)warp * a.di + base + k + lane] = emit_f[kTileCh * j + lane] - warp * a.di;
-        k += cnt;
+  if (t == 0) mark(a, 6);
+  if (!a.has_mixing) {  // expert mode: y was zeroed by CTA 0 for this call
+    if (t == 0) {
+      const unsigned long long t0 = gtime();
+      for (uint32_t it = 1;; ++it) {
+        unsigned long long v;
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a.y_flag) : "memory");
+        if (v >= y_target) break;
+        if ((it & 255u) == 0 && gtime() - t0 > floe_ptx::kWatchdogNs)
+          floe_ptx::watchdog_fire("y flag", (uint32_t)y_target, 0u);
       }
     }
+    cbar();
   }
-  cbar();
-  mark(a, 9);
-  abar();  // ALL#3: the producer streams the rest
-  if (a.k1_only) return;
-
-  // ---- phase C, segment 2: the rest of the own share, then pool records
-  const uint32_t own_b = pv[1], d_b = pv[2];
-  const uint32_t n_items = own_b + d_b;  // own_b >= P by construction of the plan
-  const uint32_t n_mine = n_items > grp ? (n_items - grp + 1) / 2 : 0u;
-  run_items(n1, n_mine);
-  mark(a, 5);
   if (processed > 0) {
     float *yo = a.y + EPT2 * gt;
 #pragma unroll

@@ -87,7 +87,7 @@ def ep_moe_layer(h, router, mixing, top_k: int, expert_fn: Callable, n_experts: 
     back = _a2a(torch, dist, group, out, s_list, r_list) if world > 1 else out
     contrib = torch.empty_like(back)
     contrib[order] = back
-    contrib = contrib.view(T, top_k, -1)
+    contrib = contrib.view(T, top_k, h.shape[1])
     y = u.clone()
     for j in range(top_k):                      # ascending expert order (model.cpp:160-166)
         y = y + w[:, j:j + 1] * contrib[:, j]

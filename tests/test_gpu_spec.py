@@ -1,10 +1,11 @@
-"""Speculative K1 streaming in the fused layer kernel (opt-in, FLOE_SPEC=1): the producer streams the
-first K1 tiles of the experts predicted by router_pred * h (router_pred =
-router + router * mixing) before the exact routing exists.  The result must not
-depend on the prediction: a correct speculation, a forced misprediction
-(FLOE_DEBUG_FLAGS bit 3 inverts the predicted logits, so the discard path runs)
-and no speculation (FLOE_SPEC=0) give the same routing, masks and outputs, and
-those match the oracle (model.cpp:145-208)."""
+"""Predicted routing in the fused layer kernel: the producer streams the K1
+tiles of the experts predicted by router_pred * h (router_pred = router +
+router * mixing) during the mixing GEMV, and the consumers run K1 on them
+before the exact routing of u exists; the prediction is verified before any
+record is read.  The result must not depend on the prediction: a correct
+prediction and a forced misprediction (FLOE_TEST_MISPREDICT=1 inverts the
+predicted logits, so the re-run path executes) give the same routing, masks
+and outputs, and those match the oracle (model.cpp:145-208)."""
 import os
 import subprocess
 import sys
@@ -71,11 +72,10 @@ def _subprocess(tmp_path, name, env_extra):
 
 
 def test_speculation_never_changes_results(tmp_path):
-    spec = _subprocess(tmp_path, "spec", {"FLOE_SPEC": "1"})
-    miss = _subprocess(tmp_path, "miss", {"FLOE_SPEC": "1", "FLOE_DEBUG_FLAGS": "8"})
-    none = _subprocess(tmp_path, "none", {"FLOE_SPEC": "0"})
+    spec = _subprocess(tmp_path, "spec", {"FLOE_TEST_MISPREDICT": "0"})
+    miss = _subprocess(tmp_path, "miss", {"FLOE_TEST_MISPREDICT": "1"})
     for key in spec:
-        for other in (miss, none):
+        for other in (miss,):
             if key.endswith("_out"):
                 assert O.rel_l2(other[key], spec[key]) <= 1e-6, key
             else:
@@ -83,7 +83,7 @@ def test_speculation_never_changes_results(tmp_path):
 
 
 def test_speculative_layer_matches_oracle(tmp_path):
-    spec = _subprocess(tmp_path, "spec2", {"FLOE_SPEC": "1"})
+    spec = _subprocess(tmp_path, "spec2", {"FLOE_TEST_MISPREDICT": "0"})
     for si, (dh, di, E, K) in enumerate(SHAPES):
         L = _layer(dh, di, E, K)
         L.mixing = L.mixing.astype(np.float16).astype(np.float32)  # the device reads f16 mixing
