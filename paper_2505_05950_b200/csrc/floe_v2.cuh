@@ -60,7 +60,7 @@ constexpr int kMaxGrid = 256;                     // plan scans: one value per c
 #define FLOE_KR 2
 #endif
 constexpr int kR = FLOE_KR;                             // phase-C records per consumer barrier
-constexpr int kMaxRowsPerCta = 32;                // phase-A router slice in smem
+constexpr int kMaxRowsPerCta = 28;                // phase-A router slice in smem (dh/148 rows)
 
 __host__ __device__ constexpr uint32_t tile_bytes(uint32_t dh) { return 5u * dh; }
 __host__ __device__ constexpr uint32_t xtab_bytes(uint32_t dh) { return (dh / 128u) * 2u * 32u * 16u; }
@@ -161,21 +161,19 @@ __device__ __forceinline__ void span_step(float2 &acc, uint32_t wa, uint32_t wb,
   acc = __ffma2_rn(s2, t2, __ffma2_rn(z2, make_float2(zxs, zxs), acc));
 }
 
-// v of rows (g, g+8) of one tile in stage memory; all four lanes of a quad
-// return the same pair.
+// v of rows (g, g+8) over span quarter `qtr` (16 spans) of one tile in stage
+// memory; all four lanes of a quad return the same pair.
+constexpr int kQ = 4;  // warps per K1 tile (span quarters)
 template <int DH>
 __device__ __forceinline__ float2 k1_tile(const uint8_t *stage, const uint8_t *xtab,
                                           const float *xs, float mult, float zx, uint32_t lane,
-                                          uint32_t half) {
-  constexpr int PAIRS = DH / 256;  // span pairs of this half of the tile
-  stage += half * PAIRS * 32 * 16;
-  const uint32_t moff = half * PAIRS * 8 * 16;
-  xtab += half * PAIRS * 64 * 16;
-  xs += half * PAIRS * 2;
-  const uint4 *cw = reinterpret_cast<const uint4 *>(stage) + lane;
-  const uint4 *mw = reinterpret_cast<const uint4 *>(stage + 4 * DH - half * PAIRS * 32 * 16 + moff) +
+                                          uint32_t qtr) {
+  constexpr int PAIRS = DH / (128 * kQ);  // span pairs of this quarter of the tile
+  const uint4 *cw = reinterpret_cast<const uint4 *>(stage + qtr * PAIRS * 32 * 16) + lane;
+  const uint4 *mw = reinterpret_cast<const uint4 *>(stage + 4 * DH + qtr * PAIRS * 8 * 16) +
                     (lane >> 2);
-  const uint4 *xw = reinterpret_cast<const uint4 *>(xtab) + lane;
+  const uint4 *xw = reinterpret_cast<const uint4 *>(xtab + qtr * PAIRS * 64 * 16) + lane;
+  xs += qtr * PAIRS * 2;
   float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll 4
   for (int p = 0; p < PAIRS; ++p) {
@@ -198,12 +196,13 @@ __device__ __forceinline__ float2 k1_tile(const uint8_t *stage, const uint8_t *x
 // as in qgemv_channels.  xf = x in shared memory.
 template <int DH>
 __device__ __noinline__ float2 k1_tile_f32(const uint8_t *stage, const float *xf, uint32_t lane,
-                                           uint32_t half) {
+                                           uint32_t qtr) {
   const uint32_t *cw = reinterpret_cast<const uint32_t *>(stage);
   const uint32_t *mw = reinterpret_cast<const uint32_t *>(stage + 4 * DH);
   const uint32_t g = lane >> 2, tig = lane & 3;
+  constexpr uint32_t SPQ = DH / 64 / kQ;  // spans per quarter
   float2 acc = make_float2(0.0f, 0.0f);
-  for (uint32_t span = half * DH / 128; span < (half + 1) * DH / 128; ++span) {
+  for (uint32_t span = qtr * SPQ; span < (qtr + 1) * SPQ; ++span) {
     const uint32_t p = span / 2, hi = span & 1;
     for (uint32_t r = 0; r < 2; ++r) {
       const uint32_t kidx = hi * 2 + r;
@@ -232,9 +231,9 @@ __device__ __forceinline__ void cbar() {  // consumers
   __syncwarp();
   asm volatile("barrier.sync 1, %0;" ::"n"(kConsumers) : "memory");
 }
-__device__ __forceinline__ void pbar(uint32_t pair) {  // the two warps of a pair
+__device__ __forceinline__ void qbar(uint32_t quad) {  // the four warps of a K1 quad
   __syncwarp();
-  asm volatile("barrier.sync %0, 64;" ::"r"(3 + pair) : "memory");
+  asm volatile("barrier.sync %0, 128;" ::"r"(3 + quad) : "memory");
 }
 __device__ __forceinline__ void gbar(uint32_t grp) {  // phase C: one 8-warp record group
   __syncwarp();
@@ -360,7 +359,7 @@ struct FusedArgs {
 
 // Dynamic shared memory layout (bytes), host and device agree.
 struct SmemLayout {
-  uint32_t ring, uni, xs, lf, lv, total;
+  uint32_t ring, uni, ubuf, xs, lf, lv, total;
 };
 
 __host__ __device__ inline SmemLayout smem_layout(uint32_t dh, uint32_t ns, uint32_t max_tiles,
@@ -369,7 +368,8 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t dh, uint32_t ns, uint
   SmemLayout L;
   uint32_t o = 0;
   L.ring = o; o += ns * tile_bytes(dh);
-  L.uni = o;  o += (4u * dh > xtab_bytes(dh) ? 4u * dh : xtab_bytes(dh));  // h | x f32 | xtab
+  L.uni = o;  o += xtab_bytes(dh);  // K1 B fragments (x limbs)
+  L.ubuf = o; o += 4u * dh;          // phase A: h; then x (u in layer mode), f32
   L.xs = o;   o += 4u * (dh / 64);
   L.lf = o;   o += 4u * kTileCh * max_tiles;  // kept list: flattened channel | kValid
   L.lv = o;   o += 4u * kTileCh * max_tiles;  //            v
@@ -378,7 +378,10 @@ __host__ __device__ inline SmemLayout smem_layout(uint32_t dh, uint32_t ns, uint
 }
 
 constexpr uint32_t kValid = 0x80000000u;
-constexpr uint32_t kEarly = 2;  // mixing stages issued before griddepcontrol.wait
+#ifndef FLOE_EARLY_STAGES
+#define FLOE_EARLY_STAGES 2
+#endif
+constexpr uint32_t kEarly = FLOE_EARLY_STAGES;  // mixing stages issued before griddepcontrol.wait
 
 // Phase trace (diagnostics): %globaltimer at fixed points by consumer thread 0
 // (marks 0..15), producer lane 0 (16..23) and router lane 0 (24..27).
@@ -429,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ float stage_scale[kMaxStages];
-  __shared__ uint64_t hbar, predbar, bar1, routebar, lreset, listbar, pubbar;
+  __shared__ uint64_t hbar, predbar, bar1, routebar, lreset, listbar, pubbar, ubar;
   __shared__ unsigned long long pc_target, y_target;
   __shared__ ExpertDesc table_s[32];
   __shared__ float rs[32 * kMaxRowsPerCta];
@@ -449,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   __shared__ uint32_t n_list;
   __shared__ uint64_t fullC[kMaxStages], emptyC[kMaxStages];
   __shared__ float redmax[kConsumerWarps];
-  __shared__ float2 xch[kPairs][2][8];  // phase B: upper-half partials of a pair's tile
+  __shared__ float2 xch[kConsumerWarps / kQ][2][kQ - 1][8];  // phase B: quarter partials
   __shared__ float red[2][2][8][kR];    // phase C: [group][batch parity][warp][record]
 
   const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -458,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   const bool router_warp = warp == kConsumerWarps + 1;
   const SmemLayout L = smem_layout(DH, a.ns, a.max_tiles, G);
   uint8_t *ring = smem + L.ring;
-  float *hs = reinterpret_cast<float *>(smem + L.uni);  // phase A: h; phase B: x (f32) or xtab
+  float *hs = reinterpret_cast<float *>(smem + L.ubuf);  // phase A: h; then x (u), f32
   uint8_t *xtab = smem + L.uni;
   float *xs = reinterpret_cast<float *>(smem + L.xs);
   uint32_t *lf = reinterpret_cast<uint32_t *>(smem + L.lf);
@@ -485,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   // Phase C re-carves the ring plus the x-table area (both free once every K1
   // tile is consumed) into 4*DH-byte record stages with their own barriers:
   // 12 records (192 KB) in flight at d_hidden 4096.
-  const uint32_t nsC = min((uint32_t)kMaxStages, (L.xs - L.ring) / REC_B);
+  const uint32_t nsC = min((uint32_t)kMaxStages, (L.ubuf - L.ring) / REC_B);
   auto stageC = [&](uint32_t k) { return ring + (k % nsC) * REC_B; };
   auto issueC = [&](uint32_t k, const void *src, float scale) {
     if (k >= nsC) floe_ptx::mbar_wait(&emptyC[k % nsC], ((k / nsC) + 1) & 1u, (5u << 28) | k);
@@ -513,6 +516,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
     floe_ptx::mbar_init(&lreset, 1);
     floe_ptx::mbar_init(&listbar, 1);  // consumers: K1 done, own list final
     floe_ptx::mbar_init(&pubbar, 1);   // warp 0: predicted partial published
+    floe_ptx::mbar_init(&ubar, 1);     // x (u) in shared memory
     floe_ptx::fence_barrier_init();
     spec_ok = 1u;
     n_list = 0u;
@@ -576,7 +580,19 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
         floe_ptx::mbar_wait(&predbar, 0, 6u << 28);  // predicted routing
         mark(a, 16);
       }
-      // K1 tiles of the predicted (layer) / given (expert) experts
+      // x into shared memory (layer mode: u, complete once the grid barrier
+      // passed; the K1 tiles are issued after it, not during phase A: a
+      // global read waits behind the SM's queued bulk copies, and the
+      // barrier's polls are global reads), then the K1 tiles of the predicted
+      // (layer) / given (expert) experts
+      if (a.has_mixing) {
+        floe_ptx::mbar_wait(&bar1, 0, 15u << 28);
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // u: generic-proxy writes
+      } else {
+        pdl_wait();
+      }
+      floe_ptx::mbar_arrive_expect_tx(&ubar, 4u * DH);
+      floe_ptx::bulk_g2s(hs, a.has_mixing ? a.u : a.x, 4u * DH, &ubar);
       for (uint32_t j = 0; j < nB; ++j) {
         const TileRef tr = tile_ref(tile_lo + j, a.slots, a.di);
         wait_empty(u);
@@ -749,17 +765,16 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
 
   // ---- K1 operand setup (warps 8..15): x -> max|x| -> limbs (IMMA B
   // fragments) + span sums
-  const float *xg = a.has_mixing ? a.u : a.x;
   const bool setup_warp = warp >= kConsumerWarps / 2;
   const uint32_t ts = t - kConsumers / 2;  // setup thread index (warps 8..15)
   const bool act = setup_warp && ts < SPANS * 4;
   const uint32_t span = ts >> 2, tig = ts & 3;
   float xv[16];
-  auto setup1 = [&]() {  // load x, this warp's max|x| and finiteness
-    const float4 *x4 = reinterpret_cast<const float4 *>(xg + (act ? 64 * span + 16 * tig : 0));
+  auto setup1 = [&]() {  // x from shared memory, this warp's max|x| and finiteness
+    const float4 *x4 = reinterpret_cast<const float4 *>(hs + (act ? 64 * span + 16 * tig : 0));
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const float4 f = __ldcg(x4 + i);
+      const float4 f = x4[i];
       xv[4 * i] = f.x;
       xv[4 * i + 1] = f.y;
       xv[4 * i + 2] = f.z;
@@ -833,11 +848,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
           xt[4 * n + tig] = make_uint4(c1 ? lw[lim][0][0] : 0u, c4 ? lw[lim][0][1] : 0u,
                                        c1 ? lw[lim][1][0] : 0u, c4 ? lw[lim][1][1] : 0u);
         }
-      } else {
-        float *xf = hs + 64 * span + 16 * tig;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) xf[i] = xv[i];
-      }
+      }  // (not finite: K1 reads x from shared memory in f32)
     }
     float s16 = 0.0f;
 #pragma unroll
@@ -946,6 +957,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   }
 
   // ---- K1 setup: x limbs, span sums, epilogue multipliers
+  floe_ptx::mbar_wait(&ubar, 0, 16u << 28);
   if (setup_warp) setup1();
   cbar();
   if (setup_warp) setup2();
@@ -963,30 +975,38 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   }
 
   // ============================ phase B: K1 ================================
-  // tile j (ring use u0 + j) belongs to pair (u0 + j) % 8: with ns a multiple
-  // of 8, every stage is consumed by ONE pair in phases A and B, so a warp
-  // never waits on a stage whose previous fill it has not consumed itself
-  // (mbarrier parity waits cannot tell phase k from phase k+2).  Warp `sub`
-  // of the pair computes span half `sub`; the upper half's partials go
-  // through xch (double-buffered by the pair's tile parity) to the lower warp,
-  // which thresholds and appends kept channels to the CTA's list.
+  // Quads of 4 warps (one per SMSP) own 2 ring stages each and alternate
+  // between them, so a quad computes one tile while its other stage refills:
+  // tile j (ring use u0 + j) belongs to quad ((u0 + j) % 8) / 2.  With ns a
+  // multiple of 8 every stage is consumed by ONE quad in phase B and every
+  // phase-A use of it was consumed before the grid barrier, so a warp never
+  // waits on a stage more than one fill ahead (mbarrier parity waits cannot
+  // tell phase k from phase k+2).  Warp `sub` of the quad computes span
+  // quarter `sub`; the partials go through xch (double-buffered by the quad's
+  // tile parity) to warp 0 of the quad, which sums them in a fixed order,
+  // thresholds and appends kept channels to the CTA's list.
   auto k1_pass = [&](uint32_t u0, const float *thr_tab) {
-    const uint32_t pair = warp % kPairs, sub = warp / kPairs;
-    uint32_t n = 0;  // tiles this pair has done
-    for (uint32_t j = (pair + kPairs - u0 % kPairs) % kPairs; j < nB; j += kPairs, ++n) {
+    const uint32_t quad = warp / kQ, sub = warp % kQ;
+    uint32_t n = 0;  // tiles this quad has done
+    for (uint32_t j = 0; j < nB; ++j) {
       const uint32_t u = u0 + j;
+      if ((u % 8) / 2 != quad) continue;
       const TileRef tr = tile_ref(tile_lo + j, a.slots, a.di);
       wait_full(u);
       float2 v2 = all_finite ? k1_tile<DH>(stage(u), xtab, xs, mult, zx, lane, sub)
                              : k1_tile_f32<DH>(stage(u), hs, lane, sub);
       __syncwarp();
-      if (lane == 0) floe_ptx::mbar_arrive_cnt(&empty[u % ns], kPairs);
-      if (sub == 1 && (lane & 3) == 0) xch[pair][n & 1][lane >> 2] = v2;
-      pbar(pair);
-      if (sub == 1) continue;
-      const float2 o2 = xch[pair][n & 1][lane >> 2];
-      v2.x += o2.x;
-      v2.y += o2.y;
+      if (lane == 0) floe_ptx::mbar_arrive_cnt(&empty[u % ns], kConsumerWarps / kQ);
+      if (sub != 0 && (lane & 3) == 0) xch[quad][n & 1][sub - 1][lane >> 2] = v2;
+      qbar(quad);
+      const uint32_t nb = n++;
+      if (sub != 0) continue;
+#pragma unroll
+      for (int q = 0; q < kQ - 1; ++q) {
+        const float2 o2 = xch[quad][nb & 1][q][lane >> 2];
+        v2.x += o2.x;
+        v2.y += o2.y;
+      }
       const uint32_t g = lane >> 2;
       const bool q0 = (lane & 3) == 0;
       const float thr = thr_tab[tr.slot];
@@ -1092,10 +1112,10 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   const uint32_t grp = warp / 8, gw = warp % 8, gt = t % 256;
   float2 x2[EPT2 / 2], y2[EPT2 / 2];
   {
-    const float4 *xa = reinterpret_cast<const float4 *>(xg + EPT2 * gt);
+    const float4 *xa = reinterpret_cast<const float4 *>(hs + EPT2 * gt);
 #pragma unroll
     for (int i = 0; i < EPT2 / 4; ++i) {
-      const float4 q = __ldcg(xa + i);
+      const float4 q = xa[i];
       x2[2 * i] = make_float2(q.x, q.y);
       x2[2 * i + 1] = make_float2(q.z, q.w);
     }
