@@ -406,7 +406,7 @@ int launch_v2_dh(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) 
   cfg.blockDim = dim3(V::kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   attr[0].id = cudaLaunchAttributeCooperative;  // grid barriers need co-residency
   attr[0].val.cooperative = 1;
   // programmatic dependent launch: back-to-back calls overlap the next
@@ -436,6 +436,20 @@ int launch_v2_dh(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) 
   const bool use_pdl = pdl_env && !ws->profiling;
   cfg.attrs = coop_env ? attr : attr + 1;
   cfg.numAttrs = coop_env ? (use_pdl ? 2 : 1) : (use_pdl ? 1 : 0);
+  // CTA pairs (clusters of 2) balance phase C over distributed shared memory;
+  // 148 SMs hold 74 pairs at one CTA per SM.  FLOE_PAIRS=0 turns it off.
+  static const bool pairs_env = [] {
+    const char *p = std::getenv("FLOE_PAIRS");
+    return !(p && std::strcmp(p, "0") == 0);
+  }();
+  a.paired = (pairs_env && !coop_env && (G % 2) == 0) ? 1 : 0;
+  if (a.paired) {
+    attr[cfg.numAttrs + 1].id = cudaLaunchAttributeClusterDimension;
+    attr[cfg.numAttrs + 1].val.clusterDim.x = 2;
+    attr[cfg.numAttrs + 1].val.clusterDim.y = 1;
+    attr[cfg.numAttrs + 1].val.clusterDim.z = 1;
+    ++cfg.numAttrs;
+  }
   StageScope prof(ws, kStageFused, st);
   const cudaError_t e =
       cudaLaunchKernelExC(&cfg, reinterpret_cast<const void *>(V::fused<DH>), kargs);

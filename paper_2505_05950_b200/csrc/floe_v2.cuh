@@ -352,6 +352,7 @@ struct FusedArgs {
   unsigned long long *stats;
   unsigned long long *place_acc;  // nullable [2]: kept records read from HBM / over PCIe
   unsigned long long *phase_ns;   // nullable [G][kTraceSlots]
+  int paired;          // launched as clusters of 2: the CTA pair balances phase C over DSMEM
   uint32_t ns;         // ring stages
   uint32_t max_tiles;  // per-CTA tile capacity of the shared-memory kept list
   uint32_t debug;      // test hook: bit 3 = invert the predicted logits (misprediction path)
@@ -433,6 +434,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
   __shared__ float stage_scale[kMaxStages];
   __shared__ uint64_t hbar, predbar, bar1, routebar, lreset, listbar, pubbar, ubar;
+  __shared__ uint64_t peerbar, donebar, totbar;  // CTA pair: partner's list final / reads done; item count
+  __shared__ uint32_t n_pub, n_total;
   __shared__ unsigned long long pc_target, y_target;
   __shared__ ExpertDesc table_s[32];
   __shared__ float rs[32 * kMaxRowsPerCta];
@@ -517,6 +520,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
     floe_ptx::mbar_init(&listbar, 1);  // consumers: K1 done, own list final
     floe_ptx::mbar_init(&pubbar, 1);   // warp 0: predicted partial published
     floe_ptx::mbar_init(&ubar, 1);     // x (u) in shared memory
+    floe_ptx::mbar_init(&peerbar, 1);  // remote arrive: the partner's kept list is final
+    floe_ptx::mbar_init(&donebar, 1);  // remote arrive: the partner finished reading ours
+    floe_ptx::mbar_init(&totbar, 1);   // producer: this CTA's phase-C item count
     floe_ptx::fence_barrier_init();
     spec_ok = 1u;
     n_list = 0u;
@@ -539,7 +545,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
     rec_s[t] = d.records;
     rhost_s[t] = d.host_records;
   }
-  __syncthreads();
+  if (a.paired) floe_ptx::cluster_sync_all();  // partner barriers initialised (remote arrivals)
+  else __syncthreads();
 
   // ---- geometry
   const uint32_t tps = tiles_per_expert(a.di);
@@ -614,15 +621,48 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
     // consumed, the list final)
     floe_ptx::mbar_wait(&listbar, 0, 12u << 28);
     const uint32_t n_own = n_list;
+    const uint32_t P = min(n_own, nsC);  // the first ring fill: always this CTA's own
+    auto own_item = [&](uint32_t k) {
+      const uint32_t f = lf[k] & ~kValid, s2 = f / a.di, c = f - s2 * a.di;
+      issueC(k, rec_s[s2] + (size_t)c * 2 * DH, lv[k] * w_s[s2]);
+    };
     if (lane == 0) {
       mark(a, 18);
-      // own kept records in list order; each CTA processes exactly its own:
-      // any cross-CTA balancing needs global reads, and those wait behind the
-      // SM's queued bulk copies for several us (measured: a published-count
-      // plan arrived 6-12 us after K1 and cost more than the tail it removed)
-      for (uint32_t k = 0; k < n_own; ++k) {
-        const uint32_t f = lf[k] & ~kValid, s2 = f / a.di, c = f - s2 * a.di;
-        issueC(k, rec_s[s2] + (size_t)c * 2 * DH, lv[k] * w_s[s2]);
+      if (a.paired) {  // publish the list to the partner CTA (release: the list writes
+        n_pub = n_own;  // were acquired through listbar)
+        floe_ptx::mbar_arrive_remote(floe_ptx::mapa(&peerbar, (b ^ 1u) & 1u));
+      }
+      for (uint32_t k = 0; k < P; ++k) own_item(k);
+      uint32_t own = n_own, take = 0, pfirst = 0;
+      const uint32_t peer = b ^ 1u;
+      if (a.paired) {
+        // CTA pair plan over distributed shared memory (no global round trip:
+        // a global read waits behind the SM's queued bulk copies): T = n_me +
+        // n_peer, even CTA target ceil(T/2), odd floor(T/2); each keeps
+        // max(min(n, nsC), min(n, target)) own records and the deficit CTA
+        // takes the partner's surplus from the end of its list
+        floe_ptx::mbar_wait_cluster(&peerbar, 0, 17u << 28);
+        const uint32_t n_p = floe_ptx::ld_cluster_u32(floe_ptx::mapa(&n_pub, peer & 1u));
+        const uint32_t T = n_own + n_p;
+        const uint32_t t_me = (b & 1u) ? T / 2 : (T + 1) / 2, t_p = T - t_me;
+        own = max(P, min(n_own, t_me));
+        const uint32_t own_p = max(min(n_p, nsC), min(n_p, t_p));
+        take = t_me > own ? min(t_me - own, n_p - own_p) : 0u;
+        pfirst = own_p;
+      }
+      n_total = own + take;
+      floe_ptx::mbar_arrive(&totbar);
+      for (uint32_t k = P; k < own; ++k) own_item(k);
+      if (a.paired) {
+        const uint32_t pr = (b ^ 1u) & 1u;
+        for (uint32_t k = 0; k < take; ++k) {
+          const uint32_t f =
+              floe_ptx::ld_cluster_u32(floe_ptx::mapa(&lf[pfirst + k], pr)) & ~kValid;
+          const float v = __uint_as_float(floe_ptx::ld_cluster_u32(floe_ptx::mapa(&lv[pfirst + k], pr)));
+          const uint32_t s2 = f / a.di, c = f - s2 * a.di;
+          issueC(own + k, rec_s[s2] + (size_t)c * 2 * DH, v * w_s[s2]);
+        }
+        floe_ptx::mbar_arrive_remote(floe_ptx::mapa(&donebar, pr));  // done reading its list
       }
       mark(a, 19);
     }
@@ -1124,8 +1164,18 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   }
   uint32_t stg = grp % nsC, ph = 0;  // ring position of item grp + 2i
   uint32_t batch = 0, processed = 0;
-  const uint32_t n_mine = n_items > grp ? (n_items - grp + 1) / 2 : 0u;
-  for (uint32_t i0 = 0; i0 < n_mine; i0 += kR, ++batch) {
+  // items k < P0 (the first ring fill, own records) always exist; past them
+  // the count comes from the producer's pair plan
+  const uint32_t P0 = min(n_items, nsC);
+  uint32_t total = a.paired ? 0xffffffffu : n_items;
+  for (uint32_t i0 = 0;; i0 += kR, ++batch) {
+    if (grp + 2 * (i0 + kR - 1) >= P0 && total == 0xffffffffu) {
+      floe_ptx::mbar_wait(&totbar, 0, 13u << 28);
+      total = n_total;
+    }
+    const uint32_t lim = total == 0xffffffffu ? P0 : total;
+    const uint32_t n_mine = lim > grp ? (lim - grp + 1) / 2 : 0u;
+    if (i0 >= n_mine) break;
     Vec dv[kR][2];
     float gp[kR], sc[kR];
     bool proc[kR];
@@ -1208,7 +1258,12 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
       }
     }
   }
-  if (t == 0) mark(a, 6);
+  if (t == 0) {
+    mark(a, 6);
+    // the partner may still read this CTA's kept list (distributed shared
+    // memory lives as long as the CTA): wait until it is done
+    if (a.paired && !a.k1_only) floe_ptx::mbar_wait_cluster(&donebar, 0, 18u << 28);
+  }
   if (!a.has_mixing) {  // expert mode: y was zeroed by CTA 0 for this call
     if (t == 0) {
       const unsigned long long t0 = gtime();
