@@ -304,6 +304,43 @@ int floe_gpu_workspace_set_phase_trace(floe_gpu_workspace *ws, int enable);
 int floe_gpu_workspace_read_phase_trace(floe_gpu_workspace *ws, uint64_t *out, uint32_t cap,
                                         uint32_t *grid);
 
+/* ------------------------------------------------------------ calibration */
+/* Threshold calibration on the device, bit-exact with the reference's
+ * collect_stats + calibrate_model (core/src/model.cpp:242-330) and
+ * SampleReservoir / calibrate / calibrate_threshold
+ * (core/src/sparsify.cpp:42-64,128-142).  A run keeps one reservoir per
+ * (layer, expert): SampleReservoir(sample_cap, seed ^ 0x5eedca11,
+ * layer*experts + expert); `seed` is collect_stats' seed (the calibration
+ * token stream's).  The caller drives the layers (the float model of a
+ * Mixtral stack does not fit in HBM at once): for each layer, calib_layer runs
+ * the DENSE float layer over the tokens' block inputs and returns the next
+ * layer's inputs, exactly as collect_stats chains them. */
+typedef struct floe_gpu_calib floe_gpu_calib;
+typedef struct floe_float_layer_view { /* f32 DEVICE pointers, reference layouts */
+  const float *router;        /* [E][dh] row-major                         */
+  const float *mixing;        /* [dh][dh] row-major                        */
+  const float *const *gate;   /* host array of E device pointers, [di][dh] */
+  const float *const *up;     /* channel-major (ExpertWeights::gate/up)    */
+  const float *const *down_t; /* [di][dh] (ExpertWeights::down_t)          */
+} floe_float_layer_view;
+int floe_gpu_calib_create(uint32_t layers, uint32_t experts, uint32_t d_hidden,
+                          uint32_t d_intermediate, uint64_t seed, uint64_t sample_cap,
+                          floe_gpu_calib **out);
+int floe_gpu_calib_destroy(floe_gpu_calib *c);
+/* One layer of collect_stats over `tokens` block inputs h_dev [tokens][dh]
+ * (in token-stream order): u = h + drift_scale*mixing h, route, and for every
+ * routed expert the dense SwiGLU forward; |up_c . u| of every channel goes to
+ * the (layer, expert) reservoir in token order; h_next_dev [tokens][dh]
+ * (nullable) receives the layer outputs.  Several calls per layer append in
+ * call order.  Synchronises `stream` once (routing readback). */
+int floe_gpu_calib_layer(floe_gpu_calib *c, uint32_t layer, const floe_float_layer_view *w,
+                         uint32_t top_k, float drift_scale, const float *h_dev,
+                         float *h_next_dev, uint32_t tokens, floe_stream_t stream);
+/* calibrate(samples, k): thresholds_host[layer*E + expert] (host, L*E floats).
+ * Fails with "calibrate: no samples for layer L expert E" like the reference
+ * when an expert was never routed (k > 0). */
+int floe_gpu_calib_thresholds(floe_gpu_calib *c, double k, float *thresholds_host);
+
 /* ------------------------------------------------------- synthetic model */
 /* Reference random streams on the device (rng.cpp:12-64): out[i] =
  * sigma * (float)normal_i.  sharded = 1 reproduces gen_model's fill_gaussian

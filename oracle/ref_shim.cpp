@@ -370,6 +370,48 @@ void *ref_cmodel_build_thresholds(std::uint32_t layers, std::uint32_t experts,
   }
 }
 
+// calibrate_model (model.cpp:323-330) on a float model given as arrays:
+// router [L][E][dh], mixing [L][dh][dh], gate/up/down_t [L][E][di][dh]; the
+// thresholds go to out[L*E].  Returns 0 or -1 (ref_last_error).
+int ref_calibrate_weights(std::uint32_t layers, std::uint32_t experts, std::uint32_t top_k_n,
+                          std::uint32_t dh, std::uint32_t di, const float *router,
+                          const float *mixing, const float *gate, const float *up,
+                          const float *down, std::uint64_t calib_seed, std::uint64_t tokens,
+                          double k, std::uint64_t cap, unsigned workers, float drift,
+                          float *out) {
+  return guarded([&] {
+    MoEModel m;
+    m.cfg.layers = layers;
+    m.cfg.experts = experts;
+    m.cfg.top_k = top_k_n;
+    m.cfg.d_hidden = dh;
+    m.cfg.d_intermediate = di;
+    m.layers.resize(layers);
+    const std::size_t n = (std::size_t)dh * di;
+    for (std::uint32_t l = 0; l < layers; ++l) {
+      MoELayer &L = m.layers[l];
+      L.router = Matrix(experts, dh);
+      std::memcpy(L.router.data.data(), router + (std::size_t)l * experts * dh,
+                  sizeof(float) * experts * dh);
+      L.mixing = Matrix(dh, dh);
+      std::memcpy(L.mixing.data.data(), mixing + (std::size_t)l * dh * dh, sizeof(float) * dh * dh);
+      for (std::uint32_t e = 0; e < experts; ++e) {
+        ExpertWeights w;
+        w.d_hidden = dh;
+        w.d_intermediate = di;
+        const std::size_t o = ((std::size_t)l * experts + e) * n;
+        w.gate.assign(gate + o, gate + o + n);
+        w.up.assign(up + o, up + o + n);
+        w.down_t.assign(down + o, down + o + n);
+        L.experts.push_back(std::move(w));
+      }
+    }
+    ThresholdTable t = calibrate_model(m, calib_seed, tokens, k, cap, workers, drift);
+    for (std::uint32_t l = 0; l < layers; ++l)
+      for (std::uint32_t e = 0; e < experts; ++e) out[l * experts + e] = t.at(l, e);
+  });
+}
+
 // Replica throughput of layer_forward(CompressedModel): `threads` host threads
 // split n_tokens independent tokens (hs: n_tokens x dh) round-robin.  Returns
 // wall seconds (steady_clock), negative on error.

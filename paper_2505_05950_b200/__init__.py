@@ -13,6 +13,7 @@ built and an sm_100 GPU is present.
 """
 from ._abi import (  # noqa: F401
     FloeError,
+    GpuCalib,
     GpuExpert,
     GpuLayer,
     GpuPredictor,
@@ -36,7 +37,7 @@ from ._abi import (  # noqa: F401
     quantize,
 )
 
-__all__ = ["FloeError", "GpuExpert", "GpuLayer", "GpuPredictor", "Offload", "Workspace",
+__all__ = ["FloeError", "GpuCalib", "GpuExpert", "GpuLayer", "GpuPredictor", "Offload", "Workspace",
            "abi_version", "dequantize", "device_info", "expert_forward_sparse",
            "exported_symbols", "layer_forward", "lib", "library_path", "predict_experts",
            "predict_mask", "qgemv_channels", "qgemv_channels_batched", "expert_forward_batched", "gen_normals", "layer_forward_host",

@@ -61,6 +61,11 @@ class LayerTrace(ct.Structure):
                 ("weights_dev", ct.c_void_p), ("masks_dev", ct.c_void_p)]
 
 
+class FloatLayerView(ct.Structure):
+    _fields_ = [("router", ct.c_void_p), ("mixing", ct.c_void_p), ("gate", ct.c_void_p),
+                ("up", ct.c_void_p), ("down_t", ct.c_void_p)]
+
+
 _P = ct.c_void_p
 _U32 = ct.c_uint32
 _F = ct.c_float
@@ -108,6 +113,12 @@ _SIGS = {
     "floe_gpu_predictor_create": (ct.c_int, [_U32, _U32, _U32, _P, _P, ct.POINTER(_P)]),
     "floe_gpu_predictor_destroy": (ct.c_int, [_P]),
     "floe_gpu_predict_experts": (ct.c_int, [_P, _P, _U32, _U32, _P, _P]),
+    "floe_gpu_calib_create": (ct.c_int, [_U32, _U32, _U32, _U32, ct.c_uint64, ct.c_uint64,
+                                         ct.POINTER(_P)]),
+    "floe_gpu_calib_destroy": (ct.c_int, [_P]),
+    "floe_gpu_calib_layer": (ct.c_int, [_P, _U32, ct.POINTER(FloatLayerView), _U32, _F, _P, _P,
+                                        _U32, _P]),
+    "floe_gpu_calib_thresholds": (ct.c_int, [_P, ct.c_double, _P]),
 }
 
 _lib = None
@@ -567,3 +578,48 @@ class Offload:
         st = OffloadStats()
         _check(lib().floe_gpu_offload_stats(self.handle, ct.byref(st), _stream(stream)))
         return {f: getattr(st, f) for f, _ in OffloadStats._fields_}
+
+
+class GpuCalib:
+    """collect_stats + calibrate_model on the device (model.cpp:242-330): one
+    reservoir per (layer, expert), fed layer by layer with dense float layers."""
+
+    def __init__(self, layers: int, experts: int, d_hidden: int, d_intermediate: int, seed: int,
+                 sample_cap: int = 1 << 16):
+        h = ct.c_void_p()
+        _check(lib().floe_gpu_calib_create(layers, experts, d_hidden, d_intermediate, seed,
+                                           sample_cap, ct.byref(h)))
+        self.handle = h.value
+        self.layers, self.experts, self.d_hidden = layers, experts, d_hidden
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().floe_gpu_calib_destroy(self.handle)
+            self.handle = None
+
+    __del__ = close
+
+    def layer(self, layer: int, router, mixing, gate, up, down_t, top_k: int, h,
+              drift_scale: float = 1.0, want_next: bool = True, stream=None):
+        """One layer of collect_stats over tokens h [T, dh] (device f32); gate/up/down_t
+        are lists of E device f32 tensors [di, dh].  Returns the next layer's inputs."""
+        torch = _torch()
+        h = h.contiguous()
+        T = h.shape[0]
+        arr = ct.c_void_p * len(gate)
+        g = arr(*[t.data_ptr() for t in gate])
+        u = arr(*[t.data_ptr() for t in up])
+        d = arr(*[t.data_ptr() for t in down_t])
+        v = FloatLayerView(router.data_ptr(), mixing.data_ptr(), ct.addressof(g), ct.addressof(u),
+                           ct.addressof(d))
+        nxt = torch.empty_like(h) if want_next else None
+        _check(lib().floe_gpu_calib_layer(self.handle, layer, ct.byref(v), top_k,
+                                          float(drift_scale), h.data_ptr(),
+                                          nxt.data_ptr() if nxt is not None else None, T,
+                                          _stream(stream)))
+        return nxt
+
+    def thresholds(self, k: float) -> np.ndarray:
+        out = np.empty(self.layers * self.experts, np.float32)
+        _check(lib().floe_gpu_calib_thresholds(self.handle, float(k), out.ctypes.data))
+        return out.reshape(self.layers, self.experts)

@@ -21,6 +21,9 @@
 #include "floe_gen.cuh"
 #include "floe_v2.cuh"
 #include "floe_tc.cuh"
+#include "floe_calib.cuh"
+
+#include <cub/device/device_segmented_radix_sort.cuh>
 
 using floe_k::ExpertDesc;
 using floe_k::K1Args;
@@ -1728,6 +1731,206 @@ int floe_gpu_offload_stats(floe_gpu_offload *o, floe_offload_stats *out, floe_st
   for (uint32_t i = 0; i < o->L * o->E; ++i)
     if (o->state[i] == floe_gpu_offload::kResident) dev += o->rec_bytes;
   out->device_record_bytes = dev;
+  return FLOE_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ calibration ---
+// collect_stats / calibrate_model on the device (floe_calib.cuh; reference
+// core/src/model.cpp:242-330, core/src/sparsify.cpp:42-64,128-142).
+struct floe_gpu_calib {
+  uint32_t L = 0, E = 0, dh = 0, di = 0;
+  uint64_t cap = 0, seed = 0;
+  float *samples = nullptr;          // [L*E][cap]
+  floe_cal::ResState *st = nullptr;  // [L*E]
+  uint32_t *owner = nullptr;         // [cap]
+};
+
+extern "C" {
+
+int floe_gpu_calib_create(uint32_t layers, uint32_t experts, uint32_t d_hidden,
+                          uint32_t d_intermediate, uint64_t seed, uint64_t sample_cap,
+                          floe_gpu_calib **out) {
+  if (!out) return fail(FLOE_ERR_INVALID, "calib_create: null argument");
+  *out = nullptr;
+  if (int rc = require_device("calib_create")) return rc;
+  if (layers == 0 || experts == 0 || experts > 32 || d_hidden == 0 || d_intermediate == 0 ||
+      sample_cap == 0 || sample_cap > 0xffffffffull)
+    return fail(FLOE_ERR_INVALID, "calib_create: need layers, d_hidden, d_intermediate, cap >= 1 "
+                                  "and 1 <= experts <= 32");
+  auto *c = new (std::nothrow) floe_gpu_calib();
+  if (!c) return fail(FLOE_ERR_OOM, "calib_create: host allocation failed");
+  c->L = layers;
+  c->E = experts;
+  c->dh = d_hidden;
+  c->di = d_intermediate;
+  c->cap = sample_cap;
+  c->seed = seed;
+  const uint32_t R = layers * experts;
+  cudaError_t ce = cudaMalloc(&c->samples, 4ull * R * sample_cap);
+  if (ce == cudaSuccess) ce = cudaMalloc(&c->st, sizeof(floe_cal::ResState) * R);
+  if (ce == cudaSuccess) ce = cudaMalloc(&c->owner, 4ull * sample_cap);
+  if (ce == cudaSuccess) {
+    // SampleReservoir(cap, seed ^ 0x5eedca11, layer * E + expert) (model.cpp:300-304)
+    floe_cal::reservoir_init<<<(R + 127) / 128, 128>>>(c->st, seed ^ 0x5eedca11ull, 0, R);
+    ce = cudaGetLastError();
+  }
+  if (ce == cudaSuccess) ce = cudaDeviceSynchronize();
+  if (ce != cudaSuccess) {
+    floe_gpu_calib_destroy(c);
+    return fail(FLOE_ERR_OOM, "calib_create: %s", cudaGetErrorString(ce));
+  }
+  *out = c;
+  return FLOE_OK;
+}
+
+int floe_gpu_calib_destroy(floe_gpu_calib *c) {
+  if (!c) return FLOE_OK;
+  cudaDeviceSynchronize();
+  if (c->samples) cudaFree(c->samples);
+  if (c->st) cudaFree(c->st);
+  if (c->owner) cudaFree(c->owner);
+  delete c;
+  return FLOE_OK;
+}
+
+int floe_gpu_calib_layer(floe_gpu_calib *c, uint32_t layer, const floe_float_layer_view *w,
+                         uint32_t top_k, float drift_scale, const float *h, float *h_next,
+                         uint32_t tokens, floe_stream_t stream) {
+  namespace C = floe_cal;
+  if (!c || !w || !h) return fail(FLOE_ERR_INVALID, "collect_stats: null argument");
+  if (tokens == 0) return fail(FLOE_ERR_INVALID, "collect_stats: empty token stream");
+  if (layer >= c->L) return fail(FLOE_ERR_INVALID, "collect_stats: bad layer");
+  if (top_k == 0 || top_k > c->E)
+    return fail(FLOE_ERR_INVALID, "model config: need 1 <= top_k <= experts");
+  if (!w->router || !w->mixing || !w->gate || !w->up || !w->down_t)
+    return fail(FLOE_ERR_INVALID, "collect_stats: incomplete layer view");
+  cudaStream_t st = S(stream);
+  const uint32_t E = c->E, dh = c->dh, di = c->di, T = tokens, K = top_k, P = T * K;
+  // scratch (stream-ordered): u, logits, sel, w, pairs, acoef, vals, out, pointer tables
+  const size_t o_u = 0, o_lg = o_u + 4ull * T * dh, o_sel = o_lg + 4ull * T * E;
+  const size_t o_w = o_sel + 4ull * P, o_pr = (o_w + 4ull * P + 15) & ~size_t(15);
+  const size_t o_pof = o_pr + sizeof(C::Pair) * P;
+  const size_t o_ac = (o_pof + 4ull * P + 255) & ~size_t(255);
+  const size_t o_val = o_ac + 4ull * P * di, o_out = o_val + 4ull * P * di;
+  const size_t o_ptr = (o_out + 4ull * P * dh + 15) & ~size_t(15);
+  const size_t total = o_ptr + 8ull * 4 * E;
+  uint8_t *sc = nullptr;
+  CK(cudaMallocAsync(reinterpret_cast<void **>(&sc), total, st));
+  float *u = reinterpret_cast<float *>(sc + o_u), *lg = reinterpret_cast<float *>(sc + o_lg);
+  uint32_t *sel = reinterpret_cast<uint32_t *>(sc + o_sel);
+  float *wt = reinterpret_cast<float *>(sc + o_w);
+  C::Pair *pairs = reinterpret_cast<C::Pair *>(sc + o_pr);
+  int32_t *pair_of = reinterpret_cast<int32_t *>(sc + o_pof);
+  float *acoef = reinterpret_cast<float *>(sc + o_ac), *vals = reinterpret_cast<float *>(sc + o_val);
+  float *outp = reinterpret_cast<float *>(sc + o_out);
+  const float **ptrs = reinterpret_cast<const float **>(sc + o_ptr);  // up | gate | down | vals
+  int rc = FLOE_OK;
+  auto done = [&](int r) {
+    cudaFreeAsync(sc, st);
+    return r;
+  };
+  // u = h + drift * mixing h; logits = router u; route
+  C::gemv_seq<<<dim3((dh + 255) / 256, T), 256, 0, st>>>(w->mixing, dh, dh, h, h, drift_scale, u);
+  C::gemv_seq<<<dim3((E + 255) / 256, T), 256, 0, st>>>(w->router, E, dh, u, nullptr, 1.0f, lg);
+  C::route_tokens<<<(T + 127) / 128, 128, 0, st>>>(lg, T, E, K, sel, wt);
+  if (cudaGetLastError() != cudaSuccess) return done(fail(FLOE_ERR_CUDA, "collect_stats: launch failed"));
+  // (token, expert) pairs in token order; position of each token among its
+  // expert's tokens (the reservoir's add order: tokens, then channels)
+  std::vector<uint32_t> hsel(P);
+  if (cudaMemcpyAsync(hsel.data(), sel, 4ull * P, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return done(fail(FLOE_ERR_CUDA, "collect_stats: routing readback failed"));
+  std::vector<uint32_t> n_e(E, 0), off(E, 0);
+  std::vector<C::Pair> hp(P);
+  std::vector<int32_t> hpof(P);
+  for (uint32_t t = 0; t < T; ++t)
+    for (uint32_t j = 0; j < K; ++j) {
+      const uint32_t e = hsel[t * K + j];
+      hp[t * K + j] = C::Pair{t, j, e, n_e[e]++};
+      hpof[t * K + j] = (int32_t)(t * K + j);
+    }
+  for (uint32_t e = 1; e < E; ++e) off[e] = off[e - 1] + n_e[e - 1];
+  std::vector<const float *> hptr(4 * E);
+  for (uint32_t e = 0; e < E; ++e) {
+    hptr[e] = w->up[e];
+    hptr[E + e] = w->gate[e];
+    hptr[2 * E + e] = w->down_t[e];
+    hptr[3 * E + e] = vals + (size_t)off[e] * di;
+  }
+  if (cudaMemcpyAsync(pairs, hp.data(), sizeof(C::Pair) * P, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaMemcpyAsync(pair_of, hpof.data(), 4ull * P, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaMemcpyAsync(ptrs, hptr.data(), 8ull * 4 * E, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return done(fail(FLOE_ERR_CUDA, "collect_stats: upload failed"));
+  C::up_gate_seq<<<dim3((di + 127) / 128, P), 128, 0, st>>>(
+      ptrs, ptrs + E, u, dh, di, pairs, reinterpret_cast<float *const *>(sc + o_ptr + 8ull * 3 * E),
+      acoef);
+  if (h_next) {
+    C::down_seq<<<dim3((dh + 127) / 128, P), 128, 0, st>>>(ptrs + 2 * E, pairs, acoef, dh, di, outp);
+    C::combine_seq<<<dim3((dh + 127) / 128, T), 128, 0, st>>>(u, outp, wt, pair_of, T, K, dh,
+                                                              drift_scale, h_next);
+  }
+  if (cudaGetLastError() != cudaSuccess) return done(fail(FLOE_ERR_CUDA, "collect_stats: launch failed"));
+  // reservoir adds, expert by expert (each reservoir sees its values in token order)
+  for (uint32_t e = 0; e < E; ++e) {
+    if (!n_e[e]) continue;
+    const uint64_t n = (uint64_t)n_e[e] * di;
+    C::ResState *rs = c->st + (size_t)layer * E + e;
+    float *smp = c->samples + ((size_t)layer * E + e) * c->cap;
+    if (cudaMemsetAsync(c->owner, 0, 4ull * c->cap, st) != cudaSuccess)
+      return done(fail(FLOE_ERR_CUDA, "collect_stats: memset failed"));
+    C::reservoir_claim<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(rs, c->cap, n, c->owner);
+    C::reservoir_apply<<<(unsigned)((c->cap + 255) / 256), 256, 0, st>>>(c->cap, vals + (size_t)off[e] * di,
+                                                                      c->owner, smp);
+    C::reservoir_advance<<<1, 1, 0, st>>>(rs, n);
+  }
+  if (cudaGetLastError() != cudaSuccess) return done(fail(FLOE_ERR_CUDA, "collect_stats: launch failed"));
+  return done(rc);
+}
+
+int floe_gpu_calib_thresholds(floe_gpu_calib *c, double k, float *thresholds_host) {
+  if (!c || !thresholds_host) return fail(FLOE_ERR_INVALID, "calibrate: null argument");
+  if (k < 0.0 || k > 1.0) return fail(FLOE_ERR_INVALID, "calibrate_threshold: k must be in [0,1]");
+  const uint32_t R = c->L * c->E;
+  std::vector<floe_cal::ResState> hs(R);
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(hs.data(), c->st, sizeof(floe_cal::ResState) * R, cudaMemcpyDeviceToHost));
+  for (uint32_t i = 0; i < R; ++i)
+    if (hs[i].seen == 0 && k != 0.0)
+      return fail(FLOE_ERR_INVALID, "calibrate: no samples for layer %u expert %u", i / c->E,
+                  i % c->E);
+  // sort every reservoir's samples (segments [i cap, i cap + min(seen, cap)))
+  std::vector<int> begin(R), end(R);
+  for (uint32_t i = 0; i < R; ++i) {
+    begin[i] = (int)((uint64_t)i * c->cap);
+    end[i] = (int)((uint64_t)i * c->cap + std::min<uint64_t>(hs[i].seen, c->cap));
+  }
+  if ((uint64_t)R * c->cap > 0x7fffffffull)
+    return fail(FLOE_ERR_UNSUPPORTED, "calibrate: more than 2^31 samples");
+  float *sorted = nullptr, *out = nullptr;
+  int *d_off = nullptr;
+  void *tmp = nullptr;
+  size_t tmp_bytes = 0;
+  const int nitems = (int)((uint64_t)R * c->cap);
+  CK(cudaMalloc(&sorted, 4ull * nitems));
+  CK(cudaMalloc(&d_off, 8ull * R));
+  CK(cudaMalloc(&out, 4ull * R));
+  CK(cudaMemcpy(d_off, begin.data(), 4ull * R, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_off + R, end.data(), 4ull * R, cudaMemcpyHostToDevice));
+  cub::DeviceSegmentedRadixSort::SortKeys(nullptr, tmp_bytes, c->samples, sorted, nitems, (int)R,
+                                          d_off, d_off + R);
+  CK(cudaMalloc(&tmp, tmp_bytes));
+  cub::DeviceSegmentedRadixSort::SortKeys(tmp, tmp_bytes, c->samples, sorted, nitems, (int)R,
+                                          d_off, d_off + R);
+  floe_cal::reservoir_pick<<<(R + 127) / 128, 128>>>(c->st, sorted, c->cap, R, k, out);
+  const cudaError_t ce = cudaGetLastError();
+  if (ce == cudaSuccess) CK(cudaMemcpy(thresholds_host, out, 4ull * R, cudaMemcpyDeviceToHost));
+  cudaFree(tmp);
+  cudaFree(sorted);
+  cudaFree(d_off);
+  cudaFree(out);
+  if (ce != cudaSuccess) return fail(FLOE_ERR_CUDA, "calibrate: %s", cudaGetErrorString(ce));
   return FLOE_OK;
 }
 
