@@ -2,23 +2,35 @@
 """bench.py -- FloE compressed-expert decode on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--layers L] [--no-offload] [--no-cpu-baseline]
 
-Workload (BASELINE.json configs[1]): one Mixtral-8x7B-shaped MoE layer --
-router top-2 of 8 compressed experts (INT2 g64 up projection, f16 gate/down
-records, ~80% contextual sparsity), mixing matrix stand-in for attention --
-single-token decode.  A step is one layer_forward of one token; value is
-decode tokens/s of that layer over all ranks.  N > 1 runs N independent
-replicas ("replicas only": single-sequence decode does not shard).
-The config-1 single-expert numbers ride along under "expert_ffn".
+Workload (BASELINE.json configs[2], the largest single-GPU configuration):
+full 32-layer Mixtral-8x7B-shaped decode -- every layer a MoE block (mixing
+matrix stand-in for attention, router top-2 of 8 compressed experts: INT2 g64
+up projection, f16 gate|down records, ~80% contextual sparsity), all 256
+experts resident in HBM (65.9 GB).  A step is one decode token through the 32
+layers (the reference's run loop, cli.cpp:86-107); value = decode tokens/s
+over all ranks.  N > 1 runs N independent replicas ("replicas only":
+single-sequence decode does not shard).
+
+Block inputs (replay): layer l of token i reads its own recorded N(0,1) block
+input token_input(1, 32 i + l).  The synthetic stack has no norms and its
+chained activations overflow by layer ~7, so a decode whose
+hidden states keep their scale is replayed layer by layer
+(predictor.cpp:60-85); every launch still waits for the previous layer (stream
+order + PDL), exactly as in a chained decode.  Thresholds: the reference's
+calibrate_model(k = 0.8) per layer (64 calibration tokens token_input(3, t)
+as block inputs), computed ON THE DEVICE by floe_gpu_calib_* (bit-exact with
+the reference, tests/test_gpu_calib.py).
+
+Sub-results: "layer" (config 2: the same launches per layer), "expert_ffn"
+(config 1 and the config-4 batched expert), "offload" (config 3 with the
+records host-resident under a VRAM budget: PCIe-bound), "e2e" (the decode
+through the host-buffer C ABI).
 
 Weights are the reference's own gen_model random streams (seed 7), generated
-and quantized on the device by the product library; thresholds are
-per-expert 0.8-quantiles of |v| over 8 calibration tokens (token_input(3, t)).
-Decode tokens are token_input(1, t).  L2: inputs larger than L2 -- the bench
-builds N_LAYERS = 4 distinct layers of the same gen_model (layers 0..3) and
-step i runs layer i % 4, as consecutive decode layers do, so every step's
-~165 MB of weights were last touched 3 steps (~500 MB) earlier and cannot be
-L2-resident (126 MB).  The K steps run back to back in one CUDA-event region.
+and quantized on the device by the product library.  L2: one token touches
+5.27 GB of weights (> 126 MB L2), no flush needed.
 
 Only the cpu_baseline leg and --impl reference touch oracle/ (the reference
 core compiled from its own sources, oracle/_ref/libfloe_ref.so).
@@ -43,9 +55,11 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "decode tokens/s (Mixtral-8x7B shape) + expert-FFN achieved HBM GB/s vs roofline"
 DH, DI, E, TOPK, BITS, G, KSP, SEED = 4096, 14336, 8, 2, 2, 64, 0.8, 7
-N_CAL = 8
-WORKLOAD = ("config2: one Mixtral-8x7B MoE layer (d=4096, ffn=14336, 8 experts, top-2), "
-            "INT2 g64 up + ~80% contextual gate/down sparsity, single-token decode")
+N_CAL = 64                           # calibration tokens per layer
+N_MODEL_LAYERS = 32
+WORKLOAD = ("config3: 32-layer Mixtral-8x7B-shaped decode (d=4096, ffn=14336, 8 experts, top-2 "
+            "per layer), INT2 g64 up + ~80% contextual gate/down sparsity, all 256 experts "
+            "HBM-resident, batch 1")
 REC_BYTES = 4 * DH                   # one f16 gate|down channel record
 CODE_BYTES = DH * DI * BITS // 8     # 14,680,064
 META_BYTES = 4 * (DH * DI // G)      # 3,670,016
@@ -137,6 +151,11 @@ def max_over_ranks(value: float, world: int, device=None) -> float:
     return float(t.item())
 
 
+def whole_job_value(world: int, units_per_rank: int, max_ms: float) -> float:
+    """Whole-job throughput: the units ALL ranks processed over the slowest rank's time."""
+    return world * units_per_rank / (max_ms / 1000.0)
+
+
 def barrier(world: int):
     if world > 1:
         import torch.distributed as dist
@@ -144,23 +163,41 @@ def barrier(world: int):
 
 
 # ------------------------------------------------------------------ our arm
-def build_layer(fb, torch, layer_idx=0):
-    """gen_model streams (model.cpp:42-74) for one layer, generated and quantized in HBM."""
+def gen_float_layer(fb, layer_idx):
+    """gen_model streams (model.cpp:25-74) of one layer as f32 device tensors."""
     sigma = float(np.float32(1.0) / np.sqrt(np.float32(DH)))
-    router = fb.gen_normals(SEED, weight_stream(layer_idx, 0, 0), E * DH, sigma, sharded=True)
-    mixing = fb.gen_normals(SEED, weight_stream(layer_idx, 1, 0), DH * DH, sigma, sharded=True)
+    g = lambda kind, e, n: fb.gen_normals(SEED, weight_stream(layer_idx, kind, e), n, sigma,  # noqa: E731
+                                          sharded=True)
+    router = g(0, 0, E * DH).view(E, DH)
+    mixing = g(1, 0, DH * DH).view(DH, DH)
+    gate = [g(2, e, DH * DI).view(DI, DH) for e in range(E)]
+    up = [g(3, e, DH * DI).view(DI, DH) for e in range(E)]
+    down = [g(4, e, DH * DI).view(DI, DH) for e in range(E)]
+    return router, mixing, gate, up, down
+
+
+def build_layer(fb, torch, layer_idx=0):
+    """One compressed layer (thresholds 0; set by calibrate() / calibrate_layer())."""
+    router, mixing, gate, up, down = gen_float_layer(fb, layer_idx)
     experts = []
     for e in range(E):
-        gate = fb.gen_normals(SEED, weight_stream(layer_idx, 2, e), DH * DI, sigma, sharded=True)
-        up = fb.gen_normals(SEED, weight_stream(layer_idx, 3, e), DH * DI, sigma, sharded=True)
-        down = fb.gen_normals(SEED, weight_stream(layer_idx, 4, e), DH * DI, sigma, sharded=True)
-        codes, scales, zeros = fb.quantize(up, BITS, G)
-        del up
-        experts.append(fb.GpuExpert(DH, DI, BITS, G, codes, scales, zeros, gate=gate, down=down,
-                                    threshold=0.0))
-        del gate, down, codes, scales, zeros
+        codes, scales, zeros = fb.quantize(up[e].reshape(-1), BITS, G)
+        experts.append(fb.GpuExpert(DH, DI, BITS, G, codes, scales, zeros, gate=gate[e],
+                                    down=down[e], threshold=0.0))
+    del gate, up, down
     torch.cuda.synchronize()
-    return router.view(E, DH), mixing.view(DH, DH), experts
+    return router, mixing, experts
+
+
+def calibrate_layer(fb, torch, router, mixing, gate, up, down):
+    """calibrate_model(k=0.8) of one layer as a 1-layer model, on the device
+    (floe_gpu_calib_*; model.cpp:242-330): N_CAL block inputs token_input(3, t)."""
+    cal = fb.GpuCalib(1, E, DH, DI, 3)
+    h = torch.stack([fb.gen_normals(3, (1 << 40) + t, DH) for t in range(N_CAL)])
+    cal.layer(0, router, mixing, gate, up, down, TOPK, h, want_next=False)
+    th = cal.thresholds(KSP)[0]
+    cal.close()
+    return [float(t) for t in th]
 
 
 def quantile_threshold(torch, mags, k):
@@ -171,11 +208,11 @@ def quantile_threshold(torch, mags, k):
     return float(s[rank - 1].item())
 
 
-def calibrate(fb, torch, router, mixing, experts, ws):
-    """Per-expert t = 0.8-quantile of |qgemv(up_e, u)| over N_CAL calibration tokens,
-    u = h + mixing.h the block input (model.cpp:150-152)."""
+def calibrate(fb, torch, router, mixing, experts, ws, n_cal=8):
+    """Quick per-expert thresholds for tools: 0.8-quantile of |qgemv(up_e, u)| over
+    n_cal calibration tokens (the compressed up projection)."""
     mags = [[] for _ in experts]
-    for t in range(N_CAL):
+    for t in range(n_cal):
         h = fb.gen_normals(3, (1 << 40) + t, DH)
         u = h + mixing @ h
         for e, ex in enumerate(experts):
@@ -188,8 +225,28 @@ def calibrate(fb, torch, router, mixing, experts, ws):
     return ths
 
 
-N_LAYERS = 4   # distinct layers cycled (inputs larger than L2)
+N_LAYERS = 4   # (tools) distinct layers cycled
 N_EXPERTS_C1 = 4  # distinct config-1 experts cycled
+
+
+def build_model(fb, torch, n_layers):
+    """n_layers compressed layers of the seed-7 model, each calibrated on the device;
+    returns GpuLayers, thresholds [L][E]."""
+    layers, ths = [], []
+    for li in range(n_layers):
+        router, mixing, gate, up, down = gen_float_layer(fb, li)
+        th = calibrate_layer(fb, torch, router, mixing, gate, up, down)
+        experts = []
+        for e in range(E):
+            codes, scales, zeros = fb.quantize(up[e].reshape(-1), BITS, G)
+            experts.append(fb.GpuExpert(DH, DI, BITS, G, codes, scales, zeros, gate=gate[e],
+                                        down=down[e], threshold=th[e]))
+        del gate, up, down
+        layers.append(fb.GpuLayer(router, mixing, experts, TOPK, mixing_f16=True))
+        del router, mixing
+        ths.append(th)
+    torch.cuda.synchronize()
+    return layers, ths
 
 
 def time_region(torch, fn, n, stream):
@@ -204,6 +261,41 @@ def time_region(torch, fn, n, stream):
     return a.elapsed_time(b)
 
 
+def replay_inputs(fb, torch, n_tokens, n_layers, first=0):
+    """[n_tokens][L][dh] block inputs token_input(1, L*i + l)."""
+    return torch.stack([torch.stack([fb.gen_normals(1, (1 << 40) + n_layers * i + l, DH)
+                                     for l in range(n_layers)])
+                        for i in range(first, first + n_tokens)])
+
+
+def run_offload(fb, torch, layers, ws, n_tokens, budget_gb, stream):
+    """Config 3 host-resident: records in pinned host memory read in place over PCIe,
+    whole experts promoted into an HBM cache under the VRAM budget."""
+    L = len(layers)
+    off = fb.Offload(layers, int(budget_gb * (1 << 30)))
+    hs = replay_inputs(fb, torch, n_tokens + 2, L, first=1000)
+    y = torch.empty(L, DH, device="cuda")
+    for i in range(2):
+        off.decode_replay(hs[i], ws, out=y)
+    torch.cuda.synchronize()
+    s0 = off.stats()
+    ms = time_region(torch, lambda i: off.decode_replay(hs[2 + i], ws, out=y), n_tokens, stream)
+    s1 = off.stats()
+    off.close()
+    rb = s1["record_bytes"]
+    pcie = (s1["records_over_pcie"] - s0["records_over_pcie"]) * rb / n_tokens
+    hbm_rec = (s1["records_from_hbm"] - s0["records_from_hbm"]) * rb / n_tokens
+    sec = ms * 1e-3 / n_tokens
+    return {"workload": f"config3: {L}-layer decode, gate|down records host-resident "
+                        f"(pinned, read in place over PCIe), HBM expert cache {budget_gb} GB",
+            "tokens": n_tokens, "value": round(1.0 / sec, 3), "unit": "tokens/s",
+            "ms_per_token": round(sec * 1e3, 3),
+            "record_bytes_per_token_over_pcie": int(pcie),
+            "record_bytes_per_token_from_hbm": int(hbm_rec),
+            "pcie_gbs": round(pcie / sec / 1e9, 2),
+            "promotions": s1["promotions"] - s0["promotions"]}
+
+
 def run_ours(args, rank, world, local):
     import torch
     import torch.distributed as dist
@@ -216,31 +308,27 @@ def run_ours(args, rank, world, local):
     dev = fb.device_info()
     hbm_peak, peak_kind = peaks()
     stream = torch.cuda.current_stream()
+    L = args.layers
 
     # ---------------- setup (untimed) ----------------
     t_setup = time.perf_counter()
     ws = fb.Workspace(DH, DI, TOPK)
-    layers, all_thresholds = [], []
-    for li in range(N_LAYERS):
-        router, mixing, experts = build_layer(fb, torch, li)
-        all_thresholds.append(calibrate(fb, torch, router, mixing, experts, ws))
-        layers.append(fb.GpuLayer(router.cpu().numpy(), mixing.cpu().numpy(), experts, TOPK,
-                                  mixing_f16=True))
-        del router, mixing, experts
-    thresholds = all_thresholds[0]
+    layers, thresholds = build_model(fb, torch, L)
+    model = fb.GpuModel(layers)
     n_tok = args.warmup + args.steps
-    tokens = torch.stack([fb.gen_normals(1, (1 << 40) + t, DH) for t in range(n_tok)])
-    y = torch.empty(DH, dtype=torch.float32, device="cuda")
+    hs = replay_inputs(fb, torch, n_tok, L)   # [tokens][L][dh]
+    y = torch.empty(L, DH, dtype=torch.float32, device="cuda")
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
 
     def step(i, off=args.warmup):
-        fb.layer_forward(layers[(off + i) % N_LAYERS], tokens[off + i], ws, out=y)
+        model.decode(hs[off + i], ws, out=y, replay=True)
 
     # ---------------- warmup + timed region ----------------
     time_region(torch, lambda i: step(i, 0), args.warmup, stream)
     barrier(world)
     torch.cuda.synchronize()
+    ws.reset_counters()
     with ClockSampler(local) as clk:
         t0 = time.perf_counter()
         my_ms = time_region(torch, step, args.steps, stream)
@@ -248,100 +336,98 @@ def run_ours(args, rank, world, local):
         torch.cuda.synchronize()
         wall_s = time.perf_counter() - t0
     clocks = clk.summary()
+    cnt = ws.read_counters()  # fused launches and kept channels in the timed region
     max_ms = max_over_ranks(my_ms, world, torch.device("cuda", local))
-    value = world * args.steps / (max_ms / 1000.0)
+    value = whole_job_value(world, args.steps, max_ms)
+    launches = int(cnt["calls"])
+    kept_per_layer = cnt["kept"] / max(launches, 1)
+    # algorithmic bytes of one layer launch: f16 mixing + router +
+    # 2 experts' up codes/meta + the kept records + the vectors
+    layer_bytes = (MIX_BYTES + E * DH * 4 + TOPK * (CODE_BYTES + META_BYTES) +
+                   kept_per_layer * REC_BYTES + 4 * 4 * DH)
+    step_ms = my_ms / args.steps
+    layer_us = step_ms * 1e3 / L
+    achieved = layer_bytes / (layer_us * 1e-6) / 1e9
 
-    # ---------------- profiled pass: per-kernel shares + byte accounting ----------------
+    # ---------------- per-launch duration without PDL overlap (stage profiling) ----
     ws.set_profiling(True)
     ws.read_profile()
-    ws.reset_counters()
-    time_region(torch, step, args.steps, stream)
+    time_region(torch, step, min(args.steps, 4), stream)
     prof = ws.read_profile()
-    cnt = ws.read_counters()
     ws.set_profiling(False)
-    kept_per_step = cnt["kept"] / max(args.steps, 1)
-    stage_bytes = {
-        "mixing": MIX_BYTES + 3 * 4 * DH,
-        "route": E * DH * 4 + 4 * DH,
-        "k1_up_threshold": TOPK * (CODE_BYTES + META_BYTES) + 4 * DH,
-        "k2_gate_down": kept_per_step * REC_BYTES + 2 * 4 * DH,
-    }
-    layer_bytes = sum(stage_bytes.values())
-    stage_bytes["fused"] = layer_bytes  # whole layer in one launch
-    prof = {k: p for k, p in prof.items() if p["launches"] > 0}
-    stage = {}
-    for k, p in prof.items():
-        avg_ms = p["ms"] / max(p["launches"], 1)
-        stage[k] = dict(avg_us=round(avg_ms * 1e3, 3), bytes=int(stage_bytes[k]),
-                        gbs=round(stage_bytes[k] / (avg_ms * 1e-3) / 1e9, 1) if avg_ms > 0 else None)
-    total_stage_ms = sum(p["ms"] for p in prof.values())
-    for k, p in prof.items():
-        stage[k]["share"] = round(p["ms"] / total_stage_ms, 4) if total_stage_ms else None
-    dominant = max(stage, key=lambda k: stage[k]["share"] or 0)
-    d = stage[dominant]
+    fused = prof.get("fused", {"ms": 0.0, "launches": 0})
+    iso_us = 1e3 * fused["ms"] / max(fused["launches"], 1)
     traffic = None
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
-        traffic = json.loads(tf.read_text()).get(dominant)
-    roofline = {"bound": "hbm", "kernel": dominant, "achieved": d["gbs"], "peak": hbm_peak,
-                "peak_kind": peak_kind, "unit": "GB/s",
-                "frac": round(d["gbs"] / hbm_peak, 4) if d["gbs"] else None,
-                "traffic": traffic, "algorithmic_bytes_per_launch": d["bytes"],
-                "avg_launch_us": d["avg_us"]}
-    step_mean_ms = my_ms / args.steps
+        traffic = json.loads(tf.read_text()).get("fused")
+    roofline = {"bound": "hbm", "kernel": "floe_v2::fused<4096> (layer mode)",
+                "achieved": round(achieved, 1), "peak": hbm_peak, "peak_kind": peak_kind,
+                "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                "algorithmic_bytes_per_launch": int(layer_bytes),
+                "avg_launch_us": round(layer_us, 3),
+                "avg_launch_us_note": ("timed region / launches: one launch per layer, "
+                                       "back to back with programmatic dependent launch"),
+                "isolated_launch_us": round(iso_us, 3)}
 
-    # ---------------- config 1: single expert (expert_ffn) ----------------
+    # ---------------- config 1 (+ config-4 expert level) ----------------
     expert_ffn = run_expert(fb, torch, args, stream, hbm_peak)
 
-    # ---------------- e2e through the host-buffer API ----------------
-    tokens_h = tokens.cpu().numpy()
-    y_h = np.empty(DH, np.float32)
+    # ---------------- e2e through the host-buffer C ABI ----------------
+    hs_h = hs.cpu().numpy()
+    y_h = np.empty((L, DH), np.float32)
     for i in range(min(args.warmup, 3)):
-        fb.layer_forward_host(layers[i % N_LAYERS], tokens_h[i], ws, out=y_h)
+        model.decode_host(hs_h[i], ws, out=y_h, replay=True)
+    torch.cuda.synchronize()
     e2e_s = 0.0
     for i in range(args.steps):
-        torch.cuda.synchronize()
         t1 = time.perf_counter()
-        fb.layer_forward_host(layers[(args.warmup + i) % N_LAYERS], tokens_h[args.warmup + i], ws,
-                              out=y_h)
+        model.decode_host(hs_h[args.warmup + i], ws, out=y_h, replay=True)
         e2e_s += time.perf_counter() - t1
     e2e_max = max_over_ranks(e2e_s, world, torch.device("cuda", local))
-    e2e = {"value": round(world * args.steps / e2e_max, 2), "unit": "tokens/s",
-           "h2d_bytes_per_step": 4 * DH, "d2h_bytes_per_step": 4 * DH,
-           "api": "floe_gpu_layer_forward_host (pinned staging, stream sync)"}
+    e2e = {"value": round(world * args.steps / e2e_max, 3), "unit": "tokens/s",
+           "h2d_bytes_per_step": 4 * DH * L, "d2h_bytes_per_step": 4 * DH * L,
+           "api": "floe_gpu_model_decode_host (replay: the token's 32 block inputs in, "
+                  "32 block outputs back; pinned staging, stream sync)"}
 
     out = {
-        "metric": METRIC, "value": round(value, 2), "unit": "tokens/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_mean_ms, 5),
+        "metric": METRIC, "value": round(value, 3), "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_ms, 5),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32 accumulate (INT2 up codes, f16 gate/down records, f16 mixing)",
-        "data": "synthetic: reference gen_model streams (seed 7) generated+quantized on device",
-        "config": {"workload": WORKLOAD, "d_hidden": DH, "d_intermediate": DI, "experts": E,
-                   "top_k": TOPK, "bits": BITS, "group_size": G, "sparsity_k": KSP,
-                   "thresholds": [round(t, 6) for t in thresholds],
-                   "kept_channels_per_step": round(kept_per_step, 1),
+        "data": ("synthetic: reference gen_model streams (seed 7) generated+quantized on "
+                 "device; block inputs token_input(1, 32 i + l) (replay)"),
+        "config": {"workload": WORKLOAD, "layers": L, "d_hidden": DH, "d_intermediate": DI,
+                   "experts": E, "top_k": TOPK, "bits": BITS, "group_size": G,
+                   "sparsity_k": KSP,
+                   "thresholds": ("calibrate_model(k=0.8) per layer on the device "
+                                  f"({N_CAL} tokens token_input(3, t)), "
+                                  f"mean {float(np.mean(thresholds)):.4f}"),
+                   "kept_channels_per_layer": round(kept_per_layer, 1),
                    "parallelism": "replicas" if world > 1 else "single-gpu",
-                   "layers_cycled": N_LAYERS,
-                   "l2": (f"inputs larger than L2: {N_LAYERS} distinct gen_model layers cycled, "
-                          "~165 MB touched per step, no flush; K steps back to back in one "
-                          "event region"),
-                   "tokens": "token_input(1, t)"},
+                   "l2": (f"inputs larger than L2: {L * 0.1645:.2f} GB of weights per token "
+                          "(126 MB L2), no flush; K steps back to back in one event region")},
         "roofline": roofline,
-        "step_roofline": {"bytes_per_step": int(layer_bytes),
-                          "achieved": round(layer_bytes / (step_mean_ms * 1e-3) / 1e9, 1),
-                          "peak": hbm_peak, "unit": "GB/s",
-                          "frac": round(layer_bytes / (step_mean_ms * 1e-3) / 1e9 / hbm_peak, 4)},
-        "stages": stage,
+        "layer": {"workload": "config2: the same layer launches (one Mixtral MoE layer, "
+                              "single-token decode)",
+                  "value": round(value * L, 1), "unit": "layer-tokens/s",
+                  "us_per_layer": round(layer_us, 3),
+                  "bytes_per_layer": int(layer_bytes)},
         "expert_ffn": expert_ffn,
         "e2e": e2e,
-        "gpu_launches": sum(p["launches"] for p in prof.values()),
+        "gpu_launches": launches,
         "clocks": clocks,
         "wall_s_timed_region": round(wall_s, 4),
         "setup_s": round(setup_s, 2),
         "device": dev,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(thresholds, tokens_h[args.warmup:])
+        out["cpu_baseline"] = cpu_baseline(thresholds, hs_h[args.warmup:], L)
+    if not args.no_offload and world == 1:
+        try:
+            out["offload"] = run_offload(fb, torch, layers, ws, 6, 16.0, stream)
+        except Exception as e:  # report, do not lose the main line
+            out["offload"] = {"error": str(e)[:200]}
     if world > 1:
         dist.destroy_process_group()
     return out
@@ -414,39 +500,47 @@ def run_expert(fb, torch, args, stream, hbm_peak):
 
 
 # ------------------------------------------------------------------ reference arm
-def build_reference_model(thresholds, workers):
-    """gen_model(seed 7) -> compress_model(INT2 g64, given thresholds) in the
-    UNMODIFIED reference core (oracle/_ref/libfloe_ref.so)."""
+REF_LAYERS = 2  # layers of the model the reference arm builds and times (a bounded sample)
+
+
+def ref_model_from_thresholds(thresholds, workers):
+    """gen_model(seed 7, REF_LAYERS layers) -> compress_model(INT2 g64, given
+    thresholds) in the UNMODIFIED reference core (oracle/_ref/libfloe_ref.so)."""
     from oracle import oracle as O
     if O.REF is None:
         return None, None
-    th = np.ascontiguousarray(thresholds, np.float32)
-    cm = O.REF.ref_cmodel_build_thresholds(1, E, TOPK, DH, DI, SEED, th, BITS, G, workers)
+    th = np.ascontiguousarray(np.asarray(thresholds, np.float32)[:REF_LAYERS].reshape(-1))
+    cm = O.REF.ref_cmodel_build_thresholds(REF_LAYERS, E, TOPK, DH, DI, SEED, th, BITS, G,
+                                           workers)
     if not cm:
         raise RuntimeError(O.ref_error())
     return O, cm
 
 
-def cpu_baseline(thresholds, tokens_h, budget_s=15.0):
+def cpu_baseline(thresholds, hs_h, L, budget_s=15.0):
     """Reference layer_forward(CompressedModel) on ONE host thread (the reference
-    path is single-threaded), on a bounded sample of the same decode tokens."""
-    O, cm = build_reference_model(thresholds, os.cpu_count() or 1)
+    path is single-threaded) over a bounded sample: the first REF_LAYERS layers
+    of the same model, the same thresholds and replayed block inputs; per-token
+    time = L x the mean layer time (every layer has the same shapes)."""
+    O, cm = ref_model_from_thresholds(thresholds, os.cpu_count() or 1)
     if cm is None:
         return {"value": None, "unit": "tokens/s", "cores": 1, "kind": "reference",
                 "sample": "unavailable: oracle/_ref/libfloe_ref.so missing"}
     y = np.empty(DH, np.float32)
     t0 = time.perf_counter()
-    O.REF.ref_layer_forward(cm, 0, np.ascontiguousarray(tokens_h[0]), y)
+    O.REF.ref_layer_forward(cm, 0, np.ascontiguousarray(hs_h[0][0]), y)
     one = time.perf_counter() - t0
-    n = int(min(max(budget_s / max(one, 1e-3), 2), 64, len(tokens_h)))
+    n = int(min(max(budget_s / max(one, 1e-3), 2), 64))
     t0 = time.perf_counter()
     for i in range(n):
-        O.REF.ref_layer_forward(cm, 0, np.ascontiguousarray(tokens_h[i]), y)
+        tok, l = divmod(i, REF_LAYERS)
+        O.REF.ref_layer_forward(cm, l, np.ascontiguousarray(hs_h[tok % len(hs_h)][l]), y)
     dt = time.perf_counter() - t0
     O.REF.ref_cmodel_destroy(cm)
-    return {"value": round(n / dt, 4), "unit": "tokens/s", "cores": 1, "kind": "reference",
-            "sample": f"{n} decode tokens of the same layer through floe::layer_forward "
-                      f"(1 thread, {dt:.1f} s)", "cpu": cpu_model()}
+    return {"value": round(n / dt / L, 5), "unit": "tokens/s", "cores": 1, "kind": "reference",
+            "sample": (f"{n} floe::layer_forward calls over layers 0..{REF_LAYERS - 1} of the "
+                       f"same model and inputs (1 thread, {dt:.1f} s); tokens/s = layer "
+                       f"calls/s / {L}"), "cpu": cpu_model()}
 
 
 def cpu_model() -> str:
@@ -459,78 +553,63 @@ def cpu_model() -> str:
     return f"unknown x{os.cpu_count()}"
 
 
-def reference_thresholds():
-    """Thresholds for the reference arm, computed by the reference itself the
-    same way the GPU arm computes them (0.8-quantile of |qgemv(up_e, u)| over
-    8 calibration tokens) but through floe::qgemv_channels on the host."""
-    from oracle import oracle as O
-    # the reference arm must not need a GPU: regenerate up projections on the host
-    sigma = float(np.float32(1.0) / np.sqrt(np.float32(DH)))
-    mixing = np.empty(DH * DH, np.float32)
-    O.C.fo_fill_gaussian(mixing, mixing.size, SEED, weight_stream(0, 1, 0), np.float32(sigma),
-                         O.THREADS)
-    mixing = mixing.reshape(DH, DH)
-    us = []
-    for t in range(N_CAL):
-        h = O.token_input(3, t, DH)
-        mixed = np.empty(DH, np.float32)
-        O.C.fo_gemv(DH, DH, mixing, h, mixed)
-        us.append(h + mixed)
-    ths = []
-    up = np.empty(DH * DI, np.float32)
-    for e in range(E):
-        O.C.fo_fill_gaussian(up, up.size, SEED, weight_stream(0, 3, e), np.float32(sigma),
-                             O.THREADS)
-        q = O.quantize(up, BITS, G)
-        mags = np.concatenate([np.abs(O.qgemv_channels(q, DH, u)) for u in us])
-        ths.append(O.calibrate_threshold(mags, KSP))
-    return ths
-
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's own CPU layer_forward on all host threads
-    (independent tokens per thread), rank 0 only."""
+    """--impl reference: the reference's own CPU path on all host threads, rank 0
+    only: gen_model(seed 7) -> calibrate_model(k=0.8) per layer (as the GPU arm
+    calibrates) -> compress_model -> layer_forward(CompressedModel) on replayed
+    block inputs, independent (token, layer) calls split over the threads.  A
+    bounded sample: REF_LAYERS of the 32 layers; tokens/s = layer calls/s / 32."""
     from oracle import oracle as O
+    L = args.layers
     if O.REF is None:
         return {"impl": "reference", "metric": METRIC, "unit": "tokens/s",
                 "unavailable": "oracle/_ref/libfloe_ref.so not built (reference sources absent)"}
     threads = os.cpu_count() or 1
     t_setup = time.perf_counter()
-    ths = reference_thresholds()
-    O_, cm = build_reference_model(ths, threads)
+    ths = np.empty(REF_LAYERS * E, np.float32)
+    cm = O.REF.ref_cmodel_build_replay(REF_LAYERS, E, TOPK, DH, DI, SEED, 3, N_CAL, KSP, BITS, G,
+                                       threads, ths)
+    if not cm:
+        raise RuntimeError(O.ref_error())
     setup_s = time.perf_counter() - t_setup
-    per_step = threads  # one token per thread per step
-    n_tok = (args.warmup + args.steps) * per_step
-    toks = np.stack([O.token_input(1, t, DH) for t in range(min(n_tok, 4096))])
-    toks = np.ascontiguousarray(np.resize(toks, (n_tok, DH)))
-    for s in range(args.warmup):
-        O.REF.ref_layer_forward_replicas(cm, 0, toks[s * per_step:(s + 1) * per_step], per_step,
-                                         threads)
+    per_step = threads  # one layer call per thread per step
+    n_calls = (args.warmup + args.steps) * per_step
+    # replayed block inputs token_input(1, 32 i + l) of the same layers as the GPU arm
+    toks = np.stack([O.token_input(1, L * (c // REF_LAYERS) + (c % REF_LAYERS), DH)
+                     for c in range(min(n_calls, 4096))])
+    toks = np.ascontiguousarray(np.resize(toks, (n_calls, DH)))
     times = []
-    for s in range(args.steps):
-        base = (args.warmup + s) * per_step
-        dt = O.REF.ref_layer_forward_replicas(cm, 0, toks[base:base + per_step], per_step,
-                                              threads)
+    for s in range(args.warmup + args.steps):
+        base = s * per_step
+        dt = O.REF.ref_layer_calls_replicas(cm, REF_LAYERS, toks[base:base + per_step], per_step,
+                                            threads)
         if dt < 0:
             raise RuntimeError("reference layer_forward failed")
-        times.append(dt)
+        if s >= args.warmup:
+            times.append(dt)
     O.REF.ref_cmodel_destroy(cm)
     total = sum(times)
-    value = args.steps * per_step / total
-    return {"impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "tokens/s",
+    value = args.steps * per_step / total / L
+    return {"impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": "tokens/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(1e3 * total / args.steps, 3), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic: reference gen_model (seed 7) + compress_model, host",
-            "config": {"workload": WORKLOAD, "d_hidden": DH, "d_intermediate": DI, "experts": E,
-                       "top_k": TOPK, "bits": BITS, "group_size": G, "sparsity_k": KSP,
-                       "thresholds": [round(float(t), 6) for t in ths],
-                       "parallelism": f"{threads} host threads, independent tokens"},
-            "cpu_baseline": {"value": round(value, 4), "unit": "tokens/s", "cores": threads,
+            "data": "synthetic: reference gen_model (seed 7) + calibrate_model + compress_model, "
+                    "host; replayed block inputs token_input(1, 32 i + l)",
+            "config": {"workload": WORKLOAD, "layers": L, "d_hidden": DH, "d_intermediate": DI,
+                       "experts": E, "top_k": TOPK, "bits": BITS, "group_size": G,
+                       "sparsity_k": KSP,
+                       "thresholds": (f"calibrate_model(k=0.8) per layer ({N_CAL} tokens), "
+                                      f"mean {float(np.mean(ths)):.4f}"),
+                       "parallelism": f"{threads} host threads, independent layer calls"},
+            "cpu_baseline": {"value": round(value, 5), "unit": "tokens/s", "cores": threads,
                              "kind": "reference",
-                             "sample": f"{per_step} tokens per step (one per thread), "
-                                       f"floe::layer_forward(CompressedModel)", "cpu": cpu_model()},
-            "e2e": {"value": round(value, 4), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                             "sample": (f"{per_step} floe::layer_forward calls per step over "
+                                        f"layers 0..{REF_LAYERS - 1} (one per thread); "
+                                        f"tokens/s = layer calls/s / {L}"),
+                             "cpu": cpu_model()},
+            "e2e": {"value": round(value, 5), "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
             "setup_s": round(setup_s, 2)}
 
@@ -538,10 +617,12 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--layers", type=int, default=N_MODEL_LAYERS)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-offload", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = dist_env()

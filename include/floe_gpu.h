@@ -304,6 +304,24 @@ int floe_gpu_workspace_set_phase_trace(floe_gpu_workspace *ws, int enable);
 int floe_gpu_workspace_read_phase_trace(floe_gpu_workspace *ws, uint64_t *out, uint32_t cap,
                                         uint32_t *grid);
 
+/* ----------------------------------------------------------------- models */
+/* A stack of HBM-resident compressed layers (floe::CompressedModel) decoded
+ * token by token: the reference's `run` loop, h = layer_forward(m, l, h) for
+ * l = 0..L-1 (tools/cli.cpp:86-107).  Layers are borrowed. */
+typedef struct floe_gpu_model floe_gpu_model;
+int floe_gpu_model_create(floe_gpu_layer *const *layers, uint32_t n_layers,
+                          floe_gpu_model **out);
+int floe_gpu_model_destroy(floe_gpu_model *m);
+/* replay == 0: h_dev [dh] through every layer into y_dev [dh].
+ * replay != 0: layer l reads h_dev[l*dh ..] and writes y_dev[l*dh ..] (the
+ * recorded block inputs of predictor.cpp:60-85); each layer still waits for
+ * the previous one, as a chained decode does.  Stream-ordered. */
+int floe_gpu_model_decode(floe_gpu_model *m, floe_gpu_workspace *ws, const float *h_dev,
+                          float *y_dev, int replay, floe_stream_t stream);
+/* The same from/to HOST memory through pinned staging; synchronises `stream`. */
+int floe_gpu_model_decode_host(floe_gpu_model *m, floe_gpu_workspace *ws, const float *h_host,
+                               float *y_host, int replay, floe_stream_t stream);
+
 /* ------------------------------------------------------------ calibration */
 /* Threshold calibration on the device, bit-exact with the reference's
  * collect_stats + calibrate_model (core/src/model.cpp:242-330) and

@@ -116,6 +116,9 @@ def _load_ref():
     _sig(lib, "ref_cmodel_build_thresholds", _vp, _u32, _u32, _u32, _u32, _u32, _u64, _f32p,
          ct.c_uint, _u32, ct.c_uint)
     _sig(lib, "ref_layer_forward_replicas", _dbl, _vp, _u32, _f32p, _u32, ct.c_uint)
+    _sig(lib, "ref_layer_calls_replicas", _dbl, _vp, _u32, _f32p, _u32, ct.c_uint)
+    _sig(lib, "ref_cmodel_build_replay", _vp, _u32, _u32, _u32, _u32, _u32, _u64, _u64, _u64,
+         _dbl, ct.c_uint, _u32, ct.c_uint, _f32p)
     _sig(lib, "ref_calibrate_weights", _int, _u32, _u32, _u32, _u32, _u32, _f32p, _f32p, _f32p,
          _f32p, _f32p, _u64, _u64, _dbl, _u64, ct.c_uint, _flt, _f32p)
     _sig(lib, "ref_cmodel_load", _vp, ct.c_char_p)

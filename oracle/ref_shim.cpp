@@ -370,6 +370,43 @@ void *ref_cmodel_build_thresholds(std::uint32_t layers, std::uint32_t experts,
   }
 }
 
+// gen_model(seed) with `layers` layers; every layer calibrated as a 1-layer
+// model (calibrate_model on layer l's weights alone: the replayed block
+// inputs the decode bench feeds each layer) -> compress_model.  The
+// thresholds go to out[L*E].
+void *ref_cmodel_build_replay(std::uint32_t layers, std::uint32_t experts, std::uint32_t top_k_n,
+                              std::uint32_t dh, std::uint32_t di, std::uint64_t seed,
+                              std::uint64_t calib_seed, std::uint64_t calib_tokens, double k,
+                              unsigned bits, std::uint32_t g, unsigned workers, float *out) {
+  try {
+    MoEConfig cfg;
+    cfg.layers = layers;
+    cfg.experts = experts;
+    cfg.top_k = top_k_n;
+    cfg.d_hidden = dh;
+    cfg.d_intermediate = di;
+    cfg.seed = seed;
+    MoEModel m = gen_model(cfg, workers);
+    ThresholdTable t(layers, experts);
+    for (std::uint32_t l = 0; l < layers; ++l) {
+      MoEModel one;
+      one.cfg = cfg;
+      one.cfg.layers = 1;
+      one.layers.push_back(std::move(m.layers[l]));
+      ThresholdTable tl = calibrate_model(one, calib_seed, calib_tokens, k, kReservoirCap, workers);
+      m.layers[l] = std::move(one.layers[0]);
+      for (std::uint32_t e = 0; e < experts; ++e) {
+        t.set(l, e, tl.at(0, e), static_cast<float>(k));
+        out[l * experts + e] = tl.at(0, e);
+      }
+    }
+    return new CompressedModel(compress_model(m, t, bits, g));
+  } catch (const std::exception &e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
 // calibrate_model (model.cpp:323-330) on a float model given as arrays:
 // router [L][E][dh], mixing [L][dh][dh], gate/up/down_t [L][E][di][dh]; the
 // thresholds go to out[L*E].  Returns 0 or -1 (ref_last_error).
@@ -428,6 +465,32 @@ double ref_layer_forward_replicas(void *cm, std::uint32_t layer, const float *hs
         for (std::uint32_t i = t; i < n_tokens; i += threads) {
           Vec out = layer_forward(*m, layer, Vec(hs + (std::size_t)i * dh,
                                                  hs + (std::size_t)(i + 1) * dh));
+          if (out.size() != dh) failed = true;
+        }
+      } catch (...) {
+        failed = true;
+      }
+    });
+  for (auto &t : pool) t.join();
+  auto t1 = std::chrono::steady_clock::now();
+  return failed ? -1.0 : std::chrono::duration<double>(t1 - t0).count();
+}
+
+// `threads` host threads split n independent layer_forward calls: call i runs
+// layer i % n_layers on input hs[i].  Returns wall seconds, negative on error.
+double ref_layer_calls_replicas(void *cm, std::uint32_t n_layers, const float *hs,
+                                std::uint32_t n, unsigned threads) {
+  auto *m = static_cast<CompressedModel *>(cm);
+  const std::uint32_t dh = m->cfg.d_hidden;
+  std::vector<std::thread> pool;
+  bool failed = false;
+  auto t0 = std::chrono::steady_clock::now();
+  for (unsigned t = 0; t < threads; ++t)
+    pool.emplace_back([&, t] {
+      try {
+        for (std::uint32_t i = t; i < n; i += threads) {
+          Vec out = layer_forward(*m, i % n_layers,
+                                  Vec(hs + (std::size_t)i * dh, hs + (std::size_t)(i + 1) * dh));
           if (out.size() != dh) failed = true;
         }
       } catch (...) {

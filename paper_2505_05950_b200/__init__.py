@@ -16,6 +16,7 @@ from ._abi import (  # noqa: F401
     GpuCalib,
     GpuExpert,
     GpuLayer,
+    GpuModel,
     GpuPredictor,
     Offload,
     Workspace,
@@ -37,7 +38,7 @@ from ._abi import (  # noqa: F401
     quantize,
 )
 
-__all__ = ["FloeError", "GpuCalib", "GpuExpert", "GpuLayer", "GpuPredictor", "Offload", "Workspace",
+__all__ = ["FloeError", "GpuCalib", "GpuExpert", "GpuLayer", "GpuModel", "GpuPredictor", "Offload", "Workspace",
            "abi_version", "dequantize", "device_info", "expert_forward_sparse",
            "exported_symbols", "layer_forward", "lib", "library_path", "predict_experts",
            "predict_mask", "qgemv_channels", "qgemv_channels_batched", "expert_forward_batched", "gen_normals", "layer_forward_host",

@@ -113,6 +113,10 @@ _SIGS = {
     "floe_gpu_predictor_create": (ct.c_int, [_U32, _U32, _U32, _P, _P, ct.POINTER(_P)]),
     "floe_gpu_predictor_destroy": (ct.c_int, [_P]),
     "floe_gpu_predict_experts": (ct.c_int, [_P, _P, _U32, _U32, _P, _P]),
+    "floe_gpu_model_create": (ct.c_int, [_P, _U32, ct.POINTER(_P)]),
+    "floe_gpu_model_destroy": (ct.c_int, [_P]),
+    "floe_gpu_model_decode": (ct.c_int, [_P, _P, _P, _P, ct.c_int, _P]),
+    "floe_gpu_model_decode_host": (ct.c_int, [_P, _P, _P, _P, ct.c_int, _P]),
     "floe_gpu_calib_create": (ct.c_int, [_U32, _U32, _U32, _U32, ct.c_uint64, ct.c_uint64,
                                          ct.POINTER(_P)]),
     "floe_gpu_calib_destroy": (ct.c_int, [_P]),
@@ -410,13 +414,20 @@ def predict_mask(e_next: GpuExpert, x_prev, t: float, ws: Workspace, *, kept=Non
 class GpuLayer:
     """One compressed MoE block (floe::CompressedLayer + top_k) on the device."""
 
-    def __init__(self, router: np.ndarray, mixing: np.ndarray, experts: list[GpuExpert],
-                 top_k: int, mixing_f16: bool = True):
-        router = np.ascontiguousarray(router, np.float32)
-        mixing = np.ascontiguousarray(mixing, np.float32)
+    def __init__(self, router, mixing, experts: list[GpuExpert], top_k: int,
+                 mixing_f16: bool = True):
+        """router [E][dh], mixing [dh][dh]: f32 numpy arrays or cuda tensors."""
+        if hasattr(router, "data_ptr"):
+            router = router.float().contiguous()
+        else:
+            router = np.ascontiguousarray(router, np.float32)
+        if hasattr(mixing, "data_ptr"):
+            mixing = mixing.float().contiguous()
+        else:
+            mixing = np.ascontiguousarray(mixing, np.float32)
         E = len(experts)
         arr = (ct.c_void_p * E)(*[e.handle for e in experts])
-        v = LayerHostView(mixing.shape[0], E, top_k, router.ctypes.data, mixing.ctypes.data,
+        v = LayerHostView(mixing.shape[0], E, top_k, _ptr(router), _ptr(mixing),
                           1 if mixing_f16 else 0, ct.addressof(arr))
         h = ct.c_void_p()
         _check(lib().floe_gpu_layer_create(ct.byref(v), ct.byref(h)))
@@ -578,6 +589,48 @@ class Offload:
         st = OffloadStats()
         _check(lib().floe_gpu_offload_stats(self.handle, ct.byref(st), _stream(stream)))
         return {f: getattr(st, f) for f, _ in OffloadStats._fields_}
+
+
+class GpuModel:
+    """A stack of HBM-resident compressed layers (floe::CompressedModel) decoded
+    token by token, the reference's run loop (cli.cpp:86-107)."""
+
+    def __init__(self, layers):
+        arr = (ct.c_void_p * len(layers))(*[l.handle for l in layers])
+        h = ct.c_void_p()
+        _check(lib().floe_gpu_model_create(arr, len(layers), ct.byref(h)))
+        self.handle = h.value
+        self.layers = layers
+        self.d_hidden = layers[0].d_hidden
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().floe_gpu_model_destroy(self.handle)
+            self.handle = None
+
+    __del__ = close
+
+    def decode(self, h, ws: Workspace, out=None, replay: bool = False, stream=None):
+        """replay=False: h [dh] -> y [dh] through every layer.  replay=True: h [L, dh]
+        -> y [L, dh], layer l on its own block input."""
+        torch = _torch()
+        shape = (len(self.layers), self.d_hidden) if replay else (self.d_hidden,)
+        if tuple(h.shape) != shape or h.dtype != torch.float32 or not h.is_cuda:
+            raise FloeError(f"model_decode: h must be a cuda float32 {shape}")
+        h = h.contiguous()
+        y = torch.empty_like(h) if out is None else out
+        _check(lib().floe_gpu_model_decode(self.handle, ws.handle, h.data_ptr(), y.data_ptr(),
+                                           1 if replay else 0, _stream(stream)))
+        return y
+
+    def decode_host(self, h: np.ndarray, ws: Workspace, out=None, replay: bool = False,
+                    stream=None):
+        h = np.ascontiguousarray(h, np.float32)
+        y = np.empty_like(h) if out is None else out
+        _check(lib().floe_gpu_model_decode_host(self.handle, ws.handle, h.ctypes.data,
+                                                y.ctypes.data, 1 if replay else 0,
+                                                _stream(stream) if stream is not None else 0))
+        return y
 
 
 class GpuCalib:

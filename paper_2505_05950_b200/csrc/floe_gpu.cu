@@ -1736,6 +1736,91 @@ int floe_gpu_offload_stats(floe_gpu_offload *o, floe_offload_stats *out, floe_st
 
 }  // extern "C"
 
+// ------------------------------------------------------------------ models ---
+// A stack of HBM-resident compressed layers decoded token by token: the
+// reference's `run` loop h = layer_forward(m, l, h) over l (cli.cpp:86-107).
+struct floe_gpu_model {
+  std::vector<const floe_gpu_layer *> layers;
+  uint32_t dh = 0;
+  float *buf = nullptr;                        // ping-pong [2][dh]
+  float *hin = nullptr, *hout = nullptr;       // device staging [L][dh]
+  float *pin_in = nullptr, *pin_out = nullptr; // pinned host staging [L][dh]
+};
+
+extern "C" {
+
+int floe_gpu_model_create(floe_gpu_layer *const *layers, uint32_t n_layers,
+                          floe_gpu_model **out) {
+  if (!layers || !out || n_layers == 0) return fail(FLOE_ERR_INVALID, "model_create: bad arguments");
+  *out = nullptr;
+  if (int rc = require_device("model_create")) return rc;
+  auto m = std::make_unique<floe_gpu_model>();
+  for (uint32_t l = 0; l < n_layers; ++l) {
+    if (!layers[l] || layers[l]->dh != layers[0]->dh)
+      return fail(FLOE_ERR_INVALID, "model_create: layer %u shape differs", l);
+    m->layers.push_back(layers[l]);
+  }
+  m->dh = layers[0]->dh;
+  const size_t v = 4ull * m->dh * n_layers;
+  CK(cudaMalloc(&m->buf, 8ull * m->dh));
+  CK(cudaMalloc(&m->hin, v));
+  CK(cudaMalloc(&m->hout, v));
+  CK(cudaMallocHost(&m->pin_in, v));
+  CK(cudaMallocHost(&m->pin_out, v));
+  *out = m.release();
+  return FLOE_OK;
+}
+
+int floe_gpu_model_destroy(floe_gpu_model *m) {
+  if (!m) return FLOE_OK;
+  cudaDeviceSynchronize();
+  cudaFree(m->buf);
+  cudaFree(m->hin);
+  cudaFree(m->hout);
+  cudaFreeHost(m->pin_in);
+  cudaFreeHost(m->pin_out);
+  delete m;
+  return FLOE_OK;
+}
+
+// replay == 0: h [dh] -> layer 0 -> ... -> y [dh];  replay != 0: layer l reads
+// h[l] and writes y[l] (recorded block inputs, predictor.cpp:60-85): every
+// layer's work is that of a decode whose hidden states keep their scale, and
+// each launch still waits for the previous layer (stream order + PDL), as a
+// chained decode does.
+int floe_gpu_model_decode(floe_gpu_model *m, floe_gpu_workspace *ws, const float *h, float *y,
+                          int replay, floe_stream_t stream) {
+  if (!m || !ws || !h || !y) return fail(FLOE_ERR_INVALID, "model_decode: null argument");
+  cudaStream_t st = S(stream);
+  const uint32_t L = (uint32_t)m->layers.size();
+  const float *in = h;
+  for (uint32_t l = 0; l < L; ++l) {
+    const floe_gpu_layer *ly = m->layers[l];
+    if (int rc = check_ws("layer_forward", ws, ly->dh, ly->di, ly->top_k)) return rc;
+    float *o = replay ? y + (size_t)l * m->dh : (l + 1 == L ? y : m->buf + (l & 1) * m->dh);
+    if (replay) in = h + (size_t)l * m->dh;
+    if (int rc = layer_forward_impl(ly, ws, in, o, nullptr, nullptr, st)) return rc;
+    in = o;
+  }
+  return FLOE_OK;
+}
+
+int floe_gpu_model_decode_host(floe_gpu_model *m, floe_gpu_workspace *ws, const float *h_host,
+                               float *y_host, int replay, floe_stream_t stream) {
+  if (!m || !ws || !h_host || !y_host) return fail(FLOE_ERR_INVALID, "model_decode: null argument");
+  cudaStream_t st = S(stream);
+  const size_t bytes = 4ull * m->dh * (replay ? m->layers.size() : 1);
+  std::memcpy(m->pin_in, h_host, bytes);
+  CK(cudaMemcpyAsync(m->hin, m->pin_in, bytes, cudaMemcpyHostToDevice, st));
+  if (int rc = floe_gpu_model_decode(m, ws, m->hin, m->hout, replay, stream)) return rc;
+  CK(cudaMemcpyAsync(m->pin_out, m->hout, bytes, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::memcpy(y_host, m->pin_out, bytes);
+  return FLOE_OK;
+}
+
+}  // extern "C"
+
 // ------------------------------------------------------------ calibration ---
 // collect_stats / calibrate_model on the device (floe_calib.cuh; reference
 // core/src/model.cpp:242-330, core/src/sparsify.cpp:42-64,128-142).

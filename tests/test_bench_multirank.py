@@ -66,6 +66,6 @@ def test_replica_value_is_whole_job_throughput():
     """value = N * steps / max-over-ranks time: the units all ranks processed."""
     sys.path.insert(0, str(ROOT))
     import bench
-    src = Path(bench.__file__).read_text()
-    assert "value = world * args.steps / (max_ms / 1000.0)" in src
+    assert bench.whole_job_value(1, 20, 1000.0) == 20.0
+    assert bench.whole_job_value(4, 20, 2000.0) == 40.0  # 4 ranks x 20 tokens in 2 s
     assert bench.max_over_ranks(3.5, 1) == 3.5
