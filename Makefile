@@ -9,7 +9,7 @@ LIB      := $(PKG)/libfloe_b200.so
 SRCS     := $(PKG)/csrc/floe_gpu.cu
 HDRS     := $(wildcard $(PKG)/csrc/*.cuh) include/floe_gpu.h
 
-all: $(LIB) oracle
+all: $(LIB) oracle integration
 
 $(LIB): $(SRCS) $(HDRS)
 	$(NVCC) $(NVFLAGS) -shared -cudart static -o $@ $(SRCS) 2> build_ptxas.log || (cat build_ptxas.log; exit 1)
@@ -17,11 +17,16 @@ $(LIB): $(SRCS) $(HDRS)
 oracle:
 	$(MAKE) -C oracle
 
+# INTEGRATION.md build: the reference core compiled in place + floe_b200.hpp (reference types)
+integration: $(LIB)
+	$(MAKE) -C tests/cpp
+
 clean:
 	rm -f $(LIB) build_ptxas.log
 	$(MAKE) -C oracle clean
+	$(MAKE) -C tests/cpp clean
 
-.PHONY: all oracle clean
+.PHONY: all oracle integration clean
 
 # Sanitizer build: same sources, a 600 s barrier watchdog (compute-sanitizer
 # slows the kernels by orders of magnitude), separate output used through

@@ -2,7 +2,7 @@
 //
 // A drop-in for the FloE hot path of the reference core (namespace floe,
 // /root/reference/proj/core/include/floe/{quant,model,predictor}.hpp): the
-// same type layouts, function names, argument meaning and error behaviour
+// same function names, argument meaning and error behaviour
 // (std::runtime_error with the reference's "<fn>: <reason>" messages), with
 // the arithmetic running on the B200 through include/floe_gpu.h.  Header-only
 // C++17; link with -lfloe_b200.
@@ -18,18 +18,39 @@
 //   std::vector<uint32_t> predict_experts(const InterExpertPredictor&, const Vec&, uint32_t,
 //                                         uint32_t)                         predictor.hpp:75-77
 //
-// The free functions take the reference's host value types and keep a
-// per-process upload cache keyed by the object's address and a fingerprint
-// of its buffers (the reference treats models as immutable after load,
-// SPEC.md:332), so repeated calls on the same expert/model pay the host->HBM
-// upload once.  DeviceExpert / DeviceLayer / Workspace give explicit control
-// (stream-ordered device calls, no hidden synchronisation) for callers that
-// manage their own device memory.
+// Two ways to use it:
+//   * inside the reference build: #include the reference's
+//     floe/model.hpp and floe/predictor.hpp first and define
+//     FLOE_B200_REFERENCE_TYPES; floe::gpu then takes the reference's own
+//     floe::CompressedExpert / CompressedModel / QuantizedTensor /
+//     InterExpertPredictor objects, zero copy (the upload reads their vectors
+//     in place);
+//   * standalone: floe::gpu defines the same types with the same field names
+//     AND storage order as the reference (quant.hpp:20-31, la.hpp:19-32,
+//     model.hpp:26-35,60-83,121-129, predictor.hpp:20-33).
+// The entry points are templates over those types (field names only), so both
+// compile to the same code.
+//
+// Upload cache: the free functions keep the device copy of each expert/layer/
+// predictor they were called with, keyed by the object's address AND a
+// content fingerprint (sizes, threshold and 64 sampled words of every weight
+// buffer), so a freed-and-reallocated or replaced object at the same address
+// is uploaded again; at most kCacheEntries objects are kept (least recently
+// used evicted); clear_cache() drops everything (call it after editing
+// weights in place: sampled fingerprints do not see every element).
+// Threads: every host thread gets its own workspace (pinned staging, device
+// scratch), and all value-type calls run on the legacy default stream, so
+// concurrent calls from several threads serialise on the device and never
+// share buffers -- thread-compatible like the reference.
+// DeviceExpert / DeviceLayer / Workspace give explicit control (stream-ordered
+// device calls, no hidden synchronisation) for callers that manage their own
+// device memory.
 #pragma once
 
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <list>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -43,15 +64,24 @@
 namespace floe {
 namespace gpu {
 
+// ---------------------------------------------------------------- types
+#ifdef FLOE_B200_REFERENCE_TYPES
+using floe::CompressedExpert;
+using floe::CompressedLayer;
+using floe::CompressedModel;
+using floe::InterExpertPredictor;
+using floe::LayerTrace;
+using floe::Matrix;
+using floe::MoEConfig;
+using floe::QuantizedTensor;
+using floe::Vec;
+#else
 using Vec = std::vector<float>;
 
-// ---------------------------------------------------------------- types
-// Same fields and meaning as the reference (quant.hpp:20-31, la.hpp:19-32,
-// model.hpp:26-35,60-83,121-129, predictor.hpp:20-33).
 struct QuantizedTensor {
-  unsigned bits = 0;
-  std::uint32_t group_size = 0;
-  std::uint64_t n = 0;
+  std::size_t n = 0;                  // element count
+  unsigned bits = 0;                  // one of {1, 2, 3, 4, 8}
+  std::uint32_t group_size = 0;       // consecutive elements per metadata group
   std::vector<std::uint8_t> codes;    // ceil(n*bits/8), LE in byte, first code in LSBs
   std::vector<std::uint16_t> scales;  // f16 bits, n / group_size
   std::vector<std::uint16_t> zeros;   // f16 bits, n / group_size
@@ -62,7 +92,6 @@ struct Matrix {  // row-major
   Vec data;
   Matrix() = default;
   Matrix(std::size_t r, std::size_t c) : rows(r), cols(c), data(r * c, 0.0f) {}
-  std::size_t size() const { return rows * cols; }
 };
 
 struct MoEConfig {
@@ -104,6 +133,7 @@ struct InterExpertPredictor {
   std::vector<Matrix> w;  // [target-1] -> experts x d_hidden
   std::vector<Vec> b;     // [target-1] -> experts
 };
+#endif
 
 // ------------------------------------------------------------ plumbing
 inline void check(int rc) {
@@ -124,29 +154,33 @@ class Workspace {
   floe_gpu_workspace *ws_ = nullptr;
 };
 
-// A compressed expert resident in HBM.  With with_ffn = false only the up
-// projection is uploaded (qgemv_channels / predict_mask on a bare tensor).
+// A compressed expert resident in HBM (the upload reads the host object's
+// buffers in place).  With with_ffn = false only the up projection is
+// uploaded (qgemv_channels / predict_mask on a bare tensor).
 class DeviceExpert {
  public:
-  DeviceExpert(const CompressedExpert &e, bool with_ffn = true) {
-    const std::uint64_t n = (std::uint64_t)e.d_hidden * e.d_intermediate;
-    if (with_ffn && (e.gate.size() != n || e.down_t.size() != n))
-      throw std::runtime_error("expert_forward_sparse: dimension mismatch");
+  template <class Q>
+  DeviceExpert(const Q &up_q, std::uint32_t d_hidden, std::uint32_t d_intermediate,
+               const float *gate, const float *down_t, float threshold) {
     floe_expert_host_view v{};
-    v.d_hidden = e.d_hidden;
-    v.d_intermediate = e.d_intermediate;
-    v.bits = e.up_q.bits;
-    v.group_size = e.up_q.group_size;
-    v.codes = e.up_q.codes.data();
-    v.scales = e.up_q.scales.data();
-    v.zeros = e.up_q.zeros.data();
-    v.gate_f32 = with_ffn ? e.gate.data() : nullptr;
-    v.down_f32 = with_ffn ? e.down_t.data() : nullptr;
-    v.threshold = e.threshold;
+    v.d_hidden = d_hidden;
+    v.d_intermediate = d_intermediate;
+    v.bits = up_q.bits;
+    v.group_size = up_q.group_size;
+    v.codes = up_q.codes.data();
+    v.scales = up_q.scales.data();
+    v.zeros = up_q.zeros.data();
+    v.gate_f32 = gate;
+    v.down_f32 = down_t;
+    v.threshold = threshold;
     check(floe_gpu_expert_create(&v, &h_));
-    dh_ = e.d_hidden;
-    di_ = e.d_intermediate;
+    dh_ = d_hidden;
+    di_ = d_intermediate;
   }
+  template <class Expert>
+  explicit DeviceExpert(const Expert &e, bool with_ffn = true)
+      : DeviceExpert(e.up_q, e.d_hidden, e.d_intermediate, with_ffn ? ffn_ptr(e, e.gate) : nullptr,
+                     with_ffn ? ffn_ptr(e, e.down_t) : nullptr, e.threshold) {}
   ~DeviceExpert() { floe_gpu_expert_destroy(h_); }
   DeviceExpert(const DeviceExpert &) = delete;
   DeviceExpert &operator=(const DeviceExpert &) = delete;
@@ -155,13 +189,20 @@ class DeviceExpert {
   std::uint32_t d_intermediate() const { return di_; }
 
  private:
+  template <class Expert>
+  static const float *ffn_ptr(const Expert &e, const Vec &v) {
+    if (v.size() != (std::size_t)e.d_hidden * e.d_intermediate)
+      throw std::runtime_error("expert_forward_sparse: dimension mismatch");
+    return v.data();
+  }
   floe_gpu_expert *h_ = nullptr;
   std::uint32_t dh_ = 0, di_ = 0;
 };
 
 class DeviceLayer {
  public:
-  DeviceLayer(const CompressedLayer &l, std::uint32_t top_k, bool mixing_f16 = false) {
+  template <class Layer>
+  DeviceLayer(const Layer &l, std::uint32_t top_k, bool mixing_f16 = false) {
     std::vector<floe_gpu_expert *> hs;
     for (const auto &e : l.experts) {
       experts_.push_back(std::make_unique<DeviceExpert>(e));
@@ -195,22 +236,50 @@ class DeviceLayer {
 
 namespace detail {
 
-// Fingerprint of a host object's buffers: the cache entry is rebuilt when the
-// object at an address was replaced.
-inline std::uint64_t fp(const void *p, std::size_t n) {
-  return (std::uint64_t)(std::uintptr_t)p * 1000003u ^ (std::uint64_t)n;
+// ---- content fingerprints (sizes + 64 sampled 8-byte words per buffer)
+inline std::uint64_t mix(std::uint64_t h, std::uint64_t v) {
+  v *= 0x9E3779B97F4A7C15ull;
+  return (h ^ (v ^ (v >> 29))) * 0xBF58476D1CE4E5B9ull;
 }
-inline std::uint64_t fp(const CompressedExpert &e) {
+inline std::uint64_t sample(std::uint64_t h, const void *p, std::size_t bytes) {
+  h = mix(h, bytes);
+  const auto *b = static_cast<const std::uint8_t *>(p);
+  if (!b) return h;
+  if (bytes < 8) {
+    for (std::size_t i = 0; i < bytes; ++i) h = mix(h, b[i]);
+    return h;
+  }
+  for (std::size_t i = 0; i < 64; ++i) {
+    std::uint64_t w;
+    std::memcpy(&w, b + (bytes - 8) * i / 63, 8);
+    h = mix(h, w);
+  }
+  return h;
+}
+template <class V>
+std::uint64_t sample_vec(std::uint64_t h, const V &v) {
+  return sample(h, v.data(), v.size() * sizeof(v[0]));
+}
+template <class Q>
+std::uint64_t fp_q(const Q &q) {
+  std::uint64_t h = mix(mix(mix(0, q.n), q.bits), q.group_size);
+  return sample_vec(sample_vec(sample_vec(h, q.codes), q.scales), q.zeros);
+}
+template <class Expert>
+std::uint64_t fp_expert(const Expert &e) {
   std::uint32_t tb;
   std::memcpy(&tb, &e.threshold, 4);
-  return fp(e.up_q.codes.data(), e.up_q.codes.size()) ^ fp(e.gate.data(), e.gate.size()) * 31 ^
-         tb;
+  std::uint64_t h = mix(mix(fp_q(e.up_q), e.d_hidden), e.d_intermediate);
+  return mix(sample_vec(sample_vec(h, e.gate), e.down_t), tb);
 }
 
+// ---- the upload cache: (address, fingerprint) -> device object, bounded LRU
+constexpr std::size_t kCacheEntries = 512;
 struct Cache {
   std::mutex mu;
-  std::map<std::pair<const void *, std::uint64_t>, std::shared_ptr<void>> objs;
-  std::map<std::tuple<std::uint32_t, std::uint32_t, std::uint32_t>, std::shared_ptr<Workspace>> ws;
+  using Key = std::pair<const void *, std::uint64_t>;
+  std::list<std::pair<Key, std::shared_ptr<void>>> lru;  // most recent first
+  std::map<Key, decltype(lru)::iterator> index;
 };
 inline Cache &cache() {
   static Cache c;
@@ -221,24 +290,35 @@ template <typename T, typename Make>
 std::shared_ptr<T> cached(const void *key, std::uint64_t f, Make make) {
   Cache &c = cache();
   std::lock_guard<std::mutex> g(c.mu);
-  auto it = c.objs.find({key, f});
-  if (it != c.objs.end()) return std::static_pointer_cast<T>(it->second);
+  const Cache::Key k{key, f};
+  auto it = c.index.find(k);
+  if (it != c.index.end()) {
+    c.lru.splice(c.lru.begin(), c.lru, it->second);
+    return std::static_pointer_cast<T>(it->second->second);
+  }
   std::shared_ptr<T> obj = make();
-  c.objs[{key, f}] = obj;
+  c.lru.emplace_front(k, obj);
+  c.index[k] = c.lru.begin();
+  while (c.lru.size() > kCacheEntries) {  // in-flight users keep their shared_ptr
+    c.index.erase(c.lru.back().first);
+    c.lru.pop_back();
+  }
   return obj;
 }
 
+// ---- one workspace per (host thread, shape)
 inline std::shared_ptr<Workspace> workspace(std::uint32_t dh, std::uint32_t di,
                                             std::uint32_t slots) {
-  Cache &c = cache();
-  std::lock_guard<std::mutex> g(c.mu);
-  auto &w = c.ws[{dh, di, slots}];
+  thread_local std::map<std::tuple<std::uint32_t, std::uint32_t, std::uint32_t>,
+                        std::shared_ptr<Workspace>>
+      ws;
+  auto &w = ws[{dh, di, slots}];
   if (!w) w = std::make_shared<Workspace>(dh, di, slots);
   return w;
 }
 
-// Shared device-side scratch vectors (the value-type calls copy through the
-// workspace's pinned staging; these hold extra outputs).
+// Device-side scratch vectors of one call (the value-type calls copy through
+// the workspace's pinned staging; these hold extra outputs).
 struct DevBuf {
   void *p = nullptr;
   explicit DevBuf(std::size_t bytes) {
@@ -249,11 +329,20 @@ struct DevBuf {
 
 }  // namespace detail
 
+// Drop every cached device copy (after editing host weights in place).
+inline void clear_cache() {
+  detail::Cache &c = detail::cache();
+  std::lock_guard<std::mutex> g(c.mu);
+  c.index.clear();
+  c.lru.clear();
+}
+
 // ------------------------------------------------------- reference API
 // y = expert_forward_sparse(e, h)  (model.cpp:128-142)
-inline Vec expert_forward_sparse(const CompressedExpert &e, const Vec &h) {
+template <class Expert>
+Vec expert_forward_sparse(const Expert &e, const Vec &h) {
   if (h.size() != e.d_hidden) throw std::runtime_error("expert_forward_sparse: dimension mismatch");
-  auto dev = detail::cached<DeviceExpert>(&e, detail::fp(e),
+  auto dev = detail::cached<DeviceExpert>(&e, detail::fp_expert(e),
                                           [&] { return std::make_shared<DeviceExpert>(e); });
   auto ws = detail::workspace(e.d_hidden, e.d_intermediate, 1);
   Vec y(e.d_hidden);
@@ -263,59 +352,60 @@ inline Vec expert_forward_sparse(const CompressedExpert &e, const Vec &h) {
 }
 
 // y[c] = sum_k dequant(q)[c*ch_len + k] * x[k]  (quant.cpp:122-136)
-inline void qgemv_channels(const QuantizedTensor &q, std::size_t ch_len, const float *x, float *y) {
+template <class Q>
+void qgemv_channels(const Q &q, std::size_t ch_len, const float *x, float *y) {
   if (ch_len == 0 || q.n % ch_len != 0)
-    throw std::runtime_error("qgemv_channels: ch_len must divide the element count");
-  CompressedExpert e;
-  e.d_hidden = (std::uint32_t)ch_len;
-  e.d_intermediate = (std::uint32_t)(q.n / ch_len);
-  e.up_q = q;
-  DeviceExpert dev(e, /*with_ffn=*/false);
-  auto ws = detail::workspace(e.d_hidden, e.d_intermediate, 1);
-  detail::DevBuf dx(4 * ch_len), dy(4ull * e.d_intermediate);
+    throw std::runtime_error("qgemv_channels: ch_len must divide element count");
+  const auto dh = (std::uint32_t)ch_len, di = (std::uint32_t)(q.n / ch_len);
+  auto dev = detail::cached<DeviceExpert>(&q, detail::fp_q(q) ^ 0x71u, [&] {
+    return std::make_shared<DeviceExpert>(q, dh, di, nullptr, nullptr, 0.0f);
+  });
+  auto ws = detail::workspace(dh, di, 1);
+  detail::DevBuf dx(4 * ch_len), dy(4ull * di);
   check(floe_gpu_copy(dx.p, x, 4 * ch_len, nullptr));
-  check(floe_gpu_qgemv_channels(dev.get(), ws->get(), static_cast<const float *>(dx.p),
+  check(floe_gpu_qgemv_channels(dev->get(), ws->get(), static_cast<const float *>(dx.p),
                                 static_cast<float *>(dy.p), nullptr));
-  check(floe_gpu_copy(y, dy.p, 4ull * e.d_intermediate, nullptr));
+  check(floe_gpu_copy(y, dy.p, 4ull * di, nullptr));
 }
 
 // mask[c] = |qgemv(up_next, x_prev)[c]| >= t  (predictor.cpp:179-189)
-inline std::vector<std::uint8_t> predict_mask(const QuantizedTensor &up_next,
-                                              std::uint32_t d_hidden, const Vec &x_prev,
-                                              float t) {
-  if (d_hidden == 0 || x_prev.size() != d_hidden || up_next.n % d_hidden != 0)
-    throw std::runtime_error("predict_mask: dimension mismatch");
-  CompressedExpert e;
-  e.d_hidden = d_hidden;
-  e.d_intermediate = (std::uint32_t)(up_next.n / d_hidden);
-  e.up_q = up_next;
-  auto dev = detail::cached<DeviceExpert>(&up_next, detail::fp(up_next.codes.data(),
-                                                               up_next.codes.size()),
-                                          [&] { return std::make_shared<DeviceExpert>(e, false); });
-  auto ws = detail::workspace(d_hidden, e.d_intermediate, 1);
-  detail::DevBuf dx(4ull * d_hidden), dm(e.d_intermediate);
+template <class Q>
+std::vector<std::uint8_t> predict_mask(const Q &up_next, std::uint32_t d_hidden, const Vec &x_prev,
+                                       float t) {
+  if (x_prev.size() != d_hidden) throw std::runtime_error("predict_mask: dimension mismatch");
+  if (d_hidden == 0 || up_next.n % d_hidden != 0)
+    throw std::runtime_error("predict_mask: tensor not channel-divisible");
+  const auto di = (std::uint32_t)(up_next.n / d_hidden);
+  auto dev = detail::cached<DeviceExpert>(&up_next, detail::fp_q(up_next) ^ 0x71u, [&] {
+    return std::make_shared<DeviceExpert>(up_next, d_hidden, di, nullptr, nullptr, 0.0f);
+  });
+  auto ws = detail::workspace(d_hidden, di, 1);
+  detail::DevBuf dx(4ull * d_hidden), dm(di);
   check(floe_gpu_copy(dx.p, x_prev.data(), 4ull * d_hidden, nullptr));
   check(floe_gpu_predict_mask(dev->get(), ws->get(), static_cast<const float *>(dx.p), t,
                               static_cast<std::uint8_t *>(dm.p), nullptr, nullptr, nullptr));
-  std::vector<std::uint8_t> m(e.d_intermediate);
+  std::vector<std::uint8_t> m(di);
   check(floe_gpu_copy(m.data(), dm.p, m.size(), nullptr));
   return m;
 }
 
 namespace detail {
-inline std::shared_ptr<DeviceLayer> layer_of(const CompressedModel &m, std::uint32_t layer) {
-  if (layer >= m.layers.size()) throw std::runtime_error("layer_forward: layer out of range");
-  const CompressedLayer &l = m.layers[layer];
-  const std::uint64_t f =
-      fp(l.mixing.data.data(), l.mixing.size()) ^ (l.experts.empty() ? 0 : fp(l.experts[0]));
+template <class Model>
+std::shared_ptr<DeviceLayer> layer_of(const Model &m, std::uint32_t layer) {
+  if (layer >= m.cfg.layers || layer >= m.layers.size())
+    throw std::runtime_error("layer_forward: bad layer");
+  const auto &l = m.layers[layer];
+  std::uint64_t f = sample_vec(sample_vec(mix(0, m.cfg.top_k), l.router.data), l.mixing.data);
+  for (const auto &e : l.experts) f = mix(f, fp_expert(e));
   return cached<DeviceLayer>(&l, f, [&] { return std::make_shared<DeviceLayer>(l, m.cfg.top_k); });
 }
 }  // namespace detail
 
-// layer_forward(CompressedModel) (model.cpp:171-190)
-inline Vec layer_forward(const CompressedModel &m, std::uint32_t layer, const Vec &h) {
-  if (h.size() != m.cfg.d_hidden) throw std::runtime_error("layer_forward: dimension mismatch");
+// layer_forward(CompressedModel) (model.cpp:182-190)
+template <class Model>
+Vec layer_forward(const Model &m, std::uint32_t layer, const Vec &h) {
   auto L = detail::layer_of(m, layer);
+  if (h.size() != L->d_hidden()) throw std::runtime_error("gemv: dimension mismatch");
   auto ws = detail::workspace(L->d_hidden(), L->d_intermediate(), L->top_k());
   Vec y(h.size());
   check(floe_gpu_layer_forward_host(L->get(), ws->get(), h.data(), y.data(), nullptr));
@@ -323,11 +413,11 @@ inline Vec layer_forward(const CompressedModel &m, std::uint32_t layer, const Ve
 }
 
 // layer_forward_traced (model.cpp:192-208)
-inline LayerTrace layer_forward_traced(const CompressedModel &m, std::uint32_t layer,
-                                       const Vec &h) {
-  if (h.size() != m.cfg.d_hidden) throw std::runtime_error("layer_forward: dimension mismatch");
+template <class Model>
+LayerTrace layer_forward_traced(const Model &m, std::uint32_t layer, const Vec &h) {
   auto L = detail::layer_of(m, layer);
   const std::uint32_t dh = L->d_hidden(), di = L->d_intermediate(), k = L->top_k();
+  if (h.size() != dh) throw std::runtime_error("gemv: dimension mismatch");
   auto ws = detail::workspace(dh, di, k);
   detail::DevBuf dh_in(4ull * dh), dy(4ull * dh), du(4ull * dh), de(4ull * k), dw(4ull * k),
       dm((std::size_t)k * di);
@@ -353,23 +443,28 @@ inline LayerTrace layer_forward_traced(const CompressedModel &m, std::uint32_t l
 }
 
 // predict_experts (predictor.cpp:164-177)
-inline std::vector<std::uint32_t> predict_experts(const InterExpertPredictor &p, const Vec &x,
-                                                  std::uint32_t layer,
-                                                  std::uint32_t prefetch_count) {
+template <class Predictor>
+std::vector<std::uint32_t> predict_experts(const Predictor &p, const Vec &x, std::uint32_t layer,
+                                           std::uint32_t prefetch_count) {
   if (layer == 0) throw std::runtime_error("predict_experts: layer 0 has no lookahead predictor");
+  if (layer >= p.layers) throw std::runtime_error("predict_experts: bad layer");
   if (x.size() != p.d_hidden) throw std::runtime_error("predict_experts: dimension mismatch");
-  auto dev = detail::cached<floe_gpu_predictor>(
-      &p, detail::fp(p.w.empty() ? nullptr : p.w[0].data.data(), p.w.size()), [&] {
-        std::vector<float> w, b;
-        for (const auto &m : p.w) w.insert(w.end(), m.data.begin(), m.data.end());
-        for (const auto &v : p.b) b.insert(b.end(), v.begin(), v.end());
-        floe_gpu_predictor *h = nullptr;
-        check(floe_gpu_predictor_create(p.layers, p.experts, p.d_hidden, w.data(), b.data(), &h));
-        return std::shared_ptr<floe_gpu_predictor>(h, [](floe_gpu_predictor *q) {
-          floe_gpu_predictor_destroy(q);
-        });
-      });
-  detail::DevBuf dx(4ull * x.size()), dout(4ull * (prefetch_count ? prefetch_count : 1));
+  if (prefetch_count == 0 || prefetch_count > p.experts)
+    throw std::runtime_error("top_k: k out of range");
+  std::uint64_t f = detail::mix(detail::mix(detail::mix(0, p.layers), p.experts), p.d_hidden);
+  for (const auto &m : p.w) f = detail::sample_vec(f, m.data);
+  for (const auto &v : p.b) f = detail::sample_vec(f, v);
+  auto dev = detail::cached<floe_gpu_predictor>(&p, f, [&] {
+    std::vector<float> w, b;
+    for (const auto &m : p.w) w.insert(w.end(), m.data.begin(), m.data.end());
+    for (const auto &v : p.b) b.insert(b.end(), v.begin(), v.end());
+    floe_gpu_predictor *h = nullptr;
+    check(floe_gpu_predictor_create(p.layers, p.experts, p.d_hidden, w.data(), b.data(), &h));
+    return std::shared_ptr<floe_gpu_predictor>(h, [](floe_gpu_predictor *q) {
+      floe_gpu_predictor_destroy(q);
+    });
+  });
+  detail::DevBuf dx(4ull * x.size()), dout(4ull * prefetch_count);
   check(floe_gpu_copy(dx.p, x.data(), 4ull * x.size(), nullptr));
   check(floe_gpu_predict_experts(dev.get(), static_cast<const float *>(dx.p), layer,
                                  prefetch_count, static_cast<std::uint32_t *>(dout.p), nullptr));
@@ -431,9 +526,9 @@ inline CompressedModel load_compressed(const std::string &path) {
   m.layers.resize(m.cfg.layers);
   for (auto &layer : m.layers) {
     layer.router = Matrix(m.cfg.experts, dh);
-    rd(layer.router.data.data(), 4 * layer.router.size());
+    rd(layer.router.data.data(), 4 * layer.router.data.size());
     layer.mixing = Matrix(dh, dh);
-    rd(layer.mixing.data.data(), 4 * layer.mixing.size());
+    rd(layer.mixing.data.data(), 4 * layer.mixing.data.size());
     layer.experts.resize(m.cfg.experts);
     for (auto &e : layer.experts) {
       e.d_hidden = m.cfg.d_hidden;

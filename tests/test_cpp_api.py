@@ -19,6 +19,30 @@ ROOT = Path(__file__).resolve().parents[1]
 LIBDIR = ROOT / "paper_2505_05950_b200"
 
 
+def _ref_view(ref, eh, dh, di):
+    n = dh * di
+    c, sc, z = ct.POINTER(ct.c_uint8)(), ct.POINTER(ct.c_uint16)(), ct.POINTER(ct.c_uint16)()
+    g, d, t = ct.POINTER(ct.c_float)(), ct.POINTER(ct.c_float)(), ct.c_float()
+    ref.ref_expert_view(eh, ct.byref(c), ct.byref(sc), ct.byref(z), ct.byref(g), ct.byref(d),
+                        ct.byref(t))
+    codes = np.ctypeslib.as_array(c, shape=(n // 4,)).copy()
+    scales = np.ctypeslib.as_array(sc, shape=(n // 64,)).copy()
+    zeros = np.ctypeslib.as_array(z, shape=(n // 64,)).copy()
+    return codes, scales, zeros, t.value
+
+
+def _ref_qgemv(ref, eh, dh, di, x):
+    codes, scales, zeros, _ = _ref_view(ref, eh, dh, di)
+    v = np.empty(di, np.float32)
+    assert ref.ref_qgemv_channels(codes, scales, zeros, dh * di, 2, 64, dh,
+                                  np.ascontiguousarray(x, np.float32), v) == 0
+    return v
+
+
+def _ref_threshold(ref, eh, dh, di):
+    return _ref_view(ref, eh, dh, di)[3]
+
+
 def build(tmp: Path) -> Path:
     exe = tmp / "test_api"
     subprocess.run(["g++", "-std=c++17", "-O2", "-Wall", "-Wextra", f"-I{ROOT / 'include'}",
@@ -72,7 +96,13 @@ def test_cpp_api_matches_reference(tmp_path, ref, dh, di):
             assert np.array_equal(got_sel[i], sel)
             assert np.allclose(got_w[i], w, rtol=1e-5, atol=1e-6)
             # masks: identical except ties (|v| within 1e-3 of the threshold)
-            assert np.mean(got_m[i] != masks) < 0.002
+            for j in range(K):
+                diff = np.nonzero(got_m[i][j] != masks[j])[0]
+                if len(diff):
+                    eh = ref.ref_cmodel_expert(cm, layer, int(sel[j]))
+                    v = _ref_qgemv(ref, eh, dh, di, u)
+                    thr = _ref_threshold(ref, eh, dh, di)
+                    assert np.all(np.abs(np.abs(v[diff]) - thr) <= 1e-3)
             assert O.rel_l2(got_y[i], y) <= 1e-2
             h = got_y[i].copy()  # chain on our output, like cmd_run
             i += 1
@@ -82,6 +112,16 @@ def test_cpp_api_matches_reference(tmp_path, ref, dh, di):
     y = np.empty(dh, np.float32)
     assert ref.ref_expert_forward(ex, x, y) == 0
     assert O.rel_l2(np.fromfile(out / "expert_y.f32", np.float32), y) <= 1e-2
+    # qgemv_channels on layer 0 expert 0, predict_mask on layer 1 expert 0
+    v = _ref_qgemv(ref, ex, dh, di, x)
+    assert np.all(np.abs(np.fromfile(out / "qgemv_v.f32", np.float32) - v) <=
+                  2e-5 + 2e-5 * np.abs(v))
+    ex1 = ref.ref_cmodel_expert(cm, 1, 0)
+    v1 = _ref_qgemv(ref, ex1, dh, di, x)
+    t1 = _ref_threshold(ref, ex1, dh, di)
+    m1 = np.fromfile(out / "predict_mask.u8", np.uint8)
+    diff = np.nonzero(m1 != (np.abs(v1) >= t1))[0]
+    assert np.all(np.abs(np.abs(v1[diff]) - t1) <= 1e-3)
     # predict_experts with the layer-0 router as the map (bias 0)
     rp = ct.POINTER(ct.c_float)()
     mp = ct.POINTER(ct.c_float)()
@@ -90,3 +130,30 @@ def test_cpp_api_matches_reference(tmp_path, ref, dh, di):
     want = O.predict_experts(router, np.zeros(E, np.float32), x, K)
     assert np.array_equal(np.fromfile(out / "predict_experts.u32", np.uint32), want)
     ref.ref_cmodel_destroy(cm)
+
+
+INTEG = ROOT / "tests" / "cpp" / "build" / "test_integration"
+
+
+def test_integration_binary_built():
+    """INTEGRATION.md's binding compiled with the reference's own headers and
+    sources (tests/cpp/Makefile; built by `make` / build() where the reference
+    exists, shipped prebuilt otherwise)."""
+    if not INTEG.exists():
+        if Path("/root/reference/proj/core/src").exists():
+            subprocess.run(["make", "-C", str(ROOT / "tests" / "cpp")], check=True,
+                           capture_output=True)
+        else:
+            pytest.skip("reference sources absent and no prebuilt test_integration")
+    assert INTEG.exists()
+
+
+@pytest.mark.gpu
+def test_integration_reference_types_two_threads():
+    """floe::gpu:: on the reference's own CompressedModel objects, 1 and 2 host
+    threads: equal outputs, reference parity, the reference's error messages."""
+    if not INTEG.exists():
+        pytest.skip("tests/cpp/build/test_integration not built")
+    r = subprocess.run([str(INTEG)], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:] + r.stdout[-1000:]
+    assert "0 failures" in r.stdout
