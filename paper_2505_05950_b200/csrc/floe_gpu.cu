@@ -22,6 +22,7 @@
 #include "floe_v2.cuh"
 #include "floe_tc.cuh"
 #include "floe_calib.cuh"
+#include "floe_blayer.cuh"
 
 #include <cub/device/device_segmented_radix_sort.cuh>
 
@@ -1732,6 +1733,82 @@ int floe_gpu_offload_stats(floe_gpu_offload *o, floe_offload_stats *out, floe_st
     if (o->state[i] == floe_gpu_offload::kResident) dev += o->rec_bytes;
   out->device_record_bytes = dev;
   return FLOE_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------- batched MoE layer ---
+extern "C" {
+
+int floe_gpu_layer_forward_batched(const floe_gpu_layer *l, const float *h, uint32_t n_tokens,
+                                   float *y, floe_stream_t stream) {
+  if (!l || !h || !y) return fail(FLOE_ERR_INVALID, "layer_forward: null argument");
+  if (n_tokens == 0) return FLOE_OK;
+  if (!l->fast)
+    return fail(FLOE_ERR_UNSUPPORTED, "layer_forward_batched: needs the tile layout");
+  if (int rc = require_device("layer_forward_batched")) return rc;
+  cudaStream_t st = S(stream);
+  const uint32_t T = n_tokens, E = l->E, K = l->top_k, dh = l->dh, P = T * K;
+  // scratch: u [T][dh] | logits [T][E] | sel [P] | w [P] | counts [E] | lists [E][T] |
+  //          X [64][dh] (one expert chunk's rows) | Y [64][dh] | out [P][dh]
+  const size_t CH = floe_tc::kMaxTokens;
+  const size_t o_u = 0, o_lg = o_u + 4ull * T * dh, o_sel = o_lg + 4ull * T * E;
+  const size_t o_w = o_sel + 4ull * P, o_cnt = o_w + 4ull * P, o_lst = o_cnt + 4ull * 32;
+  const size_t o_x = (o_lst + 4ull * E * T + 255) & ~size_t(255);
+  const size_t o_y = o_x + 4ull * CH * dh, o_out = o_y + 4ull * CH * dh;
+  const size_t total = o_out + 4ull * P * dh;
+  uint8_t *sc = nullptr;
+  CK(cudaMallocAsync(reinterpret_cast<void **>(&sc), total, st));
+  float *u = reinterpret_cast<float *>(sc + o_u), *lg = reinterpret_cast<float *>(sc + o_lg);
+  uint32_t *sel = reinterpret_cast<uint32_t *>(sc + o_sel);
+  float *w = reinterpret_cast<float *>(sc + o_w);
+  uint32_t *cnt = reinterpret_cast<uint32_t *>(sc + o_cnt), *lst = reinterpret_cast<uint32_t *>(sc + o_lst);
+  float *X = reinterpret_cast<float *>(sc + o_x), *Y = reinterpret_cast<float *>(sc + o_y);
+  float *outp = reinterpret_cast<float *>(sc + o_out);
+  auto done = [&](int rc) {
+    cudaFreeAsync(sc, st);
+    return rc;
+  };
+  // u = h + mixing h (model.cpp:150-152), kMixTok tokens per pass
+  const uint32_t mix_smem = 4u * floe_bl::kMixTok * 256u;
+  for (uint32_t t0 = 0; t0 < T; t0 += floe_bl::kMixTok) {
+    const uint32_t nt = std::min<uint32_t>(floe_bl::kMixTok, T - t0);
+    if (l->mix_f16) {
+      if (int rc = set_smem(floe_bl::mix_batched<__half>, mix_smem)) return done(rc);
+      floe_bl::mix_batched<__half><<<(dh + 7) / 8, 256, 4u * nt * 256u, st>>>(
+          static_cast<const __half *>(l->mixing), dh, h + (size_t)t0 * dh, nt, u + (size_t)t0 * dh);
+    } else {
+      if (int rc = set_smem(floe_bl::mix_batched<float>, mix_smem)) return done(rc);
+      floe_bl::mix_batched<float><<<(dh + 7) / 8, 256, 4u * nt * 256u, st>>>(
+          static_cast<const float *>(l->mixing), dh, h + (size_t)t0 * dh, nt, u + (size_t)t0 * dh);
+    }
+  }
+  // route (model.cpp:83-93) and group the (token, slot) pairs by expert
+  if (cudaMemsetAsync(cnt, 0, 4ull * E, st) != cudaSuccess)
+    return done(fail(FLOE_ERR_CUDA, "layer_forward_batched: memset failed"));
+  floe_bl::router_logits<<<(T * E * 32 + 255) / 256, 256, 0, st>>>(l->router, E, dh, u, T, lg);
+  floe_bl::route_batched<<<(T * 32 + 255) / 256, 256, 0, st>>>(lg, T, E, K, sel, w, cnt, lst);
+  if (cudaGetLastError() != cudaSuccess)
+    return done(fail(FLOE_ERR_CUDA, "layer_forward_batched: launch failed"));
+  uint32_t hc[32];
+  if (cudaMemcpyAsync(hc, cnt, 4ull * E, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return done(fail(FLOE_ERR_CUDA, "layer_forward_batched: routing readback failed"));
+  // every expert over its tokens (chunks of at most 64, the batched forward's cap)
+  for (uint32_t e = 0; e < E; ++e) {
+    for (uint32_t c0 = 0; c0 < hc[e]; c0 += (uint32_t)CH) {
+      const uint32_t n = std::min<uint32_t>((uint32_t)CH, hc[e] - c0);
+      const uint32_t *pairs = lst + (size_t)e * T + c0;
+      floe_bl::gather_rows<<<dim3(4, n), 256, 0, st>>>(u, pairs, n, K, dh, X);
+      if (int rc = floe_gpu_expert_forward_batched(l->experts[e], X, n, Y, nullptr, stream))
+        return done(rc);
+      floe_bl::scatter_rows<<<dim3(4, n), 256, 0, st>>>(Y, pairs, n, dh, outp);
+    }
+  }
+  floe_bl::combine<<<dim3(4, T), 256, 0, st>>>(u, outp, w, K, dh, y);
+  if (cudaGetLastError() != cudaSuccess)
+    return done(fail(FLOE_ERR_CUDA, "layer_forward_batched: launch failed"));
+  return done(FLOE_OK);
 }
 
 }  // extern "C"
