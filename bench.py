@@ -614,6 +614,100 @@ def run_reference(args, rank, world):
             "setup_s": round(setup_s, 2)}
 
 
+# ------------------------------------------------------------------ config 5 (--ep)
+EP_TOKENS = 4096
+
+
+def run_ep(args, rank, world, local):
+    """Config 5: one expert-parallel MoE layer prefill of EP_TOKENS tokens, the 8
+    experts sharded over the ranks (rank r owns experts [r E/W, (r+1) E/W)), each
+    rank routing its EP_TOKENS/W tokens and exchanging them with all-to-alls
+    (paper_2505_05950_b200/ep.py; NCCL over NVLink).  Strong scaling: the total
+    is fixed.  --ep-cpu runs the same plumbing on CPU with gloo and a toy shape
+    (tests/test_bench_multirank.py)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_05950_b200 import ep
+    cpu = args.ep_cpu
+    if world > 1:
+        if cpu:
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    per = E // world
+    first = rank * per
+    if cpu:
+        from oracle import oracle as O
+        dh, di, T = 64, 32, 64
+        rng = np.random.default_rng(5)
+        ex = []
+        for e in range(E):
+            gate, up, down = O.seeded_expert(dh, di, 60 + e)
+            ex.append(O.Expert(dh, di, O.quantize(up, 4, 16), gate, down, 0.3))
+        router = torch.from_numpy((rng.standard_normal((E, dh)) / 8).astype(np.float32))
+        mixing = torch.from_numpy((rng.standard_normal((dh, dh)) / 8).astype(np.float32))
+        H = torch.from_numpy(np.stack([O.token_input(1, t, dh) for t in range(T)]))
+
+        def expert_fn(e, X):
+            Xn = X.numpy()
+            return torch.from_numpy(np.stack([O.expert_forward_sparse(ex[e], x) for x in Xn])
+                                    if len(Xn) else np.zeros((0, dh), np.float32))
+        sync = lambda: None  # noqa: E731
+        clock = time.perf_counter
+    else:
+        import paper_2505_05950_b200 as fb
+        dh, T = DH, EP_TOKENS
+        router, mixing, gate, up, down = gen_float_layer(fb, 0)
+        th = calibrate_layer(fb, torch, router, mixing, gate, up, down)
+        ex = []
+        for e in range(first, first + per):
+            codes, scales, zeros = fb.quantize(up[e].reshape(-1), BITS, G)
+            ex.append(fb.GpuExpert(DH, DI, BITS, G, codes, scales, zeros, gate=gate[e],
+                                   down=down[e], threshold=th[e]))
+        del gate, up, down
+        H = torch.stack([fb.gen_normals(1, (1 << 40) + 9000 + t, DH) for t in range(T)])
+        expert_fn = ep.batched_expert_fn(ex, first_expert=first)
+        sync = torch.cuda.synchronize
+        clock = time.perf_counter
+    lo, hi = T * rank // world, T * (rank + 1) // world
+
+    def step():
+        y, _, _ = ep.ep_moe_layer(H[lo:hi], router, mixing, TOPK, expert_fn, E)
+        return y
+
+    for _ in range(args.warmup):
+        step()
+    sync()
+    barrier(world)
+    t0 = clock()
+    for _ in range(args.steps):
+        step()
+    sync()
+    my_ms = (clock() - t0) * 1e3
+    barrier(world)
+    max_ms = my_ms
+    if world > 1:
+        t = torch.tensor([my_ms], dtype=torch.float64,
+                         device="cpu" if cpu else torch.device("cuda", local))
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        max_ms = float(t.item())
+        dist.destroy_process_group()
+    value = T * args.steps / (max_ms / 1000.0)
+    return {"metric": "expert-parallel MoE layer prefill tokens/s (Mixtral-8x7B shape)",
+            "value": round(value, 1), "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 accumulate (INT2 up codes, f16 gate/down records)",
+            "data": "synthetic: gen_model layer 0 (seed 7), tokens token_input(1, 9000 + t)",
+            "config": {"workload": (f"config5: one MoE layer prefill, {T} tokens, {E} experts "
+                                    f"sharded over {world} rank(s), all-to-all dispatch/combine"),
+                       "tokens": T, "d_hidden": dh, "experts": E, "top_k": TOPK,
+                       "experts_per_rank": per,
+                       "parallelism": f"ep{world}", "device": "cpu (gloo test)" if cpu else "cuda"}}
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
@@ -623,9 +717,16 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-offload", action="store_true")
+    ap.add_argument("--ep", action="store_true", help="config 5: expert-parallel layer prefill")
+    ap.add_argument("--ep-cpu", action="store_true", help=argparse.SUPPRESS)  # gloo test mode
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank, world, local = dist_env()
+    if args.ep or args.ep_cpu:
+        out = run_ep(args, rank, world, local)
+        if rank == 0:
+            print(json.dumps(out), flush=True)
+        return
     if args.impl == "reference":
         if rank != 0:
             return

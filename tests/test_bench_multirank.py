@@ -69,3 +69,22 @@ def test_replica_value_is_whole_job_throughput():
     assert bench.whole_job_value(1, 20, 1000.0) == 20.0
     assert bench.whole_job_value(4, 20, 2000.0) == 40.0  # 4 ranks x 20 tokens in 2 s
     assert bench.max_over_ranks(3.5, 1) == 3.5
+
+
+def test_ep_mode_under_torchrun_gloo():
+    """bench.py --ep (config 5) under torchrun at world size 2: experts sharded,
+    all-to-all dispatch/combine, max-over-ranks timing; gloo + a toy shape on
+    CPU (--ep-cpu), the same plumbing NCCL runs on GPUs."""
+    import json
+    port = _free_port()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                        "--master-port", str(port), str(ROOT / "bench.py"), "--gpus", "2",
+                        "--ep-cpu", "--steps", "2", "--warmup", "1"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["experts_per_rank"] == 4 and d["value"] > 0
+    assert d["scaling"] == "strong"
