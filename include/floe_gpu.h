@@ -247,12 +247,17 @@ int floe_gpu_layer_forward(const floe_gpu_layer *l, floe_gpu_workspace *ws,
 /* block_forward (model.cpp:145-169) for n_tokens tokens at once (SURVEY
  * configs 4 and 5): h_dev [n][dh] -> y_dev [n][dh].  The mixing matrix is
  * streamed once for up to 64 tokens, the tokens are routed and grouped by
- * expert on the device, and every routed expert runs once over its tokens
- * (floe_gpu_expert_forward_batched: one tcgen05 pass over its codes, the
- * union of the kept channels' records read once).  Synchronises `stream`
- * once (the per-expert token counts decide the launches). */
-int floe_gpu_layer_forward_batched(const floe_gpu_layer *l, const float *h_dev,
-                                   uint32_t n_tokens, float *y_dev, floe_stream_t stream);
+ * expert on the device, and every routed expert runs over its tokens: a few
+ * tokens one by one through the fused single-expert kernel, more through
+ * floe_gpu_expert_forward_batched (one tcgen05 pass over its codes, the union
+ * of the kept channels' records read once).  With a workspace (`ws`
+ * nullable: then always the batched path), batches of up to 40 tokens run
+ * token by token through the fused layer kernel, which is faster there.
+ * Synchronises `stream` once (the per-expert token counts decide the
+ * launches). */
+int floe_gpu_layer_forward_batched(const floe_gpu_layer *l, floe_gpu_workspace *ws,
+                                   const float *h_dev, uint32_t n_tokens, float *y_dev,
+                                   floe_stream_t stream);
 
 /* Host-buffer layer call (the reference's value-type layer_forward): h in,
  * y out, through pinned staging; synchronises `stream`. */

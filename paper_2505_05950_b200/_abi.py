@@ -113,7 +113,7 @@ _SIGS = {
     "floe_gpu_predictor_create": (ct.c_int, [_U32, _U32, _U32, _P, _P, ct.POINTER(_P)]),
     "floe_gpu_predictor_destroy": (ct.c_int, [_P]),
     "floe_gpu_predict_experts": (ct.c_int, [_P, _P, _U32, _U32, _P, _P]),
-    "floe_gpu_layer_forward_batched": (ct.c_int, [_P, _P, _U32, _P, _P]),
+    "floe_gpu_layer_forward_batched": (ct.c_int, [_P, _P, _P, _U32, _P, _P]),
     "floe_gpu_model_create": (ct.c_int, [_P, _U32, ct.POINTER(_P)]),
     "floe_gpu_model_destroy": (ct.c_int, [_P]),
     "floe_gpu_model_decode": (ct.c_int, [_P, _P, _P, _P, ct.c_int, _P]),
@@ -501,15 +501,17 @@ def predict_experts(p: GpuPredictor, x, layer: int, count: int, stream=None):
     return out[:count]
 
 
-def layer_forward_batched(layer: GpuLayer, h, out=None, stream=None):
-    """block_forward (model.cpp:145-169) for a batch: h [n, dh] -> y [n, dh]."""
+def layer_forward_batched(layer: GpuLayer, h, ws: Workspace = None, out=None, stream=None):
+    """block_forward (model.cpp:145-169) for a batch: h [n, dh] -> y [n, dh]; with a
+    workspace, experts routed few tokens use the fused single-expert kernel."""
     torch = _torch()
     if h.dim() != 2 or h.shape[1] != layer.d_hidden or h.dtype != torch.float32 or not h.is_cuda:
         raise FloeError("layer_forward: dimension mismatch")
     h = h.contiguous()
     y = torch.empty_like(h) if out is None else out
-    _check(lib().floe_gpu_layer_forward_batched(layer.handle, h.data_ptr(), h.shape[0],
-                                                y.data_ptr(), _stream(stream)))
+    _check(lib().floe_gpu_layer_forward_batched(layer.handle, ws.handle if ws else None,
+                                                h.data_ptr(), h.shape[0], y.data_ptr(),
+                                                _stream(stream)))
     return y
 
 

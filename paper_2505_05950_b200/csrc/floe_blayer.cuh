@@ -40,10 +40,27 @@ __global__ void __launch_bounds__(256) mix_batched(const MT *__restrict__ M, uin
     __syncthreads();
     if (r >= dh) continue;
     float w[8];
+    const uint32_t kk = k0 + 8 * lane;
+    if (kk + 8 <= dh) {  // one 16-B (f16) or two 16-B (f32) loads per lane
+      if constexpr (sizeof(MT) == 2) {
+        const uint4 q = *reinterpret_cast<const uint4 *>(M + (size_t)r * dh + kk);
+        const __half2 *p2 = reinterpret_cast<const __half2 *>(&q);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t k = k0 + 8 * lane + i;
-      w[i] = k < dh ? static_cast<float>(M[(size_t)r * dh + k]) : 0.0f;
+        for (int i = 0; i < 4; ++i) {
+          const float2 f = __half22float2(p2[i]);
+          w[2 * i] = f.x;
+          w[2 * i + 1] = f.y;
+        }
+      } else {
+        const float4 a = *reinterpret_cast<const float4 *>(M + (size_t)r * dh + kk);
+        const float4 b = *reinterpret_cast<const float4 *>(M + (size_t)r * dh + kk + 4);
+        w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+        w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        w[i] = kk + i < dh ? static_cast<float>(M[(size_t)r * dh + kk + i]) : 0.0f;
     }
 #pragma unroll
     for (uint32_t t = 0; t < kMixTok; ++t) {

@@ -1738,17 +1738,41 @@ int floe_gpu_offload_stats(floe_gpu_offload *o, floe_offload_stats *out, floe_st
 }  // extern "C"
 
 // ------------------------------------------------------- batched MoE layer ---
+// Experts routed at most this many tokens of a batch run them through the fused
+// single-expert kernel (FLOE_BATCHED_SMALL overrides; measured crossover).
+static const uint32_t kBatchedSmall = [] {
+  const char *p = std::getenv("FLOE_BATCHED_SMALL");
+  return p ? (uint32_t)std::atoi(p) : 12u;
+}();
+// Batches of at most this many tokens run token by token through the fused
+// layer kernel (FLOE_LAYER_PER_TOKEN overrides).
+static const uint32_t kLayerPerToken = [] {
+  const char *p = std::getenv("FLOE_LAYER_PER_TOKEN");
+  return p ? (uint32_t)std::atoi(p) : 40u;
+}();
 extern "C" {
 
-int floe_gpu_layer_forward_batched(const floe_gpu_layer *l, const float *h, uint32_t n_tokens,
-                                   float *y, floe_stream_t stream) {
+int floe_gpu_layer_forward_batched(const floe_gpu_layer *l, floe_gpu_workspace *ws,
+                                   const float *h, uint32_t n_tokens, float *y,
+                                   floe_stream_t stream) {
   if (!l || !h || !y) return fail(FLOE_ERR_INVALID, "layer_forward: null argument");
+  if (ws)
+    if (int rc = check_ws("layer_forward_batched", ws, l->dh, l->di, 1)) return rc;
   if (n_tokens == 0) return FLOE_OK;
   if (!l->fast)
     return fail(FLOE_ERR_UNSUPPORTED, "layer_forward_batched: needs the tile layout");
   if (int rc = require_device("layer_forward_batched")) return rc;
   cudaStream_t st = S(stream);
   const uint32_t T = n_tokens, E = l->E, K = l->top_k, dh = l->dh, P = T * K;
+  // Small batches: the fused single-token layer kernel per token is faster
+  // (one launch per token, mixing + both experts; tools/bench_blayer.py)
+  if (ws && T <= kLayerPerToken && ws->slots >= K) {
+    for (uint32_t t = 0; t < T; ++t)
+      if (int rc = floe_gpu_layer_forward(l, ws, h + (size_t)t * dh, y + (size_t)t * dh, nullptr,
+                                          stream))
+        return rc;
+    return FLOE_OK;
+  }
   // scratch: u [T][dh] | logits [T][E] | sel [P] | w [P] | counts [E] | lists [E][T] |
   //          X [64][dh] (one expert chunk's rows) | Y [64][dh] | out [P][dh]
   const size_t CH = floe_tc::kMaxTokens;
@@ -1794,14 +1818,24 @@ int floe_gpu_layer_forward_batched(const floe_gpu_layer *l, const float *h, uint
   if (cudaMemcpyAsync(hc, cnt, 4ull * E, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
       cudaStreamSynchronize(st) != cudaSuccess)
     return done(fail(FLOE_ERR_CUDA, "layer_forward_batched: routing readback failed"));
-  // every expert over its tokens (chunks of at most 64, the batched forward's cap)
+  // every expert over its tokens: a few tokens go one by one through the fused
+  // single-expert kernel (one pass over the expert per token, ~15 us), more
+  // through the batched forward (one tcgen05 pass over the codes, the union
+  // of kept records once; chunks of at most 64 tokens)
   for (uint32_t e = 0; e < E; ++e) {
     for (uint32_t c0 = 0; c0 < hc[e]; c0 += (uint32_t)CH) {
       const uint32_t n = std::min<uint32_t>((uint32_t)CH, hc[e] - c0);
       const uint32_t *pairs = lst + (size_t)e * T + c0;
       floe_bl::gather_rows<<<dim3(4, n), 256, 0, st>>>(u, pairs, n, K, dh, X);
-      if (int rc = floe_gpu_expert_forward_batched(l->experts[e], X, n, Y, nullptr, stream))
+      if (ws && n <= kBatchedSmall) {
+        for (uint32_t i = 0; i < n; ++i)
+          if (int rc = floe_gpu_expert_forward_sparse(l->experts[e], ws, X + (size_t)i * dh,
+                                                      Y + (size_t)i * dh, nullptr, nullptr,
+                                                      nullptr, nullptr, stream))
+            return done(rc);
+      } else if (int rc = floe_gpu_expert_forward_batched(l->experts[e], X, n, Y, nullptr, stream)) {
         return done(rc);
+      }
       floe_bl::scatter_rows<<<dim3(4, n), 256, 0, st>>>(Y, pairs, n, dh, outp);
     }
   }
