@@ -151,6 +151,7 @@ struct floe_gpu_workspace {
   unsigned long long *y_flag = nullptr;  // fused kernel, expert mode: y-zeroed flag + CTA count
   uint32_t *kcount = nullptr;            // fused kernel: per-call kept counts per slot
   unsigned long long *pcnt = nullptr;    // fused kernel: published predicted partials
+  unsigned long long *pf_tick = nullptr; // fused kernel: next-mixing prefetch tickets
   float *pred_partial = nullptr;         // fused kernel: [32][kMaxGrid] predicted partials
   unsigned long long *phase_ns = nullptr;  // diagnostics: [grid][8] phase marks
   uint32_t *sel = nullptr;
@@ -327,6 +328,8 @@ struct FusedLaunch {
   uint8_t *mask_out;
   uint32_t *n_kept_out, *kept_out;
   unsigned long long *place_acc;  // nullable: offload engine's HBM / PCIe record counts
+  const void *next_mixing = nullptr;  // nullable: the next layer's mixing (L2 prefetch)
+  uint64_t next_mixing_bytes = 0;
 };
 
 template <int DH>
@@ -387,6 +390,9 @@ int launch_v2_dh(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) 
   a.y_flag = ws->y_flag;
   a.pred_partial = ws->pred_partial;
   a.pcnt = ws->pcnt;
+  a.next_mixing = L.next_mixing;
+  a.next_mixing_bytes = L.next_mixing_bytes;
+  a.pf_tick = ws->pf_tick;
 
   a.n_kept_out = L.n_kept_out;
   a.kept_out = L.kept_out;
@@ -800,7 +806,7 @@ int floe_gpu_workspace_create(uint32_t dh, uint32_t di, uint32_t slots,
   const uint64_t o_mp = o;    o = up256(o + 4ull * 32 * std::max<uint64_t>(1024, (dh + 7) / 8));
   const uint64_t o_md = o;    o = up256(o + 16);
   const uint64_t o_st = o;    o = up256(o + 32);  // stats[2], grid barrier counter
-  const uint64_t o_fk = o;    o = up256(o + 32 + 4ull * MS);  // tick, y flag[2], pcnt, kcount[MS]
+  const uint64_t o_fk = o;    o = up256(o + 40 + 4ull * MS);  // tick, y flag[2], pcnt, pf_tick, kcount[MS]
   const uint64_t o_pp = o;    o = up256(o + 4ull * 32 * floe_v2::kMaxGrid);
   const uint64_t o_sel = o;   o = up256(o + 4 * MS);
   const uint64_t o_w = o;     o = up256(o + 4 * MS);
@@ -825,7 +831,8 @@ int floe_gpu_workspace_create(uint32_t dh, uint32_t di, uint32_t slots,
   w->tick = reinterpret_cast<unsigned long long *>(b + o_fk);
   w->y_flag = w->tick + 1;
   w->pcnt = w->tick + 3;
-  w->kcount = reinterpret_cast<uint32_t *>(w->tick + 4);
+  w->pf_tick = w->tick + 4;
+  w->kcount = reinterpret_cast<uint32_t *>(w->tick + 5);
   w->pred_partial = reinterpret_cast<float *>(b + o_pp);
   w->sel = reinterpret_cast<uint32_t *>(b + o_sel);
   w->weights = reinterpret_cast<float *>(b + o_w);
@@ -1366,7 +1373,7 @@ namespace {
 // record count to [0] (records in HBM) or [1] (pinned host records over PCIe).
 int layer_forward_impl(const floe_gpu_layer *l, floe_gpu_workspace *ws, const float *h, float *y,
                        const floe_gpu_layer_trace *tr, unsigned long long *place_acc,
-                       cudaStream_t st);
+                       cudaStream_t st, const floe_gpu_layer *next = nullptr);
 }  // namespace
 
 int floe_gpu_layer_forward(const floe_gpu_layer *l, floe_gpu_workspace *ws, const float *h,
@@ -1381,9 +1388,13 @@ bool layer_fused(const floe_gpu_layer *l) { return l->fast && l->E <= 32; }
 
 int layer_forward_impl(const floe_gpu_layer *l, floe_gpu_workspace *ws, const float *h, float *y,
                        const floe_gpu_layer_trace *tr, unsigned long long *place_acc,
-                       cudaStream_t st) {
+                       cudaStream_t st, const floe_gpu_layer *next) {
   if (layer_fused(l)) {
     FusedLaunch f{};
+    if (next && next->fast) {  // the decode loop's next layer: its mixing goes to L2 early
+      f.next_mixing = next->mixing;
+      f.next_mixing_bytes = (uint64_t)next->dh * next->dh * (next->mix_f16 ? 2u : 4u);
+    }
     f.mixing = l->mixing;
     f.mix_f16 = l->mix_f16;
     f.h = h;
@@ -1910,7 +1921,8 @@ int floe_gpu_model_decode(floe_gpu_model *m, floe_gpu_workspace *ws, const float
     if (int rc = check_ws("layer_forward", ws, ly->dh, ly->di, ly->top_k)) return rc;
     float *o = replay ? y + (size_t)l * m->dh : (l + 1 == L ? y : m->buf + (l & 1) * m->dh);
     if (replay) in = h + (size_t)l * m->dh;
-    if (int rc = layer_forward_impl(ly, ws, in, o, nullptr, nullptr, st)) return rc;
+    const floe_gpu_layer *next = m->layers[(l + 1) % L];  // the next token starts at layer 0
+    if (int rc = layer_forward_impl(ly, ws, in, o, nullptr, nullptr, st, next)) return rc;
     in = o;
   }
   return FLOE_OK;

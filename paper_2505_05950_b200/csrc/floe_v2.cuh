@@ -353,6 +353,9 @@ struct FusedArgs {
   unsigned long long *place_acc;  // nullable [2]: kept records read from HBM / over PCIe
   unsigned long long *phase_ns;   // nullable [G][kTraceSlots]
   int paired;          // launched as clusters of 2: the CTA pair balances phase C over DSMEM
+  const void *next_mixing;      // nullable: the next launch's mixing matrix (L2 prefetch)
+  uint64_t next_mixing_bytes;
+  unsigned long long *pf_tick;  // monotonic ticket: the order CTAs finish issuing records
   uint32_t ns;         // ring stages
   uint32_t max_tiles;  // per-CTA tile capacity of the shared-memory kept list
   uint32_t debug;      // test hook: bit 3 = invert the predicted logits (misprediction path)
@@ -574,6 +577,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
             pdl_wait();
             floe_ptx::mbar_arrive_expect_tx(&hbar, 4u * DH);
             floe_ptx::bulk_g2s(hs, a.h, 4u * DH, &hbar);
+            // h lands ahead of the burst of mixing copies every CTA issues once
+            // the previous grid completes (measured: h otherwise queues 3-5 us)
+            floe_ptx::mbar_wait(&hbar, 0, 3u << 28);
           }
           const uint32_t r0 = r_lo + i * rpi, nr = min(rpi, r_hi - r0);
           wait_empty(u);
@@ -665,6 +671,24 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
         floe_ptx::mbar_arrive_remote(floe_ptx::mapa(&donebar, pr));  // done reading its list
       }
       mark(a, 19);
+      // The CTAs that finish early pull the NEXT layer's mixing matrix into L2
+      // (evict-last) while the slow ones still stream their records: the next
+      // launch's phase A, which waits for this grid, then reads it from L2.
+      // Finish order decides the chunk: the first G/2 finishers cover it all.
+      if (a.next_mixing) {
+        const uint32_t ticket = (uint32_t)(atomicAdd(a.pf_tick, 1ull) % G);
+        const uint32_t nchunk = max(1u, G / 2);
+        if (ticket < nchunk) {
+          const uint64_t per = (a.next_mixing_bytes / nchunk + 4095) & ~4095ull;
+          const uint64_t lo = per * ticket;
+          const uint64_t hi = lo + per < a.next_mixing_bytes ? lo + per : a.next_mixing_bytes;
+          const uint64_t pol = floe_ptx::policy_evict_last();
+          const uint8_t *base = static_cast<const uint8_t *>(a.next_mixing);
+          for (uint64_t o = lo; o < hi; o += 65536)
+            floe_ptx::bulk_prefetch_l2_hint(base + o, (uint32_t)(hi - o < 65536 ? hi - o : 65536),
+                                            pol);
+        }
+      }
     }
     return;
   }
@@ -788,6 +812,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
       }
     }
   pdl_wait();  // from here on: workspace, inputs and outputs shared with the previous grid
+  if (t == 0) mark(a, 11);
   if (!a.has_mixing && a.y && !a.k1_only) {
     // expert mode: CTA 0 zeroes y, the others check a flag before their final
     // reduction; the call index comes from a counter every CTA bumps once

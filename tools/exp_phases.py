@@ -34,7 +34,7 @@ def summarize(tag, traces, marks):
         print(f"   {name:24s} mean {d.mean():7.2f}  min {d.min():7.2f}  max {d.max():7.2f} us")
     end = (T[:, :, 6].max(1) - t0) / 1e3
     print(f"   first start -> last phase-C end: {end.mean():7.2f} us")
-    names = {0: "start", 7: "predicted", 8: "1st mixing", 1: "A done", 2: "barrier out", 25: "routed", 3: "K1 start",
+    names = {0: "start", 11: "pdl released", 7: "predicted", 8: "1st mixing", 1: "A done", 2: "barrier out", 25: "routed", 3: "K1 start",
              4: "K1 done", 5: "1st record", 6: "C done", 16: "P: predicted", 17: "P: tiles issued",
              18: "P: records start", 10: "published", 21: "P: all published", 19: "P: plan", 20: "P: all issued"}
     for m, nm in names.items():
@@ -78,6 +78,19 @@ def main():
                 w.read_phase_trace()
         summarize(name, traces, marks)
         T = np.stack(traces).astype(np.int64)
+        if name == "layer":
+            # steady state: 32-layer replay decode back to back (PDL), the trace
+            # of the last launch
+            layers32, _ = bench.build_model(fb, torch, 8)
+            model = fb.GpuModel(layers32)
+            hs = bench.replay_inputs(fb, torch, 4, 8)
+            ysd = torch.empty(8, bench.DH, device="cuda")
+            steady = []
+            for i in range(4):
+                model.decode(hs[i], ws, out=ysd, replay=True)
+                torch.cuda.synchronize()
+                steady.append(w.read_phase_trace())
+            summarize("layer (steady state: last of 8 back-to-back launches)", steady, LAYER)
         n = T[:, :, 9].ravel()
         d = ((T[:, :, 6] - T[:, :, 5]) / 1e3).ravel()
         print(f"   kept records per CTA: mean {n.mean():.1f} min {n.min()} max {n.max()} sd {n.std():.1f};"
