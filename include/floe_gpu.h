@@ -200,6 +200,17 @@ int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x_dev
                                     uint32_t n_tokens, float *y_dev, float *v_dev,
                                     floe_stream_t stream);
 
+/* pack_compact (core/src/offload.cpp:27-53) on the device: the channels c with
+ * mask_dev[c] != 0 in ascending order -> channels_dev [n] and their records,
+ * f16 gate row | f16 down row (element_bytes 2: 4*d_hidden bytes each, the
+ * wire format of the host-resident decode and of records_f16), into payload
+ * (device or pinned, mapped host memory: the H2D/D2H wire path); *n_out_dev =
+ * n.  element_bytes 4 is FLOE_ERR_UNSUPPORTED (the device keeps f16 records).
+ * Byte-identical to the reference for element_bytes 2. */
+int floe_gpu_pack_compact(const floe_gpu_expert *e, const uint8_t *mask_dev,
+                          uint32_t element_bytes, uint32_t *channels_dev, uint8_t *payload,
+                          uint32_t *n_out_dev, floe_stream_t stream);
+
 /* out = dequantize(up_q) in f32, bit-exact with floe::dequantize. */
 int floe_gpu_dequantize_up(const floe_gpu_expert *e, float *out_dev,
                            floe_stream_t stream);

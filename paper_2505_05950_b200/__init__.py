@@ -29,6 +29,7 @@ from ._abi import (  # noqa: F401
     layer_forward,
     layer_forward_batched,
     layer_forward_host,
+    pack_compact,
     lib,
     library_path,
     predict_experts,
@@ -42,5 +43,5 @@ from ._abi import (  # noqa: F401
 __all__ = ["FloeError", "GpuCalib", "GpuExpert", "GpuLayer", "GpuModel", "GpuPredictor", "Offload", "Workspace",
            "abi_version", "dequantize", "device_info", "expert_forward_sparse",
            "exported_symbols", "layer_forward", "layer_forward_batched", "lib", "library_path", "predict_experts",
-           "predict_mask", "qgemv_channels", "qgemv_channels_batched", "expert_forward_batched", "gen_normals", "layer_forward_host",
+           "predict_mask", "qgemv_channels", "qgemv_channels_batched", "expert_forward_batched", "gen_normals", "layer_forward_host", "pack_compact",
            "quantize"]

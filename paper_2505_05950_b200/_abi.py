@@ -113,6 +113,7 @@ _SIGS = {
     "floe_gpu_predictor_create": (ct.c_int, [_U32, _U32, _U32, _P, _P, ct.POINTER(_P)]),
     "floe_gpu_predictor_destroy": (ct.c_int, [_P]),
     "floe_gpu_predict_experts": (ct.c_int, [_P, _P, _U32, _U32, _P, _P]),
+    "floe_gpu_pack_compact": (ct.c_int, [_P, _P, _U32, _P, _P, _P, _P]),
     "floe_gpu_layer_forward_batched": (ct.c_int, [_P, _P, _P, _U32, _P, _P]),
     "floe_gpu_model_create": (ct.c_int, [_P, _U32, ct.POINTER(_P)]),
     "floe_gpu_model_destroy": (ct.c_int, [_P]),
@@ -499,6 +500,21 @@ def predict_experts(p: GpuPredictor, x, layer: int, count: int, stream=None):
     _check(lib().floe_gpu_predict_experts(p.handle, x.data_ptr(), layer, count, out.data_ptr(),
                                           _stream(stream)))
     return out[:count]
+
+
+def pack_compact(e: GpuExpert, mask, element_bytes: int = 2, stream=None):
+    """pack_compact (offload.cpp:27-53) of the masked channels: (channels [n] u32,
+    payload [n * 4 * d_hidden] u8) as cuda tensors."""
+    torch = _torch()
+    mask = mask.to(torch.uint8).contiguous()
+    di, dh = e.d_intermediate, e.d_hidden
+    ch = torch.empty(di, dtype=torch.int32, device=mask.device)
+    payload = torch.empty(di * 2 * dh * element_bytes, dtype=torch.uint8, device=mask.device)
+    n = torch.zeros(1, dtype=torch.int32, device=mask.device)
+    _check(lib().floe_gpu_pack_compact(e.handle, mask.data_ptr(), element_bytes, ch.data_ptr(),
+                                       payload.data_ptr(), n.data_ptr(), _stream(stream)))
+    k = int(n.item())
+    return ch[:k], payload[:k * 2 * dh * element_bytes]
 
 
 def layer_forward_batched(layer: GpuLayer, h, ws: Workspace = None, out=None, stream=None):

@@ -25,6 +25,8 @@
 #include "floe_blayer.cuh"
 
 #include <cub/device/device_segmented_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 
 using floe_k::ExpertDesc;
 using floe_k::K1Args;
@@ -1743,6 +1745,49 @@ int floe_gpu_offload_stats(floe_gpu_offload *o, floe_offload_stats *out, floe_st
   for (uint32_t i = 0; i < o->L * o->E; ++i)
     if (o->state[i] == floe_gpu_offload::kResident) dev += o->rec_bytes;
   out->device_record_bytes = dev;
+  return FLOE_OK;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ compact pack ---
+namespace {
+// record c of the expert (f16 gate row | f16 down row) -> slot i of the payload
+__global__ void gather_records(const __half *__restrict__ rec, const uint32_t *__restrict__ ch,
+                               const uint32_t *__restrict__ n, uint32_t dh,
+                               uint8_t *__restrict__ payload) {
+  const uint32_t i = blockIdx.x;
+  if (i >= *n) return;
+  const uint4 *src = reinterpret_cast<const uint4 *>(rec + (size_t)ch[i] * 2 * dh);
+  uint4 *dst = reinterpret_cast<uint4 *>(payload + (size_t)i * 4 * dh);
+  for (uint32_t k = threadIdx.x; k < dh / 4; k += blockDim.x) dst[k] = src[k];
+}
+}  // namespace
+
+extern "C" {
+
+int floe_gpu_pack_compact(const floe_gpu_expert *e, const uint8_t *mask, uint32_t element_bytes,
+                          uint32_t *channels, uint8_t *payload, uint32_t *n_out,
+                          floe_stream_t stream) {
+  if (!e || !mask || !channels || !payload || !n_out)
+    return fail(FLOE_ERR_INVALID, "pack_compact: null argument");
+  if (element_bytes != 2 && element_bytes != 4)
+    return fail(FLOE_ERR_INVALID, "pack_compact: element_bytes must be 2 or 4");
+  if (element_bytes == 4)
+    return fail(FLOE_ERR_UNSUPPORTED, "pack_compact: the device holds f16 records (element_bytes 2)");
+  if (e->up_only) return fail(FLOE_ERR_INVALID, "pack_compact: expert has no gate/down records");
+  if (e->dh % 8) return fail(FLOE_ERR_UNSUPPORTED, "pack_compact: d_hidden must be a multiple of 8");
+  cudaStream_t st = S(stream);
+  size_t tmp = 0;
+  cub::CountingInputIterator<uint32_t> it(0);
+  cub::DeviceSelect::Flagged(nullptr, tmp, it, mask, channels, n_out, (int)e->di, st);
+  void *t = nullptr;
+  CK(cudaMallocAsync(&t, tmp, st));
+  cub::DeviceSelect::Flagged(t, tmp, it, mask, channels, n_out, (int)e->di, st);
+  gather_records<<<e->di, 256, 0, st>>>(e->host_desc.records, channels, n_out, e->dh, payload);
+  const cudaError_t ce = cudaGetLastError();
+  cudaFreeAsync(t, st);
+  if (ce != cudaSuccess) return fail(FLOE_ERR_CUDA, "pack_compact: %s", cudaGetErrorString(ce));
   return FLOE_OK;
 }
 
