@@ -564,6 +564,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   if (producer) {
     // =================== producer warp ===================
     // lane 0 issues every copy; the whole warp computes the phase-C plan
+    uint32_t k_early = 0;  // own records issued before the end of K1
     if (lane == 0) {
       uint32_t u = 0;
       if (a.has_mixing) {
@@ -621,6 +622,35 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
             issue(u++, etiles_s[tr.slot] + (size_t)tr.t * TILE_B, TILE_B);
           }
       }
+      // Early records: while the last K1 tiles are consumed, record stage r
+      // is filled with kept record r as soon as the ring stages under it have
+      // seen their last K1 use released and the K1 epilogues have appended
+      // entry r, so phase C starts on landed data instead of a cold ring.
+      // Record stages over the x table wait for the end of K1.
+      if (!a.k1_only && spec_ok) {
+        const uint32_t uEnd = u;
+        const uint32_t r_max = min(nsC, ns * TILE_B / REC_B);
+        auto stages_free = [&](uint32_t r) {  // ring stages under record stage r: last use released
+          const uint32_t lo = r * REC_B, hi = lo + REC_B;
+          for (uint32_t st = lo / TILE_B; st <= (hi - 1) / TILE_B; ++st)
+            if (uEnd > st) {
+              const uint32_t us = st + ((uEnd - 1 - st) / ns) * ns;
+              if (!floe_ptx::mbar_test_wait(&empty[st], (us / ns) & 1u)) return false;
+            }
+          return true;
+        };
+        // never blocks past the end of K1: once the list is final the normal
+        // path issues the rest (the whole ring is free by then)
+        while (k_early < r_max && !floe_ptx::mbar_test_wait(&listbar, 0)) {
+          if ((ld_acquire_s(&lf[k_early]) & kValid) && stages_free(k_early)) {
+            const uint32_t r = k_early, f = lf[r] & ~kValid, s2 = f / a.di, c = f - s2 * a.di;
+            issueC(r, rec_s[s2] + (size_t)c * 2 * DH, lv[r] * w_s[s2]);
+            ++k_early;
+          } else {
+            __nanosleep(32);
+          }
+        }
+      }
     }
     if (a.k1_only) return;
     // ---- phase C: the record ring fills as soon as K1 is done (every tile
@@ -638,7 +668,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
         n_pub = n_own;  // were acquired through listbar)
         floe_ptx::mbar_arrive_remote(floe_ptx::mapa(&peerbar, (b ^ 1u) & 1u));
       }
-      for (uint32_t k = 0; k < P; ++k) own_item(k);
+      for (uint32_t k = k_early; k < P; ++k) own_item(k);
       uint32_t own = n_own, take = 0, pfirst = 0;
       const uint32_t peer = b ^ 1u;
       if (a.paired) {
@@ -1100,12 +1130,12 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
       if (ka) {
         const uint32_t pos = base + __popc(ba & lt);
         lv[pos] = v2.x;
-        lf[pos] = (tr.f0 + g) | kValid;
+        st_release_s(&lf[pos], (tr.f0 + g) | kValid);  // read early by the producer
       }
       if (kb) {
         const uint32_t pos = base + na + __popc(bbal & lt);
         lv[pos] = v2.y;
-        lf[pos] = (tr.f0 + g + 8) | kValid;
+        st_release_s(&lf[pos], (tr.f0 + g + 8) | kValid);
       }
     }
   };

@@ -18,7 +18,8 @@ import bench  # noqa: E402
 # verified), 19 all records issued.  router marks: 24 barrier seen, 25 routed.
 LAYER = [(0, 7, "predicted partial"), (0, 26, "P: predicted routing"), (0, 8, "first mixing stage"), (0, 1, "A mixing"), (1, 2, "grid barrier"), (2, 3, "K1 setup"), (3, 4, "K1"),
          (4, 5, "first record"), (5, 6, "records"), (24, 25, "P: exact routing"),
-         (16, 17, "P: K1 tile issue"), (17, 18, "P: wait routing"), (18, 19, "P: record issue")]
+         (16, 17, "P: K1 tile issue"), (17, 18, "P: wait routing"), (18, 19, "P: record issue"),
+         (4, 27, "K1 done -> plan known")]
 EXPERT = [(0, 3, "start -> K1")] + LAYER[6:9] + LAYER[11:]
 
 
@@ -36,7 +37,7 @@ def summarize(tag, traces, marks):
     print(f"   first start -> last phase-C end: {end.mean():7.2f} us")
     names = {0: "start", 11: "pdl released", 7: "predicted", 8: "1st mixing", 1: "A done", 2: "barrier out", 25: "routed", 3: "K1 start",
              4: "K1 done", 5: "1st record", 6: "C done", 16: "P: predicted", 17: "P: tiles issued",
-             18: "P: records start", 10: "published", 21: "P: all published", 19: "P: plan", 20: "P: all issued"}
+             18: "P: records start", 29: "published", 30: "R: all seen", 27: "R: plan known", 19: "P: all issued"}
     for m, nm in names.items():
         v = T[:, :, m]
         if not (v > 0).any():
@@ -91,7 +92,13 @@ def main():
                 torch.cuda.synchronize()
                 steady.append(w.read_phase_trace())
             summarize("layer (steady state: last of 8 back-to-back launches)", steady, LAYER)
+        for w in (0, 1, 4):
+            sl = [T[:, :, 32 + w * 4 + k].mean() / 1e3 for k in range(4)]
+            print(f"   K1 warp {w}: wait_full {sl[0]:.2f} compute {sl[1]:.2f} qbar {sl[2]:.2f} epilogue/other {sl[3]:.2f} us")
         n = T[:, :, 9].ravel()
+        m = T[:, :, 28].ravel()
+        if m.any():
+            print(f"   processed records per CTA: mean {m.mean():.1f} min {m.min()} max {m.max()} sd {m.std():.1f}")
         d = ((T[:, :, 6] - T[:, :, 5]) / 1e3).ravel()
         print(f"   kept records per CTA: mean {n.mean():.1f} min {n.min()} max {n.max()} sd {n.std():.1f};"
               f" corr(records, phase-C time) {np.corrcoef(n, d)[0, 1]:.2f};"
