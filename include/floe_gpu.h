@@ -293,6 +293,21 @@ typedef struct floe_offload_stats {
   uint64_t up_bytes_per_expert;  /* codes + f16 meta, always resident in HBM          */
   uint64_t promotions, evictions, bytes_promoted;
   uint64_t device_record_bytes;  /* records resident in HBM now                       */
+  /* DecodeTimeline (core/include/floe/offload.hpp:128-157) over the decoded
+   * tokens.  demanded == from_cache + prefetch_used + sync; the bytes moved
+   * (promotions + sync) == prefetch_used + prefetch_wasted + sync +
+   * prefetch_pending (promotions not yet demanded or evicted).  Up projections
+   * are HBM-resident (cache); a promotion is one prefetch batch. */
+  uint64_t bytes_demanded, bytes_from_cache, bytes_prefetch_used, bytes_sync;
+  uint64_t bytes_prefetch_wasted, bytes_prefetch_pending;
+  uint64_t requests_up, requests_channel;
+  /* predictor scores on the decode path (eval on; predictor.cpp:206-254):
+   * reuse masks (predict_mask of layer l's experts from layer l-1's block
+   * input) and, with a predictor attached, predict_experts sets. */
+  double mask_precision, mask_recall;
+  uint64_t mask_samples;
+  double set_precision, set_recall;
+  uint64_t set_samples;
 } floe_offload_stats;
 int floe_gpu_offload_create(floe_gpu_layer *const *layers, uint32_t n_layers,
                             uint64_t vram_budget, floe_gpu_offload **out);
@@ -305,6 +320,12 @@ int floe_gpu_offload_decode(floe_gpu_offload *o, floe_gpu_workspace *ws, const f
 int floe_gpu_offload_decode_replay(floe_gpu_offload *o, floe_gpu_workspace *ws,
                                    const float *h_dev, float *y_dev, floe_stream_t stream);
 int floe_gpu_offload_stats(floe_gpu_offload *o, floe_offload_stats *out, floe_stream_t stream);
+/* Score the predictors on the decode path (reuse masks always; expert sets
+ * when `predictor` is non-NULL, top `count` of W x + b).  Adds one K1-only
+ * pass over a layer's experts per layer (replaces
+ * predictor.cpp:reuse_mask_metrics / eval_sets offline scoring). */
+int floe_gpu_offload_set_eval(floe_gpu_offload *o, int enable, const floe_gpu_predictor *predictor,
+                              uint32_t count);
 
 /* ----------------------------------------------------- counters / profile */
 /* Device-side running totals kept by a workspace: calls (K1 launches) and

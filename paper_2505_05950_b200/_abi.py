@@ -79,6 +79,7 @@ _SIGS = {
     "floe_gpu_offload_decode": (ct.c_int, [_P, _P, _P, _P, _P]),
     "floe_gpu_offload_decode_replay": (ct.c_int, [_P, _P, _P, _P, _P]),
     "floe_gpu_offload_stats": (ct.c_int, [_P, _P, _P]),
+    "floe_gpu_offload_set_eval": (ct.c_int, [_P, ct.c_int, _P, _U32]),
     "floe_gpu_expert_set_resident": (ct.c_int, [_P, ct.c_int, _P]),
     "floe_gpu_expert_residency": (ct.c_int, [_P, _P, _P]),
     "floe_gpu_device_free": (ct.c_int, [_P]),
@@ -572,7 +573,15 @@ class OffloadStats(ct.Structure):
                 ("records_over_pcie", ct.c_uint64), ("record_bytes", ct.c_uint64),
                 ("up_bytes_per_expert", ct.c_uint64), ("promotions", ct.c_uint64),
                 ("evictions", ct.c_uint64), ("bytes_promoted", ct.c_uint64),
-                ("device_record_bytes", ct.c_uint64)]
+                ("device_record_bytes", ct.c_uint64),
+                ("bytes_demanded", ct.c_uint64), ("bytes_from_cache", ct.c_uint64),
+                ("bytes_prefetch_used", ct.c_uint64), ("bytes_sync", ct.c_uint64),
+                ("bytes_prefetch_wasted", ct.c_uint64), ("bytes_prefetch_pending", ct.c_uint64),
+                ("requests_up", ct.c_uint64), ("requests_channel", ct.c_uint64),
+                ("mask_precision", ct.c_double), ("mask_recall", ct.c_double),
+                ("mask_samples", ct.c_uint64),
+                ("set_precision", ct.c_double), ("set_recall", ct.c_double),
+                ("set_samples", ct.c_uint64)]
 
 
 class Offload:
@@ -615,6 +624,14 @@ class Offload:
         _check(lib().floe_gpu_offload_decode_replay(self.handle, ws.handle, h.data_ptr(),
                                                     y.data_ptr(), _stream(stream)))
         return y
+
+    def set_eval(self, enable: bool = True, predictor=None, count: int = 0):
+        """Score the predictors on the decode path: reuse masks (predict_mask of
+        layer l's experts from layer l-1's block input) and, with an
+        InterExpertPredictor, predict_experts sets (predictor.cpp:206-254)."""
+        _check(lib().floe_gpu_offload_set_eval(self.handle, 1 if enable else 0,
+                                               predictor.handle if predictor else None,
+                                               int(count)))
 
     def stats(self, stream=None) -> dict:
         st = OffloadStats()

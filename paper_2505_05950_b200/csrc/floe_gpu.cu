@@ -1375,7 +1375,8 @@ namespace {
 // record count to [0] (records in HBM) or [1] (pinned host records over PCIe).
 int layer_forward_impl(const floe_gpu_layer *l, floe_gpu_workspace *ws, const float *h, float *y,
                        const floe_gpu_layer_trace *tr, unsigned long long *place_acc,
-                       cudaStream_t st, const floe_gpu_layer *next = nullptr);
+                       cudaStream_t st, const floe_gpu_layer *next = nullptr,
+                       uint32_t *n_kept_out = nullptr);
 }  // namespace
 
 int floe_gpu_layer_forward(const floe_gpu_layer *l, floe_gpu_workspace *ws, const float *h,
@@ -1390,9 +1391,10 @@ bool layer_fused(const floe_gpu_layer *l) { return l->fast && l->E <= 32; }
 
 int layer_forward_impl(const floe_gpu_layer *l, floe_gpu_workspace *ws, const float *h, float *y,
                        const floe_gpu_layer_trace *tr, unsigned long long *place_acc,
-                       cudaStream_t st, const floe_gpu_layer *next) {
+                       cudaStream_t st, const floe_gpu_layer *next, uint32_t *n_kept_out) {
   if (layer_fused(l)) {
     FusedLaunch f{};
+    f.n_kept_out = n_kept_out;  // per routed slot (ascending expert order)
     if (next && next->fast) {  // the decode loop's next layer: its mixing goes to L2 early
       f.next_mixing = next->mixing;
       f.next_mixing_bytes = (uint64_t)next->dh * next->dh * (next->mix_f16 ? 2u : 4u);
@@ -1497,6 +1499,63 @@ __global__ void offload_account(const uint32_t *seg_count, uint32_t G, uint32_t 
 }
 }  // namespace
 
+// eval_masks / eval_sets (predictor.cpp:206-254): per sample precision
+// inter/|pred| (1 if both empty, 0 if only the prediction is) and recall
+// inter/|truth| (1 for an empty truth), summed for the macro average.
+__device__ __forceinline__ void accumulate_pr(uint32_t inter, uint32_t pn, uint32_t tn,
+                                              double *psum, double *rsum) {
+  atomicAdd(psum, pn == 0 ? (tn == 0 ? 1.0 : 0.0) : (double)inter / (double)pn);
+  atomicAdd(rsum, tn == 0 ? 1.0 : (double)inter / (double)tn);
+}
+
+// block k: predicted mask of routed expert sel[k] vs the layer's true mask k
+__global__ void score_masks(const uint8_t *__restrict__ pmask, const uint8_t *__restrict__ tmask,
+                            const uint32_t *__restrict__ sel, uint32_t di, double *acc,
+                            unsigned long long *samples) {
+  const uint32_t k = blockIdx.x;
+  const uint8_t *p = pmask + (size_t)sel[k] * di, *t = tmask + (size_t)k * di;
+  uint32_t inter = 0, pn = 0, tn = 0;
+  for (uint32_t i = threadIdx.x; i < di; i += blockDim.x) {
+    const bool a = p[i] != 0, b = t[i] != 0;
+    pn += a;
+    tn += b;
+    inter += a && b;
+  }
+  __shared__ uint32_t red[3][32];
+  for (int o = 16; o >= 1; o >>= 1) {
+    inter += __shfl_xor_sync(0xffffffffu, inter, o);
+    pn += __shfl_xor_sync(0xffffffffu, pn, o);
+    tn += __shfl_xor_sync(0xffffffffu, tn, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = inter;
+    red[1][threadIdx.x >> 5] = pn;
+    red[2][threadIdx.x >> 5] = tn;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t I = 0, P = 0, T = 0;
+    for (uint32_t w = 0; w < blockDim.x / 32; ++w) {
+      I += red[0][w];
+      P += red[1][w];
+      T += red[2][w];
+    }
+    accumulate_pr(I, P, T, acc, acc + 1);
+    atomicAdd(samples, 1ull);
+  }
+}
+
+// predicted expert set (count ids) vs the routed set (K ids)
+__global__ void score_sets(const uint32_t *__restrict__ pred, uint32_t count,
+                           const uint32_t *__restrict__ sel, uint32_t K, double *acc,
+                           unsigned long long *samples) {
+  uint32_t inter = 0;
+  for (uint32_t i = 0; i < count; ++i)
+    for (uint32_t j = 0; j < K; ++j) inter += pred[i] == sel[j];
+  accumulate_pr(inter, count, K, acc, acc + 1);
+  atomicAdd(samples, 1ull);
+}
+
 struct floe_gpu_offload {
   std::vector<floe_gpu_layer *> layers;
   uint32_t L = 0, E = 0, K = 0, dh = 0;
@@ -1514,10 +1573,42 @@ struct floe_gpu_offload {
   float *buf = nullptr;                       // 2 x dh ping-pong
   unsigned long long *acc = nullptr;          // [2] kept records from HBM / over PCIe
   cudaEvent_t sel_ready = nullptr;
-  bool sel_pending = false;
+  bool sel_pending = false;  // generic path: a routing readback is in flight
+  bool sel_fresh = false;    // sel_host holds a routing the policy has not used
   cudaStream_t side = nullptr;
   uint64_t tokens = 0, promotions = 0, evictions = 0, bytes_promoted = 0;
   uint64_t up_bytes = 0;
+  // DecodeTimeline (offload.hpp:128-157), classified per completed token from
+  // its routing, kept counts and the placement its kernels saw: up projections
+  // are HBM-resident (cache); records of resident experts are cache hits, or
+  // prefetch_used on an expert's first demand after its promotion landed (the
+  // rest of that promotion is wasted, as in simulate_decode: it stays cached);
+  // records of host-resident experts are sync (read in place over PCIe).
+  uint32_t *nkept_dev = nullptr;  // [L][K] kept records per routed slot, this token
+  struct Readback {
+    uint32_t *sel = nullptr, *nkept = nullptr;  // pinned [L][K]
+    cudaEvent_t ev = nullptr;
+    std::vector<uint8_t> resident, fresh;      // placement the token's kernels saw
+    bool busy = false;
+  };
+  std::vector<Readback> ring;  // tokens in flight (in order)
+  uint32_t ring_head = 0, ring_n = 0;
+  std::vector<uint8_t> fresh;  // promoted, landed, not yet demanded
+  uint64_t t_demanded = 0, t_cache = 0, t_used = 0, t_sync = 0, t_wasted = 0, t_req_ch = 0,
+           t_req_up = 0, t_tokens = 0;
+  // prediction scoring on the decode path (predictor.cpp:164-254): reuse
+  // masks of layer l's routed experts from layer l-1's block input, and the
+  // learned predictor's expert sets when one is attached
+  bool eval = false;
+  floe_gpu_workspace *ews = nullptr;  // E slots: every expert of a layer in one K1-only pass
+  uint8_t *pmask_dev = nullptr;       // [E][di]
+  uint8_t *tmask_dev = nullptr;       // [L][K][di]
+  float *u_dev = nullptr;             // [L][dh] block inputs
+  double *pr_dev = nullptr;           // [4]: mask precision/recall sums, set precision/recall sums
+  unsigned long long *pn_dev = nullptr;  // [2]: mask samples, set samples
+  const floe_gpu_predictor *pred = nullptr;
+  uint32_t pred_count = 0;
+  uint32_t *pexp_dev = nullptr;       // [E]
 };
 
 namespace {
@@ -1554,15 +1645,64 @@ int offload_switch(floe_gpu_offload *o, uint32_t i, bool to_hbm, cudaStream_t st
 constexpr float kFreqDecay = 0.98f;   // per token: a ~50-token memory of routing counts
 constexpr float kAdmitMargin = 3.0f;  // extra routings (decayed) to displace a resident expert
 
+// Timeline classification of one completed token (see floe_gpu_offload).
+void offload_classify(floe_gpu_offload *o, const floe_gpu_offload::Readback &r) {
+  const uint64_t rb = 4ull * o->dh;
+  for (uint32_t l = 0; l < o->L; ++l)
+    for (uint32_t k = 0; k < o->K; ++k) {
+      const uint32_t i = l * o->E + r.sel[l * o->K + k];
+      const uint64_t bytes = (uint64_t)r.nkept[l * o->K + k] * rb;
+      o->t_demanded += o->up_bytes + bytes;
+      o->t_cache += o->up_bytes;
+      if (!r.resident[i]) {
+        o->t_sync += bytes;
+        o->t_req_ch += r.nkept[l * o->K + k];  // one bulk copy per record
+      } else if (r.fresh[i] && o->fresh[i]) {
+        o->t_used += bytes;
+        o->t_wasted += o->rec_bytes - bytes;
+        o->fresh[i] = 0;
+      } else {
+        o->t_cache += bytes;
+      }
+    }
+  ++o->t_tokens;
+}
+
+// Completed tokens in order; `block` waits for the oldest one.
+int offload_drain(floe_gpu_offload *o, bool block) {
+  while (o->ring_n) {
+    floe_gpu_offload::Readback &r = o->ring[o->ring_head];
+    if (block) {
+      CK(cudaEventSynchronize(r.ev));
+      block = false;
+    } else if (cudaEventQuery(r.ev) != cudaSuccess) {
+      break;
+    }
+    offload_classify(o, r);
+    std::memcpy(o->sel_host, r.sel, 4ull * o->L * o->K);  // the newest routing
+    o->sel_fresh = true;
+    r.busy = false;
+    o->ring_head = (o->ring_head + 1) % (uint32_t)o->ring.size();
+    --o->ring_n;
+  }
+  return FLOE_OK;
+}
+
 int offload_policy(floe_gpu_offload *o, cudaStream_t st) {
   const uint32_t N = o->L * o->E;
   for (uint32_t i = 0; i < N; ++i)
     if (o->state[i] == floe_gpu_offload::kCopying && cudaEventQuery(o->copy_done[i]) == cudaSuccess) {
       if (int rc = offload_switch(o, i, true, st)) return rc;
       o->state[i] = floe_gpu_offload::kResident;
+      o->fresh[i] = 1;
     }
-  if (!o->sel_pending || cudaEventQuery(o->sel_ready) != cudaSuccess) return FLOE_OK;
-  o->sel_pending = false;
+  if (int rc = offload_drain(o, o->ring_n == o->ring.size())) return rc;
+  if (o->sel_pending && cudaEventQuery(o->sel_ready) == cudaSuccess) {
+    o->sel_pending = false;
+    o->sel_fresh = true;
+  }
+  if (!o->sel_fresh) return FLOE_OK;
+  o->sel_fresh = false;
   std::vector<uint32_t> want;
   for (float &f : o->freq) f *= kFreqDecay;
   for (uint32_t l = 0; l < o->L; ++l)
@@ -1588,6 +1728,10 @@ int offload_policy(floe_gpu_offload *o, cudaStream_t st) {
       // than the working set thrashes and pays more PCIe than it saves.
       if (o->freq[i] < o->freq[victim] + kAdmitMargin) break;
       if (int rc = offload_switch(o, (uint32_t)victim, false, st)) return rc;
+      if (o->fresh[victim]) {  // promoted, never demanded: the whole batch was wasted
+        o->t_wasted += o->rec_bytes;
+        o->fresh[victim] = 0;
+      }
       o->state[victim] = floe_gpu_offload::kHost;
       o->committed -= o->rec_bytes;
       ++o->evictions;
@@ -1643,6 +1787,14 @@ int floe_gpu_offload_create(floe_gpu_layer *const *layers, uint32_t n_layers,
   CK(cudaMalloc(&o->buf, 8ull * o->dh));
   CK(cudaMalloc(&o->acc, 16));
   CK(cudaMemset(o->acc, 0, 16));
+  CK(cudaMalloc(&o->nkept_dev, 4ull * o->L * o->K));
+  o->fresh.assign(N, 0);
+  o->ring.resize(4);
+  for (auto &r : o->ring) {
+    CK(cudaMallocHost(&r.sel, 4ull * o->L * o->K));
+    CK(cudaMallocHost(&r.nkept, 4ull * o->L * o->K));
+    CK(cudaEventCreateWithFlags(&r.ev, cudaEventDisableTiming));
+  }
   // every expert starts host-resident (records in pinned host memory)
   for (uint32_t i = 0; i < N; ++i) {
     floe_gpu_expert *e = o->layers[i / o->E]->experts[i % o->E];
@@ -1665,6 +1817,19 @@ int floe_gpu_offload_destroy(floe_gpu_offload *o) {
     if (o->copy_done[i]) cudaEventDestroy(o->copy_done[i]);
   }
   if (o->sel_ready) cudaEventDestroy(o->sel_ready);
+  for (auto &r : o->ring) {
+    cudaFreeHost(r.sel);
+    cudaFreeHost(r.nkept);
+    if (r.ev) cudaEventDestroy(r.ev);
+  }
+  cudaFree(o->nkept_dev);
+  if (o->ews) floe_gpu_workspace_destroy(o->ews);
+  cudaFree(o->pmask_dev);
+  cudaFree(o->tmask_dev);
+  cudaFree(o->u_dev);
+  cudaFree(o->pr_dev);
+  cudaFree(o->pn_dev);
+  cudaFree(o->pexp_dev);
   if (o->side) cudaStreamDestroy(o->side);
   cudaFree(o->resident_dev);
   cudaFree(o->sel_dev);
@@ -1685,16 +1850,51 @@ namespace {
 int offload_token(floe_gpu_offload *o, floe_gpu_workspace *ws, const float *h_dev, float *y_dev,
                   bool replay, cudaStream_t st) {
   if (int rc = offload_policy(o, st)) return rc;
+  // the placement this token's kernels see (switches happen between tokens)
+  floe_gpu_offload::Readback &rb = o->ring[(o->ring_head + o->ring_n) % o->ring.size()];
+  rb.resident = o->resident_host;
+  rb.fresh = o->fresh;
   const float *in = h_dev;
+  const uint32_t di = o->layers[0]->di;
   for (uint32_t l = 0; l < o->L; ++l) {
     float *outp = replay ? y_dev + (size_t)l * o->dh
                          : (l + 1 == o->L ? y_dev : o->buf + (l & 1) * o->dh);
     if (replay) in = h_dev + (size_t)l * o->dh;
-    floe_gpu_layer_trace tr{nullptr, o->sel_dev + l * o->K, nullptr, nullptr};
+    floe_gpu_layer_trace tr{o->eval ? o->u_dev + (size_t)l * o->dh : nullptr, o->sel_dev + l * o->K,
+                            nullptr, o->eval ? o->tmask_dev + (size_t)l * o->K * di : nullptr};
     const floe_gpu_layer *ly = o->layers[l];
     if (int rc = check_ws("offload_decode", ws, ly->dh, ly->di, ly->top_k)) return rc;
     if (layer_fused(ly)) {  // the fused kernel does the record accounting itself
-      if (int rc = layer_forward_impl(ly, ws, in, outp, &tr, o->acc, st)) return rc;
+      if (int rc = layer_forward_impl(ly, ws, in, outp, &tr, o->acc, st, nullptr,
+                                      o->nkept_dev + l * o->K))
+        return rc;
+      if (o->eval && l > 0) {
+        // reuse predictor: every expert of layer l against layer l-1's block
+        // input (one K1-only pass, each expert's own threshold), scored on
+        // the experts layer l routed to
+        for (uint32_t e0 = 0; e0 < o->E; e0 += 2) {  // two experts per pass (smem lists)
+          FusedLaunch f{};
+          f.table = ly->table + e0;
+          f.slots = std::min<uint32_t>(2, o->E - e0);
+          f.dh = ly->dh;
+          f.di = ly->di;
+          f.k1_only = true;
+          f.x = o->u_dev + (size_t)(l - 1) * o->dh;
+          f.mask_out = o->pmask_dev + (size_t)e0 * di;
+          if (int rc = launch_v2(f, o->ews, st)) return rc;
+        }
+        score_masks<<<o->K, 256, 0, st>>>(o->pmask_dev, o->tmask_dev + (size_t)l * o->K * di,
+                                          o->sel_dev + l * o->K, di, o->pr_dev, o->pn_dev);
+        CK_LAUNCH();
+        if (o->pred && l < o->pred->layers) {
+          if (int rc = floe_gpu_predict_experts(o->pred, o->u_dev + (size_t)(l - 1) * o->dh, l,
+                                                o->pred_count, o->pexp_dev, st))
+            return rc;
+          score_sets<<<1, 1, 0, st>>>(o->pexp_dev, o->pred_count, o->sel_dev + l * o->K, o->K,
+                                      o->pr_dev + 2, o->pn_dev + 1);
+          CK_LAUNCH();
+        }
+      }
     } else {
       if (int rc = layer_forward_impl(ly, ws, in, outp, &tr, nullptr, st)) return rc;
       offload_account<<<1, 32, 0, st>>>(ws->seg_count, (uint32_t)device_info().sm, o->K,
@@ -1704,7 +1904,14 @@ int offload_token(floe_gpu_offload *o, floe_gpu_workspace *ws, const float *h_de
     }
     in = outp;
   }
-  if (!o->sel_pending) {
+  // every token's routing and kept counts come back (timeline, promotions)
+  if (layer_fused(o->layers[0])) {
+    CK(cudaMemcpyAsync(rb.sel, o->sel_dev, 4ull * o->L * o->K, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(rb.nkept, o->nkept_dev, 4ull * o->L * o->K, cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(rb.ev, st));
+    rb.busy = true;
+    ++o->ring_n;
+  } else if (!o->sel_pending) {
     CK(cudaMemcpyAsync(o->sel_host, o->sel_dev, 4ull * o->L * o->K, cudaMemcpyDeviceToHost, st));
     CK(cudaEventRecord(o->sel_ready, st));
     o->sel_pending = true;
@@ -1745,6 +1952,58 @@ int floe_gpu_offload_stats(floe_gpu_offload *o, floe_offload_stats *out, floe_st
   for (uint32_t i = 0; i < o->L * o->E; ++i)
     if (o->state[i] == floe_gpu_offload::kResident) dev += o->rec_bytes;
   out->device_record_bytes = dev;
+  if (int rc = offload_drain(o, false)) return rc;  // the stream is idle: every token completes
+  out->bytes_demanded = o->t_demanded;
+  out->bytes_from_cache = o->t_cache;
+  out->bytes_prefetch_used = o->t_used;
+  out->bytes_sync = o->t_sync;
+  out->bytes_prefetch_wasted = o->t_wasted;
+  out->bytes_prefetch_pending = o->bytes_promoted - o->t_used - o->t_wasted;
+  out->requests_up = 0;
+  out->requests_channel = o->t_req_ch + o->promotions;
+  if (o->eval) {
+    double pr[4];
+    unsigned long long pn[2];
+    CK(cudaMemcpy(pr, o->pr_dev, sizeof pr, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(pn, o->pn_dev, sizeof pn, cudaMemcpyDeviceToHost));
+    out->mask_samples = pn[0];
+    out->set_samples = pn[1];
+    out->mask_precision = pn[0] ? pr[0] / pn[0] : 0.0;
+    out->mask_recall = pn[0] ? pr[1] / pn[0] : 0.0;
+    out->set_precision = pn[1] ? pr[2] / pn[1] : 0.0;
+    out->set_recall = pn[1] ? pr[3] / pn[1] : 0.0;
+  }
+  return FLOE_OK;
+}
+
+int floe_gpu_offload_set_eval(floe_gpu_offload *o, int enable, const floe_gpu_predictor *predictor,
+                              uint32_t count) {
+  if (!o) return fail(FLOE_ERR_INVALID, "offload_set_eval: null argument");
+  if (predictor && (predictor->experts != o->E || predictor->dh != o->dh ||
+                    count == 0 || count > o->E))
+    return fail(FLOE_ERR_INVALID, "offload_set_eval: predictor shape mismatch");
+  if (enable && !layer_fused(o->layers[0]))
+    return fail(FLOE_ERR_UNSUPPORTED, "offload_set_eval: needs the fused layer path");
+  if (enable && o->E > (uint32_t)floe_k::kMaxSlots)
+    return fail(FLOE_ERR_UNSUPPORTED, "offload_set_eval: at most %d experts", floe_k::kMaxSlots);
+  CK(cudaDeviceSynchronize());
+  if (enable && !o->ews) {
+    const uint32_t di = o->layers[0]->di;
+    if (int rc = floe_gpu_workspace_create(o->dh, di, o->E, &o->ews)) return rc;
+    CK(cudaMalloc(&o->pmask_dev, (size_t)o->E * di));
+    CK(cudaMalloc(&o->tmask_dev, (size_t)o->L * o->K * di));
+    CK(cudaMalloc(&o->u_dev, 4ull * o->L * o->dh));
+    CK(cudaMalloc(&o->pr_dev, 4 * sizeof(double)));
+    CK(cudaMalloc(&o->pn_dev, 2 * sizeof(unsigned long long)));
+    CK(cudaMalloc(&o->pexp_dev, 4ull * o->E));
+  }
+  if (enable) {
+    CK(cudaMemset(o->pr_dev, 0, 4 * sizeof(double)));
+    CK(cudaMemset(o->pn_dev, 0, 2 * sizeof(unsigned long long)));
+  }
+  o->eval = enable != 0;
+  o->pred = predictor;
+  o->pred_count = count;
   return FLOE_OK;
 }
 
