@@ -135,6 +135,13 @@ int floe_gpu_expert_destroy(floe_gpu_expert *e);
 int floe_gpu_expert_info(const floe_gpu_expert *e, floe_expert_info *info);
 /* Thresholds are per expert (ThresholdTable, core/src/model.cpp:237). */
 int floe_gpu_expert_set_threshold(floe_gpu_expert *e, float threshold);
+/* The quantized up projection in the reference packing (codes
+ * ceil(n*bits/8) bytes, f16 scales / zeros n/g each; quant.hpp:20-31) and
+ * the threshold, copied to host memory -- the inverse of expert_create's
+ * upload (record-cache / FLOQ writers).  Synchronous. */
+int floe_gpu_expert_download(const floe_gpu_expert *e, uint8_t *codes_host,
+                             uint16_t *scales_host, uint16_t *zeros_host,
+                             float *threshold);
 
 /* Placement of an expert's gate|down records: resident = 1 -> HBM,
  * 0 -> pinned host memory read in place over PCIe by the kernels.  Stream
@@ -326,6 +333,32 @@ int floe_gpu_offload_stats(floe_gpu_offload *o, floe_offload_stats *out, floe_st
  * predictor.cpp:reuse_mask_metrics / eval_sets offline scoring). */
 int floe_gpu_offload_set_eval(floe_gpu_offload *o, int enable, const floe_gpu_predictor *predictor,
                               uint32_t count);
+
+/* ------------------------------------------------------ record-cache file */
+/* The device-friendly counterpart of FLOQ (load_compressed,
+ * core/src/model.cpp:414-474, which stores gate/down as f32: 488 MB per
+ * Mixtral expert): "FLOR" keeps the up projection in the reference packing
+ * and every channel's gate|down record in the f16 pack_compact wire format
+ * (offload.cpp:27-53), 253 MB per expert, uploaded as-is.  Little-endian,
+ * every section 64-B aligned:
+ *   header (64 B): "FLOR", u32 version = 1, layers, experts, top_k, d_hidden,
+ *                  d_intermediate, bits, group_size, mixing_f16, 6 x u32 0
+ *   per layer:  router f32[E*dh]; mixing (f16 if mixing_f16 else f32)[dh*dh]
+ *   per expert: 64 B {f32 threshold, 15 x u32 0}; codes; f16 scales[n/g];
+ *               f16 zeros[n/g]; f16 records[di][2*dh]
+ * load creates the experts (flags: FLOE_VIEW_HOST_RECORDS keeps the records
+ * in pinned host memory, config 3) and the layers; the caller owns both and
+ * destroys the layers before the experts. */
+typedef struct floe_record_cache_info {
+  uint32_t layers, experts, top_k, d_hidden, d_intermediate, bits, group_size, mixing_f16;
+  uint64_t file_bytes;
+} floe_record_cache_info;
+int floe_gpu_record_cache_save(floe_gpu_layer *const *layers, uint32_t n_layers,
+                               const char *path);
+int floe_gpu_record_cache_info(const char *path, floe_record_cache_info *info);
+int floe_gpu_record_cache_load(const char *path, uint32_t flags,
+                               floe_gpu_layer **layers_out,
+                               floe_gpu_expert **experts_out);
 
 /* ----------------------------------------------------- counters / profile */
 /* Device-side running totals kept by a workspace: calls (K1 launches) and

@@ -80,6 +80,10 @@ _SIGS = {
     "floe_gpu_offload_decode_replay": (ct.c_int, [_P, _P, _P, _P, _P]),
     "floe_gpu_offload_stats": (ct.c_int, [_P, _P, _P]),
     "floe_gpu_offload_set_eval": (ct.c_int, [_P, ct.c_int, _P, _U32]),
+    "floe_gpu_expert_download": (ct.c_int, [_P, _P, _P, _P, _P]),
+    "floe_gpu_record_cache_save": (ct.c_int, [_P, _U32, ct.c_char_p]),
+    "floe_gpu_record_cache_info": (ct.c_int, [ct.c_char_p, _P]),
+    "floe_gpu_record_cache_load": (ct.c_int, [ct.c_char_p, _U32, _P, _P]),
     "floe_gpu_expert_set_resident": (ct.c_int, [_P, ct.c_int, _P]),
     "floe_gpu_expert_residency": (ct.c_int, [_P, _P, _P]),
     "floe_gpu_device_free": (ct.c_int, [_P]),
@@ -320,6 +324,25 @@ class GpuExpert:
     def set_threshold(self, t: float):
         _check(lib().floe_gpu_expert_set_threshold(self.handle, float(t)))
 
+    def download(self) -> dict:
+        """The quantized up projection in the reference packing and the threshold."""
+        n = self.d_hidden * self.d_intermediate
+        codes = np.empty((n * self.bits + 7) // 8, np.uint8)
+        scales = np.empty(n // self.group_size, np.uint16)
+        zeros = np.empty_like(scales)
+        t = ct.c_float()
+        _check(lib().floe_gpu_expert_download(self.handle, codes.ctypes.data, scales.ctypes.data,
+                                              zeros.ctypes.data, ct.byref(t)))
+        return dict(codes=codes, scales=scales, zeros=zeros, threshold=t.value)
+
+    @classmethod
+    def _adopt(cls, handle, d_hidden, d_intermediate, bits, group_size):
+        e = cls.__new__(cls)
+        e.handle = handle
+        e.d_hidden, e.d_intermediate = d_hidden, d_intermediate
+        e.bits, e.group_size = bits, group_size
+        return e
+
     def bytes_per_token(self, n_kept: int) -> int:
         """Algorithmic HBM bytes of one expert-token."""
         i = self.info()
@@ -440,6 +463,16 @@ class GpuLayer:
         self.d_intermediate = experts[0].d_intermediate
         self.n_experts, self.top_k = E, top_k
 
+    @classmethod
+    def _adopt(cls, handle, experts, d_hidden, top_k):
+        l = cls.__new__(cls)
+        l.handle = handle
+        l.experts = experts
+        l.d_hidden = d_hidden
+        l.d_intermediate = experts[0].d_intermediate
+        l.n_experts, l.top_k = len(experts), top_k
+        return l
+
     def close(self):
         if getattr(self, "handle", None):
             lib().floe_gpu_layer_destroy(self.handle)
@@ -470,6 +503,41 @@ def layer_forward(layer: GpuLayer, h, ws: Workspace, *, traced: bool = False, ou
         res["out"] = y
         return res
     return y
+
+
+class RecordCacheInfo(ct.Structure):
+    _fields_ = [("layers", _U32), ("experts", _U32), ("top_k", _U32), ("d_hidden", _U32),
+                ("d_intermediate", _U32), ("bits", _U32), ("group_size", _U32),
+                ("mixing_f16", _U32), ("file_bytes", ct.c_uint64)]
+
+
+def save_record_cache(path: str, layers) -> None:
+    """Write the layers as a FLOR record-cache file (include/floe_gpu.h): the
+    device-friendly counterpart of FLOQ, f16 gate|down records."""
+    arr = (ct.c_void_p * len(layers))(*[l.handle for l in layers])
+    _check(lib().floe_gpu_record_cache_save(arr, len(layers), str(path).encode()))
+
+
+def record_cache_info(path: str) -> dict:
+    i = RecordCacheInfo()
+    _check(lib().floe_gpu_record_cache_info(str(path).encode(), ct.byref(i)))
+    return {f: getattr(i, f) for f, _ in RecordCacheInfo._fields_}
+
+
+def load_record_cache(path: str, host_records: bool = False) -> list:
+    """A FLOR file -> GpuLayers (each owning its experts)."""
+    i = record_cache_info(path)
+    L, E = i["layers"], i["experts"]
+    lh = (ct.c_void_p * L)()
+    eh = (ct.c_void_p * (L * E))()
+    _check(lib().floe_gpu_record_cache_load(str(path).encode(),
+                                            FLOE_VIEW_HOST_RECORDS if host_records else 0, lh, eh))
+    layers = []
+    for l in range(L):
+        ex = [GpuExpert._adopt(eh[l * E + e], i["d_hidden"], i["d_intermediate"], i["bits"],
+                               i["group_size"]) for e in range(E)]
+        layers.append(GpuLayer._adopt(lh[l], ex, i["d_hidden"], i["top_k"]))
+    return layers
 
 
 class GpuPredictor:

@@ -785,6 +785,35 @@ int floe_gpu_expert_set_threshold(floe_gpu_expert *e, float t) {
   return FLOE_OK;
 }
 
+// The expert's quantized up projection in the reference packing (the tile
+// layout re-packed on the device) and its threshold: what a record-cache file
+// or a FLOQ writer needs.  Synchronous.
+int floe_gpu_expert_download(const floe_gpu_expert *e, uint8_t *codes_host, uint16_t *scales_host,
+                             uint16_t *zeros_host, float *threshold) {
+  if (!e || !codes_host || !scales_host || !zeros_host)
+    return fail(FLOE_ERR_INVALID, "expert_download: null argument");
+  if (int rc = require_device("expert_download")) return rc;
+  if (threshold) *threshold = e->threshold;
+  if (!e->fast) {
+    CK(cudaMemcpy(codes_host, e->host_desc.codes, e->code_bytes, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(scales_host, e->host_desc.scales, 2 * e->n_groups, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(zeros_host, e->host_desc.zeros, 2 * e->n_groups, cudaMemcpyDeviceToHost));
+    return FLOE_OK;
+  }
+  uint8_t *buf = nullptr;
+  const uint64_t nb = e->code_bytes + 4 * e->n_groups;
+  CK(cudaMalloc(&buf, nb));
+  uint16_t *sc = reinterpret_cast<uint16_t *>(buf + e->code_bytes), *zr = sc + e->n_groups;
+  floe_v2::untile_up<<<1184, 256>>>(e->host_desc.tiles, e->dh, e->di, e->g, buf, sc, zr);
+  cudaError_t ce = cudaGetLastError();
+  if (ce == cudaSuccess) ce = cudaMemcpy(codes_host, buf, e->code_bytes, cudaMemcpyDeviceToHost);
+  if (ce == cudaSuccess) ce = cudaMemcpy(scales_host, sc, 2 * e->n_groups, cudaMemcpyDeviceToHost);
+  if (ce == cudaSuccess) ce = cudaMemcpy(zeros_host, zr, 2 * e->n_groups, cudaMemcpyDeviceToHost);
+  cudaFree(buf);
+  if (ce != cudaSuccess) return fail(FLOE_ERR_CUDA, "expert_download: %s", cudaGetErrorString(ce));
+  return FLOE_OK;
+}
+
 // -------------------------------------------------------------- workspace --
 int floe_gpu_workspace_create(uint32_t dh, uint32_t di, uint32_t slots,
                               floe_gpu_workspace **out) {
@@ -2536,6 +2565,200 @@ int floe_gpu_predict_experts(const floe_gpu_predictor *p, const float *x, uint32
   floe_k::route_topk<<<1, 256, 0, S(stream)>>>(p->w + off * p->dh, p->b + off, x, p->experts,
                                                p->dh, count, 0, out, nullptr, nullptr, nullptr);
   CK_LAUNCH();
+  return FLOE_OK;
+}
+
+}  // extern "C"
+
+// --------------------------------------------------------- record cache ---
+// "FLOR" files (include/floe_gpu.h): the device image of a compressed model,
+// f16 records instead of FLOQ's f32 gate/down.
+namespace {
+constexpr uint32_t kFlorVersion = 1;
+constexpr uint64_t kFlorAlign = 64;
+uint64_t flor_pad(uint64_t n) { return (n + kFlorAlign - 1) & ~(kFlorAlign - 1); }
+
+struct FlorHeader {
+  char magic[4];
+  uint32_t version, layers, experts, top_k, dh, di, bits, g, mix_f16, reserved[6];
+};
+static_assert(sizeof(FlorHeader) == 64, "FLOR header is 64 bytes");
+
+struct File {
+  FILE *f = nullptr;
+  ~File() {
+    if (f) std::fclose(f);
+  }
+};
+
+uint64_t flor_expert_bytes(uint32_t dh, uint32_t di, uint32_t bits, uint32_t g) {
+  const uint64_t n = (uint64_t)dh * di;
+  return 64 + flor_pad((n * bits + 7) / 8) + 2 * flor_pad(2 * (n / g)) + flor_pad(4ull * dh * di);
+}
+uint64_t flor_layer_bytes(const FlorHeader &h) {
+  return flor_pad(4ull * h.experts * h.dh) + flor_pad((uint64_t)h.dh * h.dh * (h.mix_f16 ? 2 : 4)) +
+         h.experts * flor_expert_bytes(h.dh, h.di, h.bits, h.g);
+}
+
+int flor_read_header(const char *path, File &file, FlorHeader &h, uint64_t &size) {
+  if (!path) return fail(FLOE_ERR_INVALID, "record_cache: null path");
+  file.f = std::fopen(path, "rb");
+  if (!file.f) return fail(FLOE_ERR_INVALID, "record_cache: cannot open %s", path);
+  std::fseek(file.f, 0, SEEK_END);
+  size = (uint64_t)std::ftell(file.f);
+  std::fseek(file.f, 0, SEEK_SET);
+  if (std::fread(&h, sizeof h, 1, file.f) != 1) return fail(FLOE_ERR_INVALID, "record_cache: truncated file");
+  if (std::memcmp(h.magic, "FLOR", 4) != 0) return fail(FLOE_ERR_INVALID, "record_cache: bad magic");
+  if (h.version != kFlorVersion) return fail(FLOE_ERR_INVALID, "record_cache: unsupported version");
+  if (!h.layers || !h.experts || !h.top_k || h.top_k > h.experts || !h.dh || !h.di || !h.g ||
+      ((uint64_t)h.dh * h.di) % h.g)
+    return fail(FLOE_ERR_INVALID, "record_cache: bad shape");
+  if (size != 64 + (uint64_t)h.layers * flor_layer_bytes(h))
+    return fail(FLOE_ERR_INVALID, "record_cache: truncated file");
+  return FLOE_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int floe_gpu_record_cache_save(floe_gpu_layer *const *layers, uint32_t n_layers, const char *path) {
+  if (!layers || !n_layers || !path) return fail(FLOE_ERR_INVALID, "record_cache_save: bad arguments");
+  if (int rc = require_device("record_cache_save")) return rc;
+  const floe_gpu_layer *l0 = layers[0];
+  FlorHeader h{};
+  std::memcpy(h.magic, "FLOR", 4);
+  h.version = kFlorVersion;
+  h.layers = n_layers;
+  h.experts = l0->E;
+  h.top_k = l0->top_k;
+  h.dh = l0->dh;
+  h.di = l0->di;
+  const floe_gpu_expert *e0 = l0->experts[0];
+  h.bits = e0->bits;
+  h.g = e0->g;
+  h.mix_f16 = l0->mix_f16 ? 1 : 0;
+  for (uint32_t l = 0; l < n_layers; ++l) {
+    const floe_gpu_layer *ly = layers[l];
+    if (!ly || ly->E != h.experts || ly->top_k != h.top_k || ly->dh != h.dh || ly->di != h.di ||
+        (ly->mix_f16 ? 1u : 0u) != h.mix_f16)
+      return fail(FLOE_ERR_INVALID, "record_cache_save: layer %u shape differs", l);
+    for (const floe_gpu_expert *e : ly->experts)
+      if (e->bits != h.bits || e->g != h.g || e->up_only)
+        return fail(FLOE_ERR_INVALID, "record_cache_save: layer %u expert without records or "
+                                      "with another quantisation", l);
+  }
+  File file;
+  file.f = std::fopen(path, "wb");
+  if (!file.f) return fail(FLOE_ERR_INVALID, "record_cache_save: cannot open %s", path);
+  std::vector<uint8_t> buf;
+  auto put = [&](const void *p, uint64_t n) {  // one 64-B aligned section
+    static const uint8_t zero[kFlorAlign] = {};
+    if (n && std::fwrite(p, 1, n, file.f) != n) return false;
+    const uint64_t pad = flor_pad(n) - n;
+    return pad == 0 || std::fwrite(zero, 1, pad, file.f) == pad;
+  };
+  if (!put(&h, sizeof h)) return fail(FLOE_ERR_INVALID, "record_cache_save: write failed");
+  const uint64_t n = (uint64_t)h.dh * h.di, ng = n / h.g, code_bytes = (n * h.bits + 7) / 8;
+  for (uint32_t l = 0; l < n_layers; ++l) {
+    const floe_gpu_layer *ly = layers[l];
+    const uint64_t rb = 4ull * h.experts * h.dh, mb = (uint64_t)h.dh * h.dh * (h.mix_f16 ? 2 : 4);
+    buf.resize(std::max(rb, mb));
+    CK(cudaMemcpy(buf.data(), ly->router, rb, cudaMemcpyDeviceToHost));
+    if (!put(buf.data(), rb)) return fail(FLOE_ERR_INVALID, "record_cache_save: write failed");
+    CK(cudaMemcpy(buf.data(), ly->mixing, mb, cudaMemcpyDeviceToHost));
+    if (!put(buf.data(), mb)) return fail(FLOE_ERR_INVALID, "record_cache_save: write failed");
+    for (const floe_gpu_expert *e : ly->experts) {
+      uint32_t eh[16] = {};
+      float thr = 0.0f;
+      buf.resize(std::max<uint64_t>(code_bytes + 4 * ng, 4ull * n));
+      uint16_t *sc = reinterpret_cast<uint16_t *>(buf.data() + code_bytes);
+      if (int rc = floe_gpu_expert_download(e, buf.data(), sc, sc + ng, &thr)) return rc;
+      std::memcpy(&eh[0], &thr, 4);
+      if (!put(eh, sizeof eh) || !put(buf.data(), code_bytes) || !put(sc, 2 * ng) ||
+          !put(sc + ng, 2 * ng))
+        return fail(FLOE_ERR_INVALID, "record_cache_save: write failed");
+      CK(cudaMemcpy(buf.data(), e->resident ? (const void *)e->rec_dev : (const void *)e->rec_host,
+                    4ull * n, cudaMemcpyDefault));
+      if (!put(buf.data(), 4ull * n)) return fail(FLOE_ERR_INVALID, "record_cache_save: write failed");
+    }
+  }
+  return FLOE_OK;
+}
+
+int floe_gpu_record_cache_info(const char *path, floe_record_cache_info *info) {
+  if (!info) return fail(FLOE_ERR_INVALID, "record_cache_info: null argument");
+  File file;
+  FlorHeader h;
+  uint64_t size = 0;
+  if (int rc = flor_read_header(path, file, h, size)) return rc;
+  *info = floe_record_cache_info{h.layers, h.experts, h.top_k, h.dh, h.di, h.bits, h.g, h.mix_f16, size};
+  return FLOE_OK;
+}
+
+int floe_gpu_record_cache_load(const char *path, uint32_t flags, floe_gpu_layer **layers_out,
+                               floe_gpu_expert **experts_out) {
+  if (!layers_out || !experts_out) return fail(FLOE_ERR_INVALID, "record_cache_load: null argument");
+  File file;
+  FlorHeader h;
+  uint64_t size = 0;
+  if (int rc = flor_read_header(path, file, h, size)) return rc;
+  const uint64_t n = (uint64_t)h.dh * h.di, ng = n / h.g, code_bytes = (n * h.bits + 7) / 8;
+  std::vector<floe_gpu_layer *> made_l;
+  std::vector<floe_gpu_expert *> made_e;
+  auto undo = [&](int rc) {
+    for (floe_gpu_layer *l : made_l) floe_gpu_layer_destroy(l);
+    for (floe_gpu_expert *e : made_e) floe_gpu_expert_destroy(e);
+    return rc;
+  };
+  auto get = [&](void *p, uint64_t bytes) {  // one 64-B aligned section
+    if (bytes && std::fread(p, 1, bytes, file.f) != bytes) return false;
+    return std::fseek(file.f, (long)(flor_pad(bytes) - bytes), SEEK_CUR) == 0;
+  };
+  std::vector<float> router((size_t)h.experts * h.dh), mixing((size_t)h.dh * h.dh);
+  std::vector<uint16_t> mix16(h.mix_f16 ? (size_t)h.dh * h.dh : 0);
+  std::vector<uint8_t> up(code_bytes + 4 * ng);
+  std::vector<uint16_t> rec(2 * n);
+  for (uint32_t l = 0; l < h.layers; ++l) {
+    if (!get(router.data(), 4ull * router.size())) return undo(fail(FLOE_ERR_INVALID, "record_cache: truncated file"));
+    if (h.mix_f16) {
+      if (!get(mix16.data(), 2ull * mix16.size())) return undo(fail(FLOE_ERR_INVALID, "record_cache: truncated file"));
+      for (size_t i = 0; i < mix16.size(); ++i) {  // exact: f16 -> f32 (re-rounded identically on upload)
+        __half_raw r;
+        r.x = mix16[i];
+        mixing[i] = __half2float(__half(r));
+      }
+    } else if (!get(mixing.data(), 4ull * mixing.size())) {
+      return undo(fail(FLOE_ERR_INVALID, "record_cache: truncated file"));
+    }
+    std::vector<floe_gpu_expert *> ex(h.experts);
+    for (uint32_t e = 0; e < h.experts; ++e) {
+      uint32_t eh[16];
+      uint16_t *sc = reinterpret_cast<uint16_t *>(up.data() + code_bytes);
+      if (!get(eh, sizeof eh) || !get(up.data(), code_bytes) || !get(sc, 2 * ng) || !get(sc + ng, 2 * ng) ||
+          !get(rec.data(), 2ull * rec.size()))
+        return undo(fail(FLOE_ERR_INVALID, "record_cache: truncated file"));
+      floe_expert_host_view v{};
+      v.d_hidden = h.dh;
+      v.d_intermediate = h.di;
+      v.bits = h.bits;
+      v.group_size = h.g;
+      v.codes = up.data();
+      v.scales = sc;
+      v.zeros = sc + ng;
+      v.records_f16 = rec.data();
+      std::memcpy(&v.threshold, &eh[0], 4);
+      v.flags = flags & FLOE_VIEW_HOST_RECORDS;
+      if (int rc = floe_gpu_expert_create(&v, &ex[e])) return undo(rc);
+      made_e.push_back(ex[e]);
+    }
+    floe_layer_host_view lv{h.dh, h.experts, h.top_k, router.data(), mixing.data(), (int)h.mix_f16,
+                            ex.data()};
+    floe_gpu_layer *ly = nullptr;
+    if (int rc = floe_gpu_layer_create(&lv, &ly)) return undo(rc);
+    made_l.push_back(ly);
+  }
+  for (size_t i = 0; i < made_l.size(); ++i) layers_out[i] = made_l[i];
+  for (size_t i = 0; i < made_e.size(); ++i) experts_out[i] = made_e[i];
   return FLOE_OK;
 }
 

@@ -105,6 +105,45 @@ __global__ void tile_up(const uint8_t *codes, const uint16_t *scales, const uint
   }
 }
 
+// Inverse of tile_up: the tile layout -> the reference packing (codes,
+// scales, zeros; quant.hpp:20-31).  Groups of g > 64 elements appear in
+// several spans with the same scale|zero, written identically.
+__global__ void untile_up(const uint32_t *tiles, uint32_t dh, uint32_t di, uint32_t gsize,
+                          uint8_t *codes, uint16_t *scales, uint16_t *zeros) {
+  const uint32_t tb = tile_bytes(dh) / 4;
+  const uint32_t code_w = dh;
+  const uint64_t n = (uint64_t)tiles_per_expert(di) * tb;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t t = (uint32_t)(i / tb), q = (uint32_t)(i % tb);
+    uint32_t row, span, word;
+    const bool is_code = q < code_w;
+    if (is_code) {
+      const uint32_t k = q & 3, lane = (q >> 2) & 31, p = q >> 7;
+      row = (lane >> 2) + 8 * (k & 1);
+      span = 2 * p + (k >> 1);
+      word = lane & 3;
+    } else {
+      const uint32_t m = q - code_w;
+      const uint32_t k = m & 3, g = (m >> 2) & 7, p = m >> 5;
+      row = g + 8 * (k & 1);
+      span = 2 * p + (k >> 1);
+      word = 0;
+    }
+    const uint32_t c = t * kTileCh + row;
+    if (c >= di) continue;
+    const uint64_t e0 = (uint64_t)c * dh + 64u * span;
+    const uint32_t val = tiles[i];
+    if (is_code) {
+      *reinterpret_cast<uint32_t *>(codes + e0 / 4 + 4u * word) = val;
+    } else {
+      const uint64_t grp = e0 / gsize;
+      scales[grp] = (uint16_t)(val & 0xffffu);
+      zeros[grp] = (uint16_t)(val >> 16);
+    }
+  }
+}
+
 // dequantize (quant.cpp:104-120) from the tile layout: bit-exact (one fmaf of
 // an exact product, like the reference's mul-then-add).
 __global__ void dequant_tiled(const uint32_t *tiles, uint32_t dh, uint32_t di, float *out) {
