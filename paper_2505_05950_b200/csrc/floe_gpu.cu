@@ -20,6 +20,7 @@
 #include "../../include/floe_gpu.h"
 #include "floe_gen.cuh"
 #include "floe_v2.cuh"
+#include "floe_v3.cuh"
 #include "floe_tc.cuh"
 #include "floe_calib.cuh"
 #include "floe_blayer.cuh"
@@ -154,6 +155,7 @@ struct floe_gpu_workspace {
   uint32_t *kcount = nullptr;            // fused kernel: per-call kept counts per slot
   unsigned long long *pcnt = nullptr;    // fused kernel: published predicted partials
   unsigned long long *pf_tick = nullptr; // fused kernel: next-mixing prefetch tickets
+  unsigned long long *lbar = nullptr;    // multi-layer decode: end-of-layer arrivals (tickets)
   float *pred_partial = nullptr;         // fused kernel: [32][kMaxGrid] predicted partials
   unsigned long long *phase_ns = nullptr;  // diagnostics: [grid][8] phase marks
   uint32_t *sel = nullptr;
@@ -410,6 +412,16 @@ int launch_v2_dh(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) 
     return (d && std::strcmp(d, "1") == 0) ? 8u : 0u;
   }();
   a.debug = dbg;
+  static const uint32_t nsc_env = [] {
+    const char *p = std::getenv("FLOE_NSC");
+    return p ? (uint32_t)std::atoi(p) : 0u;
+  }();
+  static const uint32_t early_env = [] {
+    const char *p = std::getenv("FLOE_EARLY");
+    return p ? (uint32_t)std::atoi(p) : (uint32_t)V::kEarly;
+  }();
+  a.nsc_cap = nsc_env;
+  a.early = early_env;
 
   if (int rc = set_smem(V::fused<DH>, smem)) return rc;
   void *kargs[] = {&a};
@@ -859,6 +871,7 @@ int floe_gpu_workspace_create(uint32_t dh, uint32_t di, uint32_t slots,
   w->mix_done = reinterpret_cast<uint32_t *>(b + o_md);
   w->stats = reinterpret_cast<unsigned long long *>(b + o_st);
   w->bar = w->stats + 2;
+  w->lbar = w->stats + 3;
   w->tick = reinterpret_cast<unsigned long long *>(b + o_fk);
   w->y_flag = w->tick + 1;
   w->pcnt = w->tick + 3;
@@ -2200,7 +2213,125 @@ struct floe_gpu_model {
   float *buf = nullptr;                        // ping-pong [2][dh]
   float *hin = nullptr, *hout = nullptr;       // device staging [L][dh]
   float *pin_in = nullptr, *pin_out = nullptr; // pinned host staging [L][dh]
+  floe_v3::LayerDesc *ldesc = nullptr;         // [L] device: the multi-layer decode kernel
+  bool multi = false;                          // every layer fits floe_v3::decode
 };
+
+extern "C++" {
+namespace {
+
+// One launch of floe_v3::decode: the token through every layer of the model.
+template <int DH>
+int launch_v3_dh(const floe_gpu_model *m, floe_gpu_workspace *ws, const float *h, float *y,
+                 int replay, cudaStream_t st) {
+  namespace V = floe_v2;
+  namespace W = floe_v3;
+  const floe_gpu_layer *l0 = m->layers[0];
+  const uint32_t G = std::min<uint32_t>((uint32_t)device_info().sm, V::kMaxGrid);
+  const uint32_t NT = l0->top_k * V::tiles_per_expert(l0->di);
+  const uint32_t max_tiles = std::max<uint32_t>(1, (NT + G - 1) / G);
+  static int optin = [] {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0);
+    return v;
+  }();
+  static size_t static_smem = [] {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, W::decode<DH>);
+    return fa.sharedSizeBytes;
+  }();
+  const uint32_t ns = W::ring_stages(DH);
+  const uint32_t smem = V::smem_layout(DH, ns, max_tiles, G).total;
+  if ((int64_t)smem + (int64_t)static_smem + 1024 > (int64_t)optin)
+    return fail(FLOE_ERR_UNSUPPORTED, "decode: shared memory too small for the ring");
+  W::DecodeArgs a{};
+  a.layers = m->ldesc;
+  a.n_layers = (uint32_t)m->layers.size();
+  a.n_experts = l0->E;
+  a.top_k = l0->top_k;
+  a.di = l0->di;
+  a.h = h;
+  a.y = y;
+  a.buf = m->buf;
+  a.replay = replay;
+  a.u = ws->u;
+  a.partial = ws->mix_partial;
+  a.pred_partial = ws->pred_partial;
+  a.pcnt = ws->pcnt;
+  a.bar = ws->bar;
+  a.lbar = ws->lbar;
+  a.stats = ws->stats;
+  a.place_acc = nullptr;
+  a.phase_ns = ws->phase_ns;
+  static const uint32_t trace_layer = [] {
+    const char *p = std::getenv("FLOE_TRACE_LAYER");
+    return p ? (uint32_t)std::atoi(p) : 0xffffffffu;
+  }();
+  a.trace_layer = trace_layer == 0xffffffffu ? a.n_layers - 1 : trace_layer;
+  a.ns = ns;
+  a.max_tiles = max_tiles;
+  static const uint32_t dbg = [] {
+    const char *d = std::getenv("FLOE_TEST_MISPREDICT");
+    return (d && std::strcmp(d, "1") == 0) ? 8u : 0u;
+  }();
+  static const uint32_t dbg_flags = [] {
+    const char *d = std::getenv("FLOE_DEBUG_FLAGS");
+    return d ? (uint32_t)std::atoi(d) : 0u;
+  }();
+  a.debug = dbg | dbg_flags;
+  if (int rc = set_smem(W::decode<DH>, smem)) return rc;
+  void *kargs[] = {&a};
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(G);
+  cfg.blockDim = dim3(V::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  // Same launch as floe_v2::fused (see launch_v2_dh): one CTA per SM, PDL,
+  // CTA pairs; FLOE_COOP=1 keeps the cooperative launch (no pairs).
+  static const bool coop_env = [] {
+    const char *p = std::getenv("FLOE_COOP");
+    if (p) return std::strcmp(p, "0") != 0;
+    return std::getenv("CUDA_MPS_ACTIVE_THREAD_PERCENTAGE") != nullptr;
+  }();
+  static const bool pairs_env = [] {
+    const char *p = std::getenv("FLOE_PAIRS");
+    return !(p && std::strcmp(p, "0") == 0);
+  }();
+  cudaLaunchAttribute attr[3];
+  uint32_t na = 0;
+  if (coop_env) {
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na++].val.cooperative = 1;
+  } else if (!ws->profiling) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  a.paired = (pairs_env && !coop_env && (G % 2) == 0) ? 1 : 0;
+  if (a.paired) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na++].val.clusterDim.z = 1;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  StageScope prof(ws, kStageFused, st);
+  const cudaError_t e = cudaLaunchKernelExC(&cfg, reinterpret_cast<const void *>(W::decode<DH>), kargs);
+  if (e != cudaSuccess) return fail(FLOE_ERR_CUDA, "decode launch failed: %s", cudaGetErrorString(e));
+  CK_LAUNCH();
+  return FLOE_OK;
+}
+
+bool multi_env() {
+  static const bool on = [] {
+    const char *p = std::getenv("FLOE_MULTI");
+    return !(p && std::strcmp(p, "0") == 0);
+  }();
+  return on;
+}
+
+}  // namespace
+}  // extern "C++"
 
 extern "C" {
 
@@ -2218,6 +2349,26 @@ int floe_gpu_model_create(floe_gpu_layer *const *layers, uint32_t n_layers,
   m->dh = layers[0]->dh;
   const size_t v = 4ull * m->dh * n_layers;
   CK(cudaMalloc(&m->buf, 8ull * m->dh));
+  // the multi-layer decode kernel: fast-path layers of one shape, f16 mixing,
+  // at most 8 experts
+  const floe_gpu_layer *l0 = layers[0];
+  bool multi = (l0->dh == 4096 || l0->dh == 2048) && l0->E <= (uint32_t)floe_v3::kMaxE &&
+               l0->top_k <= (uint32_t)floe_k::kMaxSlots;
+  for (uint32_t l = 0; l < n_layers && multi; ++l) {
+    const floe_gpu_layer *ly = layers[l];
+    multi = ly->fast && ly->mix_f16 && ly->router_pred && ly->dh == l0->dh && ly->di == l0->di &&
+            ly->E == l0->E && ly->top_k == l0->top_k;
+  }
+  if (multi) {
+    std::vector<floe_v3::LayerDesc> ld(n_layers);
+    for (uint32_t l = 0; l < n_layers; ++l)
+      ld[l] = {static_cast<const __half *>(layers[l]->mixing), layers[l]->router,
+               layers[l]->router_pred, layers[l]->table};
+    CK(cudaMalloc(&m->ldesc, sizeof(floe_v3::LayerDesc) * n_layers));
+    CK(cudaMemcpy(m->ldesc, ld.data(), sizeof(floe_v3::LayerDesc) * n_layers,
+                  cudaMemcpyHostToDevice));
+    m->multi = true;
+  }
   CK(cudaMalloc(&m->hin, v));
   CK(cudaMalloc(&m->hout, v));
   CK(cudaMallocHost(&m->pin_in, v));
@@ -2230,6 +2381,7 @@ int floe_gpu_model_destroy(floe_gpu_model *m) {
   if (!m) return FLOE_OK;
   cudaDeviceSynchronize();
   cudaFree(m->buf);
+  cudaFree(m->ldesc);
   cudaFree(m->hin);
   cudaFree(m->hout);
   cudaFreeHost(m->pin_in);
@@ -2248,6 +2400,11 @@ int floe_gpu_model_decode(floe_gpu_model *m, floe_gpu_workspace *ws, const float
   if (!m || !ws || !h || !y) return fail(FLOE_ERR_INVALID, "model_decode: null argument");
   cudaStream_t st = S(stream);
   const uint32_t L = (uint32_t)m->layers.size();
+  if (m->multi && multi_env()) {  // one launch for the whole token
+    if (int rc = check_ws("model_decode", ws, m->dh, m->layers[0]->di, m->layers[0]->top_k)) return rc;
+    return m->dh == 4096 ? launch_v3_dh<4096>(m, ws, h, y, replay, st)
+                         : launch_v3_dh<2048>(m, ws, h, y, replay, st);
+  }
   const float *in = h;
   for (uint32_t l = 0; l < L; ++l) {
     const floe_gpu_layer *ly = m->layers[l];

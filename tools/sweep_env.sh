@@ -1,6 +1,7 @@
-# Layer/expert step time under a few environment settings (one short bench each).
+# Sweep runtime knobs of the fused kernel: layer us (32-layer decode, steady state) per setting.
+# usage: bash tools/sweep_env.sh "FLOE_NSC=8" "FLOE_NSC=12 FLOE_EARLY=4" ...
 for cfg in "$@"; do
-  env $cfg timeout 300 python bench.py --steps 200 --warmup 10 --no-cpu-baseline > gpurun_out/sweep.json 2> /dev/null
-  python -c "
-import json; d=json.load(open('gpurun_out/sweep.json')); print('$cfg', 'LAYER us', round(d['ms_per_step']*1e3,2), 'EXPERT us', d['expert_ffn']['us_per_expert_token'])"
+  r=$(env $cfg timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-offload 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print('us/layer %.2f frac %.3f' % (d['layer']['us_per_layer'], d['roofline']['frac']))")
+  echo "$cfg -> $r"
 done
