@@ -87,11 +87,18 @@ __device__ __forceinline__ void poll_until(const unsigned long long *p, unsigned
   }
 }
 
+// Arrive with release semantics (the CTA's writes before the preceding
+// bar.sync are ordered before the arrival: release is cumulative) and return
+// the previous count.
+__device__ __forceinline__ unsigned long long atom_add_release(unsigned long long *p) {
+  unsigned long long old;
+  asm volatile("atom.release.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(p) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ void grid_barrier(unsigned long long *bar, uint32_t G) {
-  __threadfence();
-  const unsigned long long old = atomicAdd(bar, 1ull);
-  poll_until(bar, (old / G + 1) * G, "grid barrier", (uint32_t)(old % G));
-  __threadfence();
+  const unsigned long long old = atom_add_release(bar);
+  poll_until(bar, (old / G + 1) * G, "grid barrier", (uint32_t)(old % G));  // acquire loads
 }
 
 // Item j of chunk c holds rows 2 p, 2 p + 1 of the chunk, p = (j + 5 c) mod
@@ -326,22 +333,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode(const DecodeArgs a) {
       mark(16);
       asm volatile("fence.proxy.async.global;" ::: "memory");  // u: generic-proxy writes
       mark(35);
-      // the K1 ring covers the record ring's bytes: every record-ring item
-      // issued so far must have been released
-      unsigned long long wmax = 0, wk = 0, ws_ = 0;
-      for (uint32_t s = 0; s < nsC && s < K; ++s) {
-        const uint32_t k = s + ((K - 1 - s) / nsC) * nsC;
-        const unsigned long long w0 = gtime();
-        mbar_spin(&emptyC[s], (k / nsC) & 1u, (8u << 28) | s);
-        const unsigned long long w1 = gtime() - w0;
-        if (w1 > wmax) { wmax = w1; wk = k; ws_ = s; }
-      }
-      if (a.phase_ns && l == a.trace_layer) {
-        a.phase_ns[b * kTraceSlots + 48] = wmax;
-        a.phase_ns[b * kTraceSlots + 49] = ws_;
-        a.phase_ns[b * kTraceSlots + 50] = K - wk;
-        a.phase_ns[b * kTraceSlots + 51] = tau_s;
-      }
+      // The K1 ring covers the record ring's bytes.  Every record-ring item
+      // issued so far has been released: the consumers released the last
+      // ones (this layer's mixing items, or the previous layer's records)
+      // before the bar.sync that precedes t0's arrival on bar1.
       mark(32);
       floe_ptx::mbar_arrive_expect_tx(&ubar, 4u * DH);
       floe_ptx::bulk_g2s(hs, a.u, 4u * DH, &ubar);
@@ -392,7 +387,15 @@ __global__ void __launch_bounds__(kThreads, 1) decode(const DecodeArgs a) {
       mbar_spin(&listbar, P, 12u << 28);
       const uint32_t n_own = n_list;
       const uint32_t Pf = min(n_own, nsC);
+      const uint32_t rdepth = (a.debug >> 5) & 15u;  // experiment: records in flight
+      auto depth_wait = [&](uint32_t k) {
+        if (rdepth && k >= rdepth) {
+          const uint32_t j = k - rdepth;
+          floe_ptx::mbar_wait(&emptyC[j % nsC], (j / nsC) & 1u, (24u << 28) | j);
+        }
+      };
       auto own_item = [&](uint32_t k) {
+        depth_wait(K + k);
         const uint32_t f = lf[k], s2 = (f >> kSlotShift) & 0x7fu, c = f & 0xffffffu;
         issueC(K + k, rec_s[s2] + (size_t)c * 2 * DH, lv[k] * w_s[s2], l2_stream);
       };
@@ -423,6 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode(const DecodeArgs a) {
           const uint32_t f = floe_ptx::ld_cluster_u32(floe_ptx::mapa(&lf[pfirst + k], pr));
           const float v = __uint_as_float(floe_ptx::ld_cluster_u32(floe_ptx::mapa(&lv[pfirst + k], pr)));
           const uint32_t s2 = (f >> kSlotShift) & 0x7fu, c = f & 0xffffffu;
+          depth_wait(K + own + k);
           issueC(K + own + k, rec_s[s2] + (size_t)c * 2 * DH, v * w_s[s2], l2_stream);
         }
         floe_ptx::mbar_arrive_remote(floe_ptx::mapa(&donebar, pr));
@@ -504,8 +508,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode(const DecodeArgs a) {
         __syncwarp();
       }
       if (lane == 0) {
-        if (tau < NCH) __threadfence();
-        const unsigned long long old = atomicAdd(a.pcnt, 1ull);
+        const unsigned long long old = atom_add_release(a.pcnt);
         target = (old / G + 1) * G;
         poll_until(a.pcnt, target, "prediction", l);
       }
@@ -681,9 +684,25 @@ __global__ void __launch_bounds__(kThreads, 1) decode(const DecodeArgs a) {
     // ============================ phase A ============================
     if (chunk != 0xffffffffu) {
       const uint32_t r0 = chunk * kChunkRows;
-      floe_ptx::mbar_wait(&hbar, owned & 1u, 3u << 28);
-      floe_ptx::mbar_wait(&rbar, owned & 1u, 9u << 28);
+      // warp 0 waits for h, the router slices and the prefetched items, one
+      // lane per barrier (an mbarrier wait costs ~0.1 us of latency: in
+      // parallel, not in sequence), then hands them to every consumer warp
+      constexpr uint32_t PRE = (uint32_t)kChunkItems < nsC ? (uint32_t)kChunkItems : nsC;
+      if (warp == 0 && lane < 2 + PRE) {
+        uint64_t *bar;
+        uint32_t par;
+        if (lane < 2) {
+          bar = lane == 0 ? &hbar : &rbar;
+          par = owned & 1u;
+        } else {
+          const uint32_t k = K + lane - 2;
+          bar = &fullC[k % nsC];
+          par = (k / nsC) & 1u;
+        }
+        mbar_spin(bar, par, (3u << 28) | lane);  // all lanes at once
+      }
       ++owned;
+      cbar();
       mark(7);
       // u rows: group g takes items g, g + 2, ...; thread gt owns elements
       // [EPT2 gt, EPT2 gt + EPT2) of both rows of an item
@@ -700,15 +719,23 @@ __global__ void __launch_bounds__(kThreads, 1) decode(const DecodeArgs a) {
       uint32_t k = K + grp;
       uint32_t stg = k % nsC, ph = (k / nsC) & 1u;
       for (uint32_t i0 = 0; i0 < (uint32_t)kChunkItems / 2; i0 += 2, ++batch) {
+        // one thread of the group waits for both items (the other warps do
+        // no mbarrier operation: each costs ~0.1 us of latency), the group
+        // barrier hands them over, and after the reduction barrier the same
+        // thread releases both stages for the group
         float dv[4];
+        const uint32_t stg0 = stg, ph0 = ph;
+        const uint32_t stg1 = stg0 + 2 >= nsC ? stg0 + 2 - nsC : stg0 + 2;
+        const uint32_t ph1 = stg0 + 2 >= nsC ? ph0 ^ 1u : ph0;
+        if (grp + 2 * i0 + 2 >= PRE) {  // an item past the prefetched ones
+          if (gw == 0 && lane < 2) mbar_spin(&fullC[lane ? stg1 : stg0], lane ? ph1 : ph0, (4u << 28) | lane);
+          gbar(grp);
+        }
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
-          if (!(a.debug & 1u)) floe_ptx::mbar_wait(&fullC[stg], ph, (4u << 28) | r);
           const Vec *rec = reinterpret_cast<const Vec *>(ring + stg * REC_B);
           const Vec g0 = rec[2 * gt], g1 = rec[2 * gt + 1];
           const Vec d0 = rec[512 + 2 * gt], d1 = rec[512 + 2 * gt + 1];
-          __syncwarp();
-          if (lane == 0) mbar_arrive1(&emptyC[stg]);
           const __half2 *p0 = reinterpret_cast<const __half2 *>(&g0);
           const __half2 *p1 = reinterpret_cast<const __half2 *>(&g1);
           const __half2 *q0 = reinterpret_cast<const __half2 *>(&d0);
@@ -731,7 +758,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode(const DecodeArgs a) {
         }
         warp_reduce_t(dv, std::integral_constant<int, 4>{});
         if ((lane & 7) == 0) red[grp][batch & 1][gw][lane >> 3] = dv[0];
-        if (!(a.debug & 2u)) gbar(grp);
+        gbar(grp);
+        if (gw == 0 && lane == 0) {  // every warp of the group has read both items
+          floe_ptx::mbar_arrive_cnt(&emptyC[stg0], 8);
+          floe_ptx::mbar_arrive_cnt(&emptyC[stg1], 8);
+        }
         float s = red[grp][batch & 1][lane & 7][lane >> 3];
         s += __shfl_xor_sync(0xffffffffu, s, 4);
         s += __shfl_xor_sync(0xffffffffu, s, 2);
@@ -981,8 +1012,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode(const DecodeArgs a) {
     if (l + 1 == a.n_layers) break;
     if (t == 0) {
       n_list = 0u;
-      __threadfence();  // this CTA's y adds before its arrival
-      const unsigned long long old = atomicAdd(a.lbar, 1ull);
+      const unsigned long long old = atom_add_release(a.lbar);  // after this CTA's y adds
       const uint32_t tau = (uint32_t)(old % G);
       tau_s = tau;
       mark_prev(29);
@@ -990,7 +1020,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode(const DecodeArgs a) {
       floe_ptx::mbar_arrive(&tickbar);
       if (tau < NCH) {  // a chunk owner needs h: wait for every CTA
         if (tau != G - 1) poll_until(a.lbar, (old / G + 1) * G, "layer barrier", tau);
-        __threadfence();
       }
       mark_prev(30);
       floe_ptx::mbar_arrive(&lpass);

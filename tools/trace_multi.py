@@ -62,9 +62,6 @@ def main():
     n = T[:, :, 9].ravel()
     print(f"  kept records per CTA: mean {n.mean():.1f} min {n.min()} max {n.max()}")
     by_ticket(T, t0)
-    w = T[:, :, 48].ravel() / 1e3
-    print(f"  C->K1 slowest wait: mean {w.mean():.2f} us; stage hist {np.bincount(T[:, :, 49].ravel(), minlength=12)}")
-    print(f"  K - k of slowest: {np.bincount(T[:, :, 50].ravel())}")
     own = T[:, :, 28].ravel() < 128
     dA = ((T[:, :, 14] - T[:, :, 7]) / 1e3)  # h in -> A items done, per step and CTA
     ok = T[:, :, 14] > 0
@@ -74,7 +71,6 @@ def main():
     for st in range(T.shape[0]):
         print("   step", st, "slow CTAs:", sorted(np.nonzero(slow[st])[0].tolist())[:40])
         print("          their SMs:", sorted(sm[st][slow[st]].tolist())[:40])
-    print(f"  chunk owners: wait {w[own].mean():.2f}  chunkless: {w[~own].mean():.2f}")
 
 
 def by_ticket(T, t0):
