@@ -353,11 +353,15 @@ def run_ours(args, rank, world, local):
         torch.cuda.synchronize()
         wall_s = time.perf_counter() - t0
     clocks = clk.summary()
-    cnt = ws.read_counters()  # fused launches and kept channels in the timed region
+    cnt = ws.read_counters()  # layers decoded and kept channels in the timed region
     max_ms = max_over_ranks(my_ms, world, torch.device("cuda", local))
     value = whole_job_value(world, args.steps, max_ms)
-    launches = int(cnt["calls"])
-    kept_per_layer = cnt["kept"] / max(launches, 1)
+    layer_calls = int(cnt["calls"])
+    kept_per_layer = cnt["kept"] / max(layer_calls, 1)
+    # one floe_v3::decode launch per token (every layer), or one fused launch per
+    # layer when FLOE_MULTI=0
+    multi = model.multi_layer
+    launches = args.steps if multi else layer_calls
     # algorithmic bytes of one layer launch: f16 mixing + router +
     # 2 experts' up codes/meta + the kept records + the vectors
     layer_bytes = (MIX_BYTES + E * DH * 4 + TOPK * (CODE_BYTES + META_BYTES) +
@@ -374,18 +378,26 @@ def run_ours(args, rank, world, local):
     ws.set_profiling(False)
     fused = prof.get("fused", {"ms": 0.0, "launches": 0})
     iso_us = 1e3 * fused["ms"] / max(fused["launches"], 1)
+    # dram bytes per launch from the committed ncu --set full capture of the same
+    # kernel (profiles/ncu_traffic.json, written by tools/summarize_ncu.py)
     traffic = None
     tf = ROOT / "profiles" / "ncu_traffic.json"
+    kname = "decode" if multi else "fused"
     if tf.exists():
-        traffic = json.loads(tf.read_text()).get("fused")
-    roofline = {"bound": "hbm", "kernel": "floe_v2::fused<4096> (layer mode)",
+        traffic = json.loads(tf.read_text()).get(kname)
+    per_launch = L if multi else 1
+    roofline = {"bound": "hbm",
+                "kernel": ("floe_v3::decode<4096> (every layer of the token in one launch)"
+                           if multi else "floe_v2::fused<4096> (layer mode)"),
                 "achieved": round(achieved, 1), "peak": hbm_peak, "peak_kind": peak_kind,
                 "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
-                "algorithmic_bytes_per_launch": int(layer_bytes),
-                "avg_launch_us": round(layer_us, 3),
-                "avg_launch_us_note": ("timed region / launches: one launch per layer, "
-                                       "back to back with programmatic dependent launch"),
-                "isolated_launch_us": round(iso_us, 3)}
+                "traffic_source": f"profiles/ncu_traffic.json[{kname}] (ncu --set full, per launch)",
+                "algorithmic_bytes_per_launch": int(layer_bytes * per_launch),
+                "avg_launch_us": round(layer_us * per_launch, 3),
+                "avg_launch_us_note": ("CUDA events over the timed region on the launching "
+                                       "stream / launches"),
+                "isolated_launch_us": round(iso_us, 3),
+                "isolated_launch_note": "one launch alone (no programmatic dependent launch)"}
 
     # ---------------- config 1 (+ config-4 expert level) ----------------
     expert_ffn = run_expert(fb, torch, args, stream, hbm_peak)

@@ -398,6 +398,10 @@ int floe_gpu_model_destroy(floe_gpu_model *m);
  * the previous one, as a chained decode does.  Stream-ordered. */
 int floe_gpu_model_decode(floe_gpu_model *m, floe_gpu_workspace *ws, const float *h_dev,
                           float *y_dev, int replay, floe_stream_t stream);
+/* 1 if decode runs every layer of a token in ONE launch of the multi-layer
+ * kernel (fast-path layers of one shape, f16 mixing, <= 8 experts; FLOE_MULTI=0
+ * turns it off), 0 if it launches the fused kernel once per layer. */
+int floe_gpu_model_multi_layer(const floe_gpu_model *m);
 /* The same from/to HOST memory through pinned staging; synchronises `stream`. */
 int floe_gpu_model_decode_host(floe_gpu_model *m, floe_gpu_workspace *ws, const float *h_host,
                                float *y_host, int replay, floe_stream_t stream);

@@ -122,6 +122,7 @@ _SIGS = {
     "floe_gpu_layer_forward_batched": (ct.c_int, [_P, _P, _P, _U32, _P, _P]),
     "floe_gpu_model_create": (ct.c_int, [_P, _U32, ct.POINTER(_P)]),
     "floe_gpu_model_destroy": (ct.c_int, [_P]),
+    "floe_gpu_model_multi_layer": (ct.c_int, [_P]),
     "floe_gpu_model_decode": (ct.c_int, [_P, _P, _P, _P, ct.c_int, _P]),
     "floe_gpu_model_decode_host": (ct.c_int, [_P, _P, _P, _P, ct.c_int, _P]),
     "floe_gpu_calib_create": (ct.c_int, [_U32, _U32, _U32, _U32, ct.c_uint64, ct.c_uint64,
@@ -664,6 +665,7 @@ class Offload:
         self.handle = h.value
         self.layers = layers
         self.d_hidden = layers[0].d_hidden
+        self.multi_layer = bool(lib().floe_gpu_model_multi_layer(self.handle))
 
     def close(self):
         if getattr(self, "handle", None):
@@ -718,6 +720,7 @@ class GpuModel:
         self.handle = h.value
         self.layers = layers
         self.d_hidden = layers[0].d_hidden
+        self.multi_layer = bool(lib().floe_gpu_model_multi_layer(self.handle))
 
     def close(self):
         if getattr(self, "handle", None):

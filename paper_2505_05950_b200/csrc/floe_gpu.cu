@@ -2418,6 +2418,10 @@ int floe_gpu_model_decode(floe_gpu_model *m, floe_gpu_workspace *ws, const float
   return FLOE_OK;
 }
 
+int floe_gpu_model_multi_layer(const floe_gpu_model *m) {
+  return m && m->multi && multi_env() ? 1 : 0;
+}
+
 int floe_gpu_model_decode_host(floe_gpu_model *m, floe_gpu_workspace *ws, const float *h_host,
                                float *y_host, int replay, floe_stream_t stream) {
   if (!m || !ws || !h_host || !y_host) return fail(FLOE_ERR_INVALID, "model_decode: null argument");
