@@ -1,5 +1,5 @@
 """Profiling workload for the multi-layer decode kernel (floe_v3::decode): an
-8-layer model, `steps` replay decodes (ncu -k regex:decode -s 2 -c 1)."""
+L-layer model (argv[1], default 8), `steps` replay decodes (ncu -k regex:decode -s 2 -c 1)."""
 import sys
 from pathlib import Path
 
@@ -13,7 +13,7 @@ def main():
 
     import paper_2505_05950_b200 as fb
     torch.cuda.set_device(0)
-    L = 8
+    L = int(sys.argv[1]) if len(sys.argv) > 1 else 8
     layers, _ = bench.build_model(fb, torch, L)
     model = fb.GpuModel(layers)
     ws = fb.Workspace(bench.DH, bench.DI, bench.TOPK)
