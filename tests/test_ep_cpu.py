@@ -46,7 +46,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, split=None):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     sys.path.insert(0, str(ROOT))
     import torch
@@ -57,6 +57,8 @@ def _worker(rank, world, port, q):
     try:
         O, experts, router, mixing, tokens = _model()
         lo, hi = T * rank // world, T * (rank + 1) // world  # this rank's tokens
+        if split is not None:  # uneven shards, possibly empty
+            lo, hi = split[rank]
         y, sel, w = ep.ep_moe_layer(torch.from_numpy(tokens[lo:hi]), torch.from_numpy(router),
                                     torch.from_numpy(mixing), K, _expert_fn(O, experts), E)
         q.put((rank, y.numpy(), sel.numpy()))
@@ -64,7 +66,8 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_ep_two_ranks_equals_one_rank():
+@pytest.mark.parametrize("split", [None, ((0, 0), (0, T))], ids=["even", "rank0-empty"])
+def test_ep_two_ranks_equals_one_rank(split):
     import torch
     import torch.multiprocessing as mp
 
@@ -75,7 +78,7 @@ def test_ep_two_ranks_equals_one_rank():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, split)) for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:

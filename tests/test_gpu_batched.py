@@ -132,6 +132,34 @@ def test_expert_forward_batched_matches_per_token(fb, torch, mixtral_full, B):
     _check(ref_e.up_q, 4096, X, V, [0, B - 1])
 
 
+@pytest.mark.parametrize("B", [16, 33])
+def test_expert_forward_batched_token_scales(fb, torch, mixtral_full, B):
+    """The tcgen05 gate/down GEMMs split x and the coefficients into f16 hi+lo
+    with a per-token power-of-two scale: tokens x300 (coefficients ~1e5, past
+    f16's range unscaled) and x1e-3 (against a threshold scaled the same way,
+    coefficients in f16's subnormals unscaled) equal the single-token path."""
+    ref_e, e = mixtral_full
+    q = ref_e.up_q
+    X = np.stack([O.seeded_input(4096, 300 + t) for t in range(B)])
+    X[1] *= 300.0
+    X[4] *= 300.0
+    ws = fb.Workspace(4096, 14336)
+    Y = fb.expert_forward_batched(e, torch.from_numpy(X).cuda()).cpu().numpy()
+    for t in (0, 1, 4, B - 1):
+        y1 = fb.expert_forward_sparse(e, torch.from_numpy(X[t]).cuda(), ws).cpu().numpy()
+        assert O.rel_l2(Y[t], y1) <= 1e-4, t
+    small = fb.GpuExpert(4096, 14336, 2, 64, q.codes, q.scales, q.zeros, gate=ref_e.gate,
+                         down=ref_e.down_t, threshold=ref_e.threshold * 1e-3)
+    Xs = X * 1e-3
+    Xs[1] = X[1] / 300.0 * 1e-3
+    Xs[4] = X[4] / 300.0 * 1e-3
+    Ys = fb.expert_forward_batched(small, torch.from_numpy(Xs).cuda()).cpu().numpy()
+    for t in (0, 2, B - 1):
+        y1 = fb.expert_forward_sparse(small, torch.from_numpy(Xs[t]).cuda(), ws).cpu().numpy()
+        assert np.linalg.norm(y1) > 0, t
+        assert O.rel_l2(Ys[t], y1) <= 1e-4, t
+
+
 def test_expert_forward_batched_small_and_edge(fb, torch):
     """Ragged shape, a threshold that keeps nothing for some tokens, and a
     token with a non-finite input (its NaN v keeps every channel, as the

@@ -9,12 +9,15 @@ from oracle import oracle as O
 pytestmark = pytest.mark.gpu
 
 
-def test_ep_layer_matches_fused_layer_per_token():
+@pytest.mark.parametrize("T", [96, 5], ids=["batched", "few-tokens-per-expert"])
+def test_ep_layer_matches_fused_layer_per_token(T):
+    """T = 96: ~48 tokens per expert (batched forward); T = 5: 1-3 tokens per
+    expert, which go one by one through the fused single-expert kernel."""
     import torch
 
     import paper_2505_05950_b200 as fb
     from paper_2505_05950_b200 import ep
-    dh, di, E, K, T = 2048, 512, 4, 2, 96
+    dh, di, E, K = 2048, 512, 4, 2
     rng = np.random.default_rng(9)
     experts = []
     for e in range(E):
@@ -35,4 +38,4 @@ def test_ep_layer_matches_fused_layer_per_token():
         if np.array_equal(tr["experts"].cpu().numpy().astype(np.int64), sel[t].cpu().numpy()):
             agree += 1
             assert O.rel_l2(y[t].cpu().numpy(), tr["out"].cpu().numpy()) <= 1e-3, t
-    assert agree >= T - 2
+    assert agree >= T - 2 if T > 10 else agree >= T - 1
