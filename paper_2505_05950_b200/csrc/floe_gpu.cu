@@ -1168,9 +1168,11 @@ int floe_gpu_qgemv_channels_batched(const floe_gpu_expert *e, const float *x, ui
   float *xs = reinterpret_cast<float *>(scratch + o_xs);
   uint8_t *xl = scratch + o_xl;
   floe_tc::token_scale<<<n_tokens, 256, 0, st>>>(x, e->dh, invS, Sv);
-  CK_LAUNCH();
   floe_tc::token_limbs<<<spans, 256, 0, st>>>(x, e->dh, n_tokens, Sv, xl, xs);
-  CK_LAUNCH();
+  if (cudaError_t le = cudaGetLastError(); le != cudaSuccess) {
+    cudaFreeAsync(scratch, st);
+    return fail(FLOE_ERR_CUDA, "qgemv_channels_batched: launch failed: %s", cudaGetErrorString(le));
+  }
   floe_tc::BatchedArgs a{};
   a.tiles = e->host_desc.tiles;
   a.dh = e->dh;
@@ -2274,11 +2276,7 @@ int launch_v3_dh(const floe_gpu_model *m, floe_gpu_workspace *ws, const float *h
     const char *d = std::getenv("FLOE_TEST_MISPREDICT");
     return (d && std::strcmp(d, "1") == 0) ? 8u : 0u;
   }();
-  static const uint32_t dbg_flags = [] {
-    const char *d = std::getenv("FLOE_DEBUG_FLAGS");
-    return d ? (uint32_t)std::atoi(d) : 0u;
-  }();
-  a.debug = dbg | dbg_flags;
+  a.debug = dbg;
   if (int rc = set_smem(W::decode<DH>, smem)) return rc;
   void *kargs[] = {&a};
   cudaLaunchConfig_t cfg{};

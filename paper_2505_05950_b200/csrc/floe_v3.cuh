@@ -282,18 +282,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode(const DecodeArgs a) {
       }
       const uint8_t *m = reinterpret_cast<const uint8_t *>(D.mixing) + (size_t)r0 * DH * 2u;
       const uint32_t pre = min((uint32_t)kChunkItems, nsC);
-      const uint64_t keep = floe_ptx::policy_evict_last();
-      if (a.debug & 4u)
-        for (uint32_t j = pre; j < (uint32_t)kChunkItems; ++j)  // the tail rows come from L2 after h
-          floe_ptx::bulk_prefetch_l2_hint(m + (size_t)chunk_item(c, j) * REC_B, REC_B, keep);
-      // the first half of the finishers also pull the chunks of the second
-      // half into L2: a late finisher then streams its chunk from L2
-      if ((a.debug & 16u) && c + NCH / 2 < NCH) {
-        const uint8_t *m2 = reinterpret_cast<const uint8_t *>(D.mixing) +
-                            (size_t)(c + NCH / 2) * kChunkRows * DH * 2u;
-        for (uint32_t o = 0; o < (uint32_t)kChunkItems * REC_B; o += 65536)
-          floe_ptx::bulk_prefetch_l2_hint(m2 + o, min(65536u, kChunkItems * REC_B - o), keep);
-      }
       for (uint32_t j = 0; j < pre; ++j)
         issueC(K + j, m + (size_t)chunk_item(c, j) * REC_B, 0.0f, l2_stream);
     };
@@ -387,15 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode(const DecodeArgs a) {
       mbar_spin(&listbar, P, 12u << 28);
       const uint32_t n_own = n_list;
       const uint32_t Pf = min(n_own, nsC);
-      const uint32_t rdepth = (a.debug >> 5) & 15u;  // experiment: records in flight
-      auto depth_wait = [&](uint32_t k) {
-        if (rdepth && k >= rdepth) {
-          const uint32_t j = k - rdepth;
-          floe_ptx::mbar_wait(&emptyC[j % nsC], (j / nsC) & 1u, (24u << 28) | j);
-        }
-      };
       auto own_item = [&](uint32_t k) {
-        depth_wait(K + k);
         const uint32_t f = lf[k], s2 = (f >> kSlotShift) & 0x7fu, c = f & 0xffffffu;
         issueC(K + k, rec_s[s2] + (size_t)c * 2 * DH, lv[k] * w_s[s2], l2_stream);
       };
@@ -426,7 +406,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode(const DecodeArgs a) {
           const uint32_t f = floe_ptx::ld_cluster_u32(floe_ptx::mapa(&lf[pfirst + k], pr));
           const float v = __uint_as_float(floe_ptx::ld_cluster_u32(floe_ptx::mapa(&lv[pfirst + k], pr)));
           const uint32_t s2 = (f >> kSlotShift) & 0x7fu, c = f & 0xffffffu;
-          depth_wait(K + own + k);
           issueC(K + own + k, rec_s[s2] + (size_t)c * 2 * DH, v * w_s[s2], l2_stream);
         }
         floe_ptx::mbar_arrive_remote(floe_ptx::mapa(&donebar, pr));
