@@ -12,7 +12,7 @@ HDRS     := $(wildcard $(PKG)/csrc/*.cuh) include/floe_gpu.h
 all: $(LIB) oracle integration
 
 $(LIB): $(SRCS) $(HDRS)
-	$(NVCC) $(NVFLAGS) -shared -cudart static -o $@ $(SRCS) 2> build_ptxas.log || (cat build_ptxas.log; exit 1)
+	$(NVCC) $(NVFLAGS) -shared -cudart static -o $@ $(SRCS) -lcublasLt 2> build_ptxas.log || (cat build_ptxas.log; exit 1)
 
 oracle:
 	$(MAKE) -C oracle
@@ -32,4 +32,4 @@ clean:
 # slows the kernels by orders of magnitude), separate output used through
 # FLOE_LIB=tools/libfloe_b200_sanitize.so.
 tools/libfloe_b200_sanitize.so: $(SRCS) $(HDRS)
-	$(NVCC) $(NVFLAGS) -DFLOE_WATCHDOG_NS=600000000000ull -shared -cudart static -o $@ $(SRCS) 2> /dev/null
+	$(NVCC) $(NVFLAGS) -DFLOE_WATCHDOG_NS=600000000000ull -shared -cudart static -o $@ $(SRCS) -lcublasLt 2> /dev/null

@@ -207,6 +207,18 @@ int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x_dev
                                     uint32_t n_tokens, float *y_dev, float *v_dev,
                                     floe_stream_t stream);
 
+/* expert_forward_sparse (model.cpp:128-142) for many tokens (config 5
+ * prefill, large config-4 batches): y_dev[t] = expert_forward_sparse(e,
+ * x_dev[t]), any n_tokens.  Three dense f16 tensor-core GEMMs with f32
+ * accumulation after a power-of-two scale per token: the up projection with
+ * x and the dequantized weights split into f16 hi + lo (v to ~22 bits: the
+ * masks), the gate and down products with the f16-rounded activations and
+ * SwiGLU coefficients against the f16 records; the per-token mask
+ * !(|v| < threshold) is applied to the coefficients.  Reads the expert's codes
+ * and records once per call.  Fast-layout experts with records. */
+int floe_gpu_expert_forward_prefill(const floe_gpu_expert *e, const float *x_dev,
+                                    uint32_t n_tokens, float *y_dev, floe_stream_t stream);
+
 /* pack_compact (core/src/offload.cpp:27-53) on the device: the channels c with
  * mask_dev[c] != 0 in ascending order -> channels_dev [n] and their records,
  * f16 gate row | f16 down row (element_bytes 2: 4*d_hidden bytes each, the

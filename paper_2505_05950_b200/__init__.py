@@ -37,6 +37,7 @@ from ._abi import (  # noqa: F401
     qgemv_channels,
     qgemv_channels_batched,
     expert_forward_batched,
+    expert_forward_prefill,
     quantize,
     save_record_cache,
     load_record_cache,
@@ -46,5 +47,5 @@ from ._abi import (  # noqa: F401
 __all__ = ["FloeError", "GpuCalib", "GpuExpert", "GpuLayer", "GpuModel", "GpuPredictor", "Offload", "Workspace",
            "abi_version", "dequantize", "device_info", "expert_forward_sparse",
            "exported_symbols", "layer_forward", "layer_forward_batched", "lib", "library_path", "predict_experts",
-           "predict_mask", "qgemv_channels", "qgemv_channels_batched", "expert_forward_batched", "gen_normals", "layer_forward_host", "pack_compact",
+           "predict_mask", "qgemv_channels", "qgemv_channels_batched", "expert_forward_batched", "expert_forward_prefill", "gen_normals", "layer_forward_host", "pack_compact",
            "quantize", "save_record_cache", "load_record_cache", "record_cache_info"]

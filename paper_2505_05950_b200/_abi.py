@@ -100,6 +100,7 @@ _SIGS = {
     "floe_gpu_qgemv_channels": (ct.c_int, [_P, _P, _P, _P, _P]),
     "floe_gpu_qgemv_channels_batched": (ct.c_int, [_P, _P, ct.c_uint32, _P, _P]),
     "floe_gpu_expert_forward_batched": (ct.c_int, [_P, _P, ct.c_uint32, _P, _P, _P]),
+    "floe_gpu_expert_forward_prefill": (ct.c_int, [_P, _P, ct.c_uint32, _P, _P]),
     "floe_gpu_dequantize_up": (ct.c_int, [_P, _P, _P]),
     "floe_gpu_predict_mask": (ct.c_int, [_P, _P, _P, _F, _P, _P, _P, _P]),
     "floe_gpu_layer_create": (ct.c_int, [ct.POINTER(LayerHostView), ct.POINTER(_P)]),
@@ -415,6 +416,20 @@ def expert_forward_batched(e: GpuExpert, x, *, v=None, stream=None):
     y = torch.empty_like(x)
     _check(lib().floe_gpu_expert_forward_batched(e.handle, x.data_ptr(), x.shape[0], y.data_ptr(),
                                                  _ptr(v), _stream(stream)))
+    return y
+
+
+def expert_forward_prefill(e: GpuExpert, x, *, out=None, stream=None):
+    """expert_forward_sparse for many tokens (prefill): x [n, d_hidden] -> y [n, d_hidden]
+    through dense f16 tensor-core GEMMs with hi/lo splits (any n; the codes and records
+    are read once per call)."""
+    torch = _torch()
+    if x.dim() != 2 or x.shape[1] != e.d_hidden or x.dtype != torch.float32 or not x.is_cuda:
+        raise FloeError("expert_forward_prefill: x must be a cuda float32 [n, d_hidden]")
+    x = x.contiguous()
+    y = torch.empty_like(x) if out is None else out
+    _check(lib().floe_gpu_expert_forward_prefill(e.handle, x.data_ptr(), x.shape[0], y.data_ptr(),
+                                                 _stream(stream)))
     return y
 
 

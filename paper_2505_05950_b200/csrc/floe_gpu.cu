@@ -4,6 +4,7 @@
 // layout DESIGN.md documents, per-stream workspaces, launch configuration,
 // stage profiling and the reference's error contract ("<fn>: <reason>"
 // messages).  There is deliberately no CPU fallback anywhere in this file.
+#include <cublasLt.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -24,6 +25,9 @@
 #include "floe_tc.cuh"
 #include "floe_calib.cuh"
 #include "floe_blayer.cuh"
+#include "floe_prefill.cuh"
+#include <map>
+#include <tuple>
 
 #include <cub/device/device_segmented_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
@@ -227,6 +231,22 @@ struct StageScope {  // records [a, b] around one kernel when profiling is on
 };
 
 // ---- launch helpers -------------------------------------------------------
+// Keep freed stream-ordered memory cached in the default pool (the batched and
+// prefill paths allocate their scratch per call; without this every host sync
+// returns it to the driver and the next call maps it again).
+void keep_pool() {
+  static const bool ready = [] {
+    cudaMemPool_t pool;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    return true;
+  }();
+  (void)ready;
+}
+
 template <typename F>
 int set_smem(F *fn, uint32_t bytes) {
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
@@ -1151,16 +1171,7 @@ int floe_gpu_qgemv_channels_batched(const floe_gpu_expert *e, const float *x, ui
   const uint32_t Bp = floe_tc::padded_tokens(n_tokens), spans = e->dh / 64;
   const size_t xl_bytes = (size_t)spans * floe_tc::xl_span_bytes(n_tokens);
   const size_t xs_bytes = 4ull * spans * Bp;
-  static const bool pool_ready = [] {  // keep freed stream-ordered memory cached
-    cudaMemPool_t pool;
-    int dev = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    return true;
-  }();
-  (void)pool_ready;
+  keep_pool();
   uint8_t *scratch = nullptr;  // S | invS | xs | xl (stream-ordered)
   const size_t o_inv = 256, o_xs = 512, o_xl = (o_xs + xs_bytes + 1023) & ~size_t(1023);
   CK(cudaMallocAsync(reinterpret_cast<void **>(&scratch), o_xl + xl_bytes, st));
@@ -1203,6 +1214,126 @@ int floe_gpu_qgemv_channels_batched(const floe_gpu_expert *e, const float *x, ui
     cudaFree(a.trace);
   }
   return rc;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------ prefill path ---
+// Dense f16 tensor-core GEMMs (cuBLASLt, f32 accumulation) for experts that
+// receive many tokens (floe_prefill.cuh).  Plain library GEMMs; the dequant,
+// the hi/lo splits with per-row scales, the mask and SwiGLU are this library's
+// kernels.
+namespace {
+struct Lt {
+  cublasLtHandle_t h = nullptr;
+  void *ws = nullptr;
+  size_t ws_bytes = 64ull << 20;
+  std::mutex mu;
+  std::map<std::tuple<int, int, int, int, int, int, int, int, int>, cublasLtMatmulAlgo_t> algos;
+};
+Lt *lt_get() {
+  static Lt *L = [] {
+    Lt *x = new Lt();
+    if (cublasLtCreate(&x->h) != CUBLAS_STATUS_SUCCESS || cudaMalloc(&x->ws, x->ws_bytes) != cudaSuccess) {
+      x->h = nullptr;
+    }
+    return x;
+  }();
+  return L;
+}
+
+// C (m x n, column-major, ldc, f32) = op(A) op(B) + beta C; A, B f16
+int lt_gemm(bool ta, bool tb, int m, int n, int k, const __half *A, int lda, const __half *B, int ldb,
+            float beta, float *C, int ldc, cudaStream_t st) {
+  Lt *L = lt_get();
+  if (!L->h) return fail(FLOE_ERR_CUDA, "prefill: cuBLASLt unavailable");
+  cublasLtMatmulDesc_t op = nullptr;
+  cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
+  const cublasOperation_t oa = ta ? CUBLAS_OP_T : CUBLAS_OP_N, ob = tb ? CUBLAS_OP_T : CUBLAS_OP_N;
+  bool ok = cublasLtMatmulDescCreate(&op, CUBLAS_COMPUTE_32F, CUDA_R_32F) == CUBLAS_STATUS_SUCCESS;
+  ok = ok && cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSA, &oa, sizeof(oa)) == CUBLAS_STATUS_SUCCESS;
+  ok = ok && cublasLtMatmulDescSetAttribute(op, CUBLASLT_MATMUL_DESC_TRANSB, &ob, sizeof(ob)) == CUBLAS_STATUS_SUCCESS;
+  ok = ok && cublasLtMatrixLayoutCreate(&la, CUDA_R_16F, ta ? k : m, ta ? m : k, lda) == CUBLAS_STATUS_SUCCESS;
+  ok = ok && cublasLtMatrixLayoutCreate(&lb, CUDA_R_16F, tb ? n : k, tb ? k : n, ldb) == CUBLAS_STATUS_SUCCESS;
+  ok = ok && cublasLtMatrixLayoutCreate(&lc, CUDA_R_32F, m, n, ldc) == CUBLAS_STATUS_SUCCESS;
+  cublasLtMatmulAlgo_t algo{};
+  if (ok) {
+    const auto key = std::make_tuple((int)ta, (int)tb, m, n, k, lda, ldb, ldc, beta != 0.0f ? 1 : 0);
+    std::lock_guard<std::mutex> g(L->mu);
+    auto it = L->algos.find(key);
+    if (it != L->algos.end()) {
+      algo = it->second;
+    } else {
+      cublasLtMatmulPreference_t pref = nullptr;
+      cublasLtMatmulHeuristicResult_t res{};
+      int got = 0;
+      ok = cublasLtMatmulPreferenceCreate(&pref) == CUBLAS_STATUS_SUCCESS &&
+           cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES,
+                                                &L->ws_bytes, sizeof(L->ws_bytes)) == CUBLAS_STATUS_SUCCESS &&
+           cublasLtMatmulAlgoGetHeuristic(L->h, op, la, lb, lc, lc, pref, 1, &res, &got) ==
+               CUBLAS_STATUS_SUCCESS && got > 0;
+      if (pref) cublasLtMatmulPreferenceDestroy(pref);
+      if (ok) {
+        algo = res.algo;
+        L->algos[key] = algo;
+      }
+    }
+  }
+  const float alpha = 1.0f;
+  if (ok)
+    ok = cublasLtMatmul(L->h, op, &alpha, A, la, B, lb, &beta, C, lc, C, lc, &algo, L->ws, L->ws_bytes,
+                        st) == CUBLAS_STATUS_SUCCESS;
+  if (lc) cublasLtMatrixLayoutDestroy(lc);
+  if (lb) cublasLtMatrixLayoutDestroy(lb);
+  if (la) cublasLtMatrixLayoutDestroy(la);
+  if (op) cublasLtMatmulDescDestroy(op);
+  return ok ? FLOE_OK : fail(FLOE_ERR_CUDA, "prefill: cuBLASLt matmul failed (%d x %d x %d)", m, n, k);
+}
+}  // namespace
+
+extern "C" {
+
+int floe_gpu_expert_forward_prefill(const floe_gpu_expert *e, const float *x, uint32_t n_tokens,
+                                    float *y, floe_stream_t stream) {
+  if (!e || !x || !y) return fail(FLOE_ERR_INVALID, "expert_forward_sparse: null argument");
+  if (n_tokens == 0) return FLOE_OK;
+  if (!e->fast || e->up_only || !e->host_desc.records)
+    return fail(FLOE_ERR_UNSUPPORTED, "expert_forward_prefill: needs the tile layout and records");
+  if (int rc = require_device("expert_forward_prefill")) return rc;
+  cudaStream_t st = S(stream);
+  keep_pool();
+  const uint32_t dh = e->dh, di = e->di, n = n_tokens;
+  // scratch: Wb [di][3dh] f16 | Xa [n][3dh] f16 | v, g [n][di] f32 | Ah [n][di] f16 | inv, ainv [n]
+  const size_t o_wb = 0, o_xa = o_wb + 2ull * di * 3 * dh, o_v = o_xa + 2ull * n * 3 * dh;
+  const size_t o_g = o_v + 4ull * n * di, o_a = o_g + 4ull * n * di, o_inv = o_a + 2ull * n * di;
+  const size_t o_ainv = o_inv + 4ull * n, total = o_ainv + 4ull * n;
+  uint8_t *sc = nullptr;
+  CK(cudaMallocAsync(reinterpret_cast<void **>(&sc), total, st));
+  __half *Wb = reinterpret_cast<__half *>(sc + o_wb), *Xa = reinterpret_cast<__half *>(sc + o_xa);
+  float *v = reinterpret_cast<float *>(sc + o_v), *g = reinterpret_cast<float *>(sc + o_g);
+  __half *Ac = reinterpret_cast<__half *>(sc + o_a);
+  float *inv = reinterpret_cast<float *>(sc + o_inv), *ainv = reinterpret_cast<float *>(sc + o_ainv);
+  auto done = [&](int rc) {
+    cudaFreeAsync(sc, st);
+    return rc;
+  };
+  const int sm = device_info().sm;
+  if (dh == 4096) floe_pf::wcat_tiled<4096><<<sm * 8, 256, 0, st>>>(e->host_desc.tiles, di, Wb);
+  else floe_pf::wcat_tiled<2048><<<sm * 8, 256, 0, st>>>(e->host_desc.tiles, di, Wb);
+  floe_pf::xcat<<<n, 256, 0, st>>>(x, dh, Xa, inv);
+  if (cudaGetLastError() != cudaSuccess) return done(fail(FLOE_ERR_CUDA, "prefill: launch failed"));
+  const __half *rec = e->host_desc.records;  // [di][gate row | down row]
+  const int D = (int)dh, I = (int)di, N = (int)n;
+  // v (n x di row-major == di x n column-major) = Wb^T-view . Xa, K = 3 dh
+  if (int rc = lt_gemm(true, false, I, N, 3 * D, Wb, 3 * D, Xa, 3 * D, 0.0f, v, I, st)) return done(rc);
+  // g = gate . x_hi  (gate rows: ld 2 dh)
+  if (int rc = lt_gemm(true, false, I, N, D, rec, 2 * D, Xa, 3 * D, 0.0f, g, I, st)) return done(rc);
+  floe_pf::coeffs<<<n, 256, 0, st>>>(v, g, inv, di, e->host_desc.threshold, Ac, ainv);
+  // y (n x dh row-major == dh x n column-major) = down^T-view . a_hi
+  if (int rc = lt_gemm(false, false, D, N, I, rec + dh, 2 * D, Ac, I, 0.0f, y, D, st)) return done(rc);
+  floe_pf::unscale_rows<<<n, 256, 0, st>>>(y, dh, ainv);
+  if (cudaGetLastError() != cudaSuccess) return done(fail(FLOE_ERR_CUDA, "prefill: launch failed"));
+  return done(FLOE_OK);
 }
 
 int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x, uint32_t n_tokens,

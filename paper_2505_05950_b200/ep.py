@@ -10,9 +10,14 @@ Per token the arithmetic is the reference's block (model.cpp:145-169):
   selection in ascending expert order, la.cpp:48-61);  w = softmax of the
   selected logits (la.cpp:37-46);  y = u + sum_j w_j expert_j(u) in ascending
   expert order.
-The mixing and router products for a token batch are plain GEMMs (torch,
-i.e. cuBLAS on the device); the experts run through `expert_fn` -- on the GPU
-`batched_expert_fn`, the tcgen05 batched expert forward.  The collectives are
+The mixing product for a token batch is a plain GEMM: with an f16 mixing
+matrix (the device layers' format) it runs on the tensor cores as two f16
+GEMMs with f32 accumulation over the hi and lo halves of the (row-scaled)
+activations; the router product is a small f32 GEMM.  The experts run through
+`expert_fn` -- on the GPU `batched_expert_fn`: the prefill expert forward
+(dense f16 tensor-core GEMMs, codes and records read once per expert) for
+experts with many tokens, the tcgen05 batched forward or the fused
+single-token kernel for few.  The collectives are
 NCCL over NVLink on GPUs (gloo in the CPU tests).  Fusing dispatch/combine
 with the expert kernels over peer memory is the next step; this module is the
 reference-semantics baseline for it.
@@ -31,6 +36,24 @@ def route_topk(torch, logits, k: int):
     mx = lg.max(dim=1, keepdim=True).values
     ex = torch.exp(lg - mx)
     return sel, ex / ex.sum(dim=1, keepdim=True)
+
+
+def mixing_product(torch, h, mixing):
+    """h @ mixing^T.  f16 mixing on a GPU: h scaled per row by a power of two,
+    split into f16 hi + lo, two tensor-core GEMMs with f32 output (exact up to
+    the f32 accumulation); otherwise a plain f32 GEMM."""
+    if mixing.dtype != torch.float16 or not h.is_cuda:
+        return h @ mixing.t().to(h.dtype)
+    mx = h.abs().amax(dim=1, keepdim=True)
+    e = torch.frexp(torch.where(torch.isfinite(mx) & (mx > 0), mx, torch.ones_like(mx)))[1]
+    s = torch.ldexp(torch.ones_like(mx), -e)
+    hs = h * s
+    hi = hs.half()
+    lo = (hs - hi.float()).half()
+    mt = mixing.t()
+    out = torch.mm(hi, mt, out_dtype=torch.float32)
+    out += torch.mm(lo, mt, out_dtype=torch.float32)
+    return out / s
 
 
 def _a2a(torch, dist, group, x, out_splits, in_splits):
@@ -53,7 +76,7 @@ def ep_moe_layer(h, router, mixing, top_k: int, expert_fn: Callable, n_experts: 
     if n_experts % world:
         raise ValueError("ep_moe_layer: experts must divide evenly over the ranks")
     per_rank = n_experts // world
-    u = h + h @ mixing.t()                      # block input (model.cpp:150-152)
+    u = h + mixing_product(torch, h, mixing)    # block input (model.cpp:150-152)
     sel, w = route_topk(torch, u @ router.t(), top_k)
     T = h.shape[0]
     pair_tok = torch.arange(T, device=h.device).repeat_interleave(top_k)
@@ -94,12 +117,15 @@ def ep_moe_layer(h, router, mixing, top_k: int, expert_fn: Callable, n_experts: 
     return y, sel, w
 
 
-def batched_expert_fn(experts, first_expert: int = 0, chunk: int = 64, small: int = 3):
-    """expert_fn over GpuExpert objects on this rank: the batched expert
-    forward (tcgen05 up projection + union gate/down) in chunks of <= 64
-    tokens; an expert with at most `small` tokens runs them one by one through
-    the single-token fused kernel (29 us each against the batched call's ~90 us
-    fixed cost).  experts[i] is global expert first_expert + i."""
+def batched_expert_fn(experts, first_expert: int = 0, chunk: int = 64, small: int = 3,
+                      prefill_min: int = 64):
+    """expert_fn over GpuExpert objects on this rank: an expert with at least
+    `prefill_min` tokens runs them all through the prefill expert forward
+    (dense f16 tensor-core GEMMs: its codes and records read once); fewer go
+    through the batched expert forward (tcgen05 up projection + union
+    gate/down) in chunks of <= 64 tokens, and at most `small` tokens one by one
+    through the single-token fused kernel (~25 us each against the batched
+    call's ~90 us fixed cost).  experts[i] is global expert first_expert + i."""
     from . import _abi
     wss = {}
 
@@ -114,6 +140,8 @@ def batched_expert_fn(experts, first_expert: int = 0, chunk: int = 64, small: in
             if key not in wss:
                 wss[key] = _abi.Workspace(ex.d_hidden, ex.d_intermediate, 1)
             return torch.stack([_abi.expert_forward_sparse(ex, X[i], wss[key]) for i in range(n)])
+        if n >= prefill_min:
+            return _abi.expert_forward_prefill(ex, X)
         parts = [_abi.expert_forward_batched(ex, X[i:i + chunk]) for i in range(0, n, chunk)]
         return torch.cat(parts, dim=0)
 

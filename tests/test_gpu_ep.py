@@ -9,10 +9,13 @@ from oracle import oracle as O
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("T", [96, 5], ids=["batched", "few-tokens-per-expert"])
-def test_ep_layer_matches_fused_layer_per_token(T):
+@pytest.mark.parametrize("T,f16", [(96, False), (5, False), (400, True)],
+                         ids=["batched", "few-tokens-per-expert", "prefill-f16-mixing"])
+def test_ep_layer_matches_fused_layer_per_token(T, f16):
     """T = 96: ~48 tokens per expert (batched forward); T = 5: 1-3 tokens per
-    expert, which go one by one through the fused single-expert kernel."""
+    expert, which go one by one through the fused single-expert kernel;
+    T = 400: ~200 per expert through the prefill GEMMs, with the f16 mixing
+    product on the tensor cores (hi/lo split) against the f16-mixing layer."""
     import torch
 
     import paper_2505_05950_b200 as fb
@@ -27,15 +30,24 @@ def test_ep_layer_matches_fused_layer_per_token(T):
                                     down=down, threshold=1.0))
     router = (rng.standard_normal((E, dh)) / np.sqrt(dh)).astype(np.float32)
     mixing = (rng.standard_normal((dh, dh)) / np.sqrt(dh)).astype(np.float32)
-    layer = fb.GpuLayer(router, mixing, experts, K, mixing_f16=False)
+    layer = fb.GpuLayer(router, mixing, experts, K, mixing_f16=f16)
     H = torch.from_numpy(np.stack([O.token_input(2, t, dh) for t in range(T)])).cuda()
-    y, sel, w = ep.ep_moe_layer(H, torch.from_numpy(router).cuda(), torch.from_numpy(mixing).cuda(),
+    mix_d = torch.from_numpy(mixing).cuda()
+    y, sel, w = ep.ep_moe_layer(H, torch.from_numpy(router).cuda(), mix_d.half() if f16 else mix_d,
                                 K, ep.batched_expert_fn(experts), E)
     ws = fb.Workspace(dh, di, K)
-    agree = 0
+    agree, errs = 0, []
     for t in range(T):
         tr = fb.layer_forward(layer, H[t], ws, traced=True)
         if np.array_equal(tr["experts"].cpu().numpy().astype(np.int64), sel[t].cpu().numpy()):
             agree += 1
-            assert O.rel_l2(y[t].cpu().numpy(), tr["out"].cpu().numpy()) <= 1e-3, t
+            errs.append(O.rel_l2(y[t].cpu().numpy(), tr["out"].cpu().numpy()))
+    errs = np.array(errs)
     assert agree >= T - 2 if T > 10 else agree >= T - 1
+    # same routing: the same per-token arithmetic up to summation order (the
+    # prefill GEMMs round x and the SwiGLU coefficients of the gate/down
+    # products to f16: ~1e-4 of y); a channel within rounding of its threshold
+    # may flip (~1e-2 of y)
+    assert float(np.median(errs)) <= (5e-4 if T > 200 else 1e-4), float(np.median(errs))
+    assert np.sum(errs > 1e-3) <= max(1, T // 50), np.sort(errs)[-5:]
+    assert errs.max() <= 3e-2, errs.max()
