@@ -1257,8 +1257,13 @@ int lt_gemm(bool ta, bool tb, int m, int n, int k, const __half *A, int lda, con
   ok = ok && cublasLtMatrixLayoutCreate(&lb, CUDA_R_16F, tb ? n : k, tb ? k : n, ldb) == CUBLAS_STATUS_SUCCESS;
   ok = ok && cublasLtMatrixLayoutCreate(&lc, CUDA_R_32F, m, n, ldc) == CUBLAS_STATUS_SUCCESS;
   cublasLtMatmulAlgo_t algo{};
+  // algorithms are cached per shape class; the token count (a GEMM dimension
+  // that changes with every routing) only by its power-of-two bucket: a
+  // heuristic query costs far more than the GEMMs of a small expert
+  int nb = 1;
+  while (nb < n) nb <<= 1;
   if (ok) {
-    const auto key = std::make_tuple((int)ta, (int)tb, m, n, k, lda, ldb, ldc, beta != 0.0f ? 1 : 0);
+    const auto key = std::make_tuple((int)ta, (int)tb, m, nb, k, lda, ldb, ldc, beta != 0.0f ? 1 : 0);
     std::lock_guard<std::mutex> g(L->mu);
     auto it = L->algos.find(key);
     if (it != L->algos.end()) {
@@ -1280,6 +1285,22 @@ int lt_gemm(bool ta, bool tb, int m, int n, int k, const __half *A, int lda, con
     }
   }
   const float alpha = 1.0f;
+  if (ok) {
+    cublasLtMatmulHeuristicResult_t chk{};
+    if (cublasLtMatmulAlgoCheck(L->h, op, la, lb, lc, lc, &algo, &chk) != CUBLAS_STATUS_SUCCESS ||
+        chk.workspaceSize > L->ws_bytes) {  // not valid at this n: a fresh heuristic
+      cublasLtMatmulPreference_t pref = nullptr;
+      cublasLtMatmulHeuristicResult_t res{};
+      int got = 0;
+      ok = cublasLtMatmulPreferenceCreate(&pref) == CUBLAS_STATUS_SUCCESS &&
+           cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES,
+                                                &L->ws_bytes, sizeof(L->ws_bytes)) == CUBLAS_STATUS_SUCCESS &&
+           cublasLtMatmulAlgoGetHeuristic(L->h, op, la, lb, lc, lc, pref, 1, &res, &got) ==
+               CUBLAS_STATUS_SUCCESS && got > 0;
+      if (pref) cublasLtMatmulPreferenceDestroy(pref);
+      if (ok) algo = res.algo;
+    }
+  }
   if (ok)
     ok = cublasLtMatmul(L->h, op, &alpha, A, la, B, lb, &beta, C, lc, C, lc, &algo, L->ws, L->ws_bytes,
                         st) == CUBLAS_STATUS_SUCCESS;
@@ -2236,6 +2257,14 @@ static const uint32_t kBatchedSmall = [] {
 }();
 // Batches of at most this many tokens run token by token through the fused
 // layer kernel (FLOE_LAYER_PER_TOKEN overrides).
+static const uint32_t kPrefillMin = [] {  // tokens per expert for the prefill GEMMs
+  const char *p = std::getenv("FLOE_PREFILL_MIN");
+  return p ? (uint32_t)std::atoi(p) : 32u;
+}();
+static const uint32_t kMixGemmMin = [] {  // tokens per call for the tensor-core mixing GEMM
+  const char *p = std::getenv("FLOE_MIX_GEMM_MIN");
+  return p ? (uint32_t)std::atoi(p) : 64u;
+}();
 static const uint32_t kLayerPerToken = [] {
   const char *p = std::getenv("FLOE_LAYER_PER_TOKEN");
   return p ? (uint32_t)std::atoi(p) : 40u;
@@ -2264,13 +2293,17 @@ int floe_gpu_layer_forward_batched(const floe_gpu_layer *l, floe_gpu_workspace *
     return FLOE_OK;
   }
   // scratch: u [T][dh] | logits [T][E] | sel [P] | w [P] | counts [E] | lists [E][T] |
-  //          X [64][dh] (one expert chunk's rows) | Y [64][dh] | out [P][dh]
+  //          X [T][dh] (one expert's rows) | Y [T][dh] | out [P][dh] |
+  //          mixing GEMM: Ha [T][3dh] f16, inv [T], M.h [T][dh]
   const size_t CH = floe_tc::kMaxTokens;
+  const bool mix_tc = l->mix_f16 && T >= kMixGemmMin;
   const size_t o_u = 0, o_lg = o_u + 4ull * T * dh, o_sel = o_lg + 4ull * T * E;
   const size_t o_w = o_sel + 4ull * P, o_cnt = o_w + 4ull * P, o_lst = o_cnt + 4ull * 32;
   const size_t o_x = (o_lst + 4ull * E * T + 255) & ~size_t(255);
-  const size_t o_y = o_x + 4ull * CH * dh, o_out = o_y + 4ull * CH * dh;
-  const size_t total = o_out + 4ull * P * dh;
+  const size_t o_y = o_x + 4ull * T * dh, o_out = o_y + 4ull * T * dh;
+  const size_t o_ha = o_out + 4ull * P * dh, o_hinv = o_ha + (mix_tc ? 2ull * T * 3 * dh : 0);
+  const size_t o_mh = (o_hinv + 4ull * T + 255) & ~size_t(255);
+  const size_t total = o_mh + (mix_tc ? 4ull * T * dh : 0);
   uint8_t *sc = nullptr;
   CK(cudaMallocAsync(reinterpret_cast<void **>(&sc), total, st));
   float *u = reinterpret_cast<float *>(sc + o_u), *lg = reinterpret_cast<float *>(sc + o_lg);
@@ -2283,9 +2316,22 @@ int floe_gpu_layer_forward_batched(const floe_gpu_layer *l, floe_gpu_workspace *
     cudaFreeAsync(sc, st);
     return rc;
   };
-  // u = h + mixing h (model.cpp:150-152), kMixTok tokens per pass
+  // u = h + mixing h (model.cpp:150-152).  Many tokens with f16 mixing: two
+  // tensor-core GEMMs over the hi and lo halves of the row-scaled h (f32
+  // accumulation); otherwise kMixTok tokens per pass on the CUDA cores.
   const uint32_t mix_smem = 4u * floe_bl::kMixTok * 256u;
-  for (uint32_t t0 = 0; t0 < T; t0 += floe_bl::kMixTok) {
+  if (mix_tc) {
+    keep_pool();
+    __half *Ha = reinterpret_cast<__half *>(sc + o_ha);
+    float *hinv = reinterpret_cast<float *>(sc + o_hinv), *mh = reinterpret_cast<float *>(sc + o_mh);
+    floe_pf::xcat<<<T, 256, 0, st>>>(h, dh, Ha, hinv);
+    const __half *M = static_cast<const __half *>(l->mixing);
+    const int D = (int)dh, N = (int)T;
+    if (int rc = lt_gemm(true, false, D, N, D, M, D, Ha, 3 * D, 0.0f, mh, D, st)) return done(rc);
+    if (int rc = lt_gemm(true, false, D, N, D, M, D, Ha + 2 * dh, 3 * D, 1.0f, mh, D, st)) return done(rc);
+    floe_pf::residual<<<T, 256, 0, st>>>(h, mh, hinv, dh, u);
+  }
+  for (uint32_t t0 = 0; t0 < (mix_tc ? 0u : T); t0 += floe_bl::kMixTok) {
     const uint32_t nt = std::min<uint32_t>(floe_bl::kMixTok, T - t0);
     if (l->mix_f16) {
       if (int rc = set_smem(floe_bl::mix_batched<__half>, mix_smem)) return done(rc);
@@ -2313,6 +2359,14 @@ int floe_gpu_layer_forward_batched(const floe_gpu_layer *l, floe_gpu_workspace *
   // through the batched forward (one tcgen05 pass over the codes, the union
   // of kept records once; chunks of at most 64 tokens)
   for (uint32_t e = 0; e < E; ++e) {
+    if (hc[e] >= kPrefillMin) {  // many tokens: the prefill GEMMs, the expert read once
+      const uint32_t n = hc[e];
+      const uint32_t *pairs = lst + (size_t)e * T;
+      floe_bl::gather_rows<<<dim3(4, n), 256, 0, st>>>(u, pairs, n, K, dh, X);
+      if (int rc = floe_gpu_expert_forward_prefill(l->experts[e], X, n, Y, stream)) return done(rc);
+      floe_bl::scatter_rows<<<dim3(4, n), 256, 0, st>>>(Y, pairs, n, dh, outp);
+      continue;
+    }
     for (uint32_t c0 = 0; c0 < hc[e]; c0 += (uint32_t)CH) {
       const uint32_t n = std::min<uint32_t>((uint32_t)CH, hc[e] - c0);
       const uint32_t *pairs = lst + (size_t)e * T + c0;

@@ -119,6 +119,14 @@ __global__ void coeffs(const float *v, const float *g, const float *inv, uint32_
   }
 }
 
+// u = h + mh * inv[row] (the block input, model.cpp:150-152: drift scale 1).
+__global__ void residual(const float *h, const float *mh, const float *inv, uint32_t dh, float *u) {
+  const uint32_t r = blockIdx.x;
+  const float s = inv[r];
+  for (uint32_t k = threadIdx.x; k < dh; k += blockDim.x)
+    u[(size_t)r * dh + k] = h[(size_t)r * dh + k] + mh[(size_t)r * dh + k] * s;
+}
+
 // y[row] *= ainv[row] (the coefficients' scale), in place.
 __global__ void unscale_rows(float *y, uint32_t dh, const float *ainv) {
   const uint32_t r = blockIdx.x;

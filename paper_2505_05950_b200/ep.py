@@ -118,7 +118,7 @@ def ep_moe_layer(h, router, mixing, top_k: int, expert_fn: Callable, n_experts: 
 
 
 def batched_expert_fn(experts, first_expert: int = 0, chunk: int = 64, small: int = 3,
-                      prefill_min: int = 64):
+                      prefill_min: int = 32):
     """expert_fn over GpuExpert objects on this rank: an expert with at least
     `prefill_min` tokens runs them all through the prefill expert forward
     (dense f16 tensor-core GEMMs: its codes and records read once); fewer go
