@@ -432,15 +432,10 @@ int launch_v2_dh(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) 
     return (d && std::strcmp(d, "1") == 0) ? 8u : 0u;
   }();
   a.debug = dbg;
-  static const uint32_t nsc_env = [] {
-    const char *p = std::getenv("FLOE_NSC");
-    return p ? (uint32_t)std::atoi(p) : 0u;
-  }();
   static const uint32_t early_env = [] {
     const char *p = std::getenv("FLOE_EARLY");
     return p ? (uint32_t)std::atoi(p) : (uint32_t)V::kEarly;
   }();
-  a.nsc_cap = nsc_env;
   a.early = early_env;
 
   if (int rc = set_smem(V::fused<DH>, smem)) return rc;

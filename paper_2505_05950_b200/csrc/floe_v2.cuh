@@ -398,7 +398,6 @@ struct FusedArgs {
   uint32_t ns;         // ring stages
   uint32_t max_tiles;  // per-CTA tile capacity of the shared-memory kept list
   uint32_t debug;      // test hook: bit 3 = invert the predicted logits (misprediction path)
-  uint32_t nsc_cap;    // experiments: phase-C record stages (0 = as many as fit)
   uint32_t early;      // mixing stages issued before griddepcontrol.wait
 };
 
@@ -535,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   // Phase C re-carves the ring plus the x-table area (both free once every K1
   // tile is consumed) into 4*DH-byte record stages with their own barriers:
   // 12 records (192 KB) in flight at d_hidden 4096.
-  const uint32_t nsC = min(a.nsc_cap ? a.nsc_cap : (uint32_t)kMaxStages, (L.ubuf - L.ring) / REC_B);
+  const uint32_t nsC = min((uint32_t)kMaxStages, (L.ubuf - L.ring) / REC_B);
   auto stageC = [&](uint32_t k) { return ring + (k % nsC) * REC_B; };
   auto issueC = [&](uint32_t k, const void *src, float scale) {
     if (k >= nsC) floe_ptx::mbar_wait(&emptyC[k % nsC], ((k / nsC) + 1) & 1u, (5u << 28) | k);
