@@ -1238,6 +1238,12 @@ Lt *lt_get() {
 }
 
 // C (m x n, column-major, ldc, f32) = op(A) op(B) + beta C; A, B f16
+// tokens up to which the prefill path computes v with the exact batched K1
+const uint32_t kExactK1Max = [] {
+  const char *p = std::getenv("FLOE_EXACT_K1_MAX");
+  return p ? (uint32_t)std::atoi(p) : 64u;
+}();
+
 int lt_gemm(bool ta, bool tb, int m, int n, int k, const __half *A, int lda, const __half *B, int ldb,
             float beta, float *C, int ldc, cudaStream_t st) {
   Lt *L = lt_get();
@@ -1319,8 +1325,9 @@ int floe_gpu_expert_forward_prefill(const floe_gpu_expert *e, const float *x, ui
   cudaStream_t st = S(stream);
   keep_pool();
   const uint32_t dh = e->dh, di = e->di, n = n_tokens;
-  // scratch: Wb [di][3dh] f16 | Xa [n][3dh] f16 | v, g [n][di] f32 | Ah [n][di] f16 | inv, ainv [n]
-  const size_t o_wb = 0, o_xa = o_wb + 2ull * di * 3 * dh, o_v = o_xa + 2ull * n * 3 * dh;
+  // scratch: Wb [di][3dh] f16 (large n) | Xa [n][3dh] f16 | v, g [n][di] f32 | Ah [n][di] f16 | inv, ainv [n]
+  const size_t wb_bytes = n <= kExactK1Max ? 0 : 2ull * di * 3 * dh;
+  const size_t o_wb = 0, o_xa = o_wb + wb_bytes, o_v = o_xa + 2ull * n * 3 * dh;
   const size_t o_g = o_v + 4ull * n * di, o_a = o_g + 4ull * n * di, o_inv = o_a + 2ull * n * di;
   const size_t o_ainv = o_inv + 4ull * n, total = o_ainv + 4ull * n;
   uint8_t *sc = nullptr;
@@ -1334,17 +1341,27 @@ int floe_gpu_expert_forward_prefill(const floe_gpu_expert *e, const float *x, ui
     return rc;
   };
   const int sm = device_info().sm;
-  if (dh == 4096) floe_pf::wcat_tiled<4096><<<sm * 8, 256, 0, st>>>(e->host_desc.tiles, di, Wb);
-  else floe_pf::wcat_tiled<2048><<<sm * 8, 256, 0, st>>>(e->host_desc.tiles, di, Wb);
+  // Up to kExactK1Max tokens the exact batched K1 (tcgen05 kind::i8 on the
+  // codes, no dequantized copy) computes v; above, the dequantized f16 hi/lo
+  // GEMM (its fixed cost -- writing and reading the 352 MB copy -- amortised)
+  const bool exact_k1 = n <= kExactK1Max;
   floe_pf::xcat<<<n, 256, 0, st>>>(x, dh, Xa, inv);
+  if (!exact_k1) {
+    if (dh == 4096) floe_pf::wcat_tiled<4096><<<sm * 8, 256, 0, st>>>(e->host_desc.tiles, di, Wb);
+    else floe_pf::wcat_tiled<2048><<<sm * 8, 256, 0, st>>>(e->host_desc.tiles, di, Wb);
+  }
   if (cudaGetLastError() != cudaSuccess) return done(fail(FLOE_ERR_CUDA, "prefill: launch failed"));
   const __half *rec = e->host_desc.records;  // [di][gate row | down row]
   const int D = (int)dh, I = (int)di, N = (int)n;
-  // v (n x di row-major == di x n column-major) = Wb^T-view . Xa, K = 3 dh
-  if (int rc = lt_gemm(true, false, I, N, 3 * D, Wb, 3 * D, Xa, 3 * D, 0.0f, v, I, st)) return done(rc);
+  if (exact_k1) {
+    if (int rc = floe_gpu_qgemv_channels_batched(e, x, n, v, stream)) return done(rc);
+  } else {
+    // v (n x di row-major == di x n column-major) = Wb^T-view . Xa, K = 3 dh
+    if (int rc = lt_gemm(true, false, I, N, 3 * D, Wb, 3 * D, Xa, 3 * D, 0.0f, v, I, st)) return done(rc);
+  }
   // g = gate . x_hi  (gate rows: ld 2 dh)
   if (int rc = lt_gemm(true, false, I, N, D, rec, 2 * D, Xa, 3 * D, 0.0f, g, I, st)) return done(rc);
-  floe_pf::coeffs<<<n, 256, 0, st>>>(v, g, inv, di, e->host_desc.threshold, Ac, ainv);
+  floe_pf::coeffs<<<n, 256, 0, st>>>(v, g, inv, di, e->host_desc.threshold, Ac, ainv, exact_k1 ? 1 : 0);
   // y (n x dh row-major == dh x n column-major) = down^T-view . a_hi
   if (int rc = lt_gemm(false, false, D, N, I, rec + dh, 2 * D, Ac, I, 0.0f, y, D, st)) return done(rc);
   floe_pf::unscale_rows<<<n, 256, 0, st>>>(y, dh, ainv);
@@ -2254,7 +2271,7 @@ static const uint32_t kBatchedSmall = [] {
 // layer kernel (FLOE_LAYER_PER_TOKEN overrides).
 static const uint32_t kPrefillMin = [] {  // tokens per expert for the prefill GEMMs
   const char *p = std::getenv("FLOE_PREFILL_MIN");
-  return p ? (uint32_t)std::atoi(p) : 32u;
+  return p ? (uint32_t)std::atoi(p) : 8u;
 }();
 static const uint32_t kMixGemmMin = [] {  // tokens per call for the tensor-core mixing GEMM
   const char *p = std::getenv("FLOE_MIX_GEMM_MIN");

@@ -86,19 +86,20 @@ __global__ void xcat(const float *x, uint32_t dh, __half *xa, float *inv) {
 }
 
 // a = silu(g) * v where !(|v| < t) (model.cpp:135-137, la.cpp:31), else 0;
-// v, g are the scaled GEMM outputs (times inv[row] for the true values);
+// g (and v unless v_true) are the scaled GEMM outputs (times inv[row] for the
+// true values);
 // ah [n][di] = f16(a * s_a[row]), ainv[row] = 1 / s_a.  One block per token
 // row: the row maximum first (exact power-of-two scale).
 __global__ void coeffs(const float *v, const float *g, const float *inv, uint32_t di, float t,
-                       __half *acat, float *ainv) {
+                       __half *acat, float *ainv, int v_true) {
   const uint32_t r = blockIdx.x;
-  const float iv = inv[r];
+  const float ig = inv[r], iv = v_true ? 1.0f : ig;  // v from the exact batched K1: unscaled
   const float *vr = v + (size_t)r * di, *gr = g + (size_t)r * di;
   __shared__ float red[32];
   float mx = 0.0f;
   for (uint32_t c = threadIdx.x; c < di; c += blockDim.x) {
     const float vv = vr[c] * iv;
-    const float a = !(fabsf(vv) < t) ? floe_k::silu_ref(gr[c] * iv) * vv : 0.0f;
+    const float a = !(fabsf(vv) < t) ? floe_k::silu_ref(gr[c] * ig) * vv : 0.0f;
     mx = fmaxf(mx, fabsf(a));
   }
   for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -115,7 +116,7 @@ __global__ void coeffs(const float *v, const float *g, const float *inv, uint32_
   __half *ao = acat + (size_t)r * di;
   for (uint32_t c = threadIdx.x; c < di; c += blockDim.x) {
     const float vv = vr[c] * iv;
-    ao[c] = __float2half_rn((!(fabsf(vv) < t) ? floe_k::silu_ref(gr[c] * iv) * vv : 0.0f) * s);
+    ao[c] = __float2half_rn((!(fabsf(vv) < t) ? floe_k::silu_ref(gr[c] * ig) * vv : 0.0f) * s);
   }
 }
 

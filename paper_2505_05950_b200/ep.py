@@ -117,15 +117,15 @@ def ep_moe_layer(h, router, mixing, top_k: int, expert_fn: Callable, n_experts: 
     return y, sel, w
 
 
-def batched_expert_fn(experts, first_expert: int = 0, chunk: int = 64, small: int = 3,
-                      prefill_min: int = 32):
+def batched_expert_fn(experts, first_expert: int = 0, chunk: int = 64, small: int = 7,
+                      prefill_min: int = 8):
     """expert_fn over GpuExpert objects on this rank: an expert with at least
     `prefill_min` tokens runs them all through the prefill expert forward
-    (dense f16 tensor-core GEMMs: its codes and records read once); fewer go
-    through the batched expert forward (tcgen05 up projection + union
-    gate/down) in chunks of <= 64 tokens, and at most `small` tokens one by one
-    through the single-token fused kernel (~25 us each against the batched
-    call's ~90 us fixed cost).  experts[i] is global expert first_expert + i."""
+    (exact batched up projection or dequantized f16 hi/lo GEMM, dense f16
+    gate/down GEMMs: codes and records read once, ~0.18 ms up to 64 tokens);
+    at most `small` tokens go one by one through the single-token fused kernel
+    (~25 us each); in between, the batched expert forward in chunks of <= 64.
+    experts[i] is global expert first_expert + i."""
     from . import _abi
     wss = {}
 

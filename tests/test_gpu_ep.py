@@ -33,8 +33,10 @@ def test_ep_layer_matches_fused_layer_per_token(T, f16):
     layer = fb.GpuLayer(router, mixing, experts, K, mixing_f16=f16)
     H = torch.from_numpy(np.stack([O.token_input(2, t, dh) for t in range(T)])).cuda()
     mix_d = torch.from_numpy(mixing).cuda()
+    # T = 96 keeps the tcgen05 batched forward (no prefill) so that path stays covered
+    fn = ep.batched_expert_fn(experts, prefill_min=10**9) if T == 96 else ep.batched_expert_fn(experts)
     y, sel, w = ep.ep_moe_layer(H, torch.from_numpy(router).cuda(), mix_d.half() if f16 else mix_d,
-                                K, ep.batched_expert_fn(experts), E)
+                                K, fn, E)
     ws = fb.Workspace(dh, di, K)
     agree, errs = 0, []
     for t in range(T):

@@ -20,7 +20,7 @@ def main():
     e = fb.GpuExpert(bench.DH, bench.DI, bench.BITS, bench.G, codes, scales, zeros, gate=gate,
                      down=down, threshold=1.0)
     st = torch.cuda.current_stream()
-    for n in (64, 256, 1024, 2048):
+    for n in (4, 8, 16, 32, 64, 96, 256, 1024, 2048):
         X = torch.stack([fb.gen_normals(1, (1 << 40) + t, bench.DH) for t in range(n)])
         Y = torch.empty_like(X)
         for _ in range(2):
@@ -30,7 +30,7 @@ def main():
         ms = bench.time_region(torch, lambda i: fb.expert_forward_prefill(e, X, out=Y), k, st) / k
         flops = 2.0 * n * bench.DH * bench.DI * 5  # K1 (K = 3 dh) + gate + down GEMMs
         out = {"tokens": n, "ms": round(ms, 3), "tflops": round(flops / (ms * 1e-3) / 1e12, 1)}
-        if n <= 64:
+        if n <= 64 and n >= 16:
             msb = bench.time_region(torch, lambda i: fb.expert_forward_batched(e, X), k, st) / k
             out["batched_ms"] = round(msb, 3)
         print(json.dumps(out), flush=True)
