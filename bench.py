@@ -402,6 +402,9 @@ def run_ours(args, rank, world, local):
     # ---------------- config 1 (+ config-4 expert level) ----------------
     expert_ffn = run_expert(fb, torch, args, stream, hbm_peak)
 
+    # ---------------- configs 4 and 5 at the layer level (C ABI) ----------------
+    batched_layer = run_batched_layer(fb, torch, layers[0], ws, stream)
+
     # ---------------- e2e through the host-buffer C ABI ----------------
     hs_h = hs.cpu().numpy()
     y_h = np.empty((L, DH), np.float32)
@@ -443,6 +446,7 @@ def run_ours(args, rank, world, local):
                   "us_per_layer": round(layer_us, 3),
                   "bytes_per_layer": int(layer_bytes)},
         "expert_ffn": expert_ffn,
+        "batched_layer": batched_layer,
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clocks,
@@ -459,6 +463,29 @@ def run_ours(args, rank, world, local):
             out["offload"] = {"error": str(e)[:200]}
     if world > 1:
         dist.destroy_process_group()
+    return out
+
+
+def run_batched_layer(fb, torch, layer, ws, stream):
+    """Configs 4 and 5 through floe_gpu_layer_forward_batched on layer 0 of the
+    bench model: B decode tokens (config 4: B = 16, 64) and a 4,096-token
+    prefill (config 5 on one GPU; device routing and dispatch, prefill GEMMs,
+    tensor-core mixing).  Tokens token_input(1, 7000 + t)."""
+    out = {}
+    for B, key in ((16, "config4_b16"), (64, "config4_b64"), (EP_TOKENS, "config5_prefill")):
+        H = torch.stack([fb.gen_normals(1, (1 << 40) + 7000 + t, DH) for t in range(B)])
+        Y = torch.empty_like(H)
+        for _ in range(2):
+            fb.layer_forward_batched(layer, H, ws, out=Y)
+        torch.cuda.synchronize()
+        n = 5
+        ms = time_region(torch, lambda i: fb.layer_forward_batched(layer, H, ws, out=Y), n, stream) / n
+        out[key] = {"tokens": B, "ms_per_call": round(ms, 3), "value": round(B / (ms * 1e-3), 1),
+                    "unit": "layer-tokens/s"}
+    out["note"] = ("one Mixtral MoE layer, B tokens per call: <= 40 tokens go token by token "
+                   "through the fused layer kernel; experts with >= 8 tokens through the prefill "
+                   "path (exact tcgen05 up projection or dequantized f16 hi/lo GEMM, dense f16 "
+                   "gate/down GEMMs)")
     return out
 
 
