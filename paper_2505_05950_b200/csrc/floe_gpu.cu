@@ -373,14 +373,12 @@ int launch_v2_dh(const FusedLaunch &L, floe_gpu_workspace *ws, cudaStream_t st) 
     cudaFuncGetAttributes(&fa, V::fused<DH>);
     return fa.sharedSizeBytes;
   }();
-  const uint32_t other = V::smem_layout(DH, 0, max_tiles, G).total;
-  const int64_t budget = (int64_t)optin - (int64_t)static_smem - (int64_t)other - 1024;
-  // stages: a multiple of the consumer warp count (stage ownership in phases A/B)
-  const uint32_t ns = (uint32_t)std::min<int64_t>(V::kMaxStages, budget / V::tile_bytes(DH)) /
-                      V::kPairs * V::kPairs;
-  if (ns < (uint32_t)V::kPairs)
-    return fail(FLOE_ERR_UNSUPPORTED, "fused path: shared memory too small for the ring");
+  // ring stages: fixed per d_hidden (a multiple of the consumer warp pairs:
+  // stage ownership in phases A/B)
+  const uint32_t ns = V::ring_stages(DH);
   const uint32_t smem = V::smem_layout(DH, ns, max_tiles, G).total;
+  if ((int64_t)smem + (int64_t)static_smem + 1024 > (int64_t)optin)
+    return fail(FLOE_ERR_UNSUPPORTED, "fused path: shared memory too small for the ring");
 
   V::FusedArgs a{};
   a.has_mixing = L.mixing != nullptr;

@@ -433,6 +433,15 @@ __device__ __forceinline__ void mark(const FusedArgs &a, int k) {
   if (a.phase_ns && k < kTraceSlots) a.phase_ns[blockIdx.x * kTraceSlots + k] = gtime();
 }
 
+// Ring geometry, fixed per d_hidden so every ring index is a shift or a
+// multiply by a constant (the producer is one thread: a runtime division on
+// each issued copy costs ~100 cycles on its critical path).
+__host__ __device__ constexpr uint32_t ring_stages(uint32_t dh) { return dh == 4096 ? 8u : 16u; }
+__host__ __device__ constexpr uint32_t rec_stages(uint32_t dh) {
+  return (ring_stages(dh) * tile_bytes(dh) + xtab_bytes(dh)) / (4u * dh);
+}
+constexpr uint32_t kSlotShift = 24;  // kept-list entry: kValid | slot << 24 | channel
+
 // Tile i of the launch (tile-granular split of slots x tiles_per_expert over
 // the grid, slots interleaved: every CTA gets the same channel range of each
 // slot, so its kept-record count does not depend on which expert keeps more
@@ -445,6 +454,17 @@ __device__ __forceinline__ TileRef tile_ref(uint32_t i, uint32_t slots, uint32_t
   TileRef r;
   r.slot = i % slots;
   r.t = i / slots;
+  r.nc = min((uint32_t)kTileCh, di - r.t * kTileCh);
+  r.f0 = r.slot * di + r.t * kTileCh;
+  return r;
+}
+
+// tile_ref without runtime divisions for 1 or 2 slots (the expert call, top-2)
+__device__ __forceinline__ TileRef tile_ref2(uint32_t i, uint32_t slots, uint32_t di) {
+  if (slots > 2) return tile_ref(i, slots, di);
+  TileRef r;
+  r.slot = slots == 2 ? (i & 1u) : 0u;
+  r.t = slots == 2 ? (i >> 1) : i;
   r.nc = min((uint32_t)kTileCh, di - r.t * kTileCh);
   r.f0 = r.slot * di + r.t * kTileCh;
   return r;
@@ -505,14 +525,14 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   const uint32_t G = gridDim.x, b = blockIdx.x;
   const bool producer = warp == kConsumerWarps;
   const bool router_warp = warp == kConsumerWarps + 1;
-  const SmemLayout L = smem_layout(DH, a.ns, a.max_tiles, G);
+  constexpr uint32_t ns = ring_stages(DH);
+  const SmemLayout L = smem_layout(DH, ns, a.max_tiles, G);
   uint8_t *ring = smem + L.ring;
   float *hs = reinterpret_cast<float *>(smem + L.ubuf);  // phase A: h; then x (u), f32
   uint8_t *xtab = smem + L.uni;
   float *xs = reinterpret_cast<float *>(smem + L.xs);
   uint32_t *lf = reinterpret_cast<uint32_t *>(smem + L.lf);
   float *lv = reinterpret_cast<float *>(smem + L.lv);
-  const uint32_t ns = a.ns;
   const uint32_t list_cap = kTileCh * a.max_tiles;
 
   // Streamed weights (read once per call) go through L2 as evict-first, so the
@@ -534,7 +554,8 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
   // Phase C re-carves the ring plus the x-table area (both free once every K1
   // tile is consumed) into 4*DH-byte record stages with their own barriers:
   // 12 records (192 KB) in flight at d_hidden 4096.
-  const uint32_t nsC = min((uint32_t)kMaxStages, (L.ubuf - L.ring) / REC_B);
+  constexpr uint32_t nsC = rec_stages(DH);
+  static_assert(nsC <= (uint32_t)kMaxStages, "record ring");
   auto stageC = [&](uint32_t k) { return ring + (k % nsC) * REC_B; };
   auto issueC = [&](uint32_t k, const void *src, float scale) {
     if (k >= nsC) floe_ptx::mbar_wait(&emptyC[k % nsC], ((k / nsC) + 1) & 1u, (5u << 28) | k);
@@ -648,7 +669,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
       floe_ptx::mbar_arrive_expect_tx(&ubar, 4u * DH);
       floe_ptx::bulk_g2s(hs, a.has_mixing ? a.u : a.x, 4u * DH, &ubar);
       for (uint32_t j = 0; j < nB; ++j) {
-        const TileRef tr = tile_ref(tile_lo + j, a.slots, a.di);
+        const TileRef tr = tile_ref2(tile_lo + j, a.slots, a.di);
         wait_empty(u);
         issue(u++, ptiles_s[tr.slot] + (size_t)tr.t * TILE_B, TILE_B);
       }
@@ -657,7 +678,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
         floe_ptx::mbar_wait(&routebar, 0, 7u << 28);
         if (!spec_ok)  // misprediction: the exact experts' tiles follow
           for (uint32_t j = 0; j < nB; ++j) {
-            const TileRef tr = tile_ref(tile_lo + j, a.slots, a.di);
+            const TileRef tr = tile_ref2(tile_lo + j, a.slots, a.di);
             wait_empty(u);
             issue(u++, etiles_s[tr.slot] + (size_t)tr.t * TILE_B, TILE_B);
           }
@@ -683,7 +704,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
         // path issues the rest (the whole ring is free by then)
         while (k_early < r_max && !floe_ptx::mbar_test_wait(&listbar, 0)) {
           if ((ld_acquire_s(&lf[k_early]) & kValid) && stages_free(k_early)) {
-            const uint32_t r = k_early, f = lf[r] & ~kValid, s2 = f / a.di, c = f - s2 * a.di;
+            const uint32_t r = k_early, f = lf[r], s2 = (f >> kSlotShift) & 0x7fu, c = f & 0xffffffu;
             issueC(r, rec_s[s2] + (size_t)c * 2 * DH, lv[r] * w_s[s2]);
             ++k_early;
           } else {
@@ -699,7 +720,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
     const uint32_t n_own = n_list;
     const uint32_t P = min(n_own, nsC);  // the first ring fill: always this CTA's own
     auto own_item = [&](uint32_t k) {
-      const uint32_t f = lf[k] & ~kValid, s2 = f / a.di, c = f - s2 * a.di;
+      const uint32_t f = lf[k], s2 = (f >> kSlotShift) & 0x7fu, c = f & 0xffffffu;
       issueC(k, rec_s[s2] + (size_t)c * 2 * DH, lv[k] * w_s[s2]);
     };
     if (lane == 0) {
@@ -733,9 +754,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
         const uint32_t pr = (b ^ 1u) & 1u;
         for (uint32_t k = 0; k < take; ++k) {
           const uint32_t f =
-              floe_ptx::ld_cluster_u32(floe_ptx::mapa(&lf[pfirst + k], pr)) & ~kValid;
+              floe_ptx::ld_cluster_u32(floe_ptx::mapa(&lf[pfirst + k], pr));
           const float v = __uint_as_float(floe_ptx::ld_cluster_u32(floe_ptx::mapa(&lv[pfirst + k], pr)));
-          const uint32_t s2 = f / a.di, c = f - s2 * a.di;
+          const uint32_t s2 = (f >> kSlotShift) & 0x7fu, c = f & 0xffffffu;
           issueC(own + k, rec_s[s2] + (size_t)c * 2 * DH, v * w_s[s2]);
         }
         floe_ptx::mbar_arrive_remote(floe_ptx::mapa(&donebar, pr));  // done reading its list
@@ -1126,7 +1147,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
     for (uint32_t j = 0; j < nB; ++j) {
       const uint32_t u = u0 + j;
       if ((u % 8) / 2 != quad) continue;
-      const TileRef tr = tile_ref(tile_lo + j, a.slots, a.di);
+      const TileRef tr = tile_ref2(tile_lo + j, a.slots, a.di);
       wait_full(u);
       float2 v2 = all_finite ? k1_tile<DH>(stage(u), xtab, xs, mult, zx, lane, sub)
                              : k1_tile_f32<DH>(stage(u), hs, lane, sub);
@@ -1170,12 +1191,12 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
       if (ka) {
         const uint32_t pos = base + __popc(ba & lt);
         lv[pos] = v2.x;
-        st_release_s(&lf[pos], (tr.f0 + g) | kValid);  // read early by the producer
+        st_release_s(&lf[pos], kValid | (tr.slot << kSlotShift) | (tr.t * kTileCh + g));  // read early by the producer
       }
       if (kb) {
         const uint32_t pos = base + na + __popc(bbal & lt);
         lv[pos] = v2.y;
-        st_release_s(&lf[pos], (tr.f0 + g + 8) | kValid);
+        st_release_s(&lf[pos], kValid | (tr.slot << kSlotShift) | (tr.t * kTileCh + g + 8));
       }
     }
   };
@@ -1218,9 +1239,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
     cbar();
     if (a.kept_out)
       for (uint32_t i = t; i < n_items; i += kConsumers) {
-        const uint32_t f = lf[i] & ~kValid, s = f / a.di;
+        const uint32_t f = lf[i], s = (f >> kSlotShift) & 0x7fu;
         const uint32_t pos = kbase_s[s] + atomicAdd(&kpos_s[s], 1u);
-        a.kept_out[(size_t)s * a.di + pos] = f - s * a.di;
+        a.kept_out[(size_t)s * a.di + pos] = f & 0xffffffu;
       }
     cbar();
     if (t == 0) {

@@ -121,16 +121,6 @@ __device__ __forceinline__ void mbar_spin(uint64_t *bar, uint32_t parity, uint32
   }
 }
 
-__device__ __forceinline__ TileRef tile_ref2(uint32_t i, uint32_t slots, uint32_t di) {
-  if (slots != 2) return tile_ref(i, slots, di);
-  TileRef r;
-  r.slot = i & 1u;
-  r.t = i >> 1;
-  r.nc = min((uint32_t)kTileCh, di - r.t * kTileCh);
-  r.f0 = r.slot * di + r.t * kTileCh;
-  return r;
-}
-
 template <int DH>
 __device__ __forceinline__ const float *layer_in(const DecodeArgs &a, uint32_t l) {
   if (a.replay) return a.h + (size_t)l * DH;
@@ -142,14 +132,6 @@ __device__ __forceinline__ float *layer_out(const DecodeArgs &a, uint32_t l) {
   return l + 1 == a.n_layers ? a.y : a.buf + (l & 1u) * DH;
 }
 
-// Ring geometry, fixed per d_hidden so every ring index is a shift or a
-// multiply by a constant (the producer is one thread: a runtime division on
-// each issued copy costs ~100 cycles on its critical path).
-__host__ __device__ constexpr uint32_t ring_stages(uint32_t dh) { return dh == 4096 ? 8u : 16u; }
-__host__ __device__ constexpr uint32_t rec_stages(uint32_t dh) {
-  return (ring_stages(dh) * tile_bytes(dh) + xtab_bytes(dh)) / (4u * dh);
-}
-constexpr uint32_t kSlotShift = 24;  // kept-list entry: kValid | slot << 24 | channel
 
 template <int DH>
 __global__ void __launch_bounds__(kThreads, 1) decode(const DecodeArgs a) {
