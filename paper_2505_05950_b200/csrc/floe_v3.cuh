@@ -574,6 +574,17 @@ __global__ void __launch_bounds__(kThreads, 1) decode(const DecodeArgs a) {
     bool fin_all;
     float S, invS;
     x_scale(fin_all, S, invS);
+    {  // x again from shared memory (not kept live across the barrier: registers)
+      const float4 *x4 = reinterpret_cast<const float4 *>(hs + (act ? 64 * span + 16 * tig : 0));
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float4 f = x4[i];
+        xv[4 * i] = f.x;
+        xv[4 * i + 1] = f.y;
+        xv[4 * i + 2] = f.z;
+        xv[4 * i + 3] = f.w;
+      }
+    }
     if (act && fin_all) {
       int X[16];
 #pragma unroll
