@@ -126,11 +126,14 @@ def _mispredict_run(out_path):
     np.save(out_path, y)
 
 
-def test_misprediction_path(tmp_path):
+@pytest.mark.parametrize("env_var", ["FLOE_TEST_MISPREDICT", "FLOE_COOP", "FLOE_PAIRS"])
+def test_launch_variants_agree(tmp_path, env_var):
+    """The misprediction re-run path, the cooperative launch (no CTA pairs) and
+    the unpaired launch give the default launch's outputs."""
     outs = []
-    for flag in ("0", "1"):
+    for flag in (("0", "1") if env_var != "FLOE_PAIRS" else ("1", "0")):
         out = tmp_path / f"y{flag}.npy"
-        env = dict(os.environ, FLOE_TEST_MISPREDICT=flag)
+        env = dict(os.environ, **{env_var: flag})
         code = (f"import sys; sys.path.insert(0, {str(ROOT)!r}); sys.path.insert(0, {str(ROOT / 'tests')!r}); "
                 f"import test_gpu_multi as t; t._mispredict_run({str(out)!r})")
         r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True,
