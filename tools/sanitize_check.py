@@ -1,6 +1,7 @@
 """Small workloads for compute-sanitizer (memcheck / racecheck / synccheck):
 the fused kernel in expert and layer mode (fast path), the generic kernels,
-the batched tcgen05 up projection and batched expert forward.  Run with
+the batched tcgen05 up projection and batched expert forward, the prefill
+path, and the multi-layer decode kernel.  Run with
 FLOE_LIB=tools/libfloe_b200_sanitize.so (600 s barrier watchdog)."""
 import sys
 from pathlib import Path
@@ -52,6 +53,29 @@ def main():
     X = torch.from_numpy(np.stack([O.token_input(1, i, 2048) for i in range(5)])).cuda()
     fb.qgemv_channels_batched(e3, X)
     fb.expert_forward_batched(e3, X)
+    # the prefill path (exact batched K1 at 5 tokens; dequantized GEMM at 80)
+    fb.expert_forward_prefill(e3, X)
+    X80 = torch.from_numpy(np.stack([O.token_input(1, 100 + i, 2048) for i in range(80)])).cuda()
+    fb.expert_forward_prefill(e3, X80)
+    # the multi-layer decode kernel: 3 layers (f16 mixing), replay and chained,
+    # two tokens (the second layer boundary takes the finish-order chunks)
+    layers3 = []
+    for li in range(3):
+        exs = []
+        for j in range(4):
+            gj, uj, dj = O.seeded_expert(dh, di, 40 + 4 * li + j)
+            qj = O.quantize(uj, 2, 64)
+            exs.append(fb.GpuExpert(dh, di, 2, 64, qj.codes, qj.scales, qj.zeros, gate=gj, down=dj,
+                                    threshold=t))
+        layers3.append(fb.GpuLayer((rng.standard_normal((4, dh)) / 45).astype(np.float32),
+                                   (rng.standard_normal((dh, dh)) / 45).astype(np.float32), exs, 2,
+                                   mixing_f16=True))
+    model = fb.GpuModel(layers3)
+    assert model.multi_layer
+    hs = torch.from_numpy(np.stack([O.token_input(1, 50 + i, dh) for i in range(3)])).cuda()
+    for _ in range(2):
+        model.decode(hs, ws, replay=True)
+    model.decode(hs[0], ws)
     torch.cuda.synchronize()
     print("sanitize workload ok")
 
