@@ -33,3 +33,8 @@ clean:
 # FLOE_LIB=tools/libfloe_b200_sanitize.so.
 tools/libfloe_b200_sanitize.so: $(SRCS) $(HDRS)
 	$(NVCC) $(NVFLAGS) -DFLOE_WATCHDOG_NS=600000000000ull -shared -cudart static -o $@ $(SRCS) -lcublasLt 2> /dev/null
+
+# racecheck build: as above, with the early record polling compiled out
+# (racecheck does not model shared-memory release/acquire; floe_v2.cuh).
+tools/libfloe_b200_racecheck.so: $(SRCS) $(HDRS)
+	$(NVCC) $(NVFLAGS) -DFLOE_WATCHDOG_NS=600000000000ull -DFLOE_RACECHECK -shared -cudart static -o $@ $(SRCS) -lcublasLt 2> /dev/null

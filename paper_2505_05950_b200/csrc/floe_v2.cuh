@@ -317,6 +317,22 @@ __device__ __forceinline__ void grid_arrive_wait(unsigned long long *bar, uint32
 
 
 
+// Early record issue: the producer polls the kept list (release/acquire on
+// shared-memory flag words) and streams records before K1 ends.
+// compute-sanitizer's racecheck does not model release/acquire on shared
+// memory and reports every such handoff as a hazard; the racecheck build
+// (-DFLOE_RACECHECK) compiles the polling out, so the list is read only after
+// the mbarrier that closes it, and racecheck checks everything else.
+// The same build also makes every consumer thread observe the mbarriers that
+// one thread waited on before a named-barrier handoff (racecheck only credits
+// the thread that waited; floe_v3.cuh phase A).
+#ifdef FLOE_RACECHECK
+constexpr bool kRacecheck = true;
+#else
+constexpr bool kRacecheck = false;
+#endif
+constexpr bool kEarlyRecords = !kRacecheck;
+
 // shared-memory flag words of the producer <-> consumer list protocol
 __device__ __forceinline__ uint32_t ld_acquire_s(const uint32_t *p) {
   uint32_t v;
@@ -703,8 +719,9 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
         // never blocks past the end of K1: once the list is final the normal
         // path issues the rest (the whole ring is free by then)
         while (k_early < r_max && !floe_ptx::mbar_test_wait(&listbar, 0)) {
-          if ((ld_acquire_s(&lf[k_early]) & kValid) && stages_free(k_early)) {
-            const uint32_t r = k_early, f = lf[r], s2 = (f >> kSlotShift) & 0x7fu, c = f & 0xffffffu;
+          const uint32_t f = kEarlyRecords ? ld_acquire_s(&lf[k_early]) : 0u;
+          if ((f & kValid) && stages_free(k_early)) {
+            const uint32_t r = k_early, s2 = (f >> kSlotShift) & 0x7fu, c = f & 0xffffffu;
             issueC(r, rec_s[s2] + (size_t)c * 2 * DH, lv[r] * w_s[s2]);
             ++k_early;
           } else {
@@ -836,13 +853,13 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
       if (a.debug & 8u) plg = -plg;  // test hook: force a misprediction
       const uint32_t ptaken = warp_topk(lane < a.n_experts ? plg : -__int_as_float(0x7f800000),
                                         lane, a.n_experts, a.top_k);
-      if ((ptaken >> lane) & 1u) {
-        const uint32_t i = __popc(ptaken & ((1u << lane) - 1));
-        ptiles_s[i] = reinterpret_cast<const uint8_t *>(table_s[lane].tiles);
-        pthr_s[i] = a.use_threshold ? a.threshold : table_s[lane].threshold;
-      }
-      __syncwarp();
-      if (lane == 0) {
+      if (lane == 0) {  // the thread that arrives writes them (producer reads after predbar)
+        uint32_t i = 0;
+        for (uint32_t m = ptaken; m; m &= m - 1, ++i) {
+          const uint32_t e = __ffs(m) - 1;
+          ptiles_s[i] = reinterpret_cast<const uint8_t *>(table_s[e].tiles);
+          pthr_s[i] = a.use_threshold ? a.threshold : table_s[e].threshold;
+        }
         ptaken_s = ptaken;
         mark(a, 26);
         floe_ptx::mbar_arrive(&predbar);
@@ -902,6 +919,7 @@ __global__ void __launch_bounds__(kThreads, 1) fused(const FusedArgs a) {
         rps[i] = a.router_pred[(size_t)e * DH + r_lo + lr];
       }
     }
+  if (rs_ok) cbar();  // warp 0 reads every consumer's router rows in phase A
   pdl_wait();  // from here on: workspace, inputs and outputs shared with the previous grid
   if (t == 0) mark(a, 11);
   if (!a.has_mixing && a.y && !a.k1_only) {

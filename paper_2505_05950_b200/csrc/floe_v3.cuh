@@ -344,8 +344,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode(const DecodeArgs a) {
         };
         while (k_early < nsC && (K + k_early) % nsC < c_lim &&
                !floe_ptx::mbar_test_wait(&listbar, P)) {
-          if ((ld_acquire_s(&lf[k_early]) & kValid) && stages_free((K + k_early) % nsC)) {
-            const uint32_t r = k_early, f = lf[r], s2 = (f >> kSlotShift) & 0x7fu, c = f & 0xffffffu;
+          const uint32_t f = kEarlyRecords ? ld_acquire_s(&lf[k_early]) : 0u;
+          if ((f & kValid) && stages_free((K + k_early) % nsC)) {
+            const uint32_t r = k_early, s2 = (f >> kSlotShift) & 0x7fu, c = f & 0xffffffu;
             issueC(K + r, rec_s[s2] + (size_t)c * 2 * DH, lv[r] * w_s[s2], l2_stream);
             ++k_early;
           } else {
@@ -410,6 +411,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode(const DecodeArgs a) {
         floe_ptx::mbar_arrive_expect_tx(&hbar, 4u * DH);
         floe_ptx::bulk_g2s(hs, layer_in<DH>(a, l + 1), 4u * DH, &hbar);
         mark_prev(27);
+      } else {
+        // no chunk: thread 0 arrived right after the ticket; every phase of
+        // lpass is waited on (no arrival on an unobserved phase)
+        mbar_spin(&lpass, P, 21u << 28);
       }
     }
     return;
@@ -478,13 +483,13 @@ __global__ void __launch_bounds__(kThreads, 1) decode(const DecodeArgs a) {
         float plg = sum_partials(a.pred_partial, NCH);
         if (a.debug & 8u) plg = -plg;
         const uint32_t ptaken = warp_topk(lane < E ? plg : -__int_as_float(0x7f800000), lane, E, a.top_k);
-        if ((ptaken >> lane) & 1u) {
-          const uint32_t i = __popc(ptaken & ((1u << lane) - 1));
-          ptiles_s[i] = reinterpret_cast<const uint8_t *>(tab[lane].tiles);
-          pthr_s[i] = tab[lane].threshold;
-        }
-        __syncwarp();
-        if (lane == 0) {
+        if (lane == 0) {  // the thread that arrives writes them (producer reads after predbar)
+          uint32_t i = 0;
+          for (uint32_t m = ptaken; m; m &= m - 1, ++i) {
+            const uint32_t e = __ffs(m) - 1;
+            ptiles_s[i] = reinterpret_cast<const uint8_t *>(tab[e].tiles);
+            pthr_s[i] = tab[e].threshold;
+          }
           ptaken_s = ptaken;
           mark(26);
           floe_ptx::mbar_arrive(&predbar);
@@ -673,8 +678,14 @@ __global__ void __launch_bounds__(kThreads, 1) decode(const DecodeArgs a) {
         }
         mbar_spin(bar, par, (3u << 28) | lane);  // all lanes at once
       }
-      ++owned;
       cbar();
+      if (kRacecheck) {
+        floe_ptx::mbar_wait(&hbar, owned & 1u, 3u << 28);
+        floe_ptx::mbar_wait(&rbar, owned & 1u, 3u << 28);
+        for (uint32_t j = 0; j < PRE; ++j)
+          floe_ptx::mbar_wait(&fullC[(K + j) % nsC], ((K + j) / nsC) & 1u, 3u << 28);
+      }
+      ++owned;
       mark(7);
       // u rows: group g takes items g, g + 2, ...; thread gt owns elements
       // [EPT2 gt, EPT2 gt + EPT2) of both rows of an item
@@ -702,6 +713,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode(const DecodeArgs a) {
         if (grp + 2 * i0 + 2 >= PRE) {  // an item past the prefetched ones
           if (gw == 0 && lane < 2) mbar_spin(&fullC[lane ? stg1 : stg0], lane ? ph1 : ph0, (4u << 28) | lane);
           gbar(grp);
+          if (kRacecheck) {
+            floe_ptx::mbar_wait(&fullC[stg0], ph0, 4u << 28);
+            floe_ptx::mbar_wait(&fullC[stg1], ph1, 4u << 28);
+          }
         }
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
