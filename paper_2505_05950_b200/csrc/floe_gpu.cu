@@ -26,6 +26,7 @@
 #include "floe_calib.cuh"
 #include "floe_blayer.cuh"
 #include "floe_prefill.cuh"
+#include "floe_k1b.cuh"
 #include <map>
 #include <tuple>
 
@@ -1084,6 +1085,65 @@ int launch_batched(const floe_tc::BatchedArgs &a, cudaStream_t st) {
   CK_LAUNCH();
   return FLOE_OK;
 }
+// Small batches (<= floe_k1b::kMaxTokens): the IMMA kernel, 8 tokens per pass.
+// Returns FLOE_ERR_UNSUPPORTED (nothing launched) when the layout does not fit
+// shared memory; the caller then takes the tcgen05 kernel.
+size_t k1b_smem(uint32_t dh, uint32_t di, uint32_t *grid) {
+  const uint32_t NI = (di + 15u) / 16u * floe_k1b::kItems;
+  const uint32_t G = std::min<uint32_t>((uint32_t)device_info().sm, NI);
+  if (grid) *grid = G;
+  return floe_k1b::smem_layout(dh, floe_k1b::tiles_per_cta(di, G)).total;
+}
+constexpr size_t kK1bSmemMax = 220u * 1024u;
+template <int DH>
+int launch_k1b(const floe_gpu_expert *e, const float *x, uint32_t B, float *v_out, float *invS,
+               uint8_t *xt, float *xs, cudaStream_t st) {
+  uint32_t G = 0;
+  const size_t sm = k1b_smem(DH, e->di, &G);
+  if (int rc = set_smem(floe_k1b::k1<DH>, sm)) return rc;
+  for (uint32_t p0 = 0; p0 < B; p0 += floe_k1b::kTok) {
+    const uint32_t nb = std::min<uint32_t>(floe_k1b::kTok, B - p0);
+    floe_k1b::limbs<DH><<<DH / 64, 256, 0, st>>>(x + (size_t)p0 * DH, nb, invS + p0, xt, xs,
+                                             v_out + (size_t)p0 * e->di, e->di, G);
+    floe_k1b::Args a{e->host_desc.tiles, e->di, nb, xt, xs, invS + p0, v_out + (size_t)p0 * e->di,
+                     nullptr};
+    static const bool trace = std::getenv("FLOE_K1B_TRACE") != nullptr;
+    if (trace) {
+      CK(cudaMalloc(&a.trace, 8ull * 8 * G));
+      CK(cudaMemsetAsync(a.trace, 0, 8ull * 8 * G, st));
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(floe_k1b::kThreads);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // tiles stream during limbs()
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, floe_k1b::k1<DH>, a));
+    if (trace) {  // diagnostics: per-CTA marks (us) from the first CTA start
+      std::vector<unsigned long long> h(8ull * G);
+      CK(cudaStreamSynchronize(st));
+      CK(cudaMemcpy(h.data(), a.trace, h.size() * 8, cudaMemcpyDeviceToHost));
+      unsigned long long t0 = ~0ull;
+      for (uint32_t b = 0; b < G; ++b) t0 = std::min(t0, h[8ull * b]);
+      for (uint32_t b : {0u, G / 3, G / 2, G - 1}) {
+        std::fprintf(stderr, "[k1b] cta %u:", b);
+        for (int k = 0; k < 6; ++k) std::fprintf(stderr, " %d:%.2f", k, (h[8ull * b + k] - t0) / 1e3);
+        std::fprintf(stderr, "\n");
+      }
+      double mx[6] = {0};
+      for (uint32_t b = 0; b < G; ++b)
+        for (int k = 0; k < 6; ++k) mx[k] = std::max(mx[k], (h[8ull * b + k] - t0) / 1e3);
+      std::fprintf(stderr, "[k1b] max: %.2f %.2f %.2f %.2f %.2f %.2f\n", mx[0], mx[1], mx[2], mx[3], mx[4], mx[5]);
+      cudaFree(a.trace);
+    }
+  }
+  CK_LAUNCH();
+  return FLOE_OK;
+}
 // Gate/down stage of the batched expert forward (after the batched K1 wrote
 // v): union of kept channels, gate dots (tcgen05 GEMM or CUDA-core warps),
 // down product (tcgen05 GEMM or CUDA-core tiles) into y.  Scratch layout as
@@ -1161,6 +1221,27 @@ int floe_gpu_qgemv_channels_batched(const floe_gpu_expert *e, const float *x, ui
                 "qgemv_channels_batched: needs the tile layout (bits 2, d_hidden 2048/4096, g %% 64 == 0)");
   if (int rc = require_device("qgemv_channels_batched")) return rc;
   cudaStream_t st = S(stream);
+  // up to 16 tokens: the IMMA kernel (floe_k1b.cuh); FLOE_K1_IMMA_MAX moves
+  // the switch (0: always the tcgen05 kernel)
+  static const uint32_t imma_max = [] {
+    const char *p = std::getenv("FLOE_K1_IMMA_MAX");
+    return p ? (uint32_t)std::atoi(p) : (uint32_t)floe_k1b::kDefaultMax;
+  }();
+  if (n_tokens <= std::min<uint32_t>(imma_max, floe_k1b::kMaxTokens) &&
+      k1b_smem(e->dh, e->di, nullptr) <= kK1bSmemMax) {
+    keep_pool();
+    const size_t o_xs = 256, o_xt = (o_xs + floe_k1b::xs_bytes(e->dh) + 1023) & ~size_t(1023);
+    uint8_t *scratch = nullptr;  // invS | xs | xt (stream-ordered)
+    CK(cudaMallocAsync(reinterpret_cast<void **>(&scratch), o_xt + floe_k1b::xt_bytes(e->dh), st));
+    float *invS = reinterpret_cast<float *>(scratch);
+    const int rc = e->dh == 4096
+                       ? launch_k1b<4096>(e, x, n_tokens, v_out, invS, scratch + o_xt,
+                                          reinterpret_cast<float *>(scratch + o_xs), st)
+                       : launch_k1b<2048>(e, x, n_tokens, v_out, invS, scratch + o_xt,
+                                          reinterpret_cast<float *>(scratch + o_xs), st);
+    cudaFreeAsync(scratch, st);
+    return rc;
+  }
   const uint32_t Bp = floe_tc::padded_tokens(n_tokens), spans = e->dh / 64;
   const size_t xl_bytes = (size_t)spans * floe_tc::xl_span_bytes(n_tokens);
   const size_t xs_bytes = 4ull * spans * Bp;

@@ -88,6 +88,29 @@ def test_batched_nonfinite_token_isolated(fb, torch):
     _check(q, 2048, X, V, [0, 2])
 
 
+@pytest.mark.parametrize("B", [9, 12])
+def test_small_batch_imma_path_two_passes(fb, torch, mixtral, B):
+    """<= 16 tokens run on the IMMA kernel (floe_k1b.cuh) in passes of 8: a
+    partial second pass, every token against the oracle."""
+    q, e = mixtral
+    X = np.stack([O.token_input(4, t, 4096) * (1.0 + 0.25 * t) for t in range(B)])
+    V = fb.qgemv_channels_batched(e, torch.from_numpy(X).cuda()).cpu().numpy()
+    _check(q, 4096, X, V, range(B))
+
+
+def test_imma_and_tcgen05_paths_agree(fb, torch, mixtral):
+    """16 tokens take the IMMA kernel, 17 the tcgen05 kernel: the same exact
+    integer span sums and per-span f32 steps, so the shared tokens agree to the
+    last few ulps (only the order of the final partial sums differs)."""
+    _, e = mixtral
+    X = np.stack([O.token_input(5, t, 4096) for t in range(17)])
+    Xd = torch.from_numpy(X).cuda()
+    V16 = fb.qgemv_channels_batched(e, Xd[:16]).cpu().numpy()
+    V17 = fb.qgemv_channels_batched(e, Xd).cpu().numpy()
+    scale = np.abs(V17[:16]).max()
+    assert np.max(np.abs(V16 - V17[:16])) <= 1e-6 * scale
+
+
 def test_batched_argument_errors(fb, torch, mixtral):
     _, e = mixtral
     with pytest.raises(fb.FloeError):

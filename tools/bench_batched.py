@@ -1,4 +1,5 @@
-"""Throughput of the tcgen05 batched up projection (config 4's K1) on a
+"""Throughput of the batched up projection (config 4's K1: the IMMA kernel up
+to 16 tokens, the tcgen05 kernel above) on a
 Mixtral-shaped expert: one pass over the 18.35 MB of codes+meta for B tokens.
 Prints per-B time, tokens/s and achieved HBM GB/s of the algorithmic bytes
 (codes + meta + x + v), 4 distinct experts cycled (inputs > L2).
@@ -94,7 +95,7 @@ def main():
         exs.append(fb.GpuExpert(bench.DH, bench.DI, bench.BITS, bench.G, codes, scales, zeros))
         del up
     lines = []
-    for B in (1, 4, 16, 32, 64):
+    for B in (1, 4, 8, 16, 32, 64):
         X = torch.stack([fb.gen_normals(1, (1 << 40) + t, bench.DH) for t in range(B)])
         for i in range(5):
             fb.qgemv_channels_batched(exs[i % len(exs)], X)
@@ -111,6 +112,7 @@ def main():
              "tokens": B, "us_per_call": round(us, 2), "token_expert_per_s": round(B / (us * 1e-6), 1),
              "bytes": byts, "gbs": round(byts / (us * 1e-6) / 1e9, 1), "hbm_peak_gbs": hbm_peak,
              "frac": round(byts / (us * 1e-6) / 1e9 / hbm_peak, 4),
+             "kernel": "floe_k1b::k1 (IMMA)" if B <= 16 else "floe_tc::k1_batched (tcgen05)",
              "note": "includes the per-call token prep kernels and stream-ordered scratch alloc"}
         print(json.dumps(d), flush=True)
         lines.append(d)

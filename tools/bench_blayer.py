@@ -18,7 +18,8 @@ def main():
     st = torch.cuda.current_stream()
     layers, _ = bench.build_model(fb, torch, 2)
     ws = fb.Workspace(bench.DH, bench.DI, bench.TOPK)
-    for B in (1, 4, 16, 64, 256, 1024, 4096):
+    Bs = [int(b) for b in sys.argv[1].split(",")] if len(sys.argv) > 1 else (1, 4, 16, 64, 256, 1024, 4096)
+    for B in Bs:
         H = torch.stack([fb.gen_normals(1, (1 << 40) + 7000 + t, bench.DH) for t in range(B)])
         fb.layer_forward_batched(layers[0], H)
         torch.cuda.synchronize()
