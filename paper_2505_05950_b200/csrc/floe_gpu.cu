@@ -2701,12 +2701,23 @@ int floe_gpu_model_decode_host(floe_gpu_model *m, floe_gpu_workspace *ws, const 
   if (!m || !ws || !h_host || !y_host) return fail(FLOE_ERR_INVALID, "model_decode: null argument");
   cudaStream_t st = S(stream);
   const size_t bytes = 4ull * m->dh * (replay ? m->layers.size() : 1);
-  std::memcpy(m->pin_in, h_host, bytes);
-  CK(cudaMemcpyAsync(m->hin, m->pin_in, bytes, cudaMemcpyHostToDevice, st));
+  // page-locked caller buffers are copied directly; pageable ones go through
+  // the model's pinned staging buffers (a host memcpy each way)
+  auto page_locked = [](const void *p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  };
+  const bool direct_in = page_locked(h_host), direct_out = page_locked(y_host);
+  if (!direct_in) std::memcpy(m->pin_in, h_host, bytes);
+  CK(cudaMemcpyAsync(m->hin, direct_in ? h_host : m->pin_in, bytes, cudaMemcpyHostToDevice, st));
   if (int rc = floe_gpu_model_decode(m, ws, m->hin, m->hout, replay, stream)) return rc;
-  CK(cudaMemcpyAsync(m->pin_out, m->hout, bytes, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(direct_out ? y_host : m->pin_out, m->hout, bytes, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  std::memcpy(y_host, m->pin_out, bytes);
+  if (!direct_out) std::memcpy(y_host, m->pin_out, bytes);
   return FLOE_OK;
 }
 

@@ -109,6 +109,11 @@ def test_chained_decode(fb, torch, ref, stack):
     # order of the y additions (red.add from every CTA)
     got_h = model4.decode_host(h0, ws)
     assert O.rel_l2(got_h, got) <= 1e-5
+    # page-locked caller buffers are copied directly (no staging memcpy)
+    h_pin = torch.from_numpy(h0).pin_memory()
+    y_pin = torch.empty(DH, dtype=torch.float32).pin_memory()
+    model4.decode_host(h_pin.numpy(), ws, out=y_pin.numpy())
+    assert O.rel_l2(y_pin.numpy(), got) <= 1e-5
 
 
 def _mispredict_run(out_path):
