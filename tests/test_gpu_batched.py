@@ -65,7 +65,8 @@ def test_batched_agrees_with_batch1_kernel(fb, torch, mixtral):
         assert np.allclose(V[t], v1, rtol=4e-5, atol=4e-5)
 
 
-@pytest.mark.parametrize("dh,di,B", [(2048, 520, 7), (2048, 128, 1), (4096, 16, 33)])
+@pytest.mark.parametrize("dh,di,B", [(2048, 520, 7), (2048, 128, 1), (4096, 16, 33), (4096, 24, 5),
+                                     (2048, 40, 16)])
 def test_batched_ragged_shapes(fb, torch, dh, di, B):
     """d_intermediate not a multiple of the 128-channel block (or of a tile)."""
     q, e = _expert(fb, dh, di, 7)
