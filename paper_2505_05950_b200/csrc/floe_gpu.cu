@@ -1167,12 +1167,31 @@ int batched_gate_down(const floe_gpu_expert *e, const float *x, uint32_t B, floa
   uint32_t *amax = reinterpret_cast<uint32_t *>(inv_xsc + floe_tc::kMaxTokens);
   const int sm = device_info().sm;
   CK(cudaMemsetAsync(count, 0, 4, st));
-  floe_tc::hilo_token_scale<<<B, 256, 0, st>>>(x, DH, xsc, inv_xsc, amax);
-  CK_LAUNCH();
+  // <= 4 tokens on the CUDA cores: the fused union kernel (one pass over the
+  // records through a bulk-copy ring; FLOE_UNION_FUSED=0 keeps the two-kernel
+  // coeffs + down_accum path)
+  static const bool union_fused = [] {
+    const char *p = std::getenv("FLOE_UNION_FUSED");
+    return !(p && std::strcmp(p, "0") == 0);
+  }();
+  const bool fused = union_fused && !tc_gate && !tc_down && B <= (uint32_t)floe_tc::kUTok &&
+                     di <= (uint32_t)sm * floe_tc::kUMaxRows;
+  if (!fused) {
+    floe_tc::hilo_token_scale<<<B, 256, 0, st>>>(x, DH, xsc, inv_xsc, amax);
+    CK_LAUNCH();
+  }
   floe_tc::union_masks<<<(di + 255) / 256, 256, 0, st>>>(v, B, di, e->host_desc.threshold, count,
                                                          uc, um);
   CK_LAUNCH();
   const __half *rec = e->host_desc.records;
+  if (fused) {
+    CK(cudaMemsetAsync(y_out, 0, 4ull * B * DH, st));
+    const uint32_t usm = floe_tc::kUStages * 4u * DH;
+    if (int rc = set_smem(floe_tc::union_ffn<DH>, usm)) return rc;
+    floe_tc::union_ffn<DH><<<sm, floe_tc::kUThreads, usm, st>>>(rec, x, v, B, di, count, uc, um, y_out);
+    CK_LAUNCH();
+    return FLOE_OK;
+  }
   if (tc_gate) {
     floe_tc::x_hilo<<<DH / 64, 256, 0, st>>>(x, DH, B, xsc, xh);
     CK_LAUNCH();

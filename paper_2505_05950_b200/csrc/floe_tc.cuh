@@ -533,6 +533,164 @@ __global__ void __launch_bounds__(256) coeffs(const __half *__restrict__ records
   }
 }
 
+// ------------------------------------- fused union gate/down (<= 4 tokens)
+// expert_forward_sparse's phase C (model.cpp:136-140, la.cpp:25-31) over the
+// union of kept channels for up to 4 tokens in ONE pass over the records, the
+// decode kernel's way: one CTA per SM takes a contiguous range of union rows,
+// a producer warp streams each row's gate|down record (16 KB, one bulk copy)
+// through an 8-stage ring, and 16 consumer warps each own a 1/16 column slice
+// of x (registers) and of y (register accumulators).  Per batch of kUR records:
+// per-warp gate partials -> shared memory -> fixed-order sum, silu(g) * v (0
+// for a token that drops the channel) -> every warp adds a * down into its y
+// slice.  y gets one red.add per element per CTA at the end.  (coeffs +
+// down_accum read the records with per-thread loads and stayed latency-bound
+// at ~0.3 of HBM.)
+constexpr int kUTok = 4;                  // tokens
+constexpr int kUWarps = 16;               // consumer warps
+constexpr int kUThreads = 32 * (kUWarps + 1);
+constexpr int kUStages = 8;
+constexpr int kUR = 4;                    // records per barrier batch
+constexpr uint32_t kUMaxRows = 256;       // union rows per CTA (host checks n <= G * kUMaxRows)
+
+// PL consecutive f16 values (PL = 4: one 8-B load, PL % 8 == 0: 16-B loads)
+template <uint32_t PL>
+__device__ __forceinline__ void load_half_row(const __half *p, float (&f)[PL]) {
+  if constexpr (PL % 8 == 0) {
+#pragma unroll
+    for (uint32_t e = 0; e < PL; e += 8) {
+      const uint4 q = *reinterpret_cast<const uint4 *>(p + e);
+      const __half2 *h2 = reinterpret_cast<const __half2 *>(&q);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 v2 = __half22float2(h2[j]);
+        f[e + 2 * j] = v2.x;
+        f[e + 2 * j + 1] = v2.y;
+      }
+    }
+  } else {
+    static_assert(PL == 4, "union_ffn: 4 or a multiple of 8 elements per lane");
+    const uint2 q = *reinterpret_cast<const uint2 *>(p);
+    const float2 a = __half22float2(*reinterpret_cast<const __half2 *>(&q.x));
+    const float2 b = __half22float2(*reinterpret_cast<const __half2 *>(&q.y));
+    f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
+  }
+}
+
+template <int DH>
+__global__ void __launch_bounds__(kUThreads, 1) union_ffn(const __half *__restrict__ records,
+                                                         const float *__restrict__ x,
+                                                         const float *__restrict__ v, uint32_t B,
+                                                         uint32_t di,
+                                                         const uint32_t *__restrict__ count,
+                                                         const uint32_t *__restrict__ uc,
+                                                         const unsigned long long *__restrict__ um,
+                                                         float *__restrict__ y) {
+  constexpr uint32_t PL = DH / (32u * kUWarps);  // elements per lane (8 at dh 4096)
+  constexpr uint32_t RB = 4u * DH;               // record bytes (gate | down, f16)
+  extern __shared__ __align__(128) uint8_t ring[];  // [kUStages][RB]
+  __shared__ __align__(8) uint64_t full[kUStages], empty[kUStages];
+  __shared__ uint32_t rows_s[kUMaxRows];
+  __shared__ float va_s[kUMaxRows][kUTok];   // v of the token, or 0 if it drops the row
+  __shared__ float part[kUR][kUTok][kUWarps];
+  __shared__ float acoef[kUR][kUTok];
+  const uint32_t t = threadIdx.x, warp = t >> 5, lane = t & 31u;
+  const uint32_t G = gridDim.x, b = blockIdx.x, n = *count;
+  const uint32_t r0 = (uint32_t)((uint64_t)n * b / G), r1 = (uint32_t)((uint64_t)n * (b + 1) / G);
+  const uint32_t nr = min(r1 - r0, kUMaxRows);
+  if (t == 0) {
+    for (int s = 0; s < kUStages; ++s) {
+      floe_ptx::mbar_init(&full[s], 1);
+      floe_ptx::mbar_init(&empty[s], kUWarps);
+    }
+    floe_ptx::fence_barrier_init();
+  }
+  for (uint32_t i = t; i < nr; i += blockDim.x) rows_s[i] = uc[r0 + i];
+  __syncthreads();
+  auto spin = [](uint64_t *bar, uint32_t parity) {
+    while (!floe_ptx::mbar_test_wait(bar, parity)) {
+    }
+  };
+  if (warp == kUWarps) {
+    // ============================== producer ==============================
+    if (lane == 0)
+      for (uint32_t i = 0; i < nr; ++i) {
+        const uint32_t s = i % kUStages;
+        if (i >= (uint32_t)kUStages) spin(&empty[s], ((i / kUStages) - 1u) & 1u);
+        floe_ptx::mbar_arrive_expect_tx(&full[s], RB);
+        floe_ptx::bulk_g2s(ring + s * RB, records + (size_t)rows_s[i] * 2u * DH, RB, &full[s]);
+      }
+    return;
+  }
+  // ============================== consumers ===============================
+  for (uint32_t i = t; i < nr * kUTok; i += 32u * kUWarps) {
+    const uint32_t r = i / kUTok, tk = i % kUTok;
+    const bool keep = tk < B && ((um[r0 + r] >> tk) & 1ull);
+    va_s[r][tk] = keep ? v[(size_t)tk * di + rows_s[r]] : 0.0f;
+  }
+  const uint32_t k0 = warp * (DH / kUWarps) + lane * PL;  // this lane's columns
+  float xr[kUTok][PL], ya[kUTok][PL];
+#pragma unroll
+  for (int tk = 0; tk < kUTok; ++tk)
+#pragma unroll
+    for (uint32_t e = 0; e < PL; e += 4) {
+      const float4 q = (uint32_t)tk < B ? *reinterpret_cast<const float4 *>(x + (size_t)tk * DH + k0 + e)
+                                        : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      xr[tk][e] = q.x; xr[tk][e + 1] = q.y; xr[tk][e + 2] = q.z; xr[tk][e + 3] = q.w;
+      ya[tk][e] = ya[tk][e + 1] = ya[tk][e + 2] = ya[tk][e + 3] = 0.0f;
+    }
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * kUWarps) : "memory");  // va_s complete
+  for (uint32_t i0 = 0; i0 < nr; i0 += kUR) {
+    const uint32_t nb = min((uint32_t)kUR, nr - i0);
+    // gate partials of this warp's column slice
+    for (uint32_t rr = 0; rr < nb; ++rr) {
+      const uint32_t i = i0 + rr, s = i % kUStages;
+      spin(&full[s], (i / kUStages) & 1u);
+      float gf[PL];
+      load_half_row<PL>(reinterpret_cast<const __half *>(ring + s * RB) + k0, gf);
+#pragma unroll
+      for (int tk = 0; tk < kUTok; ++tk) {
+        float p = 0.0f;
+#pragma unroll
+        for (uint32_t e = 0; e < PL; ++e) p = fmaf(gf[e], xr[tk][e], p);
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+        if (lane == 0) part[rr][tk][warp] = p;
+      }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kUWarps) : "memory");
+    if (warp == 0 && lane < nb * kUTok) {  // a = silu(g) * v, fixed-order sum of the slices
+      const uint32_t rr = lane / kUTok, tk = lane % kUTok;
+      float gs = 0.0f;
+#pragma unroll
+      for (int w = 0; w < kUWarps; ++w) gs += part[rr][tk][w];
+      const float va = va_s[i0 + rr][tk];
+      acoef[rr][tk] = va != 0.0f ? floe_k::silu_ref(gs) * va : 0.0f;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kUWarps) : "memory");
+    for (uint32_t rr = 0; rr < nb; ++rr) {
+      const uint32_t i = i0 + rr, s = i % kUStages;
+      float a[kUTok], df[PL];
+#pragma unroll
+      for (int tk = 0; tk < kUTok; ++tk) a[tk] = acoef[rr][tk];
+      load_half_row<PL>(reinterpret_cast<const __half *>(ring + s * RB) + DH + k0, df);
+#pragma unroll
+      for (uint32_t e = 0; e < PL; ++e)
+#pragma unroll
+        for (int tk = 0; tk < kUTok; ++tk) ya[tk][e] = fmaf(a[tk], df[e], ya[tk][e]);
+      __syncwarp();
+      if (lane == 0) floe_ptx::mbar_arrive(&empty[s]);
+    }
+  }
+  if (nr > 0)
+#pragma unroll
+    for (int tk = 0; tk < kUTok; ++tk)
+      if ((uint32_t)tk < B)
+#pragma unroll
+        for (uint32_t e = 0; e < PL; e += 4)
+          floe_k::red_add_v4(y + (size_t)tk * DH + k0 + e, ya[tk][e], ya[tk][e + 1], ya[tk][e + 2],
+                             ya[tk][e + 3]);
+}
+
 // ---------------------------------------------- gate GEMM on tcgen05 (f16)
 // G[u][t] = gate_{c_u} . x_t for 128 union channels per CTA as one tensor-core
 // GEMM: A = the channels' f16 gate rows (gathered with cp.async, K-major

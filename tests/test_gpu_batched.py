@@ -3,6 +3,7 @@ floe_gpu_qgemv_channels_batched == qgemv_channels (quant.cpp:122-136) for every
 token of the batch, within the batch-1 K1 tolerance (exact integer group sums,
 f32 epilogue)."""
 import numpy as np
+from pathlib import Path
 import pytest
 
 from oracle import oracle as O
@@ -137,7 +138,7 @@ def mixtral_full(fb):
     return O.Expert(dh, di, q, gate, down, t), e
 
 
-@pytest.mark.parametrize("B", [1, 7, 16, 64])
+@pytest.mark.parametrize("B", [1, 3, 4, 7, 16, 64])
 def test_expert_forward_batched_matches_per_token(fb, torch, mixtral_full, B):
     """Each token of the batch == the single-token fused path on the same
     token (same masks up to exact ties), and == the reference within 1e-2."""
@@ -237,3 +238,38 @@ def test_gate_gemm_and_cuda_core_paths_agree(tmp_path):
     for o in outs[1:]:
         for t in range(24):
             assert O.rel_l2(o[t], outs[0][t]) <= 1e-5, t
+
+
+def _union_paths_run(out_path):
+    import torch
+
+    import paper_2505_05950_b200 as fb2
+    from oracle import oracle as O2
+    gate, up, down = O2.seeded_expert(2048, 1000, 21)
+    q = O2.quantize(up, 2, 64)
+    t = O2.calibrate_threshold(np.abs(O2.qgemv_channels(q, 2048, O2.seeded_input(2048, 1))), 0.8)
+    e = fb2.GpuExpert(2048, 1000, 2, 64, q.codes, q.scales, q.zeros, gate=gate, down=down, threshold=t)
+    X = torch.from_numpy(np.stack([O2.token_input(1, 40 + i, 2048) for i in range(4)])).cuda()
+    outs = [fb2.expert_forward_batched(e, X[:b]).cpu().numpy() for b in (1, 2, 4)]
+    np.savez(out_path, *outs)
+
+
+def test_fused_union_kernel_matches_two_kernel_path(tmp_path):
+    """<= 4 tokens: the fused union gate/down kernel (union_ffn) == the
+    coeffs + down_accum path (FLOE_UNION_FUSED=0) up to summation order."""
+    import os
+    import subprocess
+    import sys
+    res = {}
+    for flag in ("1", "0"):
+        out = tmp_path / f"u{flag}.npz"
+        code = (f"import sys; sys.path.insert(0, {str(Path(__file__).resolve().parents[1])!r}); "
+                f"sys.path.insert(0, {str(Path(__file__).resolve().parent)!r}); "
+                f"import test_gpu_batched as T; T._union_paths_run({str(out)!r})")
+        env = dict(os.environ, FLOE_UNION_FUSED=flag)
+        subprocess.run([sys.executable, "-c", code], check=True, env=env, timeout=600)
+        res[flag] = np.load(out)
+    for k in res["1"].files:
+        a, b = res["1"][k], res["0"][k]
+        assert O.rel_l2(a, b) <= 1e-5, k
+

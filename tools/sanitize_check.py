@@ -53,6 +53,7 @@ def main():
     X = torch.from_numpy(np.stack([O.token_input(1, i, 2048) for i in range(5)])).cuda()
     fb.qgemv_channels_batched(e3, X)
     fb.expert_forward_batched(e3, X)
+    fb.expert_forward_batched(e3, X[:3])  # <= 4 tokens: the fused union kernel
     # the prefill path (exact batched K1 at 5 tokens; dequantized GEMM at 80)
     fb.expert_forward_prefill(e3, X)
     X80 = torch.from_numpy(np.stack([O.token_input(1, 100 + i, 2048) for i in range(80)])).cuda()
