@@ -249,14 +249,15 @@ def _union_paths_run(out_path):
     q = O2.quantize(up, 2, 64)
     t = O2.calibrate_threshold(np.abs(O2.qgemv_channels(q, 2048, O2.seeded_input(2048, 1))), 0.8)
     e = fb2.GpuExpert(2048, 1000, 2, 64, q.codes, q.scales, q.zeros, gate=gate, down=down, threshold=t)
-    X = torch.from_numpy(np.stack([O2.token_input(1, 40 + i, 2048) for i in range(4)])).cuda()
-    outs = [fb2.expert_forward_batched(e, X[:b]).cpu().numpy() for b in (1, 2, 4)]
+    X = torch.from_numpy(np.stack([O2.token_input(1, 40 + i, 2048) for i in range(7)])).cuda()
+    outs = [fb2.expert_forward_batched(e, X[:b]).cpu().numpy() for b in (1, 2, 4, 7)]
     np.savez(out_path, *outs)
 
 
 def test_fused_union_kernel_matches_two_kernel_path(tmp_path):
-    """<= 4 tokens: the fused union gate/down kernel (union_ffn) == the
-    coeffs + down_accum path (FLOE_UNION_FUSED=0) up to summation order."""
+    """<= 8 tokens: the fused union gate/down kernel (union_ffn, groups of <= 4
+    tokens) == the coeffs + down_accum path (FLOE_UNION_FUSED=0) up to
+    summation order."""
     import os
     import subprocess
     import sys
