@@ -281,8 +281,11 @@ int floe_gpu_layer_forward(const floe_gpu_layer *l, floe_gpu_workspace *ws,
  * tokens one by one through the fused single-expert kernel, more through
  * floe_gpu_expert_forward_batched (one tcgen05 pass over its codes, the union
  * of the kept channels' records read once).  With a workspace (`ws`
- * nullable: then always the batched path), batches of up to 40 tokens run
+ * nullable: then always the batched path), batches of up to 12 tokens run
  * token by token through the fused layer kernel, which is faster there.
+ * Experts routed more than one token run concurrently on up to 8 internal
+ * side streams (their up projections first, in order on `stream`); the call
+ * joins them back into `stream` before it returns.
  * Synchronises `stream` once (the per-expert token counts decide the
  * launches). */
 int floe_gpu_layer_forward_batched(const floe_gpu_layer *l, floe_gpu_workspace *ws,

@@ -1332,6 +1332,9 @@ struct Lt {
   size_t ws_bytes = 64ull << 20;
   std::mutex mu;
   std::map<std::tuple<int, int, int, int, int, int, int, int, int>, cublasLtMatmulAlgo_t> algos;
+  // one workspace per stream: experts of a batched layer run their GEMMs
+  // concurrently on side streams (ws serves the first stream seen)
+  std::map<cudaStream_t, void *> stream_ws;
 };
 Lt *lt_get() {
   static Lt *L = [] {
@@ -1409,8 +1412,22 @@ int lt_gemm(bool ta, bool tb, int m, int n, int k, const __half *A, int lda, con
       if (ok) algo = res.algo;
     }
   }
+  void *wsp = nullptr;
+  if (ok) {
+    std::lock_guard<std::mutex> g(L->mu);
+    auto it = L->stream_ws.find(st);
+    if (it != L->stream_ws.end()) {
+      wsp = it->second;
+    } else if (L->stream_ws.empty()) {
+      wsp = L->stream_ws[st] = L->ws;
+    } else if (cudaMalloc(&wsp, L->ws_bytes) == cudaSuccess) {
+      L->stream_ws[st] = wsp;
+    } else {
+      ok = false;
+    }
+  }
   if (ok)
-    ok = cublasLtMatmul(L->h, op, &alpha, A, la, B, lb, &beta, C, lc, C, lc, &algo, L->ws, L->ws_bytes,
+    ok = cublasLtMatmul(L->h, op, &alpha, A, la, B, lb, &beta, C, lc, C, lc, &algo, wsp, L->ws_bytes,
                         st) == CUBLAS_STATUS_SUCCESS;
   if (lc) cublasLtMatrixLayoutDestroy(lc);
   if (lb) cublasLtMatrixLayoutDestroy(lb);
@@ -1422,8 +1439,23 @@ int lt_gemm(bool ta, bool tb, int m, int n, int k, const __half *A, int lda, con
 
 extern "C" {
 
+}  // extern "C"
+namespace {
+// v_pre: v [n][di] already computed by the exact batched K1 (n <= kExactK1Max)
+int prefill_impl(const floe_gpu_expert *e, const float *x, uint32_t n_tokens, float *y,
+                 floe_stream_t stream, const float *v_pre);
+}  // namespace
+extern "C" {
+
 int floe_gpu_expert_forward_prefill(const floe_gpu_expert *e, const float *x, uint32_t n_tokens,
                                     float *y, floe_stream_t stream) {
+  return prefill_impl(e, x, n_tokens, y, stream, nullptr);
+}
+
+}  // extern "C"
+namespace {
+int prefill_impl(const floe_gpu_expert *e, const float *x, uint32_t n_tokens, float *y,
+                 floe_stream_t stream, const float *v_pre) {
   if (!e || !x || !y) return fail(FLOE_ERR_INVALID, "expert_forward_sparse: null argument");
   if (n_tokens == 0) return FLOE_OK;
   if (!e->fast || e->up_only || !e->host_desc.records)
@@ -1460,7 +1492,9 @@ int floe_gpu_expert_forward_prefill(const floe_gpu_expert *e, const float *x, ui
   if (cudaGetLastError() != cudaSuccess) return done(fail(FLOE_ERR_CUDA, "prefill: launch failed"));
   const __half *rec = e->host_desc.records;  // [di][gate row | down row]
   const int D = (int)dh, I = (int)di, N = (int)n;
-  if (exact_k1) {
+  if (exact_k1 && v_pre) {
+    v = const_cast<float *>(v_pre);
+  } else if (exact_k1) {
     if (int rc = floe_gpu_qgemv_channels_batched(e, x, n, v, stream)) return done(rc);
   } else {
     // v (n x di row-major == di x n column-major) = Wb^T-view . Xa, K = 3 dh
@@ -1475,9 +1509,26 @@ int floe_gpu_expert_forward_prefill(const floe_gpu_expert *e, const float *x, ui
   if (cudaGetLastError() != cudaSuccess) return done(fail(FLOE_ERR_CUDA, "prefill: launch failed"));
   return done(FLOE_OK);
 }
+}  // namespace
+extern "C" {
+
+}  // extern "C"
+namespace {
+// v_pre: v [n][di] already computed (the batched layer's up-projection stage)
+int batched_impl(const floe_gpu_expert *e, const float *x, uint32_t n_tokens, float *y_out,
+                 float *v_out, floe_stream_t stream, const float *v_pre);
+}  // namespace
+extern "C" {
 
 int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x, uint32_t n_tokens,
                                     float *y_out, float *v_out, floe_stream_t stream) {
+  return batched_impl(e, x, n_tokens, y_out, v_out, stream, nullptr);
+}
+
+}  // extern "C"
+namespace {
+int batched_impl(const floe_gpu_expert *e, const float *x, uint32_t n_tokens, float *y_out,
+                 float *v_out, floe_stream_t stream, const float *v_pre) {
   if (!e || !x || !y_out) return fail(FLOE_ERR_INVALID, "expert_forward_batched: null argument");
   if (n_tokens == 0) return FLOE_OK;
   if (e->up_only)
@@ -1499,7 +1550,7 @@ int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x, ui
   uint8_t *scratch = nullptr;
   CK(cudaMallocAsync(reinterpret_cast<void **>(&scratch), total, st));
   uint32_t *count = reinterpret_cast<uint32_t *>(scratch);
-  float *v = v_out ? v_out : reinterpret_cast<float *>(scratch + o_v);
+  float *v = v_pre ? const_cast<float *>(v_pre) : v_out ? v_out : reinterpret_cast<float *>(scratch + o_v);
   uint32_t *uc = reinterpret_cast<uint32_t *>(scratch + o_uc);
   unsigned long long *um = reinterpret_cast<unsigned long long *>(scratch + o_um);
   // K parts of the gate GEMM per 128-channel block: more CTAs in flight at
@@ -1521,7 +1572,7 @@ int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x, ui
     return p ? std::atoi(p) : -1;
   }();
   const bool tc_down = down_env >= 0 ? down_env != 0 : B >= 16;
-  int rc = floe_gpu_qgemv_channels_batched(e, x, B, v, stream);
+  int rc = v_pre ? FLOE_OK : floe_gpu_qgemv_channels_batched(e, x, B, v, stream);
   if (rc == FLOE_OK)
     rc = dh == 4096 ? batched_gate_down<4096>(e, x, B, y_out, v, scratch, o_xh, o_g, tc_gate,
                                               tc_down, kGateSplit, st)
@@ -1533,6 +1584,8 @@ int floe_gpu_expert_forward_batched(const floe_gpu_expert *e, const float *x, ui
     return fail(FLOE_ERR_CUDA, "expert_forward_batched: %s", cudaGetErrorString(fe));
   return rc;
 }
+}  // namespace
+extern "C" {
 
 int floe_gpu_dequantize_up(const floe_gpu_expert *e, float *out, floe_stream_t stream) {
   if (!e || !out) return fail(FLOE_ERR_INVALID, "dequantize: null argument");
@@ -2372,7 +2425,7 @@ int floe_gpu_pack_compact(const floe_gpu_expert *e, const uint8_t *mask, uint32_
 // single-expert kernel (FLOE_BATCHED_SMALL overrides; measured crossover).
 static const uint32_t kBatchedSmall = [] {
   const char *p = std::getenv("FLOE_BATCHED_SMALL");
-  return p ? (uint32_t)std::atoi(p) : 12u;
+  return p ? (uint32_t)std::atoi(p) : 1u;
 }();
 // Batches of at most this many tokens run token by token through the fused
 // layer kernel (FLOE_LAYER_PER_TOKEN overrides).
@@ -2387,9 +2440,38 @@ static const uint32_t kMixGemmMin = [] {
   const char *p = std::getenv("FLOE_MIX_GEMM_MIN");
   return p ? (uint32_t)std::atoi(p) : 1u;
 }();
+// Side streams of the batched layer (per device, created once, non-blocking);
+// FLOE_LAYER_STREAMS=1 keeps every expert on the caller's stream.
+constexpr int kSideStreams = 8;
+static const int kLayerStreams = [] {
+  const char *p = std::getenv("FLOE_LAYER_STREAMS");
+  return p ? std::atoi(p) : kSideStreams;
+}();
+// experts routed at least this many tokens stay on the caller's stream (the
+// default: those past the exact up projection, whose dequantized-copy scratch
+// of 352 MB per expert would be held 8 times over)
+static const uint32_t kLayerSerialMin = [] {
+  const char *p = std::getenv("FLOE_LAYER_SERIAL_MIN");
+  return p ? (uint32_t)std::atoi(p) : 65u;
+}();
+static cudaStream_t *side_streams() {
+  static std::mutex mu;
+  static cudaStream_t pool[64][kSideStreams] = {};
+  static bool made[64] = {};
+  if (kLayerStreams <= 1) return nullptr;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> g(mu);
+  if (!made[dev]) {
+    for (auto &s : pool[dev])
+      if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    made[dev] = true;
+  }
+  return pool[dev];
+}
 static const uint32_t kLayerPerToken = [] {
   const char *p = std::getenv("FLOE_LAYER_PER_TOKEN");
-  return p ? (uint32_t)std::atoi(p) : 40u;
+  return p ? (uint32_t)std::atoi(p) : 12u;
 }();
 extern "C" {
 
@@ -2422,7 +2504,8 @@ int floe_gpu_layer_forward_batched(const floe_gpu_layer *l, floe_gpu_workspace *
   const size_t o_u = 0, o_lg = o_u + 4ull * T * dh, o_sel = o_lg + 4ull * T * E;
   const size_t o_w = o_sel + 4ull * P, o_cnt = o_w + 4ull * P, o_lst = o_cnt + 4ull * 32;
   const size_t o_x = (o_lst + 4ull * E * T + 255) & ~size_t(255);
-  const size_t o_y = o_x + 4ull * T * dh, o_out = o_y + 4ull * T * dh;
+  // X and Y hold every expert's rows at its own offset (experts run concurrently)
+  const size_t o_y = o_x + 4ull * P * dh, o_out = o_y + 4ull * P * dh;
   const size_t o_ha = o_out + 4ull * P * dh, o_hinv = o_ha + (mix_tc ? 2ull * T * 3 * dh : 0);
   const size_t o_mh = (o_hinv + 4ull * T + 255) & ~size_t(255);
   const size_t total = o_mh + (mix_tc ? 4ull * T * dh : 0);
@@ -2478,33 +2561,126 @@ int floe_gpu_layer_forward_batched(const floe_gpu_layer *l, floe_gpu_workspace *
     return done(fail(FLOE_ERR_CUDA, "layer_forward_batched: routing readback failed"));
   // every expert over its tokens: a few tokens go one by one through the fused
   // single-expert kernel (one pass over the expert per token, ~15 us), more
-  // through the batched forward (one tcgen05 pass over the codes, the union
-  // of kept records once; chunks of at most 64 tokens)
-  for (uint32_t e = 0; e < E; ++e) {
+  // through the prefill GEMMs (the expert read once) or the batched forward.
+  // Experts on the prefill / batched paths run concurrently on side streams
+  // (each is a few small kernels that leave SMs idle on its own); the fused
+  // single-expert kernel synchronises its grid, so those experts stay on the
+  // caller's stream, issued before the fork.
+  uint32_t off[33];
+  off[0] = 0;
+  for (uint32_t e = 0; e < E; ++e) off[e + 1] = off[e] + hc[e];
+  auto on_main = [&](uint32_t n) { return ws && n < kPrefillMin && n <= kBatchedSmall; };
+  // The exact batched up projections of the concurrent experts run first, one
+  // after another on the caller's stream (the IMMA up projection faulted when it
+  // ran beside the cuBLASLt GEMMs of other experts); v then feeds the
+  // concurrent gate/down stage.
+  const bool concurrent = side_streams() != nullptr;
+  auto pre_k1 = [&](uint32_t n) {
+    return concurrent && n && !on_main(n) &&
+           (n >= kPrefillMin ? n <= kExactK1Max : n <= (uint32_t)CH);
+  };
+  uint32_t voff[33];
+  voff[0] = 0;
+  for (uint32_t e = 0; e < E; ++e) voff[e + 1] = voff[e] + (pre_k1(hc[e]) ? hc[e] : 0u);
+  float *V = nullptr;
+  if (voff[E]) {
+    if (cudaMallocAsync(reinterpret_cast<void **>(&V), 4ull * voff[E] * l->di, st) != cudaSuccess)
+      return done(fail(FLOE_ERR_CUDA, "layer_forward_batched: scratch allocation failed"));
+    for (uint32_t e = 0; e < E; ++e) {
+      if (voff[e + 1] == voff[e]) continue;
+      const uint32_t n = hc[e];
+      float *Xe = X + (size_t)off[e] * dh;
+      floe_bl::gather_rows<<<dim3(4, n), 256, 0, st>>>(u, lst + (size_t)e * T, n, K, dh, Xe);
+      if (int rc = floe_gpu_qgemv_channels_batched(l->experts[e], Xe, n,
+                                                   V + (size_t)voff[e] * l->di, stream)) {
+        cudaFreeAsync(V, st);
+        return done(rc);
+      }
+    }
+  }
+  auto run_expert = [&](uint32_t e, cudaStream_t es) -> int {
+    float *Xe = X + (size_t)off[e] * dh, *Ye = Y + (size_t)off[e] * dh;
+    floe_stream_t fs = reinterpret_cast<floe_stream_t>(es);
     if (hc[e] >= kPrefillMin) {  // many tokens: the prefill GEMMs, the expert read once
       const uint32_t n = hc[e];
       const uint32_t *pairs = lst + (size_t)e * T;
-      floe_bl::gather_rows<<<dim3(4, n), 256, 0, st>>>(u, pairs, n, K, dh, X);
-      if (int rc = floe_gpu_expert_forward_prefill(l->experts[e], X, n, Y, stream)) return done(rc);
-      floe_bl::scatter_rows<<<dim3(4, n), 256, 0, st>>>(Y, pairs, n, dh, outp);
-      continue;
+      const float *ve = voff[e + 1] > voff[e] ? V + (size_t)voff[e] * l->di : nullptr;
+      if (!ve) floe_bl::gather_rows<<<dim3(4, n), 256, 0, es>>>(u, pairs, n, K, dh, Xe);
+      if (int rc = prefill_impl(l->experts[e], Xe, n, Ye, fs, ve)) return rc;
+      floe_bl::scatter_rows<<<dim3(4, n), 256, 0, es>>>(Ye, pairs, n, dh, outp);
+      return FLOE_OK;
     }
+    const float *ve = voff[e + 1] > voff[e] ? V + (size_t)voff[e] * l->di : nullptr;  // one chunk
     for (uint32_t c0 = 0; c0 < hc[e]; c0 += (uint32_t)CH) {
       const uint32_t n = std::min<uint32_t>((uint32_t)CH, hc[e] - c0);
       const uint32_t *pairs = lst + (size_t)e * T + c0;
-      floe_bl::gather_rows<<<dim3(4, n), 256, 0, st>>>(u, pairs, n, K, dh, X);
-      if (ws && n <= kBatchedSmall) {
+      if (!ve) floe_bl::gather_rows<<<dim3(4, n), 256, 0, es>>>(u, pairs, n, K, dh, Xe);
+      if (ve) {
+        if (int rc = batched_impl(l->experts[e], Xe, n, Ye, nullptr, fs, ve)) return rc;
+      } else if (on_main(n)) {
         for (uint32_t i = 0; i < n; ++i)
-          if (int rc = floe_gpu_expert_forward_sparse(l->experts[e], ws, X + (size_t)i * dh,
-                                                      Y + (size_t)i * dh, nullptr, nullptr,
-                                                      nullptr, nullptr, stream))
-            return done(rc);
-      } else if (int rc = floe_gpu_expert_forward_batched(l->experts[e], X, n, Y, nullptr, stream)) {
+          if (int rc = floe_gpu_expert_forward_sparse(l->experts[e], ws, Xe + (size_t)i * dh,
+                                                      Ye + (size_t)i * dh, nullptr, nullptr,
+                                                      nullptr, nullptr, fs))
+            return rc;
+      } else if (int rc = floe_gpu_expert_forward_batched(l->experts[e], Xe, n, Ye, nullptr, fs)) {
+        return rc;
+      }
+      floe_bl::scatter_rows<<<dim3(4, n), 256, 0, es>>>(Ye, pairs, n, dh, outp);
+    }
+    return FLOE_OK;
+  };
+  // experts with many tokens (>= FLOE_LAYER_SERIAL_MIN) fill the GPU on their
+  // own and run one after another on the caller's stream too (8 experts of
+  // ~1000 tokens concurrently: 4096-token layer 5.7 -> 12 ms)
+  auto serial = [&](uint32_t n) { return on_main(n) || n >= kLayerSerialMin; };
+  for (uint32_t e = 0; e < E; ++e)
+    if (hc[e] && serial(hc[e]))
+      if (int rc = run_expert(e, st)) {
+        if (V) cudaFreeAsync(V, st);
         return done(rc);
       }
-      floe_bl::scatter_rows<<<dim3(4, n), 256, 0, st>>>(Y, pairs, n, dh, outp);
+  cudaStream_t *side = side_streams();
+  uint32_t nside = 0;
+  for (uint32_t e = 0; e < E; ++e) nside += hc[e] && !serial(hc[e]);
+  nside = std::min<uint32_t>(nside, (uint32_t)std::min(kLayerStreams, kSideStreams));
+  if (!side) nside = 0;
+  if (nside <= 1) {
+    for (uint32_t e = 0; e < E; ++e)
+      if (hc[e] && !serial(hc[e]))
+        if (int rc = run_expert(e, st)) {
+          if (V) cudaFreeAsync(V, st);
+          return done(rc);
+        }
+  } else {
+    cudaEvent_t fork = nullptr, join[kSideStreams] = {};
+    bool ok = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventRecord(fork, st) == cudaSuccess;
+    for (uint32_t i = 0; ok && i < nside; ++i)
+      ok = cudaEventCreateWithFlags(&join[i], cudaEventDisableTiming) == cudaSuccess &&
+           cudaStreamWaitEvent(side[i], fork, 0) == cudaSuccess;
+    int rc = ok ? FLOE_OK : fail(FLOE_ERR_CUDA, "layer_forward_batched: stream fork failed");
+    // the largest experts first, dealt round-robin over the side streams
+    uint32_t order[32], no = 0;
+    for (uint32_t e = 0; e < E; ++e)
+      if (hc[e] && !serial(hc[e])) order[no++] = e;
+    std::stable_sort(order, order + no, [&](uint32_t a, uint32_t b) { return hc[a] > hc[b]; });
+    for (uint32_t j = 0; rc == FLOE_OK && j < no; ++j) rc = run_expert(order[j], side[j % nside]);
+    // join on every path: the scratch is freed on the caller's stream
+    for (uint32_t i = 0; i < nside; ++i) {
+      if (!join[i]) continue;
+      if (cudaEventRecord(join[i], side[i]) != cudaSuccess ||
+          cudaStreamWaitEvent(st, join[i], 0) != cudaSuccess)
+        if (rc == FLOE_OK) rc = fail(FLOE_ERR_CUDA, "layer_forward_batched: stream join failed");
+      cudaEventDestroy(join[i]);
+    }
+    if (fork) cudaEventDestroy(fork);
+    if (rc != FLOE_OK) {
+      if (V) cudaFreeAsync(V, st);
+      return done(rc);
     }
   }
+  if (V) cudaFreeAsync(V, st);
   floe_bl::combine<<<dim3(4, T), 256, 0, st>>>(u, outp, w, K, dh, y);
   if (cudaGetLastError() != cudaSuccess)
     return done(fail(FLOE_ERR_CUDA, "layer_forward_batched: launch failed"));

@@ -645,17 +645,25 @@ __global__ void __launch_bounds__(kUThreads, 1) union_ffn(const __half *__restri
     for (uint32_t rr = 0; rr < nb; ++rr) {
       const uint32_t i = i0 + rr, s = i % kUStages;
       spin(&full[s], (i / kUStages) & 1u);
-      float gf[PL];
+      float gf[PL], p[kUTok];
       load_half_row<PL>(reinterpret_cast<const __half *>(ring + s * RB) + k0, gf);
 #pragma unroll
       for (int tk = 0; tk < kUTok; ++tk) {
-        float p = 0.0f;
+        p[tk] = 0.0f;
 #pragma unroll
-        for (uint32_t e = 0; e < PL; ++e) p = fmaf(gf[e], xr[tk][e], p);
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-        if (lane == 0) part[rr][tk][warp] = p;
+        for (uint32_t e = 0; e < PL; ++e) p[tk] = fmaf(gf[e], xr[tk][e], p[tk]);
       }
+      // transposed butterfly: the 4 token sums in 6 shuffles (not 20); lane
+      // 8 tk ends with token tk's sum
+      static_assert(kUTok == 4, "union_ffn: the butterfly reduces 4 token sums");
+      const bool hi16 = (lane & 16u) != 0, hi8 = (lane & 8u) != 0;
+      const float r0 = __shfl_xor_sync(0xffffffffu, hi16 ? p[0] : p[2], 16);
+      const float r1 = __shfl_xor_sync(0xffffffffu, hi16 ? p[1] : p[3], 16);
+      const float k0s = (hi16 ? p[2] : p[0]) + r0, k1s = (hi16 ? p[3] : p[1]) + r1;
+      float q = (hi8 ? k1s : k0s) + __shfl_xor_sync(0xffffffffu, hi8 ? k0s : k1s, 8);
+#pragma unroll
+      for (int o = 4; o >= 1; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+      if ((lane & 7u) == 0) part[rr][lane >> 3][warp] = q;
     }
     asm volatile("bar.sync 1, %0;" ::"n"(32 * kUWarps) : "memory");
     if (warp == 0 && lane < nb * kUTok) {  // a = silu(g) * v, fixed-order sum of the slices

@@ -64,14 +64,19 @@ def _check_tokens(L, H, Y, idx):
     assert max(errs) <= 5e-2, max(errs)
 
 
-@pytest.mark.parametrize("B", [16, 64])
-def test_layer_forward_batched_vs_reference(fb, torch, layer, B):
+@pytest.mark.parametrize("B,with_ws", [(16, False), (64, False), (13, True), (24, True),
+                                       (64, True), (200, True)])
+def test_layer_forward_batched_vs_reference(fb, torch, layer, B, with_ws):
+    """With a workspace (the bench's call) experts routed one token take the
+    fused single-expert kernel on the caller's stream; the rest run
+    concurrently on side streams after the serial up-projection stage."""
     L, gl, *_ = layer
-    H = np.stack([O.token_input(1, 5000 + B * 10 + t, DH) for t in range(B)])
-    Y = fb.layer_forward_batched(gl, torch.from_numpy(H).cuda()).cpu().numpy()
-    _check_tokens(L, H, Y, range(B))
-    # and the same tokens one by one through the single-token fused kernel
     ws = fb.Workspace(DH, DI, K)
+    H = np.stack([O.token_input(1, 5000 + B * 10 + t, DH) for t in range(B)])
+    Y = fb.layer_forward_batched(gl, torch.from_numpy(H).cuda(), ws if with_ws else None)
+    Y = Y.cpu().numpy()
+    _check_tokens(L, H, Y, range(0, B, max(1, B // 64)))
+    # and the same tokens one by one through the single-token fused kernel
     for t in range(0, B, 7):
         y1 = fb.layer_forward(gl, torch.from_numpy(H[t]).cuda(), ws).cpu().numpy()
         assert O.rel_l2(Y[t], y1) <= 5e-2
