@@ -1182,14 +1182,21 @@ int batched_gate_down(const floe_gpu_expert *e, const float *x, uint32_t B, floa
   if (fused) {
     const __half *rec = e->host_desc.records;
     const uint32_t usm = floe_tc::kUStages * 4u * DH;
-    if (int rc = set_smem(floe_tc::union_ffn<DH>, usm)) return rc;
+    // records per barrier batch: 8 (FLOE_UNION_UR=4: 4; 16 tokens per layer
+    // call 0.65 -> 0.64 ms with 8)
+    static const bool ur8 = [] {
+      const char *p = std::getenv("FLOE_UNION_UR");
+      return !(p && std::atoi(p) == 4);
+    }();
+    auto kern = ur8 ? floe_tc::union_ffn<DH, 8> : floe_tc::union_ffn<DH, 4>;
+    if (int rc = set_smem(kern, usm)) return rc;
     CK(cudaMemsetAsync(y_out, 0, 4ull * B * DH, st));
     for (uint32_t g0 = 0; g0 < B; g0 += floe_tc::kUTok) {
       const uint32_t nb = std::min<uint32_t>(floe_tc::kUTok, B - g0);
       if (g0) CK(cudaMemsetAsync(count, 0, 4, st));
       floe_tc::union_masks<<<(di + 255) / 256, 256, 0, st>>>(v + (size_t)g0 * di, nb, di,
                                                              e->host_desc.threshold, count, uc, um);
-      floe_tc::union_ffn<DH><<<sm, floe_tc::kUThreads, usm, st>>>(
+      kern<<<sm, floe_tc::kUThreads, usm, st>>>(
           rec, x + (size_t)g0 * DH, v + (size_t)g0 * di, nb, di, count, uc, um, y_out + (size_t)g0 * DH);
       CK_LAUNCH();
     }

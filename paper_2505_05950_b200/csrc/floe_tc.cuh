@@ -549,7 +549,7 @@ constexpr int kUTok = 4;                  // tokens
 constexpr int kUWarps = 16;               // consumer warps
 constexpr int kUThreads = 32 * (kUWarps + 1);
 constexpr int kUStages = 8;
-constexpr int kUR = 4;                    // records per barrier batch
+constexpr int kUR = 8;                    // records per barrier batch (default)
 constexpr uint32_t kUMaxRows = 256;       // union rows per CTA (host checks n <= G * kUMaxRows)
 
 // PL consecutive f16 values (PL = 4: one 8-B load, PL % 8 == 0: 16-B loads)
@@ -576,7 +576,7 @@ __device__ __forceinline__ void load_half_row(const __half *p, float (&f)[PL]) {
   }
 }
 
-template <int DH>
+template <int DH, int UR = kUR>
 __global__ void __launch_bounds__(kUThreads, 1) union_ffn(const __half *__restrict__ records,
                                                          const float *__restrict__ x,
                                                          const float *__restrict__ v, uint32_t B,
@@ -591,8 +591,9 @@ __global__ void __launch_bounds__(kUThreads, 1) union_ffn(const __half *__restri
   __shared__ __align__(8) uint64_t full[kUStages], empty[kUStages];
   __shared__ uint32_t rows_s[kUMaxRows];
   __shared__ float va_s[kUMaxRows][kUTok];   // v of the token, or 0 if it drops the row
-  __shared__ float part[kUR][kUTok][kUWarps];
-  __shared__ float acoef[kUR][kUTok];
+  static_assert(UR * kUTok <= 32, "union_ffn: one lane of warp 0 per (record, token)");
+  __shared__ float part[UR][kUTok][kUWarps];
+  __shared__ float acoef[UR][kUTok];
   const uint32_t t = threadIdx.x, warp = t >> 5, lane = t & 31u;
   const uint32_t G = gridDim.x, b = blockIdx.x, n = *count;
   const uint32_t r0 = (uint32_t)((uint64_t)n * b / G), r1 = (uint32_t)((uint64_t)n * (b + 1) / G);
@@ -639,8 +640,8 @@ __global__ void __launch_bounds__(kUThreads, 1) union_ffn(const __half *__restri
       ya[tk][e] = ya[tk][e + 1] = ya[tk][e + 2] = ya[tk][e + 3] = 0.0f;
     }
   asm volatile("bar.sync 1, %0;" ::"n"(32 * kUWarps) : "memory");  // va_s complete
-  for (uint32_t i0 = 0; i0 < nr; i0 += kUR) {
-    const uint32_t nb = min((uint32_t)kUR, nr - i0);
+  for (uint32_t i0 = 0; i0 < nr; i0 += UR) {
+    const uint32_t nb = min((uint32_t)UR, nr - i0);
     // gate partials of this warp's column slice
     for (uint32_t rr = 0; rr < nb; ++rr) {
       const uint32_t i = i0 + rr, s = i % kUStages;
