@@ -2578,9 +2578,9 @@ int floe_gpu_layer_forward_batched(const floe_gpu_layer *l, floe_gpu_workspace *
   for (uint32_t e = 0; e < E; ++e) off[e + 1] = off[e] + hc[e];
   auto on_main = [&](uint32_t n) { return ws && n < kPrefillMin && n <= kBatchedSmall; };
   // The exact batched up projections of the concurrent experts run first, one
-  // after another on the caller's stream (the IMMA up projection faulted when it
-  // ran beside the cuBLASLt GEMMs of other experts); v then feeds the
-  // concurrent gate/down stage.
+  // after another on the caller's stream (with the IMMA up projection inside
+  // the side streams, a few layer calls in a hundred ended in an unspecified
+  // launch failure); v then feeds the concurrent gate/down stage.
   const bool concurrent = side_streams() != nullptr;
   auto pre_k1 = [&](uint32_t n) {
     return concurrent && n && !on_main(n) &&
