@@ -1491,7 +1491,7 @@ int prefill_impl(const floe_gpu_expert *e, const float *x, uint32_t n_tokens, fl
   // codes, no dequantized copy) computes v; above, the dequantized f16 hi/lo
   // GEMM (its fixed cost -- writing and reading the 352 MB copy -- amortised)
   const bool exact_k1 = n <= kExactK1Max;
-  floe_pf::xcat<<<n, 256, 0, st>>>(x, dh, Xa, inv);
+  floe_pf::xcat<<<n, 1024, 0, st>>>(x, dh, Xa, inv);
   if (!exact_k1) {
     if (dh == 4096) floe_pf::wcat_tiled<4096><<<sm * 8, 256, 0, st>>>(e->host_desc.tiles, di, Wb);
     else floe_pf::wcat_tiled<2048><<<sm * 8, 256, 0, st>>>(e->host_desc.tiles, di, Wb);
@@ -1509,10 +1509,14 @@ int prefill_impl(const floe_gpu_expert *e, const float *x, uint32_t n_tokens, fl
   }
   // g = gate . x_hi  (gate rows: ld 2 dh)
   if (int rc = lt_gemm(true, false, I, N, D, rec, 2 * D, Xa, 3 * D, 0.0f, g, I, st)) return done(rc);
-  floe_pf::coeffs<<<n, 256, 0, st>>>(v, g, inv, di, e->host_desc.threshold, Ac, ainv, exact_k1 ? 1 : 0);
+  if (di <= 16u * 1024u)
+    floe_pf::coeffs_reg<16><<<n, 1024, 0, st>>>(v, g, inv, di, e->host_desc.threshold, Ac, ainv,
+                                                exact_k1 ? 1 : 0);
+  else
+    floe_pf::coeffs<<<n, 256, 0, st>>>(v, g, inv, di, e->host_desc.threshold, Ac, ainv, exact_k1 ? 1 : 0);
   // y (n x dh row-major == dh x n column-major) = down^T-view . a_hi
   if (int rc = lt_gemm(false, false, D, N, I, rec + dh, 2 * D, Ac, I, 0.0f, y, D, st)) return done(rc);
-  floe_pf::unscale_rows<<<n, 256, 0, st>>>(y, dh, ainv);
+  floe_pf::unscale_rows<<<n, 1024, 0, st>>>(y, dh, ainv);
   if (cudaGetLastError() != cudaSuccess) return done(fail(FLOE_ERR_CUDA, "prefill: launch failed"));
   return done(FLOE_OK);
 }
@@ -2536,12 +2540,12 @@ int floe_gpu_layer_forward_batched(const floe_gpu_layer *l, floe_gpu_workspace *
     keep_pool();
     __half *Ha = reinterpret_cast<__half *>(sc + o_ha);
     float *hinv = reinterpret_cast<float *>(sc + o_hinv), *mh = reinterpret_cast<float *>(sc + o_mh);
-    floe_pf::xcat<<<T, 256, 0, st>>>(h, dh, Ha, hinv);
+    floe_pf::xcat<<<T, 1024, 0, st>>>(h, dh, Ha, hinv);
     const __half *M = static_cast<const __half *>(l->mixing);
     const int D = (int)dh, N = (int)T;
     if (int rc = lt_gemm(true, false, D, N, D, M, D, Ha, 3 * D, 0.0f, mh, D, st)) return done(rc);
     if (int rc = lt_gemm(true, false, D, N, D, M, D, Ha + 2 * dh, 3 * D, 1.0f, mh, D, st)) return done(rc);
-    floe_pf::residual<<<T, 256, 0, st>>>(h, mh, hinv, dh, u);
+    floe_pf::residual<<<T, 1024, 0, st>>>(h, mh, hinv, dh, u);
   }
   for (uint32_t t0 = 0; t0 < (mix_tc ? 0u : T); t0 += floe_bl::kMixTok) {
     const uint32_t nt = std::min<uint32_t>(floe_bl::kMixTok, T - t0);

@@ -120,6 +120,50 @@ __global__ void coeffs(const float *v, const float *g, const float *inv, uint32_
   }
 }
 
+// coeffs for di <= KM * 1024 with 1024 threads per row: each thread keeps its
+// KM coefficients in registers between the row maximum and the f16 write (one
+// read of v and g, KM independent loads in flight per thread; the 256-thread
+// two-pass version took 67 us per 16-token call under ncu).  Same arithmetic,
+// so the same bits as coeffs.
+template <int KM>
+__global__ void __launch_bounds__(1024) coeffs_reg(const float *v, const float *g, const float *inv,
+                                                   uint32_t di, float t, __half *acat, float *ainv,
+                                                   int v_true) {
+  const uint32_t r = blockIdx.x;
+  const float ig = inv[r], iv = v_true ? 1.0f : ig;
+  const float *vr = v + (size_t)r * di, *gr = g + (size_t)r * di;
+  __shared__ float red[32];
+  float a[KM], mx = 0.0f;
+#pragma unroll
+  for (int k = 0; k < KM; ++k) {
+    const uint32_t c = threadIdx.x + 1024u * k;
+    float av = 0.0f;
+    if (c < di) {
+      const float vv = vr[c] * iv;
+      av = !(fabsf(vv) < t) ? floe_k::silu_ref(gr[c] * ig) * vv : 0.0f;
+    }
+    a[k] = av;
+    mx = fmaxf(mx, fabsf(av));
+  }
+  for (int o = 16; o >= 1; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float m = red[threadIdx.x];
+    for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) red[0] = m;
+  }
+  __syncthreads();
+  const float s = pow2_inv_scale(red[0]);
+  if (threadIdx.x == 0) ainv[r] = 1.0f / s;
+  __half *ao = acat + (size_t)r * di;
+#pragma unroll
+  for (int k = 0; k < KM; ++k) {
+    const uint32_t c = threadIdx.x + 1024u * k;
+    if (c < di) ao[c] = __float2half_rn(a[k] * s);
+  }
+}
+
 // u = h + mh * inv[row] (the block input, model.cpp:150-152: drift scale 1).
 __global__ void residual(const float *h, const float *mh, const float *inv, uint32_t dh, float *u) {
   const uint32_t r = blockIdx.x;
