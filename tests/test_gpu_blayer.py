@@ -94,3 +94,42 @@ def test_ep_prefill_4096_vs_reference(fb, torch, layer):
     Hn = H.cpu().numpy()
     idx = np.random.default_rng(0).choice(T, 256, replace=False)
     _check_tokens(L, Hn, Y, sorted(idx))
+
+
+_STREAMS_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import bench, paper_2505_05950_b200 as fb
+torch.cuda.set_device(0)
+layers, _ = bench.build_model(fb, torch, 1)
+ws = fb.Workspace(bench.DH, bench.DI, bench.TOPK)
+out = {{}}
+for B in (16, 64, 200):
+    H = torch.stack([fb.gen_normals(1, (1 << 40) + 3000 + t, bench.DH) for t in range(B)])
+    out[str(B)] = fb.layer_forward_batched(layers[0], H, ws).cpu().numpy()
+np.savez({path!r}, **out)
+"""
+
+
+def test_side_streams_match_single_stream(tmp_path):
+    """The batched layer with its experts on 8 side streams (default) against
+    the same calls with every kernel on the caller's stream
+    (FLOE_LAYER_STREAMS=1), in fresh processes (the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parents[1])
+    res = {}
+    for ls in ("1", "8"):
+        path = str(tmp_path / f"y{ls}.npz")
+        env = dict(os.environ, FLOE_LAYER_STREAMS=ls)
+        subprocess.run([sys.executable, "-c", _STREAMS_SCRIPT.format(root=root, path=path)],
+                       env=env, check=True, timeout=600)
+        res[ls] = np.load(path)
+    for B in ("16", "64", "200"):
+        a, b = res["1"][B], res["8"][B]
+        assert np.all(np.isfinite(b))
+        # float atomics in the union kernel add in a different order: not bitwise
+        for t in range(a.shape[0]):
+            assert O.rel_l2(b[t], a[t]) <= 1e-5, (B, t, O.rel_l2(b[t], a[t]))
