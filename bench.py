@@ -485,7 +485,7 @@ def run_batched_layer(fb, torch, layer, ws, stream):
         out[key] = {"tokens": B, "ms_per_call": round(ms, 3), "value": round(B / (ms * 1e-3), 1),
                     "unit": "layer-tokens/s"}
     out["note"] = ("one Mixtral MoE layer, B tokens per call: <= 12 tokens go token by token "
-                   "through the fused layer kernel; experts with >= 8 tokens through the prefill "
+                   "through the fused layer kernel; experts with >= 5 tokens through the prefill "
                    "path (exact tcgen05 up projection or dequantized f16 hi/lo GEMM, dense f16 "
                    "gate/down GEMMs); experts routed > 1 token run concurrently on 8 side "
                    "streams after their up projections")
