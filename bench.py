@@ -484,7 +484,7 @@ def run_batched_layer(fb, torch, layer, ws, stream):
         ms = time_region(torch, lambda i: fb.layer_forward_batched(layer, H, ws, out=Y), n, stream) / n
         out[key] = {"tokens": B, "ms_per_call": round(ms, 3), "value": round(B / (ms * 1e-3), 1),
                     "unit": "layer-tokens/s"}
-    out["note"] = ("one Mixtral MoE layer, B tokens per call: <= 12 tokens go token by token "
+    out["note"] = ("one Mixtral MoE layer, B tokens per call: <= 10 tokens go token by token "
                    "through the fused layer kernel; experts with >= 5 tokens through the prefill "
                    "path (exact tcgen05 up projection or dequantized f16 hi/lo GEMM, dense f16 "
                    "gate/down GEMMs); experts routed > 1 token run concurrently on 8 side "

@@ -277,15 +277,15 @@ int floe_gpu_layer_forward(const floe_gpu_layer *l, floe_gpu_workspace *ws,
 /* block_forward (model.cpp:145-169) for n_tokens tokens at once (SURVEY
  * configs 4 and 5): h_dev [n][dh] -> y_dev [n][dh].  The mixing matrix is
  * streamed once for up to 64 tokens, the tokens are routed and grouped by
- * expert on the device, and every routed expert runs over its tokens: a few
- * tokens one by one through the fused single-expert kernel, more through
- * floe_gpu_expert_forward_batched (one tcgen05 pass over its codes, the union
- * of the kept channels' records read once).  With a workspace (`ws`
- * nullable: then always the batched path), batches of up to 12 tokens run
+ * expert on the device, and every routed expert runs over its tokens: up to
+ * 4 tokens through floe_gpu_expert_forward_batched (one pass over its codes,
+ * the union of the kept channels' records read once), more through
+ * floe_gpu_expert_forward_prefill (tensor-core GEMMs).  With a workspace (`ws`
+ * nullable: then always the batched path), batches of up to 10 tokens run
  * token by token through the fused layer kernel, which is faster there.
- * Experts routed more than one token run concurrently on up to 8 internal
- * side streams (their up projections first, in order on `stream`); the call
- * joins them back into `stream` before it returns.
+ * The experts run concurrently on up to 8 internal side streams (their up
+ * projections first, in order on `stream`); the call joins them back into
+ * `stream` before it returns.
  * Synchronises `stream` once (the per-expert token counts decide the
  * launches). */
 int floe_gpu_layer_forward_batched(const floe_gpu_layer *l, floe_gpu_workspace *ws,

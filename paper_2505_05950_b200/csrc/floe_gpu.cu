@@ -2449,7 +2449,7 @@ int floe_gpu_pack_compact(const floe_gpu_expert *e, const uint8_t *mask, uint32_
 // single-expert kernel (FLOE_BATCHED_SMALL overrides; measured crossover).
 static const uint32_t kBatchedSmall = [] {
   const char *p = std::getenv("FLOE_BATCHED_SMALL");
-  return p ? (uint32_t)std::atoi(p) : 1u;
+  return p ? (uint32_t)std::atoi(p) : 0u;  // 0: with the experts concurrent, none
 }();
 // Batches of at most this many tokens run token by token through the fused
 // layer kernel (FLOE_LAYER_PER_TOKEN overrides).
@@ -2499,7 +2499,7 @@ static cudaStream_t *side_streams() {
 }
 static const uint32_t kLayerPerToken = [] {
   const char *p = std::getenv("FLOE_LAYER_PER_TOKEN");
-  return p ? (uint32_t)std::atoi(p) : 12u;
+  return p ? (uint32_t)std::atoi(p) : 10u;
 }();
 extern "C" {
 
