@@ -1339,8 +1339,8 @@ struct Lt {
   size_t ws_bytes = 64ull << 20;
   std::mutex mu;
   std::map<std::tuple<int, int, int, int, int, int, int, int, int>, cublasLtMatmulAlgo_t> algos;
-  // one workspace per stream: experts of a batched layer run their GEMMs
-  // concurrently on side streams (ws serves the first stream seen)
+  // the batched layer's side streams run GEMMs concurrently: each has its own
+  // workspace (lt_reserve); every other stream uses ws, as before
   std::map<cudaStream_t, void *> stream_ws;
 };
 Lt *lt_get() {
@@ -1361,17 +1361,18 @@ const uint32_t kExactK1Max = [] {
   return p ? (uint32_t)std::atoi(p) : 64u;
 }();
 
-// Give `st` its own cuBLASLt workspace now (a first GEMM on a new stream would
-// otherwise cudaMalloc -- a device-wide synchronisation -- inside a layer call).
-void lt_reserve(cudaStream_t st) {
+// Give side stream `st` its own cuBLASLt workspace (at stream creation, so no
+// cudaMalloc -- a device-wide synchronisation -- happens inside a layer call).
+// Returns false when it cannot be allocated.
+bool lt_reserve(cudaStream_t st) {
   Lt *L = lt_get();
-  if (!L->h) return;
+  if (!L->h) return true;  // no cuBLASLt: lt_gemm fails loudly on use
   std::lock_guard<std::mutex> g(L->mu);
-  if (L->stream_ws.count(st)) return;
+  if (L->stream_ws.count(st)) return true;
   void *w = nullptr;
-  if (L->stream_ws.empty()) w = L->ws;
-  else if (cudaMalloc(&w, L->ws_bytes) != cudaSuccess) return;
+  if (cudaMalloc(&w, L->ws_bytes) != cudaSuccess) return false;
   L->stream_ws[st] = w;
+  return true;
 }
 
 int lt_gemm(bool ta, bool tb, int m, int n, int k, const __half *A, int lda, const __half *B, int ldb,
@@ -1432,19 +1433,11 @@ int lt_gemm(bool ta, bool tb, int m, int n, int k, const __half *A, int lda, con
       if (ok) algo = res.algo;
     }
   }
-  void *wsp = nullptr;
+  void *wsp = L->ws;
   if (ok) {
     std::lock_guard<std::mutex> g(L->mu);
     auto it = L->stream_ws.find(st);
-    if (it != L->stream_ws.end()) {
-      wsp = it->second;
-    } else if (L->stream_ws.empty()) {
-      wsp = L->stream_ws[st] = L->ws;
-    } else if (cudaMalloc(&wsp, L->ws_bytes) == cudaSuccess) {
-      L->stream_ws[st] = wsp;
-    } else {
-      ok = false;
-    }
+    if (it != L->stream_ws.end()) wsp = it->second;
   }
   if (ok)
     ok = cublasLtMatmul(L->h, op, &alpha, A, la, B, lb, &beta, C, lc, C, lc, &algo, wsp, L->ws_bytes,
@@ -2483,19 +2476,20 @@ static const uint32_t kLayerSerialMin = [] {
 static cudaStream_t *side_streams() {
   static std::mutex mu;
   static cudaStream_t pool[64][kSideStreams] = {};
-  static bool made[64] = {};
+  static int state[64] = {};  // 0 untried, 1 ready, -1 failed (serial from then on)
   if (kLayerStreams <= 1) return nullptr;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
   std::lock_guard<std::mutex> g(mu);
-  if (!made[dev]) {
-    for (auto &s : pool[dev]) {
-      if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
-      lt_reserve(s);
-    }
-    made[dev] = true;
+  if (state[dev] == 0) {
+    state[dev] = 1;
+    for (auto &s : pool[dev])
+      if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess || !lt_reserve(s)) {
+        state[dev] = -1;  // the layer keeps every expert on the caller's stream
+        break;
+      }
   }
-  return pool[dev];
+  return state[dev] == 1 ? pool[dev] : nullptr;
 }
 static const uint32_t kLayerPerToken = [] {
   const char *p = std::getenv("FLOE_LAYER_PER_TOKEN");
